@@ -1,0 +1,270 @@
+/*
+ * pmagraph_cuda.h — C ABI of libpmagraph_cuda.so, the B200-native GPMA+ store.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, no torch or CUDA
+ * types.  Every entry point replaces one public entry of the reference's
+ * header-only C++ API (/root/reference/proj/include/pmagraph/...); the file:line
+ * of the reference interface it replaces is cited beside each declaration.
+ * The C++ wrappers in include/pmagraph/*.hpp restore the reference class and
+ * function names on top of these calls, and INTEGRATION.md shows the ctypes
+ * and C++ bindings a maintainer adds.
+ *
+ * Conventions
+ *  - Every function returns int: PMA_OK (0) or an error code.  The codes map
+ *    onto the exception types the reference throws:
+ *      PMA_EINVAL -> std::invalid_argument, PMA_ERANGE -> std::out_of_range,
+ *      PMA_ELOGIC -> std::logic_error,      PMA_ECUDA  -> std::runtime_error.
+ *    pma_last_error(h)/gpma_last_error(g) return the message of the last
+ *    failure on that handle (thread-unsafe, like the reference's single-writer
+ *    contract, pma.hpp:9-12).
+ *  - Host pointers are borrowed for the call only.  "_device" variants take
+ *    device pointers that stay owned by the caller.
+ *  - Calls are synchronous: they return after the handle's stream drained, so
+ *    wall times measured around them are end-to-end.
+ *  - Absent deletes are counted (pma_stats.deletes_missed), never errors,
+ *    exactly as segment_engine.hpp:134,294-307 and graph.hpp:140-145.
+ *  - Slot states: 0 = Empty, 1 = Valid, 2 = Tombstone (pma.hpp:29).  An Empty
+ *    slot downloads as key = value = 0 (pma.hpp:31-33).
+ *  - Update ops: 0 = insert, 1 = delete (segment_engine.hpp:24).
+ */
+#ifndef PMAGRAPH_CUDA_H
+#define PMAGRAPH_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMA_OK 0
+#define PMA_EINVAL 1
+#define PMA_ERANGE 2
+#define PMA_ELOGIC 3
+#define PMA_ECUDA 4
+
+#define PMA_MAX_LEVELS 64
+
+/* DensityProfile (pma.hpp:52-78).  NULL anywhere a profile is accepted means
+ * the reference defaults {0.08, 0.92, 0.40, 0.80, allow_shrink = 1}. */
+typedef struct pma_profile {
+    double leaf_lower;
+    double leaf_upper;
+    double root_lower;
+    double root_upper;
+    int32_t allow_shrink;
+    int32_t _pad;
+} pma_profile;
+
+/* DeletionMode (segment_engine.hpp:35) */
+#define PMA_LAZY 0
+#define PMA_EAGER 1
+/* MergeStrategy (segment_engine.hpp:41); -1 = size-tiered dispatch */
+#define PMA_STRATEGY_AUTO (-1)
+#define PMA_STRATEGY_SMALL 0
+#define PMA_STRATEGY_MEDIUM 1
+#define PMA_STRATEGY_LARGE 2
+
+/* SegmentEngineConfig + MergeTiers (segment_engine.hpp:43-60).  `workers` is
+ * accepted for drop-in compatibility and ignored: the CUDA grid replaces the
+ * WorkerPool, and results are worker-count independent by contract
+ * (pma.hpp:9-12).  The merge tier only changes the slot_writes accounting
+ * (commit_in_place counts compaction moves, segment_engine.hpp:147-230); the
+ * slot arrays are identical for every tier (segment_engine.hpp:37-40). */
+typedef struct pma_engine_config {
+    int32_t deletion_mode;   /* PMA_LAZY | PMA_EAGER */
+    uint32_t workers;        /* ignored */
+    uint64_t small_max;      /* MergeTiers::small_max  (default 32)   */
+    uint64_t medium_max;     /* MergeTiers::medium_max (default 1024) */
+    int32_t force_strategy;  /* PMA_STRATEGY_* */
+    int32_t _pad;
+} pma_engine_config;
+
+/* UpdateStats (update_stats.hpp:13-35) as a fixed POD.  touched_ranges are
+ * fetched separately with pma_touched_ranges().  Timing fields are host
+ * steady-clock nanoseconds around the device work (wall_ns) and the summed
+ * device time of the per-round segment kernels (segment_phase_ns). */
+typedef struct pma_stats {
+    uint64_t batch_size;
+    uint64_t rounds;
+    uint64_t slot_writes;
+    uint64_t wall_ns;
+    uint64_t segment_phase_ns;
+    uint64_t grow_events;
+    uint64_t shrink_events;
+    uint64_t deletes_missed;
+    uint64_t tombstones_added;
+    uint64_t num_touched_ranges;
+    int32_t resized;
+    int32_t num_levels; /* segments_per_level.size() */
+    uint64_t segments_per_level[PMA_MAX_LEVELS];
+} pma_stats;
+
+/* PmaLayout + counters (pma.hpp:82-123, 209-214, 529). */
+typedef struct pma_layout_info {
+    uint64_t capacity;
+    uint64_t leaf_size;
+    int32_t height;
+    int32_t _pad;
+    uint64_t valid_count;
+    uint64_t tombstone_count;
+    uint64_t slot_writes;
+} pma_layout_info;
+
+/* Device-event timings of the most recent call on a handle (milliseconds),
+ * for the bench's roofline: the dominant kernel's summed duration and launch
+ * count, plus the whole device-side span. */
+typedef struct pma_timing {
+    double device_ms;      /* first to last event of the call on the stream */
+    double sort_ms;        /* key sort + duplicate resolution             */
+    double search_ms;      /* leaf assignment                             */
+    double rounds_ms;      /* all per-round kernels (decide/commit/scatter) */
+    double refresh_ms;     /* leaf-header + row-offset refresh            */
+    uint64_t kernel_launches;
+    uint64_t merge_slots;  /* slots rewritten by merge commits (algorithmic scatter) */
+    uint64_t tombstone_flips;
+} pma_timing;
+
+typedef struct pma_handle pma_handle;
+
+/* ---- PackedMemoryArray (pma.hpp:125-612) ------------------------------- */
+
+/* PackedMemoryArray(DensityProfile) (pma.hpp:129-132): empty array of
+ * kMinCapacity = 16 slots on CUDA device `device`. */
+int pma_create(const pma_profile* profile, int device, pma_handle** out);
+int pma_destroy(pma_handle* h);
+const char* pma_last_error(const pma_handle* h);
+
+/* PackedMemoryArray::from_sorted (pma.hpp:160-187).  keys strictly
+ * increasing, else PMA_EINVAL with the reference's message. */
+int pma_from_sorted(pma_handle* h, const uint64_t* keys, const uint64_t* values, size_t n,
+                    double fill_target);
+
+/* Exact state restore (generalises from_slot_layout, pma.hpp:191-207, to
+ * tombstones): capacity must be a power of two >= 16.  Counters are derived
+ * from the states; slot_writes is reset to 0. */
+int pma_load_slots(pma_handle* h, size_t capacity, const uint64_t* keys, const uint64_t* values,
+                   const uint8_t* states);
+
+/* slots() (pma.hpp:214) as SoA: capacity entries each; any pointer may be NULL. */
+int pma_download(pma_handle* h, uint64_t* keys, uint64_t* values, uint8_t* states);
+
+/* layout(), capacity(), valid_count(), tombstone_count(), slot_writes()
+ * (pma.hpp:209-214, 529). */
+int pma_get_layout(const pma_handle* h, pma_layout_info* out);
+int pma_reset_slot_writes(pma_handle* h); /* pma.hpp:530 */
+
+/* min_entries/max_entries/thresholds (pma.hpp:217-230); PMA_ERANGE outside
+ * [0, height] with the reference's message (pma.hpp:533-538). */
+int pma_bounds(const pma_handle* h, int level, uint64_t* min_entries, uint64_t* max_entries,
+               double* rho, double* tau);
+
+/* batch_update(PackedMemoryArray&, std::vector<Update>, const
+ * SegmentEngineConfig&, WorkerPool*) -> UpdateStats (segment_engine.hpp:365-470).
+ * Host arrays of n updates; cfg NULL = defaults. */
+int pma_batch_update(pma_handle* h, const uint64_t* keys, const uint64_t* values,
+                     const uint8_t* ops, size_t n, const pma_engine_config* cfg, pma_stats* out);
+/* Same, with the update arrays already resident in device memory. */
+int pma_batch_update_device(pma_handle* h, const uint64_t* d_keys, const uint64_t* d_values,
+                            const uint8_t* d_ops, size_t n, const pma_engine_config* cfg,
+                            pma_stats* out);
+
+/* UpdateStats::touched_ranges of the last batch: pairs (begin, end) into
+ * `pairs` (2*cap entries); *count receives the total number of ranges. */
+int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count);
+
+/* binary_search_leaf for n keys (pma.hpp:234-245); any order. */
+int pma_binary_search_leaf(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* leaves);
+
+/* search(key) (pma.hpp:247-251) for n keys: found[i] = 1 and values[i] set
+ * when the key is Valid. */
+int pma_search(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* values, uint8_t* found);
+
+/* count_valid_in(begin, end) (pma.hpp:425-429). */
+int pma_count_valid_in(pma_handle* h, size_t begin, size_t end, uint64_t* count);
+
+/* Sequential single-key operations (pma.hpp:294-360, 365-386, 471-479).
+ * Their semantics differ from a one-update batch (in-place overwrite and
+ * tombstone revival; retry from the leaf after a grow) and are reproduced
+ * exactly.  Executed by device kernels; no CPU fallback. */
+int pma_insert(pma_handle* h, uint64_t key, uint64_t value);
+int pma_erase(pma_handle* h, uint64_t key, int* erased);
+int pma_mark_tombstone(pma_handle* h, uint64_t key, int* marked);
+int pma_redispatch(pma_handle* h, int level, size_t seg_index, const uint64_t* keys,
+                   const uint64_t* values, size_t n);
+
+int pma_last_timing(const pma_handle* h, pma_timing* out);
+
+/* ---- DynamicGraph (graph.hpp:62-240) ------------------------------------ */
+
+/* GraphConfig (graph.hpp:54-60).  engine must be the segment engine (0); the
+ * lock engine (GPMA, lock_engine.hpp) is out of scope. */
+typedef struct gpma_graph_config {
+    int32_t engine;         /* 0 = UpdateEngine::kSegment */
+    int32_t deletion_mode;  /* PMA_LAZY | PMA_EAGER */
+    uint32_t workers;       /* ignored */
+    int32_t _pad;
+    double fill_target;     /* 0.5 */
+    pma_profile profile;
+} gpma_graph_config;
+
+typedef struct gpma_graph gpma_graph;
+
+/* DynamicGraph::from_edges (graph.hpp:66-92).  weights may be NULL (1.0). */
+int gpma_from_edges(const gpma_graph_config* cfg, int device, size_t num_vertices,
+                    const uint32_t* src, const uint32_t* dst, const double* weights, size_t n,
+                    gpma_graph** out);
+/* Same with device-resident edge arrays. */
+int gpma_from_edges_device(const gpma_graph_config* cfg, int device, size_t num_vertices,
+                           const uint32_t* d_src, const uint32_t* d_dst, const double* d_weights,
+                           size_t n, gpma_graph** out);
+int gpma_destroy(gpma_graph* g);
+const char* gpma_last_error(const gpma_graph* g);
+
+/* The graph's PackedMemoryArray (graph.hpp:96); owned by the graph. */
+pma_handle* gpma_pma(gpma_graph* g);
+uint64_t gpma_num_vertices(const gpma_graph* g);
+uint64_t gpma_num_edges(const gpma_graph* g); /* graph.hpp:95 */
+
+/* DynamicGraph::apply_batch (graph.hpp:130-162): inserts (src,dst,weight),
+ * deletes (src,dst); guard deletes are dropped and counted as missed; row
+ * offsets refreshed on the device.  weights may be NULL (1.0). */
+int gpma_apply_batch(gpma_graph* g, const uint32_t* ins_src, const uint32_t* ins_dst,
+                     const double* ins_w, size_t n_ins, const uint32_t* del_src,
+                     const uint32_t* del_dst, size_t n_del, pma_stats* out);
+int gpma_apply_batch_device(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
+                            const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
+                            const uint32_t* d_del_dst, size_t n_del, pma_stats* out);
+
+/* row_offsets() (graph.hpp:97): num_vertices + 1 entries. */
+int gpma_row_offsets(gpma_graph* g, uint64_t* out);
+/* rebuild_row_offsets() (graph.hpp:182-190). */
+int gpma_rebuild_row_offsets(gpma_graph* g);
+/* csr_snapshot() (graph.hpp:192-206): row_offsets (|V|+1), col (num_edges),
+ * vals (num_edges). */
+int gpma_csr_snapshot(gpma_graph* g, uint64_t* row_offsets, uint32_t* col, double* vals);
+
+/* ---- analytics (analytics.hpp:17-158) ----------------------------------- */
+
+#define GPMA_UNREACHED 0xFFFFFFFFu /* kUnreached, analytics.hpp:17 */
+
+/* bfs(g, root) (analytics.hpp:22-48): dist has num_vertices entries;
+ * PMA_EINVAL when root >= num_vertices. *reached (may be NULL) = vertices
+ * with a finite distance. */
+int gpma_bfs(gpma_graph* g, uint32_t root, uint32_t* dist, uint64_t* reached);
+/* connected_components(g) (analytics.hpp:53-82): min-id label per component
+ * of the undirected closure. */
+int gpma_cc(gpma_graph* g, uint32_t* labels);
+/* pagerank(g, PageRankOptions) (analytics.hpp:90-143).  warm may be NULL. */
+int gpma_pagerank(gpma_graph* g, double damping, double epsilon, size_t max_iters,
+                  const double* warm, double* ranks, uint64_t* iterations, int* converged);
+/* spmv(g, x) (analytics.hpp:147-158); summation in ascending destination
+ * order per row, no FMA contraction: bit-exact with the reference. */
+int gpma_spmv(gpma_graph* g, const double* x, double* y);
+
+int gpma_last_timing(const gpma_graph* g, pma_timing* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMAGRAPH_CUDA_H */
