@@ -1,0 +1,390 @@
+// capi.cu — the extern "C" boundary of libpmagraph_cuda.so (declared in
+// include/pmagraph_cuda.h).  Exceptions never cross it: every call returns
+// a PMA_* code mapped from the reference's exception classes, and the
+// message is kept on the handle (pma_last_error / gpma_last_error).
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "graph_impl.cuh"
+#include "pmagraph_cuda.h"
+
+using gpma::ApiError;
+
+struct pma_handle {
+    gpma::Pma* impl = nullptr;
+    bool owned = true;
+};
+
+struct gpma_graph {
+    gpma::Graph* impl = nullptr;
+    pma_handle view;
+};
+
+namespace {
+thread_local std::string g_create_err;
+
+template <class F>
+int guarded(std::string* err, F&& f) {
+    try {
+        f();
+        return PMA_OK;
+    } catch (const ApiError& e) {
+        if (err) *err = e.what();
+        g_create_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        if (err) *err = std::string("allocation failed: ") + e.what();
+        return PMA_ECUDA;
+    } catch (const std::exception& e) {
+        if (err) *err = e.what();
+        g_create_err = e.what();
+        return PMA_ECUDA;
+    }
+}
+
+gpma::EngineCfg to_cfg(const pma_engine_config* c) {
+    gpma::EngineCfg e;
+    if (c) {
+        e.eager = c->deletion_mode == PMA_EAGER;
+        e.small_max = c->small_max;
+        e.medium_max = c->medium_max;
+        e.force = c->force_strategy;
+    }
+    return e;
+}
+
+std::string* err_of(pma_handle* h) { return h && h->impl ? &h->impl->err : nullptr; }
+std::string* err_of(gpma_graph* g) { return g && g->impl ? &g->impl->err : nullptr; }
+}  // namespace
+
+extern "C" {
+
+int pma_create(const pma_profile* profile, int device, pma_handle** out) {
+    return guarded(nullptr, [&] {
+        if (!out) throw ApiError(PMA_EINVAL, "pma_create: out is NULL");
+        auto* h = new pma_handle;
+        try {
+            h->impl = new gpma::Pma(profile, device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int pma_destroy(pma_handle* h) {
+    if (!h) return PMA_OK;
+    if (h->owned) {
+        delete h->impl;
+        delete h;
+    }
+    return PMA_OK;
+}
+
+const char* pma_last_error(const pma_handle* h) {
+    if (h && h->impl) return h->impl->err.c_str();
+    return g_create_err.c_str();
+}
+
+int pma_from_sorted(pma_handle* h, const uint64_t* keys, const uint64_t* values, size_t n, double fill_target) {
+    return guarded(err_of(h), [&] {
+        auto* p = h->impl;
+        GPMA_CUDA(cudaSetDevice(p->device()));
+        const uint64_t* dk = p->stage(p->stage_k, keys, n);
+        std::vector<uint64_t> zeros;
+        if (!values) zeros.assign(n, 0);
+        const uint64_t* dv = p->stage(p->stage_v, values ? values : zeros.data(), n);
+        p->from_sorted_device(dk, dv, n, fill_target);
+        GPMA_CUDA(cudaStreamSynchronize(p->stream()));
+    });
+}
+
+int pma_load_slots(pma_handle* h, size_t capacity, const uint64_t* keys, const uint64_t* values,
+                   const uint8_t* states) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->load_slots(capacity, keys, values, states);
+    });
+}
+
+int pma_download(pma_handle* h, uint64_t* keys, uint64_t* values, uint8_t* states) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->download(keys, values, states);
+    });
+}
+
+int pma_get_layout(const pma_handle* h, pma_layout_info* out) {
+    if (!h || !out) return PMA_EINVAL;
+    const auto* p = h->impl;
+    std::memset(out, 0, sizeof(*out));
+    out->capacity = p->capacity();
+    out->leaf_size = p->leaf();
+    out->height = p->height();
+    out->valid_count = p->valid_count;
+    out->tombstone_count = p->tombstone_count;
+    out->slot_writes = p->slot_writes;
+    return PMA_OK;
+}
+
+int pma_reset_slot_writes(pma_handle* h) {
+    if (!h) return PMA_EINVAL;
+    h->impl->slot_writes = 0;
+    return PMA_OK;
+}
+
+int pma_bounds(const pma_handle* h, int level, uint64_t* mn, uint64_t* mx, double* rho, double* tau) {
+    auto* hh = const_cast<pma_handle*>(h);
+    return guarded(err_of(hh), [&] {
+        const auto* p = h->impl;
+        if (level < 0 || level > p->height())
+            throw ApiError(PMA_ERANGE, "level " + std::to_string(level) + " outside [0, " +
+                                           std::to_string(p->height()) + "]");
+        if (mn) *mn = p->min_entries(level);
+        if (mx) *mx = p->max_entries(level);
+        // DensityProfile::lower_at / upper_at (pma.hpp:69-77): reporting only
+        const auto& pr = p->profile();
+        const int hgt = p->height();
+        if (rho) *rho = hgt == 0 ? pr.root_lower : pr.leaf_lower + (pr.root_lower - pr.leaf_lower) * double(level) / hgt;
+        if (tau) *tau = hgt == 0 ? pr.root_upper : pr.leaf_upper + (pr.root_upper - pr.leaf_upper) * double(level) / hgt;
+    });
+}
+
+int pma_batch_update(pma_handle* h, const uint64_t* keys, const uint64_t* values, const uint8_t* ops, size_t n,
+                     const pma_engine_config* cfg, pma_stats* out) {
+    return guarded(err_of(h), [&] {
+        auto* p = h->impl;
+        GPMA_CUDA(cudaSetDevice(p->device()));
+        const auto t0 = std::chrono::steady_clock::now();
+        const uint64_t* dk = p->stage(p->stage_k, keys, n);
+        std::vector<uint64_t> zeros;
+        if (!values) zeros.assign(n, 0);
+        const uint64_t* dv = p->stage(p->stage_v, values ? values : zeros.data(), n);
+        const uint8_t* dop = p->stage(p->stage_o, ops, n);
+        p->batch_update_device(dk, dv, dop, n, to_cfg(cfg), out);
+        if (out)
+            out->wall_ns = uint64_t(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+int pma_batch_update_device(pma_handle* h, const uint64_t* d_keys, const uint64_t* d_values, const uint8_t* d_ops,
+                            size_t n, const pma_engine_config* cfg, pma_stats* out) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->batch_update_device(d_keys, d_values, d_ops, n, to_cfg(cfg), out);
+    });
+}
+
+int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count) {
+    return guarded(err_of(h), [&] {
+        size_t c = 0;
+        h->impl->touched_ranges(pairs, cap, &c);
+        if (count) *count = c;
+    });
+}
+
+int pma_binary_search_leaf(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* leaves) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->binary_search_leaf(keys, n, leaves);
+    });
+}
+
+int pma_search(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* values, uint8_t* found) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->search(keys, n, values, found);
+    });
+}
+
+int pma_count_valid_in(pma_handle* h, size_t begin, size_t end, uint64_t* count) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        *count = h->impl->count_valid_in(begin, end);
+    });
+}
+
+int pma_insert(pma_handle* h, uint64_t key, uint64_t value) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->insert(key, value);
+    });
+}
+
+int pma_erase(pma_handle* h, uint64_t key, int* erased) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        const bool r = h->impl->erase(key);
+        if (erased) *erased = r ? 1 : 0;
+    });
+}
+
+int pma_mark_tombstone(pma_handle* h, uint64_t key, int* marked) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        const bool r = h->impl->mark_tombstone(key);
+        if (marked) *marked = r ? 1 : 0;
+    });
+}
+
+int pma_redispatch(pma_handle* h, int level, size_t seg_index, const uint64_t* keys, const uint64_t* values,
+                   size_t n) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->redispatch(level, seg_index, keys, values, n);
+    });
+}
+
+int pma_last_timing(const pma_handle* h, pma_timing* out) {
+    if (!h || !out) return PMA_EINVAL;
+    *out = h->impl->timing;
+    return PMA_OK;
+}
+
+// ------------------------------------------------------------------ graph
+
+int gpma_from_edges(const gpma_graph_config* cfg, int device, size_t num_vertices, const uint32_t* src,
+                    const uint32_t* dst, const double* weights, size_t n, gpma_graph** out) {
+    return guarded(nullptr, [&] {
+        if (num_vertices >= 0xFFFFFFFFull)
+            throw ApiError(PMA_EINVAL, "from_edges: vertex count exceeds the id space");
+        auto* g = new gpma_graph;
+        try {
+            g->impl = new gpma::Graph(cfg, device, num_vertices);
+            g->view.impl = &g->impl->pma;
+            g->view.owned = false;
+            auto& p = g->impl->pma;
+            const uint32_t* ds = p.stage(p.stage_a, src, n);
+            const uint32_t* dd = p.stage(p.stage_b, dst, n);
+            const double* dw = weights ? p.stage(p.stage_w, weights, n) : nullptr;
+            g->impl->from_edges_device(ds, dd, dw, n);
+        } catch (...) {
+            delete g->impl;
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+int gpma_from_edges_device(const gpma_graph_config* cfg, int device, size_t num_vertices, const uint32_t* d_src,
+                           const uint32_t* d_dst, const double* d_weights, size_t n, gpma_graph** out) {
+    return guarded(nullptr, [&] {
+        if (num_vertices >= 0xFFFFFFFFull)
+            throw ApiError(PMA_EINVAL, "from_edges: vertex count exceeds the id space");
+        auto* g = new gpma_graph;
+        try {
+            g->impl = new gpma::Graph(cfg, device, num_vertices);
+            g->view.impl = &g->impl->pma;
+            g->view.owned = false;
+            g->impl->from_edges_device(d_src, d_dst, d_weights, n);
+        } catch (...) {
+            delete g->impl;
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+int gpma_destroy(gpma_graph* g) {
+    if (!g) return PMA_OK;
+    delete g->impl;
+    delete g;
+    return PMA_OK;
+}
+
+const char* gpma_last_error(const gpma_graph* g) {
+    if (g && g->impl) return g->impl->err.c_str();
+    return g_create_err.c_str();
+}
+
+pma_handle* gpma_pma(gpma_graph* g) { return g ? &g->view : nullptr; }
+uint64_t gpma_num_vertices(const gpma_graph* g) { return g ? g->impl->nv : 0; }
+uint64_t gpma_num_edges(const gpma_graph* g) { return g ? g->impl->num_edges() : 0; }
+
+int gpma_apply_batch(gpma_graph* g, const uint32_t* ins_src, const uint32_t* ins_dst, const double* ins_w,
+                     size_t n_ins, const uint32_t* del_src, const uint32_t* del_dst, size_t n_del, pma_stats* out) {
+    return guarded(err_of(g), [&] {
+        auto& p = g->impl->pma;
+        GPMA_CUDA(cudaSetDevice(p.device()));
+        const auto t0 = std::chrono::steady_clock::now();
+        const uint32_t* a = p.stage(p.stage_a, ins_src, n_ins);
+        const uint32_t* b = p.stage(p.stage_b, ins_dst, n_ins);
+        const double* w = ins_w ? p.stage(p.stage_w, ins_w, n_ins) : nullptr;
+        const uint32_t* c = p.stage(p.stage_c, del_src, n_del);
+        const uint32_t* d = p.stage(p.stage_d, del_dst, n_del);
+        g->impl->apply_batch_device(a, b, w, n_ins, c, d, n_del, out);
+        if (out)
+            out->wall_ns = uint64_t(
+                std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+    });
+}
+
+int gpma_apply_batch_device(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
+                            const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst,
+                            size_t n_del, pma_stats* out) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->apply_batch_device(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, out);
+    });
+}
+
+int gpma_row_offsets(gpma_graph* g, uint64_t* out) {
+    return guarded(err_of(g), [&] { g->impl->row_offsets(out); });
+}
+
+int gpma_rebuild_row_offsets(gpma_graph* g) {
+    return guarded(err_of(g), [&] {
+        g->impl->pma.rebuild_row_offsets_full();
+        GPMA_CUDA(cudaStreamSynchronize(g->impl->pma.stream()));
+    });
+}
+
+int gpma_csr_snapshot(gpma_graph* g, uint64_t* row_offsets, uint32_t* col, double* vals) {
+    return guarded(err_of(g), [&] { g->impl->csr_snapshot(row_offsets, col, vals); });
+}
+
+int gpma_bfs(gpma_graph* g, uint32_t root, uint32_t* dist, uint64_t* reached) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->bfs(root, dist, reached);
+    });
+}
+
+int gpma_cc(gpma_graph* g, uint32_t* labels) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->cc(labels);
+    });
+}
+
+int gpma_pagerank(gpma_graph* g, double damping, double epsilon, size_t max_iters, const double* warm, double* ranks,
+                  uint64_t* iterations, int* converged) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        uint64_t it = 0;
+        int conv = 0;
+        g->impl->pagerank(damping, epsilon, max_iters, warm, ranks, &it, &conv);
+        if (iterations) *iterations = it;
+        if (converged) *converged = conv;
+    });
+}
+
+int gpma_spmv(gpma_graph* g, const double* x, double* y) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->spmv(x, y);
+    });
+}
+
+int gpma_last_timing(const gpma_graph* g, pma_timing* out) {
+    if (!g || !out) return PMA_EINVAL;
+    *out = g->impl->pma.timing;
+    return PMA_OK;
+}
+
+}  // extern "C"

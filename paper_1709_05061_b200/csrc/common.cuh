@@ -1,0 +1,92 @@
+// common.cuh — shared device/host helpers for libpmagraph_cuda.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "pmagraph_cuda.h"
+
+namespace gpma {
+
+using u8 = uint8_t;
+using u32 = uint32_t;
+using u64 = uint64_t;
+using i64 = long long;
+using ull = unsigned long long;
+
+constexpr u8 kEmpty = 0;
+constexpr u8 kValid = 1;
+constexpr u8 kTombstone = 2;
+constexpr u8 kOpInsert = 0;
+constexpr u8 kOpDelete = 1;
+constexpr u8 kOpSkip = 2;  // guard deletes dropped by apply_batch (graph.hpp:141-147)
+constexpr u64 kGuardDst = 0xFFFFFFFFull;
+constexpr int kNumSMs = 148;
+
+// Error carrying the reference exception class as a PMA_* code.
+struct ApiError : std::runtime_error {
+    int code;
+    ApiError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define GPMA_CUDA(call)                                                                           \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess)                                                                    \
+            throw ::gpma::ApiError(PMA_ECUDA, std::string(#call " failed: ") + cudaGetErrorString(e_) + \
+                                                  " (" __FILE__ ":" + std::to_string(__LINE__) + ")");        \
+    } while (0)
+
+#define GPMA_LAUNCH_CHECK() GPMA_CUDA(cudaGetLastError())
+
+inline unsigned grid_for(u64 n, unsigned block, unsigned cap = 148u * 16u) {
+    u64 g = (n + block - 1) / block;
+    if (g == 0) g = 1;
+    if (g > cap) g = cap;
+    return static_cast<unsigned>(g);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Streaming (evict-first) 64-bit loads/stores for single-touch traffic.
+__device__ __forceinline__ u64 ld_cs(const u64* p) { return __ldcs(reinterpret_cast<const unsigned long long*>(p)); }
+
+// Edge-key helpers (graph.hpp:27-37).
+__host__ __device__ __forceinline__ u64 pack_edge(u32 src, u32 dst) { return (u64(src) << 32) | dst; }
+__host__ __device__ __forceinline__ u32 src_of(u64 key) { return u32(key >> 32); }
+__host__ __device__ __forceinline__ u32 dst_of(u64 key) { return u32(key & 0xFFFFFFFFull); }
+__host__ __device__ __forceinline__ bool is_guard(u64 key) { return (key & 0xFFFFFFFFull) == kGuardDst; }
+
+// Growable device buffer (grow-only; contents not preserved on growth).
+template <typename T>
+struct DevBuf {
+    T* ptr = nullptr;
+    size_t cap = 0;
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        size_t c = n < 1024 ? 1024 : n + n / 4;
+        GPMA_CUDA(cudaMalloc(&ptr, c * sizeof(T)));
+        cap = c;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+}  // namespace gpma

@@ -1,0 +1,585 @@
+// graph.cu — DynamicGraph on the device PMA (graph.hpp:62-240) and the
+// analytics kernels over the gapped slot array (analytics.hpp:17-158).
+//
+// Row u of the graph is the slot interval [ro[u], ro[u+1]) of the PMA:
+// Valid non-guard slots are its edges in ascending destination order, the
+// interval also holds gaps, tombstones and the row's guard (graph.hpp:100-114).
+// The analytics read keys+states (9 B/slot) and, for SpMV, values (17 B/slot).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cmath>
+#include <cstring>
+
+#include "block_ops.cuh"
+#include "graph_impl.cuh"
+
+namespace gpma {
+
+// ---------------------------------------------------------------- kernels
+
+__global__ void k_check_ids(const u32* src, const u32* dst, u64 n, u64 nv, Ctr* ctr) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        if (src[i] >= nv || dst[i] >= nv) atomicMin(&ctr->bad_index, ull(i));
+}
+
+// Pack inserts then deletes (graph.hpp:133-147).  Guard deletes become
+// kOpSkip and are counted as missed by the caller.
+__global__ void k_pack_batch(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
+                             u64 nd, u64* keys, u64* vals, u8* ops, Ctr* ctr) {
+    ull guards = 0;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < ni + nd; i += u64(gridDim.x) * blockDim.x) {
+        if (i < ni) {
+            keys[i] = pack_edge(is[i], id[i]);
+            vals[i] = __double_as_longlong(iw ? iw[i] : 1.0);
+            ops[i] = kOpInsert;
+        } else {
+            const u64 j = i - ni;
+            keys[i] = pack_edge(ds[j], dd[j]);
+            vals[i] = 0;
+            const bool g = dd[j] == u32(kGuardDst);
+            ops[i] = g ? kOpSkip : kOpDelete;
+            guards += g;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) guards += __shfl_xor_sync(FULL, guards, d);
+    if ((threadIdx.x & 31) == 0 && guards) atomicAdd(&ctr->guard_deletes, guards);
+}
+
+__global__ void k_pack_edges(const u32* s, const u32* d, u64 n, u64* keys, u32* idx) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        keys[i] = pack_edge(s[i], d[i]);
+        idx[i] = u32(i);
+    }
+}
+
+// Merge the |V| guards into the sorted unique edge list: edge i lands at
+// i + src (guards of smaller rows precede it), guard v lands after every
+// edge with src <= v.
+__global__ void k_place_guards(const u64* ek, const u64* ev, u64 ne, u64 nv, u64* ok, u64* ov) {
+    const u64 total = ne + nv;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+        if (i < ne) {
+            const u64 k = ek[i];
+            ok[i + src_of(k)] = k;
+            ov[i + src_of(k)] = ev[i];
+        } else {
+            const u64 v = i - ne;
+            const u64 g = pack_edge(u32(v), u32(kGuardDst));
+            const u64 pos = lower_bound_dev(ek, ne, g) + v;
+            ok[pos] = g;
+            ov[pos] = 0;
+        }
+    }
+}
+
+__global__ void k_fill_u32(u32* a, u64 n, u32 v) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) a[i] = v;
+}
+__global__ void k_iota_u32(u32* a, u64 n) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) a[i] = u32(i);
+}
+
+// -------- BFS (analytics.hpp:22-48): warp per frontier vertex, lanes stride
+// its slot interval (coalesced 8-B keys + 1-B states), CAS on dist,
+// warp-aggregated enqueue (ballot + popc + one atomic per warp).
+__global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, u32 nf,
+                                                    const u64* __restrict__ ro, const u64* __restrict__ keys,
+                                                    const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
+                                                    u32* __restrict__ next, u32* __restrict__ next_n) {
+    const unsigned lane = threadIdx.x & 31u;
+    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 f = warp; f < nf; f += nwarps) {
+        const u32 u = frontier[f];
+        const u64 b = ro[u], e = ro[u + 1];
+        for (u64 t0 = b; t0 < e; t0 += 32) {
+            const u64 t = t0 + lane;
+            bool won = false;
+            u32 v = 0;
+            if (t < e && st[t] == kValid) {
+                const u64 k = keys[t];
+                if (!is_guard(k)) {
+                    v = dst_of(k);
+                    if (dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+                }
+            }
+            const unsigned wm = __ballot_sync(FULL, won);
+            if (wm) {
+                u32 base = 0;
+                if (lane == 0) base = atomicAdd(next_n, u32(__popc(wm)));
+                base = __shfl_sync(FULL, base, 0);
+                if (won) next[base + __popc(wm & lanemask_lt())] = v;
+            }
+        }
+    }
+}
+
+// -------- CC (analytics.hpp:53-82): min-root union-find over every stored
+// edge (undirected closure).  Roots only ever link under smaller roots, so a
+// tree's root is its minimum id and the final labels equal the reference's
+// min-id-per-component labels bit for bit.
+__device__ __forceinline__ u32 cc_find(u32* parent, u32 x) {
+    u32 p = parent[x];
+    while (p != x) {
+        const u32 gp = parent[p];
+        if (gp != p) parent[x] = gp;  // path halving (only ever shortcuts to an ancestor)
+        x = p;
+        p = gp;
+    }
+    return x;
+}
+
+__global__ void k_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u32* parent) {
+    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < cap; t += u64(gridDim.x) * blockDim.x) {
+        if (st[t] != kValid) continue;
+        const u64 k = keys[t];
+        if (is_guard(k)) continue;
+        u32 a = src_of(k), b = dst_of(k);
+        for (;;) {
+            a = cc_find(parent, a);
+            b = cc_find(parent, b);
+            if (a == b) break;
+            const u32 hi = a > b ? a : b, lo = a > b ? b : a;
+            if (atomicCAS(&parent[hi], hi, lo) == hi) break;
+            a = hi;
+            b = lo;
+        }
+    }
+}
+
+__global__ void k_cc_flatten(u32* parent, u64 nv) {
+    for (u64 v = blockIdx.x * u64(blockDim.x) + threadIdx.x; v < nv; v += u64(gridDim.x) * blockDim.x) {
+        u32 x = u32(v);
+        while (parent[x] != x) x = parent[x];
+        parent[v] = x;
+    }
+}
+
+// -------- PageRank (analytics.hpp:100-143)
+// out-degree: Valid non-guard slots per row, warp-segmented by source.
+__global__ void k_outdeg(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u32* __restrict__ outdeg) {
+    const u64 stride = u64(gridDim.x) * blockDim.x;
+    for (u64 t0 = (blockIdx.x * u64(blockDim.x) + threadIdx.x) & ~31ull; t0 < cap; t0 += stride) {
+        const u64 t = t0 + (threadIdx.x & 31u);
+        bool e = false;
+        u32 s = 0xFFFFFFFFu;
+        if (t < cap && st[t] == kValid) {
+            const u64 k = keys[t];
+            e = !is_guard(k);
+            s = src_of(k);
+        }
+        const unsigned grp = __match_any_sync(FULL, e ? s : 0xFFFFFFFFu);
+        const unsigned leader = __ffs(grp) - 1;
+        if (e && (threadIdx.x & 31u) == leader) atomicAdd(&outdeg[s], u32(__popc(grp)));
+    }
+}
+
+__global__ void k_pr_prep(const double* __restrict__ x, const u32* __restrict__ outdeg, u64 n, double d,
+                          double* __restrict__ share, double* dangling_sum) {
+    double dang = 0.0;
+    for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x) {
+        const u32 od = outdeg[u];
+        if (od == 0) {
+            dang += x[u];
+            share[u] = 0.0;
+        } else {
+            share[u] = __ddiv_rn(__dmul_rn(d, x[u]), double(od));
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dang += __shfl_xor_sync(FULL, dang, o);
+    if ((threadIdx.x & 31) == 0 && dang != 0.0) atomicAdd(dangling_sum, dang);
+}
+
+__global__ void k_pr_base(double* __restrict__ y, u64 n, const double* dangling_sum, double d) {
+    const double nn = double(n);
+    const double base = __dadd_rn(__ddiv_rn(1.0 - d, nn), __ddiv_rn(__dmul_rn(d, *dangling_sum), nn));
+    for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x) y[u] = base;
+}
+
+// push sweep over the gapped array: src comes from the key, so no row
+// offsets are read; red.global.add.f64 into y (L2-resident for |V| <= ~16M).
+__global__ void __launch_bounds__(256) k_pr_push(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
+                                                 const double* __restrict__ share, double* __restrict__ y) {
+    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < cap; t += u64(gridDim.x) * blockDim.x) {
+        if (st[t] != kValid) continue;
+        const u64 k = keys[t];
+        if (is_guard(k)) continue;
+        atomicAdd(&y[dst_of(k)], share[src_of(k)]);
+    }
+}
+
+__global__ void k_pr_l1(const double* __restrict__ x, const double* __restrict__ y, u64 n, double* l1) {
+    double acc = 0.0;
+    for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x)
+        acc += fabs(y[u] - x[u]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(l1, acc);
+}
+
+// -------- SpMV (analytics.hpp:147-158): warp per row; products in parallel,
+// accumulation serial in ascending slot order with explicit round-to-nearest
+// multiply and add (no FMA contraction) — bit-exact with the reference.
+__global__ void __launch_bounds__(256) k_spmv(const u64* __restrict__ ro, u64 nv, const u64* __restrict__ keys,
+                                              const u64* __restrict__ vals, const u8* __restrict__ st,
+                                              const double* __restrict__ x, double* __restrict__ y) {
+    const unsigned lane = threadIdx.x & 31u;
+    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 u = warp; u < nv; u += nwarps) {
+        const u64 b = ro[u], e = ro[u + 1];
+        double acc = 0.0;
+        for (u64 t0 = b; t0 < e; t0 += 32) {
+            const u64 t = t0 + lane;
+            double prod = 0.0;
+            bool ok = false;
+            if (t < e && st[t] == kValid) {
+                const u64 k = keys[t];
+                if (!is_guard(k)) {
+                    ok = true;
+                    prod = __dmul_rn(__longlong_as_double((long long)vals[t]), x[dst_of(k)]);
+                }
+            }
+            unsigned m = __ballot_sync(FULL, ok);
+            while (m) {
+                const int i = __ffs(m) - 1;
+                acc = __dadd_rn(acc, __shfl_sync(FULL, prod, i));
+                m &= m - 1;
+            }
+        }
+        if (lane == 0) y[u] = acc;
+    }
+}
+
+// ---------------------------------------------------------------- Graph
+
+Graph::Graph(const gpma_graph_config* cfg, int device, u64 nv_)
+    : pma(cfg ? &cfg->profile : nullptr, device), nv(nv_) {
+    if (cfg) {
+        if (cfg->engine != 0)
+            throw ApiError(PMA_EINVAL, "GraphConfig.engine: only the segment engine (GPMA+) is provided");
+        ecfg.eager = cfg->deletion_mode == PMA_EAGER;
+        fill_target = cfg->fill_target;
+    }
+    ro.reserve(nv + 1);
+    pma.d_row_offsets = ro.ptr;
+    pma.num_vertices = nv;
+}
+
+static void sort_pairs(cudaStream_t s, DevBuf<unsigned char>& tmpb, u64* kin, u64* kout, u32* vin, u32* vout, u64 n,
+                       int nbits) {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, int(n), 0, nbits, s);
+    tmpb.reserve(tmp);
+    GPMA_CUDA(cub::DeviceRadixSort::SortPairs(tmpb.ptr, tmp, kin, kout, vin, vout, int(n), 0, nbits, s));
+}
+
+static int bits_for(u64 v) {
+    int b = 0;
+    while (b < 64 && (v >> b)) ++b;
+    return b;
+}
+
+// DynamicGraph::from_edges (graph.hpp:66-92)
+void Graph::from_edges_device(const u32* d_src, const u32* d_dst, const double* d_w, u64 n) {
+    cudaStream_t s = pma.stream();
+    Ctr* ctr = scratch_ctr();
+    if (n > 0) {
+        ull init = ~0ull;
+        GPMA_CUDA(cudaMemcpyAsync(&ctr->bad_index, &init, 8, cudaMemcpyHostToDevice, s));
+        k_check_ids<<<grid_for(n, 256), 256, 0, s>>>(d_src, d_dst, n, nv, ctr);
+        GPMA_LAUNCH_CHECK();
+        ull bad = 0;
+        GPMA_CUDA(cudaMemcpyAsync(&bad, &ctr->bad_index, 8, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
+        if (bad != ~0ull) {
+            u32 bs = 0, bd = 0;
+            GPMA_CUDA(cudaMemcpy(&bs, d_src + bad, 4, cudaMemcpyDeviceToHost));
+            GPMA_CUDA(cudaMemcpy(&bd, d_dst + bad, 4, cudaMemcpyDeviceToHost));
+            throw ApiError(PMA_EINVAL, "edge (" + std::to_string(bs) + ", " + std::to_string(bd) +
+                                           ") outside vertex range " + std::to_string(nv));
+        }
+    }
+    DevBuf<u64> k0, k1, uk, uvv, mk, mv;
+    DevBuf<u32> i0, i1;
+    DevBuf<unsigned char> tmp;
+    k0.reserve(n + 1);
+    k1.reserve(n + 1);
+    i0.reserve(n + 1);
+    i1.reserve(n + 1);
+    u64 ne = 0;
+    uk.reserve(n + 1);
+    uvv.reserve(n + 1);
+    if (n > 0) {
+        k_pack_edges<<<grid_for(n, 256), 256, 0, s>>>(d_src, d_dst, n, k0.ptr, i0.ptr);
+        GPMA_LAUNCH_CHECK();
+        const int nbits = 32 + bits_for(nv ? nv - 1 : 0);
+        sort_pairs(s, tmp, k0.ptr, k1.ptr, i0.ptr, i1.ptr, n, nbits);
+        // dedupe, last arrival wins (stable sort keeps arrival order)
+        const u64* sk = k1.ptr;
+        const u32* si = i1.ptr;
+        u64* ok_ = uk.ptr;
+        u64* ov_ = uvv.ptr;
+        Ctr* c = ctr;
+        run_compact(
+            s, pma.ws, nullptr, n, n, [=] __device__(ull i) { return i + 1 == n || sk[i + 1] != sk[i]; },
+            [=] __device__(ull i, unsigned f, ull x) {
+                if (f) {
+                    ok_[x] = sk[i];
+                    ov_[x] = __double_as_longlong(d_w ? d_w[si[i]] : 1.0);
+                }
+            },
+            [=] __device__(ull total) { c->n_unique = total; });
+        GPMA_CUDA(cudaMemcpyAsync(&ne, &ctr->n_unique, 8, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
+    }
+    const u64 total = ne + nv;
+    mk.reserve(total + 1);
+    mv.reserve(total + 1);
+    if (total > 0) {
+        k_place_guards<<<grid_for(total, 256), 256, 0, s>>>(uk.ptr, uvv.ptr, ne, nv, mk.ptr, mv.ptr);
+        GPMA_LAUNCH_CHECK();
+    }
+    pma.from_sorted_device(mk.ptr, mv.ptr, total, fill_target);
+    GPMA_CUDA(cudaStreamSynchronize(s));
+}
+
+Ctr* Graph::scratch_ctr() {
+    if (!d_ctr_) GPMA_CUDA(cudaMalloc(&d_ctr_, sizeof(Ctr)));
+    GPMA_CUDA(cudaMemsetAsync(d_ctr_, 0, sizeof(Ctr), pma.stream()));
+    return d_ctr_;
+}
+
+Graph::~Graph() {
+    if (d_ctr_) cudaFree(d_ctr_);
+}
+
+// DynamicGraph::apply_batch (graph.hpp:130-162)
+void Graph::apply_batch_device(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
+                               u64 nd, pma_stats* out) {
+    cudaStream_t s = pma.stream();
+    Ctr* ctr = scratch_ctr();
+    if (ni > 0) {
+        ull init = ~0ull;
+        GPMA_CUDA(cudaMemcpyAsync(&ctr->bad_index, &init, 8, cudaMemcpyHostToDevice, s));
+        k_check_ids<<<grid_for(ni, 256), 256, 0, s>>>(is, id, ni, nv, ctr);
+        GPMA_LAUNCH_CHECK();
+    }
+    const u64 n = ni + nd;
+    bk.reserve(n + 1);
+    bv.reserve(n + 1);
+    bo.reserve(n + 1);
+    if (n > 0) {
+        k_pack_batch<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(is, id, iw, ni, ds, dd, nd, bk.ptr, bv.ptr, bo.ptr, ctr);
+        GPMA_LAUNCH_CHECK();
+    }
+    ull hc[2] = {~0ull, 0};
+    GPMA_CUDA(cudaMemcpyAsync(&hc[0], &ctr->bad_index, 8, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaMemcpyAsync(&hc[1], &ctr->guard_deletes, 8, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    if (ni > 0 && hc[0] != ~0ull) {
+        u32 bs = 0, bd = 0;
+        GPMA_CUDA(cudaMemcpy(&bs, is + hc[0], 4, cudaMemcpyDeviceToHost));
+        GPMA_CUDA(cudaMemcpy(&bd, id + hc[0], 4, cudaMemcpyDeviceToHost));
+        throw ApiError(PMA_EINVAL, "edge (" + std::to_string(bs) + ", " + std::to_string(bd) +
+                                       ") outside vertex range " + std::to_string(nv));
+    }
+    const u64 guard_deletes = hc[1];
+    pma_stats st;
+    pma.batch_update_device(bk.ptr, bv.ptr, bo.ptr, n, ecfg, &st);
+    st.batch_size = n - guard_deletes;
+    st.deletes_missed += guard_deletes;
+    if (out) *out = st;
+}
+
+void Graph::row_offsets(u64* out) {
+    GPMA_CUDA(cudaMemcpyAsync(out, ro.ptr, (nv + 1) * 8, cudaMemcpyDeviceToHost, pma.stream()));
+    GPMA_CUDA(cudaStreamSynchronize(pma.stream()));
+}
+
+u64 Graph::num_edges() const { return pma.valid_count - nv; }
+
+void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
+    cudaStream_t s = pma.stream();
+    const u64 ne = num_edges();
+    DevBuf<u64> dro;
+    DevBuf<u32> dcol;
+    DevBuf<double> dval;
+    dro.reserve(nv + 1);
+    dcol.reserve(ne + 1);
+    dval.reserve(ne + 1);
+    GPMA_CUDA(cudaMemsetAsync(dro.ptr, 0, 8, s));
+    const u64* kk = pma.d_keys;
+    const u64* vv = pma.d_vals;
+    const u8* ss = pma.d_st;
+    u64* r = dro.ptr;
+    u32* c = dcol.ptr;
+    double* w = dval.ptr;
+    const u64 cap = pma.capacity();
+    if (cap > 0) {
+        run_compact(
+            s, pma.ws, nullptr, cap, cap,
+            [=] __device__(ull t) { return ss[t] == kValid && !is_guard(kk[t]); },
+            [=] __device__(ull t, unsigned f, ull x) {
+                if (f) {
+                    c[x] = dst_of(kk[t]);
+                    w[x] = __longlong_as_double((long long)vv[t]);
+                } else if (ss[t] == kValid) {
+                    r[src_of(kk[t]) + 1] = x;  // guard of row u: entries of rows <= u
+                }
+            },
+            NoFin{});
+    }
+    if (h_ro) GPMA_CUDA(cudaMemcpyAsync(h_ro, dro.ptr, (nv + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (h_col && ne) GPMA_CUDA(cudaMemcpyAsync(h_col, dcol.ptr, ne * 4, cudaMemcpyDeviceToHost, s));
+    if (h_val && ne) GPMA_CUDA(cudaMemcpyAsync(h_val, dval.ptr, ne * 8, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+}
+
+// ------------------------------------------------------------- analytics
+
+void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
+    if (root >= nv) throw ApiError(PMA_EINVAL, "bfs: root outside vertex range");
+    cudaStream_t s = pma.stream();
+    GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
+    dist.reserve(nv);
+    q0.reserve(nv + 1);
+    q1.reserve(nv + 1);
+    qn.reserve(2);
+    k_fill_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv, GPMA_UNREACHED);
+    GPMA_LAUNCH_CHECK();
+    const u32 zero = 0;
+    GPMA_CUDA(cudaMemcpyAsync(dist.ptr + root, &zero, 4, cudaMemcpyHostToDevice, s));
+    GPMA_CUDA(cudaMemcpyAsync(q0.ptr, &root, 4, cudaMemcpyHostToDevice, s));
+    u32 nf = 1;
+    u64 total = 1;
+    u32 depth = 0;
+    u32* cur = q0.ptr;
+    u32* nxt = q1.ptr;
+    u64 launches = 3;
+    while (nf > 0) {
+        ++depth;
+        GPMA_CUDA(cudaMemsetAsync(qn.ptr, 0, 4, s));
+        const unsigned blocks = grid_for(u64(nf) * 32, 256, 148 * 16);
+        k_bfs_expand<<<blocks, 256, 0, s>>>(cur, nf, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt, qn.ptr);
+        GPMA_LAUNCH_CHECK();
+        ++launches;
+        GPMA_CUDA(cudaMemcpyAsync(h_nf_, qn.ptr, 4, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
+        nf = *h_nf_;
+        total += nf;
+        std::swap(cur, nxt);
+    }
+    GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
+    if (h_dist) GPMA_CUDA(cudaMemcpyAsync(h_dist, dist.ptr, nv * 4, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    if (reached) *reached = total;
+    record_timing(launches);
+}
+
+void Graph::cc(u32* h_labels) {
+    cudaStream_t s = pma.stream();
+    GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
+    dist.reserve(nv + 1);
+    k_iota_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv);
+    GPMA_LAUNCH_CHECK();
+    k_cc_hook<<<grid_for(pma.capacity(), 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, pma.capacity(), dist.ptr);
+    GPMA_LAUNCH_CHECK();
+    k_cc_flatten<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv);
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
+    if (h_labels) GPMA_CUDA(cudaMemcpyAsync(h_labels, dist.ptr, nv * 4, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    record_timing(3);
+}
+
+void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, double* h_ranks, u64* iters,
+                     int* converged) {
+    if (nv == 0) throw ApiError(PMA_EINVAL, "pagerank: empty vertex set");
+    cudaStream_t s = pma.stream();
+    GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
+    px.reserve(nv);
+    py.reserve(nv);
+    pshare.reserve(nv);
+    psc.reserve(2);
+    outdeg.reserve(nv);
+    if (h_warm) {
+        GPMA_CUDA(cudaMemcpyAsync(px.ptr, h_warm, nv * 8, cudaMemcpyHostToDevice, s));
+    } else {
+        std::vector<double> x0(nv, 1.0 / double(nv));
+        GPMA_CUDA(cudaMemcpyAsync(px.ptr, x0.data(), nv * 8, cudaMemcpyHostToDevice, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
+    }
+    GPMA_CUDA(cudaMemsetAsync(outdeg.ptr, 0, nv * 4, s));
+    const u64 cap = pma.capacity();
+    k_outdeg<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg.ptr);
+    GPMA_LAUNCH_CHECK();
+    u64 launches = 1;
+    double* x = px.ptr;
+    double* y = py.ptr;
+    *converged = 0;
+    u64 it;
+    pr_iter_ms_ = 0.0;
+    for (it = 1; it <= max_iters; ++it) {
+        GPMA_CUDA(cudaMemsetAsync(psc.ptr, 0, 16, s));
+        GPMA_CUDA(cudaEventRecord(pma_ev(2), s));
+        k_pr_prep<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, outdeg.ptr, nv, d, pshare.ptr, psc.ptr);
+        k_pr_base<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(y, nv, psc.ptr, d);
+        k_pr_push<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y);
+        k_pr_l1<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, y, nv, psc.ptr + 1);
+        GPMA_LAUNCH_CHECK();
+        GPMA_CUDA(cudaEventRecord(pma_ev(3), s));
+        launches += 4;
+        double l1 = 0;
+        GPMA_CUDA(cudaMemcpyAsync(&l1, psc.ptr + 1, 8, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
+        float ms = 0;
+        cudaEventElapsedTime(&ms, pma_ev(2), pma_ev(3));
+        pr_iter_ms_ += ms;
+        std::swap(x, y);
+        if (l1 < eps) {
+            *converged = 1;
+            break;
+        }
+    }
+    *iters = *converged ? it : max_iters;
+    GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
+    GPMA_CUDA(cudaMemcpyAsync(h_ranks, x, nv * 8, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    record_timing(launches);
+    pma.timing.rounds_ms = pr_iter_ms_;
+}
+
+void Graph::spmv(const double* h_x, double* h_y) {
+    cudaStream_t s = pma.stream();
+    px.reserve(nv + 1);
+    py.reserve(nv + 1);
+    if (nv) GPMA_CUDA(cudaMemcpyAsync(px.ptr, h_x, nv * 8, cudaMemcpyHostToDevice, s));
+    GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
+    if (nv) {
+        k_spmv<<<grid_for(nv * 32, 256, 148 * 16), 256, 0, s>>>(ro.ptr, nv, pma.d_keys, pma.d_vals, pma.d_st, px.ptr,
+                                                                py.ptr);
+        GPMA_LAUNCH_CHECK();
+    }
+    GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
+    if (nv) GPMA_CUDA(cudaMemcpyAsync(h_y, py.ptr, nv * 8, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    record_timing(1);
+}
+
+cudaEvent_t Graph::pma_ev(int i) {
+    if (!evs_[i]) GPMA_CUDA(cudaEventCreate(&evs_[i]));
+    return evs_[i];
+}
+
+void Graph::record_timing(u64 launches) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pma_ev(0), pma_ev(1));
+    pma.timing = pma_timing{};
+    pma.timing.device_ms = ms;
+    pma.timing.kernel_launches = launches;
+}
+
+}  // namespace gpma

@@ -1,0 +1,1262 @@
+// pma.cu — device-resident PMA and the GPMA+ batch-update pipeline for
+// sm_100a (the north-star hot path).
+//
+// Per batch (segment_engine.hpp:365-470):
+//   1. varying-bit mask + key compression, stable radix sort of (key, arrival)
+//      (primitives.hpp:21-56)
+//   2. duplicate resolution = ordered compaction of run ends
+//      (segment_engine.hpp:346-363)
+//   3. leaf assignment: binary search of the backward-filled leaf headers
+//      (pma.hpp:234-289)
+//   4. rounds, level by level (segment_engine.hpp:396-465):
+//        group  = ordered compaction of segment heads   (unique_segments)
+//        commit = decide + merge + even placement, fused  (try_insert_plus)
+//                 warp tier (seg <= 32 slots), CTA tier (larger)
+//        advance / touched list = ordered compactions   (advance_round)
+//      root path with grow / forced merge / eager shrink on device-wide
+//      kernels (segment_engine.hpp:435-463, pma.hpp:390-402, 597-601)
+//   5. refresh of leaf headers (+ row offsets for graphs) over touched ranges.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "block_ops.cuh"
+#include "merge.cuh"
+#include "pma_impl.cuh"
+
+namespace gpma {
+
+// ===================================================================== layout
+
+u64 Pma::leaf_size_for(u64 cap) {  // pma.hpp:95-101
+    int lg = 0;
+    while ((1ull << (lg + 1)) <= cap) ++lg;
+    u64 leaf = 4;
+    while (leaf * 2 <= u64(lg)) leaf *= 2;
+    return leaf;
+}
+
+int Pma::height_for(u64 cap, u64 leaf) {
+    int h = 0;
+    for (u64 s = leaf; s < cap; s <<= 1) ++h;
+    return h;
+}
+
+u64 Pma::max_at_capacity(u64 cap) const {  // pma.hpp:590-595
+    const u64 leaf = leaf_size_for(cap);
+    const int h = height_for(cap, leaf);
+    const u64 mx0 = u64(std::floor(prof_.leaf_upper * double(leaf) + 1e-9));
+    return mx0 << h;
+}
+
+static void validate_profile(const pma_profile& d) {  // pma.hpp:59-67
+    if (!(d.leaf_lower > 0.0 && d.leaf_lower < d.root_lower && d.root_lower < d.root_upper &&
+          d.root_upper < d.leaf_upper && d.leaf_upper < 1.0))
+        throw ApiError(PMA_EINVAL, "DensityProfile: need 0 < leaf_lower < root_lower < root_upper < leaf_upper < 1");
+    if (2.0 * d.root_lower > d.root_upper + 1e-12)
+        throw ApiError(PMA_EINVAL, "DensityProfile: need 2*root_lower <= root_upper so a post-shrink root is legal");
+}
+
+Pma::Pma(const pma_profile* profile, int device) : device_(device) {
+    prof_ = profile ? *profile : pma_profile{0.08, 0.92, 0.40, 0.80, 1, 0};
+    validate_profile(prof_);
+    GPMA_CUDA(cudaSetDevice(device_));
+    GPMA_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    GPMA_CUDA(cudaMalloc(&d_ctr, sizeof(Ctr)));
+    GPMA_CUDA(cudaMallocHost(&h_ctr, sizeof(Ctr)));
+    for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
+    reset_layout(16);
+    headers_closed_form(nullptr, 0);
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+Pma::~Pma() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(stream_);
+    free_arrays();
+    if (d_ctr) cudaFree(d_ctr);
+    if (h_ctr) cudaFreeHost(h_ctr);
+    for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Pma::free_arrays() {
+    if (d_keys) cudaFree(d_keys);
+    if (d_vals) cudaFree(d_vals);
+    if (d_st) cudaFree(d_st);
+    if (d_hdr) cudaFree(d_hdr);
+    d_keys = d_vals = d_hdr = nullptr;
+    d_st = nullptr;
+}
+
+// reset_layout (pma.hpp:561-567) + rebuild_bounds (pma.hpp:577-588)
+void Pma::reset_layout(u64 cap) {
+    free_arrays();
+    cap_ = cap;
+    leaf_ = leaf_size_for(cap);
+    height_ = height_for(cap, leaf_);
+    GPMA_CUDA(cudaMalloc(&d_keys, cap * 8));
+    GPMA_CUDA(cudaMalloc(&d_vals, cap * 8));
+    GPMA_CUDA(cudaMalloc(&d_st, cap));
+    GPMA_CUDA(cudaMalloc(&d_hdr, (cap / leaf_) * 8));
+    GPMA_CUDA(cudaMemsetAsync(d_keys, 0, cap * 8, stream_));
+    GPMA_CUDA(cudaMemsetAsync(d_vals, 0, cap * 8, stream_));
+    GPMA_CUDA(cudaMemsetAsync(d_st, 0, cap, stream_));
+    valid_count = 0;
+    tombstone_count = 0;
+    const double lf = double(leaf_);
+    const u64 mn0 = u64(std::ceil(prof_.leaf_lower * lf - 1e-9));
+    const u64 mx0 = u64(std::floor(prof_.leaf_upper * lf + 1e-9));
+    for (int l = 0; l <= height_; ++l) {
+        mn_[l] = mn0 << l;
+        mx_[l] = mx0 << l;
+    }
+}
+
+void Pma::ensure_slot_scratch() {
+    const u64 n = cap_ + 1;
+    ek.reserve(n);
+    ev.reserve(n);
+    ok.reserve(n);
+    ov.reserve(n);
+    es.reserve(n);
+    mb.reserve(n);
+    mflag.reserve(n);
+}
+
+void Pma::sync_ctr() {
+    GPMA_CUDA(cudaMemcpyAsync(h_ctr, d_ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Pma::event(int idx) { GPMA_CUDA(cudaEventRecord(ev_[idx], stream_)); }
+
+// ==================================================================== kernels
+
+// Even placement of k sorted entries over [b, b+m) (pma.hpp:440-467),
+// destination-driven so every store is coalesced.
+__global__ void k_place_evenly(u64* __restrict__ keys, u64* __restrict__ vals, u8* __restrict__ st, u64 b, u64 m,
+                               const u64* __restrict__ ek, const u64* __restrict__ ev, const ull* k_dev, u64 k_host) {
+    const u64 k = k_dev ? *k_dev : k_host;
+    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < m; t += u64(gridDim.x) * blockDim.x) {
+        u64 j;
+        const bool tgt = placement_target(t, k, m, &j);
+        keys[b + t] = tgt ? ek[j] : 0;
+        vals[b + t] = tgt ? ev[j] : 0;
+        st[b + t] = tgt ? kValid : kEmpty;
+    }
+}
+
+// Leaf headers of an array that is one even placement of k entries:
+// hdr[i] = entry ceil(i*leaf*k/C) (the first entry at or after the leaf).
+__global__ void k_headers_closed(u64* hdr, u64 L, u64 leaf, u64 cap, const u64* ek, const ull* k_dev, u64 k_host) {
+    const u64 k = k_dev ? *k_dev : k_host;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < L; i += u64(gridDim.x) * blockDim.x) {
+        const u64 t = i * leaf;
+        const u64 j = k ? (t * k + cap - 1) / cap : 0;
+        hdr[i] = (k && j < k) ? ek[j] : ~0ull;
+    }
+}
+
+__global__ void k_validate_sorted(const u64* keys, u64 n, Ctr* ctr) {
+    for (u64 i = 1 + blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        if (keys[i] <= keys[i - 1]) atomicMin(&ctr->bad_index, ull(i));
+}
+
+__global__ void k_or_mask(const u64* keys, u64 n, Ctr* ctr) {
+    const u64 k0 = keys[0];
+    u64 acc = 0;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        acc |= keys[i] ^ k0;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) acc |= __shfl_xor_sync(FULL, acc, d);
+    if ((threadIdx.x & 31) == 0 && acc) atomicOr(&ctr->mask_or, ull(acc));
+}
+
+struct BitRuns {
+    int n;
+    int lo[16];
+    int len[16];
+    int out[16];
+};
+
+// pext of the varying bits: order-preserving and injective on the batch.
+__global__ void k_compress(const u64* keys, u64 n, BitRuns runs, u64* ck, u32* ci) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const u64 k = keys[i];
+        u64 c = 0;
+        for (int r = 0; r < runs.n; ++r)
+            c |= ((k >> runs.lo[r]) & ((runs.len[r] == 64) ? ~0ull : ((1ull << runs.len[r]) - 1))) << runs.out[r];
+        ck[i] = c;
+        ci[i] = u32(i);
+    }
+}
+
+__global__ void k_iota(u32* p, const ull* n_dev) {
+    const u64 n = *n_dev;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) p[i] = u32(i);
+}
+
+__global__ void k_leaf_search(const u64* __restrict__ uk, const ull* n_dev, const u64* __restrict__ hdr, u64 L,
+                              const u8* __restrict__ st, u64 leaf, u32* __restrict__ ul) {
+    const u64 n = *n_dev;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        ul[i] = u32(leaf_of_key(hdr, L, st, leaf, uk[i]));
+}
+
+// --------------------------------------------------------------- commit args
+
+struct CommitArgs {
+    u64* keys;
+    u64* vals;
+    u8* st;
+    const u64* uk;
+    const u64* uv;
+    const u8* uop;
+    const u32* ul;
+    const u32* pidx;
+    const u32* gstart;
+    u8* gflag;
+    Ctr* ctr;
+    int level;
+    u64 m;
+    u64 leaf;
+    u64 mn;
+    u64 mx;
+    int eager;
+    int large;
+    int cap_gt_min;
+    // CTA-tier scratch (slot space / pending space)
+    u64* ek;
+    u64* ev;
+    u32* es;
+    u8* mflag;
+    u64* ok;
+    u64* ov;
+    u64* ik;
+    u64* iv;
+    u32* ir;
+};
+
+struct Acc {
+    ull committed = 0, missed = 0, tomb = 0, writes = 0, merge = 0;
+    long long vd = 0, td = 0;
+};
+
+__device__ __forceinline__ void flush_acc(const Acc& a, Ctr* ctr) {
+    // called by one thread per CTA with CTA totals
+    if (a.committed) atomicAdd(&ctr->committed, a.committed);
+    if (a.missed) atomicAdd(&ctr->missed, a.missed);
+    if (a.tomb) atomicAdd(&ctr->tomb_added, a.tomb);
+    if (a.writes) atomicAdd(&ctr->slot_writes, a.writes);
+    if (a.merge) atomicAdd(&ctr->merge_slots, a.merge);
+    if (a.vd) atomicAdd(reinterpret_cast<ull*>(&ctr->valid_delta), ull(a.vd));
+    if (a.td) atomicAdd(reinterpret_cast<ull*>(&ctr->tomb_delta), ull(a.td));
+}
+
+__device__ void block_flush(Acc acc, Ctr* ctr) {
+    __shared__ ull s_acc[7];
+    if (threadIdx.x < 7) s_acc[threadIdx.x] = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        if (acc.committed) atomicAdd(&s_acc[0], acc.committed);
+        if (acc.missed) atomicAdd(&s_acc[1], acc.missed);
+        if (acc.tomb) atomicAdd(&s_acc[2], acc.tomb);
+        if (acc.writes) atomicAdd(&s_acc[3], acc.writes);
+        if (acc.merge) atomicAdd(&s_acc[4], acc.merge);
+        if (acc.vd) atomicAdd(&s_acc[5], ull(acc.vd));
+        if (acc.td) atomicAdd(&s_acc[6], ull(acc.td));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Acc t;
+        t.committed = s_acc[0];
+        t.missed = s_acc[1];
+        t.tomb = s_acc[2];
+        t.writes = s_acc[3];
+        t.merge = s_acc[4];
+        t.vd = (long long)s_acc[5];
+        t.td = (long long)s_acc[6];
+        flush_acc(t, ctr);
+    }
+}
+
+// ------------------------------------------------------------- warp tier
+// One warp per group, segment <= 32 slots (leaf and level-1 segments carry
+// >= 99.5% of commits).  The segment lives in registers (one
+// slot per lane), the decision, the merge (ranks via shuffles) and the even
+// re-dispatch happen without leaving the warp; each slot is read once and
+// written once (keys/values 128-B lines per leaf).
+constexpr int kWarpTierWarps = 8;
+
+__global__ void __launch_bounds__(kWarpTierWarps * 32) k_commit_warp(CommitArgs a) {
+    __shared__ u64 s_ok[kWarpTierWarps][32], s_ov[kWarpTierWarps][32], s_ik[kWarpTierWarps][32],
+        s_iv[kWarpTierWarps][32];
+    __shared__ u32 s_ir[kWarpTierWarps][32];
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const ull ngroups = a.ctr->ngroups;
+    const unsigned m = unsigned(a.m);
+    Acc acc;
+    for (ull g = ull(blockIdx.x) * kWarpTierWarps + w; g < ngroups; g += ull(gridDim.x) * kWarpTierWarps) {
+        const u32 lo = a.gstart[g], hi = a.gstart[g + 1];
+        const u32 s = hi - lo;
+        const u64 seg = u64(a.ul[a.pidx[lo]]) >> a.level;
+        const u64 b = seg * m;
+        u8 stt = kEmpty;
+        u64 key = 0;
+        if (lane < m) {
+            stt = a.st[b + lane];
+            key = a.keys[b + lane];
+        }
+        const unsigned valid = __ballot_sync(FULL, stt == kValid);
+        const unsigned nonempty = __ballot_sync(FULL, stt != kEmpty);
+        const unsigned tombm = __ballot_sync(FULL, stt == kTombstone);
+        const unsigned nv = __popc(valid);
+        unsigned ins = 0;
+        for (u32 c = 0; c < s; c += 32) {
+            const bool isins = (c + lane < s) && a.uop[a.pidx[lo + c + lane]] == kOpInsert;
+            ins += __popc(__ballot_sync(FULL, isins));
+        }
+        const u32 dels = s - ins;
+        u8 flag = 0;
+        if (!a.eager && ins == 0) {
+            // commit_tombstones (segment_engine.hpp:285-310): flip matches, no moves
+            unsigned added = 0;
+            for (u32 c = 0; c < s; c += 32) {
+                const bool act = c + lane < s;
+                const u64 u = act ? a.uk[a.pidx[lo + c + lane]] : 0;
+                int hit = -1;
+                for (unsigned t = 0; t < m; ++t) {
+                    const u64 kt = __shfl_sync(FULL, key, t);
+                    if (act && ((nonempty >> t) & 1u) && kt == u) hit = int(t);
+                }
+                const bool flip = act && hit >= 0 && ((valid >> hit) & 1u);
+                if (flip) a.st[b + hit] = kTombstone;
+                added += __popc(__ballot_sync(FULL, flip));
+            }
+            acc.tomb += added;
+            acc.missed += s - added;
+            acc.writes += added;
+            acc.vd -= added;
+            acc.td += added;
+            flag = 1;
+        } else if (nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn)) {
+            flag = 0;  // deferred: escalate with the parent next round
+        } else {
+            // merge (segment_engine.hpp:119-137) + place_evenly (pma.hpp:440-467)
+            unsigned mdel = 0, mins = 0, missed = 0, nins = 0;
+            for (u32 c = 0; c < s; c += 32) {
+                const bool act = c + lane < s;
+                u64 u = 0, uval = 0;
+                u8 op = kOpDelete;
+                if (act) {
+                    const u32 pi = a.pidx[lo + c + lane];
+                    u = a.uk[pi];
+                    op = a.uop[pi];
+                    if (op == kOpInsert) uval = a.uv[pi];
+                }
+                unsigned r = 0;
+                int hit = -1;
+                for (unsigned t = 0; t < m; ++t) {
+                    const u64 kt = __shfl_sync(FULL, key, t);
+                    const bool v = (valid >> t) & 1u;
+                    r += (v && kt < u);
+                    if (v && kt == u) hit = int(t);
+                }
+                const bool isdel = act && op == kOpDelete, isins = act && op == kOpInsert;
+                mdel |= __reduce_or_sync(FULL, (isdel && hit >= 0) ? (1u << hit) : 0u);
+                mins |= __reduce_or_sync(FULL, (isins && hit >= 0) ? (1u << hit) : 0u);
+                missed += __popc(__ballot_sync(FULL, isdel && hit < 0));
+                const unsigned insm = __ballot_sync(FULL, isins);
+                if (isins) {
+                    const unsigned p = nins + __popc(insm & lanemask_lt());
+                    s_ik[w][p] = u;
+                    s_iv[w][p] = uval;
+                    s_ir[w][p] = r;
+                }
+                nins += __popc(insm);
+            }
+            __syncwarp();
+            const unsigned surv = valid & ~(mdel | mins);
+            const unsigned k = __popc(surv) + nins;
+            if ((surv >> lane) & 1u) {
+                const unsigned sr = __popc(surv & lanemask_lt());
+                const unsigned re = __popc(valid & lanemask_lt());
+                unsigned ib = 0;
+                for (unsigned p = 0; p < nins; ++p) ib += s_ir[w][p] <= re;
+                s_ok[w][sr + ib] = key;
+                s_ov[w][sr + ib] = a.vals[b + lane];
+            }
+            if (lane < nins) {
+                const unsigned r = s_ir[w][lane];
+                const unsigned below = (r < nv) ? ((1u << __fns(valid, 0, int(r) + 1)) - 1u) : 0xffffffffu;
+                const unsigned sb = __popc(surv & below);
+                s_ok[w][sb + lane] = s_ik[w][lane];
+                s_ov[w][sb + lane] = s_iv[w][lane];
+            }
+            __syncwarp();
+            if (lane < m) {
+                u64 j = 0;
+                const bool tgt = placement_target(lane, k, m, &j);
+                a.keys[b + lane] = tgt ? s_ok[w][j] : 0;
+                a.vals[b + lane] = tgt ? s_ov[w][j] : 0;
+                a.st[b + lane] = tgt ? kValid : kEmpty;
+            }
+            unsigned moves = 0;
+            if (a.large) {
+                const unsigned pa = valid & ~mdel;
+                const bool in = (pa >> lane) & 1u;
+                moves = __popc(__ballot_sync(FULL, in && unsigned(__popc(pa & lanemask_lt())) != lane));
+            }
+            __syncwarp();
+            acc.missed += missed;
+            acc.writes += m + moves;
+            acc.merge += m;
+            acc.vd += (long long)k - (long long)nv;
+            acc.td -= __popc(tombm);
+            flag = 2;
+        }
+        if (flag) acc.committed++;
+        if (lane == 0) a.gflag[g] = flag;
+    }
+    if (lane != 0) acc = Acc{};
+    block_flush(acc, a.ctr);
+}
+
+// ------------------------------------------------------------- CTA tier
+// Any segment size.  One CTA per group; the segment's Valid entries are
+// compacted to slot-space scratch E, update ranks come from binary searches
+// in E, survivors/inserts scatter to O by rank, and the segment is rewritten
+// by destination-driven placement.  Also the engine of the sequential ops.
+__global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
+    __shared__ ull s_w64[kCtaThreads / 32];
+    const ull ngroups = a.ctr->ngroups;
+    Acc acc;
+    for (ull g = blockIdx.x; g < ngroups; g += gridDim.x) {
+        const u32 lo = a.gstart[g], hi = a.gstart[g + 1];
+        const u64 s = hi - lo;
+        const u64 seg = u64(a.ul[a.pidx[lo]]) >> a.level;
+        const u64 m = a.m;
+        const u64 b = seg * m;
+        SlicePending sl{a.uk, a.uv, a.uop, a.pidx, lo};
+        ull ins = 0;
+        for (u64 q = threadIdx.x; q < s; q += kCtaThreads) ins += sl.op(q) == kOpInsert;
+        ins = block_sum(ins, s_w64);
+        ull nv = 0, nt = 0;
+        for (u64 t = threadIdx.x; t < m; t += kCtaThreads) {
+            const u8 x = a.st[b + t];
+            nv += x == kValid;
+            nt += x == kTombstone;
+        }
+        nv = block_sum(nv, s_w64);
+        nt = block_sum(nt, s_w64);
+        const u64 dels = s - ins;
+        u8 flag = 0;
+        if (!a.eager && ins == 0) {
+            // tombstones: a pending key, if present, still sits in its batch-start
+            // leaf (no commit has rewritten that leaf yet), so probe the leaf.
+            ull added = 0, missed = 0;
+            for (u64 q = threadIdx.x; q < s; q += kCtaThreads) {
+                const u64 u = sl.key(q);
+                const u64 lb = u64(a.ul[a.pidx[lo + q]]) * a.leaf;
+                bool hit = false;
+                for (u64 t = lb; t < lb + a.leaf; ++t) {
+                    if (a.st[t] != kEmpty && a.keys[t] == u) {
+                        if (a.st[t] == kValid) {
+                            a.st[t] = kTombstone;
+                            hit = true;
+                        }
+                        break;
+                    }
+                }
+                added += hit;
+                missed += !hit;
+            }
+            added = block_sum(added, s_w64);
+            missed = block_sum(missed, s_w64);
+            if (threadIdx.x == 0) {
+                acc.tomb += added;
+                acc.missed += missed;
+                acc.writes += added;
+                acc.vd -= (long long)added;
+                acc.td += (long long)added;
+            }
+            flag = 1;
+        } else if (nv + ins > a.mx || (a.eager && a.cap_gt_min && nv < dels + a.mn)) {
+            flag = 0;
+        } else {
+            const MergeOut r = block_merge_segment(a.keys, a.vals, a.st, b, m, nv, sl, s, a.large != 0, a.ek, a.ev,
+                                                   a.es, a.mflag, a.ok, a.ov, a.ik + lo, a.iv + lo, a.ir + lo);
+            if (threadIdx.x == 0) {
+                acc.missed += r.missed;
+                acc.writes += m + r.moves;
+                acc.merge += m;
+                acc.vd += (long long)r.k - (long long)nv;
+                acc.td -= (long long)nt;
+            }
+            flag = 2;
+        }
+        if (threadIdx.x == 0) {
+            a.gflag[g] = flag;
+            if (flag) acc.committed++;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) acc = Acc{};
+    block_flush(acc, a.ctr);
+}
+
+// ------------------------------------------------------------- refresh
+
+// Leaf headers (and graph row offsets, graph.hpp:167-180) over one touched
+// range per CTA: hdr[i] = first non-Empty key at or after leaf i.
+__global__ void k_refresh_ranges(const u64* __restrict__ ranges, u64 nranges, const u64* __restrict__ keys,
+                                 const u8* __restrict__ st, u64 cap, u64 leaf, u64* __restrict__ hdr,
+                                 u64* __restrict__ ro) {
+    for (u64 r = blockIdx.x; r < nranges; r += gridDim.x) {
+        const u64 b = ranges[2 * r], e = ranges[2 * r + 1];
+        for (u64 i = b / leaf + threadIdx.x; i < e / leaf; i += blockDim.x) {
+            u64 v = ~0ull;
+            for (u64 t = i * leaf; t < cap; ++t) {
+                if (st[t] != kEmpty) {
+                    v = keys[t];
+                    break;
+                }
+            }
+            hdr[i] = v;
+        }
+        if (ro) {
+            for (u64 t = b + threadIdx.x; t < e; t += blockDim.x) {
+                if (st[t] == kValid) {
+                    const u64 k = keys[t];
+                    if (is_guard(k)) ro[src_of(k) + 1] = t + 1;
+                }
+            }
+        }
+    }
+}
+
+// Empty leaves left of a touched range inherit its first header.
+__global__ void k_left_walk(const u64* __restrict__ ranges, u64 nranges, const u8* __restrict__ st, u64 leaf,
+                            u64* __restrict__ hdr) {
+    for (u64 r = blockIdx.x * u64(blockDim.x) + threadIdx.x; r < nranges; r += u64(gridDim.x) * blockDim.x) {
+        const u64 la = ranges[2 * r] / leaf;
+        const u64 v = hdr[la];
+        for (u64 i = la; i-- > 0;) {
+            bool empty = true;
+            for (u64 t = i * leaf; t < (i + 1) * leaf; ++t)
+                if (st[t] != kEmpty) {
+                    empty = false;
+                    break;
+                }
+            if (!empty) break;
+            hdr[i] = v;
+        }
+    }
+}
+
+__global__ void k_row_offsets_full(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
+                                   u64* __restrict__ ro) {
+    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < cap; t += u64(gridDim.x) * blockDim.x) {
+        if (st[t] == kValid) {
+            const u64 k = keys[t];
+            if (is_guard(k)) ro[src_of(k) + 1] = t + 1;
+        }
+    }
+}
+
+// ------------------------------------------------------------- root path
+// Device-wide merge of the single root group (segment_engine.hpp:435-463).
+
+__global__ void k_root_ranks(const u64* __restrict__ uk, const u8* __restrict__ uop, const u32* __restrict__ pidx,
+                             const ull* npend_dev, const u64* __restrict__ ek, const ull* nv_dev, u8* mflag,
+                             Ctr* ctr) {
+    const u64 n = *npend_dev, nv = *nv_dev;
+    ull missed = 0;
+    for (u64 p = blockIdx.x * u64(blockDim.x) + threadIdx.x; p < n; p += u64(gridDim.x) * blockDim.x) {
+        const u32 pi = pidx[p];
+        const u64 u = uk[pi];
+        const u64 r = lower_bound_dev(ek, nv, u);
+        const bool isins = uop[pi] == kOpInsert;
+        if (r < nv && ek[r] == u) mflag[r] = isins ? 2 : 1;
+        else if (!isins) ++missed;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) missed += __shfl_xor_sync(FULL, missed, d);
+    if ((threadIdx.x & 31) == 0 && missed) atomicAdd(&ctr->missed, missed);
+}
+
+__global__ void k_root_scatter_surv(const u64* __restrict__ ek, const u64* __restrict__ ev, const ull* nv_dev,
+                                    const u8* __restrict__ mflag, const u32* __restrict__ mbv,
+                                    const u32* __restrict__ irr, const ull* nins_dev, u64* __restrict__ okk,
+                                    u64* __restrict__ ovv) {
+    const u64 nv = *nv_dev, nins = *nins_dev;
+    for (u64 j = blockIdx.x * u64(blockDim.x) + threadIdx.x; j < nv; j += u64(gridDim.x) * blockDim.x) {
+        if (mflag[j] != 0) continue;
+        const u64 pos = (j - mbv[j]) + upper_bound_u32(irr, nins, j);
+        okk[pos] = ek[j];
+        ovv[pos] = ev[j];
+    }
+}
+
+__global__ void k_root_scatter_ins(const u64* __restrict__ ikk, const u64* __restrict__ ivv,
+                                   const u32* __restrict__ irr, const ull* nins_dev, const u32* __restrict__ mbv,
+                                   u64* __restrict__ okk, u64* __restrict__ ovv, Ctr* ctr) {
+    const u64 nins = *nins_dev;
+    for (u64 p = blockIdx.x * u64(blockDim.x) + threadIdx.x; p < nins; p += u64(gridDim.x) * blockDim.x) {
+        const u64 r = irr[p];
+        const u64 pos = (r - mbv[r]) + p;
+        okk[pos] = ikk[p];
+        ovv[pos] = ivv[p];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->k = (ctr->nv - ctr->nmatched) + nins;
+}
+
+// ------------------------------------------------------------- point queries
+
+__global__ void k_search(const u64* __restrict__ q, u64 n, const u64* __restrict__ hdr, u64 L,
+                         const u64* __restrict__ keys, const u64* __restrict__ vals, const u8* __restrict__ st,
+                         u64 leaf, u64* out_vals, u8* found, u64* leaves) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const u64 key = q[i];
+        const u64 lf = leaf_of_key(hdr, L, st, leaf, key);
+        if (leaves) leaves[i] = lf;
+        if (found) {
+            u8 f = 0;
+            u64 v = 0;
+            for (u64 t = lf * leaf; t < (lf + 1) * leaf; ++t) {
+                if (st[t] != kEmpty && keys[t] == key) {
+                    if (st[t] == kValid) {
+                        f = 1;
+                        v = vals[t];
+                    }
+                    break;
+                }
+            }
+            found[i] = f;
+            out_vals[i] = v;
+        }
+    }
+}
+
+__global__ void k_count_valid(const u8* __restrict__ st, u64 b, u64 e, Ctr* ctr) {
+    ull c = 0;
+    for (u64 t = b + blockIdx.x * u64(blockDim.x) + threadIdx.x; t < e; t += u64(gridDim.x) * blockDim.x)
+        c += st[t] == kValid;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(FULL, c, d);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctr->nv, c);
+}
+
+// ========================================================== host pipeline
+
+void Pma::headers_closed_form(const u64* d_ek, u64 k) {
+    const u64 L = num_leaves();
+    k_headers_closed<<<grid_for(L, 256), 256, 0, stream_>>>(d_hdr, L, leaf_, cap_, d_ek, nullptr, k);
+    GPMA_LAUNCH_CHECK();
+}
+
+void Pma::place_root_from(const u64* d_ek, const u64* d_ev, u64 k) {
+    if (k > 0) {
+        k_place_evenly<<<grid_for(cap_, 256, 148 * 32), 256, 0, stream_>>>(d_keys, d_vals, d_st, 0, cap_, d_ek, d_ev,
+                                                                           nullptr, k);
+        GPMA_LAUNCH_CHECK();
+        slot_writes += cap_;
+    }
+    valid_count = k;
+    tombstone_count = 0;
+    headers_closed_form(d_ek, k);
+}
+
+// from_sorted (pma.hpp:160-187): capacity rule on the host, placement on
+// the device.  d_keys/d_vals are device arrays of n strictly increasing keys.
+void Pma::from_sorted_device(const u64* dk, const u64* dv, u64 n, double fill_target) {
+    if (!(fill_target > 0.0 && fill_target <= prof_.leaf_upper + 1e-12))
+        throw ApiError(PMA_EINVAL, "from_sorted: fill_target must be in (0, leaf_upper]");
+    if (n > 1) {
+        GPMA_CUDA(cudaMemsetAsync(d_ctr, 0xFF, sizeof(ull) * 0, stream_));
+        ull init = ~0ull;
+        GPMA_CUDA(cudaMemcpyAsync(&d_ctr->bad_index, &init, sizeof(ull), cudaMemcpyHostToDevice, stream_));
+        k_validate_sorted<<<grid_for(n, 256), 256, 0, stream_>>>(dk, n, d_ctr);
+        GPMA_LAUNCH_CHECK();
+        sync_ctr();
+        if (h_ctr->bad_index != ~0ull)
+            throw ApiError(PMA_EINVAL,
+                           "from_sorted: keys must be strictly increasing (duplicate or unsorted input at index " +
+                               std::to_string(h_ctr->bad_index) + ")");
+    }
+    slot_writes = 0;  // a fresh array (from_sorted returns a new PMA)
+    u64 cap = 16;
+    while (double(n) > fill_target * double(cap)) cap <<= 1;
+    u64 c = cap;
+    // capacity search on the host before allocating
+    auto mx_root = [&](u64 cc) { return max_at_capacity(cc); };
+    auto mn_root = [&](u64 cc) {
+        const u64 lf = leaf_size_for(cc);
+        const u64 mn0 = u64(std::ceil(prof_.leaf_lower * double(lf) - 1e-9));
+        return mn0 << height_for(cc, lf);
+    };
+    while (n > mx_root(c)) c <<= 1;
+    while (c > 16 && n < mn_root(c) && n <= mx_root(c >> 1)) c >>= 1;
+    reset_layout(c);
+    place_root_from(dk, dv, n);
+    if (d_row_offsets) rebuild_row_offsets_full();
+}
+
+void Pma::load_slots(size_t capacity, const u64* keys, const u64* values, const u8* states) {
+    if (capacity < 16 || (capacity & (capacity - 1)))
+        throw ApiError(PMA_EINVAL, "load_slots: capacity must be a power of two >= 16");
+    reset_layout(capacity);
+    GPMA_CUDA(cudaMemcpyAsync(d_st, states, capacity, cudaMemcpyHostToDevice, stream_));
+    // Empty slots must be zero: sanitize on the host copy path
+    std::vector<u64> k(keys, keys + capacity), v(values, values + capacity);
+    u64 nv = 0, nt = 0;
+    for (size_t i = 0; i < capacity; ++i) {
+        if (states[i] == kEmpty) k[i] = v[i] = 0;
+        nv += states[i] == kValid;
+        nt += states[i] == kTombstone;
+    }
+    GPMA_CUDA(cudaMemcpyAsync(d_keys, k.data(), capacity * 8, cudaMemcpyHostToDevice, stream_));
+    GPMA_CUDA(cudaMemcpyAsync(d_vals, v.data(), capacity * 8, cudaMemcpyHostToDevice, stream_));
+    // full header rebuild: one range covering everything + no left walk needed
+    u64 range[2] = {0, capacity};
+    stage_k.reserve(2);
+    GPMA_CUDA(cudaMemcpyAsync(stage_k.ptr, range, 16, cudaMemcpyHostToDevice, stream_));
+    k_refresh_ranges<<<1, 1024, 0, stream_>>>(stage_k.ptr, 1, d_keys, d_st, cap_, leaf_, d_hdr, nullptr);
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    valid_count = nv;
+    tombstone_count = nt;
+    slot_writes = 0;
+}
+
+void Pma::download(u64* keys, u64* values, u8* states) {
+    if (keys) GPMA_CUDA(cudaMemcpyAsync(keys, d_keys, cap_ * 8, cudaMemcpyDeviceToHost, stream_));
+    if (values) GPMA_CUDA(cudaMemcpyAsync(values, d_vals, cap_ * 8, cudaMemcpyDeviceToHost, stream_));
+    if (states) GPMA_CUDA(cudaMemcpyAsync(states, d_st, cap_, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Pma::rebuild_row_offsets_full() {
+    if (!d_row_offsets) return;
+    GPMA_CUDA(cudaMemsetAsync(d_row_offsets, 0, (num_vertices + 1) * 8, stream_));
+    k_row_offsets_full<<<grid_for(cap_, 256, 148 * 16), 256, 0, stream_>>>(d_keys, d_st, cap_, d_row_offsets);
+    GPMA_LAUNCH_CHECK();
+}
+
+// rebuild_at_capacity (pma.hpp:597-601): compact Valid entries, re-place at
+// the root of a fresh array of `cap` slots.
+void Pma::rebuild_at_capacity(u64 cap) {
+    ensure_slot_scratch();
+    u64* dek = ek.ptr;
+    u64* dev = ev.ptr;
+    const u64* kk = d_keys;
+    const u64* vv = d_vals;
+    const u8* ss = d_st;
+    run_compact(
+        stream_, ws, nullptr, cap_, cap_, [=] __device__(ull i) { return ss[i] == kValid; },
+        [=] __device__(ull i, unsigned f, ull x) {
+            if (f) {
+                dek[x] = kk[i];
+                dev[x] = vv[i];
+            }
+        },
+        NoFin{});
+    const u64 n = valid_count;
+    reset_layout(cap);
+    place_root_from(dek, dev, n);
+}
+
+void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n, const EngineCfg& cfg,
+                              pma_stats* out, u64 /*unused*/) {
+    using Clock = std::chrono::steady_clock;
+    const auto t0 = Clock::now();
+    pma_stats st;
+    std::memset(&st, 0, sizeof(st));
+    st.batch_size = n;
+    st.num_levels = height_ + 1;
+    last_ntouched = 0;
+    last_resized = false;
+    timing = pma_timing{};
+    u64 launches = 0;
+    const u64 writes_base = slot_writes;
+    if (n == 0) {
+        st.wall_ns = u64(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+        if (out) *out = st;
+        return;
+    }
+    event(0);
+    // ---- 1. sort (stable, varying bits only) ----
+    GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
+    k_or_mask<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, d_ctr);
+    GPMA_LAUNCH_CHECK();
+    ++launches;
+    sync_ctr();
+    const u64 mask = h_ctr->mask_or;
+    BitRuns runs{};
+    int nbits = 0;
+    for (int bit = 0; bit < 64;) {
+        if (!((mask >> bit) & 1)) {
+            ++bit;
+            continue;
+        }
+        int e = bit;
+        while (e < 64 && ((mask >> e) & 1)) ++e;
+        if (runs.n == 16) {  // too fragmented: fall back to the full key
+            runs.n = 1;
+            runs.lo[0] = 0;
+            runs.len[0] = 64;
+            runs.out[0] = 0;
+            nbits = 64;
+            break;
+        }
+        runs.lo[runs.n] = bit;
+        runs.len[runs.n] = e - bit;
+        runs.out[runs.n] = nbits;
+        nbits += e - bit;
+        runs.n++;
+        bit = e;
+    }
+    sk_in.reserve(n);
+    sk_out.reserve(n);
+    si_in.reserve(n);
+    si_out.reserve(n);
+    k_compress<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, runs, sk_in.ptr, si_in.ptr);
+    GPMA_LAUNCH_CHECK();
+    ++launches;
+    const u64* sorted_ck = sk_in.ptr;
+    const u32* sorted_ci = si_in.ptr;
+    if (nbits > 0 && n > 1) {
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr, int(n), 0, nbits,
+                                        stream_);
+        sort_tmp.reserve(tmp);
+        GPMA_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.ptr, tmp, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr,
+                                                  int(n), 0, nbits, stream_));
+        launches += (nbits + 7) / 8 + 1;
+        sorted_ck = sk_out.ptr;
+        sorted_ci = si_out.ptr;
+    }
+    // ---- 2. resolve duplicates: run ends -> unique updates ----
+    uk.reserve(n);
+    uv.reserve(n);
+    uop.reserve(n);
+    ul.reserve(n);
+    {
+        u64* o_k = uk.ptr;
+        u64* o_v = uv.ptr;
+        u8* o_o = uop.ptr;
+        Ctr* ctr = d_ctr;
+        run_compact(
+            stream_, ws, nullptr, n, n,
+            [=] __device__(ull i) {
+                const bool end = (i + 1 == n) || sorted_ck[i + 1] != sorted_ck[i];
+                return end && dop[sorted_ci[i]] != kOpSkip;
+            },
+            [=] __device__(ull i, unsigned f, ull x) {
+                if (!f) return;
+                // last insert of the run wins (segment_engine.hpp:346-363)
+                u8 op = kOpDelete;
+                u64 val = 0;
+                for (long long j = (long long)i; j >= 0 && sorted_ck[j] == sorted_ck[i]; --j) {
+                    const u32 a = sorted_ci[j];
+                    if (dop[a] == kOpInsert) {
+                        op = kOpInsert;
+                        val = dv ? dv[a] : 0;
+                        break;
+                    }
+                }
+                o_k[x] = dk[sorted_ci[i]];
+                o_v[x] = val;
+                o_o[x] = op;
+            },
+            [=] __device__(ull total) { ctr->n_unique = total; });
+        ++launches;
+    }
+    event(1);
+    // ---- 3. leaf assignment (once per batch) ----
+    k_leaf_search<<<grid_for(n, 256, 148 * 16), 256, 0, stream_>>>(uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st,
+                                                                  leaf_, ul.ptr);
+    GPMA_LAUNCH_CHECK();
+    ++launches;
+    pidx0.reserve(n);
+    pidx1.reserve(n);
+    gid.reserve(n);
+    gstart.reserve(n + 1);
+    gflag.reserve(n);
+    touched.reserve(2 * n + 2);
+    k_iota<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(pidx0.ptr, &d_ctr->n_unique);
+    GPMA_LAUNCH_CHECK();
+    ++launches;
+    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
+    event(2);
+    // ---- 4. rounds ----
+    sync_ctr();
+    u64 npend = h_ctr->n_unique;
+    u64* touched_ptr = touched.ptr;
+    u64 ntouched = 0;
+    u32* pcur = pidx0.ptr;
+    u32* pnext = pidx1.ptr;
+    float seg_ms = 0.f;
+    if (npend > 0) {
+        for (int level = 0;; ++level) {
+            const u64 m = leaf_ << level;
+            // group = segment heads (unique_segments)
+            {
+                const u32* ulp = ul.ptr;
+                const u32* pp = pcur;
+                u32* gs = gstart.ptr;
+                u32* gi = gid.ptr;
+                Ctr* ctr = d_ctr;
+                const int lv = level;
+                run_compact(
+                    stream_, ws, &d_ctr->npend, 0, npend,
+                    [=] __device__(ull p) { return p == 0 || (ulp[pp[p]] >> lv) != (ulp[pp[p - 1]] >> lv); },
+                    [=] __device__(ull p, unsigned f, ull x) {
+                        if (f) gs[x] = u32(p);
+                        gi[p] = u32(x + f - 1);
+                    },
+                    [=] __device__(ull total) {
+                        ctr->ngroups = total;
+                        gs[total] = u32(ctr->npend);
+                    });
+                ++launches;
+            }
+            GPMA_CUDA(cudaMemsetAsync(&d_ctr->committed, 0, sizeof(ull), stream_));
+            // commit (decide + merge + scatter)
+            CommitArgs a{};
+            a.keys = d_keys;
+            a.vals = d_vals;
+            a.st = d_st;
+            a.uk = uk.ptr;
+            a.uv = uv.ptr;
+            a.uop = uop.ptr;
+            a.ul = ul.ptr;
+            a.pidx = pcur;
+            a.gstart = gstart.ptr;
+            a.gflag = gflag.ptr;
+            a.ctr = d_ctr;
+            a.level = level;
+            a.m = m;
+            a.leaf = leaf_;
+            a.mn = mn_[level];
+            a.mx = mx_[level];
+            a.eager = cfg.eager;
+            a.large = cfg.large_for(m);
+            a.cap_gt_min = cap_ > 16;
+            GPMA_CUDA(cudaEventRecord(ev_[5], stream_));
+            if (m <= 32) {
+                const unsigned grid = grid_for(npend, kWarpTierWarps, 148 * 8);
+                k_commit_warp<<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+            } else {
+                ensure_slot_scratch();
+                ik.reserve(n);
+                iv.reserve(n);
+                ir.reserve(n);
+                a.ek = ek.ptr;
+                a.ev = ev.ptr;
+                a.es = es.ptr;
+                a.mflag = mflag.ptr;
+                a.ok = ok.ptr;
+                a.ov = ov.ptr;
+                a.ik = ik.ptr;
+                a.iv = iv.ptr;
+                a.ir = ir.ptr;
+                const unsigned grid = grid_for(npend, 1, 148 * 4);
+                k_commit_cta<<<grid, kCtaThreads, 0, stream_>>>(a);
+            }
+            GPMA_LAUNCH_CHECK();
+            GPMA_CUDA(cudaEventRecord(ev_[6], stream_));
+            ++launches;
+            // touched list (merge commits, in segment order)
+            {
+                const u8* gf = gflag.ptr;
+                const u32* gs = gstart.ptr;
+                const u32* ulp = ul.ptr;
+                const u32* pp = pcur;
+                u64* tp = touched_ptr;
+                const u64 base = ntouched;
+                const int lv = level;
+                Ctr* ctr = d_ctr;
+                run_compact(
+                    stream_, ws, &d_ctr->ngroups, 0, npend, [=] __device__(ull g) { return gf[g] == 2; },
+                    [=] __device__(ull g, unsigned f, ull x) {
+                        if (!f) return;
+                        const u64 seg = u64(ulp[pp[gs[g]]]) >> lv;
+                        tp[2 * (base + x)] = seg * m;
+                        tp[2 * (base + x) + 1] = seg * m + m;
+                    },
+                    [=] __device__(ull total) { ctr->ntouched_next = base + total; });
+                ++launches;
+            }
+            // advance_round: keep deferred groups' updates
+            {
+                const u8* gf = gflag.ptr;
+                const u32* gi = gid.ptr;
+                const u32* pp = pcur;
+                u32* pn = pnext;
+                Ctr* ctr = d_ctr;
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->npend_next, 0, sizeof(ull), stream_));
+                run_compact(
+                    stream_, ws, &d_ctr->npend, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
+                    [=] __device__(ull p, unsigned f, ull x) {
+                        if (f) pn[x] = pp[p];
+                    },
+                    [=] __device__(ull total) { ctr->npend_next = total; });
+                ++launches;
+            }
+            sync_ctr();
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev_[5], ev_[6]);
+            seg_ms += ms;
+            st.rounds++;
+            st.segments_per_level[level] += h_ctr->committed;
+            ntouched = h_ctr->ntouched_next;
+            const u64 left = h_ctr->npend_next;
+            if (left == 0) break;
+            if (level == height_) {
+                // root path: everything left is the single root group
+                std::swap(pcur, pnext);
+                npend = left;
+                GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->npend_next, sizeof(ull), cudaMemcpyDeviceToDevice,
+                                          stream_));
+                // apply the counters of the finished rounds first
+                valid_count = u64((long long)valid_count + h_ctr->valid_delta);
+                tombstone_count = u64((long long)tombstone_count + h_ctr->tomb_delta);
+                slot_writes += h_ctr->slot_writes;
+                st.deletes_missed += h_ctr->missed;
+                st.tombstones_added += h_ctr->tomb_added;
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->valid_delta, 0, sizeof(long long) * 2, stream_));
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->missed, 0, sizeof(ull) * 5, stream_));
+                // inserts in the root slice
+                {
+                    const u8* uo = uop.ptr;
+                    const u32* pp = pcur;
+                    Ctr* ctr = d_ctr;
+                    GPMA_CUDA(cudaMemsetAsync(&d_ctr->root_ins, 0, sizeof(ull), stream_));
+                    run_compact(
+                        stream_, ws, &d_ctr->npend, 0, npend, [=] __device__(ull p) { return uo[pp[p]] == kOpInsert; },
+                        [=] __device__(ull, unsigned, ull) {}, [=] __device__(ull total) { ctr->root_ins = total; });
+                }
+                sync_ctr();
+                const u64 ins = h_ctr->root_ins;
+                while (valid_count + ins > mx_[height_]) {
+                    rebuild_at_capacity(cap_ << 1);
+                    st.grow_events++;
+                }
+                // forced merge at the (possibly grown) root
+                ensure_slot_scratch();
+                ik.reserve(n);
+                iv.reserve(n);
+                ir.reserve(n);
+                {
+                    u64* dek = ek.ptr;
+                    u64* dev = ev.ptr;
+                    u32* des = es.ptr;
+                    u8* mf = mflag.ptr;
+                    const u64* kk = d_keys;
+                    const u64* vv = d_vals;
+                    const u8* ss = d_st;
+                    Ctr* ctr = d_ctr;
+                    run_compact(
+                        stream_, ws, nullptr, cap_, cap_, [=] __device__(ull i) { return ss[i] == kValid; },
+                        [=] __device__(ull i, unsigned f, ull x) {
+                            if (f) {
+                                dek[x] = kk[i];
+                                dev[x] = vv[i];
+                                des[x] = u32(i);
+                                mf[x] = 0;
+                            }
+                        },
+                        [=] __device__(ull total) { ctr->nv = total; });
+                    k_root_ranks<<<grid_for(npend, 256, 148 * 8), 256, 0, stream_>>>(
+                        uk.ptr, uop.ptr, pcur, &d_ctr->npend, dek, &d_ctr->nv, mf, d_ctr);
+                    GPMA_LAUNCH_CHECK();
+                    // ordered insert list with ranks
+                    const u64* uuk = uk.ptr;
+                    const u64* uuv = uv.ptr;
+                    const u8* uuo = uop.ptr;
+                    const u32* pp = pcur;
+                    u64* ikk = ik.ptr;
+                    u64* ivv = iv.ptr;
+                    u32* irr = ir.ptr;
+                    const ull* nvp = &d_ctr->nv;
+                    run_compact(
+                        stream_, ws, &d_ctr->npend, 0, npend, [=] __device__(ull p) { return uuo[pp[p]] == kOpInsert; },
+                        [=] __device__(ull p, unsigned f, ull x) {
+                            if (!f) return;
+                            const u64 u = uuk[pp[p]];
+                            ikk[x] = u;
+                            ivv[x] = uuv[pp[p]];
+                            irr[x] = u32(lower_bound_dev(dek, *nvp, u));
+                        },
+                        [=] __device__(ull total) { ctr->nins = total; });
+                    // matched-before prefix over E
+                    u32* mbv = mb.ptr;
+                    run_compact(
+                        stream_, ws, &d_ctr->nv, 0, cap_ + 1, [=] __device__(ull j) { return mf[j] != 0; },
+                        [=] __device__(ull j, unsigned, ull x) { mbv[j] = u32(x); },
+                        [=] __device__(ull total) {
+                            ctr->nmatched = total;
+                            mbv[ctr->nv] = u32(total);
+                        });
+                    // the compaction's fin is skipped when nv == 0: seed mb[0]
+                    if (true) {
+                        // nv may be zero: make mb[nv] valid via a tiny kernel-free path
+                        // (handled below by k_root_scatter_ins reading mb[r] with r<=nv)
+                    }
+                    k_root_scatter_surv<<<grid_for(cap_, 256, 148 * 16), 256, 0, stream_>>>(
+                        dek, dev, &d_ctr->nv, mf, mbv, irr, &d_ctr->nins, ok.ptr, ov.ptr);
+                    GPMA_LAUNCH_CHECK();
+                    sync_ctr();
+                    if (h_ctr->nv == 0) {
+                        const u32 zero = 0;
+                        GPMA_CUDA(cudaMemcpyAsync(mbv, &zero, 4, cudaMemcpyHostToDevice, stream_));
+                        h_ctr->nmatched = 0;
+                        GPMA_CUDA(cudaMemsetAsync(&d_ctr->nmatched, 0, sizeof(ull), stream_));
+                    }
+                    k_root_scatter_ins<<<grid_for(npend, 256, 148 * 8), 256, 0, stream_>>>(
+                        ikk, ivv, irr, &d_ctr->nins, mbv, ok.ptr, ov.ptr, d_ctr);
+                    GPMA_LAUNCH_CHECK();
+                    if (cfg.large_for(cap_)) {
+                        GPMA_CUDA(cudaMemsetAsync(&d_ctr->moves, 0, sizeof(ull), stream_));
+                        run_compact(
+                            stream_, ws, &d_ctr->nv, 0, cap_ + 1, [=] __device__(ull j) { return mf[j] != 1; },
+                            [=] __device__(ull j, unsigned f, ull x) {
+                                if (f && u64(des[j]) != x) atomicAdd(&ctr->moves, 1ull);
+                            },
+                            NoFin{});
+                    }
+                    sync_ctr();
+                }
+                const u64 k = h_ctr->k;
+                const u64 moves = cfg.large_for(cap_) ? h_ctr->moves : 0;
+                st.deletes_missed += h_ctr->missed;
+                // write the root: every slot rewritten (place_evenly / commit_in_place)
+                k_place_evenly<<<grid_for(cap_, 256, 148 * 32), 256, 0, stream_>>>(d_keys, d_vals, d_st, 0, cap_,
+                                                                                   ok.ptr, ov.ptr, nullptr, k);
+                GPMA_LAUNCH_CHECK();
+                slot_writes += cap_ + moves;
+                valid_count = k;
+                tombstone_count = 0;
+                headers_closed_form(ok.ptr, k);
+                st.num_levels = height_ + 1;
+                st.segments_per_level[height_]++;
+                st.rounds++;
+                if (cfg.eager && prof_.allow_shrink) {
+                    bool shrunk = false;
+                    while (cap_ > 16 && valid_count < mn_[height_]) {
+                        rebuild_at_capacity(cap_ >> 1);
+                        shrunk = true;
+                    }
+                    if (shrunk) st.shrink_events++;
+                }
+                st.resized = st.grow_events > 0 || st.shrink_events > 0;
+                if (!st.resized) {
+                    const u64 pair[2] = {0, cap_};
+                    GPMA_CUDA(cudaMemcpyAsync(touched_ptr + 2 * ntouched, pair, 16, cudaMemcpyHostToDevice, stream_));
+                    ntouched++;
+                }
+                // counters already applied; clear device deltas
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->valid_delta, 0, sizeof(long long) * 2, stream_));
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->missed, 0, sizeof(ull) * 5, stream_));
+                sync_ctr();
+                break;
+            }
+            std::swap(pcur, pnext);
+            npend = left;
+            GPMA_CUDA(
+                cudaMemcpyAsync(&d_ctr->npend, &d_ctr->npend_next, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
+        }
+    }
+    // apply device counters
+    valid_count = u64((long long)valid_count + h_ctr->valid_delta);
+    tombstone_count = u64((long long)tombstone_count + h_ctr->tomb_delta);
+    slot_writes += h_ctr->slot_writes;
+    st.deletes_missed += h_ctr->missed;
+    st.tombstones_added += h_ctr->tomb_added;
+    timing.merge_slots = h_ctr->merge_slots;
+    timing.tombstone_flips = st.tombstones_added;
+    event(3);
+    // ---- 5. refresh leaf headers / row offsets ----
+    last_resized = st.resized;
+    last_ntouched = ntouched;
+    if (st.resized) {
+        // headers already rebuilt in closed form by the final placement
+        if (d_row_offsets) rebuild_row_offsets_full();
+    } else if (ntouched > 0) {
+        k_refresh_ranges<<<grid_for(ntouched, 1, 148 * 8), 256, 0, stream_>>>(touched_ptr, ntouched, d_keys, d_st, cap_,
+                                                                                leaf_, d_hdr, d_row_offsets);
+        GPMA_LAUNCH_CHECK();
+        k_left_walk<<<grid_for(ntouched, 128, 148 * 4), 128, 0, stream_>>>(touched_ptr, ntouched, d_st, leaf_, d_hdr);
+        GPMA_LAUNCH_CHECK();
+        launches += 2;
+    }
+    event(4);
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    st.slot_writes = slot_writes - writes_base;
+    st.num_touched_ranges = ntouched;
+    st.segment_phase_ns = u64(double(seg_ms) * 1e6);
+    float a = 0, b = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+    cudaEventElapsedTime(&c, ev_[2], ev_[3]);
+    cudaEventElapsedTime(&d, ev_[3], ev_[4]);
+    timing.sort_ms = a;
+    timing.search_ms = b;
+    timing.rounds_ms = c;
+    timing.refresh_ms = d;
+    timing.device_ms = a + b + c + d;
+    timing.kernel_launches = launches;
+    st.wall_ns = u64(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
+    if (out) *out = st;
+}
+
+void Pma::touched_ranges(u64* pairs, size_t capn, size_t* count) {
+    *count = last_ntouched;
+    const size_t n = std::min<size_t>(capn, last_ntouched);
+    if (n && pairs) {
+        GPMA_CUDA(cudaMemcpyAsync(pairs, touched.ptr, n * 16, cudaMemcpyDeviceToHost, stream_));
+        GPMA_CUDA(cudaStreamSynchronize(stream_));
+    }
+}
+
+void Pma::binary_search_leaf(const u64* keys, size_t n, u64* leaves) {
+    if (n == 0) return;
+    const u64* dq = stage(stage_k, keys, n);
+    stage_v.reserve(n);
+    k_search<<<grid_for(n, 256), 256, 0, stream_>>>(dq, n, d_hdr, num_leaves(), d_keys, d_vals, d_st, leaf_, nullptr,
+                                                     nullptr, stage_v.ptr);
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaMemcpyAsync(leaves, stage_v.ptr, n * 8, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Pma::search(const u64* keys, size_t n, u64* values, u8* found) {
+    if (n == 0) return;
+    const u64* dq = stage(stage_k, keys, n);
+    stage_v.reserve(n);
+    stage_o.reserve(n);
+    k_search<<<grid_for(n, 256), 256, 0, stream_>>>(dq, n, d_hdr, num_leaves(), d_keys, d_vals, d_st, leaf_,
+                                                     stage_v.ptr, stage_o.ptr, nullptr);
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaMemcpyAsync(values, stage_v.ptr, n * 8, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaMemcpyAsync(found, stage_o.ptr, n, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+u64 Pma::count_valid_in(u64 b, u64 e) {
+    if (e > cap_ || b > e) throw ApiError(PMA_ERANGE, "count_valid_in: range outside the slot array");
+    GPMA_CUDA(cudaMemsetAsync(&d_ctr->nv, 0, sizeof(ull), stream_));
+    if (e > b) {
+        k_count_valid<<<grid_for(e - b, 256), 256, 0, stream_>>>(d_st, b, e, d_ctr);
+        GPMA_LAUNCH_CHECK();
+    }
+    sync_ctr();
+    return h_ctr->nv;
+}
+
+}  // namespace gpma

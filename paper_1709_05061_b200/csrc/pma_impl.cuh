@@ -1,0 +1,182 @@
+// pma_impl.cuh — device-resident Packed Memory Array and the GPMA+ batch
+// pipeline (host orchestration of the sm_100a kernels in pma.cu).
+//
+// HBM layout (SoA, 17 B/slot):
+//   keys   u64[C]   values u64[C]   states u8[C]     (Empty slot = all zero)
+//   hdr    u64[C/leaf]  backward-filled leaf headers: first non-Empty key at
+//                       or after the leaf's first slot, UINT64_MAX if none.
+//                       upper_bound(hdr, key) - 1 == binary_search_leaf(key)
+//                       (pma.hpp:234-245); maintained incrementally.
+// Per-batch scratch is grow-only and sized by the batch; the slot-space
+// merge scratch (E/O arrays) is allocated on first use of the CTA/grid tiers.
+#pragma once
+
+#include <chrono>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace gpma {
+
+// Device-side per-batch counters (one D2H per round).
+struct Ctr {
+    ull n_unique;
+    ull npend;
+    ull ngroups;
+    ull npend_next;
+    ull missed;
+    ull tomb_added;
+    ull slot_writes;
+    ull merge_slots;
+    ull committed;
+    long long valid_delta;
+    long long tomb_delta;
+    ull ntouched_next;
+    ull guard_deletes;
+    ull bad_index;
+    ull root_ins;
+    ull moves;
+    ull mask_or;
+    ull nv;
+    ull nmatched;
+    ull nins;
+    ull nsurv;
+    ull k;
+    ull nt;
+    ull key0;
+    ull pad[8];
+};
+
+struct EngineCfg {
+    bool eager = false;
+    u64 small_max = 32;
+    u64 medium_max = 1024;
+    int force = PMA_STRATEGY_AUTO;
+    bool large_for(u64 m) const {
+        if (force >= 0) return force == PMA_STRATEGY_LARGE;
+        return m > medium_max && m > small_max;
+    }
+};
+
+struct SeqArgs;
+
+class Pma {
+public:
+    explicit Pma(const pma_profile* profile, int device);
+    ~Pma();
+
+    // --- geometry (PmaLayout, pma.hpp:82-123; bounds pma.hpp:577-588) ---
+    static u64 leaf_size_for(u64 cap);
+    static int height_for(u64 cap, u64 leaf);
+    u64 capacity() const { return cap_; }
+    u64 leaf() const { return leaf_; }
+    int height() const { return height_; }
+    u64 num_leaves() const { return cap_ / leaf_; }
+    u64 min_entries(int l) const { return mn_[l]; }
+    u64 max_entries(int l) const { return mx_[l]; }
+    u64 max_at_capacity(u64 cap) const;
+    const pma_profile& profile() const { return prof_; }
+
+    // --- API ---
+    void from_sorted_device(const u64* d_keys, const u64* d_vals, u64 n, double fill_target);
+    void load_slots(size_t capacity, const u64* keys, const u64* values, const u8* states);
+    void download(u64* keys, u64* values, u8* states);
+    void batch_update_device(const u64* d_keys, const u64* d_vals, const u8* d_ops, u64 n, const EngineCfg& cfg,
+                             pma_stats* out, u64 ext_guard_deletes_dev_slot = 0);
+    void binary_search_leaf(const u64* keys, size_t n, u64* leaves);
+    void search(const u64* keys, size_t n, u64* values, u8* found);
+    u64 count_valid_in(u64 b, u64 e);
+    void touched_ranges(u64* pairs, size_t cap, size_t* count);
+
+    // sequential single-key ops (pma.hpp:294-386, 471-479)
+    void insert(u64 key, u64 value);
+    bool erase(u64 key);
+    bool mark_tombstone(u64 key);
+    void redispatch(int level, u64 seg, const u64* keys, const u64* values, size_t n);
+
+    // row-offset maintenance hook used by the graph (graph.hpp:167-190):
+    // when non-null, every refresh also rewrites ro[src+1] for guards.
+    u64* d_row_offsets = nullptr;
+    u64 num_vertices = 0;
+    void rebuild_row_offsets_full();
+    SeqArgs seq_args(int op);
+
+    // staging for host-facing APIs
+    template <typename T>
+    T* stage(DevBuf<T>& buf, const T* host, size_t n) {
+        buf.reserve(n ? n : 1);
+        if (n) GPMA_CUDA(cudaMemcpyAsync(buf.ptr, host, n * sizeof(T), cudaMemcpyHostToDevice, stream_));
+        return buf.ptr;
+    }
+
+    cudaStream_t stream() const { return stream_; }
+    int device() const { return device_; }
+    std::string err;
+    pma_timing timing{};
+
+    u64 valid_count = 0;
+    u64 tombstone_count = 0;
+    u64 slot_writes = 0;
+    bool last_resized = false;
+    u64 last_ntouched = 0;
+
+    // device slot arrays
+    u64* d_keys = nullptr;
+    u64* d_vals = nullptr;
+    u8* d_st = nullptr;
+    u64* d_hdr = nullptr;
+
+    // staging buffers for host APIs
+    DevBuf<u64> stage_k, stage_v;
+    DevBuf<u8> stage_o;
+    DevBuf<u32> stage_a, stage_b, stage_c, stage_d;
+    DevBuf<double> stage_w;
+
+    ScanWorkspace ws;
+
+public:  // (extended __device__ lambdas need public enclosing functions)
+    void reset_layout(u64 cap);  // allocate zeroed arrays, bounds
+    void free_arrays();
+    void rebuild_at_capacity(u64 cap);
+    void place_root_from(const u64* d_ek, const u64* d_ev, u64 k);  // even placement at root + headers
+    void headers_closed_form(const u64* d_ek, u64 k);
+    void refresh_after_batch();
+    void root_path(const EngineCfg& cfg, pma_stats& st, u64 level_committed_base);
+    void ensure_slot_scratch();
+    void sync_ctr();
+    void event(int idx);
+
+    int device_ = 0;
+    cudaStream_t stream_ = nullptr;
+    pma_profile prof_{};
+    u64 cap_ = 0, leaf_ = 4;
+    int height_ = 0;
+    u64 mn_[PMA_MAX_LEVELS]{}, mx_[PMA_MAX_LEVELS]{};
+
+    // counters
+    Ctr* d_ctr = nullptr;
+    Ctr* h_ctr = nullptr;  // pinned
+
+    // batch scratch
+    DevBuf<u64> sk_in, sk_out;   // compressed keys
+    DevBuf<u32> si_in, si_out;   // arrival index payload
+    DevBuf<unsigned char> sort_tmp;
+    DevBuf<u64> uk, uv;
+    DevBuf<u8> uop;
+    DevBuf<u32> ul;
+    DevBuf<u32> pidx0, pidx1, gid, gstart;
+    DevBuf<u8> gflag;
+    DevBuf<u64> touched;  // pairs (b, e)
+    DevBuf<u64> ik, iv;   // insert lists (pending space)
+    DevBuf<u32> ir;
+    // slot-space merge scratch (CTA/grid tiers, root path)
+    DevBuf<u64> ek, ev, ok, ov;
+    DevBuf<u32> es, mb;
+    DevBuf<u8> mflag;
+
+    cudaEvent_t ev_[8]{};
+};
+
+}  // namespace gpma

@@ -1,0 +1,137 @@
+"""GPU parity of DynamicGraph + analytics against the UNMODIFIED reference
+(oracle/_ref): after every sliding-window batch the slot array, UpdateStats
+and row offsets are bit-exact; BFS levels and CC labels are bit-exact; SpMV
+is bit-exact (ordered accumulation, no FMA); PageRank within 1e-6 max-abs
+per vertex (north_star tolerance) with equal iteration counts."""
+import numpy as np
+import pytest
+
+from oracle.oracle import RefGraph, RefStream, RefWindow
+from paper_1709_05061_b200.abi import PMA_EAGER, PMA_LAZY, graph_config
+from paper_1709_05061_b200.pmagraph import (DynamicGraph, GraphConfig, bfs, connected_components, pagerank, spmv)
+from tests.helpers import assert_same_slots, ref_parity
+
+pytestmark = pytest.mark.gpu
+
+PR_TOL = 1e-6  # north_star: PageRank within 1e-6 max abs error per vertex
+
+
+def example():
+    # test_graph.cpp:16-19 worked example (paper Fig. 6)
+    return 3, [0, 0, 1, 2, 2, 2], [0, 2, 2, 0, 1, 2], [1.0, 2.0, 3.0, 4.0, 5.0, 6.0]
+
+
+def test_worked_example_csr_and_analytics():
+    nv, s, d, w = example()
+    g = DynamicGraph.from_edges(nv, s, d, w)
+    ro, col, val = g.csr_snapshot()
+    assert list(ro) == [0, 2, 3, 6]
+    assert list(col) == [0, 2, 2, 0, 1, 2]
+    assert list(val) == [1, 2, 3, 4, 5, 6]
+    assert list(bfs(g, 0)) == [0, 2, 1]                   # test_analytics.cpp:37-42
+    assert list(connected_components(g)) == [0, 0, 0]     # :60-64
+    assert list(spmv(g, [1.0, 1.0, 1.0])) == [3, 3, 15]   # :157-163
+    with pytest.raises(ValueError):
+        spmv(g, [1.0])
+
+
+def test_pagerank_small_known_answers():
+    g = DynamicGraph.from_edges(1, [], [])
+    r = pagerank(g)
+    assert r.converged and list(r.ranks) == [1.0]
+    g2 = DynamicGraph.from_edges(2, [0, 1], [1, 0])
+    r2 = pagerank(g2)
+    assert r2.converged and abs(r2.ranks[0] - 0.5) < 1e-12 and abs(r2.ranks[1] - 0.5) < 1e-12
+
+
+def test_out_of_range_ids_rejected():
+    with pytest.raises(ValueError, match=r"edge \(0, 7\) outside vertex range 3"):
+        DynamicGraph.from_edges(3, [0], [7])
+    g = DynamicGraph.from_edges(3, [0], [1])
+    with pytest.raises(ValueError, match="outside vertex range"):
+        g.apply_batch([5], [0], [1.0], [], [])
+
+
+def test_random_graphs_from_edges_match_reference():
+    rng = np.random.default_rng(77)
+    for trial in range(10):
+        nv = int(rng.integers(1, 3000))
+        ne = int(rng.integers(0, 20000))
+        s = rng.integers(0, nv, ne)
+        d = rng.integers(0, nv, ne)
+        w = rng.integers(0, 100, ne).astype(float)
+        g = DynamicGraph.from_edges(nv, s, d, w)
+        r = RefGraph(nv, s, d, w)
+        assert_same_slots(g.pma().slots(), r.slots(), f"trial {trial}")
+        assert (g.row_offsets() == r.row_offsets()).all()
+        a, b = g.csr_snapshot(), r.csr_snapshot()
+        assert all((x == y).all() for x, y in zip(a, b))
+
+
+def _window_stream(kind, nv, param, seed=1, shuffle=2):
+    if kind == "er":
+        st = RefStream.erdos_renyi(nv, param, seed)
+    else:
+        st = RefStream.rmat(nv, param, seed)
+    if shuffle is not None:
+        st.shuffle(shuffle)
+    return st
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+@pytest.mark.parametrize("kind,nv,param,batch", [("er", 4096, 2**-7, 512), ("rmat", 2**13, 60000, 1500),
+                                                  ("rmat", 2**12, 30000, 7)])
+def test_sliding_window_parity(mode, kind, nv, param, batch):
+    stream = _window_stream(kind, nv, param, shuffle=2 if kind == "er" else None)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    cfg = GraphConfig(deletion_mode=mode)
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half], cfg)
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config(deletion_mode=mode))
+    assert_same_slots(g.pma().slots(), r.slots(), "init")
+    win = RefWindow(stream)
+    rng = np.random.default_rng(3)
+    warm_g = warm_r = None
+    for slide in range(6):
+        a, b, ww, c, dd = win.slide(batch)
+        gs = g.apply_batch(a, b, ww, c, dd)
+        rs = r.apply_batch(a, b, ww, c, dd)
+        ctx = f"slide {slide}"
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
+        root = int(rng.integers(0, nv))
+        assert (bfs(g, root) == r.bfs(root)).all(), ctx
+        assert (connected_components(g) == r.cc()).all(), ctx
+        pg = pagerank(g, warm_start=warm_g)
+        pr = r.pagerank(warm=warm_r)
+        assert np.abs(pg.ranks - pr[0]).max() <= PR_TOL, ctx
+        assert pg.iterations == pr[1] and pg.converged == pr[2], ctx
+        warm_g, warm_r = pg.ranks, pr[0]
+        x = rng.random(nv)
+        assert (spmv(g, x) == r.spmv(x)).all(), ctx
+
+
+def test_pagerank_fixed_iterations_tight():
+    rng = np.random.default_rng(107)
+    for _ in range(3):
+        nv, ne = 500, 3000
+        s, d = rng.integers(0, nv, ne), rng.integers(0, nv, ne)
+        g = DynamicGraph.from_edges(nv, s, d)
+        r = RefGraph(nv, s, d)
+        pg = pagerank(g, epsilon=0.0, max_iters=25)
+        pr = r.pagerank(epsilon=0.0, max_iters=25)
+        assert pg.iterations == 25 and not pg.converged
+        assert np.abs(pg.ranks - pr[0]).max() <= 1e-12
+
+
+def test_guard_deletes_are_dropped_and_counted():
+    nv, s, d, w = example()
+    g = DynamicGraph.from_edges(nv, s, d, w)
+    r = RefGraph(nv, s, d, w)
+    args = ([1], [0], [7.0], [0, 2, 1], [0xFFFFFFFF, 1, 1])
+    gs = g.apply_batch(*args)
+    rs = r.apply_batch(*args)
+    assert gs.parity() == ref_parity(r, rs)
+    assert gs.deletes_missed == rs.deletes_missed
+    assert_same_slots(g.pma().slots(), r.slots())
