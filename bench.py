@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""bench.py — GPMA+ sliding-window update throughput on B200 (+ analytics).
+
+Metric (BASELINE.json): "GPMA+ updates/sec vs batch size; BFS/PageRank/CC
+time per sliding window".  A step is one slide of the C2 workload
+(configs[1]): an RMAT 2^21 / 30.6M-edge stream (gen_rmat seed 1, shuffle
+seed 2, generators.hpp:26-63 + streaming.hpp:58-67) whose first half seeds the
+window; each slide inserts the next B arrivals and deletes the expired edges
+whose multiplicity reaches zero (streaming.hpp:107-123).  updates = the
+reference's UpdateStats::batch_size (inserts + non-guard deletes).
+
+  value : updates/s with the slide batches already resident in HBM,
+          CUDA events on the library's own stream around K steps.
+  e2e   : the same K slides through the host C ABI (gpma_apply_batch) from
+          pinned host buffers: H2D of inputs + D2H of the stats in the region.
+  --impl reference : the unmodified reference (oracle/_ref) on the host cores
+          (all hardware threads), same config/metric.
+
+N > 1 (torchrun): every rank owns an independent source-vertex shard of the
+same shape (its own stream seed), so there is no data-path collective;
+value = all ranks' updates / max-over-ranks time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GPMA+ updates/sec vs batch size; BFS/PageRank/CC time per sliding window"
+UNIT = "updates/s"
+NV = 1 << 21
+NE = 30_600_000
+GEN_SEED, SHUFFLE_SEED, ROOT_SEED = 1, 2, 7
+BYTES_PER_MERGE_SLOT = 34  # 17 B read + 17 B write per rewritten slot
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1_000_000)
+    ap.add_argument("--sweep", default="100,1000,10000,100000,1000000")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-analytics", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no sweep/baseline/analytics)")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ ours --
+
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1709_05061_b200 import pmagraph as pg
+
+    dev = local
+    B = args.batch
+    K, W = args.steps, args.warmup
+    t0 = time.time()
+    stream = pg.EdgeStream.rmat(NV, NE, seed=GEN_SEED + rank).shuffle(SHUFFLE_SEED)
+    gen_s = time.time() - t0
+    win = pg.SlidingWindow(stream, dev)
+    info = win.info()
+    win.reserve((W + K) * B + 16)
+    info = win.info()
+    t1 = time.time()
+    g = pg.DynamicGraph.from_edges_device(NV, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
+    load_s = time.time() - t1
+    cap = g.pma().capacity()
+    slides = [win.slide(B) for _ in range(W + K)]
+    info = win.info()
+    lib = g._lib
+    ext = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
+
+    def apply_dev(graph, s):
+        return graph.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset,
+                                        None, s.n_ins, info.del_src + 4 * s.del_offset,
+                                        info.del_dst + 4 * s.del_offset, s.n_del)
+
+    for s in slides[:W]:
+        apply_dev(g, s)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(ext)
+    updates = 0
+    seg_ms = 0.0
+    merge_slots = 0
+    launches = 0
+    rounds = 0
+    stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
+    for s in slides[W:]:
+        st = apply_dev(g, s)
+        tm = g.last_timing()
+        updates += st.batch_size
+        seg_ms += st.segment_phase_ns / 1e6
+        merge_slots += tm.merge_slots
+        launches += tm.kernel_launches
+        rounds += st.rounds
+        for k in stage:
+            stage[k] += getattr(tm, k)
+    ev1.record(ext)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    # max over ranks
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        u = torch.tensor([float(updates)], device="cuda")
+        torch.distributed.all_reduce(u)
+        ms_max, total_updates = float(t.item()), float(u.item())
+    else:
+        ms_max, total_updates = ms, float(updates)
+    value = total_updates / (ms_max / 1e3)
+
+    # ---- e2e through the host C ABI from pinned buffers (same slides) ----
+    g2 = pg.DynamicGraph.from_edges_device(NV, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
+    hs, hd = stream.arrays()
+    host = []
+    for s in slides:
+        a = torch.from_numpy(hs[s.ins_offset:s.ins_offset + s.n_ins]).pin_memory()
+        b = torch.from_numpy(hd[s.ins_offset:s.ins_offset + s.n_ins]).pin_memory()
+        c = torch.empty(s.n_del, dtype=torch.int32).pin_memory()
+        d = torch.empty(s.n_del, dtype=torch.int32).pin_memory()
+        win.deletions_host(s.del_offset, s.n_del, c.numpy().view(np.uint32), d.numpy().view(np.uint32))
+        host.append((a.numpy().view(np.uint32), b.numpy().view(np.uint32), c.numpy().view(np.uint32),
+                     d.numpy().view(np.uint32), (a, b, c, d)))
+    for a, b, c, d, _ in host[:W]:
+        g2.apply_batch(a, b, None, c, d, with_touched=False)
+    ext2 = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g2.h), device=torch.device("cuda", dev))
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    h2d = d2h = 0
+    e2e_updates = 0
+    e0.record(ext2)
+    for a, b, c, d, _ in host[W:]:
+        st = g2.apply_batch(a, b, None, c, d, with_touched=False)
+        e2e_updates += st.batch_size
+        h2d += a.nbytes + b.nbytes + c.nbytes + d.nbytes
+        d2h += 632  # pma_stats read back every step
+    e1.record(ext2)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        u = torch.tensor([float(e2e_updates)], device="cuda")
+        torch.distributed.all_reduce(u)
+        e2e_ms, e2e_updates = float(t.item()), float(u.item())
+    e2e = {"value": e2e_updates / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
+           "d2h_bytes_per_step": d2h // K}
+    del g2
+
+    # ---- roofline of the dominant kernel (warp-tier commit: decide+merge+scatter) ----
+    peak, peak_kind = measured_peak()
+    achieved = (BYTES_PER_MERGE_SLOT * merge_slots / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            traffic = json.load(f).get("commit_kernel_dram_bytes_per_launch")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": "k_commit_warp (decide + merge + even re-dispatch)",
+                "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_step": BYTES_PER_MERGE_SLOT * merge_slots // K,
+                "kernel_ms_per_step": seg_ms / K, "step_ms": ms / K,
+                "stage_ms_per_step": {k: v / K for k, v in stage.items()}}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+           "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "u64", "data": "synthetic: RMAT stream restated from generators.hpp (seed 1+rank, shuffle 2)",
+           "config": {"workload": "C2 Pokec-shaped sliding window: RMAT 2^21 vertices / 30.6M-edge stream, "
+                                  "15.3M-edge window, GPMA+ apply_batch per slide",
+                      "batch": B, "num_vertices": NV, "stream_edges": NE, "pma_capacity": cap,
+                      "parallelism": f"dp{world} (independent source-range shards)",
+                      "l2": "inputs larger than L2 (PMA slot array 1.1 GB per GPU)",
+                      "deletion_mode": "lazy", "rounds_per_step": rounds / K},
+           "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk,
+           "setup_s": {"generate": round(gen_s, 2), "from_edges": round(load_s, 3)}}
+
+    if rank == 0 and not args.profile:
+        if not args.no_analytics:
+            out["analytics"] = analytics(pg, g, ext)
+        out["sweep"] = sweep(pg, stream, dev, [int(x) for x in args.sweep.split(",") if x])
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(stream, slides, win, W)
+    if world > 1:
+        torch.distributed.barrier()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def analytics(pg, g, ext):
+    """Per-window analytic time on the live gapped graph (bench.hpp:226-313)."""
+    import torch
+    roots = pg.draw_below_sequence(ROOT_SEED, NV, 5)
+    bfs_ms, reached = [], []
+    for r in roots:
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        _, n = pg.bfs(g, int(r), return_reached=True)
+        bfs_ms.append((time.perf_counter() - t) * 1e3)
+        reached.append(int(n))
+    # roots among non-isolated vertices (SURVEY §8d BFS-root caveat)
+    ro = g.row_offsets()
+    deg = np.diff(ro.astype(np.int64))
+    nz = np.nonzero(deg > 1)[0]
+    rng = np.random.default_rng(ROOT_SEED)
+    hub_ms = []
+    for r in rng.choice(nz, 3):
+        t = time.perf_counter()
+        _, n = pg.bfs(g, int(r), return_reached=True)
+        hub_ms.append(((time.perf_counter() - t) * 1e3, int(n)))
+    t = time.perf_counter()
+    pg.connected_components(g)
+    cc_ms = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    pr = pg.pagerank(g)
+    pr_ms = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    pr2 = pg.pagerank(g, warm_start=pr.ranks)
+    pr2_ms = (time.perf_counter() - t) * 1e3
+    return {"bfs_ms_reference_roots": bfs_ms, "bfs_reached": reached,
+            "bfs_ms_nonisolated_roots": [x[0] for x in hub_ms], "bfs_reached_nonisolated": [x[1] for x in hub_ms],
+            "cc_ms": cc_ms, "pagerank_ms_cold": pr_ms, "pagerank_iters_cold": pr.iterations,
+            "pagerank_ms_warm": pr2_ms, "pagerank_iters_warm": pr2.iterations,
+            "pagerank_iter_ms": g.last_timing().rounds_ms / max(pr2.iterations, 1)}
+
+
+def sweep(pg, stream, dev, batches):
+    """updates/s vs batch size (device-resident inputs, 2 warmup + 3 timed slides)."""
+    import torch
+    res = {}
+    for B in batches:
+        win = pg.SlidingWindow(stream, dev)
+        win.reserve(6 * B + 16)
+        info = win.info()
+        g = pg.DynamicGraph.from_edges_device(NV, info.stream_src, info.stream_dst, None, info.initial_size,
+                                              device=dev)
+        slides = [win.slide(B) for _ in range(5)]
+        info = win.info()
+        ext = torch.cuda.ExternalStream(g._lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
+
+        def go(s):
+            return g.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset,
+                                        None, s.n_ins, info.del_src + 4 * s.del_offset,
+                                        info.del_dst + 4 * s.del_offset, s.n_del)
+        for s in slides[:2]:
+            go(s)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(ext)
+        n = 0
+        for s in slides[2:]:
+            n += go(s).batch_size
+        e1.record(ext)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        res[str(B)] = {"updates_per_s": n / (ms / 1e3), "us_per_batch": ms * 1e3 / 3}
+        del g, win
+    return res
+
+
+def cpu_baseline(stream, slides, win, W):
+    """The reference (oracle/_ref) on the host cores, bounded sample: its
+    DynamicGraph over the same initial window, then 2 of the same slides
+    through apply_batch with all hardware threads (steady_clock around the
+    call)."""
+    from oracle import oracle
+    if not oracle.have_ref():
+        return None
+    s, d = stream.arrays()
+    half = (len(s) + 1) // 2
+    t = time.time()
+    ref = oracle.RefGraph(NV, s[:half], d[:half])
+    build_s = time.time() - t
+    cores = oracle.hardware_concurrency()
+    ms_total, n_total = 0.0, 0
+    sample = slides[:2]
+    for sl in sample:
+        a, b = s[sl.ins_offset:sl.ins_offset + sl.n_ins], d[sl.ins_offset:sl.ins_offset + sl.n_ins]
+        c, dd = win.deletions_host(sl.del_offset, sl.n_del)
+        st, ms = ref.apply_batch_timed(a, b, None, c, dd, cores)
+        ms_total += ms
+        n_total += st.batch_size
+    return {"value": n_total / (ms_total / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"2 slides of batch {slides[0].n_ins} on the C2 window via reference apply_batch "
+                      f"({cores} workers); reference from_edges setup {build_s:.1f}s excluded"}
+
+
+# ------------------------------------------------------------- reference --
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle
+    if not oracle.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpmagraph_ref.so not built"}))
+        return
+    B, K, W = args.batch, args.steps, args.warmup
+    cores = oracle.hardware_concurrency()
+    st = oracle.RefStream.rmat(NV, NE, seed=GEN_SEED).shuffle(SHUFFLE_SEED)
+    s, d, w, _ = st.arrays()
+    half = (len(s) + 1) // 2
+    ref = oracle.RefGraph(NV, s[:half], d[:half], w[:half])
+    win = oracle.RefWindow(st)
+    total_ms, total_n = 0.0, 0
+    for i in range(W + K):
+        a, b, ww, c, dd = win.slide(B)
+        stt, ms = ref.apply_batch_timed(a, b, ww, c, dd, cores)
+        if i >= W:
+            total_ms += ms
+            total_n += stt.batch_size
+    value = total_n / (total_ms / 1e3)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+           "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u64", "data": "synthetic: reference gen_rmat(2^21, 30.6M, seed 1) + shuffle 2",
+           "config": {"workload": "C2 Pokec-shaped sliding window: RMAT 2^21 vertices / 30.6M-edge stream, "
+                                  "15.3M-edge window, GPMA+ apply_batch per slide", "batch": B,
+                      "num_vertices": NV, "stream_edges": NE},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                            "sample": f"{K} slides of batch {B} (after {W} warmup) through the reference "
+                                      f"DynamicGraph::apply_batch with {cores} workers"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -264,6 +264,11 @@ int gpma_spmv(gpma_graph* g, const double* x, double* y);
 
 int gpma_last_timing(const gpma_graph* g, pma_timing* out);
 
+/* The cudaStream_t (as void*) every call on this handle runs on, so callers
+ * can bracket calls with CUDA events on the launching stream. */
+void* gpma_cuda_stream(gpma_graph* g);
+void* pma_cuda_stream(pma_handle* h);
+
 #ifdef __cplusplus
 }
 #endif

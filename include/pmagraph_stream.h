@@ -1,0 +1,74 @@
+/*
+ * pmagraph_stream.h — synthetic streams and the device sliding window
+ * (part of libpmagraph_cuda.so).  These replace the reference's stream
+ * drivers (generators.hpp, streaming.hpp) on the GPU side so a GPU pipeline
+ * is not bottlenecked by a host deque + hash map; the
+ * emitted streams and batches are identical to the reference's.
+ */
+#ifndef PMAGRAPH_STREAM_H
+#define PMAGRAPH_STREAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gpma_stream gpma_stream;
+typedef struct gpma_window gpma_window;
+
+/* Device pointers and sizes of a window (valid until the next reserve). */
+typedef struct gpma_window_info_t {
+    const uint32_t* stream_src; /* device, stream_size entries */
+    const uint32_t* stream_dst;
+    const uint32_t* del_src;    /* device, num_deletions entries (all slides) */
+    const uint32_t* del_dst;
+    uint64_t stream_size;
+    uint64_t initial_size;      /* first ceil(n/2) arrivals (streaming.hpp:83) */
+    uint64_t cursor;
+    uint64_t num_deletions;
+} gpma_window_info_t;
+
+/* One slide (SlideBatch, streaming.hpp:69-74): inserts are stream positions
+ * [ins_offset, ins_offset + n_ins); deletions are entries
+ * [del_offset, del_offset + n_del) of the window's deletion arrays. */
+typedef struct gpma_slide_t {
+    uint64_t ins_offset;
+    uint64_t n_ins;
+    uint64_t del_offset;
+    uint64_t n_del;
+    int32_t final_partial;
+    int32_t _pad;
+} gpma_slide_t;
+
+const char* gpma_stream_last_error(void);
+
+/* gen_rmat (generators.hpp:26-63), weights 1.0 */
+int gpma_stream_rmat(size_t nv, size_t ne, double a, double b, double c, double d, uint64_t seed,
+                     gpma_stream** out);
+/* gen_erdos_renyi (generators.hpp:67-89) */
+int gpma_stream_erdos_renyi(size_t nv, double density, uint64_t seed, gpma_stream** out);
+/* assign_random_timestamps (streaming.hpp:58-67) */
+int gpma_stream_shuffle(gpma_stream* s, uint64_t seed);
+int gpma_stream_from_arrays(size_t nv, const uint32_t* src, const uint32_t* dst, size_t n, gpma_stream** out);
+uint64_t gpma_stream_size(const gpma_stream* s);
+uint64_t gpma_stream_num_vertices(const gpma_stream* s);
+int gpma_stream_edges(const gpma_stream* s, uint32_t* src, uint32_t* dst);
+int gpma_stream_destroy(gpma_stream* s);
+/* draw_below (streaming.hpp:43-50) sequence from mt19937_64(seed) */
+int gpma_draw_below_sequence(uint64_t seed, uint64_t bound, size_t n, uint64_t* out);
+
+/* SlidingWindow (streaming.hpp:76-123) on CUDA device `device`. */
+int gpma_window_create(const gpma_stream* s, int device, gpma_window** out);
+int gpma_window_destroy(gpma_window* w);
+int gpma_window_info(const gpma_window* w, gpma_window_info_t* out);
+int gpma_window_reserve(gpma_window* w, size_t max_deletions);
+int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out);
+/* Copy deletions [offset, offset+n) of the window to host arrays. */
+int gpma_window_deletions_host(gpma_window* w, size_t offset, size_t n, uint32_t* src, uint32_t* dst);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMAGRAPH_STREAM_H */

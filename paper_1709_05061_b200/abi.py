@@ -96,6 +96,30 @@ class gpma_graph_config(C.Structure):
     ]
 
 
+class gpma_window_info_t(C.Structure):
+    _fields_ = [
+        ("stream_src", C.c_void_p),
+        ("stream_dst", C.c_void_p),
+        ("del_src", C.c_void_p),
+        ("del_dst", C.c_void_p),
+        ("stream_size", C.c_uint64),
+        ("initial_size", C.c_uint64),
+        ("cursor", C.c_uint64),
+        ("num_deletions", C.c_uint64),
+    ]
+
+
+class gpma_slide_t(C.Structure):
+    _fields_ = [
+        ("ins_offset", C.c_uint64),
+        ("n_ins", C.c_uint64),
+        ("del_offset", C.c_uint64),
+        ("n_del", C.c_uint64),
+        ("final_partial", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
 def default_profile() -> pma_profile:
     """DensityProfile defaults (pma.hpp:52-57)."""
     return pma_profile(0.08, 0.92, 0.40, 0.80, 1, 0)
@@ -172,6 +196,25 @@ SIGNATURES = [
     ("gpma_pagerank", C.c_int, [_P, C.c_double, C.c_double, C.c_size_t, _P, _P, _U64P, C.POINTER(C.c_int)]),
     ("gpma_spmv", C.c_int, [_P, _P, _P]),
     ("gpma_last_timing", C.c_int, [_P, C.POINTER(pma_timing)]),
+    ("gpma_cuda_stream", _P, [_P]),
+    ("pma_cuda_stream", _P, [_P]),
+    # pmagraph_stream.h
+    ("gpma_stream_last_error", C.c_char_p, []),
+    ("gpma_stream_rmat", C.c_int, [C.c_size_t, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(_P)]),
+    ("gpma_stream_erdos_renyi", C.c_int, [C.c_size_t, C.c_double, C.c_uint64, C.POINTER(_P)]),
+    ("gpma_stream_shuffle", C.c_int, [_P, C.c_uint64]),
+    ("gpma_stream_from_arrays", C.c_int, [C.c_size_t, _P, _P, C.c_size_t, C.POINTER(_P)]),
+    ("gpma_stream_size", C.c_uint64, [_P]),
+    ("gpma_stream_num_vertices", C.c_uint64, [_P]),
+    ("gpma_stream_edges", C.c_int, [_P, _P, _P]),
+    ("gpma_stream_destroy", C.c_int, [_P]),
+    ("gpma_draw_below_sequence", C.c_int, [C.c_uint64, C.c_uint64, C.c_size_t, _P]),
+    ("gpma_window_create", C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    ("gpma_window_destroy", C.c_int, [_P]),
+    ("gpma_window_info", C.c_int, [_P, C.POINTER(gpma_window_info_t)]),
+    ("gpma_window_reserve", C.c_int, [_P, C.c_size_t]),
+    ("gpma_window_slide", C.c_int, [_P, C.c_size_t, C.POINTER(gpma_slide_t)]),
+    ("gpma_window_deletions_host", C.c_int, [_P, C.c_size_t, C.c_size_t, _P, _P]),
 ]
 
 _lib = None

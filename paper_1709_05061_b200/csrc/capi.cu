@@ -387,4 +387,7 @@ int gpma_last_timing(const gpma_graph* g, pma_timing* out) {
     return PMA_OK;
 }
 
+void* gpma_cuda_stream(gpma_graph* g) { return g ? (void*)g->impl->pma.stream() : nullptr; }
+void* pma_cuda_stream(pma_handle* h) { return h ? (void*)h->impl->stream() : nullptr; }
+
 }  // extern "C"

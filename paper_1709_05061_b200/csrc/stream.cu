@@ -1,0 +1,354 @@
+// stream.cu — synthetic edge streams and the sliding window, on the device.
+//
+// Generators restate generators.hpp:26-89 and streaming.hpp:43-67 with the
+// same std::mt19937_64 draws (the engine is fully specified by the C++
+// standard), so they emit the reference's exact streams.
+//
+// SlidingWindow (streaming.hpp:76-123) is re-derived for the GPU: the window
+// is a FIFO of stream positions [lo, cursor); a slide admits
+// [cursor, cursor + take) and expires [lo, lo + take).  The reference emits a
+// deletion for an expiring arrival p iff its key's multiplicity drops to zero,
+// i.e. iff the key has no later arrival inside the new window:
+// next_occurrence(p) >= cursor + take.  With next_occurrence precomputed once
+// by a stable sort of (key, position), every slide is one ordered compaction
+// — no hash map, and the emitted batches are byte-identical to the reference.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "pmagraph_cuda.h"
+#include "pmagraph_stream.h"
+#include "scan.cuh"
+
+namespace gpma {
+
+// draw_below / draw_unit (streaming.hpp:43-54)
+static inline uint64_t draw_below(std::mt19937_64& rng, uint64_t bound) {
+    const uint64_t limit = bound * (UINT64_MAX / bound);
+    uint64_t x;
+    do {
+        x = rng();
+    } while (x >= limit);
+    return x % bound;
+}
+
+static inline double draw_unit(std::mt19937_64& rng) { return static_cast<double>(rng() >> 11) * 0x1.0p-53; }
+
+struct Stream {
+    uint64_t nv = 0;
+    std::vector<uint32_t> src, dst;
+};
+
+__global__ void k_next_occ(const u64* sk, const u32* sp, u64 n, u32* next) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        next[sp[i]] = (i + 1 < n && sk[i + 1] == sk[i]) ? sp[i + 1] : 0xFFFFFFFFu;
+}
+
+__global__ void k_pack_stream(const u32* s, const u32* d, u64 n, u64* k, u32* p) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        k[i] = (u64(s[i]) << 32) | d[i];
+        p[i] = u32(i);
+    }
+}
+
+struct Window {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t n = 0, lo = 0, cursor = 0;
+    DevBuf<u32> src, dst, next;
+    DevBuf<u32> del_src, del_dst;  // all deletions emitted so far (appended)
+    uint64_t ndel = 0;
+    ScanWorkspace ws;
+    DevBuf<ull> cnt;
+};
+
+}  // namespace gpma
+
+struct gpma_stream {
+    gpma::Stream s;
+};
+struct gpma_window {
+    gpma::Window w;
+};
+
+using gpma::ApiError;
+
+namespace {
+thread_local std::string g_stream_err;
+template <class F>
+int sguard(F&& f) {
+    try {
+        f();
+        return PMA_OK;
+    } catch (const ApiError& e) {
+        g_stream_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_stream_err = e.what();
+        return PMA_ECUDA;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+const char* gpma_stream_last_error(void) { return g_stream_err.c_str(); }
+
+// gen_rmat (generators.hpp:26-63)
+int gpma_stream_rmat(size_t nv, size_t ne, double a, double b, double c, double d, uint64_t seed,
+                     gpma_stream** out) {
+    return sguard([&] {
+        if (nv == 0 || (nv & (nv - 1)) != 0) throw ApiError(PMA_EINVAL, "gen_rmat: num_vertices must be a power of two");
+        const double sum = a + b + c + d;
+        if (std::abs(sum - 1.0) > 1e-9 || a < 0 || b < 0 || c < 0 || d < 0)
+            throw ApiError(PMA_EINVAL, "gen_rmat: quadrant probabilities must be non-negative and sum to 1");
+        int scale = 0;
+        while ((size_t{1} << scale) < nv) ++scale;
+        auto* s = new gpma_stream;
+        s->s.nv = nv;
+        s->s.src.resize(ne);
+        s->s.dst.resize(ne);
+        std::mt19937_64 rng(seed);
+        const double ab = a + b, abc = ab + c;
+        for (size_t e = 0; e < ne; ++e) {
+            uint64_t row = 0, col = 0;
+            for (int bit = 0; bit < scale; ++bit) {
+                // quadrant a:(0,0) b:(0,1) c:(1,0) d:(1,1), decided by the same
+                // three comparisons as generators.hpp:47-58, without branches
+                const double r = gpma::draw_unit(rng);
+                const uint64_t rb = r >= ab;
+                const uint64_t cb = uint64_t(r >= a) ^ rb ^ uint64_t(r >= abc);
+                row = (row << 1) | rb;
+                col = (col << 1) | cb;
+            }
+            s->s.src[e] = uint32_t(row);
+            s->s.dst[e] = uint32_t(col);
+        }
+        *out = s;
+    });
+}
+
+// gen_erdos_renyi (generators.hpp:67-89)
+int gpma_stream_erdos_renyi(size_t nv, double density, uint64_t seed, gpma_stream** out) {
+    return sguard([&] {
+        if (density < 0.0 || density >= 1.0) throw ApiError(PMA_EINVAL, "gen_erdos_renyi: density must be in [0, 1)");
+        auto* s = new gpma_stream;
+        s->s.nv = nv;
+        if (density > 0.0 && nv > 0) {
+            std::mt19937_64 rng(seed);
+            const double log1mp = std::log1p(-density);
+            const uint64_t total = uint64_t(nv) * nv;
+            uint64_t pos = 0;
+            s->s.src.reserve(size_t(double(total) * density * 1.01) + 16);
+            s->s.dst.reserve(size_t(double(total) * density * 1.01) + 16);
+            for (;;) {
+                const double u = gpma::draw_unit(rng);
+                const double gap = std::floor(std::log1p(-u) / log1mp);
+                pos += uint64_t(gap) + 1;
+                if (pos > total) break;
+                const uint64_t idx = pos - 1;
+                s->s.src.push_back(uint32_t(idx / nv));
+                s->s.dst.push_back(uint32_t(idx % nv));
+            }
+        }
+        *out = s;
+    });
+}
+
+// assign_random_timestamps (streaming.hpp:58-67): Fisher-Yates with draw_below
+int gpma_stream_shuffle(gpma_stream* s, uint64_t seed) {
+    return sguard([&] {
+        std::mt19937_64 rng(seed);
+        auto& a = s->s.src;
+        auto& b = s->s.dst;
+        for (size_t i = a.size(); i > 1; --i) {
+            const size_t j = size_t(gpma::draw_below(rng, i));
+            std::swap(a[i - 1], a[j]);
+            std::swap(b[i - 1], b[j]);
+        }
+    });
+}
+
+int gpma_stream_from_arrays(size_t nv, const uint32_t* src, const uint32_t* dst, size_t n, gpma_stream** out) {
+    return sguard([&] {
+        auto* s = new gpma_stream;
+        s->s.nv = nv;
+        s->s.src.assign(src, src + n);
+        s->s.dst.assign(dst, dst + n);
+        *out = s;
+    });
+}
+
+uint64_t gpma_stream_size(const gpma_stream* s) { return s ? s->s.src.size() : 0; }
+uint64_t gpma_stream_num_vertices(const gpma_stream* s) { return s ? s->s.nv : 0; }
+
+int gpma_stream_edges(const gpma_stream* s, uint32_t* src, uint32_t* dst) {
+    return sguard([&] {
+        if (src) std::memcpy(src, s->s.src.data(), s->s.src.size() * 4);
+        if (dst) std::memcpy(dst, s->s.dst.data(), s->s.dst.size() * 4);
+    });
+}
+
+int gpma_stream_destroy(gpma_stream* s) {
+    delete s;
+    return PMA_OK;
+}
+
+// draw_below over mt19937_64(seed): the bench's BFS-root sequence (bench.hpp:244,266)
+int gpma_draw_below_sequence(uint64_t seed, uint64_t bound, size_t n, uint64_t* out) {
+    return sguard([&] {
+        std::mt19937_64 rng(seed);
+        for (size_t i = 0; i < n; ++i) out[i] = gpma::draw_below(rng, bound);
+    });
+}
+
+int gpma_window_create(const gpma_stream* s, int device, gpma_window** out) {
+    return sguard([&] {
+        const uint64_t n = s->s.src.size();
+        if (n < 2) throw ApiError(PMA_EINVAL, "SlidingWindow: stream needs at least two edges");
+        if (n >= 0xFFFFFFFFull) throw ApiError(PMA_EINVAL, "SlidingWindow: stream too long for 32-bit positions");
+        auto* w = new gpma_window;
+        auto& W = w->w;
+        W.device = device;
+        GPMA_CUDA(cudaSetDevice(device));
+        GPMA_CUDA(cudaStreamCreateWithFlags(&W.stream, cudaStreamNonBlocking));
+        W.n = n;
+        W.src.reserve(n);
+        W.dst.reserve(n);
+        W.next.reserve(n);
+        W.cnt.reserve(2);
+        GPMA_CUDA(cudaMemcpyAsync(W.src.ptr, s->s.src.data(), n * 4, cudaMemcpyHostToDevice, W.stream));
+        GPMA_CUDA(cudaMemcpyAsync(W.dst.ptr, s->s.dst.data(), n * 4, cudaMemcpyHostToDevice, W.stream));
+        {
+            gpma::DevBuf<gpma::u64> k0, k1;
+            gpma::DevBuf<gpma::u32> p0, p1;
+            gpma::DevBuf<unsigned char> tmp;
+            k0.reserve(n);
+            k1.reserve(n);
+            p0.reserve(n);
+            p1.reserve(n);
+            gpma::k_pack_stream<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(W.src.ptr, W.dst.ptr, n, k0.ptr, p0.ptr);
+            GPMA_LAUNCH_CHECK();
+            size_t tb = 0;
+            cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.ptr, k1.ptr, p0.ptr, p1.ptr, int(n), 0, 64, W.stream);
+            tmp.reserve(tb);
+            GPMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, k0.ptr, k1.ptr, p0.ptr, p1.ptr, int(n), 0, 64,
+                                                      W.stream));
+            gpma::k_next_occ<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(k1.ptr, p1.ptr, n, W.next.ptr);
+            GPMA_LAUNCH_CHECK();
+            GPMA_CUDA(cudaStreamSynchronize(W.stream));
+        }
+        W.lo = 0;
+        W.cursor = (n + 1) / 2;  // streaming.hpp:83-85
+        *out = w;
+    });
+}
+
+int gpma_window_destroy(gpma_window* w) {
+    if (!w) return PMA_OK;
+    cudaSetDevice(w->w.device);
+    cudaStreamSynchronize(w->w.stream);
+    cudaStreamDestroy(w->w.stream);
+    delete w;
+    return PMA_OK;
+}
+
+int gpma_window_info(const gpma_window* w, gpma_window_info_t* out) {
+    if (!w || !out) return PMA_EINVAL;
+    out->stream_src = w->w.src.ptr;
+    out->stream_dst = w->w.dst.ptr;
+    out->del_src = w->w.del_src.ptr;
+    out->del_dst = w->w.del_dst.ptr;
+    out->stream_size = w->w.n;
+    out->initial_size = (w->w.n + 1) / 2;
+    out->cursor = w->w.cursor;
+    out->num_deletions = w->w.ndel;
+    return PMA_OK;
+}
+
+// Reserve room for `max_deletions` appended deletions (device pointers in
+// gpma_window_info stay valid until the next reserve).
+int gpma_window_reserve(gpma_window* w, size_t max_deletions) {
+    return sguard([&] {
+        auto& W = w->w;
+        if (max_deletions <= W.del_src.cap) return;
+        GPMA_CUDA(cudaSetDevice(W.device));
+        gpma::DevBuf<gpma::u32> a, b;
+        a.reserve(max_deletions);
+        b.reserve(max_deletions);
+        if (W.ndel) {
+            GPMA_CUDA(cudaMemcpyAsync(a.ptr, W.del_src.ptr, W.ndel * 4, cudaMemcpyDeviceToDevice, W.stream));
+            GPMA_CUDA(cudaMemcpyAsync(b.ptr, W.del_dst.ptr, W.ndel * 4, cudaMemcpyDeviceToDevice, W.stream));
+        }
+        GPMA_CUDA(cudaStreamSynchronize(W.stream));
+        std::swap(W.del_src.ptr, a.ptr);
+        std::swap(W.del_src.cap, a.cap);
+        std::swap(W.del_dst.ptr, b.ptr);
+        std::swap(W.del_dst.cap, b.cap);
+    });
+}
+
+// SlidingWindow::slide (streaming.hpp:107-123) on the device.  Inserts are
+// stream positions [ins_offset, ins_offset + n_ins); deletions are appended
+// at [del_offset, del_offset + n_del) of the window's deletion arrays.
+int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out) {
+    return sguard([&] {
+        auto& W = w->w;
+        GPMA_CUDA(cudaSetDevice(W.device));
+        const uint64_t remaining = W.n - W.cursor;
+        const uint64_t take = batch < remaining ? batch : remaining;
+        const uint64_t end = W.cursor + take;
+        if (W.ndel + take > W.del_src.cap) {
+            const size_t want = size_t((W.ndel + take) * 2 + 1024);
+            int rc = gpma_window_reserve(w, want);
+            if (rc) throw ApiError(rc, g_stream_err);
+        }
+        out->ins_offset = W.cursor;
+        out->n_ins = take;
+        out->del_offset = W.ndel;
+        out->final_partial = take < batch ? 1 : 0;
+        uint64_t nd = 0;
+        if (take > 0) {
+            const gpma::u32* nx = W.next.ptr;
+            const gpma::u32* ss = W.src.ptr;
+            const gpma::u32* dd = W.dst.ptr;
+            gpma::u32* os = W.del_src.ptr + W.ndel;
+            gpma::u32* od = W.del_dst.ptr + W.ndel;
+            gpma::ull* cnt = W.cnt.ptr;
+            const uint64_t lo = W.lo;
+            GPMA_CUDA(cudaMemsetAsync(cnt, 0, 8, W.stream));
+            gpma::run_compact(
+                W.stream, W.ws, nullptr, take, take,
+                [=] __device__(gpma::ull i) { return uint64_t(nx[lo + i]) >= end; },
+                [=] __device__(gpma::ull i, unsigned f, gpma::ull x) {
+                    if (f) {
+                        os[x] = ss[lo + i];
+                        od[x] = dd[lo + i];
+                    }
+                },
+                [=] __device__(gpma::ull total) { *cnt = total; });
+            GPMA_CUDA(cudaMemcpyAsync(&nd, cnt, 8, cudaMemcpyDeviceToHost, W.stream));
+            GPMA_CUDA(cudaStreamSynchronize(W.stream));
+        }
+        out->n_del = nd;
+        W.ndel += nd;
+        W.lo += take;
+        W.cursor = end;
+    });
+}
+
+}  // extern "C"
+
+extern "C" int gpma_window_deletions_host(gpma_window* w, size_t offset, size_t n, uint32_t* src, uint32_t* dst) {
+    return sguard([&] {
+        auto& W = w->w;
+        if (offset + n > W.ndel) throw ApiError(PMA_ERANGE, "window deletions: range outside emitted deletions");
+        GPMA_CUDA(cudaSetDevice(W.device));
+        if (n && src) GPMA_CUDA(cudaMemcpyAsync(src, W.del_src.ptr + offset, n * 4, cudaMemcpyDeviceToHost, W.stream));
+        if (n && dst) GPMA_CUDA(cudaMemcpyAsync(dst, W.del_dst.ptr + offset, n * 4, cudaMemcpyDeviceToHost, W.stream));
+        GPMA_CUDA(cudaStreamSynchronize(W.stream));
+    });
+}

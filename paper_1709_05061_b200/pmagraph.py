@@ -454,6 +454,113 @@ def spmv(g: DynamicGraph, x):
     return y
 
 
-__all__ = ["PackedMemoryArray", "DynamicGraph", "DensityProfile", "UpdateStats", "SegmentEngineConfig",
+class EdgeStream:
+    """Synthetic stream (generators.hpp:26-89 + streaming.hpp:58-67) built by
+    the library's own generators (identical mt19937_64 draws)."""
+
+    def __init__(self, handle, lib):
+        self.h = handle
+        self._lib = lib
+
+    @staticmethod
+    def _chk(lib, rc):
+        if rc:
+            _raise(rc, lib.gpma_stream_last_error().decode())
+
+    @classmethod
+    def rmat(cls, num_vertices, num_edges, seed=1, a=0.57, b=0.19, c=0.19, d=0.05) -> "EdgeStream":
+        lib = load_library()
+        h = C.c_void_p()
+        cls._chk(lib, lib.gpma_stream_rmat(num_vertices, num_edges, a, b, c, d, seed, C.byref(h)))
+        return cls(h, lib)
+
+    @classmethod
+    def erdos_renyi(cls, num_vertices, density, seed=1) -> "EdgeStream":
+        lib = load_library()
+        h = C.c_void_p()
+        cls._chk(lib, lib.gpma_stream_erdos_renyi(num_vertices, C.c_double(density), seed, C.byref(h)))
+        return cls(h, lib)
+
+    @classmethod
+    def from_arrays(cls, num_vertices, src, dst) -> "EdgeStream":
+        lib = load_library()
+        s, d = _u32(src), _u32(dst)
+        h = C.c_void_p()
+        cls._chk(lib, lib.gpma_stream_from_arrays(num_vertices, _p(s), _p(d), len(s), C.byref(h)))
+        return cls(h, lib)
+
+    def shuffle(self, seed) -> "EdgeStream":
+        """assign_random_timestamps (streaming.hpp:58-67)."""
+        self._chk(self._lib, self._lib.gpma_stream_shuffle(self.h, seed))
+        return self
+
+    def __len__(self):
+        return int(self._lib.gpma_stream_size(self.h))
+
+    @property
+    def num_vertices(self):
+        return int(self._lib.gpma_stream_num_vertices(self.h))
+
+    def arrays(self):
+        n = len(self)
+        s = np.zeros(n, np.uint32)
+        d = np.zeros(n, np.uint32)
+        self._chk(self._lib, self._lib.gpma_stream_edges(self.h, _p(s), _p(d)))
+        return s, d
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.gpma_stream_destroy(self.h)
+            self.h = None
+
+
+def draw_below_sequence(seed: int, bound: int, n: int):
+    """draw_below (streaming.hpp:43-50) over mt19937_64(seed)."""
+    lib = load_library()
+    out = np.zeros(n, np.uint64)
+    EdgeStream._chk(lib, lib.gpma_draw_below_sequence(seed, bound, n, _p(out)))
+    return out
+
+
+class SlidingWindow:
+    """Device sliding window (streaming.hpp:76-123): slides return device
+    offsets into the stream (inserts) and the window's deletion arrays."""
+
+    def __init__(self, stream: EdgeStream, device: int = 0):
+        from .abi import gpma_slide_t, gpma_window_info_t  # noqa: F401
+        self._lib = stream._lib
+        self.stream = stream
+        self.h = C.c_void_p()
+        EdgeStream._chk(self._lib, self._lib.gpma_window_create(stream.h, device, C.byref(self.h)))
+
+    def info(self):
+        from .abi import gpma_window_info_t
+        i = gpma_window_info_t()
+        self._lib.gpma_window_info(self.h, C.byref(i))
+        return i
+
+    def reserve(self, max_deletions: int):
+        EdgeStream._chk(self._lib, self._lib.gpma_window_reserve(self.h, max_deletions))
+
+    def slide(self, batch: int):
+        from .abi import gpma_slide_t
+        s = gpma_slide_t()
+        EdgeStream._chk(self._lib, self._lib.gpma_window_slide(self.h, batch, C.byref(s)))
+        return s
+
+    def deletions_host(self, offset: int, n: int, src=None, dst=None):
+        """Copy deletions [offset, offset+n) to host arrays (pinned if given)."""
+        s = np.zeros(n, np.uint32) if src is None else src
+        d = np.zeros(n, np.uint32) if dst is None else dst
+        EdgeStream._chk(self._lib, self._lib.gpma_window_deletions_host(self.h, offset, n, _p(s), _p(d)))
+        return s, d
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.gpma_window_destroy(self.h)
+            self.h = None
+
+
+__all__ = ["EdgeStream", "SlidingWindow", "draw_below_sequence", "PackedMemoryArray", "DynamicGraph", "DensityProfile", "UpdateStats", "SegmentEngineConfig",
            "GraphConfig", "PageRankResult", "batch_update", "bfs", "connected_components", "pagerank", "spmv",
            "LogicError", "kUnreached", "kMinCapacity", "PMA_LAZY", "PMA_EAGER"]
