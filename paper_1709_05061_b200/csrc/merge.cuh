@@ -21,10 +21,11 @@ struct SlicePending {
     const u64* uv;
     const u8* uop;
     const u32* pidx;
-    u32 lo;
-    __device__ u64 key(u64 q) const { return uk[pidx[lo + q]]; }
-    __device__ u64 val(u64 q) const { return uv[pidx[lo + q]]; }
-    __device__ u8 op(u64 q) const { return uop[pidx[lo + q]]; }
+    u32 lo;  // pidx == nullptr: identity (round 0)
+    __device__ u32 pid(u64 q) const { return pidx ? pidx[lo + q] : u32(lo + q); }
+    __device__ u64 key(u64 q) const { return uk[pid(q)]; }
+    __device__ u64 val(u64 q) const { return uv[pid(q)]; }
+    __device__ u8 op(u64 q) const { return uop[pid(q)]; }
 };
 
 struct SliceDirect {

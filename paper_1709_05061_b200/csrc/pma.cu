@@ -219,8 +219,13 @@ struct CommitArgs {
     const u32* ul;
     const u32* pidx;
     const u32* gstart;
+    const u32* gseg;
     u8* gflag;
     Ctr* ctr;
+    u64* hdr;
+    u64* ro;
+    u64* rlist;
+    u32* biglist;
     int level;
     u64 m;
     u64 leaf;
@@ -243,7 +248,7 @@ struct CommitArgs {
 
 struct Acc {
     ull committed = 0, missed = 0, tomb = 0, writes = 0, merge = 0;
-    long long vd = 0, td = 0;
+    long long vd = 0, td = 0, ed = 0;
 };
 
 __device__ __forceinline__ void flush_acc(const Acc& a, Ctr* ctr) {
@@ -255,11 +260,12 @@ __device__ __forceinline__ void flush_acc(const Acc& a, Ctr* ctr) {
     if (a.merge) atomicAdd(&ctr->merge_slots, a.merge);
     if (a.vd) atomicAdd(reinterpret_cast<ull*>(&ctr->valid_delta), ull(a.vd));
     if (a.td) atomicAdd(reinterpret_cast<ull*>(&ctr->tomb_delta), ull(a.td));
+    if (a.ed) atomicAdd(reinterpret_cast<ull*>(&ctr->empty_delta), ull(a.ed));
 }
 
 __device__ void block_flush(Acc acc, Ctr* ctr) {
-    __shared__ ull s_acc[7];
-    if (threadIdx.x < 7) s_acc[threadIdx.x] = 0;
+    __shared__ ull s_acc[8];
+    if (threadIdx.x < 8) s_acc[threadIdx.x] = 0;
     __syncthreads();
     if ((threadIdx.x & 31) == 0) {
         if (acc.committed) atomicAdd(&s_acc[0], acc.committed);
@@ -269,6 +275,7 @@ __device__ void block_flush(Acc acc, Ctr* ctr) {
         if (acc.merge) atomicAdd(&s_acc[4], acc.merge);
         if (acc.vd) atomicAdd(&s_acc[5], ull(acc.vd));
         if (acc.td) atomicAdd(&s_acc[6], ull(acc.td));
+        if (acc.ed) atomicAdd(&s_acc[7], ull(acc.ed));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -280,148 +287,524 @@ __device__ void block_flush(Acc acc, Ctr* ctr) {
         t.merge = s_acc[4];
         t.vd = (long long)s_acc[5];
         t.td = (long long)s_acc[6];
+        t.ed = (long long)s_acc[7];
         flush_acc(t, ctr);
     }
 }
 
 // ------------------------------------------------------------- warp tier
 // One warp per group, segment <= 32 slots (leaf and level-1 segments carry
-// >= 99.5% of commits).  The segment lives in registers (one
-// slot per lane), the decision, the merge (ranks via shuffles) and the even
-// re-dispatch happen without leaving the warp; each slot is read once and
-// written once (keys/values 128-B lines per leaf).
+// >= 99.5% of commits).  Slot t of the segment lives in lane t;
+// the (typically 1-3) updates of the group are broadcast one by one and
+// ranked against the segment with two ballots, so a group costs O(|slice|)
+// warp instructions.  Inserts keep their merged position in lane p; survivors
+// take the remaining positions in order (__fns over the free-position mask).
+// Decision, merge, even re-dispatch and — when every leaf of the rewritten
+// segment is non-empty — the leaf-header and row-offset refresh are fused, so
+// each slot is read once and written once (128-B key/value lines per leaf).
 constexpr int kWarpTierWarps = 8;
 
-__global__ void __launch_bounds__(kWarpTierWarps * 32) k_commit_warp(CommitArgs a) {
-    __shared__ u64 s_ok[kWarpTierWarps][32], s_ov[kWarpTierWarps][32], s_ik[kWarpTierWarps][32],
-        s_iv[kWarpTierWarps][32];
-    __shared__ u32 s_ir[kWarpTierWarps][32];
+__device__ __forceinline__ void warp_reduce_acc(Acc& acc) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        acc.committed += __shfl_xor_sync(FULL, acc.committed, d);
+        acc.missed += __shfl_xor_sync(FULL, acc.missed, d);
+        acc.tomb += __shfl_xor_sync(FULL, acc.tomb, d);
+        acc.writes += __shfl_xor_sync(FULL, acc.writes, d);
+        acc.merge += __shfl_xor_sync(FULL, acc.merge, d);
+        acc.vd += __shfl_xor_sync(FULL, acc.vd, d);
+        acc.td += __shfl_xor_sync(FULL, acc.td, d);
+        acc.ed += __shfl_xor_sync(FULL, acc.ed, d);
+    }
+}
+
+// Group descriptors for a tile of 32 groups, one per lane (one coalesced
+// round trip instead of one dependent load chain per group).
+__device__ __forceinline__ void load_group_tile(const CommitArgs& a, ull g0, ull ngroups, unsigned lane, u32& t_lo,
+                                                u32& t_hi, u32& t_seg) {
+    const ull gl = g0 + lane;
+    t_lo = t_hi = t_seg = 0;
+    if (gl < ngroups) {
+        t_lo = a.gstart[gl];
+        t_hi = a.gstart[gl + 1];
+        t_seg = a.gseg[gl];
+    }
+}
+
+// --- leaf tier: thread per group, 16-slot segments (>= 99.5% of commits).
+// The warp stages the 32 leaves of its group tile in shared memory with
+// coalesced 16-byte loads (8 lanes per 128-byte key/value line), each thread
+// then runs the reference's in-place merge on its own row — pass A compacts
+// survivors left and applies deletes, pass B merges right-to-left onto the
+// even targets floor(j*m/k) (commit_in_place, segment_engine.hpp:147-230;
+// identical output to place_evenly) — and the warp stores the rewritten
+// leaves back coalesced.  O(16 + |slice|) thread work per group, one staged
+// round trip per 32 groups.  Groups with more than kBigSlice updates (RMAT hub
+// rows) are handed to the lane-parallel kernel through `biglist`.
+constexpr int kLeafWarps = 4;
+constexpr int kRow = 17;        // padded u64 row (conflict-free column access)
+constexpr u32 kBigSlice = 32;
+
+__global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
+    __shared__ u64 s_k[kLeafWarps][32 * kRow];
+    __shared__ u64 s_v[kLeafWarps][32 * kRow];
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    u64* rk = &s_k[w][lane * kRow];
+    u64* rv = &s_v[w][lane * kRow];
+    const ull ngroups = a.ctr->ngroups;
+    Acc acc;
+    for (ull g0 = (ull(blockIdx.x) * kLeafWarps + w) * 32; g0 < ngroups; g0 += ull(gridDim.x) * kLeafWarps * 32) {
+        const ull gl = g0 + lane;
+        const bool act = gl < ngroups;
+        u32 lo = 0, hi = 0;
+        u64 b = 0;
+        uint4 sv = make_uint4(0, 0, 0, 0);
+        if (act) {
+            lo = a.gstart[gl];
+            hi = a.gstart[gl + 1];
+            b = u64(a.gseg[gl]) * 16;
+            sv = *reinterpret_cast<const uint4*>(a.st + b);
+        }
+        const u32 s = hi - lo;
+        // keys of the tile: 8 lanes per leaf line, 4 leaves per instruction
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+            const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
+            const u64 gb = __shfl_sync(FULL, b, grp);
+            if (__shfl_sync(FULL, act ? 1 : 0, grp)) {
+                const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(a.keys + gb + 2 * part);
+                s_k[w][grp * kRow + 2 * part] = kk.x;
+                s_k[w][grp * kRow + 2 * part + 1] = kk.y;
+            }
+        }
+        // state masks (bit i = slot i)
+        const u32 words[4] = {sv.x, sv.y, sv.z, sv.w};
+        unsigned valid = 0, nonempty = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int by = 0; by < 4; ++by) {
+                const u32 x = (words[q] >> (8 * by)) & 0xffu;
+                valid |= unsigned(x == kValid) << (q * 4 + by);
+                nonempty |= unsigned(x != kEmpty) << (q * 4 + by);
+            }
+        }
+        const unsigned nv = __popc(valid);
+        int mode = 0;  // 0 defer, 1 tombstones, 2 merge, 3 big slice (lane kernel)
+        u32 ins = 0;
+        if (act) {
+            if (s > kBigSlice) {
+                mode = 3;
+            } else {
+                for (u32 q = 0; q < s; ++q) ins += a.uop[a.pidx ? a.pidx[lo + q] : lo + q] == kOpInsert;
+                const u32 dels = s - ins;
+                if (!a.eager && ins == 0) mode = 1;
+                else if (!(nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn))) mode = 2;
+            }
+        }
+        const unsigned mergemask = __ballot_sync(FULL, mode == 2);
+        if (mergemask) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
+                const u64 gb = __shfl_sync(FULL, b, grp);
+                if ((mergemask >> grp) & 1u) {
+                    const ulonglong2 vv = *reinterpret_cast<const ulonglong2*>(a.vals + gb + 2 * part);
+                    s_v[w][grp * kRow + 2 * part] = vv.x;
+                    s_v[w][grp * kRow + 2 * part + 1] = vv.y;
+                }
+            }
+        }
+        __syncwarp();
+        unsigned newvalid = valid;
+        u32 missed = 0, added = 0, moves = 0, k = 0;
+        if (mode == 1) {
+            // commit_tombstones: one ordered pass over slots and deletes
+            u32 q = 0;
+            u64 uq = q < s ? a.uk[a.pidx ? a.pidx[lo] : lo] : 0;
+            for (unsigned i = 0; i < 16 && q < s; ++i) {
+                if (!((nonempty >> i) & 1u)) continue;
+                const u64 ki = rk[i];
+                while (q < s && uq < ki) {
+                    ++missed;
+                    ++q;
+                    if (q < s) uq = a.uk[a.pidx ? a.pidx[lo + q] : lo + q];
+                }
+                if (q < s && uq == ki) {
+                    if ((valid >> i) & 1u) {
+                        newvalid &= ~(1u << i);
+                        ++added;
+                    } else {
+                        ++missed;
+                    }
+                    ++q;
+                    if (q < s) uq = a.uk[a.pidx ? a.pidx[lo + q] : lo + q];
+                }
+            }
+            missed += s - q;
+        } else if (mode == 2) {
+            // pass A: compact survivors left, apply deletes (count missed)
+            u32 wpos = 0, q = 0;
+            for (unsigned i = 0; i < 16; ++i) {
+                if (!((valid >> i) & 1u)) continue;
+                const u64 ki = rk[i];
+                bool keep = true;
+                while (q < s) {
+                    const u32 pi = a.pidx ? a.pidx[lo + q] : lo + q;
+                    const u64 u = a.uk[pi];
+                    if (u > ki) break;
+                    if (a.uop[pi] == kOpDelete) {
+                        if (u == ki) keep = false;
+                        else ++missed;
+                    }
+                    ++q;
+                }
+                if (!keep) continue;
+                if (wpos != i) {
+                    rk[wpos] = ki;
+                    rv[wpos] = rv[i];
+                    ++moves;
+                }
+                ++wpos;
+            }
+            for (; q < s; ++q) missed += a.uop[a.pidx ? a.pidx[lo + q] : lo + q] == kOpDelete;
+            const u32 n1 = wpos;
+            // merged size: survivors + inserts that do not overwrite one
+            k = n1;
+            {
+                u32 p = 0;
+                for (u32 j = 0; j < s; ++j) {
+                    const u32 pi = a.pidx ? a.pidx[lo + j] : lo + j;
+                    if (a.uop[pi] != kOpInsert) continue;
+                    const u64 u = a.uk[pi];
+                    while (p < n1 && rk[p] < u) ++p;
+                    if (p < n1 && rk[p] == u) ++p;
+                    else ++k;
+                }
+            }
+            // pass B: right-to-left onto the even targets (never clobbers an unread survivor)
+            int p = int(n1) - 1, uj = int(s) - 1, t = int(k) - 1;
+            newvalid = 0;
+            for (int x = 15; x >= 0; --x) {
+                const int target = t >= 0 ? int((u32(t) * 16u) / k) : 16;
+                if (x != target) {
+                    rk[x] = 0;
+                    rv[x] = 0;
+                    continue;
+                }
+                u32 pj = 0;
+                while (uj >= 0) {
+                    pj = a.pidx ? a.pidx[lo + uj] : lo + uj;
+                    if (a.uop[pj] != kOpDelete) break;
+                    --uj;
+                }
+                u64 ok_, ov_;
+                const u64 uk_ = uj >= 0 ? a.uk[pj] : 0;
+                if (uj < 0 || (p >= 0 && rk[p] > uk_)) {
+                    ok_ = rk[p];
+                    ov_ = rv[p];
+                    --p;
+                } else {
+                    if (p >= 0 && rk[p] == uk_) --p;
+                    ok_ = uk_;
+                    ov_ = a.uv[pj];
+                    --uj;
+                }
+                rk[x] = ok_;
+                rv[x] = ov_;
+                newvalid |= 1u << x;
+                --t;
+            }
+        }
+        __syncwarp();
+        // write back: states (own leaf), keys/values (merge groups, coalesced)
+        if (mode == 1 || mode == 2) {
+            uint4 ns;
+            u32* o = reinterpret_cast<u32*>(&ns);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                u32 word = 0;
+#pragma unroll
+                for (int by = 0; by < 4; ++by) {
+                    const int i = q * 4 + by;
+                    u32 x;
+                    if (mode == 1) x = ((newvalid >> i) & 1u) ? kValid : (((nonempty >> i) & 1u) ? kTombstone : kEmpty);
+                    else x = ((newvalid >> i) & 1u) ? kValid : kEmpty;
+                    word |= x << (8 * by);
+                }
+                o[q] = word;
+            }
+            *reinterpret_cast<uint4*>(a.st + b) = ns;
+        }
+        if (mergemask) {
+#pragma unroll
+            for (int it = 0; it < 8; ++it) {
+                const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
+                const u64 gb = __shfl_sync(FULL, b, grp);
+                if ((mergemask >> grp) & 1u) {
+                    *reinterpret_cast<ulonglong2*>(a.keys + gb + 2 * part) =
+                        make_ulonglong2(s_k[w][grp * kRow + 2 * part], s_k[w][grp * kRow + 2 * part + 1]);
+                    *reinterpret_cast<ulonglong2*>(a.vals + gb + 2 * part) =
+                        make_ulonglong2(s_v[w][grp * kRow + 2 * part], s_v[w][grp * kRow + 2 * part + 1]);
+                }
+            }
+        }
+        if (mode == 2) {
+            if (k > 0) a.hdr[b / 16] = rk[0];  // entry 0 always lands on slot 0
+            else {
+                const ull slot = atomicAdd(&a.ctr->nrefresh, 1ull);
+                a.rlist[2 * slot] = b;
+                a.rlist[2 * slot + 1] = b + 16;
+            }
+            if (a.ro) {
+                for (unsigned x = 0; x < 16; ++x) {
+                    if ((newvalid >> x) & 1u) {
+                        const u64 kx = rk[x];
+                        if (is_guard(kx)) a.ro[src_of(kx) + 1] = b + x + 1;  // graph.hpp:176
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (act) {
+            a.gflag[gl] = u8(mode == 3 ? 0 : mode);
+            if (mode == 3) {
+                const ull slot = atomicAdd(&a.ctr->nbig, 1ull);
+                a.biglist[slot] = u32(gl);
+            } else if (mode == 1) {
+                acc.committed++;
+                acc.tomb += added;
+                acc.missed += missed;
+                acc.writes += added;
+                acc.vd -= added;
+                acc.td += added;
+            } else if (mode == 2) {
+                acc.committed++;
+                acc.missed += missed;
+                acc.writes += 16 + (a.large ? moves : 0u);
+                acc.merge += 16;
+                acc.vd += (long long)k - (long long)nv;
+                acc.td -= __popc(nonempty & ~valid);
+                acc.ed += (k == 0 ? 1 : 0) - (nonempty == 0 ? 1 : 0);
+            }
+        }
+    }
+    warp_reduce_acc(acc);
+    if ((threadIdx.x & 31u) != 0) acc = Acc{};
+    block_flush(acc, a.ctr);
+}
+
+// --- warp tiers.  G = 16 (half-warp per group: leaf-level segments, two
+// groups per warp) or G = 32 (full warp: level-1 segments).  Lane hl of a
+// group owns slot hl of its segment (keys, values, state in registers).
+// Updates are ranked lane-parallel, G at a time: each lane binary-searches its
+// update among the segment's Valid keys (the r-th Valid key sits in lane
+// __fns(valid, 0, r+1)), so a group costs O(|slice| / G) warp iterations even
+// for hub rows with thousands of updates.  Every ballot / shuffle runs on all
+// 32 lanes and is split per group, so the two half-warp groups never diverge
+// around a warp collective.  Outcomes: tombstone flips, merge + even
+// re-dispatch with fused leaf-header / row-offset refresh, or deferral.
+template <int G>
+__global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitArgs a) {
+    static_assert(G == 16 || G == 32, "group width");
+    constexpr unsigned GM = G == 32 ? 0xffffffffu : 0xffffu;
+    constexpr int kSearch = G == 32 ? 6 : 5;
+    __shared__ u64 s_ok[kWarpTierWarps][32], s_ov[kWarpTierWarps][32];
+    __shared__ u64 s_ik[kWarpTierWarps][32], s_iv[kWarpTierWarps][32];
+    __shared__ u64 s_vk[kWarpTierWarps][32];             // Valid keys of the segment, compacted
+    __shared__ unsigned char s_vl[kWarpTierWarps][32];   // their lanes
+    __shared__ unsigned char s_ir[kWarpTierWarps][32];   // insert p: # Valid keys below it
+    const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
+    const unsigned hb = G == 32 ? 0u : (lane & 16u), hl = lane & unsigned(G - 1);
     const ull ngroups = a.ctr->ngroups;
     const unsigned m = unsigned(a.m);
+    const unsigned leaf = unsigned(a.leaf);
+    const unsigned nleaves = m / leaf;
+    const unsigned leafmask = (leaf >= 32) ? 0xffffffffu : ((1u << leaf) - 1u);
+    const unsigned below = (1u << hl) - 1u;  // lanes of my group below me (hl < 32)
+    // big-slice mode: process only the groups the leaf kernel handed over
+    const ull nlist = a.biglist ? a.ctr->nbig : ngroups;
     Acc acc;
-    for (ull g = ull(blockIdx.x) * kWarpTierWarps + w; g < ngroups; g += ull(gridDim.x) * kWarpTierWarps) {
-        const u32 lo = a.gstart[g], hi = a.gstart[g + 1];
-        const u32 s = hi - lo;
-        const u64 seg = u64(a.ul[a.pidx[lo]]) >> a.level;
-        const u64 b = seg * m;
-        u8 stt = kEmpty;
-        u64 key = 0;
-        if (lane < m) {
-            stt = a.st[b + lane];
-            key = a.keys[b + lane];
-        }
-        const unsigned valid = __ballot_sync(FULL, stt == kValid);
-        const unsigned nonempty = __ballot_sync(FULL, stt != kEmpty);
-        const unsigned tombm = __ballot_sync(FULL, stt == kTombstone);
-        const unsigned nv = __popc(valid);
-        unsigned ins = 0;
-        for (u32 c = 0; c < s; c += 32) {
-            const bool isins = (c + lane < s) && a.uop[a.pidx[lo + c + lane]] == kOpInsert;
-            ins += __popc(__ballot_sync(FULL, isins));
-        }
-        const u32 dels = s - ins;
-        u8 flag = 0;
-        if (!a.eager && ins == 0) {
-            // commit_tombstones (segment_engine.hpp:285-310): flip matches, no moves
-            unsigned added = 0;
-            for (u32 c = 0; c < s; c += 32) {
-                const bool act = c + lane < s;
-                const u64 u = act ? a.uk[a.pidx[lo + c + lane]] : 0;
-                int hit = -1;
-                for (unsigned t = 0; t < m; ++t) {
-                    const u64 kt = __shfl_sync(FULL, key, t);
-                    if (act && ((nonempty >> t) & 1u) && kt == u) hit = int(t);
-                }
-                const bool flip = act && hit >= 0 && ((valid >> hit) & 1u);
-                if (flip) a.st[b + hit] = kTombstone;
-                added += __popc(__ballot_sync(FULL, flip));
+    for (ull g0 = (ull(blockIdx.x) * kWarpTierWarps + w) * 32; g0 < nlist;
+         g0 += ull(gridDim.x) * kWarpTierWarps * 32) {
+        u32 t_lo = 0, t_hi = 0, t_seg = 0, t_gid = 0;
+        if (a.biglist) {
+            if (g0 + lane < nlist) {
+                t_gid = a.biglist[g0 + lane];
+                t_lo = a.gstart[t_gid];
+                t_hi = a.gstart[t_gid + 1];
+                t_seg = a.gseg[t_gid];
             }
-            acc.tomb += added;
-            acc.missed += s - added;
-            acc.writes += added;
-            acc.vd -= added;
-            acc.td += added;
-            flag = 1;
-        } else if (nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn)) {
-            flag = 0;  // deferred: escalate with the parent next round
         } else {
-            // merge (segment_engine.hpp:119-137) + place_evenly (pma.hpp:440-467)
-            unsigned mdel = 0, mins = 0, missed = 0, nins = 0;
-            for (u32 c = 0; c < s; c += 32) {
-                const bool act = c + lane < s;
-                u64 u = 0, uval = 0;
-                u8 op = kOpDelete;
-                if (act) {
-                    const u32 pi = a.pidx[lo + c + lane];
-                    u = a.uk[pi];
-                    op = a.uop[pi];
-                    if (op == kOpInsert) uval = a.uv[pi];
-                }
-                unsigned r = 0;
-                int hit = -1;
-                for (unsigned t = 0; t < m; ++t) {
-                    const u64 kt = __shfl_sync(FULL, key, t);
-                    const bool v = (valid >> t) & 1u;
-                    r += (v && kt < u);
-                    if (v && kt == u) hit = int(t);
-                }
-                const bool isdel = act && op == kOpDelete, isins = act && op == kOpInsert;
-                mdel |= __reduce_or_sync(FULL, (isdel && hit >= 0) ? (1u << hit) : 0u);
-                mins |= __reduce_or_sync(FULL, (isins && hit >= 0) ? (1u << hit) : 0u);
-                missed += __popc(__ballot_sync(FULL, isdel && hit < 0));
-                const unsigned insm = __ballot_sync(FULL, isins);
-                if (isins) {
-                    const unsigned p = nins + __popc(insm & lanemask_lt());
-                    s_ik[w][p] = u;
-                    s_iv[w][p] = uval;
-                    s_ir[w][p] = r;
-                }
-                nins += __popc(insm);
-            }
-            __syncwarp();
-            const unsigned surv = valid & ~(mdel | mins);
-            const unsigned k = __popc(surv) + nins;
-            if ((surv >> lane) & 1u) {
-                const unsigned sr = __popc(surv & lanemask_lt());
-                const unsigned re = __popc(valid & lanemask_lt());
-                unsigned ib = 0;
-                for (unsigned p = 0; p < nins; ++p) ib += s_ir[w][p] <= re;
-                s_ok[w][sr + ib] = key;
-                s_ov[w][sr + ib] = a.vals[b + lane];
-            }
-            if (lane < nins) {
-                const unsigned r = s_ir[w][lane];
-                const unsigned below = (r < nv) ? ((1u << __fns(valid, 0, int(r) + 1)) - 1u) : 0xffffffffu;
-                const unsigned sb = __popc(surv & below);
-                s_ok[w][sb + lane] = s_ik[w][lane];
-                s_ov[w][sb + lane] = s_iv[w][lane];
-            }
-            __syncwarp();
-            if (lane < m) {
-                u64 j = 0;
-                const bool tgt = placement_target(lane, k, m, &j);
-                a.keys[b + lane] = tgt ? s_ok[w][j] : 0;
-                a.vals[b + lane] = tgt ? s_ov[w][j] : 0;
-                a.st[b + lane] = tgt ? kValid : kEmpty;
-            }
-            unsigned moves = 0;
-            if (a.large) {
-                const unsigned pa = valid & ~mdel;
-                const bool in = (pa >> lane) & 1u;
-                moves = __popc(__ballot_sync(FULL, in && unsigned(__popc(pa & lanemask_lt())) != lane));
-            }
-            __syncwarp();
-            acc.missed += missed;
-            acc.writes += m + moves;
-            acc.merge += m;
-            acc.vd += (long long)k - (long long)nv;
-            acc.td -= __popc(tombm);
-            flag = 2;
+            load_group_tile(a, g0, ngroups, lane, t_lo, t_hi, t_seg);
+            t_gid = u32(g0 + lane);
         }
-        if (flag) acc.committed++;
-        if (lane == 0) a.gflag[g] = flag;
+        const unsigned tile_n = (nlist - g0) < 32 ? unsigned(nlist - g0) : 32u;
+        for (unsigned j = 0; j < tile_n; j += 32 / G) {
+            const unsigned gi = j + (hb >> 4);
+            const bool act = gi < tile_n;
+            const u32 lo = __shfl_sync(FULL, t_lo, gi & 31u);
+            const u32 hi = __shfl_sync(FULL, t_hi, gi & 31u);
+            const u32 sv = __shfl_sync(FULL, t_seg, gi & 31u);
+            const u32 s = act ? hi - lo : 0u;
+            const u64 b = u64(sv) * m;
+            u8 stt = kEmpty;
+            u64 key = 0, val = 0;
+            if (act && hl < m) {
+                stt = a.st[b + hl];
+                key = a.keys[b + hl];
+                val = a.vals[b + hl];
+            }
+            u64 ck = 0, cv = 0;
+            u8 co = kOpDelete;
+            if (hl < s) {
+                const u32 pi = a.pidx ? a.pidx[lo + hl] : lo + hl;
+                ck = a.uk[pi];
+                co = a.uop[pi];
+                cv = a.uv[pi];
+            }
+            const unsigned valid = (__ballot_sync(FULL, stt == kValid) >> hb) & GM;
+            const unsigned nonempty = (__ballot_sync(FULL, stt != kEmpty) >> hb) & GM;
+            const unsigned nv = __popc(valid);
+            unsigned ins = __popc((__ballot_sync(FULL, hl < s && co == kOpInsert) >> hb) & GM);
+            const u32 smax = __reduce_max_sync(FULL, s);
+            for (u32 c = G; c < smax; c += G) {
+                bool isins = false;
+                if (c + hl < s) isins = a.uop[a.pidx ? a.pidx[lo + c + hl] : lo + c + hl] == kOpInsert;
+                ins += __popc((__ballot_sync(FULL, isins) >> hb) & GM);
+            }
+            const u32 dels = s - ins;
+            int mode = 0;  // 0 defer, 1 tombstones, 2 merge
+            if (act) {
+                if (!a.eager && ins == 0) mode = 1;
+                else if (!(nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn))) mode = 2;
+            }
+            unsigned hits = 0, mdel = 0, missed = 0, nins = 0;
+            const unsigned vrank = __popc(valid & below);
+            if ((valid >> hl) & 1u) {
+                s_vk[w][hb + vrank] = key;
+                s_vl[w][hb + vrank] = (unsigned char)hl;
+            }
+            __syncwarp();
+            if (__any_sync(FULL, mode != 0)) {
+                for (u32 c = 0; c < smax; c += G) {
+                    if (c > 0) {
+                        ck = cv = 0;
+                        co = kOpDelete;
+                        if (mode != 0 && c + hl < s) {
+                            const u32 pi = a.pidx ? a.pidx[lo + c + hl] : lo + c + hl;
+                            ck = a.uk[pi];
+                            co = a.uop[pi];
+                            cv = a.uv[pi];
+                        }
+                    }
+                    const bool in = mode != 0 && c + hl < s;
+                    // rank of my update among the Valid keys (binary search in smem)
+                    unsigned rlo = 0, rhi = nv;
+#pragma unroll
+                    for (int it = 0; it < kSearch; ++it) {
+                        if (rlo < rhi) {
+                            const unsigned mid = (rlo + rhi) >> 1;
+                            if (s_vk[w][hb + mid] < ck) rlo = mid + 1;
+                            else rhi = mid;
+                        }
+                    }
+                    const bool hit = in && rlo < nv && s_vk[w][hb + rlo] == ck;
+                    const bool isins = in && co == kOpInsert;
+                    const unsigned hitbit = hit ? (1u << (unsigned(s_vl[w][hb + rlo]) + hb)) : 0u;
+                    hits |= (__reduce_or_sync(FULL, hitbit) >> hb) & GM;
+                    mdel |= (__reduce_or_sync(FULL, (hit && !isins) ? hitbit : 0u) >> hb) & GM;
+                    missed += __popc((__ballot_sync(FULL, in && !isins && !hit) >> hb) & GM);
+                    const unsigned im = (__ballot_sync(FULL, isins) >> hb) & GM;
+                    if (isins && mode == 2) {
+                        const unsigned p = nins + __popc(im & below);
+                        s_ik[w][hb + p] = ck;
+                        s_iv[w][hb + p] = cv;
+                        s_ir[w][hb + p] = (unsigned char)rlo;
+                    }
+                    nins += __popc(im);
+                }
+            }
+            __syncwarp();
+            if (mode == 1 && ((hits >> hl) & 1u)) a.st[b + hl] = kTombstone;
+            // merge output (merge_entries order): insert p lands at p + survivors
+            // below it; survivor t lands at its survivor rank + inserts below it
+            const unsigned surv = valid & ~hits;
+            const unsigned k = __popc(surv) + nins;
+            const bool is_ins = mode == 2 && hl < nins;
+            unsigned ipos = 0;
+            u64 ik = 0, iv = 0;
+            if (is_ins) {
+                ik = s_ik[w][hb + hl];
+                iv = s_iv[w][hb + hl];
+                const unsigned r = s_ir[w][hb + hl];
+                const unsigned vbelow = r < nv ? ((1u << s_vl[w][hb + r]) - 1u) : GM;
+                ipos = hl + __popc(surv & vbelow);
+            }
+            unsigned spos = 0;
+            const bool is_surv = mode == 2 && ((surv >> hl) & 1u);
+            if (is_surv) {
+                unsigned ib = 0;
+                for (unsigned p = 0; p < nins; ++p) ib += s_ir[w][hb + p] <= vrank;
+                spos = __popc(surv & below) + ib;
+            }
+            const unsigned pa = valid & ~mdel;  // commit_in_place pass-A survivors
+            const unsigned moved =
+                (__ballot_sync(FULL, mode == 2 && ((pa >> hl) & 1u) && unsigned(__popc(pa & below)) != hl) >> hb) & GM;
+            if (is_ins) {
+                s_ok[w][hb + ipos] = ik;
+                s_ov[w][hb + ipos] = iv;
+            }
+            if (is_surv) {
+                s_ok[w][hb + spos] = key;
+                s_ov[w][hb + spos] = val;
+            }
+            __syncwarp();
+            if (mode == 2) {
+                if (hl < m) {
+                    u64 jj = 0;
+                    const bool tgt = placement_target(hl, k, m, &jj);
+                    const u64 nk = tgt ? s_ok[w][hb + jj] : 0;
+                    a.keys[b + hl] = nk;
+                    a.vals[b + hl] = tgt ? s_ov[w][hb + jj] : 0;
+                    a.st[b + hl] = tgt ? kValid : kEmpty;
+                    if (a.ro && tgt && is_guard(nk)) a.ro[src_of(nk) + 1] = b + hl + 1;  // graph.hpp:176
+                }
+                if (k >= nleaves) {
+                    if (hl < nleaves) a.hdr[b / leaf + hl] = s_ok[w][hb + (u64(hl) * leaf * k + m - 1) / m];
+                } else if (hl == 0) {
+                    const ull slot = atomicAdd(&a.ctr->nrefresh, 1ull);
+                    a.rlist[2 * slot] = b;
+                    a.rlist[2 * slot + 1] = b + m;
+                }
+            }
+            const u32 gid_ = __shfl_sync(FULL, t_gid, gi & 31u);
+            if (hl == 0 && act) {
+                a.gflag[gid_] = u8(mode);
+                if (mode == 1) {
+                    const unsigned added = __popc(hits);
+                    acc.committed++;
+                    acc.tomb += added;
+                    acc.missed += missed;
+                    acc.writes += added;
+                    acc.vd -= added;
+                    acc.td += added;
+                } else if (mode == 2) {
+                    int old_empty = 0;
+                    for (unsigned l = 0; l < nleaves; ++l) old_empty += ((nonempty >> (l * leaf)) & leafmask) == 0;
+                    acc.committed++;
+                    acc.missed += missed;
+                    acc.writes += m + (a.large ? __popc(moved) : 0u);
+                    acc.merge += m;
+                    acc.vd += (long long)k - (long long)nv;
+                    acc.td -= __popc(nonempty & ~valid);
+                    acc.ed += (k >= nleaves ? 0 : int(nleaves - k)) - old_empty;
+                }
+            }
+            __syncwarp();
+        }
     }
+    warp_reduce_acc(acc);
     if (lane != 0) acc = Acc{};
     block_flush(acc, a.ctr);
 }
@@ -438,7 +821,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
     for (ull g = blockIdx.x; g < ngroups; g += gridDim.x) {
         const u32 lo = a.gstart[g], hi = a.gstart[g + 1];
         const u64 s = hi - lo;
-        const u64 seg = u64(a.ul[a.pidx[lo]]) >> a.level;
+        const u64 seg = a.gseg[g];
         const u64 m = a.m;
         const u64 b = seg * m;
         SlicePending sl{a.uk, a.uv, a.uop, a.pidx, lo};
@@ -461,7 +844,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
             ull added = 0, missed = 0;
             for (u64 q = threadIdx.x; q < s; q += kCtaThreads) {
                 const u64 u = sl.key(q);
-                const u64 lb = u64(a.ul[a.pidx[lo + q]]) * a.leaf;
+                const u64 lb = u64(a.ul[sl.pid(q)]) * a.leaf;
                 bool hit = false;
                 for (u64 t = lb; t < lb + a.leaf; ++t) {
                     if (a.st[t] != kEmpty && a.keys[t] == u) {
@@ -488,6 +871,14 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
         } else if (nv + ins > a.mx || (a.eager && a.cap_gt_min && nv < dels + a.mn)) {
             flag = 0;
         } else {
+            const u64 nleaves = m / a.leaf;
+            ull old_empty = 0;
+            for (u64 l = threadIdx.x; l < nleaves; l += kCtaThreads) {
+                bool e = true;
+                for (u64 t = b + l * a.leaf; t < b + (l + 1) * a.leaf; ++t) e &= a.st[t] == kEmpty;
+                old_empty += e;
+            }
+            old_empty = block_sum(old_empty, s_w64);
             const MergeOut r = block_merge_segment(a.keys, a.vals, a.st, b, m, nv, sl, s, a.large != 0, a.ek, a.ev,
                                                    a.es, a.mflag, a.ok, a.ov, a.ik + lo, a.iv + lo, a.ir + lo);
             if (threadIdx.x == 0) {
@@ -496,6 +887,11 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
                 acc.merge += m;
                 acc.vd += (long long)r.k - (long long)nv;
                 acc.td -= (long long)nt;
+                const long long new_empty = r.k >= nleaves ? 0 : (long long)(nleaves - r.k);
+                acc.ed += new_empty - (long long)old_empty;
+                const ull slot = atomicAdd(&a.ctr->nrefresh, 1ull);  // headers/row offsets: post-pass
+                a.rlist[2 * slot] = b;
+                a.rlist[2 * slot + 1] = b + m;
             }
             flag = 2;
         }
@@ -511,14 +907,20 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
 
 // ------------------------------------------------------------- refresh
 
-// Leaf headers (and graph row offsets, graph.hpp:167-180) over one touched
-// range per CTA: hdr[i] = first non-Empty key at or after leaf i.
-__global__ void k_refresh_ranges(const u64* __restrict__ ranges, u64 nranges, const u64* __restrict__ keys,
-                                 const u8* __restrict__ st, u64 cap, u64 leaf, u64* __restrict__ hdr,
-                                 u64* __restrict__ ro) {
-    for (u64 r = blockIdx.x; r < nranges; r += gridDim.x) {
+// Leaf headers (and graph row offsets, graph.hpp:167-180) over the ranges
+// the commit kernels could not refresh in place (sparse or CTA-tier
+// segments), one warp per range: hdr[i] = first non-Empty key at or after
+// leaf i (the scan may run past the range end into untouched leaves).
+__global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_dev, u64 n_host,
+                                 const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u64 leaf,
+                                 u64* __restrict__ hdr, u64* __restrict__ ro) {
+    const u64 nranges = n_dev ? *n_dev : n_host;
+    const unsigned lane = threadIdx.x & 31u;
+    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 r = warp; r < nranges; r += nwarps) {
         const u64 b = ranges[2 * r], e = ranges[2 * r + 1];
-        for (u64 i = b / leaf + threadIdx.x; i < e / leaf; i += blockDim.x) {
+        for (u64 i = b / leaf + lane; i < (e + leaf - 1) / leaf; i += 32) {
             u64 v = ~0ull;
             for (u64 t = i * leaf; t < cap; ++t) {
                 if (st[t] != kEmpty) {
@@ -529,7 +931,7 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, u64 nranges, co
             hdr[i] = v;
         }
         if (ro) {
-            for (u64 t = b + threadIdx.x; t < e; t += blockDim.x) {
+            for (u64 t = b + lane; t < e; t += 32) {
                 if (st[t] == kValid) {
                     const u64 k = keys[t];
                     if (is_guard(k)) ro[src_of(k) + 1] = t + 1;
@@ -668,6 +1070,7 @@ void Pma::place_root_from(const u64* d_ek, const u64* d_ev, u64 k) {
     }
     valid_count = k;
     tombstone_count = 0;
+    empty_leaves = k >= num_leaves() ? 0 : (long long)(num_leaves() - k);  // spacing >= leaf: one entry per leaf
     headers_closed_form(d_ek, k);
 }
 
@@ -721,16 +1124,29 @@ void Pma::load_slots(size_t capacity, const u64* keys, const u64* values, const 
     }
     GPMA_CUDA(cudaMemcpyAsync(d_keys, k.data(), capacity * 8, cudaMemcpyHostToDevice, stream_));
     GPMA_CUDA(cudaMemcpyAsync(d_vals, v.data(), capacity * 8, cudaMemcpyHostToDevice, stream_));
-    // full header rebuild: one range covering everything + no left walk needed
-    u64 range[2] = {0, capacity};
-    stage_k.reserve(2);
-    GPMA_CUDA(cudaMemcpyAsync(stage_k.ptr, range, 16, cudaMemcpyHostToDevice, stream_));
-    k_refresh_ranges<<<1, 1024, 0, stream_>>>(stage_k.ptr, 1, d_keys, d_st, cap_, leaf_, d_hdr, nullptr);
+    // full header rebuild over 4096-slot chunks (forward scans cross chunks)
+    const u64 chunk = capacity < 4096 ? capacity : 4096;
+    std::vector<u64> ranges;
+    for (u64 b = 0; b < capacity; b += chunk) {
+        ranges.push_back(b);
+        ranges.push_back(b + chunk);
+    }
+    u64 empties = 0;
+    for (u64 l = 0; l < capacity / leaf_; ++l) {
+        bool e = true;
+        for (u64 t = l * leaf_; t < (l + 1) * leaf_; ++t) e &= states[t] == kEmpty;
+        empties += e;
+    }
+    stage_k.reserve(ranges.size());
+    GPMA_CUDA(cudaMemcpyAsync(stage_k.ptr, ranges.data(), ranges.size() * 8, cudaMemcpyHostToDevice, stream_));
+    k_refresh_ranges<<<grid_for(ranges.size() / 2 * 32, 256), 256, 0, stream_>>>(
+        stage_k.ptr, nullptr, ranges.size() / 2, d_keys, d_st, cap_, leaf_, d_hdr, nullptr);
     GPMA_LAUNCH_CHECK();
     GPMA_CUDA(cudaStreamSynchronize(stream_));
     valid_count = nv;
     tombstone_count = nt;
     slot_writes = 0;
+    empty_leaves = (long long)empties;
 }
 
 void Pma::download(u64* keys, u64* values, u8* states) {
@@ -886,11 +1302,10 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     pidx1.reserve(n);
     gid.reserve(n);
     gstart.reserve(n + 1);
+    gseg.reserve(n + 1);
     gflag.reserve(n);
     touched.reserve(2 * n + 2);
-    k_iota<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(pidx0.ptr, &d_ctr->n_unique);
-    GPMA_LAUNCH_CHECK();
-    ++launches;
+    rlist.reserve(2 * n + 4);
     GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
     event(2);
     // ---- 4. rounds ----
@@ -898,9 +1313,10 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     u64 npend = h_ctr->n_unique;
     u64* touched_ptr = touched.ptr;
     u64 ntouched = 0;
-    u32* pcur = pidx0.ptr;
-    u32* pnext = pidx1.ptr;
+    u32* pcur = nullptr;  // round 0: pending = all unique updates in order (identity)
+    u32* pnext = pidx0.ptr;
     float seg_ms = 0.f;
+    bool root_done = false;
     if (npend > 0) {
         for (int level = 0;; ++level) {
             const u64 m = leaf_ << level;
@@ -909,14 +1325,20 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 const u32* ulp = ul.ptr;
                 const u32* pp = pcur;
                 u32* gs = gstart.ptr;
+                u32* gg = gseg.ptr;
                 u32* gi = gid.ptr;
                 Ctr* ctr = d_ctr;
                 const int lv = level;
                 run_compact(
                     stream_, ws, &d_ctr->npend, 0, npend,
-                    [=] __device__(ull p) { return p == 0 || (ulp[pp[p]] >> lv) != (ulp[pp[p - 1]] >> lv); },
+                    [=] __device__(ull p) {
+                        return p == 0 || (ulp[pp ? pp[p] : p] >> lv) != (ulp[pp ? pp[p - 1] : p - 1] >> lv);
+                    },
                     [=] __device__(ull p, unsigned f, ull x) {
-                        if (f) gs[x] = u32(p);
+                        if (f) {
+                            gs[x] = u32(p);
+                            gg[x] = ulp[pp ? pp[p] : p] >> lv;
+                        }
                         gi[p] = u32(x + f - 1);
                     },
                     [=] __device__(ull total) {
@@ -937,8 +1359,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             a.ul = ul.ptr;
             a.pidx = pcur;
             a.gstart = gstart.ptr;
+            a.gseg = gseg.ptr;
             a.gflag = gflag.ptr;
             a.ctr = d_ctr;
+            a.hdr = d_hdr;
+            a.ro = d_row_offsets;
+            a.rlist = rlist.ptr;
             a.level = level;
             a.m = m;
             a.leaf = leaf_;
@@ -948,9 +1374,21 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             a.large = cfg.large_for(m);
             a.cap_gt_min = cap_ > 16;
             GPMA_CUDA(cudaEventRecord(ev_[5], stream_));
-            if (m <= 32) {
-                const unsigned grid = grid_for(npend, kWarpTierWarps, 148 * 8);
-                k_commit_warp<<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+            if (m == 16 && leaf_ == 16) {
+                biglist.reserve(npend + 1);
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->nbig, 0, sizeof(ull), stream_));
+                const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, 148 * 16);
+                k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
+                GPMA_LAUNCH_CHECK();
+                a.biglist = biglist.ptr;  // hub groups: lane-parallel ranking
+                const unsigned grid2 = grid_for((npend / kBigSlice + 31) / 32 + 1, kWarpTierWarps, 148 * 2);
+                k_commit_lanes<16><<<grid2, kWarpTierWarps * 32, 0, stream_>>>(a);
+            } else if (m <= 16) {
+                const unsigned grid = grid_for((npend + 31) / 32, kWarpTierWarps, 148 * 8);
+                k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+            } else if (m <= 32) {
+                const unsigned grid = grid_for((npend + 31) / 32, kWarpTierWarps, 148 * 8);
+                k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
             } else {
                 ensure_slot_scratch();
                 ik.reserve(n);
@@ -974,18 +1412,15 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             // touched list (merge commits, in segment order)
             {
                 const u8* gf = gflag.ptr;
-                const u32* gs = gstart.ptr;
-                const u32* ulp = ul.ptr;
-                const u32* pp = pcur;
+                const u32* gg = gseg.ptr;
                 u64* tp = touched_ptr;
                 const u64 base = ntouched;
-                const int lv = level;
                 Ctr* ctr = d_ctr;
                 run_compact(
                     stream_, ws, &d_ctr->ngroups, 0, npend, [=] __device__(ull g) { return gf[g] == 2; },
                     [=] __device__(ull g, unsigned f, ull x) {
                         if (!f) return;
-                        const u64 seg = u64(ulp[pp[gs[g]]]) >> lv;
+                        const u64 seg = gg[g];
                         tp[2 * (base + x)] = seg * m;
                         tp[2 * (base + x) + 1] = seg * m + m;
                     },
@@ -1003,7 +1438,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 run_compact(
                     stream_, ws, &d_ctr->npend, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
                     [=] __device__(ull p, unsigned f, ull x) {
-                        if (f) pn[x] = pp[p];
+                        if (f) pn[x] = pp ? pp[p] : u32(p);
                     },
                     [=] __device__(ull total) { ctr->npend_next = total; });
                 ++launches;
@@ -1019,7 +1454,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             if (left == 0) break;
             if (level == height_) {
                 // root path: everything left is the single root group
-                std::swap(pcur, pnext);
+                pcur = pnext;
+                pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
                 npend = left;
                 GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->npend_next, sizeof(ull), cudaMemcpyDeviceToDevice,
                                           stream_));
@@ -1142,7 +1578,9 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 slot_writes += cap_ + moves;
                 valid_count = k;
                 tombstone_count = 0;
+                empty_leaves = k >= num_leaves() ? 0 : (long long)(num_leaves() - k);
                 headers_closed_form(ok.ptr, k);
+                root_done = true;
                 st.num_levels = height_ + 1;
                 st.segments_per_level[height_]++;
                 st.rounds++;
@@ -1162,11 +1600,14 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 }
                 // counters already applied; clear device deltas
                 GPMA_CUDA(cudaMemsetAsync(&d_ctr->valid_delta, 0, sizeof(long long) * 2, stream_));
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->empty_delta, 0, sizeof(long long), stream_));
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->nrefresh, 0, sizeof(ull), stream_));
                 GPMA_CUDA(cudaMemsetAsync(&d_ctr->missed, 0, sizeof(ull) * 5, stream_));
                 sync_ctr();
                 break;
             }
-            std::swap(pcur, pnext);
+            pcur = pnext;
+            pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
             npend = left;
             GPMA_CUDA(
                 cudaMemcpyAsync(&d_ctr->npend, &d_ctr->npend_next, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
@@ -1182,18 +1623,30 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.tombstone_flips = st.tombstones_added;
     event(3);
     // ---- 5. refresh leaf headers / row offsets ----
+    // The warp tier refreshed dense segments in place; sparse and CTA-tier
+    // segments were queued on rlist; left walks are needed only while empty
+    // leaves exist (their headers inherit the next leaf's first key).
     last_resized = st.resized;
     last_ntouched = ntouched;
-    if (st.resized) {
-        // headers already rebuilt in closed form by the final placement
+    if (root_done) {
+        // whole array re-placed: headers rebuilt in closed form already
         if (d_row_offsets) rebuild_row_offsets_full();
-    } else if (ntouched > 0) {
-        k_refresh_ranges<<<grid_for(ntouched, 1, 148 * 8), 256, 0, stream_>>>(touched_ptr, ntouched, d_keys, d_st, cap_,
-                                                                                leaf_, d_hdr, d_row_offsets);
-        GPMA_LAUNCH_CHECK();
-        k_left_walk<<<grid_for(ntouched, 128, 148 * 4), 128, 0, stream_>>>(touched_ptr, ntouched, d_st, leaf_, d_hdr);
-        GPMA_LAUNCH_CHECK();
-        launches += 2;
+        ++launches;
+    } else {
+        if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
+        const u64 nref = h_ctr->nrefresh;
+        if (nref > 0) {
+            k_refresh_ranges<<<grid_for(nref * 32, 256, 148 * 16), 256, 0, stream_>>>(
+                rlist.ptr, nullptr, nref, d_keys, d_st, cap_, leaf_, d_hdr, d_row_offsets);
+            GPMA_LAUNCH_CHECK();
+            ++launches;
+        }
+        if (ntouched > 0 && empty_leaves != 0) {
+            k_left_walk<<<grid_for(ntouched, 128, 148 * 8), 128, 0, stream_>>>(touched_ptr, ntouched, d_st, leaf_,
+                                                                               d_hdr);
+            GPMA_LAUNCH_CHECK();
+            ++launches;
+        }
     }
     event(4);
     GPMA_CUDA(cudaStreamSynchronize(stream_));

@@ -46,7 +46,10 @@ struct Ctr {
     ull k;
     ull nt;
     ull key0;
-    ull pad[8];
+    ull nrefresh;
+    long long empty_delta;
+    ull nbig;
+    ull pad[5];
 };
 
 struct EngineCfg {
@@ -120,6 +123,9 @@ public:
     u64 tombstone_count = 0;
     u64 slot_writes = 0;
     bool last_resized = false;
+    // number of all-Empty leaves (-1 = unknown after sequential ops): the
+    // left-walk header pass only runs when empty leaves can exist
+    long long empty_leaves = 0;
     u64 last_ntouched = 0;
 
     // device slot arrays
@@ -166,7 +172,9 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u64> uk, uv;
     DevBuf<u8> uop;
     DevBuf<u32> ul;
-    DevBuf<u32> pidx0, pidx1, gid, gstart;
+    DevBuf<u32> pidx0, pidx1, gid, gstart, gseg;
+    DevBuf<u64> rlist;  // ranges whose headers/row offsets need the post-pass
+    DevBuf<u32> biglist;  // leaf groups with > kBigSlice updates (lane-parallel kernel)
     DevBuf<u8> gflag;
     DevBuf<u64> touched;  // pairs (b, e)
     DevBuf<u64> ik, iv;   // insert lists (pending space)

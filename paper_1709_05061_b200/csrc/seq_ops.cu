@@ -255,6 +255,7 @@ static SeqResult run_seq(Pma& p, SeqArgs a, cudaStream_t s, DevBuf<u64>& ikb, De
     p.valid_count = u64((long long)p.valid_count + h.vd);
     p.tombstone_count = u64((long long)p.tombstone_count + h.td);
     p.slot_writes += h.writes;
+    if (h.writes > 0 && a.op != kSeqMark) p.empty_leaves = -1;  // unknown until the next full placement
     return h;
 }
 

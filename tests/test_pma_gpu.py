@@ -148,6 +148,40 @@ def test_skewed_batches_escalate_levels():
         assert g.capacity() >= 1024
 
 
+def _sparse_layout(rng, cap, occupancy, tomb_frac):
+    """Sorted keys at random slots (runs of empty leaves), some tombstones."""
+    n = int(cap * occupancy)
+    slots = np.sort(rng.choice(cap, n, replace=False))
+    keys = np.sort(rng.choice(2**30, n, replace=False)).astype(np.uint64)
+    k = np.zeros(cap, np.uint64)
+    v = np.zeros(cap, np.uint64)
+    s = np.zeros(cap, np.uint8)
+    k[slots], v[slots] = keys, keys * 3
+    s[slots] = np.where(rng.random(n) < tomb_frac, 2, 1)
+    return k, v, s, keys
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_empty_leaf_runs_and_header_refresh(mode):
+    """Layouts with long runs of empty leaves exercise the backward-filled
+    header refresh (left walks, forward scans) against the reference's
+    top-down leaf search."""
+    rng = np.random.default_rng(17 + mode)
+    for trial in range(10):
+        cap = int(2 ** rng.integers(8, 15))
+        k, v, s, keys = _sparse_layout(rng, cap, float(rng.uniform(0.02, 0.3)), 0.2)
+        g, r = pair(k, v, s)
+        probe = rng.integers(0, 2**30, 500, dtype=np.uint64)
+        assert (g.binary_search_leaf(probe) == r.binary_search_leaf(probe)).all()
+        for b in range(6):
+            nb = int(rng.integers(1, 400))
+            kk = np.where(rng.random(nb) < 0.5, rng.choice(keys, nb), rng.integers(0, 2**30, nb)).astype(np.uint64)
+            vv = rng.integers(0, 2**63, nb, dtype=np.uint64)
+            oo = (rng.random(nb) < 0.6).astype(np.uint8)
+            run_both(g, r, kk, vv, oo, mode, -1, f"trial {trial} batch {b}")
+            assert (g.binary_search_leaf(probe) == r.binary_search_leaf(probe)).all(), f"trial {trial} batch {b}"
+
+
 def test_large_array_and_batch():
     rng = np.random.default_rng(11)
     keys = np.unique(rng.integers(0, 2**40, 300000, dtype=np.uint64))
