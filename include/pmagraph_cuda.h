@@ -123,6 +123,10 @@ typedef struct pma_timing {
     uint64_t kernel_launches;
     uint64_t merge_slots;  /* slots rewritten by merge commits (algorithmic scatter) */
     uint64_t tombstone_flips;
+    double level_ms[16];   /* commit-kernel time per tree level (rounds) */
+    uint64_t level_groups[16]; /* groups examined per level */
+    uint64_t level_big[16];    /* hub groups sent to the CTA kernel per level */
+    uint64_t level_max_slice[16]; /* largest update slice per level */
 } pma_timing;
 
 typedef struct pma_handle pma_handle;
@@ -268,6 +272,10 @@ int gpma_last_timing(const gpma_graph* g, pma_timing* out);
  * can bracket calls with CUDA events on the launching stream. */
 void* gpma_cuda_stream(gpma_graph* g);
 void* pma_cuda_stream(pma_handle* h);
+
+/* Drive every kernel once on small synthetic inputs so CUDA's lazy module
+ * loading never lands inside a timed region (call once per process/device). */
+int gpma_warmup(int device);
 
 #ifdef __cplusplus
 }

@@ -82,6 +82,10 @@ class pma_timing(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("merge_slots", C.c_uint64),
         ("tombstone_flips", C.c_uint64),
+        ("level_ms", C.c_double * 16),
+        ("level_groups", C.c_uint64 * 16),
+        ("level_big", C.c_uint64 * 16),
+        ("level_max_slice", C.c_uint64 * 16),
     ]
 
 
@@ -198,6 +202,7 @@ SIGNATURES = [
     ("gpma_last_timing", C.c_int, [_P, C.POINTER(pma_timing)]),
     ("gpma_cuda_stream", _P, [_P]),
     ("pma_cuda_stream", _P, [_P]),
+    ("gpma_warmup", C.c_int, [C.c_int]),
     # pmagraph_stream.h
     ("gpma_stream_last_error", C.c_char_p, []),
     ("gpma_stream_rmat", C.c_int, [C.c_size_t, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(_P)]),

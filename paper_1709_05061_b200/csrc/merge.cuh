@@ -15,6 +15,7 @@ namespace gpma {
 constexpr int kCtaThreads = 256;
 constexpr int kCtaItems = 4;
 constexpr int kCtaTile = kCtaThreads * kCtaItems;
+constexpr int kCtaSmemE = 2048;  // E entries staged in smem for the rank searches
 
 struct SlicePending {
     const u64* uk;
@@ -79,29 +80,38 @@ __device__ MergeOut block_merge_segment(u64* keys, u64* vals, u8* st, u64 b, u64
         base += tot;
     }
     __syncthreads();
-    // B: slice ranks in E; mark matches; ordered insert list
+    // B: slice ranks in E; mark matches; ordered insert list.  One block
+    // scan orders the inserts; each thread then walks a contiguous run of the
+    // sorted slice, ranking each update by binary search from its previous
+    // rank (E staged in smem when it fits).
+    __shared__ u64 s_e[kCtaSmemE];
+    const bool e_smem = nv <= kCtaSmemE;
+    if (e_smem)
+        for (u64 j = threadIdx.x; j < nv; j += kCtaThreads) s_e[j] = ek[b + j];
+    __syncthreads();
+    const u64* E = e_smem ? s_e : ek + b;
+    const u64 R = (s + kCtaThreads - 1) / kCtaThreads;
+    const u64 q0 = u64(threadIdx.x) * R;
+    const u64 q1 = (q0 + R < s) ? q0 + R : s;
+    u32 myins = 0;
+    for (u64 q = q0; q < q1; ++q) myins += sl.op(q) == kOpInsert;
     u32 nins = 0;
+    u32 p = block_excl_scan(myins, &nins, s_w);
     ull missed = 0;
-    for (u64 q0 = 0; q0 < s; q0 += kCtaThreads) {
-        const u64 q = q0 + threadIdx.x;
-        bool isins = false;
-        u64 u = 0, r = 0;
-        if (q < s) {
-            u = sl.key(q);
-            isins = sl.op(q) == kOpInsert;
-            r = lower_bound_dev(ek + b, nv, u);
-            const bool match = r < nv && ek[b + r] == u;
-            if (match) mflag[b + r] = isins ? 2 : 1;
-            else if (!isins) ++missed;
-        }
-        u32 tot;
-        const u32 p = block_excl_scan(isins ? 1u : 0u, &tot, s_w) + nins;
+    u64 r = 0;
+    for (u64 q = q0; q < q1; ++q) {
+        const u64 u = sl.key(q);
+        r += lower_bound_dev(E + r, nv - r, u);
+        const bool isins = sl.op(q) == kOpInsert;
+        const bool match = r < nv && E[r] == u;
+        if (match) mflag[b + r] = isins ? 2 : 1;
+        else if (!isins) ++missed;
         if (isins) {
             ik[p] = u;
             iv[p] = sl.val(q);
             ir[p] = u32(r);
+            ++p;
         }
-        nins += tot;
     }
     missed = block_sum(missed, s_w64);
     __syncthreads();

@@ -195,6 +195,17 @@ __global__ void k_compress(const u64* keys, u64 n, BitRuns runs, u64* ck, u32* c
     }
 }
 
+__global__ void k_gather_sorted(const u32* __restrict__ ci, const u64* __restrict__ dk, const u64* __restrict__ dv,
+                                const u8* __restrict__ dop, u64 n, u64* __restrict__ gk, u64* __restrict__ gv,
+                                u8* __restrict__ go) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const u32 a = ci[i];
+        gk[i] = dk[a];
+        gv[i] = dv ? dv[a] : 0;
+        go[i] = dop[a];
+    }
+}
+
 __global__ void k_iota(u32* p, const ull* n_dev) {
     const u64 n = *n_dev;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) p[i] = u32(i);
@@ -226,6 +237,7 @@ struct CommitArgs {
     u64* ro;
     u64* rlist;
     u32* biglist;
+    unsigned tile;  // groups per warp tile (lane tiers)
     int level;
     u64 m;
     u64 leaf;
@@ -343,52 +355,99 @@ __device__ __forceinline__ void load_group_tile(const CommitArgs& a, ull g0, ull
 // rows) are handed to the lane-parallel kernel through `biglist`.
 constexpr int kLeafWarps = 4;
 constexpr int kRow = 17;        // padded u64 row (conflict-free column access)
-constexpr u32 kBigSlice = 32;
+constexpr u32 kBigSlice = 32;   // leaf kernel: larger slices go to the CTA kernel
+constexpr u32 kLaneBig = 64;    // lane kernels: larger slices go to the CTA kernel
+constexpr u32 kStage = 128;     // updates of a 32-group tile staged in smem
 
 __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
     __shared__ u64 s_k[kLeafWarps][32 * kRow];
     __shared__ u64 s_v[kLeafWarps][32 * kRow];
+    __shared__ u64 s_uk[kLeafWarps][kStage];
+    __shared__ u64 s_uv[kLeafWarps][kStage];
+    __shared__ u8 s_uo[kLeafWarps][kStage];
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     u64* rk = &s_k[w][lane * kRow];
     u64* rv = &s_v[w][lane * kRow];
     const ull ngroups = a.ctr->ngroups;
+    const ull gstride = ull(gridDim.x) * kLeafWarps * 32;
+    ull g0 = (ull(blockIdx.x) * kLeafWarps + w) * 32;
+    // descriptors of the first tile; each iteration prefetches the next tile's
+    u32 n_lo = 0, n_hi = 0, n_seg = 0;
+    if (g0 + lane < ngroups) {
+        n_lo = a.gstart[g0 + lane];
+        n_hi = a.gstart[g0 + lane + 1];
+        n_seg = a.gseg[g0 + lane];
+    }
     Acc acc;
-    for (ull g0 = (ull(blockIdx.x) * kLeafWarps + w) * 32; g0 < ngroups; g0 += ull(gridDim.x) * kLeafWarps * 32) {
+    for (; g0 < ngroups; g0 += gstride) {
         const ull gl = g0 + lane;
         const bool act = gl < ngroups;
-        u32 lo = 0, hi = 0;
-        u64 b = 0;
+        const u32 lo = n_lo, hi = n_hi;
+        const u64 b = u64(n_seg) * 16;
+        const unsigned tile_n = (ngroups - g0) < 32 ? unsigned(ngroups - g0) : 32u;
+        {
+            const ull gn = gl + gstride;
+            n_lo = n_hi = n_seg = 0;
+            if (gn < ngroups) {
+                n_lo = a.gstart[gn];
+                n_hi = a.gstart[gn + 1];
+                n_seg = a.gseg[gn];
+            }
+        }
         uint4 sv = make_uint4(0, 0, 0, 0);
-        if (act) {
-            lo = a.gstart[gl];
-            hi = a.gstart[gl + 1];
-            b = u64(a.gseg[gl]) * 16;
-            sv = *reinterpret_cast<const uint4*>(a.st + b);
+        if (act) sv = *reinterpret_cast<const uint4*>(a.st + b);
+        // stage the tile's updates (contiguous in pending order)
+        const u32 tlo = __shfl_sync(FULL, lo, 0);
+        const u32 thi = __shfl_sync(FULL, hi, tile_n - 1);
+        const u32 staged = (thi - tlo) < kStage ? (thi - tlo) : kStage;
+        for (u32 i = lane; i < staged; i += 32) {
+            const u32 pi = a.pidx ? a.pidx[tlo + i] : tlo + i;
+            s_uk[w][i] = a.uk[pi];
+            s_uv[w][i] = a.uv[pi];
+            s_uo[w][i] = a.uop[pi];
         }
         const u32 s = hi - lo;
+        const u32 soff = lo - tlo;
+        auto U = [&](u32 q, u64& key, u8& op) {
+            const u32 i = soff + q;
+            if (i < staged) {
+                key = s_uk[w][i];
+                op = s_uo[w][i];
+            } else {
+                const u32 pi = a.pidx ? a.pidx[lo + q] : lo + q;
+                key = a.uk[pi];
+                op = a.uop[pi];
+            }
+        };
+        auto UVAL = [&](u32 q) -> u64 {
+            const u32 i = soff + q;
+            return i < staged ? s_uv[w][i] : a.uv[a.pidx ? a.pidx[lo + q] : lo + q];
+        };
         // keys of the tile: 8 lanes per leaf line, 4 leaves per instruction
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
             const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
             const u64 gb = __shfl_sync(FULL, b, grp);
-            if (__shfl_sync(FULL, act ? 1 : 0, grp)) {
+            if (grp < tile_n) {
                 const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(a.keys + gb + 2 * part);
                 s_k[w][grp * kRow + 2 * part] = kk.x;
                 s_k[w][grp * kRow + 2 * part + 1] = kk.y;
             }
         }
         // state masks (bit i = slot i)
-        const u32 words[4] = {sv.x, sv.y, sv.z, sv.w};
         unsigned valid = 0, nonempty = 0;
+        {
+            const u32 words[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-#pragma unroll
-            for (int by = 0; by < 4; ++by) {
-                const u32 x = (words[q] >> (8 * by)) & 0xffu;
-                valid |= unsigned(x == kValid) << (q * 4 + by);
-                nonempty |= unsigned(x != kEmpty) << (q * 4 + by);
+            for (int q = 0; q < 4; ++q) {
+                const u32 x = words[q];
+                const u32 v1 = x & 0x01010101u;             // state 1 = Valid
+                const u32 ne = (x | (x >> 1)) & 0x01010101u; // non-zero byte
+                valid |= ((v1 * 0x01020408u) >> 24 & 0xfu) << (4 * q);
+                nonempty |= ((ne * 0x01020408u) >> 24 & 0xfu) << (4 * q);
             }
         }
+        __syncwarp();
         const unsigned nv = __popc(valid);
         int mode = 0;  // 0 defer, 1 tombstones, 2 merge, 3 big slice (lane kernel)
         u32 ins = 0;
@@ -396,7 +455,12 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
             if (s > kBigSlice) {
                 mode = 3;
             } else {
-                for (u32 q = 0; q < s; ++q) ins += a.uop[a.pidx ? a.pidx[lo + q] : lo + q] == kOpInsert;
+                for (u32 q = 0; q < s; ++q) {
+                    u64 kq;
+                    u8 oq;
+                    U(q, kq, oq);
+                    ins += oq == kOpInsert;
+                }
                 const u32 dels = s - ins;
                 if (!a.eager && ins == 0) mode = 1;
                 else if (!(nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn))) mode = 2;
@@ -418,107 +482,89 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
         __syncwarp();
         unsigned newvalid = valid;
         u32 missed = 0, added = 0, moves = 0, k = 0;
-        if (mode == 1) {
-            // commit_tombstones: one ordered pass over slots and deletes
-            u32 q = 0;
-            u64 uq = q < s ? a.uk[a.pidx ? a.pidx[lo] : lo] : 0;
-            for (unsigned i = 0; i < 16 && q < s; ++i) {
-                if (!((nonempty >> i) & 1u)) continue;
-                const u64 ki = rk[i];
-                while (q < s && uq < ki) {
-                    ++missed;
-                    ++q;
-                    if (q < s) uq = a.uk[a.pidx ? a.pidx[lo + q] : lo + q];
-                }
-                if (q < s && uq == ki) {
-                    if ((valid >> i) & 1u) {
-                        newvalid &= ~(1u << i);
-                        ++added;
-                    } else {
-                        ++missed;
-                    }
-                    ++q;
-                    if (q < s) uq = a.uk[a.pidx ? a.pidx[lo + q] : lo + q];
-                }
-            }
-            missed += s - q;
-        } else if (mode == 2) {
-            // pass A: compact survivors left, apply deletes (count missed)
-            u32 wpos = 0, q = 0;
+        if (mode == 1 || mode == 2) {
+            // pass A (both outcomes): walk Valid slots and the sorted slice;
+            // a delete matching a Valid key flips it (tombstones) or drops it
+            // (merge: survivors compact left); other deletes are missed
+            // (commit_tombstones / commit_in_place pass A).
+            u32 wpos = 0, q = 0, over = 0;
+            u64 uq = 0;
+            u8 oq = kOpDelete;
+            if (s > 0) U(0, uq, oq);
             for (unsigned i = 0; i < 16; ++i) {
                 if (!((valid >> i) & 1u)) continue;
                 const u64 ki = rk[i];
                 bool keep = true;
-                while (q < s) {
-                    const u32 pi = a.pidx ? a.pidx[lo + q] : lo + q;
-                    const u64 u = a.uk[pi];
-                    if (u > ki) break;
-                    if (a.uop[pi] == kOpDelete) {
-                        if (u == ki) keep = false;
+                while (q < s && uq <= ki) {
+                    if (oq == kOpDelete) {
+                        if (uq == ki) keep = false;
                         else ++missed;
+                    } else if (uq == ki) {
+                        ++over;  // insert overwrites this survivor
                     }
-                    ++q;
+                    if (++q < s) U(q, uq, oq);
                 }
-                if (!keep) continue;
-                if (wpos != i) {
-                    rk[wpos] = ki;
-                    rv[wpos] = rv[i];
-                    ++moves;
-                }
-                ++wpos;
-            }
-            for (; q < s; ++q) missed += a.uop[a.pidx ? a.pidx[lo + q] : lo + q] == kOpDelete;
-            const u32 n1 = wpos;
-            // merged size: survivors + inserts that do not overwrite one
-            k = n1;
-            {
-                u32 p = 0;
-                for (u32 j = 0; j < s; ++j) {
-                    const u32 pi = a.pidx ? a.pidx[lo + j] : lo + j;
-                    if (a.uop[pi] != kOpInsert) continue;
-                    const u64 u = a.uk[pi];
-                    while (p < n1 && rk[p] < u) ++p;
-                    if (p < n1 && rk[p] == u) ++p;
-                    else ++k;
-                }
-            }
-            // pass B: right-to-left onto the even targets (never clobbers an unread survivor)
-            int p = int(n1) - 1, uj = int(s) - 1, t = int(k) - 1;
-            newvalid = 0;
-            for (int x = 15; x >= 0; --x) {
-                const int target = t >= 0 ? int((u32(t) * 16u) / k) : 16;
-                if (x != target) {
-                    rk[x] = 0;
-                    rv[x] = 0;
+                if (!keep) {
+                    newvalid &= ~(1u << i);
+                    ++added;
                     continue;
                 }
-                u32 pj = 0;
-                while (uj >= 0) {
-                    pj = a.pidx ? a.pidx[lo + uj] : lo + uj;
-                    if (a.uop[pj] != kOpDelete) break;
-                    --uj;
+                if (mode == 2) {
+                    if (wpos != i) {
+                        rk[wpos] = ki;
+                        rv[wpos] = rv[i];
+                        ++moves;
+                    }
+                    ++wpos;
                 }
-                u64 ok_, ov_;
-                const u64 uk_ = uj >= 0 ? a.uk[pj] : 0;
-                if (uj < 0 || (p >= 0 && rk[p] > uk_)) {
-                    ok_ = rk[p];
-                    ov_ = rv[p];
-                    --p;
-                } else {
-                    if (p >= 0 && rk[p] == uk_) --p;
-                    ok_ = uk_;
-                    ov_ = a.uv[pj];
-                    --uj;
+            }
+            for (; q < s; ++q) {
+                U(q, uq, oq);
+                missed += oq == kOpDelete;
+            }
+            if (mode == 2) {
+                const u32 n1 = wpos;
+                k = n1 + ins - over;
+                // pass B: right-to-left onto the even targets floor(j*16/k)
+                // (never clobbers an unread survivor, segment_engine.hpp:196-225)
+                int p = int(n1) - 1, uj = int(s) - 1, t = int(k) - 1;
+                newvalid = 0;
+                for (int x = 15; x >= 0; --x) {
+                    const int target = t >= 0 ? int((u32(t) * 16u) / k) : 16;
+                    if (x != target) {
+                        rk[x] = 0;
+                        rv[x] = 0;
+                        continue;
+                    }
+                    u64 uk_ = 0;
+                    u8 uo_ = kOpDelete;
+                    while (uj >= 0) {
+                        U(u32(uj), uk_, uo_);
+                        if (uo_ != kOpDelete) break;
+                        --uj;
+                    }
+                    u64 ok_, ov_;
+                    if (uj < 0 || (p >= 0 && rk[p] > uk_)) {
+                        ok_ = rk[p];
+                        ov_ = rv[p];
+                        --p;
+                    } else {
+                        if (p >= 0 && rk[p] == uk_) --p;
+                        ok_ = uk_;
+                        ov_ = UVAL(u32(uj));
+                        --uj;
+                    }
+                    rk[x] = ok_;
+                    rv[x] = ov_;
+                    newvalid |= 1u << x;
+                    --t;
                 }
-                rk[x] = ok_;
-                rv[x] = ov_;
-                newvalid |= 1u << x;
-                --t;
             }
         }
         __syncwarp();
         // write back: states (own leaf), keys/values (merge groups, coalesced)
         if (mode == 1 || mode == 2) {
+            const unsigned tombs = mode == 1 ? (nonempty & ~newvalid) : 0u;
             uint4 ns;
             u32* o = reinterpret_cast<u32*>(&ns);
 #pragma unroll
@@ -527,9 +573,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
 #pragma unroll
                 for (int by = 0; by < 4; ++by) {
                     const int i = q * 4 + by;
-                    u32 x;
-                    if (mode == 1) x = ((newvalid >> i) & 1u) ? kValid : (((nonempty >> i) & 1u) ? kTombstone : kEmpty);
-                    else x = ((newvalid >> i) & 1u) ? kValid : kEmpty;
+                    const u32 x = ((newvalid >> i) & 1u) ? kValid : (((tombs >> i) & 1u) ? kTombstone : kEmpty);
                     word |= x << (8 * by);
                 }
                 o[q] = word;
@@ -622,35 +666,27 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
     const unsigned nleaves = m / leaf;
     const unsigned leafmask = (leaf >= 32) ? 0xffffffffu : ((1u << leaf) - 1u);
     const unsigned below = (1u << hl) - 1u;  // lanes of my group below me (hl < 32)
-    // big-slice mode: process only the groups the leaf kernel handed over
-    const ull nlist = a.biglist ? a.ctr->nbig : ngroups;
     Acc acc;
-    for (ull g0 = (ull(blockIdx.x) * kWarpTierWarps + w) * 32; g0 < nlist;
-         g0 += ull(gridDim.x) * kWarpTierWarps * 32) {
-        u32 t_lo = 0, t_hi = 0, t_seg = 0, t_gid = 0;
-        if (a.biglist) {
-            if (g0 + lane < nlist) {
-                t_gid = a.biglist[g0 + lane];
-                t_lo = a.gstart[t_gid];
-                t_hi = a.gstart[t_gid + 1];
-                t_seg = a.gseg[t_gid];
-            }
-        } else {
-            load_group_tile(a, g0, ngroups, lane, t_lo, t_hi, t_seg);
-            t_gid = u32(g0 + lane);
-        }
-        const unsigned tile_n = (nlist - g0) < 32 ? unsigned(nlist - g0) : 32u;
+    // a.tile groups per warp tile (<= 32): small rounds spread over more warps
+    const unsigned T = a.tile;
+    for (ull g0 = (ull(blockIdx.x) * kWarpTierWarps + w) * T; g0 < ngroups; g0 += ull(gridDim.x) * kWarpTierWarps * T) {
+        u32 t_lo = 0, t_hi = 0, t_seg = 0;
+        if (lane < T) load_group_tile(a, g0, ngroups, lane, t_lo, t_hi, t_seg);
+        const u32 t_gid = u32(g0 + lane);
+        const unsigned tile_n = (ngroups - g0) < T ? unsigned(ngroups - g0) : T;
         for (unsigned j = 0; j < tile_n; j += 32 / G) {
             const unsigned gi = j + (hb >> 4);
             const bool act = gi < tile_n;
             const u32 lo = __shfl_sync(FULL, t_lo, gi & 31u);
             const u32 hi = __shfl_sync(FULL, t_hi, gi & 31u);
             const u32 sv = __shfl_sync(FULL, t_seg, gi & 31u);
-            const u32 s = act ? hi - lo : 0u;
+            const u32 sfull = act ? hi - lo : 0u;
+            const bool big = sfull > kLaneBig;  // hub group: CTA kernel takes it
+            const u32 s = big ? 0u : sfull;
             const u64 b = u64(sv) * m;
             u8 stt = kEmpty;
             u64 key = 0, val = 0;
-            if (act && hl < m) {
+            if (act && !big && hl < m) {
                 stt = a.st[b + hl];
                 key = a.keys[b + hl];
                 val = a.vals[b + hl];
@@ -675,7 +711,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
             }
             const u32 dels = s - ins;
             int mode = 0;  // 0 defer, 1 tombstones, 2 merge
-            if (act) {
+            if (act && !big) {
                 if (!a.eager && ins == 0) mode = 1;
                 else if (!(nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn))) mode = 2;
             }
@@ -779,7 +815,12 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
                 }
             }
             const u32 gid_ = __shfl_sync(FULL, t_gid, gi & 31u);
-            if (hl == 0 && act) {
+            if (hl == 0 && act && big) {
+                a.gflag[gid_] = 0;
+                const ull slot = atomicAdd(&a.ctr->nbig, 1ull);
+                a.biglist[slot] = gid_;
+            }
+            if (hl == 0 && act && !big) {
                 a.gflag[gid_] = u8(mode);
                 if (mode == 1) {
                     const unsigned added = __popc(hits);
@@ -816,11 +857,14 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
 // by destination-driven placement.  Also the engine of the sequential ops.
 __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
     __shared__ ull s_w64[kCtaThreads / 32];
-    const ull ngroups = a.ctr->ngroups;
+    // biglist mode: only the hub groups the warp tiers handed over
+    const ull ngroups = a.biglist ? a.ctr->nbig : a.ctr->ngroups;
     Acc acc;
-    for (ull g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    for (ull gi = blockIdx.x; gi < ngroups; gi += gridDim.x) {
+        const ull g = a.biglist ? a.biglist[gi] : gi;
         const u32 lo = a.gstart[g], hi = a.gstart[g + 1];
         const u64 s = hi - lo;
+        if (threadIdx.x == 0) atomicMax(&a.ctr->max_slice, ull(s));
         const u64 seg = a.gseg[g];
         const u64 m = a.m;
         const u64 b = seg * m;
@@ -1261,31 +1305,39 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     uv.reserve(n);
     uop.reserve(n);
     ul.reserve(n);
+    gv_.reserve(n);
+    go_.reserve(n);
     {
+        // gather key/value/op into sorted order (parallel random reads), so the
+        // ordered compaction below streams contiguous arrays
+        u64* gk = sk_in.ptr;  // free after the sort
+        k_gather_sorted<<<grid_for(n, 256, 148 * 16), 256, 0, stream_>>>(sorted_ci, dk, dv, dop, n, gk, gv_.ptr,
+                                                                        go_.ptr);
+        GPMA_LAUNCH_CHECK();
+        ++launches;
+        const u64* sk = gk;
+        const u64* sv = gv_.ptr;
+        const u8* so = go_.ptr;
         u64* o_k = uk.ptr;
         u64* o_v = uv.ptr;
         u8* o_o = uop.ptr;
         Ctr* ctr = d_ctr;
         run_compact(
             stream_, ws, nullptr, n, n,
-            [=] __device__(ull i) {
-                const bool end = (i + 1 == n) || sorted_ck[i + 1] != sorted_ck[i];
-                return end && dop[sorted_ci[i]] != kOpSkip;
-            },
+            [=] __device__(ull i) { return ((i + 1 == n) || sk[i + 1] != sk[i]) && so[i] != kOpSkip; },
             [=] __device__(ull i, unsigned f, ull x) {
                 if (!f) return;
                 // last insert of the run wins (segment_engine.hpp:346-363)
                 u8 op = kOpDelete;
                 u64 val = 0;
-                for (long long j = (long long)i; j >= 0 && sorted_ck[j] == sorted_ck[i]; --j) {
-                    const u32 a = sorted_ci[j];
-                    if (dop[a] == kOpInsert) {
+                for (long long j = (long long)i; j >= 0 && sk[j] == sk[i]; --j) {
+                    if (so[j] == kOpInsert) {
                         op = kOpInsert;
-                        val = dv ? dv[a] : 0;
+                        val = sv[j];
                         break;
                     }
                 }
-                o_k[x] = dk[sorted_ci[i]];
+                o_k[x] = sk[i];
                 o_v[x] = val;
                 o_o[x] = op;
             },
@@ -1374,26 +1426,13 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             a.large = cfg.large_for(m);
             a.cap_gt_min = cap_ > 16;
             GPMA_CUDA(cudaEventRecord(ev_[5], stream_));
-            if (m == 16 && leaf_ == 16) {
-                biglist.reserve(npend + 1);
-                GPMA_CUDA(cudaMemsetAsync(&d_ctr->nbig, 0, sizeof(ull), stream_));
-                const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, 148 * 16);
-                k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
-                GPMA_LAUNCH_CHECK();
-                a.biglist = biglist.ptr;  // hub groups: lane-parallel ranking
-                const unsigned grid2 = grid_for((npend / kBigSlice + 31) / 32 + 1, kWarpTierWarps, 148 * 2);
-                k_commit_lanes<16><<<grid2, kWarpTierWarps * 32, 0, stream_>>>(a);
-            } else if (m <= 16) {
-                const unsigned grid = grid_for((npend + 31) / 32, kWarpTierWarps, 148 * 8);
-                k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
-            } else if (m <= 32) {
-                const unsigned grid = grid_for((npend + 31) / 32, kWarpTierWarps, 148 * 8);
-                k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
-            } else {
+            const bool cta_scratch = true;
+            if (cta_scratch) {
                 ensure_slot_scratch();
                 ik.reserve(n);
                 iv.reserve(n);
                 ir.reserve(n);
+                biglist.reserve(npend + 1);
                 a.ek = ek.ptr;
                 a.ev = ev.ptr;
                 a.es = es.ptr;
@@ -1403,6 +1442,29 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 a.ik = ik.ptr;
                 a.iv = iv.ptr;
                 a.ir = ir.ptr;
+                a.biglist = biglist.ptr;
+                GPMA_CUDA(cudaMemsetAsync(&d_ctr->nbig, 0, 2 * sizeof(ull), stream_));
+            }
+            if (m <= 32) {
+                // warp tiers; hub groups (large slices) are appended to biglist
+                if (m == 16 && leaf_ == 16) {
+                    const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, 148 * 16);
+                    k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
+                } else {
+                    // tile: enough warps to cover the SMs before packing 32 groups per warp
+                    unsigned T = unsigned((npend + 148 * 32 - 1) / (148 * 32));
+                    T = T < 1 ? 1 : (T > 32 ? 32 : T);
+                    if (m <= 16) T = (T + 1) & ~1u;  // half-warp tier handles pairs
+                    a.tile = T;
+                    const unsigned grid = grid_for((npend + T - 1) / T, kWarpTierWarps, 148 * 8);
+                    if (m <= 16) k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+                    else k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+                }
+                GPMA_LAUNCH_CHECK();
+                // CTA kernel over the hub groups only (grid bounded by npend / kBigSlice)
+                k_commit_cta<<<grid_for(npend / kBigSlice + 1, 1, 148 * 2), kCtaThreads, 0, stream_>>>(a);
+            } else {
+                a.biglist = nullptr;
                 const unsigned grid = grid_for(npend, 1, 148 * 4);
                 k_commit_cta<<<grid, kCtaThreads, 0, stream_>>>(a);
             }
@@ -1447,6 +1509,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             float ms = 0.f;
             cudaEventElapsedTime(&ms, ev_[5], ev_[6]);
             seg_ms += ms;
+            if (level < 16) {
+                timing.level_ms[level] += ms;
+                timing.level_groups[level] += h_ctr->ngroups;
+                timing.level_big[level] += h_ctr->nbig;
+                timing.level_max_slice[level] = std::max<u64>(timing.level_max_slice[level], h_ctr->max_slice);
+            }
             st.rounds++;
             st.segments_per_level[level] += h_ctr->committed;
             ntouched = h_ctr->ntouched_next;
