@@ -66,3 +66,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+
+
+def build_cpp_tests() -> str:
+    """C++ drop-in test (tests/cpp/test_dropin.cpp) against include/pmagraph/*.hpp,
+    linked to the in-tree library (rpath $ORIGIN/../../paper_1709_05061_b200)."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    out = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    if os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(src), os.path.getmtime(OUT)) and \
+            all(os.path.getmtime(h) < os.path.getmtime(out) for h in glob.glob(os.path.join(ROOT, "include", "pmagraph", "*.hpp"))):
+        return out
+    subprocess.check_call(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", out,
+                           "-L" + HERE, "-lpmagraph_cuda", "-Wl,-rpath,$ORIGIN/../../paper_1709_05061_b200"])
+    return out
