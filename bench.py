@@ -191,6 +191,7 @@ def run_ours(args):
     updates = 0
     seg_ms = 0.0
     merge_slots = 0
+    commit_bytes = 0
     launches = 0
     rounds = 0
     stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
@@ -204,6 +205,7 @@ def run_ours(args):
         updates += st.batch_size
         seg_ms += st.segment_phase_ns / 1e6
         merge_slots += tm.merge_slots
+        commit_bytes += tm.commit_bytes
         launches += tm.kernel_launches
         rounds += st.rounds
         for k in stage:
@@ -271,7 +273,11 @@ def run_ours(args):
 
     # ---- roofline of the dominant kernel (warp-tier commit: decide+merge+scatter) ----
     peak, peak_kind = measured_peak()
-    achieved = (BYTES_PER_MERGE_SLOT * merge_slots / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
+    # algorithmic bytes of the commit kernels, counted per examined group by the
+    # kernels themselves (alg_bytes in csrc/pma.cu): slice + state
+    # and key reads of every examined segment, value reads + key/value/state
+    # writes of merged segments, state writes of tombstone commits
+    achieved = (commit_bytes / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -281,7 +287,8 @@ def run_ours(args):
     roofline = {"bound": "hbm", "kernel": "commit tier kernels (k_commit_leaf + k_commit_lanes: decide + merge + even re-dispatch + fused header/row-offset refresh)",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "algorithmic_bytes_per_step": BYTES_PER_MERGE_SLOT * merge_slots // K,
+                "algorithmic_bytes_per_step": commit_bytes // K,
+                "scatter_bytes_per_step": BYTES_PER_MERGE_SLOT * merge_slots // K,
                 "kernel_ms_per_step": seg_ms / K, "step_ms": ms / K,
                 "stage_ms_per_step": {k: v / K for k, v in stage.items()},
                 "commit_ms_per_level": [round(x / K, 4) for x in level_ms if x > 0],

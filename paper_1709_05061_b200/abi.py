@@ -86,6 +86,7 @@ class pma_timing(C.Structure):
         ("level_groups", C.c_uint64 * 16),
         ("level_big", C.c_uint64 * 16),
         ("level_max_slice", C.c_uint64 * 16),
+        ("commit_bytes", C.c_uint64),
     ]
 
 

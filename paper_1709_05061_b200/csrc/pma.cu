@@ -261,7 +261,17 @@ struct CommitArgs {
 struct Acc {
     ull committed = 0, missed = 0, tomb = 0, writes = 0, merge = 0;
     long long vd = 0, td = 0, ed = 0;
+    ull bytes = 0;  // algorithmic HBM bytes of the commit (alg_bytes)
 };
+
+// Algorithmic bytes of one examined group of an m-slot segment with an
+// s-update slice: descriptor (gstart, gseg, gflag) + slice
+// (key, value, op) + the segment's states and keys (decision and matching),
+// plus 1 B/slot of state writes for tombstone commits or, for merges, the
+// values read and keys/values/states written back (25 B/slot).
+__device__ __forceinline__ ull alg_bytes(ull m, ull s, int mode) {
+    return 9ull + 17ull * s + 9ull * m + (mode == 1 ? m : (mode == 2 ? 25ull * m : 0ull));
+}
 
 __device__ __forceinline__ void flush_acc(const Acc& a, Ctr* ctr) {
     // called by one thread per CTA with CTA totals
@@ -273,11 +283,12 @@ __device__ __forceinline__ void flush_acc(const Acc& a, Ctr* ctr) {
     if (a.vd) atomicAdd(reinterpret_cast<ull*>(&ctr->valid_delta), ull(a.vd));
     if (a.td) atomicAdd(reinterpret_cast<ull*>(&ctr->tomb_delta), ull(a.td));
     if (a.ed) atomicAdd(reinterpret_cast<ull*>(&ctr->empty_delta), ull(a.ed));
+    if (a.bytes) atomicAdd(&ctr->commit_bytes, a.bytes);
 }
 
 __device__ void block_flush(Acc acc, Ctr* ctr) {
-    __shared__ ull s_acc[8];
-    if (threadIdx.x < 8) s_acc[threadIdx.x] = 0;
+    __shared__ ull s_acc[9];
+    if (threadIdx.x < 9) s_acc[threadIdx.x] = 0;
     __syncthreads();
     if ((threadIdx.x & 31) == 0) {
         if (acc.committed) atomicAdd(&s_acc[0], acc.committed);
@@ -288,6 +299,7 @@ __device__ void block_flush(Acc acc, Ctr* ctr) {
         if (acc.vd) atomicAdd(&s_acc[5], ull(acc.vd));
         if (acc.td) atomicAdd(&s_acc[6], ull(acc.td));
         if (acc.ed) atomicAdd(&s_acc[7], ull(acc.ed));
+        if (acc.bytes) atomicAdd(&s_acc[8], acc.bytes);
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -300,6 +312,7 @@ __device__ void block_flush(Acc acc, Ctr* ctr) {
         t.vd = (long long)s_acc[5];
         t.td = (long long)s_acc[6];
         t.ed = (long long)s_acc[7];
+        t.bytes = s_acc[8];
         flush_acc(t, ctr);
     }
 }
@@ -327,6 +340,7 @@ __device__ __forceinline__ void warp_reduce_acc(Acc& acc) {
         acc.vd += __shfl_xor_sync(FULL, acc.vd, d);
         acc.td += __shfl_xor_sync(FULL, acc.td, d);
         acc.ed += __shfl_xor_sync(FULL, acc.ed, d);
+        acc.bytes += __shfl_xor_sync(FULL, acc.bytes, d);
     }
 }
 
@@ -345,29 +359,77 @@ __device__ __forceinline__ void load_group_tile(const CommitArgs& a, ull g0, ull
 
 // --- leaf tier: thread per group, 16-slot segments (>= 99.5% of commits).
 // The warp stages the 32 leaves of its group tile in shared memory with
-// coalesced 16-byte loads (8 lanes per 128-byte key/value line), each thread
-// then runs the reference's in-place merge on its own row — pass A compacts
-// survivors left and applies deletes, pass B merges right-to-left onto the
-// even targets floor(j*m/k) (commit_in_place, segment_engine.hpp:147-230;
-// identical output to place_evenly) — and the warp stores the rewritten
-// leaves back coalesced.  O(16 + |slice|) thread work per group, one staged
-// round trip per 32 groups.  Groups with more than kBigSlice updates (RMAT hub
-// rows) are handed to the lane-parallel kernel through `biglist`.
+// coalesced 16-byte loads (8 lanes per 128-byte key/value line); each thread
+// then commits its own leaf with branch-light bit arithmetic instead of a
+// serial merge walk:
+//   * every update of the slice is ranked against the 16 slot keys (held in
+//     registers) by 16 unrolled 64-bit compares -> lt mask; the only possible
+//     match is the first non-Empty slot not below it (non-Empty keys of a leaf
+//     are strictly increasing);
+//   * deletes hit -> del mask, inserts hit -> overwrite mask; an insert's
+//     final rank is popc(kept & lt) + #inserts before it (updates are sorted,
+//     so every earlier drop/overwrite below it is already known), and every
+//     slot at or above it gets +1 in a nibble-packed "inserts below" counter;
+//   * survivor i lands on floor(16 j_i / k) with j_i = popc(kept below i) +
+//     nibble_i (commit_in_place / place_evenly give the same layout,
+//     segment_engine.hpp:147-230, pma.hpp:440-467): the division is a
+//     multiply by ceil(2^16 / k), exact for 16 j <= 240;
+//   * the row is permuted in place: survivors moving right in decreasing
+//     source order, then survivors moving left in increasing order (the
+//     placement is monotone, so neither pass reads a clobbered slot), vacated
+//     slots cleared, inserts written last.
+// Leaf header, row offsets of moved guards and the state bytes are refreshed
+// in the same pass and the warp stores the rewritten leaves back coalesced.
+// Groups with more than kBigSlice updates (RMAT hub rows) are handed to the
+// CTA kernel through `biglist`.
 constexpr int kLeafWarps = 4;
 constexpr int kRow = 17;        // padded u64 row (conflict-free column access)
 constexpr u32 kBigSlice = 32;   // leaf kernel: larger slices go to the CTA kernel
 constexpr u32 kLaneBig = 64;    // lane kernels: larger slices go to the CTA kernel
-constexpr u32 kStage = 128;     // updates of a 32-group tile staged in smem
+constexpr u32 kStage = 64;      // updates of a 32-group tile staged in smem (overflow read from HBM)
 
-__global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
+// bit i of m (i < 16) -> bit 4i
+__device__ __forceinline__ u64 spread_nibbles(u32 m) {
+    u64 x = m & 0xffffu;
+    x = (x | (x << 24)) & 0x000000FF000000FFull;
+    x = (x | (x << 12)) & 0x000F000F000F000Full;
+    x = (x | (x << 6)) & 0x0303030303030303ull;
+    x = (x | (x << 3)) & 0x1111111111111111ull;
+    return x;
+}
+
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(unsigned(__cvta_generic_to_shared(smem))),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(unsigned(__cvta_generic_to_shared(smem))),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(unsigned(__cvta_generic_to_shared(smem))),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Only launched at level 0 (m == leaf == 16), where the pending list is the
+// identity (a.pidx == nullptr): a tile's updates are one contiguous range.
+// Staging is asynchronous (cp.async, no registers held): phase 1 brings the
+// tile's states, keys and update slice in one round trip; the decision then
+// issues phase 2 (values of the merge groups only), which overlaps the
+// ranking of the slices.
+__global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a) {
     __shared__ u64 s_k[kLeafWarps][32 * kRow];
     __shared__ u64 s_v[kLeafWarps][32 * kRow];
+    __shared__ uint4 s_st[kLeafWarps][32];
     __shared__ u64 s_uk[kLeafWarps][kStage];
     __shared__ u64 s_uv[kLeafWarps][kStage];
-    __shared__ u8 s_uo[kLeafWarps][kStage];
+    __shared__ u32 s_uo[kLeafWarps][kStage / 4 + 2];
+    __shared__ u64 s_b[kLeafWarps][32];  // slot base of each group of the tile
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     u64* rk = &s_k[w][lane * kRow];
     u64* rv = &s_v[w][lane * kRow];
+    const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
     const ull ngroups = a.ctr->ngroups;
     const ull gstride = ull(gridDim.x) * kLeafWarps * 32;
     ull g0 = (ull(blockIdx.x) * kLeafWarps + w) * 32;
@@ -385,6 +447,28 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
         const u32 lo = n_lo, hi = n_hi;
         const u64 b = u64(n_seg) * 16;
         const unsigned tile_n = (ngroups - g0) < 32 ? unsigned(ngroups - g0) : 32u;
+        const u32 tlo = __shfl_sync(FULL, lo, 0);
+        const u32 thi = __shfl_sync(FULL, hi, tile_n - 1);
+        s_b[w][lane] = b;
+        __syncwarp();
+        // ---- phase 1: states, keys, update slice of the tile
+        if (act) cp_async16(&s_st[w][lane], a.st + b);
+        const u32 staged = (thi - tlo) < kStage ? (thi - tlo) : kStage;
+        for (u32 i = lane; i < staged; i += 32) {
+            cp_async8(&s_uk[w][i], a.uk + tlo + i);
+            cp_async8(&s_uv[w][i], a.uv + tlo + i);
+        }
+        {
+            const u32 w0 = tlo >> 2, w1 = (tlo + staged + 3) >> 2;
+            for (u32 i = lane; i < w1 - w0; i += 32)
+                cp_async4(&s_uo[w][i], reinterpret_cast<const u32*>(a.uop) + w0 + i);
+        }
+#pragma unroll
+        for (int it = 0; it < 16; ++it) {  // half a warp per 128-byte key line
+            const unsigned row = it * 2 + (lane >> 4), slot = lane & 15u;
+            if (row < tile_n) cp_async8(&s_k[w][row * kRow + slot], a.keys + s_b[w][row] + slot);
+        }
+        // descriptors of the next tile while the copies fly
         {
             const ull gn = gl + gstride;
             n_lo = n_hi = n_seg = 0;
@@ -394,49 +478,29 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
                 n_seg = a.gseg[gn];
             }
         }
-        uint4 sv = make_uint4(0, 0, 0, 0);
-        if (act) sv = *reinterpret_cast<const uint4*>(a.st + b);
-        // stage the tile's updates (contiguous in pending order)
-        const u32 tlo = __shfl_sync(FULL, lo, 0);
-        const u32 thi = __shfl_sync(FULL, hi, tile_n - 1);
-        const u32 staged = (thi - tlo) < kStage ? (thi - tlo) : kStage;
-        for (u32 i = lane; i < staged; i += 32) {
-            const u32 pi = a.pidx ? a.pidx[tlo + i] : tlo + i;
-            s_uk[w][i] = a.uk[pi];
-            s_uv[w][i] = a.uv[pi];
-            s_uo[w][i] = a.uop[pi];
-        }
+        cp_async_wait_all();
+        __syncwarp();
         const u32 s = hi - lo;
         const u32 soff = lo - tlo;
+        const u32 obase = tlo & 3u;
         auto U = [&](u32 q, u64& key, u8& op) {
             const u32 i = soff + q;
             if (i < staged) {
                 key = s_uk[w][i];
-                op = s_uo[w][i];
+                op = s_op[obase + i];
             } else {
-                const u32 pi = a.pidx ? a.pidx[lo + q] : lo + q;
-                key = a.uk[pi];
-                op = a.uop[pi];
+                key = a.uk[lo + q];
+                op = a.uop[lo + q];
             }
         };
         auto UVAL = [&](u32 q) -> u64 {
             const u32 i = soff + q;
-            return i < staged ? s_uv[w][i] : a.uv[a.pidx ? a.pidx[lo + q] : lo + q];
+            return i < staged ? s_uv[w][i] : a.uv[lo + q];
         };
-        // keys of the tile: 8 lanes per leaf line, 4 leaves per instruction
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-            const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
-            const u64 gb = __shfl_sync(FULL, b, grp);
-            if (grp < tile_n) {
-                const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(a.keys + gb + 2 * part);
-                s_k[w][grp * kRow + 2 * part] = kk.x;
-                s_k[w][grp * kRow + 2 * part + 1] = kk.y;
-            }
-        }
         // state masks (bit i = slot i)
         unsigned valid = 0, nonempty = 0;
-        {
+        if (act) {
+            const uint4 sv = s_st[w][lane];
             const u32 words[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -447,18 +511,16 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
                 nonempty |= ((ne * 0x01020408u) >> 24 & 0xfu) << (4 * q);
             }
         }
-        __syncwarp();
         const unsigned nv = __popc(valid);
-        int mode = 0;  // 0 defer, 1 tombstones, 2 merge, 3 big slice (lane kernel)
+        int mode = 0;  // 0 defer, 1 tombstones, 2 merge, 3 big slice (CTA kernel)
         u32 ins = 0;
         if (act) {
             if (s > kBigSlice) {
                 mode = 3;
             } else {
                 for (u32 q = 0; q < s; ++q) {
-                    u64 kq;
-                    u8 oq;
-                    U(q, kq, oq);
+                    const u32 i = soff + q;
+                    const u8 oq = i < staged ? s_op[obase + i] : a.uop[lo + q];
                     ins += oq == kOpInsert;
                 }
                 const u32 dels = s - ins;
@@ -466,105 +528,118 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
                 else if (!(nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn))) mode = 2;
             }
         }
+        // ---- phase 2: values of the merge groups (overlaps the ranking)
         const unsigned mergemask = __ballot_sync(FULL, mode == 2);
         if (mergemask) {
 #pragma unroll
-            for (int it = 0; it < 8; ++it) {
-                const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
-                const u64 gb = __shfl_sync(FULL, b, grp);
-                if ((mergemask >> grp) & 1u) {
-                    const ulonglong2 vv = *reinterpret_cast<const ulonglong2*>(a.vals + gb + 2 * part);
-                    s_v[w][grp * kRow + 2 * part] = vv.x;
-                    s_v[w][grp * kRow + 2 * part + 1] = vv.y;
+            for (int it = 0; it < 16; ++it) {
+                const unsigned row = it * 2 + (lane >> 4), slot = lane & 15u;
+                if ((mergemask >> row) & 1u) cp_async8(&s_v[w][row * kRow + slot], a.vals + s_b[w][row] + slot);
+            }
+        }
+        unsigned newvalid = valid, tombs = 0;
+        u32 missed = 0, del_hit = 0, moves = 0, k = 0;
+        u32 ovr = 0, nins = 0, guards = 0;
+        u64 cnt = 0, insj = 0;
+        if (mode == 1 || mode == 2) {
+            // ---- rank the slice against the leaf (commit_tombstones /
+            // merge_entries, segment_engine.hpp:119-137, 285-310)
+            u64 K[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) K[i] = rk[i];
+            if (mode == 2 && a.ro) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) guards |= (u32(K[i]) == u32(kGuardDst) ? 1u : 0u) << i;
+            }
+            for (u32 q = 0; q < s; ++q) {
+                u64 u;
+                u8 op;
+                U(q, u, op);
+                u32 lt = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) lt |= (K[i] < u ? 1u : 0u) << i;
+                const u32 cm = nonempty & ~lt;
+                const int c = __ffs(cm) - 1;  // the only slot that can hold u
+                const bool hit = cm != 0 && ((valid >> c) & 1u) && rk[c] == u;
+                if (op == kOpDelete) {
+                    if (hit) del_hit |= 1u << c;
+                    else ++missed;
+                } else {
+                    if (hit) ovr |= 1u << c;
+                    const u32 j = __popc(valid & ~(del_hit | ovr) & lt) + nins;
+                    insj |= u64(j) << (4 * nins);
+                    cnt += spread_nibbles(~lt);
+                    ++nins;
                 }
             }
         }
+        cp_async_wait_all();
         __syncwarp();
-        unsigned newvalid = valid;
-        u32 missed = 0, added = 0, moves = 0, k = 0;
-        if (mode == 1 || mode == 2) {
-            // pass A (both outcomes): walk Valid slots and the sorted slice;
-            // a delete matching a Valid key flips it (tombstones) or drops it
-            // (merge: survivors compact left); other deletes are missed
-            // (commit_tombstones / commit_in_place pass A).
-            u32 wpos = 0, q = 0, over = 0;
-            u64 uq = 0;
-            u8 oq = kOpDelete;
-            if (s > 0) U(0, uq, oq);
-            for (unsigned i = 0; i < 16; ++i) {
-                if (!((valid >> i) & 1u)) continue;
-                const u64 ki = rk[i];
-                bool keep = true;
-                while (q < s && uq <= ki) {
-                    if (oq == kOpDelete) {
-                        if (uq == ki) keep = false;
-                        else ++missed;
-                    } else if (uq == ki) {
-                        ++over;  // insert overwrites this survivor
-                    }
-                    if (++q < s) U(q, uq, oq);
-                }
-                if (!keep) {
-                    newvalid &= ~(1u << i);
-                    ++added;
-                    continue;
-                }
-                if (mode == 2) {
-                    if (wpos != i) {
-                        rk[wpos] = ki;
-                        rv[wpos] = rv[i];
-                        ++moves;
-                    }
-                    ++wpos;
+        if (mode == 1) {
+            newvalid = valid & ~del_hit;
+            tombs = nonempty & ~newvalid;
+        } else if (mode == 2) {
+            const u32 keepa = valid & ~del_hit;
+            const u32 keepf = keepa & ~ovr;
+            k = __popc(keepf) + nins;
+            const int tz = __ffs(~keepa) - 1;  // <= 16
+            moves = __popc(keepa & (0xffffffffu << tz));
+            const u32 mk = k ? (65536u + k - 1) / k : 0u;
+            // destinations of the survivors (nibble-packed)
+            u64 dst = 0;
+            u32 right = 0, out = 0;
+            for (u32 m = keepf; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                const u32 j = __popc(keepf & ((1u << i) - 1u)) + u32((cnt >> (4 * i)) & 0xfu);
+                const u32 x = (j * 16u * mk) >> 16;
+                dst |= u64(x) << (4 * i);
+                out |= 1u << x;
+                if (x > u32(i)) right |= 1u << i;
+            }
+            for (u32 m = right; m; m &= ~(1u << (31 - __clz(m)))) {
+                const int i = 31 - __clz(m);
+                const u32 x = u32(dst >> (4 * i)) & 0xfu;
+                rk[x] = rk[i];
+                rv[x] = rv[i];
+            }
+            for (u32 m = keepf & ~right; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                const u32 x = u32(dst >> (4 * i)) & 0xfu;
+                if (x != u32(i)) {
+                    rk[x] = rk[i];
+                    rv[x] = rv[i];
                 }
             }
-            for (; q < s; ++q) {
-                U(q, uq, oq);
-                missed += oq == kOpDelete;
+            for (u32 m = nonempty & ~out; m; m &= m - 1) {
+                const int x = __ffs(m) - 1;
+                rk[x] = 0;
+                rv[x] = 0;
             }
-            if (mode == 2) {
-                const u32 n1 = wpos;
-                k = n1 + ins - over;
-                // pass B: right-to-left onto the even targets floor(j*16/k)
-                // (never clobbers an unread survivor, segment_engine.hpp:196-225)
-                int p = int(n1) - 1, uj = int(s) - 1, t = int(k) - 1;
-                newvalid = 0;
-                for (int x = 15; x >= 0; --x) {
-                    const int target = t >= 0 ? int((u32(t) * 16u) / k) : 16;
-                    if (x != target) {
-                        rk[x] = 0;
-                        rv[x] = 0;
-                        continue;
-                    }
-                    u64 uk_ = 0;
-                    u8 uo_ = kOpDelete;
-                    while (uj >= 0) {
-                        U(u32(uj), uk_, uo_);
-                        if (uo_ != kOpDelete) break;
-                        --uj;
-                    }
-                    u64 ok_, ov_;
-                    if (uj < 0 || (p >= 0 && rk[p] > uk_)) {
-                        ok_ = rk[p];
-                        ov_ = rv[p];
-                        --p;
-                    } else {
-                        if (p >= 0 && rk[p] == uk_) --p;
-                        ok_ = uk_;
-                        ov_ = UVAL(u32(uj));
-                        --uj;
-                    }
-                    rk[x] = ok_;
-                    rv[x] = ov_;
-                    newvalid |= 1u << x;
-                    --t;
-                }
+            // inserts, in key order
+            u32 nth = 0;
+            for (u32 q = 0; nth < nins; ++q) {
+                u64 u;
+                u8 op;
+                U(q, u, op);
+                if (op == kOpDelete) continue;
+                const u32 j = u32(insj >> (4 * nth)) & 0xfu;
+                const u32 x = (j * 16u * mk) >> 16;
+                rk[x] = u;
+                rv[x] = UVAL(q);
+                out |= 1u << x;
+                ++nth;
+            }
+            newvalid = out;
+            // row offsets: every guard of the rewritten leaf (graph.hpp:176)
+            for (u32 m = keepf & guards; m; m &= m - 1) {
+                const int i = __ffs(m) - 1;
+                const u32 x = u32(dst >> (4 * i)) & 0xfu;
+                a.ro[src_of(rk[x]) + 1] = b + x + 1;
             }
         }
         __syncwarp();
         // write back: states (own leaf), keys/values (merge groups, coalesced)
         if (mode == 1 || mode == 2) {
-            const unsigned tombs = mode == 1 ? (nonempty & ~newvalid) : 0u;
             uint4 ns;
             u32* o = reinterpret_cast<u32*>(&ns);
 #pragma unroll
@@ -584,8 +659,8 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
 #pragma unroll
             for (int it = 0; it < 8; ++it) {
                 const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
-                const u64 gb = __shfl_sync(FULL, b, grp);
                 if ((mergemask >> grp) & 1u) {
+                    const u64 gb = s_b[w][grp];
                     *reinterpret_cast<ulonglong2*>(a.keys + gb + 2 * part) =
                         make_ulonglong2(s_k[w][grp * kRow + 2 * part], s_k[w][grp * kRow + 2 * part + 1]);
                     *reinterpret_cast<ulonglong2*>(a.vals + gb + 2 * part) =
@@ -600,22 +675,15 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
                 a.rlist[2 * slot] = b;
                 a.rlist[2 * slot + 1] = b + 16;
             }
-            if (a.ro) {
-                for (unsigned x = 0; x < 16; ++x) {
-                    if ((newvalid >> x) & 1u) {
-                        const u64 kx = rk[x];
-                        if (is_guard(kx)) a.ro[src_of(kx) + 1] = b + x + 1;  // graph.hpp:176
-                    }
-                }
-            }
         }
-        __syncwarp();
         if (act) {
             a.gflag[gl] = u8(mode == 3 ? 0 : mode);
+            if (mode != 3) acc.bytes += alg_bytes(16, s, mode);
             if (mode == 3) {
                 const ull slot = atomicAdd(&a.ctr->nbig, 1ull);
                 a.biglist[slot] = u32(gl);
             } else if (mode == 1) {
+                const u32 added = __popc(del_hit);
                 acc.committed++;
                 acc.tomb += added;
                 acc.missed += missed;
@@ -632,6 +700,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32) k_commit_leaf(CommitArgs a) {
                 acc.ed += (k == 0 ? 1 : 0) - (nonempty == 0 ? 1 : 0);
             }
         }
+        __syncwarp();  // smem of this tile is reused by the next
     }
     warp_reduce_acc(acc);
     if ((threadIdx.x & 31u) != 0) acc = Acc{};
@@ -822,6 +891,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
             }
             if (hl == 0 && act && !big) {
                 a.gflag[gid_] = u8(mode);
+                acc.bytes += alg_bytes(m, s, mode);
                 if (mode == 1) {
                     const unsigned added = __popc(hits);
                     acc.committed++;
@@ -941,6 +1011,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
         }
         if (threadIdx.x == 0) {
             a.gflag[g] = flag;
+            acc.bytes += alg_bytes(m, s, flag);
             if (flag) acc.committed++;
         }
         __syncthreads();
@@ -1303,7 +1374,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     // ---- 2. resolve duplicates: run ends -> unique updates ----
     uk.reserve(n);
     uv.reserve(n);
-    uop.reserve(n);
+    uop.reserve(n + 8);  // k_commit_leaf stages ops as aligned 4-byte words
     ul.reserve(n);
     gv_.reserve(n);
     go_.reserve(n);
@@ -1447,7 +1518,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             }
             if (m <= 32) {
                 // warp tiers; hub groups (large slices) are appended to biglist
-                if (m == 16 && leaf_ == 16) {
+                if (m == 16 && leaf_ == 16 && pcur == nullptr) {  // level 0: identity pending list
                     const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, 148 * 16);
                     k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
                 } else {
@@ -1688,6 +1759,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     st.deletes_missed += h_ctr->missed;
     st.tombstones_added += h_ctr->tomb_added;
     timing.merge_slots = h_ctr->merge_slots;
+    timing.commit_bytes = h_ctr->commit_bytes;
     timing.tombstone_flips = st.tombstones_added;
     event(3);
     // ---- 5. refresh leaf headers / row offsets ----

@@ -50,7 +50,8 @@ struct Ctr {
     long long empty_delta;
     ull nbig;
     ull max_slice;
-    ull pad[4];
+    ull commit_bytes;
+    ull pad[3];
 };
 
 struct EngineCfg {
