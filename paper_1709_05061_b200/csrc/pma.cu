@@ -418,17 +418,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // tile's states, keys and update slice in one round trip; the decision then
 // issues phase 2 (values of the merge groups only), which overlaps the
 // ranking of the slices.
+constexpr int kRowB = 18;  // u64 per staged row: 16 slots + 16 B pad (16-B aligned, conflict-free 16-B reads)
+
 __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a) {
-    __shared__ u64 s_k[kLeafWarps][32 * kRow];
-    __shared__ u64 s_v[kLeafWarps][32 * kRow];
-    __shared__ uint4 s_st[kLeafWarps][32];
+    __shared__ __align__(16) u64 s_k[kLeafWarps][32 * kRowB];
+    __shared__ __align__(16) u64 s_v[kLeafWarps][32 * kRowB];
     __shared__ u64 s_uk[kLeafWarps][kStage];
     __shared__ u64 s_uv[kLeafWarps][kStage];
     __shared__ u32 s_uo[kLeafWarps][kStage / 4 + 2];
     __shared__ u64 s_b[kLeafWarps][32];  // slot base of each group of the tile
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    u64* rk = &s_k[w][lane * kRow];
-    u64* rv = &s_v[w][lane * kRow];
+    u64* rk = &s_k[w][lane * kRowB];
+    u64* rv = &s_v[w][lane * kRowB];
     const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
     const ull ngroups = a.ctr->ngroups;
     const ull gstride = ull(gridDim.x) * kLeafWarps * 32;
@@ -452,7 +453,8 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
         s_b[w][lane] = b;
         __syncwarp();
         // ---- phase 1: states, keys, update slice of the tile
-        if (act) cp_async16(&s_st[w][lane], a.st + b);
+        uint4 sv = make_uint4(0, 0, 0, 0);
+        if (act) sv = *reinterpret_cast<const uint4*>(a.st + b);  // in flight with the copies
         const u32 staged = (thi - tlo) < kStage ? (thi - tlo) : kStage;
         for (u32 i = lane; i < staged; i += 32) {
             cp_async8(&s_uk[w][i], a.uk + tlo + i);
@@ -464,9 +466,9 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
                 cp_async4(&s_uo[w][i], reinterpret_cast<const u32*>(a.uop) + w0 + i);
         }
 #pragma unroll
-        for (int it = 0; it < 16; ++it) {  // half a warp per 128-byte key line
-            const unsigned row = it * 2 + (lane >> 4), slot = lane & 15u;
-            if (row < tile_n) cp_async8(&s_k[w][row * kRow + slot], a.keys + s_b[w][row] + slot);
+        for (int it = 0; it < 8; ++it) {  // 8 lanes per 128-byte key line
+            const unsigned row = it * 4 + (lane >> 3), part = lane & 7u;
+            if (row < tile_n) cp_async16(&s_k[w][row * kRowB + 2 * part], a.keys + s_b[w][row] + 2 * part);
         }
         // descriptors of the next tile while the copies fly
         {
@@ -500,7 +502,6 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
         // state masks (bit i = slot i)
         unsigned valid = 0, nonempty = 0;
         if (act) {
-            const uint4 sv = s_st[w][lane];
             const u32 words[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -532,9 +533,10 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
         const unsigned mergemask = __ballot_sync(FULL, mode == 2);
         if (mergemask) {
 #pragma unroll
-            for (int it = 0; it < 16; ++it) {
-                const unsigned row = it * 2 + (lane >> 4), slot = lane & 15u;
-                if ((mergemask >> row) & 1u) cp_async8(&s_v[w][row * kRow + slot], a.vals + s_b[w][row] + slot);
+            for (int it = 0; it < 8; ++it) {
+                const unsigned row = it * 4 + (lane >> 3), part = lane & 7u;
+                if ((mergemask >> row) & 1u)
+                    cp_async16(&s_v[w][row * kRowB + 2 * part], a.vals + s_b[w][row] + 2 * part);
             }
         }
         unsigned newvalid = valid, tombs = 0;
@@ -546,7 +548,11 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             // merge_entries, segment_engine.hpp:119-137, 285-310)
             u64 K[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) K[i] = rk[i];
+            for (int i = 0; i < 16; i += 2) {  // 16-B row reads: conflict-free per quarter warp
+                const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(rk + i);
+                K[i] = kk.x;
+                K[i + 1] = kk.y;
+            }
             if (mode == 2 && a.ro) {
 #pragma unroll
                 for (int i = 0; i < 16; ++i) guards |= (u32(K[i]) == u32(kGuardDst) ? 1u : 0u) << i;
@@ -662,9 +668,9 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
                 if ((mergemask >> grp) & 1u) {
                     const u64 gb = s_b[w][grp];
                     *reinterpret_cast<ulonglong2*>(a.keys + gb + 2 * part) =
-                        make_ulonglong2(s_k[w][grp * kRow + 2 * part], s_k[w][grp * kRow + 2 * part + 1]);
+                        *reinterpret_cast<const ulonglong2*>(&s_k[w][grp * kRowB + 2 * part]);
                     *reinterpret_cast<ulonglong2*>(a.vals + gb + 2 * part) =
-                        make_ulonglong2(s_v[w][grp * kRow + 2 * part], s_v[w][grp * kRow + 2 * part + 1]);
+                        *reinterpret_cast<const ulonglong2*>(&s_v[w][grp * kRowB + 2 * part]);
                 }
             }
         }
