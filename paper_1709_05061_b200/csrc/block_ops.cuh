@@ -6,7 +6,7 @@
 
 namespace gpma {
 
-constexpr unsigned FULL = 0xffffffffu;
+
 
 // Exclusive scan of one u32 per thread across the CTA.  All threads call it.
 // s_w needs blockDim.x/32 entries.

@@ -25,6 +25,7 @@ constexpr u8 kOpDelete = 1;
 constexpr u8 kOpSkip = 2;  // guard deletes dropped by apply_batch (graph.hpp:141-147)
 constexpr u64 kGuardDst = 0xFFFFFFFFull;
 constexpr int kNumSMs = 148;
+constexpr unsigned FULL = 0xffffffffu;
 
 // Error carrying the reference exception class as a PMA_* code.
 struct ApiError : std::runtime_error {

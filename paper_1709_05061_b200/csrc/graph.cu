@@ -22,30 +22,6 @@ __global__ void k_check_ids(const u32* src, const u32* dst, u64 n, u64 nv, Ctr* 
         if (src[i] >= nv || dst[i] >= nv) atomicMin(&ctr->bad_index, ull(i));
 }
 
-// Pack inserts then deletes (graph.hpp:133-147).  Guard deletes become
-// kOpSkip and are counted as missed by the caller.
-__global__ void k_pack_batch(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
-                             u64 nd, u64* keys, u64* vals, u8* ops, Ctr* ctr) {
-    ull guards = 0;
-    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < ni + nd; i += u64(gridDim.x) * blockDim.x) {
-        if (i < ni) {
-            keys[i] = pack_edge(is[i], id[i]);
-            vals[i] = __double_as_longlong(iw ? iw[i] : 1.0);
-            ops[i] = kOpInsert;
-        } else {
-            const u64 j = i - ni;
-            keys[i] = pack_edge(ds[j], dd[j]);
-            vals[i] = 0;
-            const bool g = dd[j] == u32(kGuardDst);
-            ops[i] = g ? kOpSkip : kOpDelete;
-            guards += g;
-        }
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) guards += __shfl_xor_sync(FULL, guards, d);
-    if ((threadIdx.x & 31) == 0 && guards) atomicAdd(&ctr->guard_deletes, guards);
-}
-
 __global__ void k_pack_edges(const u32* s, const u32* d, u64 n, u64* keys, u32* idx) {
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         keys[i] = pack_edge(s[i], d[i]);
@@ -359,38 +335,22 @@ Graph::~Graph() {
 // DynamicGraph::apply_batch (graph.hpp:130-162)
 void Graph::apply_batch_device(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
                                u64 nd, pma_stats* out) {
-    cudaStream_t s = pma.stream();
-    Ctr* ctr = scratch_ctr();
-    if (ni > 0) {
-        ull init = ~0ull;
-        GPMA_CUDA(cudaMemcpyAsync(&ctr->bad_index, &init, 8, cudaMemcpyHostToDevice, s));
-        k_check_ids<<<grid_for(ni, 256), 256, 0, s>>>(is, id, ni, nv, ctr);
-        GPMA_LAUNCH_CHECK();
-    }
     const u64 n = ni + nd;
     bk.reserve(n + 1);
     bv.reserve(n + 1);
     bo.reserve(n + 1);
-    if (n > 0) {
-        k_pack_batch<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(is, id, iw, ni, ds, dd, nd, bk.ptr, bv.ptr, bo.ptr, ctr);
-        GPMA_LAUNCH_CHECK();
-    }
-    ull hc[2] = {~0ull, 0};
-    GPMA_CUDA(cudaMemcpyAsync(&hc[0], &ctr->bad_index, 8, cudaMemcpyDeviceToHost, s));
-    GPMA_CUDA(cudaMemcpyAsync(&hc[1], &ctr->guard_deletes, 8, cudaMemcpyDeviceToHost, s));
-    GPMA_CUDA(cudaStreamSynchronize(s));
-    if (ni > 0 && hc[0] != ~0ull) {
+    GraphFront gf{is, id, iw, ni, ds, dd, nd, nv, bk.ptr, bv.ptr, bo.ptr};
+    pma_stats st;
+    pma.batch_update_device(nullptr, nullptr, nullptr, n, ecfg, &st, &gf);
+    if (gf.bad_insert >= 0) {
         u32 bs = 0, bd = 0;
-        GPMA_CUDA(cudaMemcpy(&bs, is + hc[0], 4, cudaMemcpyDeviceToHost));
-        GPMA_CUDA(cudaMemcpy(&bd, id + hc[0], 4, cudaMemcpyDeviceToHost));
+        GPMA_CUDA(cudaMemcpy(&bs, is + gf.bad_insert, 4, cudaMemcpyDeviceToHost));
+        GPMA_CUDA(cudaMemcpy(&bd, id + gf.bad_insert, 4, cudaMemcpyDeviceToHost));
         throw ApiError(PMA_EINVAL, "edge (" + std::to_string(bs) + ", " + std::to_string(bd) +
                                        ") outside vertex range " + std::to_string(nv));
     }
-    const u64 guard_deletes = hc[1];
-    pma_stats st;
-    pma.batch_update_device(bk.ptr, bv.ptr, bo.ptr, n, ecfg, &st);
-    st.batch_size = n - guard_deletes;
-    st.deletes_missed += guard_deletes;
+    st.batch_size = n - gf.guard_deletes;
+    st.deletes_missed += gf.guard_deletes;
     if (out) *out = st;
 }
 

@@ -195,6 +195,60 @@ __global__ void k_compress(const u64* keys, u64 n, BitRuns runs, u64* ck, u32* c
     }
 }
 
+// Graph-mode front end (DynamicGraph::apply_batch, graph.hpp:133-147): pack
+// inserts then deletes, check insert ids, count guard deletes (kOpSkip, sorted
+// last), and emit the sort input with the |V|-derived compressed layout
+// (src << db | dst).  A non-guard delete outside that layout raises `oor`
+// (the batch is then redone on the generic path).
+__global__ void k_prep_graph(GraphFront f, int db, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
+    const u64 n = f.ni + f.nd;
+    const u64 lim = 1ull << db;
+    ull guards = 0, bad = 0, oor = 0;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        u32 s, d;
+        u64 v = 0;
+        u8 op;
+        if (i < f.ni) {
+            s = f.is[i];
+            d = f.id[i];
+            v = u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0));
+            op = kOpInsert;
+            if (s >= f.nv || d >= f.nv) bad = max(bad, ~ull(i));  // first offending insert
+        } else {
+            const u64 j = i - f.ni;
+            s = f.ds[j];
+            d = f.dd[j];
+            op = d == u32(kGuardDst) ? kOpSkip : kOpDelete;
+            guards += op == kOpSkip;
+        }
+        f.bk[i] = pack_edge(s, d);
+        f.bv[i] = v;
+        f.bo[i] = op;
+        u64 c;
+        if (op == kOpSkip) {
+            c = 1ull << (2 * db);
+        } else if (s >= lim || d >= lim) {
+            c = 0;
+            oor |= op == kOpDelete;
+        } else {
+            c = (u64(s) << db) | d;
+        }
+        ck[i] = c;
+        ci[i] = u32(i);
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        guards += __shfl_xor_sync(FULL, guards, d);
+        bad = max(bad, __shfl_xor_sync(FULL, bad, d));
+        oor |= __shfl_xor_sync(FULL, oor, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (guards) atomicAdd(&ctr->gdel, guards);
+        if (bad) atomicMax(&ctr->bad_ins, bad);
+        if (oor) atomicOr(&ctr->oor, 1ull);
+    }
+}
+
 __global__ void k_gather_sorted(const u32* __restrict__ ci, const u64* __restrict__ dk, const u64* __restrict__ dv,
                                 const u8* __restrict__ dop, u64 n, u64* __restrict__ gk, u64* __restrict__ gv,
                                 u8* __restrict__ go) {
@@ -1308,7 +1362,7 @@ void Pma::rebuild_at_capacity(u64 cap) {
 }
 
 void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n, const EngineCfg& cfg,
-                              pma_stats* out, u64 /*unused*/) {
+                              pma_stats* out, GraphFront* gf) {
     using Clock = std::chrono::steady_clock;
     const auto t0 = Clock::now();
     pma_stats st;
@@ -1328,42 +1382,56 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     event(0);
     // ---- 1. sort (stable, varying bits only) ----
     GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
-    k_or_mask<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, d_ctr);
-    GPMA_LAUNCH_CHECK();
-    ++launches;
-    sync_ctr();
-    const u64 mask = h_ctr->mask_or;
-    BitRuns runs{};
-    int nbits = 0;
-    for (int bit = 0; bit < 64;) {
-        if (!((mask >> bit) & 1)) {
-            ++bit;
-            continue;
-        }
-        int e = bit;
-        while (e < 64 && ((mask >> e) & 1)) ++e;
-        if (runs.n == 16) {  // too fragmented: fall back to the full key
-            runs.n = 1;
-            runs.lo[0] = 0;
-            runs.len[0] = 64;
-            runs.out[0] = 0;
-            nbits = 64;
-            break;
-        }
-        runs.lo[runs.n] = bit;
-        runs.len[runs.n] = e - bit;
-        runs.out[runs.n] = nbits;
-        nbits += e - bit;
-        runs.n++;
-        bit = e;
-    }
     sk_in.reserve(n);
     sk_out.reserve(n);
     si_in.reserve(n);
     si_out.reserve(n);
-    k_compress<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, runs, sk_in.ptr, si_in.ptr);
-    GPMA_LAUNCH_CHECK();
-    ++launches;
+    int nbits = 0;
+    if (gf) {
+        // graph front end: pack + id check + compression in one pass; the
+        // key layout is fixed by |V| (src, dst < 2^db), so no host round trip
+        int db = 1;
+        while (db < 32 && (1ull << db) < gf->nv) ++db;
+        nbits = 2 * db + 1;  // + the skip bit (guard deletes sort last)
+        dk = gf->bk;
+        dv = gf->bv;
+        dop = gf->bo;
+        k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, sk_in.ptr, si_in.ptr, d_ctr);
+        GPMA_LAUNCH_CHECK();
+        ++launches;
+    } else {
+        k_or_mask<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, d_ctr);
+        GPMA_LAUNCH_CHECK();
+        ++launches;
+        sync_ctr();
+        const u64 mask = h_ctr->mask_or;
+        BitRuns runs{};
+        for (int bit = 0; bit < 64;) {
+            if (!((mask >> bit) & 1)) {
+                ++bit;
+                continue;
+            }
+            int e = bit;
+            while (e < 64 && ((mask >> e) & 1)) ++e;
+            if (runs.n == 16) {  // too fragmented: fall back to the full key
+                runs.n = 1;
+                runs.lo[0] = 0;
+                runs.len[0] = 64;
+                runs.out[0] = 0;
+                nbits = 64;
+                break;
+            }
+            runs.lo[runs.n] = bit;
+            runs.len[runs.n] = e - bit;
+            runs.out[runs.n] = nbits;
+            nbits += e - bit;
+            runs.n++;
+            bit = e;
+        }
+        k_compress<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, runs, sk_in.ptr, si_in.ptr);
+        GPMA_LAUNCH_CHECK();
+        ++launches;
+    }
     const u64* sorted_ck = sk_in.ptr;
     const u32* sorted_ci = si_in.ptr;
     if (nbits > 0 && n > 1) {
@@ -1377,56 +1445,67 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         sorted_ck = sk_out.ptr;
         sorted_ci = si_out.ptr;
     }
-    // ---- 2. resolve duplicates: run ends -> unique updates ----
-    uk.reserve(n);
-    uv.reserve(n);
-    uop.reserve(n + 8);  // k_commit_leaf stages ops as aligned 4-byte words
+    // ---- 2+3. resolve duplicates (run ends -> unique updates) fused with the
+    // leaf assignment of each unique key (computed once per batch) ----
+    uk.reserve(n + 4);
+    uv.reserve(n + 4);
+    uop.reserve(n + 32);  // k_commit_leaf stages 16-byte aligned runs of uk / uv / uop
     ul.reserve(n);
-    gv_.reserve(n);
-    go_.reserve(n);
+    event(1);
     {
-        // gather key/value/op into sorted order (parallel random reads), so the
-        // ordered compaction below streams contiguous arrays
-        u64* gk = sk_in.ptr;  // free after the sort
-        k_gather_sorted<<<grid_for(n, 256, 148 * 16), 256, 0, stream_>>>(sorted_ci, dk, dv, dop, n, gk, gv_.ptr,
-                                                                        go_.ptr);
-        GPMA_LAUNCH_CHECK();
-        ++launches;
-        const u64* sk = gk;
-        const u64* sv = gv_.ptr;
-        const u8* so = go_.ptr;
+        const u64* ck = sorted_ck;
+        const u32* ci = sorted_ci;
+        const u64* kk = dk;
+        const u64* vv = dv;
+        const u8* oo = dop;
         u64* o_k = uk.ptr;
         u64* o_v = uv.ptr;
         u8* o_o = uop.ptr;
+        u32* o_l = ul.ptr;
+        const u64* hdr = d_hdr;
+        const u64 L = num_leaves();
+        const u8* sst = d_st;
+        const u64 lf = leaf_;
         Ctr* ctr = d_ctr;
         run_compact(
             stream_, ws, nullptr, n, n,
-            [=] __device__(ull i) { return ((i + 1 == n) || sk[i + 1] != sk[i]) && so[i] != kOpSkip; },
+            [=] __device__(ull i) { return ((i + 1 == n) || ck[i + 1] != ck[i]) && oo[ci[i]] != kOpSkip; },
             [=] __device__(ull i, unsigned f, ull x) {
                 if (!f) return;
                 // last insert of the run wins (segment_engine.hpp:346-363)
                 u8 op = kOpDelete;
                 u64 val = 0;
-                for (long long j = (long long)i; j >= 0 && sk[j] == sk[i]; --j) {
-                    if (so[j] == kOpInsert) {
+                for (long long j = (long long)i; j >= 0 && ck[j] == ck[i]; --j) {
+                    const u32 a = ci[j];
+                    if (oo[a] == kOpInsert) {
                         op = kOpInsert;
-                        val = sv[j];
+                        val = vv ? vv[a] : 0;
                         break;
                     }
                 }
-                o_k[x] = sk[i];
+                const u64 key = kk[ci[i]];
+                o_k[x] = key;
                 o_v[x] = val;
                 o_o[x] = op;
+                o_l[x] = u32(leaf_of_key(hdr, L, sst, lf, key));  // pma.hpp:234-289
             },
             [=] __device__(ull total) { ctr->n_unique = total; });
         ++launches;
     }
-    event(1);
-    // ---- 3. leaf assignment (once per batch) ----
-    k_leaf_search<<<grid_for(n, 256, 148 * 16), 256, 0, stream_>>>(uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st,
-                                                                  leaf_, ul.ptr);
-    GPMA_LAUNCH_CHECK();
-    ++launches;
+    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
+    event(2);
+    sync_ctr();
+    if (gf) {
+        gf->guard_deletes = h_ctr->gdel;
+        gf->bad_insert = h_ctr->bad_ins ? (long long)(~h_ctr->bad_ins) : -1;
+        if (gf->bad_insert >= 0) return;  // caller throws; nothing was mutated
+        if (h_ctr->oor) {
+            // a delete key outside the |V|-derived layout: redo the batch on
+            // the generic path (key reduction over the packed keys)
+            batch_update_device(gf->bk, gf->bv, gf->bo, n, cfg, out, nullptr);
+            return;
+        }
+    }
     pidx0.reserve(n);
     pidx1.reserve(n);
     gid.reserve(n);
@@ -1435,10 +1514,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     gflag.reserve(n);
     touched.reserve(2 * n + 2);
     rlist.reserve(2 * n + 4);
-    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
-    event(2);
     // ---- 4. rounds ----
-    sync_ctr();
     u64 npend = h_ctr->n_unique;
     u64* touched_ptr = touched.ptr;
     u64 ntouched = 0;

@@ -51,7 +51,10 @@ struct Ctr {
     ull nbig;
     ull max_slice;
     ull commit_bytes;
-    ull pad[3];
+    ull bad_ins;    // graph front end: ~(first insert index with an id >= |V|), 0 = none
+    ull oor;        // graph front end: a delete key outside the compressed key range
+    ull gdel;       // graph front end: guard deletes (dropped, counted missed)
+    ull pad[4];
 };
 
 struct EngineCfg {
@@ -66,6 +69,27 @@ struct EngineCfg {
 };
 
 struct SeqArgs;
+
+// Graph-mode batch front end (DynamicGraph::apply_batch, graph.hpp:130-162):
+// raw insert / delete arrays, packed on the device by the same kernel that
+// builds the sort input, with |V| fixing the compressed key layout (no key
+// reduction + host round trip).  Packed (key, value, op) land in bk/bv/bo.
+struct GraphFront {
+    const u32* is;
+    const u32* id;
+    const double* iw;
+    u64 ni;
+    const u32* ds;
+    const u32* dd;
+    u64 nd;
+    u64 nv;
+    u64* bk;
+    u64* bv;
+    u8* bo;
+    // results
+    u64 guard_deletes = 0;
+    long long bad_insert = -1;  // first insert index with an id >= nv
+};
 
 class Pma {
 public:
@@ -89,7 +113,7 @@ public:
     void load_slots(size_t capacity, const u64* keys, const u64* values, const u8* states);
     void download(u64* keys, u64* values, u8* states);
     void batch_update_device(const u64* d_keys, const u64* d_vals, const u8* d_ops, u64 n, const EngineCfg& cfg,
-                             pma_stats* out, u64 ext_guard_deletes_dev_slot = 0);
+                             pma_stats* out, GraphFront* gf = nullptr);
     void binary_search_leaf(const u64* keys, size_t n, u64* leaves);
     void search(const u64* keys, size_t n, u64* values, u8* found);
     u64 count_valid_in(u64 b, u64 e);

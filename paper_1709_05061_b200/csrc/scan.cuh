@@ -5,9 +5,13 @@
 // advance_round (segment_engine.hpp:90-105) and the touched-range list.
 //
 // One pass: every element is read once by `flag(i)` and handed to
-// `emit(i, f, exclusive_prefix)`; tiles of 2048 elements are claimed in order
-// through an atomic ticket so the look-back never waits on an unscheduled
-// tile, and the grid is persistent (<= 4 CTAs per SM).
+// `emit(i, f, exclusive_prefix)`.  A tile is 2048 elements, one CTA of 256
+// threads, items STRIPED (item j of thread t is element base + 256 j + t) so
+// every flag/emit access of a warp is one contiguous run; ranks come from warp
+// ballots, the 8 x 8 (item row, warp) counts are scanned by one warp, and that
+// warp runs the look-back.  Tile ids are block ids (blocks are dispatched in
+// order, as CUB's single-pass scans assume), and tile status words carry a
+// launch epoch, so no memset / ticket is needed between launches.
 #pragma once
 
 #include "common.cuh"
@@ -16,13 +20,17 @@ namespace gpma {
 
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
+constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kScanTile = kScanThreads * kScanItems;
-constexpr ull kStatusShift = 62;
-constexpr ull kValueMask = (1ull << kStatusShift) - 1;
+// status word: [63:36] epoch | [35:34] flag (1 aggregate, 2 inclusive) | [33:0] value
+constexpr int kEpochShift = 36;
+constexpr int kFlagShift = 34;
+constexpr ull kValueMask = (1ull << kFlagShift) - 1;
+constexpr ull kEpochMask = (1ull << (64 - kEpochShift)) - 1;
 
 struct ScanWorkspace {
     DevBuf<ull> tiles;
-    DevBuf<unsigned> ticket;
+    ull epoch = 0;
 };
 
 __device__ __forceinline__ ull ld_volatile(const ull* p) { return *reinterpret_cast<const volatile ull*>(p); }
@@ -30,80 +38,79 @@ __device__ __forceinline__ void st_volatile(ull* p, ull v) { *reinterpret_cast<v
 
 template <class Flag, class Emit, class Fin>
 __global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev, ull n_host, Flag flag, Emit emit,
-                                                               Fin fin, ull* tiles, unsigned* ticket) {
-    __shared__ unsigned s_tile;
-    __shared__ ull s_warp[kScanThreads / 32];
-    __shared__ ull s_prefix;
+                                                               Fin fin, ull* tiles, ull epoch) {
+    __shared__ unsigned s_off[kScanItems * kScanWarps];  // (item row, warp) counts -> exclusive offsets
+    __shared__ ull s_prefix, s_total;
     const ull n = n_dev ? *n_dev : n_host;
     const ull ntiles = (n + kScanTile - 1) / kScanTile;
+    const ull tile = blockIdx.x;
+    if (tile >= ntiles) return;
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    for (;;) {
-        if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-        __syncthreads();
-        const ull tile = s_tile;
-        if (tile >= ntiles) break;
-        const ull base = tile * kScanTile + ull(threadIdx.x) * kScanItems;
-        unsigned f[kScanItems];
-        unsigned cnt = 0;
+    const ull base = tile * kScanTile + threadIdx.x;
+    const unsigned below = lanemask_lt();
+    unsigned fm = 0;
+    unsigned char pre[kScanItems];
 #pragma unroll
-        for (int j = 0; j < kScanItems; ++j) {
-            const ull i = base + j;
-            f[j] = i < n ? (flag(i) ? 1u : 0u) : 0u;
-            cnt += f[j];
-        }
-        // block exclusive scan of per-thread counts
-        unsigned inc = cnt;
+    for (int j = 0; j < kScanItems; ++j) {
+        const ull i = base + ull(j) * kScanThreads;
+        const bool f = i < n && flag(i);
+        const unsigned bal = __ballot_sync(FULL, f);
+        pre[j] = (unsigned char)__popc(bal & below);
+        if (lane == 0) s_off[j * kScanWarps + warp] = __popc(bal);
+        fm |= (f ? 1u : 0u) << j;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // counts in element order: (row j, warp w) -> index j * 8 + w; two per lane
+        const unsigned a0 = s_off[2 * lane], a1 = s_off[2 * lane + 1];
+        const unsigned sum = a0 + a1;
+        unsigned inc = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            const unsigned o = __shfl_up_sync(0xffffffffu, inc, d);
+            const unsigned o = __shfl_up_sync(FULL, inc, d);
             if (lane >= unsigned(d)) inc += o;
         }
-        if (lane == 31) s_warp[warp] = inc;
-        __syncthreads();
-        ull warp_base = 0, block_total = 0;
-#pragma unroll
-        for (int w = 0; w < kScanThreads / 32; ++w) {
-            if (w < int(warp)) warp_base += s_warp[w];
-            block_total += s_warp[w];
-        }
-        const ull excl = warp_base + inc - cnt;
-        // decoupled look-back by warp 0
-        if (warp == 0) {
-            ull prefix = 0;
-            if (tile == 0) {
-                if (lane == 0) st_volatile(&tiles[0], (2ull << kStatusShift) | block_total);
-            } else {
-                if (lane == 0) st_volatile(&tiles[tile], (1ull << kStatusShift) | block_total);
-                long long t = (long long)tile - 1 - lane;
-                for (;;) {
-                    ull st = t >= 0 ? ld_volatile(&tiles[t]) : (2ull << kStatusShift);
-                    while (__any_sync(0xffffffffu, (st >> kStatusShift) == 0)) {
-                        if ((st >> kStatusShift) == 0) st = ld_volatile(&tiles[t]);
-                    }
-                    const unsigned incl_mask = __ballot_sync(0xffffffffu, (st >> kStatusShift) == 2);
-                    const int first = incl_mask ? __ffs(incl_mask) - 1 : 32;
-                    ull v = (int(lane) <= first) ? (st & kValueMask) : 0;
-#pragma unroll
-                    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-                    prefix += v;
-                    if (incl_mask) break;
-                    t -= 32;
+        const unsigned ex = inc - sum;
+        s_off[2 * lane] = ex;
+        s_off[2 * lane + 1] = ex + a0;
+        const ull total = __shfl_sync(FULL, inc, 31);
+        const ull ep = (epoch & kEpochMask) << kEpochShift;
+        ull prefix = 0;
+        if (tile == 0) {
+            if (lane == 0) st_volatile(&tiles[0], ep | (2ull << kFlagShift) | total);
+        } else {
+            if (lane == 0) st_volatile(&tiles[tile], ep | (1ull << kFlagShift) | total);
+            long long t = (long long)tile - 1 - lane;
+            for (;;) {
+                ull st = t >= 0 ? ld_volatile(&tiles[t]) : (ep | (2ull << kFlagShift));
+                auto ready = [&](ull x) { return (x & ~((1ull << kEpochShift) - 1)) == ep && ((x >> kFlagShift) & 3ull); };
+                while (__any_sync(FULL, !ready(st))) {
+                    if (!ready(st)) st = ld_volatile(&tiles[t]);
                 }
-                if (lane == 0) st_volatile(&tiles[tile], (2ull << kStatusShift) | (prefix + block_total));
-            }
-            if (lane == 0) s_prefix = prefix;
-        }
-        __syncthreads();
-        ull run = s_prefix + excl;
+                const unsigned incl_mask = __ballot_sync(FULL, ((st >> kFlagShift) & 3ull) == 2);
+                const int first = incl_mask ? __ffs(incl_mask) - 1 : 32;
+                ull v = (int(lane) <= first) ? (st & kValueMask) : 0;
 #pragma unroll
-        for (int j = 0; j < kScanItems; ++j) {
-            const ull i = base + j;
-            if (i < n) emit(i, f[j], run);
-            run += f[j];
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+                prefix += v;
+                if (incl_mask) break;
+                t -= 32;
+            }
+            if (lane == 0) st_volatile(&tiles[tile], ep | (2ull << kFlagShift) | (prefix + total));
         }
-        if (tile == ntiles - 1 && threadIdx.x == 0) fin(s_prefix + block_total);
-        __syncthreads();
+        if (lane == 0) {
+            s_prefix = prefix;
+            s_total = total;
+        }
     }
+    __syncthreads();
+    const ull pfx = s_prefix;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const ull i = base + ull(j) * kScanThreads;
+        if (i < n) emit(i, (fm >> j) & 1u, pfx + s_off[j * kScanWarps + warp] + pre[j]);
+    }
+    if (tile == ntiles - 1 && threadIdx.x == 0) fin(pfx + s_total);
 }
 
 // Launch helper: n is either device-resident (n_dev) or host-known (n_host);
@@ -114,12 +121,17 @@ void run_compact(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host
                  Fin fin) {
     const ull ntiles = (n_bound + kScanTile - 1) / kScanTile;
     if (ntiles == 0) return;
-    ws.tiles.reserve(ntiles);
-    ws.ticket.reserve(1);
-    GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ntiles * sizeof(ull), s));
-    GPMA_CUDA(cudaMemsetAsync(ws.ticket.ptr, 0, sizeof(unsigned), s));
-    const unsigned grid = static_cast<unsigned>(ntiles < ull(kNumSMs) * 4 ? ntiles : ull(kNumSMs) * 4);
-    compact_kernel<<<grid, kScanThreads, 0, s>>>(n_dev, n_host, flag, emit, fin, ws.tiles.ptr, ws.ticket.ptr);
+    if (ntiles > ws.tiles.cap) {
+        ws.tiles.reserve(ntiles);
+        GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), s));  // epoch 0 never issued
+    }
+    ws.epoch = (ws.epoch + 1) & kEpochMask;
+    if (ws.epoch == 0) {  // wrapped: stale words could carry any epoch again
+        GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), s));
+        ws.epoch = 1;
+    }
+    compact_kernel<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(n_dev, n_host, flag, emit, fin,
+                                                                          ws.tiles.ptr, ws.epoch);
     GPMA_LAUNCH_CHECK();
 }
 

@@ -135,3 +135,39 @@ def test_guard_deletes_are_dropped_and_counted():
     assert gs.parity() == ref_parity(r, rs)
     assert gs.deletes_missed == rs.deletes_missed
     assert_same_slots(g.pma().slots(), r.slots())
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_out_of_layout_deletes_match_reference(mode):
+    """Deletes whose ids lie outside [0, |V|) (not guards) stay in the batch as
+    missed deletes and still shape the decisions (graph.hpp:141-147); the
+    device front end's |V|-derived key layout cannot hold them, so the batch is
+    redone on the generic key-reduction path — results must not change."""
+    rng = np.random.default_rng(5)
+    nv = 300
+    s = rng.integers(0, nv, 2000)
+    d = rng.integers(0, nv, 2000)
+    g = DynamicGraph.from_edges(nv, s, d, None, GraphConfig(deletion_mode=mode))
+    r = RefGraph(nv, s, d, None, graph_config(deletion_mode=mode))
+    for t in range(6):
+        ins_s = rng.integers(0, nv, 200)
+        ins_d = rng.integers(0, nv, 200)
+        del_s = np.concatenate([s[rng.integers(0, len(s), 150)], rng.integers(nv, 2**32 - 1, 20), [7, 7]])
+        del_d = np.concatenate([d[rng.integers(0, len(d), 150)], rng.integers(0, 2**32 - 2, 20), [2**31, 2**31]])
+        args = (ins_s, ins_d, None, del_s.astype(np.uint32), del_d.astype(np.uint32))
+        gs = g.apply_batch(*args)
+        rs = r.apply_batch(*args)
+        assert gs.parity() == ref_parity(r, rs), t
+        assert_same_slots(g.pma().slots(), r.slots())
+        assert (g.row_offsets() == r.row_offsets()).all()
+
+
+def test_bad_insert_reports_first_offender_and_leaves_graph_unchanged():
+    nv, s, d, w = example()
+    g = DynamicGraph.from_edges(nv, s, d, w)
+    before = g.pma().slots()
+    with pytest.raises(ValueError, match=r"edge \(5, 0\) outside vertex range 3"):
+        g.apply_batch([0, 5, 9], [1, 0, 0], None, [0], [2])
+    after = g.pma().slots()
+    assert all((a == b).all() for a, b in zip(before, after))
+    assert list(bfs(g, 0)) == [0, 2, 1]
