@@ -103,6 +103,23 @@ __device__ __forceinline__ u64 leaf_of_key(const u64* hdr, u64 L, const u8* st, 
     return lo ? lo - 1 : 0;
 }
 
+// N leaf searches at once (keys < 2^64-1; pma.hpp:234-289 through the
+// backward-filled headers): uniform power-of-two descent (L = C/leaf is a
+// power of two) to the last header <= key, else 0 — the same leaf as
+// leaf_of_key — with the N searches interleaved so every level issues N
+// independent loads instead of one dependent chain per key.
+template <int N>
+__device__ __forceinline__ void leaf_search_interleaved(const u64* __restrict__ hdr, u64 L, unsigned act,
+                                                        const u64 (&key)[N], u64 (&pos)[N]) {
+#pragma unroll
+    for (int j = 0; j < N; ++j) pos[j] = 0;
+    for (u64 s = L >> 1; s; s >>= 1) {
+#pragma unroll
+        for (int j = 0; j < N; ++j)
+            if (((act >> j) & 1u) && __ldg(&hdr[pos[j] + s]) <= key[j]) pos[j] += s;
+    }
+}
+
 // Destination-driven even placement (pma.hpp:440-467): slot t of the
 // segment holds entry j = ceil(t*k/m) iff floor(j*m/k) == t.
 __device__ __forceinline__ bool placement_target(u64 t, u64 k, u64 m, u64* j_out) {

@@ -184,57 +184,54 @@ struct BitRuns {
 };
 
 // pext of the varying bits: order-preserving and injective on the batch.
-__global__ void k_compress(const u64* keys, u64 n, BitRuns runs, u64* ck, u32* ci) {
+// Payload = arrival index << 1 | is_insert, so duplicate resolution never
+// gathers the op.
+__global__ void k_compress(const u64* keys, const u8* ops, u64 n, BitRuns runs, u64* ck, u32* ci) {
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         const u64 k = keys[i];
         u64 c = 0;
         for (int r = 0; r < runs.n; ++r)
             c |= ((k >> runs.lo[r]) & ((runs.len[r] == 64) ? ~0ull : ((1ull << runs.len[r]) - 1))) << runs.out[r];
         ck[i] = c;
-        ci[i] = u32(i);
+        ci[i] = (u32(i) << 1) | (ops[i] == kOpInsert ? 1u : 0u);
     }
 }
 
-// Graph-mode front end (DynamicGraph::apply_batch, graph.hpp:133-147): pack
-// inserts then deletes, check insert ids, count guard deletes (kOpSkip, sorted
-// last), and emit the sort input with the |V|-derived compressed layout
-// (src << db | dst).  A non-guard delete outside that layout raises `oor`
-// (the batch is then redone on the generic path).
+// Graph-mode front end (DynamicGraph::apply_batch, graph.hpp:133-147): check
+// insert ids, count guard deletes, and emit the sort input with the
+// |V|-derived compressed layout (src << db | dst); guard deletes (dropped by
+// the reference before the engine) get key 1 << 2db and sort last.  Payload =
+// arrival index << 1 | is_insert.  A non-guard delete outside the layout
+// raises `oor` (the batch is then redone on the generic path).
 __global__ void k_prep_graph(GraphFront f, int db, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
     const u64 n = f.ni + f.nd;
     const u64 lim = 1ull << db;
     ull guards = 0, bad = 0, oor = 0;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         u32 s, d;
-        u64 v = 0;
-        u8 op;
-        if (i < f.ni) {
+        bool ins = i < f.ni, skip = false;
+        if (ins) {
             s = f.is[i];
             d = f.id[i];
-            v = u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0));
-            op = kOpInsert;
             if (s >= f.nv || d >= f.nv) bad = max(bad, ~ull(i));  // first offending insert
         } else {
             const u64 j = i - f.ni;
             s = f.ds[j];
             d = f.dd[j];
-            op = d == u32(kGuardDst) ? kOpSkip : kOpDelete;
-            guards += op == kOpSkip;
+            skip = d == u32(kGuardDst);
+            guards += skip;
         }
-        f.bk[i] = pack_edge(s, d);
-        f.bv[i] = v;
-        f.bo[i] = op;
         u64 c;
-        if (op == kOpSkip) {
+        if (skip) {
             c = 1ull << (2 * db);
         } else if (s >= lim || d >= lim) {
             c = 0;
-            oor |= op == kOpDelete;
+            oor |= !ins;
         } else {
             c = (u64(s) << db) | d;
         }
         ck[i] = c;
-        ci[i] = u32(i);
+        ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -249,17 +246,6 @@ __global__ void k_prep_graph(GraphFront f, int db, u64* __restrict__ ck, u32* __
     }
 }
 
-__global__ void k_gather_sorted(const u32* __restrict__ ci, const u64* __restrict__ dk, const u64* __restrict__ dv,
-                                const u8* __restrict__ dop, u64 n, u64* __restrict__ gk, u64* __restrict__ gv,
-                                u8* __restrict__ go) {
-    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
-        const u32 a = ci[i];
-        gk[i] = dk[a];
-        gv[i] = dv ? dv[a] : 0;
-        go[i] = dop[a];
-    }
-}
-
 __global__ void k_iota(u32* p, const ull* n_dev) {
     const u64 n = *n_dev;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) p[i] = u32(i);
@@ -270,6 +256,45 @@ __global__ void k_leaf_search(const u64* __restrict__ uk, const ull* n_dev, cons
     const u64 n = *n_dev;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
         ul[i] = u32(leaf_of_key(hdr, L, st, leaf, uk[i]));
+}
+
+// Leaf assignment of the sorted unique keys (assign_leaves_sorted,
+// pma.hpp:258-289, through the backward-filled headers: last header <= key,
+// else 0).  Graph PMAs bracket the answer with the row offsets first: edge
+// (u, v) sorts between the guards of u - 1 (slot ro[u] - 1) and u (slot
+// ro[u+1] - 1), so its leaf lies in [leaf(ro[u] - 1), leaf(ro[u+1] - 1)] —
+// two adjacent loads plus a bisection over the row's few leaves instead of a
+// log2(C/16)-level descent.  Other keys (plain PMAs, ids >= |V|) take the
+// uniform descent; keys are in order across the warp either way.
+__global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_dev, const u64* __restrict__ hdr, u64 L,
+                                     const u8* __restrict__ st, u64 leaf, const u64* __restrict__ ro, u64 nv,
+                                     u32* __restrict__ ul) {
+    const u64 n = *n_dev;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const u64 key = uk[i];
+        const u64 u = key >> 32;
+        u64 out;
+        if (ro && u < nv && !is_guard(key)) {
+            const u64 a = __ldg(&ro[u]), b = __ldg(&ro[u + 1]);
+            u64 lo = a ? (a - 1) / leaf : 0;  // hdr[lo] <= guard(u - 1) < key (or lo == 0)
+            u64 hi = (b - 1) / leaf + 1;      // hdr[hi] > guard(u) > key (or hi == L)
+            if (hi > L) hi = L;
+            while (hi - lo > 1) {
+                const u64 mid = (lo + hi) >> 1;
+                if (__ldg(&hdr[mid]) <= key) lo = mid;
+                else hi = mid;
+            }
+            out = lo;
+        } else if (key == ~0ull) {
+            out = leaf_of_key(hdr, L, st, leaf, key);
+        } else {
+            const u64 kk[1] = {key};
+            u64 pos[1];
+            leaf_search_interleaved<1>(hdr, L, 1u, kk, pos);
+            out = pos[0];
+        }
+        ul[i] = u32(out);
+    }
 }
 
 // --------------------------------------------------------------- commit args
@@ -1393,9 +1418,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         int db = 1;
         while (db < 32 && (1ull << db) < gf->nv) ++db;
         nbits = 2 * db + 1;  // + the skip bit (guard deletes sort last)
-        dk = gf->bk;
-        dv = gf->bv;
-        dop = gf->bo;
         k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, sk_in.ptr, si_in.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
         ++launches;
@@ -1428,7 +1450,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             runs.n++;
             bit = e;
         }
-        k_compress<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, n, runs, sk_in.ptr, si_in.ptr);
+        k_compress<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(dk, dop, n, runs, sk_in.ptr, si_in.ptr);
         GPMA_LAUNCH_CHECK();
         ++launches;
     }
@@ -1457,39 +1479,60 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         const u32* ci = sorted_ci;
         const u64* kk = dk;
         const u64* vv = dv;
-        const u8* oo = dop;
+        const double* gw = gf ? gf->iw : nullptr;
+        const int gdb = gf ? (nbits - 1) / 2 : 0;  // graph layout: key = src << gdb | dst
+        const u64 skipkey = gf ? (1ull << (nbits - 1)) : ~0ull;
         u64* o_k = uk.ptr;
         u64* o_v = uv.ptr;
         u8* o_o = uop.ptr;
-        u32* o_l = ul.ptr;
-        const u64* hdr = d_hdr;
-        const u64 L = num_leaves();
-        const u8* sst = d_st;
-        const u64 lf = leaf_;
         Ctr* ctr = d_ctr;
-        run_compact(
+        run_compact_tile(
             stream_, ws, nullptr, n, n,
-            [=] __device__(ull i) { return ((i + 1 == n) || ck[i + 1] != ck[i]) && oo[ci[i]] != kOpSkip; },
-            [=] __device__(ull i, unsigned f, ull x) {
-                if (!f) return;
-                // last insert of the run wins (segment_engine.hpp:346-363)
-                u8 op = kOpDelete;
-                u64 val = 0;
-                for (long long j = (long long)i; j >= 0 && ck[j] == ck[i]; --j) {
-                    const u32 a = ci[j];
-                    if (oo[a] == kOpInsert) {
-                        op = kOpInsert;
-                        val = vv ? vv[a] : 0;
-                        break;
+            [=] __device__(ull i) {
+                const u64 c = ck[i];
+                return ((i + 1 == n) || ck[i + 1] != c) && c < skipkey;
+            },
+            [=] __device__(ull i0, ull nn, unsigned fm, const ull* xs) {
+                // last insert of each equal-key run wins (segment_engine.hpp:346-363);
+                // the op rides in the sort payload and, for graphs, the key is the
+                // decompressed sort key — only insert values are gathered
+#pragma unroll
+                for (int j = 0; j < kScanItems; ++j) {
+                    if (!((fm >> j) & 1u)) continue;
+                    const ull i = i0 + ull(j) * kScanThreads;
+                    const u64 c = ck[i];
+                    const u32 p0 = ci[i];
+                    u32 p = p0;
+                    if (!(p & 1u) && i > 0 && ck[i - 1] == c) {  // delete at a run end: any earlier insert?
+                        for (long long t = (long long)i - 1; t >= 0 && ck[t] == c; --t) {
+                            const u32 q = ci[t];
+                            if (q & 1u) {
+                                p = q;
+                                break;
+                            }
+                        }
                     }
+                    const u32 a = p >> 1;
+                    const bool ins = p & 1u;
+                    u64 key, val = 0;
+                    if (gdb) {
+                        key = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
+                        if (ins) val = u64(__double_as_longlong(gw ? gw[a] : 1.0));
+                    } else {
+                        key = kk[p0 >> 1];
+                        if (ins && vv) val = vv[a];
+                    }
+                    o_k[xs[j]] = key;
+                    o_v[xs[j]] = val;
+                    o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
                 }
-                const u64 key = kk[ci[i]];
-                o_k[x] = key;
-                o_v[x] = val;
-                o_o[x] = op;
-                o_l[x] = u32(leaf_of_key(hdr, L, sst, lf, key));  // pma.hpp:234-289
             },
             [=] __device__(ull total) { ctr->n_unique = total; });
+        ++launches;
+        // leaf assignment (pma.hpp:234-289), once per batch
+        k_leaf_search_sorted<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
+            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, d_row_offsets, num_vertices, ul.ptr);
+        GPMA_LAUNCH_CHECK();
         ++launches;
     }
     GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
@@ -1500,9 +1543,34 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         gf->bad_insert = h_ctr->bad_ins ? (long long)(~h_ctr->bad_ins) : -1;
         if (gf->bad_insert >= 0) return;  // caller throws; nothing was mutated
         if (h_ctr->oor) {
-            // a delete key outside the |V|-derived layout: redo the batch on
-            // the generic path (key reduction over the packed keys)
-            batch_update_device(gf->bk, gf->bv, gf->bo, n, cfg, out, nullptr);
+            // a delete key outside the |V|-derived layout: pack the batch
+            // without its guard deletes (the reference drops them before the
+            // engine) and redo it on the generic key-reduction path
+            const GraphFront f = *gf;
+            u64* bk = f.bk;
+            u64* bv = f.bv;
+            u8* bo = f.bo;
+            Ctr* ctr = d_ctr;
+            run_compact(
+                stream_, ws, nullptr, n, n,
+                [=] __device__(ull i) { return i < f.ni || f.dd[i - f.ni] != u32(kGuardDst); },
+                [=] __device__(ull i, unsigned fl, ull x) {
+                    if (!fl) return;
+                    if (i < f.ni) {
+                        bk[x] = pack_edge(f.is[i], f.id[i]);
+                        bv[x] = u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0));
+                        bo[x] = kOpInsert;
+                    } else {
+                        bk[x] = pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
+                        bv[x] = 0;
+                        bo[x] = kOpDelete;
+                    }
+                },
+                [=] __device__(ull total) { ctr->nt = total; });
+            sync_ctr();
+            const u64 m = h_ctr->nt;
+            batch_update_device(bk, bv, bo, m, cfg, out, nullptr);
+            if (out) out->batch_size = n;  // the caller subtracts the guard deletes
             return;
         }
     }

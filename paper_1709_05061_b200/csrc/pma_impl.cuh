@@ -195,8 +195,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u64> sk_in, sk_out;   // compressed keys
     DevBuf<u32> si_in, si_out;   // arrival index payload
     DevBuf<unsigned char> sort_tmp;
-    DevBuf<u64> uk, uv, gv_;
-    DevBuf<u8> go_;
+    DevBuf<u64> uk, uv;
     DevBuf<u8> uop;
     DevBuf<u32> ul;
     DevBuf<u32> pidx0, pidx1, gid, gstart, gseg;

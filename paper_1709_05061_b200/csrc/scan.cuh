@@ -36,9 +36,12 @@ struct ScanWorkspace {
 __device__ __forceinline__ ull ld_volatile(const ull* p) { return *reinterpret_cast<const volatile ull*>(p); }
 __device__ __forceinline__ void st_volatile(ull* p, ull v) { *reinterpret_cast<volatile ull*>(p) = v; }
 
-template <class Flag, class Emit, class Fin>
-__global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev, ull n_host, Flag flag, Emit emit,
-                                                               Fin fin, ull* tiles, ull epoch) {
+// emit_tile(i0, n, fm, x[]) handles the thread's kScanItems items i0 + 256 j
+// (j < kScanItems, i < n) at once: bit j of fm = flag, x[j] = exclusive prefix.
+// Lets a caller interleave independent per-item work (e.g. 8 binary searches).
+template <class Flag, class EmitTile, class Fin>
+__global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev, ull n_host, Flag flag,
+                                                               EmitTile emit_tile, Fin fin, ull* tiles, ull epoch) {
     __shared__ unsigned s_off[kScanItems * kScanWarps];  // (item row, warp) counts -> exclusive offsets
     __shared__ ull s_prefix, s_total;
     const ull n = n_dev ? *n_dev : n_host;
@@ -50,10 +53,15 @@ __global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev,
     const unsigned below = lanemask_lt();
     unsigned fm = 0;
     unsigned char pre[kScanItems];
+    bool fl[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {  // all flags first: their loads overlap
+        const ull i = base + ull(j) * kScanThreads;
+        fl[j] = i < n && flag(i);
+    }
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        const ull i = base + ull(j) * kScanThreads;
-        const bool f = i < n && flag(i);
+        const bool f = fl[j];
         const unsigned bal = __ballot_sync(FULL, f);
         pre[j] = (unsigned char)__popc(bal & below);
         if (lane == 0) s_off[j * kScanWarps + warp] = __popc(bal);
@@ -105,20 +113,31 @@ __global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev,
     }
     __syncthreads();
     const ull pfx = s_prefix;
+    ull xs[kScanItems];
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-        const ull i = base + ull(j) * kScanThreads;
-        if (i < n) emit(i, (fm >> j) & 1u, pfx + s_off[j * kScanWarps + warp] + pre[j]);
-    }
+    for (int j = 0; j < kScanItems; ++j) xs[j] = pfx + s_off[j * kScanWarps + warp] + pre[j];
+    emit_tile(base, n, fm, xs);
     if (tile == ntiles - 1 && threadIdx.x == 0) fin(pfx + s_total);
 }
 
 // Launch helper: n is either device-resident (n_dev) or host-known (n_host);
 // n_bound is a host-known upper bound used to size the workspace and grid.
 // If n can be 0 at run time, `fin` is not called (callers pre-set totals).
-template <class Flag, class Emit, class Fin>
-void run_compact(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host, ull n_bound, Flag flag, Emit emit,
-                 Fin fin) {
+template <class Emit>
+struct PerItemEmit {
+    Emit emit;
+    __device__ __forceinline__ void operator()(ull i0, ull n, unsigned fm, const ull* xs) const {
+#pragma unroll
+        for (int j = 0; j < kScanItems; ++j) {
+            const ull i = i0 + ull(j) * kScanThreads;
+            if (i < n) emit(i, (fm >> j) & 1u, xs[j]);
+        }
+    }
+};
+
+template <class Flag, class EmitTile, class Fin>
+void run_compact_tile(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host, ull n_bound, Flag flag,
+                      EmitTile emit_tile, Fin fin) {
     const ull ntiles = (n_bound + kScanTile - 1) / kScanTile;
     if (ntiles == 0) return;
     if (ntiles > ws.tiles.cap) {
@@ -130,9 +149,15 @@ void run_compact(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host
         GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), s));
         ws.epoch = 1;
     }
-    compact_kernel<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(n_dev, n_host, flag, emit, fin,
+    compact_kernel<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(n_dev, n_host, flag, emit_tile, fin,
                                                                           ws.tiles.ptr, ws.epoch);
     GPMA_LAUNCH_CHECK();
+}
+
+template <class Flag, class Emit, class Fin>
+void run_compact(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host, ull n_bound, Flag flag, Emit emit,
+                 Fin fin) {
+    run_compact_tile(s, ws, n_dev, n_host, n_bound, flag, PerItemEmit<Emit>{emit}, fin);
 }
 
 struct NoFin {

@@ -15,8 +15,12 @@ if [[ $WHAT == all || $WHAT == bench ]]; then
   head -c 600 gpurun_out/bench_$TAG.json; echo
 fi
 if [[ $WHAT == all || $WHAT == ncu ]]; then
-  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-     --log-file gpurun_out/launches_$TAG.csv python bench.py --profile --steps 2 --warmup 3 > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu list rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-k_commit_leaf} -s ${KSKIP:-3} -c 2 \
-     -f -o gpurun_out/full_$TAG python bench.py --profile --steps 2 --warmup 3 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
+  # one C2 step (tools/prof_step.py brackets it with cudaProfilerStart/Stop)
+  timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+     --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python tools/prof_step.py > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "ncu list rc=$?"
+  IFS=',' read -ra KS <<< "${KREGEX:-k_commit_leaf}"
+  for k in "${KS[@]}"; do
+    timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:$k -c 1 \
+       -f -o gpurun_out/full_${TAG}_$k python tools/prof_step.py > gpurun_out/ncu_full_${TAG}_$k.log 2>&1; echo "ncu full $k rc=$?"
+  done
 fi
