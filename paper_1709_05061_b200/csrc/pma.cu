@@ -67,6 +67,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     GPMA_CUDA(cudaMalloc(&d_ctr, sizeof(Ctr)));
     GPMA_CUDA(cudaMallocHost(&h_ctr, sizeof(Ctr)));
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
+    for (auto& e : lev_ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
     headers_closed_form(nullptr, 0);
     GPMA_CUDA(cudaStreamSynchronize(stream_));
@@ -79,6 +80,8 @@ Pma::~Pma() {
     if (d_ctr) cudaFree(d_ctr);
     if (h_ctr) cudaFreeHost(h_ctr);
     for (auto& e : ev_)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : lev_ev_)
         if (e) cudaEventDestroy(e);
     if (stream_) cudaStreamDestroy(stream_);
 }
@@ -316,7 +319,6 @@ struct CommitArgs {
     u64* ro;
     u64* rlist;
     u32* biglist;
-    unsigned tile;  // groups per warp tile (lane tiers)
     int level;
     u64 m;
     u64 leaf;
@@ -821,8 +823,11 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
     const unsigned leafmask = (leaf >= 32) ? 0xffffffffu : ((1u << leaf) - 1u);
     const unsigned below = (1u << hl) - 1u;  // lanes of my group below me (hl < 32)
     Acc acc;
-    // a.tile groups per warp tile (<= 32): small rounds spread over more warps
-    const unsigned T = a.tile;
+    // groups per warp tile (<= 32), from the device-side group count: small
+    // rounds spread over many warps (one group each), big ones pack 32
+    unsigned T = unsigned((ngroups + 148 * 32 - 1) / (148 * 32));
+    T = T < 1 ? 1 : (T > 32 ? 32 : T);
+    if (G == 16) T = (T + 1) & ~1u;  // half-warp tier handles pairs
     for (ull g0 = (ull(blockIdx.x) * kWarpTierWarps + w) * T; g0 < ngroups; g0 += ull(gridDim.x) * kWarpTierWarps * T) {
         u32 t_lo = 0, t_hi = 0, t_seg = 0;
         if (lane < T) load_group_tile(a, g0, ngroups, lane, t_lo, t_hi, t_seg);
@@ -1535,7 +1540,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         GPMA_LAUNCH_CHECK();
         ++launches;
     }
-    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
+    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->np[0], &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
     event(2);
     sync_ctr();
     if (gf) {
@@ -1583,7 +1588,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     touched.reserve(2 * n + 2);
     rlist.reserve(2 * n + 4);
     // ---- 4. rounds ----
-    u64 npend = h_ctr->n_unique;
+    // Rounds are device-driven: every kernel reads its counts from d_ctr, the
+    // per-level stats land in d_ctr->lvl_*, so while the pending list is large
+    // (more rounds are near certain) the next round is launched without a host
+    // round trip; the host syncs after odd levels, before the root, and
+    // whenever the pending list is small.
+    u64 npend = h_ctr->n_unique;  // host-known upper bound of the pending count
     u64* touched_ptr = touched.ptr;
     u64 ntouched = 0;
     u32* pcur = nullptr;  // round 0: pending = all unique updates in order (identity)
@@ -1591,8 +1601,11 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     float seg_ms = 0.f;
     bool root_done = false;
     if (npend > 0) {
+        int synced_upto = -1;  // per-level stats collected for levels <= synced_upto
         for (int level = 0;; ++level) {
             const u64 m = leaf_ << level;
+            ull* np_cur = &d_ctr->np[level & 1];
+            ull* np_next = &d_ctr->np[(level + 1) & 1];
             // group = segment heads (unique_segments)
             {
                 const u32* ulp = ul.ptr;
@@ -1603,7 +1616,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 Ctr* ctr = d_ctr;
                 const int lv = level;
                 run_compact(
-                    stream_, ws, &d_ctr->npend, 0, npend,
+                    stream_, ws, np_cur, 0, npend,
                     [=] __device__(ull p) {
                         return p == 0 || (ulp[pp ? pp[p] : p] >> lv) != (ulp[pp ? pp[p - 1] : p - 1] >> lv);
                     },
@@ -1616,11 +1629,11 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                     },
                     [=] __device__(ull total) {
                         ctr->ngroups = total;
-                        gs[total] = u32(ctr->npend);
+                        gs[total] = u32(*np_cur);
+                        ctr->lvl_npend[lv] = *np_cur;
                     });
                 ++launches;
             }
-            GPMA_CUDA(cudaMemsetAsync(&d_ctr->committed, 0, sizeof(ull), stream_));
             // commit (decide + merge + scatter)
             CommitArgs a{};
             a.keys = d_keys;
@@ -1646,38 +1659,31 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             a.eager = cfg.eager;
             a.large = cfg.large_for(m);
             a.cap_gt_min = cap_ > 16;
-            GPMA_CUDA(cudaEventRecord(ev_[5], stream_));
-            const bool cta_scratch = true;
-            if (cta_scratch) {
-                ensure_slot_scratch();
-                ik.reserve(n);
-                iv.reserve(n);
-                ir.reserve(n);
-                biglist.reserve(npend + 1);
-                a.ek = ek.ptr;
-                a.ev = ev.ptr;
-                a.es = es.ptr;
-                a.mflag = mflag.ptr;
-                a.ok = ok.ptr;
-                a.ov = ov.ptr;
-                a.ik = ik.ptr;
-                a.iv = iv.ptr;
-                a.ir = ir.ptr;
-                a.biglist = biglist.ptr;
-                GPMA_CUDA(cudaMemsetAsync(&d_ctr->nbig, 0, 2 * sizeof(ull), stream_));
-            }
+            GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level], stream_));
+            ensure_slot_scratch();
+            ik.reserve(n);
+            iv.reserve(n);
+            ir.reserve(n);
+            biglist.reserve(npend + 1);
+            a.ek = ek.ptr;
+            a.ev = ev.ptr;
+            a.es = es.ptr;
+            a.mflag = mflag.ptr;
+            a.ok = ok.ptr;
+            a.ov = ov.ptr;
+            a.ik = ik.ptr;
+            a.iv = iv.ptr;
+            a.ir = ir.ptr;
+            a.biglist = biglist.ptr;
             if (m <= 32) {
                 // warp tiers; hub groups (large slices) are appended to biglist
                 if (m == 16 && leaf_ == 16 && pcur == nullptr) {  // level 0: identity pending list
                     const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, 148 * 16);
                     k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
                 } else {
-                    // tile: enough warps to cover the SMs before packing 32 groups per warp
-                    unsigned T = unsigned((npend + 148 * 32 - 1) / (148 * 32));
-                    T = T < 1 ? 1 : (T > 32 ? 32 : T);
-                    if (m <= 16) T = (T + 1) & ~1u;  // half-warp tier handles pairs
-                    a.tile = T;
-                    const unsigned grid = grid_for((npend + T - 1) / T, kWarpTierWarps, 148 * 8);
+                    // grid for the host bound; the kernel sizes its tiles from the
+                    // device-side group count (<= npend)
+                    const unsigned grid = grid_for(npend, kWarpTierWarps, 148 * 8);
                     if (m <= 16) k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
                     else k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
                 }
@@ -1690,24 +1696,34 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 k_commit_cta<<<grid, kCtaThreads, 0, stream_>>>(a);
             }
             GPMA_LAUNCH_CHECK();
-            GPMA_CUDA(cudaEventRecord(ev_[6], stream_));
+            GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));
             ++launches;
-            // touched list (merge commits, in segment order)
+            // touched list (merge commits, in segment order) + the level's stats
             {
                 const u8* gf = gflag.ptr;
                 const u32* gg = gseg.ptr;
                 u64* tp = touched_ptr;
-                const u64 base = ntouched;
                 Ctr* ctr = d_ctr;
+                const int lv = level;
                 run_compact(
                     stream_, ws, &d_ctr->ngroups, 0, npend, [=] __device__(ull g) { return gf[g] == 2; },
                     [=] __device__(ull g, unsigned f, ull x) {
                         if (!f) return;
+                        const u64 base = ctr->ntouched_base;
                         const u64 seg = gg[g];
                         tp[2 * (base + x)] = seg * m;
                         tp[2 * (base + x) + 1] = seg * m + m;
                     },
-                    [=] __device__(ull total) { ctr->ntouched_next = base + total; });
+                    [=] __device__(ull total) {
+                        ctr->ntouched_next = ctr->ntouched_base + total;
+                        ctr->lvl_committed[lv] = ctr->committed;
+                        ctr->lvl_groups[lv] = ctr->ngroups;
+                        ctr->lvl_big[lv] = ctr->nbig;
+                        ctr->lvl_maxslice[lv] = ctr->max_slice;
+                        ctr->committed = 0;
+                        ctr->nbig = 0;
+                        ctr->max_slice = 0;
+                    });
                 ++launches;
             }
             // advance_round: keep deferred groups' updates
@@ -1717,37 +1733,44 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 const u32* pp = pcur;
                 u32* pn = pnext;
                 Ctr* ctr = d_ctr;
-                GPMA_CUDA(cudaMemsetAsync(&d_ctr->npend_next, 0, sizeof(ull), stream_));
                 run_compact(
-                    stream_, ws, &d_ctr->npend, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
+                    stream_, ws, np_cur, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
                     [=] __device__(ull p, unsigned f, ull x) {
                         if (f) pn[x] = pp ? pp[p] : u32(p);
                     },
-                    [=] __device__(ull total) { ctr->npend_next = total; });
+                    [=] __device__(ull total) {
+                        *np_next = total;
+                        ctr->ntouched_base = ctr->ntouched_next;
+                    });
                 ++launches;
             }
+            pcur = pnext;
+            pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
+            const bool speculate = npend >= (1u << 16) && (level & 1) == 0 && level < height_;
+            if (speculate) continue;  // next round straight away; stats at the next sync
             sync_ctr();
-            float ms = 0.f;
-            cudaEventElapsedTime(&ms, ev_[5], ev_[6]);
-            seg_ms += ms;
-            if (level < 16) {
-                timing.level_ms[level] += ms;
-                timing.level_groups[level] += h_ctr->ngroups;
-                timing.level_big[level] += h_ctr->nbig;
-                timing.level_max_slice[level] = std::max<u64>(timing.level_max_slice[level], h_ctr->max_slice);
+            for (int l = synced_upto + 1; l <= level; ++l) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, lev_ev_[2 * l], lev_ev_[2 * l + 1]);
+                seg_ms += ms;
+                if (l < 16) {
+                    timing.level_ms[l] += ms;
+                    timing.level_groups[l] += h_ctr->lvl_groups[l];
+                    timing.level_big[l] += h_ctr->lvl_big[l];
+                    timing.level_max_slice[l] = std::max<u64>(timing.level_max_slice[l], h_ctr->lvl_maxslice[l]);
+                }
+                if (h_ctr->lvl_npend[l] > 0) st.rounds++;
+                st.segments_per_level[l] += h_ctr->lvl_committed[l];
             }
-            st.rounds++;
-            st.segments_per_level[level] += h_ctr->committed;
+            synced_upto = level;
             ntouched = h_ctr->ntouched_next;
-            const u64 left = h_ctr->npend_next;
+            const u64 left = h_ctr->np[(level + 1) & 1];
             if (left == 0) break;
+            npend = left;
             if (level == height_) {
                 // root path: everything left is the single root group
-                pcur = pnext;
-                pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
-                npend = left;
-                GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->npend_next, sizeof(ull), cudaMemcpyDeviceToDevice,
-                                          stream_));
+                GPMA_CUDA(cudaMemcpyAsync(&d_ctr->npend, &d_ctr->np[(level + 1) & 1], sizeof(ull),
+                                          cudaMemcpyDeviceToDevice, stream_));
                 // apply the counters of the finished rounds first
                 valid_count = u64((long long)valid_count + h_ctr->valid_delta);
                 tombstone_count = u64((long long)tombstone_count + h_ctr->tomb_delta);
@@ -1895,11 +1918,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 sync_ctr();
                 break;
             }
-            pcur = pnext;
-            pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
-            npend = left;
-            GPMA_CUDA(
-                cudaMemcpyAsync(&d_ctr->npend, &d_ctr->npend_next, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
         }
     }
     // apply device counters

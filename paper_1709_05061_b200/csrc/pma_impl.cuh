@@ -21,6 +21,8 @@
 namespace gpma {
 
 // Device-side per-batch counters (one D2H per round).
+constexpr int kMaxLevels = 64;
+
 struct Ctr {
     ull n_unique;
     ull npend;
@@ -54,6 +56,16 @@ struct Ctr {
     ull bad_ins;    // graph front end: ~(first insert index with an id >= |V|), 0 = none
     ull oor;        // graph front end: a delete key outside the compressed key range
     ull gdel;       // graph front end: guard deletes (dropped, counted missed)
+    // device-driven rounds: pending counts alternate between np[level & 1] and
+    // np[(level + 1) & 1]; per-level stats are kept here and read at the next
+    // host sync (rounds may run back to back without one)
+    ull np[2];
+    ull ntouched_base;
+    ull lvl_npend[kMaxLevels];
+    ull lvl_committed[kMaxLevels];
+    ull lvl_groups[kMaxLevels];
+    ull lvl_big[kMaxLevels];
+    ull lvl_maxslice[kMaxLevels];
     ull pad[4];
 };
 
@@ -211,6 +223,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u8> mflag;
 
     cudaEvent_t ev_[8]{};
+    cudaEvent_t lev_ev_[2 * kMaxLevels]{};  // commit-kernel span of each level
 };
 
 }  // namespace gpma

@@ -47,7 +47,10 @@ __global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev,
     const ull n = n_dev ? *n_dev : n_host;
     const ull ntiles = (n + kScanTile - 1) / kScanTile;
     const ull tile = blockIdx.x;
-    if (tile >= ntiles) return;
+    if (tile >= ntiles) {
+        if (ntiles == 0 && tile == 0 && threadIdx.x == 0) fin(0);  // empty input: fin(0) all the same
+        return;
+    }
     const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const ull base = tile * kScanTile + threadIdx.x;
     const unsigned below = lanemask_lt();
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev,
 
 // Launch helper: n is either device-resident (n_dev) or host-known (n_host);
 // n_bound is a host-known upper bound used to size the workspace and grid.
-// If n can be 0 at run time, `fin` is not called (callers pre-set totals).
+// `fin(total)` runs exactly once, also for an empty input (n_bound > 0).
 template <class Emit>
 struct PerItemEmit {
     Emit emit;
