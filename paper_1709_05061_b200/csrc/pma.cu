@@ -204,9 +204,12 @@ __global__ void k_compress(const u64* keys, const u8* ops, u64 n, BitRuns runs, 
 // insert ids, count guard deletes, and emit the sort input with the
 // |V|-derived compressed layout (src << db | dst); guard deletes (dropped by
 // the reference before the engine) get key 1 << 2db and sort last.  Payload =
-// arrival index << 1 | is_insert.  A non-guard delete outside the layout
-// raises `oor` (the batch is then redone on the generic path).
-__global__ void k_prep_graph(GraphFront f, int db, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
+// arrival index << 1 | is_insert — or, when key and index fit one word
+// (ib > 0), the single u64 (key << ib | index), sorted keys-only on the key
+// bits: LSD radix is stable, so this is the same order at 16 instead of 24
+// bytes per element per pass.  A non-guard delete outside the layout raises
+// `oor` (the batch is then redone on the generic path).
+__global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
     const u64 n = f.ni + f.nd;
     const u64 lim = 1ull << db;
     ull guards = 0, bad = 0, oor = 0;
@@ -233,8 +236,12 @@ __global__ void k_prep_graph(GraphFront f, int db, u64* __restrict__ ck, u32* __
         } else {
             c = (u64(s) << db) | d;
         }
-        ck[i] = c;
-        ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
+        if (ib) {
+            ck[i] = (c << ib) | i;  // packed: key above the arrival index (op = index < ni)
+        } else {
+            ck[i] = c;
+            ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
+        }
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
@@ -1417,13 +1424,18 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     si_in.reserve(n);
     si_out.reserve(n);
     int nbits = 0;
+    int packed_ib = 0;
     if (gf) {
         // graph front end: pack + id check + compression in one pass; the
         // key layout is fixed by |V| (src, dst < 2^db), so no host round trip
         int db = 1;
         while (db < 32 && (1ull << db) < gf->nv) ++db;
         nbits = 2 * db + 1;  // + the skip bit (guard deletes sort last)
-        k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, sk_in.ptr, si_in.ptr, d_ctr);
+        int ib = 1;
+        while ((1ull << ib) < n) ++ib;
+        if (nbits + ib > 64) ib = 0;  // no room: key + index payload pairs
+        packed_ib = ib;
+        k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
         ++launches;
     } else {
@@ -1461,7 +1473,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     }
     const u64* sorted_ck = sk_in.ptr;
     const u32* sorted_ci = si_in.ptr;
-    if (nbits > 0 && n > 1) {
+    if (packed_ib && n > 1) {
+        size_t tmp = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tmp, sk_in.ptr, sk_out.ptr, int(n), packed_ib, packed_ib + nbits,
+                                       stream_);
+        sort_tmp.reserve(tmp);
+        GPMA_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp.ptr, tmp, sk_in.ptr, sk_out.ptr, int(n), packed_ib,
+                                                 packed_ib + nbits, stream_));
+        launches += (nbits + 7) / 8 + 1;
+        sorted_ck = sk_out.ptr;
+    } else if (nbits > 0 && n > 1) {
         size_t tmp = 0;
         cub::DeviceRadixSort::SortPairs(nullptr, tmp, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr, int(n), 0, nbits,
                                         stream_);
@@ -1487,6 +1508,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         const double* gw = gf ? gf->iw : nullptr;
         const int gdb = gf ? (nbits - 1) / 2 : 0;  // graph layout: key = src << gdb | dst
         const u64 skipkey = gf ? (1ull << (nbits - 1)) : ~0ull;
+        const int pib = packed_ib;
+        const u64 pmask = (1ull << pib) - 1;
+        const u64 gni = gf ? gf->ni : 0;
+        // sorted element i -> compressed key / payload (arrival index << 1 | is_insert)
+        auto KEY = [=] __device__(ull i) -> u64 { return pib ? (ck[i] >> pib) : ck[i]; };
+        auto PAY = [=] __device__(ull i) -> u32 {
+            if (!pib) return ci[i];
+            const u32 a = u32(ck[i] & pmask);
+            return (a << 1) | (a < gni ? 1u : 0u);
+        };
         u64* o_k = uk.ptr;
         u64* o_v = uv.ptr;
         u8* o_o = uop.ptr;
@@ -1494,8 +1525,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         run_compact_tile(
             stream_, ws, nullptr, n, n,
             [=] __device__(ull i) {
-                const u64 c = ck[i];
-                return ((i + 1 == n) || ck[i + 1] != c) && c < skipkey;
+                const u64 c = KEY(i);
+                return ((i + 1 == n) || KEY(i + 1) != c) && c < skipkey;
             },
             [=] __device__(ull i0, ull nn, unsigned fm, const ull* xs) {
                 // last insert of each equal-key run wins (segment_engine.hpp:346-363);
@@ -1505,12 +1536,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 for (int j = 0; j < kScanItems; ++j) {
                     if (!((fm >> j) & 1u)) continue;
                     const ull i = i0 + ull(j) * kScanThreads;
-                    const u64 c = ck[i];
-                    const u32 p0 = ci[i];
+                    const u64 c = KEY(i);
+                    const u32 p0 = PAY(i);
                     u32 p = p0;
-                    if (!(p & 1u) && i > 0 && ck[i - 1] == c) {  // delete at a run end: any earlier insert?
-                        for (long long t = (long long)i - 1; t >= 0 && ck[t] == c; --t) {
-                            const u32 q = ci[t];
+                    if (!(p & 1u) && i > 0 && KEY(i - 1) == c) {  // delete at a run end: any earlier insert?
+                        for (long long t = (long long)i - 1; t >= 0 && KEY(t) == c; --t) {
+                            const u32 q = PAY(t);
                             if (q & 1u) {
                                 p = q;
                                 break;
