@@ -274,6 +274,69 @@ int gpma_last_timing(const gpma_graph* g, pma_timing* out);
 void* gpma_cuda_stream(gpma_graph* g);
 void* pma_cuda_stream(pma_handle* h);
 
+/* ---- key-range sharding across GPUs ------------------------
+ * One GPMA+ per GPU over the source range [lo, hi) (keys are src << 32 | dst,
+ * so a source range is a key range; segments never cross shards).  The
+ * reference has no multi-GPU interface: these entry points are the device
+ * side of the paper's partitioned deployment; the
+ * collectives (NCCL all-to-all / all-reduce) run in the caller between these
+ * synchronous calls, on device pointers.  Vertex ids stay global. */
+
+/* DynamicGraph::from_edges (graph.hpp:66-92) restricted to the sources
+ * [lo, hi): edges with other sources are skipped (so every shard may be fed
+ * the same global edge list), guards only for [lo, hi), row offsets over
+ * [lo, hi] (gpma_row_offsets returns hi - lo + 1 entries).  apply_batch on a
+ * shard rejects inserts whose source lies outside [lo, hi). */
+int gpma_shard_from_edges_device(const gpma_graph_config* cfg, int device, size_t num_vertices, uint32_t lo,
+                                 uint32_t hi, const uint32_t* d_src, const uint32_t* d_dst, const double* d_weights,
+                                 size_t n, gpma_graph** out);
+int gpma_shard_range(const gpma_graph* g, uint64_t* lo, uint64_t* hi);
+
+/* Routing: stable partition of n device-resident updates by owner rank
+ * (d_bounds[r] <= src < d_bounds[r+1], world + 1 entries, world <= 64; ids
+ * >= |V| go to the last rank) as EdgeKeys into d_out_keys (owner-major,
+ * arrival order kept inside each owner); counts[r] (host) = updates for rank
+ * r.  d_w / d_out_w may be NULL. */
+int gpma_route_partition(gpma_graph* g, const uint32_t* d_src, const uint32_t* d_dst, const double* d_w, size_t n,
+                         const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
+                         uint64_t* counts);
+
+/* DynamicGraph::apply_batch (graph.hpp:130-162) with EdgeKey-packed device
+ * updates (key = src << 32 | dst, graph.hpp:27-37) — the routed form. */
+int gpma_apply_batch_keys_device(gpma_graph* g, const uint64_t* d_ins_keys, const double* d_ins_w, size_t n_ins,
+                                 const uint64_t* d_del_keys, size_t n_del, pma_stats* stats);
+
+/* BFS (analytics.hpp:22-48), one level: mark (flags[v] = 1, |V| bytes,
+ * zeroed by the call) the out-neighbours of the owned frontier vertices; the
+ * caller max-reduces the flags across shards, then the owners admit their
+ * unreached flagged vertices at `depth` (dist_local: hi - lo entries) as the
+ * next frontier (global ids, count to *nf). */
+int gpma_shard_bfs_mark(gpma_graph* g, const uint32_t* d_frontier, uint32_t nf, uint8_t* d_flags);
+int gpma_shard_bfs_update(gpma_graph* g, const uint8_t* d_flags, uint32_t* d_dist_local, uint32_t depth,
+                          uint32_t* d_next, uint32_t* nf);
+
+/* Connected components (analytics.hpp:53-82) as min-label propagation over
+ * replicated labels (|V| entries): hook the owned edges (atomic min), the
+ * caller min-reduces the labels across shards, then pointer jumping makes
+ * every label its root; *changed = any label differs from d_prev.  The
+ * fixpoint labels are the component minima — the reference's labels. */
+int gpma_shard_cc_hook(gpma_graph* g, uint32_t* d_labels);
+int gpma_cc_jump(gpma_graph* g, uint32_t* d_labels, size_t n, const uint32_t* d_prev, int* changed);
+
+/* PageRank (analytics.hpp:84-143): out-degrees of the owned rows (|V|
+ * entries, zeroed by the call; the caller sum-reduces them once); per
+ * iteration the owners push d*x[u]/outdeg[u] into d_y (zeroed by the call),
+ * the caller sum-reduces d_y, then gpma_pr_finish adds the base term
+ * ((1-d)/n + d*dangling/n) and returns the L1 residual (replicated). */
+int gpma_shard_outdeg(gpma_graph* g, uint32_t* d_outdeg);
+int gpma_shard_pr_push(gpma_graph* g, const double* d_x, const uint32_t* d_outdeg, double damping, double* d_y);
+int gpma_pr_finish(gpma_graph* g, const double* d_x, double* d_y, size_t n, const uint32_t* d_outdeg, double damping,
+                   double* l1);
+
+/* SpMV (analytics.hpp:147-158) of the owned rows: d_y_local[u - lo] for u in
+ * [lo, hi), same ordered accumulation as gpma_spmv. */
+int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local);
+
 /* Drive every kernel once on small synthetic inputs so CUDA's lazy module
  * loading never lands inside a timed region (call once per process/device). */
 int gpma_warmup(int device);

@@ -381,6 +381,111 @@ int gpma_spmv(gpma_graph* g, const double* x, double* y) {
     });
 }
 
+// ---- key-range sharding (shard.cu)
+int gpma_shard_from_edges_device(const gpma_graph_config* cfg, int device, size_t num_vertices, uint32_t lo,
+                                 uint32_t hi, const uint32_t* d_src, const uint32_t* d_dst, const double* d_weights,
+                                 size_t n, gpma_graph** out) {
+    return guarded(nullptr, [&] {
+        if (num_vertices >= 0xFFFFFFFFull)
+            throw ApiError(PMA_EINVAL, "from_edges: vertex count exceeds the id space");
+        if (lo > hi || hi > num_vertices) throw ApiError(PMA_EINVAL, "shard: need lo <= hi <= num_vertices");
+        auto* g = new gpma_graph;
+        try {
+            g->impl = new gpma::Graph(cfg, device, num_vertices, lo, hi);
+            g->view.impl = &g->impl->pma;
+            g->view.owned = false;
+            g->impl->from_edges_device(d_src, d_dst, d_weights, n);
+        } catch (...) {
+            delete g->impl;
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+int gpma_shard_range(const gpma_graph* g, uint64_t* lo, uint64_t* hi) {
+    if (!g || !g->impl) return PMA_EINVAL;
+    if (lo) *lo = g->impl->lo;
+    if (hi) *hi = g->impl->hi;
+    return PMA_OK;
+}
+
+int gpma_route_partition(gpma_graph* g, const uint32_t* d_src, const uint32_t* d_dst, const double* d_w, size_t n,
+                         const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
+                         uint64_t* counts) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->route_partition(d_src, d_dst, d_w, n, d_bounds, world, d_out_keys, d_out_w, counts);
+    });
+}
+
+int gpma_apply_batch_keys_device(gpma_graph* g, const uint64_t* d_ins_keys, const double* d_ins_w, size_t n_ins,
+                                 const uint64_t* d_del_keys, size_t n_del, pma_stats* stats) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->apply_batch_keys_device(d_ins_keys, d_ins_w, n_ins, d_del_keys, n_del, stats);
+    });
+}
+
+int gpma_shard_bfs_mark(gpma_graph* g, const uint32_t* d_frontier, uint32_t nf, uint8_t* d_flags) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->shard_bfs_mark(d_frontier, nf, d_flags);
+    });
+}
+
+int gpma_shard_bfs_update(gpma_graph* g, const uint8_t* d_flags, uint32_t* d_dist_local, uint32_t depth,
+                          uint32_t* d_next, uint32_t* nf) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->shard_bfs_update(d_flags, d_dist_local, depth, d_next, nf);
+    });
+}
+
+int gpma_shard_cc_hook(gpma_graph* g, uint32_t* d_labels) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->shard_cc_hook(d_labels);
+    });
+}
+
+int gpma_cc_jump(gpma_graph* g, uint32_t* d_labels, size_t n, const uint32_t* d_prev, int* changed) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->cc_jump(d_labels, n, d_prev, changed);
+    });
+}
+
+int gpma_shard_outdeg(gpma_graph* g, uint32_t* d_outdeg) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->shard_outdeg(d_outdeg);
+    });
+}
+
+int gpma_shard_pr_push(gpma_graph* g, const double* d_x, const uint32_t* d_outdeg, double damping, double* d_y) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->shard_pr_push(d_x, d_outdeg, damping, d_y);
+    });
+}
+
+int gpma_pr_finish(gpma_graph* g, const double* d_x, double* d_y, size_t n, const uint32_t* d_outdeg, double damping,
+                   double* l1) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->pr_finish(d_x, d_y, n, d_outdeg, damping, l1);
+    });
+}
+
+int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->shard_spmv(d_x, d_y_local);
+    });
+}
+
 int gpma_last_timing(const gpma_graph* g, pma_timing* out) {
     if (!g || !out) return PMA_EINVAL;
     *out = g->impl->pma.timing;

@@ -11,6 +11,7 @@
 #include <cstring>
 
 #include "block_ops.cuh"
+#include "analytics_kernels.cuh"
 #include "graph_impl.cuh"
 
 namespace gpma {
@@ -20,6 +21,15 @@ namespace gpma {
 __global__ void k_check_ids(const u32* src, const u32* dst, u64 n, u64 nv, Ctr* ctr) {
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
         if (src[i] >= nv || dst[i] >= nv) atomicMin(&ctr->bad_index, ull(i));
+}
+
+// Shard build: edges whose source lies outside the owned range [lo, hi) get
+// key 2^64-1 (sorted last, dropped by the dedupe).
+__global__ void k_pack_edges_shard(const u32* s, const u32* d, u64 n, u64 lo, u64 hi, u64* keys, u32* idx) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        keys[i] = (s[i] >= lo && s[i] < hi) ? pack_edge(s[i], d[i]) : ~0ull;
+        idx[i] = u32(i);
+    }
 }
 
 __global__ void k_pack_edges(const u32* s, const u32* d, u64 n, u64* keys, u32* idx) {
@@ -32,17 +42,17 @@ __global__ void k_pack_edges(const u32* s, const u32* d, u64 n, u64* keys, u32* 
 // Merge the |V| guards into the sorted unique edge list: edge i lands at
 // i + src (guards of smaller rows precede it), guard v lands after every
 // edge with src <= v.
-__global__ void k_place_guards(const u64* ek, const u64* ev, u64 ne, u64 nv, u64* ok, u64* ov) {
-    const u64 total = ne + nv;
+__global__ void k_place_guards(const u64* ek, const u64* ev, u64 ne, u64 lo, u64 hi, u64* ok, u64* ov) {
+    const u64 total = ne + (hi - lo);
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
         if (i < ne) {
             const u64 k = ek[i];
-            ok[i + src_of(k)] = k;
-            ov[i + src_of(k)] = ev[i];
+            ok[i + src_of(k) - lo] = k;
+            ov[i + src_of(k) - lo] = ev[i];
         } else {
-            const u64 v = i - ne;
+            const u64 v = lo + (i - ne);
             const u64 g = pack_edge(u32(v), u32(kGuardDst));
-            const u64 pos = lower_bound_dev(ek, ne, g) + v;
+            const u64 pos = lower_bound_dev(ek, ne, g) + (v - lo);
             ok[pos] = g;
             ov[pos] = 0;
         }
@@ -133,24 +143,6 @@ __global__ void k_cc_flatten(u32* parent, u64 nv) {
 }
 
 // -------- PageRank (analytics.hpp:100-143)
-// out-degree: Valid non-guard slots per row, warp-segmented by source.
-__global__ void k_outdeg(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u32* __restrict__ outdeg) {
-    const u64 stride = u64(gridDim.x) * blockDim.x;
-    for (u64 t0 = (blockIdx.x * u64(blockDim.x) + threadIdx.x) & ~31ull; t0 < cap; t0 += stride) {
-        const u64 t = t0 + (threadIdx.x & 31u);
-        bool e = false;
-        u32 s = 0xFFFFFFFFu;
-        if (t < cap && st[t] == kValid) {
-            const u64 k = keys[t];
-            e = !is_guard(k);
-            s = src_of(k);
-        }
-        const unsigned grp = __match_any_sync(FULL, e ? s : 0xFFFFFFFFu);
-        const unsigned leader = __ffs(grp) - 1;
-        if (e && (threadIdx.x & 31u) == leader) atomicAdd(&outdeg[s], u32(__popc(grp)));
-    }
-}
-
 __global__ void k_pr_prep(const double* __restrict__ x, const u32* __restrict__ outdeg, u64 n, double d,
                           double* __restrict__ share, double* dangling_sum) {
     double dang = 0.0;
@@ -174,18 +166,6 @@ __global__ void k_pr_base(double* __restrict__ y, u64 n, const double* dangling_
     for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x) y[u] = base;
 }
 
-// push sweep over the gapped array: src comes from the key, so no row
-// offsets are read; red.global.add.f64 into y (L2-resident for |V| <= ~16M).
-__global__ void __launch_bounds__(256) k_pr_push(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
-                                                 const double* __restrict__ share, double* __restrict__ y) {
-    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < cap; t += u64(gridDim.x) * blockDim.x) {
-        if (st[t] != kValid) continue;
-        const u64 k = keys[t];
-        if (is_guard(k)) continue;
-        atomicAdd(&y[dst_of(k)], share[src_of(k)]);
-    }
-}
-
 __global__ void k_pr_l1(const double* __restrict__ x, const double* __restrict__ y, u64 n, double* l1) {
     double acc = 0.0;
     for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x)
@@ -195,53 +175,21 @@ __global__ void k_pr_l1(const double* __restrict__ x, const double* __restrict__
     if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(l1, acc);
 }
 
-// -------- SpMV (analytics.hpp:147-158): warp per row; products in parallel,
-// accumulation serial in ascending slot order with explicit round-to-nearest
-// multiply and add (no FMA contraction) — bit-exact with the reference.
-__global__ void __launch_bounds__(256) k_spmv(const u64* __restrict__ ro, u64 nv, const u64* __restrict__ keys,
-                                              const u64* __restrict__ vals, const u8* __restrict__ st,
-                                              const double* __restrict__ x, double* __restrict__ y) {
-    const unsigned lane = threadIdx.x & 31u;
-    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
-    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
-    for (u64 u = warp; u < nv; u += nwarps) {
-        const u64 b = ro[u], e = ro[u + 1];
-        double acc = 0.0;
-        for (u64 t0 = b; t0 < e; t0 += 32) {
-            const u64 t = t0 + lane;
-            double prod = 0.0;
-            bool ok = false;
-            if (t < e && st[t] == kValid) {
-                const u64 k = keys[t];
-                if (!is_guard(k)) {
-                    ok = true;
-                    prod = __dmul_rn(__longlong_as_double((long long)vals[t]), x[dst_of(k)]);
-                }
-            }
-            unsigned m = __ballot_sync(FULL, ok);
-            while (m) {
-                const int i = __ffs(m) - 1;
-                acc = __dadd_rn(acc, __shfl_sync(FULL, prod, i));
-                m &= m - 1;
-            }
-        }
-        if (lane == 0) y[u] = acc;
-    }
-}
-
 // ---------------------------------------------------------------- Graph
 
-Graph::Graph(const gpma_graph_config* cfg, int device, u64 nv_)
-    : pma(cfg ? &cfg->profile : nullptr, device), nv(nv_) {
+Graph::Graph(const gpma_graph_config* cfg, int device, u64 nv_, u64 lo_, u64 hi_)
+    : pma(cfg ? &cfg->profile : nullptr, device), nv(nv_), lo(lo_), hi(hi_ > nv_ ? nv_ : hi_) {
+    if (lo > hi) throw ApiError(PMA_EINVAL, "shard: need lo <= hi <= num_vertices");
     if (cfg) {
         if (cfg->engine != 0)
             throw ApiError(PMA_EINVAL, "GraphConfig.engine: only the segment engine (GPMA+) is provided");
         ecfg.eager = cfg->deletion_mode == PMA_EAGER;
         fill_target = cfg->fill_target;
     }
-    ro.reserve(nv + 1);
+    ro.reserve(nloc() + 1);
     pma.d_row_offsets = ro.ptr;
-    pma.num_vertices = nv;
+    pma.num_vertices = nloc();
+    pma.ro_lo = lo;
 }
 
 static void sort_pairs(cudaStream_t s, DevBuf<unsigned char>& tmpb, u64* kin, u64* kout, u32* vin, u32* vout, u64 n,
@@ -289,9 +237,14 @@ void Graph::from_edges_device(const u32* d_src, const u32* d_dst, const double* 
     uk.reserve(n + 1);
     uvv.reserve(n + 1);
     if (n > 0) {
-        k_pack_edges<<<grid_for(n, 256), 256, 0, s>>>(d_src, d_dst, n, k0.ptr, i0.ptr);
+        int nbits = 32 + bits_for(nv ? nv - 1 : 0);
+        if (is_shard()) {
+            k_pack_edges_shard<<<grid_for(n, 256), 256, 0, s>>>(d_src, d_dst, n, lo, hi, k0.ptr, i0.ptr);
+            nbits = 64;
+        } else {
+            k_pack_edges<<<grid_for(n, 256), 256, 0, s>>>(d_src, d_dst, n, k0.ptr, i0.ptr);
+        }
         GPMA_LAUNCH_CHECK();
-        const int nbits = 32 + bits_for(nv ? nv - 1 : 0);
         sort_pairs(s, tmp, k0.ptr, k1.ptr, i0.ptr, i1.ptr, n, nbits);
         // dedupe, last arrival wins (stable sort keeps arrival order)
         const u64* sk = k1.ptr;
@@ -300,7 +253,8 @@ void Graph::from_edges_device(const u32* d_src, const u32* d_dst, const double* 
         u64* ov_ = uvv.ptr;
         Ctr* c = ctr;
         run_compact(
-            s, pma.ws, nullptr, n, n, [=] __device__(ull i) { return i + 1 == n || sk[i + 1] != sk[i]; },
+            s, pma.ws, nullptr, n, n,
+            [=] __device__(ull i) { return (i + 1 == n || sk[i + 1] != sk[i]) && sk[i] != ~0ull; },
             [=] __device__(ull i, unsigned f, ull x) {
                 if (f) {
                     ok_[x] = sk[i];
@@ -311,11 +265,11 @@ void Graph::from_edges_device(const u32* d_src, const u32* d_dst, const double* 
         GPMA_CUDA(cudaMemcpyAsync(&ne, &ctr->n_unique, 8, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
     }
-    const u64 total = ne + nv;
+    const u64 total = ne + nloc();
     mk.reserve(total + 1);
     mv.reserve(total + 1);
     if (total > 0) {
-        k_place_guards<<<grid_for(total, 256), 256, 0, s>>>(uk.ptr, uvv.ptr, ne, nv, mk.ptr, mv.ptr);
+        k_place_guards<<<grid_for(total, 256), 256, 0, s>>>(uk.ptr, uvv.ptr, ne, lo, hi, mk.ptr, mv.ptr);
         GPMA_LAUNCH_CHECK();
     }
     pma.from_sorted_device(mk.ptr, mv.ptr, total, fill_target);
@@ -335,17 +289,37 @@ Graph::~Graph() {
 // DynamicGraph::apply_batch (graph.hpp:130-162)
 void Graph::apply_batch_device(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
                                u64 nd, pma_stats* out) {
+    apply_batch_impl(is, id, nullptr, iw, ni, ds, dd, nullptr, nd, out);
+}
+
+void Graph::apply_batch_keys_device(const u64* ik, const double* iw, u64 ni, const u64* dk, u64 nd, pma_stats* out) {
+    apply_batch_impl(nullptr, nullptr, ik, iw, ni, nullptr, nullptr, dk, nd, out);
+}
+
+void Graph::apply_batch_impl(const u32* is, const u32* id, const u64* ik, const double* iw, u64 ni, const u32* ds,
+                             const u32* dd, const u64* dk, u64 nd, pma_stats* out) {
     const u64 n = ni + nd;
     bk.reserve(n + 1);
     bv.reserve(n + 1);
     bo.reserve(n + 1);
-    GraphFront gf{is, id, iw, ni, ds, dd, nd, nv, bk.ptr, bv.ptr, bo.ptr};
+    GraphFront gf{is, id, iw, ni, ds, dd, nd, nv, lo, hi, ik, dk, bk.ptr, bv.ptr, bo.ptr};
     pma_stats st;
     pma.batch_update_device(nullptr, nullptr, nullptr, n, ecfg, &st, &gf);
     if (gf.bad_insert >= 0) {
         u32 bs = 0, bd = 0;
-        GPMA_CUDA(cudaMemcpy(&bs, is + gf.bad_insert, 4, cudaMemcpyDeviceToHost));
-        GPMA_CUDA(cudaMemcpy(&bd, id + gf.bad_insert, 4, cudaMemcpyDeviceToHost));
+        if (ik) {
+            u64 key = 0;
+            GPMA_CUDA(cudaMemcpy(&key, ik + gf.bad_insert, 8, cudaMemcpyDeviceToHost));
+            bs = src_of(key);
+            bd = dst_of(key);
+        } else {
+            GPMA_CUDA(cudaMemcpy(&bs, is + gf.bad_insert, 4, cudaMemcpyDeviceToHost));
+            GPMA_CUDA(cudaMemcpy(&bd, id + gf.bad_insert, 4, cudaMemcpyDeviceToHost));
+        }
+        if (is_shard() && bd < nv && bs < nv)
+            throw ApiError(PMA_EINVAL, "edge (" + std::to_string(bs) + ", " + std::to_string(bd) +
+                                           ") outside shard source range [" + std::to_string(lo) + ", " +
+                                           std::to_string(hi) + ")");
         throw ApiError(PMA_EINVAL, "edge (" + std::to_string(bs) + ", " + std::to_string(bd) +
                                        ") outside vertex range " + std::to_string(nv));
     }
@@ -355,11 +329,11 @@ void Graph::apply_batch_device(const u32* is, const u32* id, const double* iw, u
 }
 
 void Graph::row_offsets(u64* out) {
-    GPMA_CUDA(cudaMemcpyAsync(out, ro.ptr, (nv + 1) * 8, cudaMemcpyDeviceToHost, pma.stream()));
+    GPMA_CUDA(cudaMemcpyAsync(out, ro.ptr, (nloc() + 1) * 8, cudaMemcpyDeviceToHost, pma.stream()));
     GPMA_CUDA(cudaStreamSynchronize(pma.stream()));
 }
 
-u64 Graph::num_edges() const { return pma.valid_count - nv; }
+u64 Graph::num_edges() const { return pma.valid_count - nloc(); }
 
 void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
     cudaStream_t s = pma.stream();
@@ -367,7 +341,7 @@ void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
     DevBuf<u64> dro;
     DevBuf<u32> dcol;
     DevBuf<double> dval;
-    dro.reserve(nv + 1);
+    dro.reserve(nloc() + 1);
     dcol.reserve(ne + 1);
     dval.reserve(ne + 1);
     GPMA_CUDA(cudaMemsetAsync(dro.ptr, 0, 8, s));
@@ -378,6 +352,7 @@ void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
     u32* c = dcol.ptr;
     double* w = dval.ptr;
     const u64 cap = pma.capacity();
+    const u64 rlo = lo;
     if (cap > 0) {
         run_compact(
             s, pma.ws, nullptr, cap, cap,
@@ -387,12 +362,12 @@ void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
                     c[x] = dst_of(kk[t]);
                     w[x] = __longlong_as_double((long long)vv[t]);
                 } else if (ss[t] == kValid) {
-                    r[src_of(kk[t]) + 1] = x;  // guard of row u: entries of rows <= u
+                    r[src_of(kk[t]) - rlo + 1] = x;  // guard of row u: entries of rows <= u
                 }
             },
             NoFin{});
     }
-    if (h_ro) GPMA_CUDA(cudaMemcpyAsync(h_ro, dro.ptr, (nv + 1) * 8, cudaMemcpyDeviceToHost, s));
+    if (h_ro) GPMA_CUDA(cudaMemcpyAsync(h_ro, dro.ptr, (nloc() + 1) * 8, cudaMemcpyDeviceToHost, s));
     if (h_col && ne) GPMA_CUDA(cudaMemcpyAsync(h_col, dcol.ptr, ne * 4, cudaMemcpyDeviceToHost, s));
     if (h_val && ne) GPMA_CUDA(cudaMemcpyAsync(h_val, dval.ptr, ne * 8, cudaMemcpyDeviceToHost, s));
     GPMA_CUDA(cudaStreamSynchronize(s));
@@ -401,6 +376,7 @@ void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
 // ------------------------------------------------------------- analytics
 
 void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
+    if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     if (root >= nv) throw ApiError(PMA_EINVAL, "bfs: root outside vertex range");
     cudaStream_t s = pma.stream();
     GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
@@ -440,6 +416,7 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
 }
 
 void Graph::cc(u32* h_labels) {
+    if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     cudaStream_t s = pma.stream();
     GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
     dist.reserve(nv + 1);
@@ -457,6 +434,7 @@ void Graph::cc(u32* h_labels) {
 
 void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, double* h_ranks, u64* iters,
                      int* converged) {
+    if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     if (nv == 0) throw ApiError(PMA_EINVAL, "pagerank: empty vertex set");
     cudaStream_t s = pma.stream();
     GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
@@ -513,6 +491,7 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
 }
 
 void Graph::spmv(const double* h_x, double* h_y) {
+    if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     cudaStream_t s = pma.stream();
     px.reserve(nv + 1);
     py.reserve(nv + 1);

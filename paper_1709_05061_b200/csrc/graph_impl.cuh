@@ -7,10 +7,13 @@ namespace gpma {
 
 class Graph {
 public:
-    Graph(const gpma_graph_config* cfg, int device, u64 nv);
+    Graph(const gpma_graph_config* cfg, int device, u64 nv, u64 lo = 0, u64 hi = ~0ull);
     ~Graph();
     Pma pma;
-    u64 nv;
+    u64 nv;      // global vertex count (ids)
+    u64 lo, hi;  // owned source range: a shard of a key-range sharded graph, or [0, nv)
+    u64 nloc() const { return hi - lo; }
+    bool is_shard() const { return lo != 0 || hi != nv; }
     EngineCfg ecfg;
     double fill_target = 0.5;
     DevBuf<u64> ro;  // row offsets, |V| + 1 (graph.hpp:97)
@@ -26,6 +29,23 @@ public:
     void cc(u32* labels);
     void pagerank(double d, double eps, u64 max_iters, const double* warm, double* ranks, u64* iters, int* converged);
     void spmv(const double* x, double* y);
+
+    // key-range sharding (shard.cu): routing partition and the device steps of
+    // the sharded analytics (collectives run in the caller between them)
+    void route_partition(const u32* src, const u32* dst, const double* w, u64 n, const u32* d_bounds, int world,
+                         u64* okeys, double* ow, u64* h_counts);
+    // apply_batch with EdgeKey-packed updates (src << 32 | dst), as routed
+    void apply_batch_keys_device(const u64* ik, const double* iw, u64 ni, const u64* dk, u64 nd, pma_stats* out);
+    void apply_batch_impl(const u32* is, const u32* id, const u64* ik, const double* iw, u64 ni, const u32* ds,
+                          const u32* dd, const u64* dk, u64 nd, pma_stats* out);
+    void shard_bfs_mark(const u32* frontier, u32 nf, u8* flags);
+    void shard_bfs_update(const u8* flags, u32* dist_local, u32 depth, u32* next, u32* nf_out);
+    void shard_cc_hook(u32* labels);
+    void cc_jump(u32* labels, u64 n, const u32* prev, int* changed);
+    void shard_outdeg(u32* outdeg);
+    void shard_pr_push(const double* x, const u32* outdeg, double d, double* y);
+    void pr_finish(const double* x, double* y, u64 n, const u32* outdeg, double d, double* l1);
+    void shard_spmv(const double* x, double* y_local);
     double pr_iter_ms_ = 0.0;
     std::string err;
 
@@ -38,6 +58,8 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u8> bo;
     DevBuf<u32> dist, q0, q1, qn, outdeg;
     DevBuf<double> px, py, pshare, psc;
+    DevBuf<u32> rt_counts;
+    DevBuf<u64> rt_offsets, rt_totals;
     u32 h_nf_store_ = 0;
     u32* h_nf_ = &h_nf_store_;
     cudaEvent_t evs_[4]{};

@@ -217,13 +217,23 @@ __global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck,
         u32 s, d;
         bool ins = i < f.ni, skip = false;
         if (ins) {
-            s = f.is[i];
-            d = f.id[i];
-            if (s >= f.nv || d >= f.nv) bad = max(bad, ~ull(i));  // first offending insert
+            if (f.ik) {
+                s = src_of(f.ik[i]);
+                d = dst_of(f.ik[i]);
+            } else {
+                s = f.is[i];
+                d = f.id[i];
+            }
+            if (s < f.lo || s >= f.hi || d >= f.nv) bad = max(bad, ~ull(i));  // first offending insert
         } else {
             const u64 j = i - f.ni;
-            s = f.ds[j];
-            d = f.dd[j];
+            if (f.dk) {
+                s = src_of(f.dk[j]);
+                d = dst_of(f.dk[j]);
+            } else {
+                s = f.ds[j];
+                d = f.dd[j];
+            }
             skip = d == u32(kGuardDst);
             guards += skip;
         }
@@ -277,14 +287,14 @@ __global__ void k_leaf_search(const u64* __restrict__ uk, const ull* n_dev, cons
 // log2(C/16)-level descent.  Other keys (plain PMAs, ids >= |V|) take the
 // uniform descent; keys are in order across the warp either way.
 __global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_dev, const u64* __restrict__ hdr, u64 L,
-                                     const u8* __restrict__ st, u64 leaf, const u64* __restrict__ ro, u64 nv,
-                                     u32* __restrict__ ul) {
+                                     const u8* __restrict__ st, u64 leaf, const u64* __restrict__ ro, u64 rlo,
+                                     u64 rhi, u32* __restrict__ ul) {
     const u64 n = *n_dev;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         const u64 key = uk[i];
         const u64 u = key >> 32;
         u64 out;
-        if (ro && u < nv && !is_guard(key)) {
+        if (ro && u >= rlo && u < rhi && !is_guard(key)) {
             const u64 a = __ldg(&ro[u]), b = __ldg(&ro[u + 1]);
             u64 lo = a ? (a - 1) / leaf : 0;  // hdr[lo] <= guard(u - 1) < key (or lo == 0)
             u64 hi = (b - 1) / leaf + 1;      // hdr[hi] > guard(u) > key (or hi == L)
@@ -1371,7 +1381,7 @@ void Pma::download(u64* keys, u64* values, u8* states) {
 void Pma::rebuild_row_offsets_full() {
     if (!d_row_offsets) return;
     GPMA_CUDA(cudaMemsetAsync(d_row_offsets, 0, (num_vertices + 1) * 8, stream_));
-    k_row_offsets_full<<<grid_for(cap_, 256, 148 * 16), 256, 0, stream_>>>(d_keys, d_st, cap_, d_row_offsets);
+    k_row_offsets_full<<<grid_for(cap_, 256, 148 * 16), 256, 0, stream_>>>(d_keys, d_st, cap_, ro_base());
     GPMA_LAUNCH_CHECK();
 }
 
@@ -1567,7 +1577,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         ++launches;
         // leaf assignment (pma.hpp:234-289), once per batch
         k_leaf_search_sorted<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
-            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, d_row_offsets, num_vertices, ul.ptr);
+            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices,
+            ul.ptr);
         GPMA_LAUNCH_CHECK();
         ++launches;
     }
@@ -1589,15 +1600,17 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             Ctr* ctr = d_ctr;
             run_compact(
                 stream_, ws, nullptr, n, n,
-                [=] __device__(ull i) { return i < f.ni || f.dd[i - f.ni] != u32(kGuardDst); },
+                [=] __device__(ull i) {
+                    return i < f.ni || (f.dk ? dst_of(f.dk[i - f.ni]) : f.dd[i - f.ni]) != u32(kGuardDst);
+                },
                 [=] __device__(ull i, unsigned fl, ull x) {
                     if (!fl) return;
                     if (i < f.ni) {
-                        bk[x] = pack_edge(f.is[i], f.id[i]);
+                        bk[x] = f.ik ? f.ik[i] : pack_edge(f.is[i], f.id[i]);
                         bv[x] = u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0));
                         bo[x] = kOpInsert;
                     } else {
-                        bk[x] = pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
+                        bk[x] = f.dk ? f.dk[i - f.ni] : pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
                         bv[x] = 0;
                         bo[x] = kOpDelete;
                     }
@@ -1680,7 +1693,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             a.gflag = gflag.ptr;
             a.ctr = d_ctr;
             a.hdr = d_hdr;
-            a.ro = d_row_offsets;
+            a.ro = ro_base();
             a.rlist = rlist.ptr;
             a.level = level;
             a.m = m;
@@ -1976,7 +1989,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         const u64 nref = h_ctr->nrefresh;
         if (nref > 0) {
             k_refresh_ranges<<<grid_for(nref * 32, 256, 148 * 16), 256, 0, stream_>>>(
-                rlist.ptr, nullptr, nref, d_keys, d_st, cap_, leaf_, d_hdr, d_row_offsets);
+                rlist.ptr, nullptr, nref, d_keys, d_st, cap_, leaf_, d_hdr, ro_base());
             GPMA_LAUNCH_CHECK();
             ++launches;
         }

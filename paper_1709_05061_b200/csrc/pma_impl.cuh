@@ -95,6 +95,9 @@ struct GraphFront {
     const u32* dd;
     u64 nd;
     u64 nv;
+    u64 lo, hi;  // owned source range (a shard; [0, nv) for a whole graph)
+    const u64* ik = nullptr;  // EdgeKey-packed inserts / deletes instead of (src, dst) arrays
+    const u64* dk = nullptr;
     u64* bk;
     u64* bv;
     u8* bo;
@@ -139,8 +142,12 @@ public:
 
     // row-offset maintenance hook used by the graph (graph.hpp:167-190):
     // when non-null, every refresh also rewrites ro[src+1] for guards.
-    u64* d_row_offsets = nullptr;
+    u64* d_row_offsets = nullptr;  // rows [ro_lo, ro_lo + num_vertices) of a graph (shard)
     u64 num_vertices = 0;
+    u64 ro_lo = 0;
+    // row-offset array indexed by GLOBAL source id (ro_base()[src + 1]): a
+    // shard's array starts at its first owned vertex
+    u64* ro_base() const { return d_row_offsets ? d_row_offsets - ro_lo : nullptr; }
     void rebuild_row_offsets_full();
     SeqArgs seq_args(int op);
 

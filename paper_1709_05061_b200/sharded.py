@@ -1,0 +1,389 @@
+"""Key-range sharded GPMA+ across GPUs — the device data path.
+
+One GPMA+ per GPU holds the edges whose source lies in its range [lo, hi)
+(keys are ``src << 32 | dst``, so a source range is a key range: segments never
+cross shards, every round / density decision / rebalance is shard-local) plus
+the guards of its vertices.  What crosses GPUs:
+
+* update routing, once per batch: every rank holds a contiguous share of the
+  global batch (its arrivals); ``gpma_route_partition`` stably partitions it by
+  owner on the device into EdgeKey words, then one variable-size all-to-all
+  (counts first) per op type moves them to the owners.  Chunks arrive in
+  sender-rank order, so every key keeps its global arrival order and "last
+  insert wins" (segment_engine.hpp:346-363) resolves as on one GPU;
+* BFS: per level the owners mark the out-neighbours of their frontier in a
+  |V|-byte flag array, one MAX all-reduce, owners admit their unreached
+  flagged vertices (owner-computes, analytics.hpp:22-48);
+* CC: min-label propagation over replicated labels, one MIN all-reduce per
+  round + pointer jumping (analytics.hpp:53-82; fixpoint = component minima);
+* PageRank: owners push over their edges, one SUM all-reduce of y per
+  iteration, replicated finish (analytics.hpp:84-143);
+* SpMV: owners compute their rows, one all-gather (analytics.hpp:147-158).
+
+Collectives go through a ``Comm`` over a LIST of local shards:
+``TorchComm`` = one shard per process, torch.distributed (NCCL on GPUs);
+``LocalComm`` = every shard in this process (tests on one GPU: the same code
+path, collectives as loops).  Every library call is synchronous on its own
+stream; tensors produced by torch ops are synchronised before the library
+reads them.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from .abi import load_library, pma_stats
+from .pmagraph import GraphConfig, UpdateStats, _raise
+
+UNREACHED = 0xFFFFFFFF
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _vp(t):
+    return C.c_void_p(t.data_ptr()) if t is not None and t.numel() else None
+
+
+def _sync(t):
+    torch = _torch()
+    if t.is_cuda:
+        torch.cuda.current_stream(t.device).synchronize()
+
+
+# ------------------------------------------------------------------ comms
+
+class LocalComm:
+    """All shards in this process; collectives are reductions over the list."""
+
+    def __init__(self, world: int):
+        self.world = world
+        self.ranks = list(range(world))
+
+    def all_reduce(self, ts, op: str):
+        torch = _torch()
+        acc = ts[0].clone()
+        for t in ts[1:]:
+            if op == "sum":
+                acc += t
+            elif op == "max":
+                acc = torch.maximum(acc, t)
+            elif op == "min":
+                acc = torch.minimum(acc, t)
+            else:
+                raise ValueError(op)
+        for t in ts:
+            t.copy_(acc)
+
+    def all_to_all_v(self, sends, send_counts):
+        """sends[i]: local rank i's buffer, owner-major; send_counts[i][r]:
+        elements for rank r.  Returns per local rank the received buffer
+        (sender-rank order) and its per-sender counts."""
+        torch = _torch()
+        offs = [np.concatenate([[0], np.cumsum(c)]) for c in send_counts]
+        recvs, rcounts = [], []
+        for r in range(self.world):
+            parts = [sends[s][int(offs[s][r]):int(offs[s][r + 1])] for s in range(self.world)]
+            recvs.append(torch.cat(parts) if parts else sends[r][:0])
+            rcounts.append([int(send_counts[s][r]) for s in range(self.world)])
+        return recvs, rcounts
+
+    def all_gather_v(self, pieces):
+        torch = _torch()
+        full = torch.cat(pieces)
+        return [full.clone() for _ in pieces]
+
+
+class TorchComm:
+    """One shard per process over torch.distributed (NCCL between GPUs)."""
+
+    _OPS = {"sum": "SUM", "max": "MAX", "min": "MIN"}
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.ranks = [dist.get_rank(group)]
+
+    def all_reduce(self, ts, op: str):
+        (t,) = ts
+        self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, self._OPS[op]), group=self.group)
+
+    def all_to_all_v(self, sends, send_counts):
+        torch = _torch()
+        (buf,), (cnt,) = sends, send_counts
+        sc = torch.as_tensor(np.asarray(cnt, np.int64), device=buf.device)
+        rc = torch.empty_like(sc)
+        self.dist.all_to_all_single(rc, sc, group=self.group)
+        rcl = [int(x) for x in rc.cpu()]
+        out = torch.empty(sum(rcl), dtype=buf.dtype, device=buf.device)
+        self.dist.all_to_all_single(out, buf, output_split_sizes=rcl, input_split_sizes=[int(x) for x in cnt],
+                                    group=self.group)
+        return [out], [rcl]
+
+    def all_gather_v(self, pieces):
+        torch = _torch()
+        (p,) = pieces
+        n = torch.tensor([p.numel()], device=p.device)
+        ns = [torch.empty_like(n) for _ in range(self.world)]
+        self.dist.all_gather(ns, n, group=self.group)
+        m = int(max(int(x) for x in ns))
+        pad = torch.zeros(m, dtype=p.dtype, device=p.device)
+        pad[:p.numel()] = p
+        outs = [torch.empty_like(pad) for _ in range(self.world)]
+        self.dist.all_gather(outs, pad, group=self.group)
+        return [torch.cat([o[:int(k)] for o, k in zip(outs, ns)])]
+
+
+# ------------------------------------------------------------------ graph
+
+@dataclass
+class ShardStats:
+    stats: list          # UpdateStats of every local shard
+    routed: list         # updates each local shard received
+    sent: list           # updates each local shard sent to other ranks
+
+
+class ShardedGraph:
+    """Key-range sharded DynamicGraph; `shards[i]` is local rank comm.ranks[i]."""
+
+    def __init__(self, comm, num_vertices: int, bounds, handles, devices):
+        self.comm = comm
+        self.nv = int(num_vertices)
+        self.bounds = np.asarray(bounds, np.int64)
+        self.h = handles
+        self.devices = devices
+        self._lib = load_library()
+        torch = _torch()
+        self._dbounds = [torch.as_tensor(self.bounds.astype(np.uint32).view(np.int32), device=f"cuda:{d}")
+                         for d in devices]
+
+    # ---- construction
+    @classmethod
+    def from_edges_device(cls, comm, num_vertices: int, bounds, edges, config: GraphConfig | None = None,
+                          devices=None):
+        """edges[i] = (src, dst, weights|None) device tensors given to local
+        rank i — typically the same global edge list: each shard keeps the
+        edges of its own sources (gpma_shard_from_edges_device)."""
+        lib = load_library()
+        bounds = np.asarray(bounds, np.int64)
+        devices = devices if devices is not None else [e[0].device.index for e in edges]
+        cfg = (config or GraphConfig()).c()
+        hs = []
+        for i, r in enumerate(comm.ranks):
+            s, d, w = edges[i]
+            _sync(s)
+            h = C.c_void_p()
+            rc = lib.gpma_shard_from_edges_device(C.byref(cfg), devices[i], num_vertices, int(bounds[r]),
+                                                  int(bounds[r + 1]), _vp(s), _vp(d), _vp(w), s.numel(), C.byref(h))
+            if rc:
+                _raise(rc, lib.gpma_last_error(None).decode())
+            hs.append(h)
+        return cls(comm, num_vertices, bounds, hs, devices)
+
+    def __del__(self):
+        for h in getattr(self, "h", []) or []:
+            if h:
+                self._lib.gpma_destroy(h)
+        self.h = []
+
+    def _check(self, i, rc):
+        if rc:
+            _raise(rc, self._lib.gpma_last_error(self.h[i]).decode())
+
+    def range(self, i):
+        r = self.comm.ranks[i]
+        return int(self.bounds[r]), int(self.bounds[r + 1])
+
+    # ---- updates
+    def _route(self, i, src, dst, w):
+        torch = _torch()
+        n = src.numel()
+        keys = torch.empty(max(n, 1), dtype=torch.int64, device=src.device)
+        ow = torch.empty(max(n, 1), dtype=torch.float64, device=src.device) if w is not None else None
+        counts = (C.c_uint64 * self.comm.world)()
+        _sync(src)
+        self._check(i, self._lib.gpma_route_partition(self.h[i], _vp(src), _vp(dst), _vp(w), n,
+                                                       _vp(self._dbounds[i]), self.comm.world, _vp(keys), _vp(ow),
+                                                       counts))
+        return keys[:n], (ow[:n] if ow is not None else None), [int(c) for c in counts]
+
+    def apply_batch(self, slices) -> ShardStats:
+        """slices[i] = (ins_src, ins_dst, ins_w|None, del_src, del_dst):
+        local rank i's share of the global batch (device tensors, u32 ids as
+        int32).  Routes every update to its owner and applies the routed
+        batch to each shard (DynamicGraph::apply_batch, graph.hpp:130-162)."""
+        L = len(self.h)
+        ik, iw, ic, dk, dc = [], [], [], [], []
+        for i in range(L):
+            a, b, w, c, d = slices[i]
+            k, ww, cnt = self._route(i, a, b, w)
+            ik.append(k)
+            iw.append(ww)
+            ic.append(cnt)
+            k2, _, cnt2 = self._route(i, c, d, None)
+            dk.append(k2)
+            dc.append(cnt2)
+        rik, _ = self.comm.all_to_all_v(ik, ic)
+        riw = self.comm.all_to_all_v(iw, ic)[0] if iw[0] is not None else [None] * L
+        rdk, _ = self.comm.all_to_all_v(dk, dc)
+        out, routed, sent = [], [], []
+        for i in range(L):
+            st = pma_stats()
+            _sync(rik[i])
+            _sync(rdk[i])
+            self._check(i, self._lib.gpma_apply_batch_keys_device(self.h[i], _vp(rik[i]), _vp(riw[i]), rik[i].numel(),
+                                                                   _vp(rdk[i]), rdk[i].numel(), C.byref(st)))
+            out.append(UpdateStats.from_c(st))
+            routed.append(rik[i].numel() + rdk[i].numel())
+            me = self.comm.ranks[i]
+            sent.append(sum(ic[i]) - ic[i][me] + sum(dc[i]) - dc[i][me])
+        return ShardStats(out, routed, sent)
+
+    # ---- analytics
+    def bfs(self, root: int):
+        """Level-synchronous BFS (analytics.hpp:22-48); dist[v] = level,
+        UNREACHED = 0xFFFFFFFF.  Returns the full |V| vector per local rank."""
+        torch = _torch()
+        L = len(self.h)
+        if not 0 <= root < self.nv:
+            raise ValueError("bfs: root outside vertex range")
+        dist, fr, nx, flags, nf = [], [], [], [], []
+        for i in range(L):
+            lo, hi = self.range(i)
+            dev = f"cuda:{self.devices[i]}"
+            dl = torch.full((max(hi - lo, 1),), -1, dtype=torch.int32, device=dev)
+            f = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=dev)
+            n = 0
+            if lo <= root < hi:
+                dl[root - lo] = 0
+                f[0] = root
+                n = 1
+            dist.append(dl)
+            fr.append(f)
+            nx.append(torch.empty_like(f))
+            flags.append(torch.empty(self.nv, dtype=torch.uint8, device=dev))
+            nf.append(n)
+        depth = 0
+        while True:
+            for i in range(L):
+                _sync(fr[i])
+                self._check(i, self._lib.gpma_shard_bfs_mark(self.h[i], _vp(fr[i]), nf[i], _vp(flags[i])))
+            self.comm.all_reduce(flags, "max")
+            depth += 1
+            tot = []
+            for i in range(L):
+                _sync(flags[i])
+                c = C.c_uint32(0)
+                self._check(i, self._lib.gpma_shard_bfs_update(self.h[i], _vp(flags[i]), _vp(dist[i]), depth,
+                                                                _vp(nx[i]), C.byref(c)))
+                nf[i] = c.value
+                tot.append(torch.tensor([c.value], dtype=torch.int64, device=flags[i].device))
+            self.comm.all_reduce(tot, "sum")
+            fr, nx = nx, fr
+            if int(tot[0].item()) == 0:
+                break
+        pieces = [dist[i][:self.range(i)[1] - self.range(i)[0]] for i in range(L)]
+        return self.comm.all_gather_v(pieces)
+
+    def connected_components(self):
+        """Labels = minimum vertex id of each (undirected) component
+        (analytics.hpp:53-82)."""
+        torch = _torch()
+        L = len(self.h)
+        lab = [torch.arange(self.nv, dtype=torch.int32, device=f"cuda:{d}") for d in self.devices]
+        rounds = 0
+        while True:
+            prev = [t.clone() for t in lab]
+            for i in range(L):
+                _sync(lab[i])
+                self._check(i, self._lib.gpma_shard_cc_hook(self.h[i], _vp(lab[i])))
+            self.comm.all_reduce(lab, "min")
+            ch = []
+            for i in range(L):
+                _sync(lab[i])
+                c = C.c_int(0)
+                self._check(i, self._lib.gpma_cc_jump(self.h[i], _vp(lab[i]), self.nv, _vp(prev[i]), C.byref(c)))
+                ch.append(torch.tensor([c.value], dtype=torch.int32, device=lab[i].device))
+            self.comm.all_reduce(ch, "max")
+            rounds += 1
+            if int(ch[0].item()) == 0:
+                break
+        self.cc_rounds = rounds
+        return lab
+
+    def pagerank(self, damping: float = 0.85, epsilon: float = 1e-3, max_iters: int = 200, warm_start=None):
+        """Power iteration (analytics.hpp:84-143); returns (ranks per local
+        rank, iterations, converged) with the reference's stopping rule."""
+        torch = _torch()
+        L = len(self.h)
+        n = self.nv
+        if n == 0:
+            raise ValueError("pagerank: empty vertex set")
+        od, x, y = [], [], []
+        for i in range(L):
+            dev = f"cuda:{self.devices[i]}"
+            o = torch.empty(n, dtype=torch.int32, device=dev)
+            self._check(i, self._lib.gpma_shard_outdeg(self.h[i], _vp(o)))
+            od.append(o)
+            if warm_start is not None:
+                xi = torch.as_tensor(np.asarray(warm_start, np.float64), device=dev).clone()
+            else:
+                xi = torch.full((n,), 1.0 / n, dtype=torch.float64, device=dev)
+            x.append(xi)
+            y.append(torch.empty(n, dtype=torch.float64, device=dev))
+        self.comm.all_reduce(od, "sum")
+        converged = False
+        it = 0
+        for it in range(1, max_iters + 1):
+            for i in range(L):
+                _sync(x[i])
+                _sync(od[i])
+                self._check(i, self._lib.gpma_shard_pr_push(self.h[i], _vp(x[i]), _vp(od[i]), damping, _vp(y[i])))
+            self.comm.all_reduce(y, "sum")
+            l1 = C.c_double(0)
+            for i in range(L):
+                _sync(y[i])
+                self._check(i, self._lib.gpma_pr_finish(self.h[i], _vp(x[i]), _vp(y[i]), n, _vp(od[i]), damping,
+                                                        C.byref(l1)))
+            x, y = y, x
+            if l1.value < epsilon:
+                converged = True
+                break
+        return x, (it if converged else max_iters), converged
+
+    def spmv(self, x):
+        """y = A x (analytics.hpp:147-158): owners compute their rows with the
+        single-GPU ordered accumulation, one all-gather."""
+        torch = _torch()
+        L = len(self.h)
+        pieces = []
+        for i in range(L):
+            lo, hi = self.range(i)
+            dev = f"cuda:{self.devices[i]}"
+            xi = x.to(dev) if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, np.float64), device=dev)
+            yl = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
+            _sync(xi)
+            self._check(i, self._lib.gpma_shard_spmv(self.h[i], _vp(xi), _vp(yl)))
+            pieces.append(yl[:hi - lo])
+        return self.comm.all_gather_v(pieces)
+
+    # ---- inspection (tests)
+    def shard_slots(self, i):
+        from .pmagraph import PackedMemoryArray
+        p = PackedMemoryArray(_handle=self._lib.gpma_pma(self.h[i]), _owner=self)
+        return p.slots()
+
+    def shard_row_offsets(self, i):
+        lo, hi = self.range(i)
+        out = np.zeros(hi - lo + 1, np.uint64)
+        self._check(i, self._lib.gpma_row_offsets(self.h[i], out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def num_edges(self):
+        return [int(self._lib.gpma_num_edges(h)) for h in self.h]
