@@ -292,19 +292,23 @@ int gpma_shard_from_edges_device(const gpma_graph_config* cfg, int device, size_
                                  size_t n, gpma_graph** out);
 int gpma_shard_range(const gpma_graph* g, uint64_t* lo, uint64_t* hi);
 
-/* Routing: stable partition of n device-resident updates by owner rank
- * (d_bounds[r] <= src < d_bounds[r+1], world + 1 entries, world <= 64; ids
- * >= |V| go to the last rank) as EdgeKeys into d_out_keys (owner-major,
- * arrival order kept inside each owner); counts[r] (host) = updates for rank
- * r.  d_w / d_out_w may be NULL. */
-int gpma_route_partition(gpma_graph* g, const uint32_t* d_src, const uint32_t* d_dst, const double* d_w, size_t n,
-                         const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
-                         uint64_t* counts);
+/* Routing: one rank's share of a batch (inserts then deletes, device
+ * arrays) stably partitioned by owner rank (d_bounds[r] <= src <
+ * d_bounds[r+1], world + 1 entries, world <= 64; ids >= |V| go to the last
+ * rank) into EdgeKeys d_out_keys (owner-major, arrival order kept inside each
+ * owner; bit 63 set on deletes, so |V| <= 2^31), with the insert weights in
+ * d_out_w (NULL: none; deletes get 1.0); counts[r] (host) = updates for rank
+ * r.  One all-to-all of these words (8 B / update) is the whole exchange. */
+int gpma_route_batch(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
+                     size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
+                     const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w, uint64_t* counts);
 
-/* DynamicGraph::apply_batch (graph.hpp:130-162) with EdgeKey-packed device
- * updates (key = src << 32 | dst, graph.hpp:27-37) — the routed form. */
-int gpma_apply_batch_keys_device(gpma_graph* g, const uint64_t* d_ins_keys, const double* d_ins_w, size_t n_ins,
-                                 const uint64_t* d_del_keys, size_t n_del, pma_stats* stats);
+/* DynamicGraph::apply_batch (graph.hpp:130-162) on a routed batch: n
+ * EdgeKeys with bit 63 = delete (inserts keep their arrival order among
+ * themselves, which is all "last insert wins" needs), weights d_w (NULL =
+ * 1.0) parallel to the keys. */
+int gpma_apply_batch_routed_device(gpma_graph* g, const uint64_t* d_keys, const double* d_w, size_t n,
+                                   pma_stats* stats);
 
 /* BFS (analytics.hpp:22-48), one level: mark (flags[v] = 1, |V| bytes,
  * zeroed by the call) the out-neighbours of the owned frontier vertices; the

@@ -205,8 +205,8 @@ SIGNATURES = [
     ("pma_cuda_stream", _P, [_P]),
     ("gpma_shard_from_edges_device", C.c_int, [C.POINTER(gpma_graph_config), C.c_int, C.c_size_t, C.c_uint32, C.c_uint32, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
     ("gpma_shard_range", C.c_int, [_P, _U64P, _U64P]),
-    ("gpma_route_partition", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, C.c_int, _P, _P, _U64P]),
-    ("gpma_apply_batch_keys_device", C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_size_t, C.POINTER(pma_stats)]),
+    ("gpma_route_batch", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, _P, C.c_int, _P, _P, _U64P]),
+    ("gpma_apply_batch_routed_device", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
     ("gpma_shard_bfs_mark", C.c_int, [_P, _P, C.c_uint32, _P]),
     ("gpma_shard_bfs_update", C.c_int, [_P, _P, _P, C.c_uint32, _P, C.POINTER(C.c_uint32)]),
     ("gpma_shard_cc_hook", C.c_int, [_P, _P]),

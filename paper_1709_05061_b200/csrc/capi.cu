@@ -411,20 +411,21 @@ int gpma_shard_range(const gpma_graph* g, uint64_t* lo, uint64_t* hi) {
     return PMA_OK;
 }
 
-int gpma_route_partition(gpma_graph* g, const uint32_t* d_src, const uint32_t* d_dst, const double* d_w, size_t n,
-                         const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
-                         uint64_t* counts) {
+int gpma_route_batch(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
+                     size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
+                     const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w, uint64_t* counts) {
     return guarded(err_of(g), [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
-        g->impl->route_partition(d_src, d_dst, d_w, n, d_bounds, world, d_out_keys, d_out_w, counts);
+        g->impl->route_partition(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, d_bounds, world,
+                                 d_out_keys, d_out_w, counts);
     });
 }
 
-int gpma_apply_batch_keys_device(gpma_graph* g, const uint64_t* d_ins_keys, const double* d_ins_w, size_t n_ins,
-                                 const uint64_t* d_del_keys, size_t n_del, pma_stats* stats) {
+int gpma_apply_batch_routed_device(gpma_graph* g, const uint64_t* d_keys, const double* d_w, size_t n,
+                                   pma_stats* stats) {
     return guarded(err_of(g), [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
-        g->impl->apply_batch_keys_device(d_ins_keys, d_ins_w, n_ins, d_del_keys, n_del, stats);
+        g->impl->apply_batch_mixed_device(d_keys, d_w, n, stats);
     });
 }
 

@@ -289,27 +289,28 @@ Graph::~Graph() {
 // DynamicGraph::apply_batch (graph.hpp:130-162)
 void Graph::apply_batch_device(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
                                u64 nd, pma_stats* out) {
-    apply_batch_impl(is, id, nullptr, iw, ni, ds, dd, nullptr, nd, out);
+    apply_batch_impl(is, id, nullptr, iw, ni, ds, dd, nd, out);
 }
 
-void Graph::apply_batch_keys_device(const u64* ik, const double* iw, u64 ni, const u64* dk, u64 nd, pma_stats* out) {
-    apply_batch_impl(nullptr, nullptr, ik, iw, ni, nullptr, nullptr, dk, nd, out);
+void Graph::apply_batch_mixed_device(const u64* keys, const double* w, u64 n, pma_stats* out) {
+    if (nv > (1ull << 31)) throw ApiError(PMA_EINVAL, "apply_batch_mixed: vertex ids must be < 2^31");
+    apply_batch_impl(nullptr, nullptr, keys, w, n, nullptr, nullptr, 0, out);
 }
 
-void Graph::apply_batch_impl(const u32* is, const u32* id, const u64* ik, const double* iw, u64 ni, const u32* ds,
-                             const u32* dd, const u64* dk, u64 nd, pma_stats* out) {
+void Graph::apply_batch_impl(const u32* is, const u32* id, const u64* mk, const double* iw, u64 ni, const u32* ds,
+                             const u32* dd, u64 nd, pma_stats* out) {
     const u64 n = ni + nd;
     bk.reserve(n + 1);
     bv.reserve(n + 1);
     bo.reserve(n + 1);
-    GraphFront gf{is, id, iw, ni, ds, dd, nd, nv, lo, hi, ik, dk, bk.ptr, bv.ptr, bo.ptr};
+    GraphFront gf{is, id, iw, ni, ds, dd, nd, nv, lo, hi, mk, bk.ptr, bv.ptr, bo.ptr};
     pma_stats st;
     pma.batch_update_device(nullptr, nullptr, nullptr, n, ecfg, &st, &gf);
     if (gf.bad_insert >= 0) {
         u32 bs = 0, bd = 0;
-        if (ik) {
+        if (mk) {
             u64 key = 0;
-            GPMA_CUDA(cudaMemcpy(&key, ik + gf.bad_insert, 8, cudaMemcpyDeviceToHost));
+            GPMA_CUDA(cudaMemcpy(&key, mk + gf.bad_insert, 8, cudaMemcpyDeviceToHost));
             bs = src_of(key);
             bd = dst_of(key);
         } else {

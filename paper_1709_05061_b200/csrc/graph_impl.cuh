@@ -32,12 +32,12 @@ public:
 
     // key-range sharding (shard.cu): routing partition and the device steps of
     // the sharded analytics (collectives run in the caller between them)
-    void route_partition(const u32* src, const u32* dst, const double* w, u64 n, const u32* d_bounds, int world,
-                         u64* okeys, double* ow, u64* h_counts);
-    // apply_batch with EdgeKey-packed updates (src << 32 | dst), as routed
-    void apply_batch_keys_device(const u64* ik, const double* iw, u64 ni, const u64* dk, u64 nd, pma_stats* out);
-    void apply_batch_impl(const u32* is, const u32* id, const u64* ik, const double* iw, u64 ni, const u32* ds,
-                          const u32* dd, const u64* dk, u64 nd, pma_stats* out);
+    void route_partition(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
+                         u64 nd, const u32* d_bounds, int world, u64* okeys, double* ow, u64* h_counts);
+    // apply_batch with routed EdgeKeys, bit 63 = delete (arrival order kept among inserts)
+    void apply_batch_mixed_device(const u64* keys, const double* w, u64 n, pma_stats* out);
+    void apply_batch_impl(const u32* is, const u32* id, const u64* mk, const double* iw, u64 ni, const u32* ds,
+                          const u32* dd, u64 nd, pma_stats* out);
     void shard_bfs_mark(const u32* frontier, u32 nf, u8* flags);
     void shard_bfs_update(const u8* flags, u32* dist_local, u32 depth, u32* next, u32* nf_out);
     void shard_cc_hook(u32* labels);

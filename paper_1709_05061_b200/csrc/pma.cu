@@ -215,25 +215,24 @@ __global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck,
     ull guards = 0, bad = 0, oor = 0;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         u32 s, d;
-        bool ins = i < f.ni, skip = false;
+        bool ins, skip = false;
+        if (f.mk) {
+            const u64 k = f.mk[i];
+            ins = !(k >> 63);
+            s = src_of(k) & 0x7FFFFFFFu;
+            d = dst_of(k);
+        } else if (i < f.ni) {
+            ins = true;
+            s = f.is[i];
+            d = f.id[i];
+        } else {
+            ins = false;
+            s = f.ds[i - f.ni];
+            d = f.dd[i - f.ni];
+        }
         if (ins) {
-            if (f.ik) {
-                s = src_of(f.ik[i]);
-                d = dst_of(f.ik[i]);
-            } else {
-                s = f.is[i];
-                d = f.id[i];
-            }
             if (s < f.lo || s >= f.hi || d >= f.nv) bad = max(bad, ~ull(i));  // first offending insert
         } else {
-            const u64 j = i - f.ni;
-            if (f.dk) {
-                s = src_of(f.dk[j]);
-                d = dst_of(f.dk[j]);
-            } else {
-                s = f.ds[j];
-                d = f.dd[j];
-            }
             skip = d == u32(kGuardDst);
             guards += skip;
         }
@@ -1443,7 +1442,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         nbits = 2 * db + 1;  // + the skip bit (guard deletes sort last)
         int ib = 1;
         while ((1ull << ib) < n) ++ib;
-        if (nbits + ib > 64) ib = 0;  // no room: key + index payload pairs
+        if (nbits + ib > 64 || gf->mk) ib = 0;  // no room (or ops not index-ordered): key + payload pairs
         packed_ib = ib;
         k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
@@ -1601,19 +1600,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             run_compact(
                 stream_, ws, nullptr, n, n,
                 [=] __device__(ull i) {
-                    return i < f.ni || (f.dk ? dst_of(f.dk[i - f.ni]) : f.dd[i - f.ni]) != u32(kGuardDst);
+                    if (f.mk) return !(f.mk[i] >> 63) || dst_of(f.mk[i]) != u32(kGuardDst);
+                    return i < f.ni || f.dd[i - f.ni] != u32(kGuardDst);
                 },
                 [=] __device__(ull i, unsigned fl, ull x) {
                     if (!fl) return;
-                    if (i < f.ni) {
-                        bk[x] = f.ik ? f.ik[i] : pack_edge(f.is[i], f.id[i]);
-                        bv[x] = u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0));
-                        bo[x] = kOpInsert;
-                    } else {
-                        bk[x] = f.dk ? f.dk[i - f.ni] : pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
-                        bv[x] = 0;
-                        bo[x] = kOpDelete;
-                    }
+                    const bool ins = f.mk ? !(f.mk[i] >> 63) : i < f.ni;
+                    if (f.mk) bk[x] = f.mk[i] & ~(1ull << 63);
+                    else bk[x] = ins ? pack_edge(f.is[i], f.id[i]) : pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
+                    bv[x] = ins ? u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0)) : 0;
+                    bo[x] = ins ? kOpInsert : kOpDelete;
                 },
                 [=] __device__(ull total) { ctr->nt = total; });
             sync_ctr();

@@ -96,8 +96,7 @@ struct GraphFront {
     u64 nd;
     u64 nv;
     u64 lo, hi;  // owned source range (a shard; [0, nv) for a whole graph)
-    const u64* ik = nullptr;  // EdgeKey-packed inserts / deletes instead of (src, dst) arrays
-    const u64* dk = nullptr;
+    const u64* mk = nullptr;  // routed EdgeKeys (bit 63 = delete), ni of them, instead of the arrays
     u64* bk;
     u64* bv;
     u8* bo;

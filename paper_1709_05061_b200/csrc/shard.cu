@@ -25,6 +25,22 @@ constexpr int kRouteItems = 8;
 constexpr int kRouteTile = kRouteThreads * kRouteItems;
 constexpr int kMaxWorld = 64;
 
+// One rank's share of a batch: inserts then deletes (graph.hpp:133-147).
+struct RouteIn {
+    const u32* is;
+    const u32* id;
+    const double* iw;
+    u64 ni;
+    const u32* ds;
+    const u32* dd;
+    u64 nd;
+    __device__ __forceinline__ u32 src(u64 i) const { return i < ni ? is[i] : ds[i - ni]; }
+    // EdgeKey on the wire; bit 63 marks a delete (ids < 2^31)
+    __device__ __forceinline__ u64 key(u64 i) const {
+        return i < ni ? pack_edge(is[i], id[i]) : (pack_edge(ds[i - ni], dd[i - ni]) | (1ull << 63));
+    }
+};
+
 __device__ __forceinline__ int owner_of(u32 s, const u32* __restrict__ b, int world) {
     int lo = 0, hi = world;  // last r with b[r] <= s (ids >= |V| go to the last rank)
     while (hi - lo > 1) {
@@ -35,8 +51,8 @@ __device__ __forceinline__ int owner_of(u32 s, const u32* __restrict__ b, int wo
     return lo;
 }
 
-__global__ void k_route_hist(const u32* __restrict__ src, u64 n, const u32* __restrict__ bounds, int world,
-                             u32* __restrict__ tile_counts) {
+__global__ void k_route_hist(RouteIn in, const u32* __restrict__ bounds, int world, u32* __restrict__ tile_counts) {
+    const u64 n = in.ni + in.nd;
     __shared__ u32 s_b[kMaxWorld + 1];
     __shared__ u32 s_c[kMaxWorld];
     for (int i = threadIdx.x; i <= world; i += blockDim.x) s_b[i] = bounds[i];
@@ -45,7 +61,7 @@ __global__ void k_route_hist(const u32* __restrict__ src, u64 n, const u32* __re
     const u64 base = u64(blockIdx.x) * kRouteTile;
     for (int j = 0; j < kRouteItems; ++j) {
         const u64 i = base + u64(j) * kRouteThreads + threadIdx.x;
-        if (i < n) atomicAdd(&s_c[owner_of(src[i], s_b, world)], 1u);
+        if (i < n) atomicAdd(&s_c[owner_of(in.src(i), s_b, world)], 1u);
     }
     __syncthreads();
     for (int r = threadIdx.x; r < world; r += blockDim.x) tile_counts[u64(r) * gridDim.x + blockIdx.x] = s_c[r];
@@ -84,9 +100,9 @@ __global__ void k_route_scan(const u32* __restrict__ tile_counts, u64 ntiles, in
     }
 }
 
-__global__ void k_route_scatter(const u32* __restrict__ src, const u32* __restrict__ dst, const double* __restrict__ w,
-                                u64 n, const u32* __restrict__ bounds, int world, const u64* __restrict__ tile_offsets,
-                                u64* __restrict__ okeys, double* __restrict__ ow) {
+__global__ void k_route_scatter(RouteIn in, const u32* __restrict__ bounds, int world,
+                                const u64* __restrict__ tile_offsets, u64* __restrict__ okeys, double* __restrict__ ow) {
+    const u64 n = in.ni + in.nd;
     constexpr int kWarps = kRouteThreads / 32;
     __shared__ u32 s_b[kMaxWorld + 1];
     // (item row j, warp, owner) counts -> owner-local exclusive offsets; rows
@@ -102,7 +118,7 @@ __global__ void k_route_scatter(const u32* __restrict__ src, const u32* __restri
 #pragma unroll
     for (int j = 0; j < kRouteItems; ++j) {
         const u64 i = base + u64(j) * kRouteThreads + threadIdx.x;
-        own[j] = i < n ? owner_of(src[i], s_b, world) : -1;
+        own[j] = i < n ? owner_of(in.src(i), s_b, world) : -1;
         const unsigned peers = __match_any_sync(FULL, own[j]);
         rank[j] = __popc(peers & lanemask_lt());
         if (own[j] >= 0 && rank[j] == 0) s_wc[(j * kWarps + warp) * world + own[j]] = __popc(peers);
@@ -123,8 +139,8 @@ __global__ void k_route_scatter(const u32* __restrict__ src, const u32* __restri
         const u64 i = base + u64(j) * kRouteThreads + threadIdx.x;
         const u64 o = tile_offsets[u64(own[j]) * gridDim.x + blockIdx.x] + s_wc[(j * kWarps + warp) * world + own[j]] +
                       rank[j];
-        okeys[o] = pack_edge(src[i], dst[i]);  // EdgeKey (graph.hpp:27-37): one 8-B word on the wire
-        if (ow) ow[o] = w ? w[i] : 1.0;
+        okeys[o] = in.key(i);  // EdgeKey (graph.hpp:27-37) + delete bit: one 8-B word on the wire
+        if (ow) ow[o] = (i < in.ni && in.iw) ? in.iw[i] : 1.0;
     }
 }
 
@@ -236,10 +252,13 @@ __global__ void k_pr_finish(const double* __restrict__ x, double* __restrict__ y
 
 // ================================================================ host side
 
-void Graph::route_partition(const u32* src, const u32* dst, const double* w, u64 n, const u32* d_bounds, int world,
-                            u64* okeys, double* ow, u64* h_counts) {
+void Graph::route_partition(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
+                            u64 nd, const u32* d_bounds, int world, u64* okeys, double* ow, u64* h_counts) {
     if (world < 1 || world > kMaxWorld) throw ApiError(PMA_EINVAL, "route: world size must be in [1, 64]");
+    if (nv > (1ull << 31)) throw ApiError(PMA_EINVAL, "route: vertex ids must be < 2^31 (bit 63 marks deletes)");
     cudaStream_t s = pma.stream();
+    const RouteIn in{is, id, iw, ni, ds, dd, nd};
+    const u64 n = ni + nd;
     if (n == 0) {
         for (int r = 0; r < world; ++r) h_counts[r] = 0;
         return;
@@ -248,12 +267,11 @@ void Graph::route_partition(const u32* src, const u32* dst, const double* w, u64
     rt_counts.reserve(ntiles * world);
     rt_offsets.reserve(ntiles * world);
     rt_totals.reserve(world);
-    k_route_hist<<<unsigned(ntiles), kRouteThreads, 0, s>>>(src, n, d_bounds, world, rt_counts.ptr);
+    k_route_hist<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_counts.ptr);
     GPMA_LAUNCH_CHECK();
     k_route_scan<<<1, 1024, 0, s>>>(rt_counts.ptr, ntiles, world, rt_offsets.ptr, rt_totals.ptr);
     GPMA_LAUNCH_CHECK();
-    k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, s>>>(src, dst, w, n, d_bounds, world, rt_offsets.ptr, okeys,
-                                                               ow);
+    k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_offsets.ptr, okeys, ow);
     GPMA_LAUNCH_CHECK();
     GPMA_CUDA(cudaMemcpyAsync(h_counts, rt_totals.ptr, world * sizeof(u64), cudaMemcpyDeviceToHost, s));
     GPMA_CUDA(cudaStreamSynchronize(s));

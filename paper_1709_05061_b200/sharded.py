@@ -201,48 +201,49 @@ class ShardedGraph:
         return int(self.bounds[r]), int(self.bounds[r + 1])
 
     # ---- updates
-    def _route(self, i, src, dst, w):
+    def _route(self, i, a, b, w, c=None, d=None):
+        """Stable owner partition of local rank i's share (inserts a,b,w then
+        deletes c,d) into EdgeKeys (bit 63 = delete) + weights + counts."""
         torch = _torch()
-        n = src.numel()
-        keys = torch.empty(max(n, 1), dtype=torch.int64, device=src.device)
-        ow = torch.empty(max(n, 1), dtype=torch.float64, device=src.device) if w is not None else None
+        ni = a.numel()
+        nd = c.numel() if c is not None else 0
+        n = ni + nd
+        keys = torch.empty(max(n, 1), dtype=torch.int64, device=a.device)
+        ow = torch.empty(max(n, 1), dtype=torch.float64, device=a.device) if w is not None else None
         counts = (C.c_uint64 * self.comm.world)()
-        _sync(src)
-        self._check(i, self._lib.gpma_route_partition(self.h[i], _vp(src), _vp(dst), _vp(w), n,
-                                                       _vp(self._dbounds[i]), self.comm.world, _vp(keys), _vp(ow),
-                                                       counts))
-        return keys[:n], (ow[:n] if ow is not None else None), [int(c) for c in counts]
+        _sync(a)
+        self._check(i, self._lib.gpma_route_batch(self.h[i], _vp(a), _vp(b), _vp(w), ni, _vp(c), _vp(d), nd,
+                                                   _vp(self._dbounds[i]), self.comm.world, _vp(keys), _vp(ow),
+                                                   counts))
+        return keys[:n], (ow[:n] if ow is not None else None), [int(x) for x in counts]
 
     def apply_batch(self, slices) -> ShardStats:
         """slices[i] = (ins_src, ins_dst, ins_w|None, del_src, del_dst):
         local rank i's share of the global batch (device tensors, u32 ids as
-        int32).  Routes every update to its owner and applies the routed
-        batch to each shard (DynamicGraph::apply_batch, graph.hpp:130-162)."""
+        int32; weights given on every rank or on none).  One owner partition
+        (gpma_route_batch) and one all-to-all of 8-B EdgeKeys per batch, then
+        each shard applies its routed batch (DynamicGraph::apply_batch,
+        graph.hpp:130-162)."""
         L = len(self.h)
-        ik, iw, ic, dk, dc = [], [], [], [], []
+        ks, ws, cs = [], [], []
         for i in range(L):
             a, b, w, c, d = slices[i]
-            k, ww, cnt = self._route(i, a, b, w)
-            ik.append(k)
-            iw.append(ww)
-            ic.append(cnt)
-            k2, _, cnt2 = self._route(i, c, d, None)
-            dk.append(k2)
-            dc.append(cnt2)
-        rik, _ = self.comm.all_to_all_v(ik, ic)
-        riw = self.comm.all_to_all_v(iw, ic)[0] if iw[0] is not None else [None] * L
-        rdk, _ = self.comm.all_to_all_v(dk, dc)
+            k, ww, cnt = self._route(i, a, b, w, c, d)
+            ks.append(k)
+            ws.append(ww)
+            cs.append(cnt)
+        rk, _ = self.comm.all_to_all_v(ks, cs)
+        rw = self.comm.all_to_all_v(ws, cs)[0] if ws[0] is not None else [None] * L
         out, routed, sent = [], [], []
         for i in range(L):
             st = pma_stats()
-            _sync(rik[i])
-            _sync(rdk[i])
-            self._check(i, self._lib.gpma_apply_batch_keys_device(self.h[i], _vp(rik[i]), _vp(riw[i]), rik[i].numel(),
-                                                                   _vp(rdk[i]), rdk[i].numel(), C.byref(st)))
+            _sync(rk[i])
+            self._check(i, self._lib.gpma_apply_batch_routed_device(self.h[i], _vp(rk[i]), _vp(rw[i]), rk[i].numel(),
+                                                                     C.byref(st)))
             out.append(UpdateStats.from_c(st))
-            routed.append(rik[i].numel() + rdk[i].numel())
+            routed.append(rk[i].numel())
             me = self.comm.ranks[i]
-            sent.append(sum(ic[i]) - ic[i][me] + sum(dc[i]) - dc[i][me])
+            sent.append(sum(cs[i]) - cs[i][me])
         return ShardStats(out, routed, sent)
 
     # ---- analytics
@@ -387,3 +388,12 @@ class ShardedGraph:
 
     def num_edges(self):
         return [int(self._lib.gpma_num_edges(h)) for h in self.h]
+
+    def last_timing(self, i=0):
+        from .abi import pma_timing
+        t = pma_timing()
+        self._check(i, self._lib.gpma_last_timing(self.h[i], C.byref(t)))
+        return t
+
+    def cuda_stream(self, i=0):
+        return self._lib.gpma_cuda_stream(self.h[i])

@@ -129,10 +129,14 @@ def test_route_partition_is_stable_and_exact():
         src = rng.integers(0, nv + 50, n).astype(np.uint32)
         dst = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
         w = rng.random(n)
-        keys, ow, counts = G._route(0, _dev(src, "u32"), _dev(dst, "u32"), _dev(w, "f64"))
+        ni = n // 3  # first third inserts, rest deletes (bit 63 on the wire)
+        keys, ow, counts = G._route(0, _dev(src[:ni], "u32"), _dev(dst[:ni], "u32"), _dev(w[:ni], "f64"),
+                                    _dev(src[ni:], "u32"), _dev(dst[ni:], "u32"))
         own = np.minimum(np.searchsorted(bounds, src.astype(np.int64), side="right") - 1, world - 1)
         order = np.argsort(own, kind="stable")
-        exp = (src[order].astype(np.uint64) << np.uint64(32)) | dst[order].astype(np.uint64)
+        dbit = (np.arange(n) >= ni).astype(np.uint64) << np.uint64(63)
+        exp = ((src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64) | dbit)[order]
+        wexp = np.where(np.arange(n) < ni, w, 1.0)[order]
         assert counts == list(np.bincount(own, minlength=world))
         assert (keys.cpu().numpy().view(np.uint64) == exp).all()
-        assert (ow.cpu().numpy() == w[order]).all()
+        assert (ow.cpu().numpy() == wexp).all()

@@ -97,3 +97,49 @@ def test_vertex_bounds_balance_edges():
     w = np.add.reduceat(deg + 1, b[:-1])
     assert w.max() <= 2 * w.mean()
     assert list(sh.vertex_bounds(10, 3)) == [0, 3, 6, 10]
+
+
+def _comm_worker(rank, world, port, result_q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_05061_b200.sharded import TorchComm
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        c = TorchComm()
+        # all_to_all_v: owner-major send buffers with variable counts
+        rng = np.random.default_rng(rank)
+        cnt = [int(x) for x in rng.integers(0, 5, world)]
+        buf = torch.tensor([1000 * rank + 10 * r + j for r in range(world) for j in range(cnt[r])], dtype=torch.int64)
+        (out,), (rc,) = c.all_to_all_v([buf], [cnt])
+        allc = [[int(x) for x in np.random.default_rng(s).integers(0, 5, world)] for s in range(world)]
+        exp = [1000 * s + 10 * rank + j for s in range(world) for j in range(allc[s][rank])]
+        ok = out.tolist() == exp and rc == [allc[s][rank] for s in range(world)]
+        for op, f in (("sum", sum), ("max", max), ("min", min)):
+            t = torch.tensor([rank, 7 - rank, 3], dtype=torch.int32)
+            c.all_reduce([t], op)
+            ok &= t.tolist() == [f(range(world)), f(7 - r for r in range(world)), f([3] * world)]
+        (g,) = c.all_gather_v([torch.arange(rank + 2, dtype=torch.float64) + rank])
+        ok &= g.tolist() == [float(x + r) for r in range(world) for x in range(r + 2)]
+        result_q.put(("ok", ok))
+    except Exception as e:  # pragma: no cover
+        result_q.put(("error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_torch_comm_collectives_gloo(world):
+    """The collectives ShardedGraph runs between its device steps
+    (paper_1709_05061_b200/sharded.py TorchComm): variable all-to-all in
+    sender-rank order, sum/max/min all-reduce, variable all-gather."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    mp.start_processes(_comm_worker, args=(world, port, q), nprocs=world, join=True, start_method="spawn")
+    res = [q.get(timeout=60) for _ in range(world)]
+    assert all(s == "ok" and ok for s, ok in res), res
