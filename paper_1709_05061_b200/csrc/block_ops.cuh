@@ -103,6 +103,23 @@ __device__ __forceinline__ u64 leaf_of_key(const u64* hdr, u64 L, const u8* st, 
     return lo ? lo - 1 : 0;
 }
 
+// Block-wide sum of a per-thread double, one atomicAdd per CTA (same-address
+// atomics serialise in L2, so per-warp atomics on one counter cost ~us each).
+__device__ __forceinline__ void block_atomic_add(double v, double* dst) {
+    __shared__ double s_part[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    const unsigned w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) s_part[w] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0;
+        for (unsigned i = 0; i < (blockDim.x >> 5); ++i) a += s_part[i];
+        if (a != 0.0) atomicAdd(dst, a);
+    }
+    __syncthreads();
+}
+
 // N leaf searches at once (keys < 2^64-1; pma.hpp:234-289 through the
 // backward-filled headers): uniform power-of-two descent (L = C/leaf is a
 // power of two) to the last header <= key, else 0 — the same leaf as

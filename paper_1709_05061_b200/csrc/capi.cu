@@ -589,6 +589,57 @@ extern "C" int gpma_warmup(int device) {
         gpma_row_offsets(g, ro.data());
         gpma_csr_snapshot(g, ro.data(), col.data(), vals.data());
         gpma_destroy(g);
+        {  // key-range sharding path (shard.cu): shard build, routing, routed apply, sharded analytics
+            uint32_t *ds_ = nullptr, *dd_ = nullptr, *db_ = nullptr, *fr_ = nullptr, *dl_ = nullptr, *lab_ = nullptr,
+                     *pv_ = nullptr, *od_ = nullptr;
+            uint64_t* dk_ = nullptr;
+            uint8_t* fl_ = nullptr;
+            double *dx_ = nullptr, *dy_ = nullptr;
+            GPMA_CUDA(cudaMalloc(&ds_, ne * 4));
+            GPMA_CUDA(cudaMalloc(&dd_, ne * 4));
+            GPMA_CUDA(cudaMalloc(&db_, 3 * 4));
+            GPMA_CUDA(cudaMalloc(&fr_, nv * 4));
+            GPMA_CUDA(cudaMalloc(&dl_, nv * 4));
+            GPMA_CUDA(cudaMalloc(&lab_, nv * 4));
+            GPMA_CUDA(cudaMalloc(&pv_, nv * 4));
+            GPMA_CUDA(cudaMalloc(&od_, nv * 4));
+            GPMA_CUDA(cudaMalloc(&dk_, ne * 8));
+            GPMA_CUDA(cudaMalloc(&fl_, nv));
+            GPMA_CUDA(cudaMalloc(&dx_, nv * 8));
+            GPMA_CUDA(cudaMalloc(&dy_, nv * 8));
+            const uint32_t bnd[3] = {0, uint32_t(nv / 2), uint32_t(nv)};
+            std::vector<uint32_t> iota(nv);
+            for (size_t i = 0; i < nv; ++i) iota[i] = uint32_t(i);
+            GPMA_CUDA(cudaMemcpy(ds_, s.data(), ne * 4, cudaMemcpyHostToDevice));
+            GPMA_CUDA(cudaMemcpy(dd_, d.data(), ne * 4, cudaMemcpyHostToDevice));
+            GPMA_CUDA(cudaMemcpy(db_, bnd, sizeof(bnd), cudaMemcpyHostToDevice));
+            GPMA_CUDA(cudaMemcpy(fr_, iota.data(), nv * 4, cudaMemcpyHostToDevice));
+            GPMA_CUDA(cudaMemcpy(lab_, iota.data(), nv * 4, cudaMemcpyHostToDevice));
+            GPMA_CUDA(cudaMemcpy(pv_, iota.data(), nv * 4, cudaMemcpyHostToDevice));
+            GPMA_CUDA(cudaMemcpy(dx_, xs.data(), nv * 8, cudaMemcpyHostToDevice));
+            gpma_graph* sg = nullptr;
+            if (gpma_shard_from_edges_device(nullptr, device, nv, 0, uint32_t(nv / 2), ds_, dd_, nullptr, ne, &sg))
+                throw ApiError(PMA_ECUDA, gpma_last_error(nullptr));
+            uint64_t cnt[2] = {0, 0};
+            gpma_route_batch(sg, ds_, dd_, nullptr, 300, ds_ + 300, dd_ + 300, 300, db_, 2, dk_, nullptr, cnt);
+            gpma_apply_batch_routed_device(sg, dk_, nullptr, cnt[0], &st);
+            uint32_t nf = 0;
+            int ch = 0;
+            double l1 = 0;
+            gpma_shard_bfs_mark(sg, fr_, 4, fl_);
+            GPMA_CUDA(cudaMemset(dl_, 0xFF, nv * 4));
+            gpma_shard_bfs_update(sg, fl_, dl_, 1, fr_, &nf);
+            gpma_shard_cc_hook(sg, lab_);
+            gpma_cc_jump(sg, lab_, nv, pv_, &ch);
+            gpma_shard_outdeg(sg, od_);
+            gpma_shard_pr_push(sg, dx_, od_, 0.85, dy_);
+            gpma_pr_finish(sg, dx_, dy_, nv, od_, 0.85, &l1);
+            gpma_shard_spmv(sg, dx_, dy_);
+            gpma_destroy(sg);
+            for (void* p : {(void*)ds_, (void*)dd_, (void*)db_, (void*)fr_, (void*)dl_, (void*)lab_, (void*)pv_,
+                            (void*)od_, (void*)dk_, (void*)fl_, (void*)dx_, (void*)dy_})
+                cudaFree(p);
+        }
         GPMA_CUDA(cudaDeviceSynchronize());
     });
 }

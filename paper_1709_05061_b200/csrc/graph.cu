@@ -66,38 +66,73 @@ __global__ void k_iota_u32(u32* a, u64 n) {
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) a[i] = u32(i);
 }
 
-// -------- BFS (analytics.hpp:22-48): warp per frontier vertex, lanes stride
-// its slot interval (coalesced 8-B keys + 1-B states), CAS on dist,
-// warp-aggregated enqueue (ballot + popc + one atomic per warp).
+// -------- BFS (analytics.hpp:22-48): frontier queues split by row length.
+// Light rows (<= kHeavyRow slots): a warp per frontier vertex, lanes stride
+// its slot interval (coalesced 8-B keys + 1-B states).  Heavy rows (RMAT
+// hubs): kHeavyParts CTAs per vertex, each striding 1/kHeavyParts of the row,
+// so one hub never serialises a level on a single warp.  Discovery is a CAS on
+// dist; discovered vertices are enqueued (warp-aggregated: ballot + popc + one
+// atomic per warp and queue) into the light or heavy next queue by their own
+// row length.
+constexpr u64 kHeavyRow = 1024;
+constexpr u32 kHeavyParts = 32;
+
+__device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64* __restrict__ keys,
+                                          const u8* __restrict__ st, u32* __restrict__ dist, u32 depth, u64 t, u64 e,
+                                          u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
+    const unsigned lane = threadIdx.x & 31u;
+    bool won = false;
+    u32 v = 0;
+    if (t < e && st[t] == kValid) {
+        const u64 k = keys[t];
+        if (!is_guard(k)) {
+            v = dst_of(k);
+            if (dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+        }
+    }
+    const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
+    const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
+    if (lm) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
+        base = __shfl_sync(FULL, base, 0);
+        if (won && !heavy) next[base + __popc(lm & lanemask_lt())] = v;
+    }
+    if (hm) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
+        base = __shfl_sync(FULL, base, 0);
+        if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, u32 nf,
                                                     const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                     const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
-                                                    u32* __restrict__ next, u32* __restrict__ next_n) {
+                                                    u32* __restrict__ next, u32* __restrict__ hnext,
+                                                    u32* __restrict__ qn) {
     const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
     for (u64 f = warp; f < nf; f += nwarps) {
         const u32 u = frontier[f];
         const u64 b = ro[u], e = ro[u + 1];
-        for (u64 t0 = b; t0 < e; t0 += 32) {
-            const u64 t = t0 + lane;
-            bool won = false;
-            u32 v = 0;
-            if (t < e && st[t] == kValid) {
-                const u64 k = keys[t];
-                if (!is_guard(k)) {
-                    v = dst_of(k);
-                    if (dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
-                }
-            }
-            const unsigned wm = __ballot_sync(FULL, won);
-            if (wm) {
-                u32 base = 0;
-                if (lane == 0) base = atomicAdd(next_n, u32(__popc(wm)));
-                base = __shfl_sync(FULL, base, 0);
-                if (won) next[base + __popc(wm & lanemask_lt())] = v;
-            }
-        }
+        for (u64 t0 = b; t0 < e; t0 += 32) bfs_visit(ro, keys, st, dist, depth, t0 + lane, e, next, hnext, qn);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, u32 nh,
+                                                          const u64* __restrict__ ro, const u64* __restrict__ keys,
+                                                          const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
+                                                          u32* __restrict__ next, u32* __restrict__ hnext,
+                                                          u32* __restrict__ qn) {
+    for (u64 task = blockIdx.x; task < u64(nh) * kHeavyParts; task += gridDim.x) {
+        const u32 u = hfrontier[task / kHeavyParts];
+        const u64 p = task % kHeavyParts;
+        const u64 b0 = ro[u], e0 = ro[u + 1], len = e0 - b0;
+        const u64 b = b0 + (len * p) / kHeavyParts, e = b0 + (len * (p + 1)) / kHeavyParts;
+        for (u64 t0 = b; t0 < e; t0 += blockDim.x)  // whole warps iterate together (ballots inside)
+            bfs_visit(ro, keys, st, dist, depth, t0 + threadIdx.x, e, next, hnext, qn);
     }
 }
 
@@ -155,24 +190,33 @@ __global__ void k_pr_prep(const double* __restrict__ x, const u32* __restrict__ 
             share[u] = __ddiv_rn(__dmul_rn(d, x[u]), double(od));
         }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) dang += __shfl_xor_sync(FULL, dang, o);
-    if ((threadIdx.x & 31) == 0 && dang != 0.0) atomicAdd(dangling_sum, dang);
+    block_atomic_add(dang, dangling_sum);
 }
 
-__global__ void k_pr_base(double* __restrict__ y, u64 n, const double* dangling_sum, double d) {
+// One |V| pass per iteration after the push (analytics.hpp:112-141): y =
+// base + pushed mass (base from the current dangling mass), L1 += |y - x|,
+// and already the next iteration's inputs — share = d y / outdeg, the next
+// dangling mass.
+__global__ void k_pr_finish_next(double* __restrict__ x, double* __restrict__ y, const u32* __restrict__ outdeg, u64 n,
+                                 double d, const double* dangling, double* next_dangling, double* l1,
+                                 double* __restrict__ share) {
     const double nn = double(n);
-    const double base = __dadd_rn(__ddiv_rn(1.0 - d, nn), __ddiv_rn(__dmul_rn(d, *dangling_sum), nn));
-    for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x) y[u] = base;
-}
-
-__global__ void k_pr_l1(const double* __restrict__ x, const double* __restrict__ y, u64 n, double* l1) {
-    double acc = 0.0;
-    for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x)
-        acc += fabs(y[u] - x[u]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(l1, acc);
+    const double base = __dadd_rn(__ddiv_rn(1.0 - d, nn), __ddiv_rn(__dmul_rn(d, *dangling), nn));
+    double acc = 0.0, dang = 0.0;
+    for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x) {
+        const double v = __dadd_rn(base, y[u]);
+        y[u] = v;
+        acc += fabs(v - x[u]);
+        const u32 od = outdeg[u];
+        if (od) {
+            share[u] = __ddiv_rn(__dmul_rn(d, v), double(od));
+        } else {
+            share[u] = 0.0;
+            dang += v;
+        }
+    }
+    block_atomic_add(acc, l1);
+    block_atomic_add(dang, next_dangling);
 }
 
 // ---------------------------------------------------------------- Graph
@@ -384,30 +428,45 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     dist.reserve(nv);
     q0.reserve(nv + 1);
     q1.reserve(nv + 1);
+    h0.reserve(nv + 1);
+    h1.reserve(nv + 1);
     qn.reserve(2);
     k_fill_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv, GPMA_UNREACHED);
     GPMA_LAUNCH_CHECK();
     const u32 zero = 0;
     GPMA_CUDA(cudaMemcpyAsync(dist.ptr + root, &zero, 4, cudaMemcpyHostToDevice, s));
-    GPMA_CUDA(cudaMemcpyAsync(q0.ptr, &root, 4, cudaMemcpyHostToDevice, s));
-    u32 nf = 1;
+    u64 rr[2] = {0, 0};
+    GPMA_CUDA(cudaMemcpyAsync(rr, ro.ptr + root, 16, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    const bool root_heavy = rr[1] - rr[0] > kHeavyRow;
+    GPMA_CUDA(cudaMemcpyAsync(root_heavy ? h0.ptr : q0.ptr, &root, 4, cudaMemcpyHostToDevice, s));
+    u32 nf = root_heavy ? 0 : 1, nh = root_heavy ? 1 : 0;
     u64 total = 1;
     u32 depth = 0;
-    u32* cur = q0.ptr;
-    u32* nxt = q1.ptr;
+    u32 *cur = q0.ptr, *nxt = q1.ptr, *hcur = h0.ptr, *hnxt = h1.ptr;
     u64 launches = 3;
-    while (nf > 0) {
+    while (nf + nh > 0) {
         ++depth;
-        GPMA_CUDA(cudaMemsetAsync(qn.ptr, 0, 4, s));
-        const unsigned blocks = grid_for(u64(nf) * 32, 256, 148 * 16);
-        k_bfs_expand<<<blocks, 256, 0, s>>>(cur, nf, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt, qn.ptr);
-        GPMA_LAUNCH_CHECK();
-        ++launches;
-        GPMA_CUDA(cudaMemcpyAsync(h_nf_, qn.ptr, 4, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaMemsetAsync(qn.ptr, 0, 8, s));
+        if (nf) {
+            k_bfs_expand<<<grid_for(u64(nf) * 32, 256, 148 * 16), 256, 0, s>>>(cur, nf, ro.ptr, pma.d_keys, pma.d_st,
+                                                                               dist.ptr, depth, nxt, hnxt, qn.ptr);
+            GPMA_LAUNCH_CHECK();
+            ++launches;
+        }
+        if (nh) {
+            k_bfs_expand_heavy<<<grid_for(u64(nh) * kHeavyParts, 1, 148 * 8), 256, 0, s>>>(
+                hcur, nh, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt, hnxt, qn.ptr);
+            GPMA_LAUNCH_CHECK();
+            ++launches;
+        }
+        GPMA_CUDA(cudaMemcpyAsync(h_nf_, qn.ptr, 8, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
-        nf = *h_nf_;
-        total += nf;
+        nf = h_nf_[0];
+        nh = h_nf_[1];
+        total += u64(nf) + nh;
         std::swap(cur, nxt);
+        std::swap(hcur, hnxt);
     }
     GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
     if (h_dist) GPMA_CUDA(cudaMemcpyAsync(h_dist, dist.ptr, nv * 4, cudaMemcpyDeviceToHost, s));
@@ -453,31 +512,43 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
     }
     GPMA_CUDA(cudaMemsetAsync(outdeg.ptr, 0, nv * 4, s));
     const u64 cap = pma.capacity();
-    k_outdeg<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg.ptr);
+    k_outdeg<<<grid_for(cap / 8, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg.ptr);
     GPMA_LAUNCH_CHECK();
-    u64 launches = 1;
+    prepare_hot(outdeg.ptr, nv);
+    u64 launches = 3;
     double* x = px.ptr;
     double* y = py.ptr;
     *converged = 0;
     u64 it;
     pr_iter_ms_ = 0.0;
+    // psc = [dangling_A, l1_A, dangling_B, l1_B]: iteration parity p reads
+    // dangling at psc[2p] and produces the next dangling + this L1 at psc[2(1-p)]
+    psc.reserve(4);
+    GPMA_CUDA(cudaMemsetAsync(psc.ptr, 0, 32, s));
+    GPMA_CUDA(cudaMemsetAsync(y, 0, nv * 8, s));
+    k_pr_prep<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, outdeg.ptr, nv, d, pshare.ptr, psc.ptr);
+    GPMA_LAUNCH_CHECK();
+    ++launches;
     for (it = 1; it <= max_iters; ++it) {
-        GPMA_CUDA(cudaMemsetAsync(psc.ptr, 0, 16, s));
+        const int p = int(it & 1) ^ 1;  // it = 1 -> p = 0
+        double* cur = psc.ptr + 2 * p;
+        double* nxt = psc.ptr + 2 * (1 - p);
+        GPMA_CUDA(cudaMemsetAsync(nxt, 0, 16, s));
         GPMA_CUDA(cudaEventRecord(pma_ev(2), s));
-        k_pr_prep<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, outdeg.ptr, nv, d, pshare.ptr, psc.ptr);
-        k_pr_base<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(y, nv, psc.ptr, d);
-        k_pr_push<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y);
-        k_pr_l1<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, y, nv, psc.ptr + 1);
+        k_pr_push<<<148 * 8, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr, nhot_);
+        k_pr_finish_next<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, y, outdeg.ptr, nv, d, cur, nxt, nxt + 1,
+                                                                   pshare.ptr);
         GPMA_LAUNCH_CHECK();
         GPMA_CUDA(cudaEventRecord(pma_ev(3), s));
-        launches += 4;
+        launches += 2;
         double l1 = 0;
-        GPMA_CUDA(cudaMemcpyAsync(&l1, psc.ptr + 1, 8, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaMemcpyAsync(&l1, nxt + 1, 8, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
         float ms = 0;
         cudaEventElapsedTime(&ms, pma_ev(2), pma_ev(3));
         pr_iter_ms_ += ms;
-        std::swap(x, y);
+        std::swap(x, y);  // y (finished) is the next x; x (zeroed) accumulates the next pushes
+        GPMA_CUDA(cudaMemsetAsync(y, 0, nv * 8, s));
         if (l1 < eps) {
             *converged = 1;
             break;
@@ -489,6 +560,35 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
     GPMA_CUDA(cudaStreamSynchronize(s));
     record_timing(launches);
     pma.timing.rounds_ms = pr_iter_ms_;
+}
+
+// Hot-destination set of the push (analytics_kernels.cuh): the <= kHotMax
+// vertices of largest out-degree (>= 64), from a bit-length histogram.
+void Graph::prepare_hot(const u32* od, u64 n) {
+    cudaStream_t s = pma.stream();
+    hot_table.reserve(2 * kHotTable);
+    hot_ids.reserve(kHotMax);
+    hot_hist.reserve(34);
+    GPMA_CUDA(cudaMemsetAsync(hot_hist.ptr, 0, 34 * 4, s));
+    k_hot_hist<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(od, n, hot_hist.ptr);
+    GPMA_LAUNCH_CHECK();
+    u32 h[34] = {};
+    GPMA_CUDA(cudaMemcpyAsync(h, hot_hist.ptr, 33 * 4, cudaMemcpyDeviceToHost, s));
+    GPMA_CUDA(cudaStreamSynchronize(s));
+    u32 min_bits = 33, total = 0;
+    for (int b = 32; b >= 7; --b) {  // bit length >= 7: out-degree >= 64
+        if (total + h[b] > kHotMax) break;
+        total += h[b];
+        if (h[b]) min_bits = u32(b);
+    }
+    nhot_ = 0;
+    if (total == 0) return;
+    GPMA_CUDA(cudaMemsetAsync(hot_table.ptr, 0xFF, 2 * kHotTable * 4, s));
+    GPMA_CUDA(cudaMemsetAsync(hot_hist.ptr + 33, 0, 4, s));
+    k_hot_select<<<grid_for(n, 256, 148 * 4), 256, 0, s>>>(od, n, min_bits, hot_table.ptr, hot_ids.ptr,
+                                                          hot_hist.ptr + 33);
+    GPMA_LAUNCH_CHECK();
+    nhot_ = total;
 }
 
 void Graph::spmv(const double* h_x, double* h_y) {

@@ -56,12 +56,15 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     Ctr* d_ctr_ = nullptr;
     DevBuf<u64> bk, bv;
     DevBuf<u8> bo;
-    DevBuf<u32> dist, q0, q1, qn, outdeg;
+    DevBuf<u32> dist, q0, q1, h0, h1, qn, outdeg;
     DevBuf<double> px, py, pshare, psc;
-    DevBuf<u32> rt_counts;
+    DevBuf<u32> rt_counts, hot_table, hot_ids, hot_hist;
+    u32 nhot_ = 0;
+    bool hot_ready_ = false;
+    void prepare_hot(const u32* outdeg, u64 n);
     DevBuf<u64> rt_offsets, rt_totals;
-    u32 h_nf_store_ = 0;
-    u32* h_nf_ = &h_nf_store_;
+    u32 h_nf_store_[2] = {0, 0};
+    u32* h_nf_ = h_nf_store_;
     cudaEvent_t evs_[4]{};
 };
 

@@ -188,19 +188,17 @@ __global__ void k_shard_bfs_update(const u8* __restrict__ flags, u64 lo, u64 nlo
 // the caller min-reduces the labels across shards; pointer jumping then makes
 // every label a root.  At the fixpoint each label is its component's minimum
 // id — the reference's labels.
-__global__ void k_shard_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u32* labels) {
-    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < cap; t += u64(gridDim.x) * blockDim.x) {
-        if (st[t] != kValid) continue;
-        const u64 k = keys[t];
-        if (is_guard(k)) continue;
+__global__ void __launch_bounds__(256) k_shard_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
+                                                       u32* labels) {
+    sweep_edges8(keys, st, cap, [&](u64 k) {
         const u32 u = src_of(k), v = dst_of(k);
         const u32 a = labels[u], b = labels[v];
-        if (a == b) continue;
+        if (a == b) return;
         const u32 hi = a > b ? a : b, lo = a > b ? b : a;
         atomicMin(&labels[hi], lo);
         atomicMin(&labels[u], lo);
         atomicMin(&labels[v], lo);
-    }
+    });
 }
 
 __global__ void k_cc_jump(u32* labels, u64 n, const u32* __restrict__ prev, u32* changed) {
@@ -230,9 +228,7 @@ __global__ void k_pr_dangling(const double* __restrict__ x, const u32* __restric
     double acc = 0.0;
     for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x)
         if (outdeg[u] == 0) acc += x[u];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(sum, acc);
+    block_atomic_add(acc, sum);
 }
 
 __global__ void k_pr_finish(const double* __restrict__ x, double* __restrict__ y, u64 n, const double* dangling,
@@ -245,9 +241,7 @@ __global__ void k_pr_finish(const double* __restrict__ x, double* __restrict__ y
         y[u] = v;
         acc += fabs(v - x[u]);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(l1, acc);
+    block_atomic_add(acc, l1);
 }
 
 // ================================================================ host side
@@ -305,7 +299,7 @@ void Graph::shard_bfs_update(const u8* flags, u32* dist_local, u32 depth, u32* n
 void Graph::shard_cc_hook(u32* labels) {
     cudaStream_t s = pma.stream();
     const u64 cap = pma.capacity();
-    k_shard_cc_hook<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, labels);
+    k_shard_cc_hook<<<grid_for(cap / 8, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, labels);
     GPMA_LAUNCH_CHECK();
     GPMA_CUDA(cudaStreamSynchronize(s));
 }
@@ -325,9 +319,10 @@ void Graph::cc_jump(u32* labels, u64 n, const u32* prev, int* changed) {
 
 void Graph::shard_outdeg(u32* outdeg) {
     cudaStream_t s = pma.stream();
+    hot_ready_ = false;
     GPMA_CUDA(cudaMemsetAsync(outdeg, 0, nv * 4, s));
     const u64 cap = pma.capacity();
-    k_outdeg<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg);
+    k_outdeg<<<grid_for(cap / 8, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg);
     GPMA_LAUNCH_CHECK();
     GPMA_CUDA(cudaStreamSynchronize(s));
 }
@@ -341,7 +336,11 @@ void Graph::shard_pr_push(const double* x, const u32* outdeg, double d, double* 
         GPMA_LAUNCH_CHECK();
     }
     const u64 cap = pma.capacity();
-    k_pr_push<<<grid_for(cap, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y);
+    if (!hot_ready_) {  // once per PageRank call (the out-degrees are global by now)
+        prepare_hot(outdeg, nv);
+        hot_ready_ = true;
+    }
+    k_pr_push<<<148 * 8, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr, nhot_);
     GPMA_LAUNCH_CHECK();
     GPMA_CUDA(cudaStreamSynchronize(s));
 }
