@@ -171,3 +171,27 @@ def test_bad_insert_reports_first_offender_and_leaves_graph_unchanged():
     after = g.pma().slots()
     assert all((a == b).all() for a, b in zip(before, after))
     assert list(bfs(g, 0)) == [0, 2, 1]
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_large_batches_parity(mode):
+    """Batches of >= 2^16 updates take the sample-sort front end (sorted
+    packed words, csrc/sample_sort.cuh): slots, stats and row offsets stay
+    bit-exact with the reference over several 150K-arrival slides."""
+    nv = 2**16
+    stream = _window_stream("rmat", nv, 900000, shuffle=2)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    cfg = GraphConfig(deletion_mode=mode)
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half], cfg)
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config(deletion_mode=mode))
+    win = RefWindow(stream)
+    for slide in range(3):
+        a, b, ww, c, dd = win.slide(150000)
+        gs = g.apply_batch(a, b, ww, c, dd)
+        rs = r.apply_batch(a, b, ww, c, dd)
+        assert gs.batch_size >= 2**16
+        ctx = f"slide {slide}"
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
