@@ -265,6 +265,8 @@ __global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck,
     }
 }
 
+__global__ void k_gate_npend(Ctr* ctr) { ctr->np[0] = (ctr->bad_ins || ctr->oor) ? 0ull : ctr->n_unique; }
+
 __global__ void k_iota(u32* p, const ull* n_dev) {
     const u64 n = *n_dev;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) p[i] = u32(i);
@@ -1581,44 +1583,14 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         GPMA_LAUNCH_CHECK();
         ++launches;
     }
-    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->np[0], &d_ctr->n_unique, sizeof(ull), cudaMemcpyDeviceToDevice, stream_));
+    // pending count of round 0 = the unique updates, or 0 when the graph
+    // front end flagged a bad insert id / an out-of-layout delete: every
+    // round is then a no-op (nothing is mutated) and the batch is rejected or
+    // redone after the first host sync — no round trip before the rounds
+    k_gate_npend<<<1, 1, 0, stream_>>>(d_ctr);
+    GPMA_LAUNCH_CHECK();
+    ++launches;
     event(2);
-    sync_ctr();
-    if (gf) {
-        gf->guard_deletes = h_ctr->gdel;
-        gf->bad_insert = h_ctr->bad_ins ? (long long)(~h_ctr->bad_ins) : -1;
-        if (gf->bad_insert >= 0) return;  // caller throws; nothing was mutated
-        if (h_ctr->oor) {
-            // a delete key outside the |V|-derived layout: pack the batch
-            // without its guard deletes (the reference drops them before the
-            // engine) and redo it on the generic key-reduction path
-            const GraphFront f = *gf;
-            u64* bk = f.bk;
-            u64* bv = f.bv;
-            u8* bo = f.bo;
-            Ctr* ctr = d_ctr;
-            run_compact(
-                stream_, ws, nullptr, n, n,
-                [=] __device__(ull i) {
-                    if (f.mk) return !(f.mk[i] >> 63) || dst_of(f.mk[i]) != u32(kGuardDst);
-                    return i < f.ni || f.dd[i - f.ni] != u32(kGuardDst);
-                },
-                [=] __device__(ull i, unsigned fl, ull x) {
-                    if (!fl) return;
-                    const bool ins = f.mk ? !(f.mk[i] >> 63) : i < f.ni;
-                    if (f.mk) bk[x] = f.mk[i] & ~(1ull << 63);
-                    else bk[x] = ins ? pack_edge(f.is[i], f.id[i]) : pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
-                    bv[x] = ins ? u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0)) : 0;
-                    bo[x] = ins ? kOpInsert : kOpDelete;
-                },
-                [=] __device__(ull total) { ctr->nt = total; });
-            sync_ctr();
-            const u64 m = h_ctr->nt;
-            batch_update_device(bk, bv, bo, m, cfg, out, nullptr);
-            if (out) out->batch_size = n;  // the caller subtracts the guard deletes
-            return;
-        }
-    }
     pidx0.reserve(n);
     pidx1.reserve(n);
     gid.reserve(n);
@@ -1633,7 +1605,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     // (more rounds are near certain) the next round is launched without a host
     // round trip; the host syncs after odd levels, before the root, and
     // whenever the pending list is small.
-    u64 npend = h_ctr->n_unique;  // host-known upper bound of the pending count
+    u64 npend = n;  // host-known upper bound of the pending count
     u64* touched_ptr = touched.ptr;
     u64 ntouched = 0;
     u32* pcur = nullptr;  // round 0: pending = all unique updates in order (identity)
@@ -2012,6 +1984,41 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.refresh_ms = d;
     timing.device_ms = a + b + c + d;
     timing.kernel_launches = launches;
+    if (gf) {
+        gf->guard_deletes = h_ctr->gdel;
+        gf->bad_insert = h_ctr->bad_ins ? (long long)(~h_ctr->bad_ins) : -1;
+        if (gf->bad_insert >= 0) return;  // caller throws; the gated rounds mutated nothing
+        if (h_ctr->oor) {
+            // a delete key outside the |V|-derived layout: pack the batch
+            // without its guard deletes (the reference drops them before the
+            // engine) and redo it on the generic key-reduction path
+            const GraphFront f = *gf;
+            u64* bk = f.bk;
+            u64* bv = f.bv;
+            u8* bo = f.bo;
+            Ctr* ctr = d_ctr;
+            run_compact(
+                stream_, ws, nullptr, n, n,
+                [=] __device__(ull i) {
+                    if (f.mk) return !(f.mk[i] >> 63) || dst_of(f.mk[i]) != u32(kGuardDst);
+                    return i < f.ni || f.dd[i - f.ni] != u32(kGuardDst);
+                },
+                [=] __device__(ull i, unsigned fl, ull x) {
+                    if (!fl) return;
+                    const bool ins = f.mk ? !(f.mk[i] >> 63) : i < f.ni;
+                    if (f.mk) bk[x] = f.mk[i] & ~(1ull << 63);
+                    else bk[x] = ins ? pack_edge(f.is[i], f.id[i]) : pack_edge(f.ds[i - f.ni], f.dd[i - f.ni]);
+                    bv[x] = ins ? u64(__double_as_longlong(f.iw ? f.iw[i] : 1.0)) : 0;
+                    bo[x] = ins ? kOpInsert : kOpDelete;
+                },
+                [=] __device__(ull total) { ctr->nt = total; });
+            sync_ctr();
+            const u64 m = h_ctr->nt;
+            batch_update_device(bk, bv, bo, m, cfg, out, nullptr);
+            if (out) out->batch_size = n;  // the caller subtracts the guard deletes
+            return;
+        }
+    }
     st.wall_ns = u64(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
     if (out) *out = st;
 }
