@@ -40,6 +40,33 @@ UNIT = "updates/s"
 NV = 1 << 21
 NE = 30_600_000
 GEN_SEED, SHUFFLE_SEED, ROOT_SEED = 1, 2, 7
+
+# BASELINE.json configs.  The headline bench line is
+# C2 (configs[1]); the others run with --config for evidence at their sizes.
+CONFIGS = {
+    "C1": dict(gen="er", nv=1 << 16, param=2.0 ** -12, shuffle=2, batch=1024,
+               workload="C1 uniform random graph 2^16 vertices / 1M-edge stream, sliding window, batches of 1024"),
+    "C2": dict(gen="rmat", nv=NV, param=NE, shuffle=2, batch=1_000_000,
+               workload="C2 Pokec-shaped sliding window: RMAT 2^21 vertices / 30.6M-edge stream, 15.3M-edge "
+                        "window, GPMA+ apply_batch per slide"),
+    "C3": dict(gen="rmat", nv=1 << 22, param=34_400_000, shuffle=None, batch=344_000,
+               workload="C3 Reddit-like skewed stream: RMAT 2^22 / 34.4M edges in generation order, batch 1% "
+                        "(344,000), PageRank per window"),
+    "C4": dict(gen="rmat", nv=1 << 24, param=1 << 28, shuffle=2, batch=2_684_354,
+               workload="C4 Graph500 RMAT scale 24, edge factor 16 (268M-edge stream, 134M-edge window), batch 1% "
+                        "(2,684,354), CC per window"),
+    "C5": dict(gen="er", nv=1_000_000, param=2e-4, shuffle=2, batch=1_000_000,
+               workload="C5 random graph 1M vertices / 200M-edge stream (100M-edge window), batch 10^6 "
+                        "(~50% deletions)"),
+}
+
+
+def make_stream(pg, cfg, seed):
+    st = (pg.EdgeStream.rmat(cfg["nv"], int(cfg["param"]), seed=seed) if cfg["gen"] == "rmat"
+          else pg.EdgeStream.erdos_renyi(cfg["nv"], cfg["param"], seed=seed))
+    if cfg["shuffle"] is not None:
+        st.shuffle(cfg["shuffle"])
+    return st
 BYTES_PER_MERGE_SLOT = 34  # 17 B read + 17 B write per rewritten slot
 
 
@@ -49,7 +76,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=1_000_000)
+    ap.add_argument("--batch", type=int, default=None, help="default: the config's batch")
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--sweep", default="100,1000,10000,100000,1000000")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-analytics", action="store_true")
@@ -163,17 +191,19 @@ def run_ours(args):
     dev = local
     from paper_1709_05061_b200.abi import load_library
     load_library().gpma_warmup(dev)  # load every kernel before any timed region
-    B = args.batch
+    cfg = CONFIGS[args.config]
+    nvx = cfg["nv"]
+    B = args.batch or cfg["batch"]
     K, W = args.steps, args.warmup
     t0 = time.time()
-    stream = pg.EdgeStream.rmat(NV, NE, seed=GEN_SEED + rank).shuffle(SHUFFLE_SEED)
+    stream = make_stream(pg, cfg, GEN_SEED + rank)
     gen_s = time.time() - t0
     win = pg.SlidingWindow(stream, dev)
     info = win.info()
     win.reserve((W + K) * B + 16)
     info = win.info()
     t1 = time.time()
-    g = pg.DynamicGraph.from_edges_device(NV, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
+    g = pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
     load_s = time.time() - t1
     cap = g.pma().capacity()
     slides = [win.slide(B) for _ in range(W + K)]
@@ -241,7 +271,7 @@ def run_ours(args):
     value = total_updates / (ms_max / 1e3)
 
     # ---- e2e through the host C ABI from pinned buffers (same slides) ----
-    g2 = pg.DynamicGraph.from_edges_device(NV, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
+    g2 = pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
     hs, hd = stream.arrays()
     host = []
     for s in slides:
@@ -306,10 +336,10 @@ def run_ours(args):
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
            "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "u64", "data": "synthetic: RMAT stream restated from generators.hpp (seed 1+rank, shuffle 2)",
-           "config": {"workload": "C2 Pokec-shaped sliding window: RMAT 2^21 vertices / 30.6M-edge stream, "
-                                  "15.3M-edge window, GPMA+ apply_batch per slide",
-                      "batch": B, "num_vertices": NV, "stream_edges": NE, "pma_capacity": cap,
+           "dtype": "u64", "data": f"synthetic: {cfg['gen'].upper()} stream restated from generators.hpp (seed 1+rank"
+                                   f"{', shuffle 2' if cfg['shuffle'] else ', generation order'})",
+           "config": {"workload": cfg["workload"],
+                      "batch": B, "num_vertices": nvx, "stream_edges": len(stream), "pma_capacity": cap,
                       "parallelism": f"dp{world} (independent source-range shards)",
                       "l2": "inputs larger than L2 (PMA slot array 1.1 GB per GPU)",
                       "deletion_mode": "lazy", "rounds_per_step": rounds / K},
@@ -318,10 +348,10 @@ def run_ours(args):
 
     if rank == 0 and not args.profile:
         if not args.no_analytics:
-            out["analytics"] = analytics(pg, g, ext)
-        out["sweep"] = sweep(pg, stream, dev, [int(x) for x in args.sweep.split(",") if x])
-        if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(stream, slides, win, W)
+            out["analytics"] = analytics(pg, g, ext, nvx)
+        out["sweep"] = sweep(pg, stream, dev, [int(x) for x in args.sweep.split(",") if x], nvx)
+        if world == 1 and not args.no_cpu_baseline and args.config in ("C1", "C2"):
+            out["cpu_baseline"] = cpu_baseline(stream, slides, win, W, nvx)
     if world > 1:
         torch.distributed.barrier()
     if rank == 0:
@@ -351,7 +381,7 @@ def run_sharded(args, rank, world, local):
 
     dev = local
     load_library().gpma_warmup(dev)
-    B, K, W = args.batch, args.steps, args.warmup
+    B, K, W = args.batch or 1_000_000, args.steps, args.warmup
     nv, ne = NV * world, NE * world
     t0 = time.time()
     stream = pg.EdgeStream.rmat(nv, ne, seed=GEN_SEED).shuffle(SHUFFLE_SEED)
@@ -523,10 +553,12 @@ def sharded_analytics(G, nv, rank):
     return out
 
 
-def analytics(pg, g, ext):
-    """Per-window analytic time on the live gapped graph (bench.hpp:226-313)."""
+def analytics(pg, g, ext, nv):
+    """Per-window analytic time on the live gapped graph (bench.hpp:226-313),
+    plus the PageRank iteration against the HBM roofline (SURVEY §8d:
+    9 C + 8 E + 36 |V| bytes per iteration)."""
     import torch
-    roots = pg.draw_below_sequence(ROOT_SEED, NV, 5)
+    roots = pg.draw_below_sequence(ROOT_SEED, nv, 5)
     bfs_ms, reached = [], []
     for r in roots:
         torch.cuda.synchronize()
@@ -553,14 +585,26 @@ def analytics(pg, g, ext):
     t = time.perf_counter()
     pr2 = pg.pagerank(g, warm_start=pr.ranks)
     pr2_ms = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
+    pr3 = pg.pagerank(g, warm_start=pr.ranks, epsilon=0.0, max_iters=10)  # 10 fixed iterations: the roofline
+    pr3_ms = (time.perf_counter() - t) * 1e3
+    it_ms = g.last_timing().rounds_ms / max(pr3.iterations, 1)
+    cap = g.pma().capacity()
+    ne = g.num_edges()
+    it_bytes = 9 * cap + 8 * ne + 36 * nv
+    peak, peak_kind = measured_peak()
     return {"bfs_ms_reference_roots": bfs_ms, "bfs_reached": reached,
             "bfs_ms_nonisolated_roots": [x[0] for x in hub_ms], "bfs_reached_nonisolated": [x[1] for x in hub_ms],
             "cc_ms": cc_ms, "pagerank_ms_cold": pr_ms, "pagerank_iters_cold": pr.iterations,
             "pagerank_ms_warm": pr2_ms, "pagerank_iters_warm": pr2.iterations,
-            "pagerank_iter_ms": g.last_timing().rounds_ms / max(pr2.iterations, 1)}
+            "pagerank_10_iters_ms": pr3_ms, "pagerank_iter_ms": it_ms,
+            "pagerank_iter_roofline": {"bound": "hbm", "algorithmic_bytes": it_bytes,
+                                       "achieved": it_bytes / (it_ms / 1e3) / 1e9 if it_ms > 0 else None,
+                                       "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                                       "frac": it_bytes / (it_ms / 1e3) / 1e9 / peak if it_ms > 0 else None}}
 
 
-def sweep(pg, stream, dev, batches):
+def sweep(pg, stream, dev, batches, nv):
     """updates/s vs batch size (device-resident inputs, 2 warmup + 3 timed slides)."""
     import torch
     res = {}
@@ -568,7 +612,7 @@ def sweep(pg, stream, dev, batches):
         win = pg.SlidingWindow(stream, dev)
         win.reserve(6 * B + 16)
         info = win.info()
-        g = pg.DynamicGraph.from_edges_device(NV, info.stream_src, info.stream_dst, None, info.initial_size,
+        g = pg.DynamicGraph.from_edges_device(nv, info.stream_src, info.stream_dst, None, info.initial_size,
                                               device=dev)
         slides = [win.slide(B) for _ in range(5)]
         info = win.info()
@@ -595,7 +639,7 @@ def sweep(pg, stream, dev, batches):
     return res
 
 
-def cpu_baseline(stream, slides, win, W):
+def cpu_baseline(stream, slides, win, W, nv):
     """The reference (oracle/_ref) on the host cores, bounded sample: its
     DynamicGraph over the same initial window, then 2 of the same slides
     through apply_batch with all hardware threads (steady_clock around the
@@ -606,7 +650,7 @@ def cpu_baseline(stream, slides, win, W):
     s, d = stream.arrays()
     half = (len(s) + 1) // 2
     t = time.time()
-    ref = oracle.RefGraph(NV, s[:half], d[:half])
+    ref = oracle.RefGraph(nv, s[:half], d[:half])
     build_s = time.time() - t
     cores = oracle.hardware_concurrency()
     ms_total, n_total = 0.0, 0
@@ -618,7 +662,7 @@ def cpu_baseline(stream, slides, win, W):
         ms_total += ms
         n_total += st.batch_size
     return {"value": n_total / (ms_total / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"2 slides of batch {slides[0].n_ins} on the C2 window via reference apply_batch "
+            "sample": f"2 slides of batch {slides[0].n_ins} on the same window via reference apply_batch "
                       f"({cores} workers); reference from_edges setup {build_s:.1f}s excluded"}
 
 
@@ -632,12 +676,18 @@ def run_reference(args):
     if not oracle.have_ref():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpmagraph_ref.so not built"}))
         return
-    B, K, W = args.batch, args.steps, args.warmup
+    cfg = CONFIGS[args.config]
+    B = args.batch or cfg["batch"]
+    K, W = args.steps, args.warmup
     cores = oracle.hardware_concurrency()
-    st = oracle.RefStream.rmat(NV, NE, seed=GEN_SEED).shuffle(SHUFFLE_SEED)
+    nvx = cfg["nv"]
+    st = (oracle.RefStream.rmat(nvx, int(cfg["param"]), seed=GEN_SEED) if cfg["gen"] == "rmat"
+          else oracle.RefStream.erdos_renyi(nvx, cfg["param"], seed=GEN_SEED))
+    if cfg["shuffle"] is not None:
+        st.shuffle(cfg["shuffle"])
     s, d, w, _ = st.arrays()
     half = (len(s) + 1) // 2
-    ref = oracle.RefGraph(NV, s[:half], d[:half], w[:half])
+    ref = oracle.RefGraph(nvx, s[:half], d[:half], w[:half])
     win = oracle.RefWindow(st)
     total_ms, total_n = 0.0, 0
     for i in range(W + K):
@@ -647,15 +697,21 @@ def run_reference(args):
             total_ms += ms
             total_n += stt.batch_size
     value = total_n / (total_ms / 1e3)
+    if world > 1:  # our arm: C2 per GPU over `world` key-range shards (run_sharded)
+        workload = (f"C2 per GPU, key-range sharded over {world} GPUs (the reference runs one C2-sized share of "
+                    f"it on the host cores: a bounded sample of the {world} x C2 workload)")
+        sample = (f"{K} slides of batch {B} (after {W} warmup) of one C2-sized share through the reference "
+                  f"DynamicGraph::apply_batch with {cores} workers")
+    else:
+        workload = cfg["workload"]
+        sample = (f"{K} slides of batch {B} (after {W} warmup) through the reference DynamicGraph::apply_batch "
+                  f"with {cores} workers")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
            "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "u64", "data": "synthetic: reference gen_rmat(2^21, 30.6M, seed 1) + shuffle 2",
-           "config": {"workload": "C2 Pokec-shaped sliding window: RMAT 2^21 vertices / 30.6M-edge stream, "
-                                  "15.3M-edge window, GPMA+ apply_batch per slide", "batch": B,
-                      "num_vertices": NV, "stream_edges": NE},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                            "sample": f"{K} slides of batch {B} (after {W} warmup) through the reference "
-                                      f"DynamicGraph::apply_batch with {cores} workers"},
+           "vs_baseline": None, "dtype": "u64",
+           "data": f"synthetic: reference generators ({cfg['gen']}, seed 1{', shuffle 2' if cfg['shuffle'] else ''})",
+           "config": {"workload": workload, "batch": B, "num_vertices": nvx, "stream_edges": len(s)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
