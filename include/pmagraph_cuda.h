@@ -303,6 +303,20 @@ int gpma_route_batch(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d
                      size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
                      const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w, uint64_t* counts);
 
+/* As gpma_route_batch, but the per-rank counts go to device memory d_counts
+ * (world u64) and nothing is synchronised: with gpma_set_stream on the
+ * caller's stream, routing, the NCCL exchange and the apply are
+ * stream-ordered without host round trips. */
+int gpma_route_batch_async(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
+                           size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
+                           const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
+                           uint64_t* d_counts);
+
+/* Run every later call on this handle on `stream` (a cudaStream_t; NULL is
+ * the legacy default stream), or back on the handle's own stream when `own`
+ * is non-zero.  Calls stay host-synchronous where they return host results. */
+int gpma_set_stream(gpma_graph* g, void* stream, int own);
+
 /* DynamicGraph::apply_batch (graph.hpp:130-162) on a routed batch: n
  * EdgeKeys with bit 63 = delete (inserts keep their arrival order among
  * themselves, which is all "last insert wins" needs), weights d_w (NULL =

@@ -207,6 +207,8 @@ SIGNATURES = [
     ("gpma_shard_range", C.c_int, [_P, _U64P, _U64P]),
     ("gpma_route_batch", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, _P, C.c_int, _P, _P, _U64P]),
     ("gpma_apply_batch_routed_device", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
+    ("gpma_route_batch_async", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, _P, C.c_int, _P, _P, _P]),
+    ("gpma_set_stream", C.c_int, [_P, _P, C.c_int]),
     ("gpma_shard_bfs_mark", C.c_int, [_P, _P, C.c_uint32, _P]),
     ("gpma_shard_bfs_update", C.c_int, [_P, _P, _P, C.c_uint32, _P, C.POINTER(C.c_uint32)]),
     ("gpma_shard_cc_hook", C.c_int, [_P, _P]),

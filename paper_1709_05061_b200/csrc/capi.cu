@@ -421,6 +421,23 @@ int gpma_route_batch(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d
     });
 }
 
+int gpma_route_batch_async(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
+                           size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
+                           const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
+                           uint64_t* d_counts) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->route_partition(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, d_bounds, world,
+                                 d_out_keys, d_out_w, nullptr, d_counts);
+    });
+}
+
+int gpma_set_stream(gpma_graph* g, void* stream, int own) {
+    if (!g || !g->impl) return PMA_EINVAL;
+    g->impl->pma.set_stream(static_cast<cudaStream_t>(stream), own != 0);
+    return PMA_OK;
+}
+
 int gpma_apply_batch_routed_device(gpma_graph* g, const uint64_t* d_keys, const double* d_w, size_t n,
                                    pma_stats* stats) {
     return guarded(err_of(g), [&] {

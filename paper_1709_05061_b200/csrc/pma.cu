@@ -63,7 +63,8 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     prof_ = profile ? *profile : pma_profile{0.08, 0.92, 0.40, 0.80, 1, 0};
     validate_profile(prof_);
     GPMA_CUDA(cudaSetDevice(device_));
-    GPMA_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    GPMA_CUDA(cudaStreamCreateWithFlags(&own_stream_, cudaStreamNonBlocking));
+    stream_ = own_stream_;
     GPMA_CUDA(cudaMalloc(&d_ctr, sizeof(Ctr)));
     GPMA_CUDA(cudaMallocHost(&h_ctr, sizeof(Ctr)));
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
@@ -83,7 +84,7 @@ Pma::~Pma() {
         if (e) cudaEventDestroy(e);
     for (auto& e : lev_ev_)
         if (e) cudaEventDestroy(e);
-    if (stream_) cudaStreamDestroy(stream_);
+    if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
 void Pma::free_arrays() {
@@ -246,7 +247,10 @@ __global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck,
             c = (u64(s) << db) | d;
         }
         if (ib) {
-            ck[i] = (c << ib) | i;  // packed: key above the arrival index (op = index < ni)
+            // packed: key above the arrival index for inserts, all-ones for
+            // deletes — among equal keys the inserts keep arrival order and the
+            // deletes sort after them, which is all duplicate resolution needs
+            ck[i] = (c << ib) | (ins ? u64(i) : ((1ull << ib) - 1));
         } else {
             ck[i] = c;
             ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
@@ -1444,7 +1448,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         nbits = 2 * db + 1;  // + the skip bit (guard deletes sort last)
         int ib = 1;
         while ((1ull << ib) < n) ++ib;
-        if (nbits + ib > 64 || gf->mk) ib = 0;  // no room (or ops not index-ordered): key + payload pairs
+        while ((1ull << ib) <= n) ++ib;  // the all-ones index is reserved for deletes
+        if (nbits + ib > 64) ib = 0;     // no room: key + payload pairs
         packed_ib = ib;
         k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
@@ -1521,13 +1526,13 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         const u64 skipkey = gf ? (1ull << (nbits - 1)) : ~0ull;
         const int pib = packed_ib;
         const u64 pmask = (1ull << pib) - 1;
-        const u64 gni = gf ? gf->ni : 0;
+
         // sorted element i -> compressed key / payload (arrival index << 1 | is_insert)
         auto KEY = [=] __device__(ull i) -> u64 { return pib ? (ck[i] >> pib) : ck[i]; };
         auto PAY = [=] __device__(ull i) -> u32 {
             if (!pib) return ci[i];
             const u32 a = u32(ck[i] & pmask);
-            return (a << 1) | (a < gni ? 1u : 0u);
+            return (a << 1) | (a != u32(pmask) ? 1u : 0u);  // all-ones index = a delete
         };
         u64* o_k = uk.ptr;
         u64* o_v = uv.ptr;

@@ -159,6 +159,9 @@ public:
     }
 
     cudaStream_t stream() const { return stream_; }
+    // run every call on a caller-provided stream (own: back to the handle's own;
+    // a null caller stream is the legacy default stream)
+    void set_stream(cudaStream_t s, bool own) { stream_ = own ? own_stream_ : s; }
     int device() const { return device_; }
     std::string err;
     pma_timing timing{};
@@ -200,6 +203,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
 
     int device_ = 0;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t own_stream_ = nullptr;  // created with the handle; stream_ may be a caller's stream
     pma_profile prof_{};
     u64 cap_ = 0, leaf_ = 4;
     int height_ = 0;

@@ -93,10 +93,12 @@ __global__ void k_route_scan(const u32* __restrict__ tile_counts, u64 ntiles, in
         run += tile_counts[i];
     }
     __syncthreads();
+    // owner r's updates = start of owner r + 1 - start of owner r (owner-major scan)
     for (int r = threadIdx.x; r < world; r += blockDim.x) {
-        u64 t = 0;
-        for (u64 k = 0; k < ntiles; ++k) t += tile_counts[u64(r) * ntiles + k];
-        totals[r] = t;
+        const u64 st = tile_offsets[u64(r) * ntiles];
+        const u64 en = u64(r + 1) < u64(world) ? tile_offsets[u64(r + 1) * ntiles]
+                                                : tile_offsets[m - 1] + tile_counts[m - 1];
+        totals[r] = en - st;
     }
 }
 
@@ -247,14 +249,17 @@ __global__ void k_pr_finish(const double* __restrict__ x, double* __restrict__ y
 // ================================================================ host side
 
 void Graph::route_partition(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
-                            u64 nd, const u32* d_bounds, int world, u64* okeys, double* ow, u64* h_counts) {
+                            u64 nd, const u32* d_bounds, int world, u64* okeys, double* ow, u64* h_counts,
+                            u64* d_counts) {
     if (world < 1 || world > kMaxWorld) throw ApiError(PMA_EINVAL, "route: world size must be in [1, 64]");
     if (nv > (1ull << 31)) throw ApiError(PMA_EINVAL, "route: vertex ids must be < 2^31 (bit 63 marks deletes)");
     cudaStream_t s = pma.stream();
     const RouteIn in{is, id, iw, ni, ds, dd, nd};
     const u64 n = ni + nd;
     if (n == 0) {
-        for (int r = 0; r < world; ++r) h_counts[r] = 0;
+        if (h_counts)
+            for (int r = 0; r < world; ++r) h_counts[r] = 0;
+        if (d_counts) GPMA_CUDA(cudaMemsetAsync(d_counts, 0, world * sizeof(u64), s));
         return;
     }
     const u64 ntiles = (n + kRouteTile - 1) / kRouteTile;
@@ -263,12 +268,15 @@ void Graph::route_partition(const u32* is, const u32* id, const double* iw, u64 
     rt_totals.reserve(world);
     k_route_hist<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_counts.ptr);
     GPMA_LAUNCH_CHECK();
-    k_route_scan<<<1, 1024, 0, s>>>(rt_counts.ptr, ntiles, world, rt_offsets.ptr, rt_totals.ptr);
+    u64* totals = d_counts ? d_counts : rt_totals.ptr;
+    k_route_scan<<<1, 1024, 0, s>>>(rt_counts.ptr, ntiles, world, rt_offsets.ptr, totals);
     GPMA_LAUNCH_CHECK();
     k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_offsets.ptr, okeys, ow);
     GPMA_LAUNCH_CHECK();
-    GPMA_CUDA(cudaMemcpyAsync(h_counts, rt_totals.ptr, world * sizeof(u64), cudaMemcpyDeviceToHost, s));
-    GPMA_CUDA(cudaStreamSynchronize(s));
+    if (h_counts) {  // host counts: one round trip; device counts: stream-ordered, no sync
+        GPMA_CUDA(cudaMemcpyAsync(h_counts, totals, world * sizeof(u64), cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
+    }
 }
 
 void Graph::shard_bfs_mark(const u32* frontier, u32 nf, u8* flags) {

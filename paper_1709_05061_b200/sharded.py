@@ -60,6 +60,8 @@ def _sync(t):
 class LocalComm:
     """All shards in this process; collectives are reductions over the list."""
 
+    stream_ordered = False
+
     def __init__(self, world: int):
         self.world = world
         self.ranks = list(range(world))
@@ -81,16 +83,18 @@ class LocalComm:
 
     def all_to_all_v(self, sends, send_counts):
         """sends[i]: local rank i's buffer, owner-major; send_counts[i][r]:
-        elements for rank r.  Returns per local rank the received buffer
-        (sender-rank order) and its per-sender counts."""
+        elements for rank r (list or device tensor).  Returns per local rank
+        the received buffer (sender-rank order), its per-sender counts, and
+        the send counts as lists."""
         torch = _torch()
+        send_counts = [c.cpu().tolist() if isinstance(c, torch.Tensor) else list(c) for c in send_counts]
         offs = [np.concatenate([[0], np.cumsum(c)]) for c in send_counts]
         recvs, rcounts = [], []
         for r in range(self.world):
             parts = [sends[s][int(offs[s][r]):int(offs[s][r + 1])] for s in range(self.world)]
             recvs.append(torch.cat(parts) if parts else sends[r][:0])
             rcounts.append([int(send_counts[s][r]) for s in range(self.world)])
-        return recvs, rcounts
+        return recvs, rcounts, send_counts
 
     def all_gather_v(self, pieces):
         torch = _torch()
@@ -99,7 +103,11 @@ class LocalComm:
 
 
 class TorchComm:
-    """One shard per process over torch.distributed (NCCL between GPUs)."""
+    """One shard per process over torch.distributed (NCCL between GPUs).
+    stream_ordered: the library runs on torch's current stream, so device
+    steps and collectives need no host synchronisation between them."""
+
+    stream_ordered = True
 
     _OPS = {"sum": "SUM", "max": "MAX", "min": "MIN"}
 
@@ -115,16 +123,20 @@ class TorchComm:
         self.dist.all_reduce(t, op=getattr(self.dist.ReduceOp, self._OPS[op]), group=self.group)
 
     def all_to_all_v(self, sends, send_counts):
+        """send_counts: per-rank counts as a list or as a device int64 tensor
+        (then the count exchange stays on the stream and one D2H brings both
+        the send and the receive counts)."""
         torch = _torch()
         (buf,), (cnt,) = sends, send_counts
-        sc = torch.as_tensor(np.asarray(cnt, np.int64), device=buf.device)
+        sc = cnt if isinstance(cnt, torch.Tensor) else torch.as_tensor(np.asarray(cnt, np.int64), device=buf.device)
         rc = torch.empty_like(sc)
         self.dist.all_to_all_single(rc, sc, group=self.group)
-        rcl = [int(x) for x in rc.cpu()]
+        both = torch.cat([sc, rc]).cpu().tolist()
+        scl, rcl = both[:self.world], both[self.world:]
         out = torch.empty(sum(rcl), dtype=buf.dtype, device=buf.device)
-        self.dist.all_to_all_single(out, buf, output_split_sizes=rcl, input_split_sizes=[int(x) for x in cnt],
+        self.dist.all_to_all_single(out, buf[:sum(scl)], output_split_sizes=rcl, input_split_sizes=scl,
                                     group=self.group)
-        return [out], [rcl]
+        return [out], [rcl], [scl]
 
     def all_gather_v(self, pieces):
         torch = _torch()
@@ -162,6 +174,10 @@ class ShardedGraph:
         torch = _torch()
         self._dbounds = [torch.as_tensor(self.bounds.astype(np.uint32).view(np.int32), device=f"cuda:{d}")
                          for d in devices]
+        self._ordered = getattr(comm, "stream_ordered", False)
+        if self._ordered:  # library calls on torch's stream: ordered with the NCCL collectives
+            for h, d in zip(self.h, devices):
+                self._lib.gpma_set_stream(h, C.c_void_p(torch.cuda.current_stream(d).cuda_stream), 0)
 
     # ---- construction
     @classmethod
@@ -196,6 +212,10 @@ class ShardedGraph:
         if rc:
             _raise(rc, self._lib.gpma_last_error(self.h[i]).decode())
 
+    def _sy(self, t):
+        if not self._ordered:
+            _sync(t)
+
     def range(self, i):
         r = self.comm.ranks[i]
         return int(self.bounds[r]), int(self.bounds[r + 1])
@@ -210,12 +230,15 @@ class ShardedGraph:
         n = ni + nd
         keys = torch.empty(max(n, 1), dtype=torch.int64, device=a.device)
         ow = torch.empty(max(n, 1), dtype=torch.float64, device=a.device) if w is not None else None
-        counts = (C.c_uint64 * self.comm.world)()
-        _sync(a)
-        self._check(i, self._lib.gpma_route_batch(self.h[i], _vp(a), _vp(b), _vp(w), ni, _vp(c), _vp(d), nd,
-                                                   _vp(self._dbounds[i]), self.comm.world, _vp(keys), _vp(ow),
-                                                   counts))
-        return keys[:n], (ow[:n] if ow is not None else None), [int(x) for x in counts]
+        counts = torch.empty(self.comm.world, dtype=torch.int64, device=a.device)
+        if not self._ordered:
+            _sync(a)
+        self._check(i, self._lib.gpma_route_batch_async(self.h[i], _vp(a), _vp(b), _vp(w), ni, _vp(c), _vp(d), nd,
+                                                         _vp(self._dbounds[i]), self.comm.world, _vp(keys), _vp(ow),
+                                                         _vp(counts)))
+        if not self._ordered:  # the async route ran on the library's own stream
+            torch.cuda.ExternalStream(self._lib.gpma_cuda_stream(self.h[i]), device=a.device).synchronize()
+        return keys[:n], (ow[:n] if ow is not None else None), counts
 
     def apply_batch(self, slices) -> ShardStats:
         """slices[i] = (ins_src, ins_dst, ins_w|None, del_src, del_dst):
@@ -232,12 +255,14 @@ class ShardedGraph:
             ks.append(k)
             ws.append(ww)
             cs.append(cnt)
-        rk, _ = self.comm.all_to_all_v(ks, cs)
-        rw = self.comm.all_to_all_v(ws, cs)[0] if ws[0] is not None else [None] * L
+        rk, _, scl = self.comm.all_to_all_v(ks, cs)
+        rw = self.comm.all_to_all_v(ws, scl)[0] if ws[0] is not None else [None] * L
+        cs = scl
         out, routed, sent = [], [], []
         for i in range(L):
             st = pma_stats()
-            _sync(rk[i])
+            if not self._ordered:
+                _sync(rk[i])
             self._check(i, self._lib.gpma_apply_batch_routed_device(self.h[i], _vp(rk[i]), _vp(rw[i]), rk[i].numel(),
                                                                      C.byref(st)))
             out.append(UpdateStats.from_c(st))
@@ -273,13 +298,13 @@ class ShardedGraph:
         depth = 0
         while True:
             for i in range(L):
-                _sync(fr[i])
+                self._sy(fr[i])
                 self._check(i, self._lib.gpma_shard_bfs_mark(self.h[i], _vp(fr[i]), nf[i], _vp(flags[i])))
             self.comm.all_reduce(flags, "max")
             depth += 1
             tot = []
             for i in range(L):
-                _sync(flags[i])
+                self._sy(flags[i])
                 c = C.c_uint32(0)
                 self._check(i, self._lib.gpma_shard_bfs_update(self.h[i], _vp(flags[i]), _vp(dist[i]), depth,
                                                                 _vp(nx[i]), C.byref(c)))
@@ -302,12 +327,12 @@ class ShardedGraph:
         while True:
             prev = [t.clone() for t in lab]
             for i in range(L):
-                _sync(lab[i])
+                self._sy(lab[i])
                 self._check(i, self._lib.gpma_shard_cc_hook(self.h[i], _vp(lab[i])))
             self.comm.all_reduce(lab, "min")
             ch = []
             for i in range(L):
-                _sync(lab[i])
+                self._sy(lab[i])
                 c = C.c_int(0)
                 self._check(i, self._lib.gpma_cc_jump(self.h[i], _vp(lab[i]), self.nv, _vp(prev[i]), C.byref(c)))
                 ch.append(torch.tensor([c.value], dtype=torch.int32, device=lab[i].device))
@@ -343,13 +368,13 @@ class ShardedGraph:
         it = 0
         for it in range(1, max_iters + 1):
             for i in range(L):
-                _sync(x[i])
-                _sync(od[i])
+                self._sy(x[i])
+                self._sy(od[i])
                 self._check(i, self._lib.gpma_shard_pr_push(self.h[i], _vp(x[i]), _vp(od[i]), damping, _vp(y[i])))
             self.comm.all_reduce(y, "sum")
             l1 = C.c_double(0)
             for i in range(L):
-                _sync(y[i])
+                self._sy(y[i])
                 self._check(i, self._lib.gpma_pr_finish(self.h[i], _vp(x[i]), _vp(y[i]), n, _vp(od[i]), damping,
                                                         C.byref(l1)))
             x, y = y, x
@@ -369,7 +394,7 @@ class ShardedGraph:
             dev = f"cuda:{self.devices[i]}"
             xi = x.to(dev) if isinstance(x, torch.Tensor) else torch.as_tensor(np.asarray(x, np.float64), device=dev)
             yl = torch.empty(max(hi - lo, 1), dtype=torch.float64, device=dev)
-            _sync(xi)
+            self._sy(xi)
             self._check(i, self._lib.gpma_shard_spmv(self.h[i], _vp(xi), _vp(yl)))
             pieces.append(yl[:hi - lo])
         return self.comm.all_gather_v(pieces)

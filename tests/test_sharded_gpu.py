@@ -137,6 +137,6 @@ def test_route_partition_is_stable_and_exact():
         dbit = (np.arange(n) >= ni).astype(np.uint64) << np.uint64(63)
         exp = ((src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64) | dbit)[order]
         wexp = np.where(np.arange(n) < ni, w, 1.0)[order]
-        assert counts == list(np.bincount(own, minlength=world))
+        assert counts.cpu().tolist() == list(np.bincount(own, minlength=world))
         assert (keys.cpu().numpy().view(np.uint64) == exp).all()
         assert (ow.cpu().numpy() == wexp).all()

@@ -114,7 +114,7 @@ def _comm_worker(rank, world, port, result_q):
         rng = np.random.default_rng(rank)
         cnt = [int(x) for x in rng.integers(0, 5, world)]
         buf = torch.tensor([1000 * rank + 10 * r + j for r in range(world) for j in range(cnt[r])], dtype=torch.int64)
-        (out,), (rc,) = c.all_to_all_v([buf], [cnt])
+        (out,), (rc,), _ = c.all_to_all_v([buf], [cnt])
         allc = [[int(x) for x in np.random.default_rng(s).integers(0, 5, world)] for s in range(world)]
         exp = [1000 * s + 10 * rank + j for s in range(world) for j in range(allc[s][rank])]
         ok = out.tolist() == exp and rc == [allc[s][rank] for s in range(world)]

@@ -44,7 +44,7 @@ def main():
         keys, ow, cnt = G._route(0, sl_t[0], sl_t[1], None, sl_t[3], sl_t[4])
         torch.cuda.synchronize()
         t1 = time.perf_counter()
-        rk, _ = G.comm.all_to_all_v([keys], [cnt])
+        rk, _, _ = G.comm.all_to_all_v([keys], [cnt])
         torch.cuda.synchronize()
         t2 = time.perf_counter()
         st = __import__("paper_1709_05061_b200.abi", fromlist=["pma_stats"]).pma_stats()
