@@ -559,6 +559,13 @@ def analytics(pg, g, ext, nv):
     9 C + 8 E + 36 |V| bytes per iteration)."""
     import torch
     roots = pg.draw_below_sequence(ROOT_SEED, nv, 5)
+    # steady state of a window loop: one untimed call of each analytic first
+    # (pinned result buffers of the caching host allocator, lazy module loads)
+    _w = pg.pagerank(g, max_iters=2)
+    _w2 = pg.pagerank(g, warm_start=_w.ranks, max_iters=2)
+    del _w, _w2
+    pg.bfs(g, 0)
+    pg.connected_components(g)
     bfs_ms, reached = [], []
     for r in roots:
         torch.cuda.synchronize()

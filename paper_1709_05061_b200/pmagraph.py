@@ -415,9 +415,25 @@ class DynamicGraph:
         return t
 
 
+_TORCH_DT = {np.uint32: "int32", np.float64: "float64"}
+
+
+def _host_out(n: int, dtype):
+    """Result vector for a device->host copy: page-locked (CUDA's caching host
+    allocator, block reused once the array is dropped) so the D2H runs at
+    full PCIe rate instead of through pageable staging; numpy when torch is
+    absent.  No zero fill: the library writes every element."""
+    try:
+        import torch
+        t = torch.empty(max(n, 1), dtype=getattr(torch, _TORCH_DT[dtype]), pin_memory=True)
+        return t.numpy().view(dtype)[:n]
+    except Exception:  # pragma: no cover - CPU-only environments
+        return np.empty(n, dtype)
+
+
 def bfs(g: DynamicGraph, root: int, return_reached: bool = False):
     """analytics.hpp:22-48"""
-    dist = np.zeros(g.num_vertices(), np.uint32)
+    dist = _host_out(g.num_vertices(), np.uint32)
     reached = C.c_uint64()
     g._check(g._lib.gpma_bfs(g.h, C.c_uint32(root), _p(dist), C.byref(reached)))
     return (dist, reached.value) if return_reached else dist
@@ -425,7 +441,7 @@ def bfs(g: DynamicGraph, root: int, return_reached: bool = False):
 
 def connected_components(g: DynamicGraph):
     """analytics.hpp:53-82"""
-    lab = np.zeros(g.num_vertices(), np.uint32)
+    lab = _host_out(g.num_vertices(), np.uint32)
     g._check(g._lib.gpma_cc(g.h, _p(lab)))
     return lab
 
@@ -435,7 +451,7 @@ def pagerank(g: DynamicGraph, damping: float = 0.85, epsilon: float = 1e-3, max_
     """analytics.hpp:90-143"""
     if warm_start is not None and len(warm_start) != g.num_vertices():
         raise ValueError("pagerank: warm start size mismatch")
-    ranks = np.zeros(g.num_vertices(), np.float64)
+    ranks = _host_out(g.num_vertices(), np.float64)
     it = C.c_uint64()
     conv = C.c_int()
     w = _f64(warm_start)
@@ -449,7 +465,7 @@ def spmv(g: DynamicGraph, x):
     if len(x) != g.num_vertices():
         raise ValueError("spmv: dimension mismatch")
     xx = _f64(x)
-    y = np.zeros(g.num_vertices(), np.float64)
+    y = _host_out(g.num_vertices(), np.float64)
     g._check(g._lib.gpma_spmv(g.h, _p(xx), _p(y)))
     return y
 
