@@ -612,7 +612,8 @@ def analytics(pg, g, ext, nv):
 
 
 def sweep(pg, stream, dev, batches, nv):
-    """updates/s vs batch size (device-resident inputs, 2 warmup + 3 timed slides)."""
+    """updates/s vs batch size (device-resident inputs, 2 warmup + 3 timed slides),
+    GPMA+ and the rebuild-the-CSR-per-batch baseline on the same slides."""
     import torch
     res = {}
     for B in batches:
@@ -642,7 +643,30 @@ def sweep(pg, stream, dev, batches, nv):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
         res[str(B)] = {"updates_per_s": n / (ms / 1e3), "us_per_batch": ms * 1e3 / 3}
-        del g, win
+        del g
+        # the paper's comparison point on the same slides: the CSR rebuilt per
+        # batch (RebuildCsrGraph, baselines.hpp:85-181) on the device
+        r = pg.RebuildCsrGraph.from_edges_device(nv, info.stream_src, info.stream_dst, None, info.initial_size,
+                                                 device=dev)
+        rext = torch.cuda.ExternalStream(r._lib.gpma_rebuild_cuda_stream(r.h), device=torch.device("cuda", dev))
+
+        def rgo(s):
+            return r.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset,
+                                        None, s.n_ins, info.del_src + 4 * s.del_offset,
+                                        info.del_dst + 4 * s.del_offset, s.n_del)
+        for s in slides[:2]:
+            rgo(s)
+        torch.cuda.synchronize()
+        e0.record(rext)
+        n = 0
+        for s in slides[2:]:
+            n += rgo(s).batch_size
+        e1.record(rext)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        res[str(B)]["rebuild_csr_updates_per_s"] = n / (ms / 1e3)
+        res[str(B)]["rebuild_csr_us_per_batch"] = ms * 1e3 / 3
+        del r, win
     return res
 
 

@@ -359,6 +359,38 @@ int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local);
  * loading never lands inside a timed region (call once per process/device). */
 int gpma_warmup(int device);
 
+/* ---- Rebuild-CSR baseline (the paper's rebuild-per-batch comparison point)
+ * RebuildCsrGraph (baselines.hpp:85-181) on the device: sorted unique edge
+ * list + CSR arrays rebuilt from scratch after every batch.  Same contract as
+ * the reference: construction rejects ids >= num_vertices with PMA_EINVAL
+ * ("RebuildCsrGraph: vertex id out of range", baselines.hpp:91-93) and keeps
+ * the last of duplicate edges (dedupe_last_wins, :160-167); a batch resolves
+ * duplicates last-insert-wins (segment_engine.hpp:346-363), counts absent
+ * deletes in deletes_missed and reports slot_writes = 2|E| + |V| + 1
+ * (:153).  Vertex ids of a batch must be < num_vertices (the reference
+ * indexes counts[] with them, :171). */
+typedef struct gpma_rebuild gpma_rebuild;
+
+/* RebuildCsrGraph(num_vertices, edges) — baselines.hpp:87-98 (host arrays; w may be NULL = 1.0) */
+int gpma_rebuild_create(int device, size_t num_vertices, const uint32_t* src, const uint32_t* dst, const double* w,
+                        size_t n, gpma_rebuild** out);
+int gpma_rebuild_create_device(int device, size_t num_vertices, const uint32_t* d_src, const uint32_t* d_dst,
+                               const double* d_w, size_t n, gpma_rebuild** out);
+int gpma_rebuild_destroy(gpma_rebuild* r);
+const char* gpma_rebuild_last_error(const gpma_rebuild* r);
+/* RebuildCsrGraph::apply_batch — baselines.hpp:114-155 */
+int gpma_rebuild_apply_batch(gpma_rebuild* r, const uint32_t* ins_src, const uint32_t* ins_dst, const double* ins_w,
+                             size_t n_ins, const uint32_t* del_src, const uint32_t* del_dst, size_t n_del,
+                             pma_stats* stats);
+int gpma_rebuild_apply_batch_device(gpma_rebuild* r, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
+                                    const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
+                                    const uint32_t* d_del_dst, size_t n_del, pma_stats* stats);
+/* RebuildCsrGraph::csr_snapshot — baselines.hpp:157-158: row_offsets has
+ * num_vertices + 1 entries, col / vals num_edges */
+int gpma_rebuild_csr(gpma_rebuild* r, uint64_t* row_offsets, uint32_t* col, double* vals);
+uint64_t gpma_rebuild_num_edges(const gpma_rebuild* r);
+void* gpma_rebuild_cuda_stream(gpma_rebuild* r);
+
 #ifdef __cplusplus
 }
 #endif

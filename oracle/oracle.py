@@ -76,7 +76,7 @@ def ref_lib():
         _ref = C.CDLL(REF_SO)
         _ref.ref_last_error.restype = C.c_char_p
         for n in ("ref_stream_size", "ref_stream_num_vertices", "ref_window_size", "ref_window_remaining",
-                  "ref_graph_num_edges"):
+                  "ref_graph_num_edges", "ref_rebuild_num_edges"):
             getattr(_ref, n).restype = C.c_uint64
         _ref.ref_hardware_concurrency.restype = C.c_uint
     return _ref
@@ -478,3 +478,36 @@ def hardware_concurrency():
 
 __all__ = ["RefPMA", "PortPMA", "RefGraph", "PortGraph", "RefStream", "RefWindow", "OracleError", "build",
            "have_ref", "stats_dict", "draw_below_sequence", "hardware_concurrency", "PMA_MAX_LEVELS"]
+
+
+class RefRebuildCsr:
+    """The reference RebuildCsrGraph (baselines.hpp:85-181) — test oracle of
+    the GPU rebuild-CSR baseline."""
+
+    def __init__(self, nv, src, dst, w=None):
+        self.nv = nv
+        s, d, ww = _u32(src), _u32(dst), _f64(w)
+        self.h = C.c_void_p()
+        _check(ref_lib(), ref_lib().ref_rebuild_create(C.c_size_t(nv), _p(s), _p(d), _p(ww), C.c_size_t(len(s)),
+                                                      C.byref(self.h)), "ref_last_error")
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_rebuild_destroy(self.h)
+            self.h = None
+
+    def apply_batch(self, ins_src, ins_dst, ins_w, del_src, del_dst):
+        a, b, w = _u32(ins_src), _u32(ins_dst), _f64(ins_w)
+        c, d = _u32(del_src), _u32(del_dst)
+        st = pma_stats()
+        _check(ref_lib(), ref_lib().ref_rebuild_apply_batch(self.h, _p(a), _p(b), _p(w), C.c_size_t(len(a)), _p(c),
+                                                           _p(d), C.c_size_t(len(c)), C.byref(st)), "ref_last_error")
+        return st
+
+    def csr(self):
+        ne = int(ref_lib().ref_rebuild_num_edges(self.h))
+        ro = np.zeros(self.nv + 1, np.uint64)
+        col = np.zeros(max(ne, 1), np.uint32)
+        val = np.zeros(max(ne, 1), np.float64)
+        _check(ref_lib(), ref_lib().ref_rebuild_csr(self.h, _p(ro), _p(col), _p(val)), "ref_last_error")
+        return ro, col[:ne], val[:ne]

@@ -6,12 +6,13 @@
 // bench.py's cpu_baseline / --impl reference leg can drive it via ctypes.
 // Nothing here is copied from the reference: this file only calls its public
 // API (pma.hpp, segment_engine.hpp, graph.hpp, analytics.hpp, streaming.hpp,
-// generators.hpp).  The POD structs are shared with the product ABI
+// generators.hpp, baselines.hpp).  The POD structs are shared with the product ABI
 // (include/pmagraph_cuda.h) so results compare field by field.
 //
 // Output: oracle/_ref/libpmagraph_ref.so (git-ignored, travels to the GPU box).
 
 #include <pmagraph/analytics.hpp>
+#include <pmagraph/baselines.hpp>
 #include <pmagraph/generators.hpp>
 #include <pmagraph/graph.hpp>
 #include <pmagraph/pma.hpp>
@@ -374,6 +375,54 @@ int ref_graph_csr_snapshot(ref_graph* g, uint64_t* ro, uint32_t* col, double* va
         for (size_t i = 0; i < s.col_indices.size(); ++i) {
             col[i] = s.col_indices[i];
             val[i] = s.values[i];
+        }
+    });
+}
+
+// RebuildCsrGraph (baselines.hpp:85-181): the rebuild-the-CSR-per-batch
+// baseline of the paper's comparison.
+struct ref_rebuild {
+    std::optional<RebuildCsrGraph> g;
+};
+
+int ref_rebuild_create(size_t nv, const uint32_t* src, const uint32_t* dst, const double* w, size_t n,
+                       ref_rebuild** out) {
+    return guarded([&] {
+        std::vector<WeightedEdge> edges(n);
+        for (size_t i = 0; i < n; ++i) edges[i] = WeightedEdge{src[i], dst[i], w ? w[i] : 1.0};
+        auto* g = new ref_rebuild{};
+        try {
+            g->g.emplace(nv, edges);
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+    });
+}
+
+void ref_rebuild_destroy(ref_rebuild* g) { delete g; }
+
+uint64_t ref_rebuild_num_edges(ref_rebuild* g) { return g->g->num_edges(); }
+
+int ref_rebuild_apply_batch(ref_rebuild* g, const uint32_t* is, const uint32_t* id, const double* iw, size_t ni,
+                            const uint32_t* ds, const uint32_t* dd, size_t nd, pma_stats* out) {
+    return guarded([&] {
+        std::vector<WeightedEdge> ins(ni);
+        for (size_t i = 0; i < ni; ++i) ins[i] = WeightedEdge{is[i], id[i], iw ? iw[i] : 1.0};
+        std::vector<std::pair<VertexId, VertexId>> del(nd);
+        for (size_t i = 0; i < nd; ++i) del[i] = {ds[i], dd[i]};
+        fill_stats(g->g->apply_batch(ins, del), out);
+    });
+}
+
+int ref_rebuild_csr(ref_rebuild* g, uint64_t* ro, uint32_t* col, double* val) {
+    return guarded([&] {
+        const CsrSnapshot& c = g->g->csr();
+        for (size_t i = 0; i < c.row_offsets.size(); ++i) ro[i] = c.row_offsets[i];
+        for (size_t i = 0; i < c.col_indices.size(); ++i) {
+            col[i] = c.col_indices[i];
+            val[i] = c.values[i];
         }
     });
 }

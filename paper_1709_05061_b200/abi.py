@@ -218,6 +218,15 @@ SIGNATURES = [
     ("gpma_pr_finish", C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_double, C.POINTER(C.c_double)]),
     ("gpma_shard_spmv", C.c_int, [_P, _P, _P]),
     ("gpma_warmup", C.c_int, [C.c_int]),
+    ("gpma_rebuild_create", C.c_int, [C.c_int, C.c_size_t, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
+    ("gpma_rebuild_create_device", C.c_int, [C.c_int, C.c_size_t, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
+    ("gpma_rebuild_destroy", C.c_int, [_P]),
+    ("gpma_rebuild_last_error", C.c_char_p, [_P]),
+    ("gpma_rebuild_apply_batch", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
+    ("gpma_rebuild_apply_batch_device", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
+    ("gpma_rebuild_csr", C.c_int, [_P, _P, _P, _P]),
+    ("gpma_rebuild_num_edges", C.c_uint64, [_P]),
+    ("gpma_rebuild_cuda_stream", _P, [_P]),
     # pmagraph_stream.h
     ("gpma_stream_last_error", C.c_char_p, []),
     ("gpma_stream_rmat", C.c_int, [C.c_size_t, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(_P)]),

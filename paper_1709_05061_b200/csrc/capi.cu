@@ -606,6 +606,15 @@ extern "C" int gpma_warmup(int device) {
         gpma_row_offsets(g, ro.data());
         gpma_csr_snapshot(g, ro.data(), col.data(), vals.data());
         gpma_destroy(g);
+        {  // rebuild-CSR baseline (rebuild.cu)
+            gpma_rebuild* rb = nullptr;
+            if (gpma_rebuild_create(device, nv, s.data(), d.data(), nullptr, ne, &rb))
+                throw ApiError(PMA_ECUDA, gpma_rebuild_last_error(nullptr));
+            gpma_rebuild_apply_batch(rb, s.data(), d.data() + 1, nullptr, 500, s.data() + 500, d.data() + 500, 500,
+                                     &st);
+            gpma_rebuild_csr(rb, ro.data(), col.data(), vals.data());
+            gpma_rebuild_destroy(rb);
+        }
         {  // key-range sharding path (shard.cu): shard build, routing, routed apply, sharded analytics
             uint32_t *ds_ = nullptr, *dd_ = nullptr, *db_ = nullptr, *fr_ = nullptr, *dl_ = nullptr, *lab_ = nullptr,
                      *pv_ = nullptr, *od_ = nullptr;

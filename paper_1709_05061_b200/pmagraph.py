@@ -415,6 +415,76 @@ class DynamicGraph:
         return t
 
 
+class RebuildCsrGraph:
+    """The rebuild-the-CSR-per-batch baseline (baselines.hpp:85-181) on the
+    device: the comparison point GPMA+ is measured against in the paper."""
+
+    def __init__(self, num_vertices: int, src=(), dst=(), weights=None, device: int = 0, _handle=None):
+        self._lib = load_library()
+        self._nv = num_vertices
+        if _handle is not None:
+            self.h = _handle
+            return
+        s, d, w = _u32(src), _u32(dst), _f64(weights)
+        self.h = C.c_void_p()
+        rc = self._lib.gpma_rebuild_create(device, num_vertices, _p(s), _p(d), _p(w), len(s), C.byref(self.h))
+        if rc:
+            self.h = None
+            _raise(rc, self._lib.gpma_rebuild_last_error(None).decode())
+
+    @classmethod
+    def from_edges_device(cls, num_vertices: int, d_src: int, d_dst: int, d_w: int | None, n: int,
+                          device: int = 0) -> "RebuildCsrGraph":
+        lib = load_library()
+        h = C.c_void_p()
+        rc = lib.gpma_rebuild_create_device(device, num_vertices, C.c_void_p(d_src), C.c_void_p(d_dst),
+                                            C.c_void_p(d_w) if d_w else None, n, C.byref(h))
+        if rc:
+            _raise(rc, lib.gpma_rebuild_last_error(None).decode())
+        return cls(num_vertices, _handle=h)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.gpma_rebuild_destroy(self.h)
+            self.h = None
+
+    def _check(self, rc):
+        if rc:
+            _raise(rc, self._lib.gpma_rebuild_last_error(self.h).decode())
+
+    def num_vertices(self) -> int:
+        return self._nv
+
+    def num_edges(self) -> int:
+        return int(self._lib.gpma_rebuild_num_edges(self.h))
+
+    def apply_batch(self, ins_src, ins_dst, ins_w, del_src, del_dst) -> UpdateStats:
+        a, b, w = _u32(ins_src), _u32(ins_dst), _f64(ins_w)
+        c, d = _u32(del_src), _u32(del_dst)
+        st = pma_stats()
+        self._check(self._lib.gpma_rebuild_apply_batch(self.h, _p(a), _p(b), _p(w), len(a), _p(c), _p(d), len(c),
+                                                       C.byref(st)))
+        return UpdateStats.from_c(st)
+
+    def apply_batch_device(self, d_is: int, d_id: int, d_iw: int | None, ni: int, d_ds: int, d_dd: int,
+                           nd: int) -> UpdateStats:
+        st = pma_stats()
+        vp = C.c_void_p
+        self._check(self._lib.gpma_rebuild_apply_batch_device(self.h, vp(d_is), vp(d_id), vp(d_iw) if d_iw else None,
+                                                              ni, vp(d_ds), vp(d_dd), nd, C.byref(st)))
+        return UpdateStats.from_c(st)
+
+    def csr_snapshot(self):
+        ne = self.num_edges()
+        ro = np.zeros(self._nv + 1, np.uint64)
+        col = np.zeros(max(ne, 1), np.uint32)
+        val = np.zeros(max(ne, 1), np.float64)
+        self._check(self._lib.gpma_rebuild_csr(self.h, _p(ro), _p(col), _p(val)))
+        return ro, col[:ne], val[:ne]
+
+    csr = csr_snapshot
+
+
 _TORCH_DT = {np.uint32: "int32", np.float64: "float64"}
 
 

@@ -73,6 +73,28 @@ def test_reference_csr_of_worked_example():
     assert list(ro) == [0, 2, 3, 6] and list(col) == [0, 2, 2, 0, 1, 2] and list(val) == [1, 2, 3, 4, 5, 6]
 
 
+def test_reference_rebuild_csr_baseline():
+    """RebuildCsrGraph (baselines.hpp:85-181), the oracle of the GPU baseline:
+    the worked example, one batch, and agreement with the PMA graph's CSR."""
+    r = oracle.RefRebuildCsr(3, [0, 0, 1, 2, 2, 2], [0, 2, 2, 0, 1, 2], [1.0, 2.0, 3.0, 4.0, 5.0, 6.0])
+    ro, col, val = r.csr()
+    assert list(ro) == [0, 2, 3, 6] and list(col) == [0, 2, 2, 0, 1, 2] and list(val) == [1, 2, 3, 4, 5, 6]
+    st = r.apply_batch([1], [0], [7.0], [0, 2], [2, 9])
+    assert (st.batch_size, st.deletes_missed, st.slot_writes) == (3, 1, 16)
+    ro, col, val = r.csr()
+    assert list(ro) == [0, 1, 3, 6] and list(col) == [0, 0, 2, 0, 1, 2] and list(val) == [1, 7, 3, 4, 5, 6]
+    with pytest.raises(oracle.OracleError, match="vertex id out of range"):
+        oracle.RefRebuildCsr(3, [0], [3])
+    rng = np.random.default_rng(4)
+    s, d = rng.integers(0, 500, 4000), rng.integers(0, 500, 4000)
+    r, g = oracle.RefRebuildCsr(500, s, d), RefGraph(500, s, d)
+    for _ in range(3):
+        a, b, c, e = (rng.integers(0, 500, 800) for _ in range(4))
+        r.apply_batch(a, b, None, c, e)
+        g.apply_batch(a, b, None, c, e)
+        assert all((x == y).all() for x, y in zip(r.csr(), g.csr_snapshot()))
+
+
 @pytest.mark.parametrize("name", ["window_er.npz", "window_rmat.npz"])
 @pytest.mark.parametrize("G", GRAPHS)
 def test_golden_windows(name, G):
