@@ -312,11 +312,15 @@ int gpma_apply_batch(gpma_graph* g, const uint32_t* ins_src, const uint32_t* ins
         auto& p = g->impl->pma;
         GPMA_CUDA(cudaSetDevice(p.device()));
         const auto t0 = std::chrono::steady_clock::now();
-        const uint32_t* a = p.stage(p.stage_a, ins_src, n_ins);
-        const uint32_t* b = p.stage(p.stage_b, ins_dst, n_ins);
+        // Endpoint arrays are read exactly once, in order, by the front-end
+        // kernel: page-locked ones are read in place over PCIe (zero-copy,
+        // the transfer overlaps the packing), pageable ones staged first.
+        // Weights are gathered by arrival index later, so they are staged.
+        const uint32_t* a = p.stage_or_map(p.stage_a, ins_src, n_ins);
+        const uint32_t* b = p.stage_or_map(p.stage_b, ins_dst, n_ins);
         const double* w = ins_w ? p.stage(p.stage_w, ins_w, n_ins) : nullptr;
-        const uint32_t* c = p.stage(p.stage_c, del_src, n_del);
-        const uint32_t* d = p.stage(p.stage_d, del_dst, n_del);
+        const uint32_t* c = p.stage_or_map(p.stage_c, del_src, n_del);
+        const uint32_t* d = p.stage_or_map(p.stage_d, del_dst, n_del);
         g->impl->apply_batch_device(a, b, w, n_ins, c, d, n_del, out);
         if (out)
             out->wall_ns = uint64_t(

@@ -210,62 +210,101 @@ __global__ void k_compress(const u64* keys, const u8* ops, u64 n, BitRuns runs, 
 // bits: LSD radix is stable, so this is the same order at 16 instead of 24
 // bytes per element per pass.  A non-guard delete outside the layout raises
 // `oor` (the batch is then redone on the generic path).
-__global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
-    const u64 n = f.ni + f.nd;
-    const u64 lim = 1ull << db;
+struct PrepAcc {
     ull guards = 0, bad = 0, oor = 0;
-    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
-        u32 s, d;
-        bool ins, skip = false;
-        if (f.mk) {
+};
+
+__device__ __forceinline__ void prep_one(const GraphFront& f, int db, int ib, u64* ck, u32* ci, u64 i, u32 s, u32 d,
+                                         bool ins, PrepAcc& acc) {
+    const u64 lim = 1ull << db;
+    bool skip = false;
+    if (ins) {
+        if (s < f.lo || s >= f.hi || d >= f.nv) acc.bad = max(acc.bad, ~ull(i));  // first offending insert
+    } else {
+        skip = d == u32(kGuardDst);
+        acc.guards += skip;
+    }
+    u64 c;
+    if (skip) {
+        c = 1ull << (2 * db);
+    } else if (s >= lim || d >= lim) {
+        c = 0;
+        acc.oor |= !ins;
+    } else {
+        c = (u64(s) << db) | d;
+    }
+    if (ib) {
+        // packed: key above the arrival index for inserts, all-ones for
+        // deletes — among equal keys the inserts keep arrival order and the
+        // deletes sort after them, which is all duplicate resolution needs
+        ck[i] = (c << ib) | (ins ? u64(i) : ((1ull << ib) - 1));
+    } else {
+        ck[i] = c;
+        ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
+    }
+}
+
+// one endpoint-array segment (inserts or deletes): 16-byte vector loads when
+// both arrays are aligned alike — the arrays may be page-locked host memory
+// read in place over PCIe, where wide requests are what keeps the link busy
+__device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib, u64* ck, u32* ci, const u32* sa,
+                                             const u32* da, u64 n, u64 base, bool ins, PrepAcc& acc) {
+    const u64 tid = blockIdx.x * u64(blockDim.x) + threadIdx.x, nt = u64(gridDim.x) * blockDim.x;
+    u64 head = 0;
+    if ((reinterpret_cast<uintptr_t>(sa) & 15) == (reinterpret_cast<uintptr_t>(da) & 15) &&
+        (reinterpret_cast<uintptr_t>(sa) & 3) == 0) {
+        head = ((16 - (reinterpret_cast<uintptr_t>(sa) & 15)) & 15) / 4;
+        if (head > n) head = n;
+        const u64 nq = (n - head) / 4;
+        const uint4* s4 = reinterpret_cast<const uint4*>(sa + head);
+        const uint4* d4 = reinterpret_cast<const uint4*>(da + head);
+        for (u64 q = tid; q < nq; q += nt) {
+            const uint4 a = s4[q], b = d4[q];
+            const u64 i = base + head + 4 * q;
+            prep_one(f, db, ib, ck, ci, i, a.x, b.x, ins, acc);
+            prep_one(f, db, ib, ck, ci, i + 1, a.y, b.y, ins, acc);
+            prep_one(f, db, ib, ck, ci, i + 2, a.z, b.z, ins, acc);
+            prep_one(f, db, ib, ck, ci, i + 3, a.w, b.w, ins, acc);
+        }
+        // scalar head and tail
+        for (u64 j = tid; j < head; j += nt) prep_one(f, db, ib, ck, ci, base + j, sa[j], da[j], ins, acc);
+        for (u64 j = head + 4 * nq + tid; j < n; j += nt) prep_one(f, db, ib, ck, ci, base + j, sa[j], da[j], ins, acc);
+        return;
+    }
+    for (u64 j = tid; j < n; j += nt) prep_one(f, db, ib, ck, ci, base + j, sa[j], da[j], ins, acc);
+}
+
+// Graph-mode front end (DynamicGraph::apply_batch, graph.hpp:133-147): check
+// insert ids, count guard deletes, and emit the sort input with the
+// |V|-derived compressed layout (src << db | dst); guard deletes (dropped by
+// the reference before the engine) get key 1 << 2db and sort last.  Payload =
+// arrival index << 1 | is_insert — or, when key and index fit one word
+// (ib > 0), the single u64 (key << ib | index), sorted keys-only on the key
+// bits: LSD radix is stable, so this is the same order at 16 instead of 24
+// bytes per element per pass.  A non-guard delete outside the layout raises
+// `oor` (the batch is then redone on the generic path).
+__global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
+    PrepAcc acc;
+    if (f.mk) {
+        const u64 n = f.ni + f.nd;
+        for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
             const u64 k = f.mk[i];
-            ins = !(k >> 63);
-            s = src_of(k) & 0x7FFFFFFFu;
-            d = dst_of(k);
-        } else if (i < f.ni) {
-            ins = true;
-            s = f.is[i];
-            d = f.id[i];
-        } else {
-            ins = false;
-            s = f.ds[i - f.ni];
-            d = f.dd[i - f.ni];
+            prep_one(f, db, ib, ck, ci, i, src_of(k) & 0x7FFFFFFFu, dst_of(k), !(k >> 63), acc);
         }
-        if (ins) {
-            if (s < f.lo || s >= f.hi || d >= f.nv) bad = max(bad, ~ull(i));  // first offending insert
-        } else {
-            skip = d == u32(kGuardDst);
-            guards += skip;
-        }
-        u64 c;
-        if (skip) {
-            c = 1ull << (2 * db);
-        } else if (s >= lim || d >= lim) {
-            c = 0;
-            oor |= !ins;
-        } else {
-            c = (u64(s) << db) | d;
-        }
-        if (ib) {
-            // packed: key above the arrival index for inserts, all-ones for
-            // deletes — among equal keys the inserts keep arrival order and the
-            // deletes sort after them, which is all duplicate resolution needs
-            ck[i] = (c << ib) | (ins ? u64(i) : ((1ull << ib) - 1));
-        } else {
-            ck[i] = c;
-            ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
-        }
+    } else {
+        if (f.ni) prep_segment(f, db, ib, ck, ci, f.is, f.id, f.ni, 0, true, acc);
+        if (f.nd) prep_segment(f, db, ib, ck, ci, f.ds, f.dd, f.nd, f.ni, false, acc);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
-        guards += __shfl_xor_sync(FULL, guards, d);
-        bad = max(bad, __shfl_xor_sync(FULL, bad, d));
-        oor |= __shfl_xor_sync(FULL, oor, d);
+        acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
+        acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
+        acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
     }
     if ((threadIdx.x & 31) == 0) {
-        if (guards) atomicAdd(&ctr->gdel, guards);
-        if (bad) atomicMax(&ctr->bad_ins, bad);
-        if (oor) atomicOr(&ctr->oor, 1ull);
+        if (acc.guards) atomicAdd(&ctr->gdel, acc.guards);
+        if (acc.bad) atomicMax(&ctr->bad_ins, acc.bad);
+        if (acc.oor) atomicOr(&ctr->oor, 1ull);
     }
 }
 

@@ -158,6 +158,19 @@ public:
         return buf.ptr;
     }
 
+    // a page-locked host array the device can read in place (UVA: the device
+    // pointer of a cudaHostAlloc / cudaHostRegister block), else a staged copy
+    template <class T>
+    const T* stage_or_map(DevBuf<T>& buf, const T* host, size_t n) {
+        if (!n) return stage(buf, host, n);
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, host) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+            at.devicePointer != nullptr)
+            return static_cast<const T*>(at.devicePointer);
+        cudaGetLastError();  // pageable memory: not an error worth keeping
+        return stage(buf, host, n);
+    }
+
     cudaStream_t stream() const { return stream_; }
     // run every call on a caller-provided stream (own: back to the handle's own;
     // a null caller stream is the legacy default stream)

@@ -195,3 +195,36 @@ def test_large_batches_parity(mode):
         assert gs.parity() == ref_parity(r, rs), ctx
         assert_same_slots(g.pma().slots(), r.slots(), ctx)
         assert (g.row_offsets() == r.row_offsets()).all(), ctx
+
+
+def test_pinned_host_batches_read_in_place():
+    """gpma_apply_batch reads page-locked endpoint arrays in place over PCIe
+    (zero-copy) and stages pageable ones: both give the reference's result."""
+    torch = pytest.importorskip("torch")
+    stream = _window_stream("rmat", 2**12, 30000)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    g = DynamicGraph.from_edges(2**12, s[:half], d[:half], w[:half])
+    r = RefGraph(2**12, s[:half], d[:half], w[:half])
+    win = RefWindow(stream)
+
+    def pin(x, off=0):
+        t = torch.empty(len(x) + 3, dtype=torch.int32).pin_memory()
+        v = t.numpy().view(np.uint32)[off:off + len(x)]  # off: 16-byte misaligned starts
+        v[:] = x
+        return v, t
+
+    for slide in range(6):
+        a, b, ww, c, dd = win.slide(1500 + slide)
+        if slide % 2 == 0:
+            o = slide // 2
+            (a, _ta), (b, _tb), (c, _tc), (dd, _td) = pin(a, o), pin(b, o), pin(c, (o + 1) % 3), pin(dd, o)
+        gs = g.apply_batch(a, b, ww, c, dd)
+        rs = r.apply_batch(a, b, ww, c, dd)
+        assert gs.parity() == ref_parity(r, rs), slide
+        assert_same_slots(g.pma().slots(), r.slots(), f"slide {slide}")
+    # a guard delete and an invalid insert arriving through mapped memory
+    (a, _ta), (b, _tb) = pin(np.array([1], np.uint32)), pin(np.array([2**12 + 5], np.uint32))
+    with pytest.raises(ValueError, match="outside vertex range"):
+        g.apply_batch(a, b, None, [], [])
+    assert_same_slots(g.pma().slots(), r.slots(), "after rejected batch")
