@@ -17,6 +17,7 @@
 //      kernels (segment_engine.hpp:435-463, pma.hpp:390-402, 597-601)
 //   5. refresh of leaf headers (+ row offsets for graphs) over touched ranges.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -201,20 +202,55 @@ __global__ void k_compress(const u64* keys, const u8* ops, u64 n, BitRuns runs, 
     }
 }
 
-// Graph-mode front end (DynamicGraph::apply_batch, graph.hpp:133-147): check
-// insert ids, count guard deletes, and emit the sort input with the
-// |V|-derived compressed layout (src << db | dst); guard deletes (dropped by
-// the reference before the engine) get key 1 << 2db and sort last.  Payload =
-// arrival index << 1 | is_insert — or, when key and index fit one word
-// (ib > 0), the single u64 (key << ib | index), sorted keys-only on the key
-// bits: LSD radix is stable, so this is the same order at 16 instead of 24
-// bytes per element per pass.  A non-guard delete outside the layout raises
-// `oor` (the batch is then redone on the generic path).
 struct PrepAcc {
-    ull guards = 0, bad = 0, oor = 0;
+    ull guards = 0, bad = 0, oor = 0, bigrun = 0;
 };
 
-__device__ __forceinline__ void prep_one(const GraphFront& f, int db, int ib, u64* ck, u32* ci, u64 i, u32 s, u32 d,
+// leaf of a graph key (pma.hpp:234-289 binary_search_leaf): keys of a vertex
+// in the row-offset range are bracketed by its guards' slots first, so the
+// header search spans only the leaves of that vertex's run
+__device__ __forceinline__ u64 leaf_for_key(u64 key, const u64* __restrict__ hdr, u64 L, const u8* __restrict__ st,
+                                            u64 leaf, const u64* __restrict__ ro, u64 rlo, u64 rhi) {
+    const u64 u = key >> 32;
+    if (ro && u >= rlo && u < rhi && !is_guard(key)) {
+        const u64 a = __ldg(&ro[u]), b = __ldg(&ro[u + 1]);
+        u64 lo = a ? (a - 1) / leaf : 0;  // hdr[lo] <= guard(u - 1) < key (or lo == 0)
+        u64 hi = (b - 1) / leaf + 1;      // hdr[hi] > guard(u) > key (or hi == L)
+        if (hi > L) hi = L;
+        while (hi - lo > 1) {
+            const u64 mid = (lo + hi) >> 1;
+            if (__ldg(&hdr[mid]) <= key) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    }
+    if (key == ~0ull) return leaf_of_key(hdr, L, st, leaf, key);
+    const u64 kk[1] = {key};
+    u64 pos[1];
+    leaf_search_interleaved<1>(hdr, L, 1u, kk, pos);
+    return pos[0];
+}
+
+// Leaf-bucket front end (graph batches): each update's leaf is found in
+// arrival order and counted (the atomic's return = its ordinal in the
+// bucket); bucket L holds the guard deletes.  A bucket reaching kRunMax
+// raises `bigrun` (the batch is then redone through the radix sort).
+constexpr u32 kRunMax = 1024;
+struct BucketArgs {
+    const u64* hdr;
+    u64 L;
+    const u8* st;
+    u64 leaf;
+    const u64* ro;
+    u64 rlo, rhi;
+    u32* cnt;  // L + 2 bucket counters (zeroed)
+    u32* lf;   // per update: bucket
+    u32* od;   // per update: ordinal in the bucket
+};
+
+// one update of the graph front end: checks + the packed sort word; returns
+// the bucket class: -1 guard delete (bucket L), -2 outside the layout, else 0
+__device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u64* ck, u32* ci, u64 i, u32 s, u32 d,
                                          bool ins, PrepAcc& acc) {
     const u64 lim = 1ull << db;
     bool skip = false;
@@ -225,11 +261,14 @@ __device__ __forceinline__ void prep_one(const GraphFront& f, int db, int ib, u6
         acc.guards += skip;
     }
     u64 c;
+    int cls = 0;
     if (skip) {
         c = 1ull << (2 * db);
+        cls = -1;
     } else if (s >= lim || d >= lim) {
         c = 0;
         acc.oor |= !ins;
+        cls = -2;
     } else {
         c = (u64(s) << db) | d;
     }
@@ -242,13 +281,74 @@ __device__ __forceinline__ void prep_one(const GraphFront& f, int db, int ib, u6
         ck[i] = c;
         ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
     }
+    return cls;
+}
+
+// bucket N updates at once: the leaf searches advance in lock-step so each
+// step has N independent header loads in flight (unsorted keys: the searches
+// miss cache, latency is the cost), then N independent counter atomics.
+// (an out-of-layout key only occurs with a bad insert or an oor delete: the
+// batch is rejected or redone, its bucket is immaterial)
+template <int N>
+__device__ __forceinline__ void bucket_n(const BucketArgs& ba, const u64* idx, const u32* s, const u32* d,
+                                         const int* cls, PrepAcc& acc) {
+    u64 lo[N], hi[N], key[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        key[j] = pack_edge(s[j], d[j]);
+        lo[j] = cls[j] == -1 ? ba.L : 0;
+        hi[j] = lo[j] + 1;  // settled
+        if (cls[j] == 0) {
+            const u64 u = s[j];
+            if (ba.ro && u >= ba.rlo && u < ba.rhi && !is_guard(key[j])) {
+                const u64 a = __ldg(&ba.ro[u]), b = __ldg(&ba.ro[u + 1]);
+                lo[j] = a ? (a - 1) / ba.leaf : 0;
+                hi[j] = (b - 1) / ba.leaf + 1;
+                if (hi[j] > ba.L) hi[j] = ba.L;
+            } else {
+                lo[j] = leaf_for_key(key[j], ba.hdr, ba.L, ba.st, ba.leaf, ba.ro, ba.rlo, ba.rhi);
+                hi[j] = lo[j] + 1;
+            }
+        }
+    }
+    for (;;) {
+        bool more = false;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+            if (hi[j] - lo[j] > 1) {
+                const u64 mid = (lo[j] + hi[j]) >> 1;
+                if (__ldg(&ba.hdr[mid]) <= key[j]) lo[j] = mid;
+                else hi[j] = mid;
+                more |= hi[j] - lo[j] > 1;
+            }
+        }
+        if (!more) break;
+    }
+    u32 o[N];
+#pragma unroll
+    for (int j = 0; j < N; ++j) o[j] = atomicAdd(&ba.cnt[lo[j]], 1u);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+        ba.lf[idx[j]] = u32(lo[j]);
+        ba.od[idx[j]] = o[j];
+        acc.bigrun |= o[j] == kRunMax && lo[j] != ba.L;
+    }
+}
+
+template <bool kBucket>
+__device__ __forceinline__ void prep_one(const GraphFront& f, int db, int ib, u64* ck, u32* ci, const BucketArgs& ba,
+                                         u64 i, u32 s, u32 d, bool ins, PrepAcc& acc) {
+    const int cls = prep_word(f, db, ib, ck, ci, i, s, d, ins, acc);
+    if constexpr (kBucket) bucket_n<1>(ba, &i, &s, &d, &cls, acc);
 }
 
 // one endpoint-array segment (inserts or deletes): 16-byte vector loads when
 // both arrays are aligned alike — the arrays may be page-locked host memory
 // read in place over PCIe, where wide requests are what keeps the link busy
-__device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib, u64* ck, u32* ci, const u32* sa,
-                                             const u32* da, u64 n, u64 base, bool ins, PrepAcc& acc) {
+template <bool kBucket>
+__device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib, u64* ck, u32* ci,
+                                             const BucketArgs& ba, const u32* sa, const u32* da, u64 n, u64 base,
+                                             bool ins, PrepAcc& acc) {
     const u64 tid = blockIdx.x * u64(blockDim.x) + threadIdx.x, nt = u64(gridDim.x) * blockDim.x;
     u64 head = 0;
     if ((reinterpret_cast<uintptr_t>(sa) & 15) == (reinterpret_cast<uintptr_t>(da) & 15) &&
@@ -261,17 +361,20 @@ __device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib
         for (u64 q = tid; q < nq; q += nt) {
             const uint4 a = s4[q], b = d4[q];
             const u64 i = base + head + 4 * q;
-            prep_one(f, db, ib, ck, ci, i, a.x, b.x, ins, acc);
-            prep_one(f, db, ib, ck, ci, i + 1, a.y, b.y, ins, acc);
-            prep_one(f, db, ib, ck, ci, i + 2, a.z, b.z, ins, acc);
-            prep_one(f, db, ib, ck, ci, i + 3, a.w, b.w, ins, acc);
+            const u32 ss[4] = {a.x, a.y, a.z, a.w}, dd[4] = {b.x, b.y, b.z, b.w};
+            const u64 ii[4] = {i, i + 1, i + 2, i + 3};
+            int cls[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) cls[j] = prep_word(f, db, ib, ck, ci, ii[j], ss[j], dd[j], ins, acc);
+            if constexpr (kBucket) bucket_n<4>(ba, ii, ss, dd, cls, acc);
         }
         // scalar head and tail
-        for (u64 j = tid; j < head; j += nt) prep_one(f, db, ib, ck, ci, base + j, sa[j], da[j], ins, acc);
-        for (u64 j = head + 4 * nq + tid; j < n; j += nt) prep_one(f, db, ib, ck, ci, base + j, sa[j], da[j], ins, acc);
+        for (u64 j = tid; j < head; j += nt) prep_one<kBucket>(f, db, ib, ck, ci, ba, base + j, sa[j], da[j], ins, acc);
+        for (u64 j = head + 4 * nq + tid; j < n; j += nt)
+            prep_one<kBucket>(f, db, ib, ck, ci, ba, base + j, sa[j], da[j], ins, acc);
         return;
     }
-    for (u64 j = tid; j < n; j += nt) prep_one(f, db, ib, ck, ci, base + j, sa[j], da[j], ins, acc);
+    for (u64 j = tid; j < n; j += nt) prep_one<kBucket>(f, db, ib, ck, ci, ba, base + j, sa[j], da[j], ins, acc);
 }
 
 // Graph-mode front end (DynamicGraph::apply_batch, graph.hpp:133-147): check
@@ -282,33 +385,151 @@ __device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib
 // (ib > 0), the single u64 (key << ib | index), sorted keys-only on the key
 // bits: LSD radix is stable, so this is the same order at 16 instead of 24
 // bytes per element per pass.  A non-guard delete outside the layout raises
-// `oor` (the batch is then redone on the generic path).
-__global__ void k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
+// `oor` (the batch is then redone on the generic path).  kBucket: also the
+// leaf bucket of every update (leaf-bucket front end, see batch_update_device).
+template <bool kBucket>
+__global__ void __launch_bounds__(256, kBucket ? 5 : 1) k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr,
+                             BucketArgs ba) {
     PrepAcc acc;
     if (f.mk) {
         const u64 n = f.ni + f.nd;
         for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
             const u64 k = f.mk[i];
-            prep_one(f, db, ib, ck, ci, i, src_of(k) & 0x7FFFFFFFu, dst_of(k), !(k >> 63), acc);
+            prep_one<kBucket>(f, db, ib, ck, ci, ba, i, src_of(k) & 0x7FFFFFFFu, dst_of(k), !(k >> 63), acc);
         }
     } else {
-        if (f.ni) prep_segment(f, db, ib, ck, ci, f.is, f.id, f.ni, 0, true, acc);
-        if (f.nd) prep_segment(f, db, ib, ck, ci, f.ds, f.dd, f.nd, f.ni, false, acc);
+        if (f.ni) prep_segment<kBucket>(f, db, ib, ck, ci, ba, f.is, f.id, f.ni, 0, true, acc);
+        if (f.nd) prep_segment<kBucket>(f, db, ib, ck, ci, ba, f.ds, f.dd, f.nd, f.ni, false, acc);
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
         acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
         acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
+        acc.bigrun |= __shfl_xor_sync(FULL, acc.bigrun, d);
     }
     if ((threadIdx.x & 31) == 0) {
         if (acc.guards) atomicAdd(&ctr->gdel, acc.guards);
         if (acc.bad) atomicMax(&ctr->bad_ins, acc.bad);
         if (acc.oor) atomicOr(&ctr->oor, 1ull);
+        if (acc.bigrun) atomicOr(&ctr->bigrun, 1ull);
     }
 }
 
-__global__ void k_gate_npend(Ctr* ctr) { ctr->np[0] = (ctr->bad_ins || ctr->oor) ? 0ull : ctr->n_unique; }
+// bucket scatter: update i -> position off[bucket] + ordinal (bucket order,
+// arbitrary order inside a bucket)
+__global__ void k_bucket_scatter(const u64* __restrict__ ck, const u32* __restrict__ lf, const u32* __restrict__ od,
+                                 const u32* __restrict__ off, u64 n, u64* __restrict__ out) {
+    // four updates per thread per step: four independent offset lookups in flight
+    const u64 nt = u64(gridDim.x) * blockDim.x;
+    for (u64 i0 = blockIdx.x * u64(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * nt) {
+        u32 b[4], o[4];
+        u64 w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const u64 i = i0 + j * nt;
+            if (i < n) {
+                b[j] = lf[i];
+                o[j] = od[i];
+                w[j] = ck[i];
+            }
+        }
+        u64 p[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (i0 + j * nt < n) p[j] = off[b[j]] + o[j];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (i0 + j * nt < n) out[p[j]] = w[j];
+    }
+}
+
+// in-bucket sort by the whole packed word (key, then arrival index): a warp
+// takes 32 consecutive buckets, i.e. the contiguous positions
+// [off[b0], off[b0 + 32]), one lane per position; a lane finds its bucket
+// among the warp's 33 offsets (shuffle binary search) and ranks its word
+// among the bucket's (ties — identical delete words — by position).  Buckets
+// are short (updates per leaf, ~1 on average); longer ones (> kSmallRun) are
+// listed for k_bucket_sort_big.  Also writes each sorted position's leaf (the
+// resolve pass emits it).  The guard-delete bucket L holds identical words:
+// copied as is.  `out` is the front end's word array, so positions of an
+// overflowed bucket (batch redone) keep valid words of this batch.
+constexpr u32 kSmallRun = 16;
+__global__ void k_bucket_sort_small(const u64* __restrict__ in, const u32* __restrict__ off, u64 L,
+                                    u64* __restrict__ out, u32* __restrict__ slf, u32* __restrict__ big, Ctr* ctr) {
+    const unsigned lane = threadIdx.x & 31u;
+    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    const u64 nb = L + 1;  // buckets 0..L (L = guard deletes)
+    for (u64 b0 = warp * 32; b0 < nb; b0 += nwarps * 32) {
+        const u64 bl = b0 + lane < nb ? b0 + lane : nb;
+        const u32 o = off[bl];            // start of bucket b0 + lane (or the end)
+        const u32 P1 = __shfl_sync(FULL, off[b0 + 32 < nb ? b0 + 32 : nb], 0);
+        const u32 P0 = __shfl_sync(FULL, o, 0);
+        const u32 oe = __shfl_down_sync(FULL, o, 1);
+        const u32 last_end = lane == 31 ? P1 : oe;  // end of bucket b0 + lane
+        // long buckets: their first lane lists them
+        if (b0 + lane < nb && last_end - o > kSmallRun && b0 + lane != L)
+            big[atomicAdd(&ctr->nbig_buckets, 1ull)] = u32(b0 + lane);
+        for (u32 base = P0; base < P1; base += 32) {  // warp-uniform
+            const u32 p = base + lane;
+            const bool act = p < P1;
+            // bucket of p: the largest k with off[b0 + k] <= p
+            int k = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const u32 ok = __shfl_sync(FULL, o, k + step);
+                if (k + step < 32 && ok <= p) k += step;
+            }
+            const u32 a = __shfl_sync(FULL, o, k);
+            const u32 e = __shfl_sync(FULL, last_end, k);
+            if (!act) continue;
+            const u64 b = b0 + k;
+            slf[p] = u32(b);
+            const u64 w = in[p];
+            if (e - a == 1 || b == L) {
+                out[p] = w;
+                continue;
+            }
+            if (e - a > kSmallRun) continue;
+            u32 r = 0;
+            for (u32 t = a; t < e; ++t) {
+                const u64 x = in[t];
+                r += (x < w) || (x == w && t < p);
+            }
+            out[a + r] = w;
+        }
+    }
+}
+
+// the long buckets, one CTA each: staged in shared memory, ranked there
+__global__ void __launch_bounds__(256) k_bucket_sort_big(const u64* __restrict__ in, const u32* __restrict__ off,
+                                                         const u32* __restrict__ big, const ull* nbig,
+                                                         u64* __restrict__ out) {
+    __shared__ u64 sm[kRunMax];
+    const u64 nb = *nbig;
+    for (u64 k = blockIdx.x; k < nb; k += gridDim.x) {
+        const u32 b = big[k];
+        const u32 a = off[b], len = off[b + 1] - a;
+        if (len > kRunMax) continue;  // flagged: the batch is redone
+        __syncthreads();
+        for (u32 q = threadIdx.x; q < len; q += blockDim.x) sm[q] = in[a + q];
+        __syncthreads();
+        for (u32 q = threadIdx.x; q < len; q += blockDim.x) {
+            const u64 w = sm[q];
+            u32 r = 0;
+            for (u32 t = 0; t < len; ++t) {
+                const u64 x = sm[t];
+                r += (x < w) || (x == w && t < q);
+            }
+            out[a + r] = w;
+        }
+    }
+}
+
+__global__ void k_gate_npend(Ctr* ctr) {
+    ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : ctr->n_unique;
+}
 
 __global__ void k_iota(u32* p, const ull* n_dev) {
     const u64 n = *n_dev;
@@ -334,31 +555,8 @@ __global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_de
                                      const u8* __restrict__ st, u64 leaf, const u64* __restrict__ ro, u64 rlo,
                                      u64 rhi, u32* __restrict__ ul) {
     const u64 n = *n_dev;
-    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
-        const u64 key = uk[i];
-        const u64 u = key >> 32;
-        u64 out;
-        if (ro && u >= rlo && u < rhi && !is_guard(key)) {
-            const u64 a = __ldg(&ro[u]), b = __ldg(&ro[u + 1]);
-            u64 lo = a ? (a - 1) / leaf : 0;  // hdr[lo] <= guard(u - 1) < key (or lo == 0)
-            u64 hi = (b - 1) / leaf + 1;      // hdr[hi] > guard(u) > key (or hi == L)
-            if (hi > L) hi = L;
-            while (hi - lo > 1) {
-                const u64 mid = (lo + hi) >> 1;
-                if (__ldg(&hdr[mid]) <= key) lo = mid;
-                else hi = mid;
-            }
-            out = lo;
-        } else if (key == ~0ull) {
-            out = leaf_of_key(hdr, L, st, leaf, key);
-        } else {
-            const u64 kk[1] = {key};
-            u64 pos[1];
-            leaf_search_interleaved<1>(hdr, L, 1u, kk, pos);
-            out = pos[0];
-        }
-        ul[i] = u32(out);
-    }
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        ul[i] = u32(leaf_for_key(uk[i], hdr, L, st, leaf, ro, rlo, rhi));
 }
 
 // --------------------------------------------------------------- commit args
@@ -1479,6 +1677,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     si_out.reserve(n);
     int nbits = 0;
     int packed_ib = 0;
+    bool bucket = false;
     if (gf) {
         // graph front end: pack + id check + compression in one pass; the
         // key layout is fixed by |V| (src, dst < 2^db), so no host round trip
@@ -1490,7 +1689,30 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         while ((1ull << ib) <= n) ++ib;  // the all-ones index is reserved for deletes
         if (nbits + ib > 64) ib = 0;     // no room: key + payload pairs
         packed_ib = ib;
-        k_prep_graph<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
+        // leaf-bucket front end for large batches: the leaf of every update is
+        // found up front and the batch counting-sorted by leaf (one scatter)
+        // then ranked inside each leaf's short bucket — the same order as the
+        // radix sort over all 2db + 1 key bits, in ~4 light passes instead of
+        // one per 8 bits.  Skipped after a batch whose buckets overflowed.
+        BucketArgs ba{};
+        const u64 L = num_leaves();
+        bucket = ib && ro_base() && n >= kBucketMinBatch && n < (1ull << 31) && L + 2 < (1ull << 31) &&
+                 bucket_skip_ == 0;
+        if (bucket_skip_) --bucket_skip_;
+        if (bucket) {
+            bcnt.reserve(L + 2);
+            boff.reserve(L + 2);
+            blf.reserve(n);
+            bod.reserve(n);
+            bslf.reserve(n);
+            GPMA_CUDA(cudaMemsetAsync(bcnt.ptr, 0, (L + 2) * sizeof(u32), stream_));
+            ba = BucketArgs{d_hdr, L, d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, bcnt.ptr, blf.ptr, bod.ptr};
+            k_prep_graph<true><<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr,
+                                                                               d_ctr, ba);
+        } else {
+            k_prep_graph<false><<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr,
+                                                                                d_ctr, ba);
+        }
         GPMA_LAUNCH_CHECK();
         ++launches;
     } else {
@@ -1528,7 +1750,24 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     }
     const u64* sorted_ck = sk_in.ptr;
     const u32* sorted_ci = si_in.ptr;
-    if (packed_ib && n > 1) {
+    if (bucket) {
+        const u64 L = num_leaves();
+        size_t tmp = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_);
+        sort_tmp.reserve(tmp);
+        GPMA_CUDA(cub::DeviceScan::ExclusiveSum(sort_tmp.ptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_));
+        k_bucket_scatter<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(sk_in.ptr, blf.ptr, bod.ptr, boff.ptr, n,
+                                                                         sk_out.ptr);
+        GPMA_LAUNCH_CHECK();
+        bbig.reserve(n / (kSmallRun + 1) + 1);
+        k_bucket_sort_small<<<grid_for((L + 1 + 31) / 32 * 32, 256, 148 * 16), 256, 0, stream_>>>(
+            sk_out.ptr, boff.ptr, L, sk_in.ptr, bslf.ptr, bbig.ptr, d_ctr);
+        GPMA_LAUNCH_CHECK();
+        k_bucket_sort_big<<<148 * 2, 256, 0, stream_>>>(sk_out.ptr, boff.ptr, bbig.ptr, &d_ctr->nbig_buckets,
+                                                         sk_in.ptr);
+        GPMA_LAUNCH_CHECK();
+        launches += 5;
+    } else if (packed_ib && n > 1) {
         size_t tmp = 0;
         cub::DeviceRadixSort::SortKeys(nullptr, tmp, sk_in.ptr, sk_out.ptr, int(n), packed_ib, packed_ib + nbits,
                                        stream_);
@@ -1576,6 +1815,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         u64* o_k = uk.ptr;
         u64* o_v = uv.ptr;
         u8* o_o = uop.ptr;
+        u32* o_l = ul.ptr;
+        const u32* slf = bucket ? bslf.ptr : nullptr;  // leaf-bucket front end: leaves already known
         Ctr* ctr = d_ctr;
         run_compact_tile(
             stream_, ws, nullptr, n, n,
@@ -1616,16 +1857,19 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                     o_k[xs[j]] = key;
                     o_v[xs[j]] = val;
                     o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
+                    if (slf) o_l[xs[j]] = slf[i];
                 }
             },
             [=] __device__(ull total) { ctr->n_unique = total; });
         ++launches;
-        // leaf assignment (pma.hpp:234-289), once per batch
-        k_leaf_search_sorted<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
-            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices,
-            ul.ptr);
-        GPMA_LAUNCH_CHECK();
-        ++launches;
+        if (!bucket) {
+            // leaf assignment (pma.hpp:234-289), once per batch
+            k_leaf_search_sorted<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
+                uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices,
+                ul.ptr);
+            GPMA_LAUNCH_CHECK();
+            ++launches;
+        }
     }
     // pending count of round 0 = the unique updates, or 0 when the graph
     // front end flagged a bad insert id / an out-of-layout delete: every
@@ -2028,6 +2272,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.refresh_ms = d;
     timing.device_ms = a + b + c + d;
     timing.kernel_launches = launches;
+    timing.front_end = bucket ? 1 : 0;
     if (gf) {
         gf->guard_deletes = h_ctr->gdel;
         gf->bad_insert = h_ctr->bad_ins ? (long long)(~h_ctr->bad_ins) : -1;
@@ -2060,6 +2305,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             const u64 m = h_ctr->nt;
             batch_update_device(bk, bv, bo, m, cfg, out, nullptr);
             if (out) out->batch_size = n;  // the caller subtracts the guard deletes
+            return;
+        }
+        if (h_ctr->bigrun) {
+            // a leaf bucket too long to rank in place (many updates between two
+            // neighbouring keys, e.g. a burst into an empty vertex): the gated
+            // rounds mutated nothing; redo through the radix sort and keep it
+            // for the next batches
+            bucket_skip_ = kBucketCooldown;
+            batch_update_device(dk, dv, dop, n, cfg, out, gf);
+            timing.front_end = 2;
             return;
         }
     }

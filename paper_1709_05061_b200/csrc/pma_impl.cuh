@@ -56,6 +56,8 @@ struct Ctr {
     ull bad_ins;    // graph front end: ~(first insert index with an id >= |V|), 0 = none
     ull oor;        // graph front end: a delete key outside the compressed key range
     ull gdel;       // graph front end: guard deletes (dropped, counted missed)
+    ull bigrun;     // leaf-bucket front end: a bucket reached kRunMax updates
+    ull nbig_buckets;  // leaf-bucket front end: buckets sorted by the CTA kernel
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
     // host sync (rounds may run back to back without one)
@@ -230,6 +232,12 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u64> sk_in, sk_out;   // compressed keys
     DevBuf<u32> si_in, si_out;   // arrival index payload
     DevBuf<unsigned char> sort_tmp;
+    // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
+    // update bucket + ordinal, per sorted position bucket
+    DevBuf<u32> bcnt, boff, blf, bod, bslf, bbig;
+    int bucket_skip_ = 0;  // batches left on the radix sort after a bucket overflow
+    static constexpr u64 kBucketMinBatch = 1u << 16;
+    static constexpr int kBucketCooldown = 16;
     DevBuf<u64> uk, uv;
     DevBuf<u8> uop;
     DevBuf<u32> ul;

@@ -228,3 +228,58 @@ def test_pinned_host_batches_read_in_place():
     with pytest.raises(ValueError, match="outside vertex range"):
         g.apply_batch(a, b, None, [], [])
     assert_same_slots(g.pma().slots(), r.slots(), "after rejected batch")
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+@pytest.mark.parametrize("kind,nv,param,batch", [("er", 2**15, 2**-6, 70000), ("rmat", 2**16, 600000, 90000)])
+def test_leaf_bucket_front_end_parity(mode, kind, nv, param, batch):
+    """Batches >= 2^16 updates take the leaf-bucket front end (leaf found per
+    update, counting sort by leaf, in-bucket rank): slot arrays, stats and row
+    offsets must stay bit-exact with the reference."""
+    stream = _window_stream(kind, nv, param)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half], GraphConfig(deletion_mode=mode))
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config(deletion_mode=mode))
+    win = RefWindow(stream)
+    seen = set()
+    for slide in range(3):
+        a, b, ww, c, dd = win.slide(batch)
+        gs = g.apply_batch(a, b, ww, c, dd)
+        seen.add(int(g.last_timing().front_end))
+        rs = r.apply_batch(a, b, ww, c, dd)
+        assert gs.parity() == ref_parity(r, rs), slide
+        assert_same_slots(g.pma().slots(), r.slots(), f"slide {slide}")
+        assert (g.row_offsets() == r.row_offsets()).all()
+    assert 1 in seen or 2 in seen, seen
+
+
+def test_leaf_bucket_overflow_redo():
+    """A burst of inserts between two neighbouring keys overflows one leaf
+    bucket: the batch is redone through the radix sort (front_end 2) with the
+    same result, and duplicate / cancelling updates inside buckets resolve as
+    in the reference."""
+    rng = np.random.default_rng(12)
+    nv = 2**14
+    s = rng.integers(0, nv, 50000)
+    d = rng.integers(0, nv, 50000)
+    g = DynamicGraph.from_edges(nv, s, d)
+    r = RefGraph(nv, s, d)
+    # 80k inserts: 3000 onto vertex 77 (one bucket), the rest random with duplicates
+    a = np.concatenate([np.full(3000, 77), rng.integers(0, nv, 77000)])
+    b = np.concatenate([np.arange(3000) % nv, rng.integers(0, nv, 77000)])
+    a, b = np.concatenate([a, a[:5000]]), np.concatenate([b, b[:5000]])
+    w = rng.integers(0, 9, len(a)).astype(float)
+    c, dd = s[:20000], d[:20000]
+    gs = g.apply_batch(a, b, w, c, dd)
+    assert int(g.last_timing().front_end) == 2
+    rs = r.apply_batch(a, b, w, c, dd)
+    assert gs.parity() == ref_parity(r, rs)
+    assert_same_slots(g.pma().slots(), r.slots(), "overflow redo")
+    # the next batch stays on the radix sort (cool-down), still exact
+    a2, b2 = rng.integers(0, nv, 70000), rng.integers(0, nv, 70000)
+    gs = g.apply_batch(a2, b2, None, a[:9000], b[:9000])
+    assert int(g.last_timing().front_end) == 0
+    rs = r.apply_batch(a2, b2, None, a[:9000], b[:9000])
+    assert gs.parity() == ref_parity(r, rs)
+    assert_same_slots(g.pma().slots(), r.slots(), "after cool-down")
