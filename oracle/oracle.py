@@ -511,3 +511,56 @@ class RefRebuildCsr:
         val = np.zeros(max(ne, 1), np.float64)
         _check(ref_lib(), ref_lib().ref_rebuild_csr(self.h, _p(ro), _p(col), _p(val)), "ref_last_error")
         return ro, col[:ne], val[:ne]
+
+
+class RefIO:
+    """The reference's file formats (io.hpp:24-181) — test oracle of
+    paper_1709_05061_b200.io (byte-identical files, identical parses)."""
+
+    @staticmethod
+    def format_double(v: float) -> str:
+        buf = C.create_string_buffer(64)
+        _check(ref_lib(), ref_lib().ref_io_format_double(C.c_double(v), buf, C.c_size_t(64)), "ref_last_error")
+        return buf.value.decode()
+
+    @staticmethod
+    def write_pairs(path, keys, values, text=False):
+        k, v = np.ascontiguousarray(keys, np.uint64), np.ascontiguousarray(values, np.uint64)
+        _check(ref_lib(), ref_lib().ref_io_write_pairs(str(path).encode(), int(text), _p(k), _p(v),
+                                                       C.c_size_t(len(k))), "ref_last_error")
+
+    @staticmethod
+    def read_pairs(path, text=False):
+        n = C.c_uint64()
+        _check(ref_lib(), ref_lib().ref_io_read_pairs(str(path).encode(), int(text), C.byref(n)), "ref_last_error")
+        k = np.zeros(max(n.value, 1), np.uint64)
+        v = np.zeros(max(n.value, 1), np.uint64)
+        _check(ref_lib(), ref_lib().ref_io_pairs_copy(_p(k), _p(v)), "ref_last_error")
+        return k[:n.value], v[:n.value]
+
+    @staticmethod
+    def write_stream(path, nv, src, dst, w, ts, text=False):
+        s, d = _u32(src), _u32(dst)
+        ww, t = _f64(w), np.ascontiguousarray(ts, np.uint64)
+        _check(ref_lib(), ref_lib().ref_io_write_stream(str(path).encode(), int(text), C.c_size_t(nv), _p(s), _p(d),
+                                                        _p(ww), _p(t), C.c_size_t(len(s))), "ref_last_error")
+
+    @staticmethod
+    def read_stream(path, mode=0):
+        """mode 0 read_stream (format probe), 1 text, 2 binary -> (nv, src, dst, w, ts)"""
+        nv, n = C.c_uint64(), C.c_uint64()
+        _check(ref_lib(), ref_lib().ref_io_read_stream(str(path).encode(), mode, C.byref(nv), C.byref(n)),
+               "ref_last_error")
+        m = max(n.value, 1)
+        s, d = np.zeros(m, np.uint32), np.zeros(m, np.uint32)
+        w, t = np.zeros(m, np.float64), np.zeros(m, np.uint64)
+        _check(ref_lib(), ref_lib().ref_io_stream_copy(_p(s), _p(d), _p(w), _p(t)), "ref_last_error")
+        k = n.value
+        return nv.value, s[:k], d[:k], w[:k], t[:k]
+
+    @staticmethod
+    def write_vector(path, v, text=False):
+        a = np.ascontiguousarray(v)
+        kind = {np.dtype(np.float64): 0, np.dtype(np.uint32): 1, np.dtype(np.uint64): 2}[a.dtype]
+        _check(ref_lib(), ref_lib().ref_io_write_vector(str(path).encode(), int(text), kind, _p(a),
+                                                        C.c_size_t(len(a))), "ref_last_error")

@@ -15,6 +15,7 @@
 #include <pmagraph/baselines.hpp>
 #include <pmagraph/generators.hpp>
 #include <pmagraph/graph.hpp>
+#include <pmagraph/io.hpp>
 #include <pmagraph/pma.hpp>
 #include <pmagraph/segment_engine.hpp>
 #include <pmagraph/streaming.hpp>
@@ -573,6 +574,92 @@ int ref_draw_below_sequence(uint64_t seed, uint64_t bound, size_t n, uint64_t* o
     return guarded([&] {
         std::mt19937_64 rng(seed);
         for (size_t i = 0; i < n; ++i) out[i] = draw_below(rng, bound);
+    });
+}
+
+// ---- io.hpp: the reference's file formats, for byte-level comparisons ----
+int ref_io_format_double(double v, char* buf, size_t cap) {
+    return guarded([&] {
+        const std::string s = format_double(v);
+        if (s.size() + 1 > cap) throw std::length_error("buffer too small");
+        std::memcpy(buf, s.c_str(), s.size() + 1);
+    });
+}
+
+int ref_io_write_pairs(const char* path, int text, const uint64_t* keys, const uint64_t* values, size_t n) {
+    return guarded([&] {
+        std::vector<Entry> e(n);
+        for (size_t i = 0; i < n; ++i) e[i] = Entry{keys[i], values[i]};
+        if (text) write_pairs_text(path, e);
+        else write_pairs_binary(path, e);
+    });
+}
+
+namespace {
+thread_local std::vector<Entry> g_pairs;
+thread_local EdgeStream g_stream;
+}  // namespace
+
+int ref_io_read_pairs(const char* path, int text, uint64_t* n) {
+    return guarded([&] {
+        g_pairs = text ? read_pairs_text(path) : read_pairs_binary(path);
+        *n = g_pairs.size();
+    });
+}
+
+int ref_io_pairs_copy(uint64_t* keys, uint64_t* values) {
+    return guarded([&] {
+        for (size_t i = 0; i < g_pairs.size(); ++i) {
+            keys[i] = g_pairs[i].key;
+            values[i] = g_pairs[i].value;
+        }
+    });
+}
+
+int ref_io_write_stream(const char* path, int text, size_t nv, const uint32_t* src, const uint32_t* dst,
+                        const double* w, const uint64_t* ts, size_t n) {
+    return guarded([&] {
+        EdgeStream st;
+        st.num_vertices = nv;
+        st.edges.resize(n);
+        for (size_t i = 0; i < n; ++i) st.edges[i] = TimestampedEdge{src[i], dst[i], w[i], ts[i]};
+        if (text) write_stream_text(path, st);
+        else write_stream_binary(path, st);
+    });
+}
+
+// mode: 0 read_stream (format probe), 1 text, 2 binary
+int ref_io_read_stream(const char* path, int mode, uint64_t* nv, uint64_t* n) {
+    return guarded([&] {
+        g_stream = mode == 1 ? read_stream_text(path) : mode == 2 ? read_stream_binary(path) : read_stream(path);
+        *nv = g_stream.num_vertices;
+        *n = g_stream.edges.size();
+    });
+}
+
+int ref_io_stream_copy(uint32_t* src, uint32_t* dst, double* w, uint64_t* ts) {
+    return guarded([&] {
+        for (size_t i = 0; i < g_stream.edges.size(); ++i) {
+            src[i] = g_stream.edges[i].src;
+            dst[i] = g_stream.edges[i].dst;
+            w[i] = g_stream.edges[i].weight;
+            ts[i] = g_stream.edges[i].ts;
+        }
+    });
+}
+
+// kind: 0 f64, 1 u32, 2 u64
+int ref_io_write_vector(const char* path, int text, int kind, const void* data, size_t n) {
+    return guarded([&] {
+        auto go = [&](auto* p) {
+            using T = std::remove_cv_t<std::remove_pointer_t<decltype(p)>>;
+            std::vector<T> v(p, p + n);
+            if (text) write_vector_text(path, v);
+            else write_vector_binary(path, v);
+        };
+        if (kind == 0) go(static_cast<const double*>(data));
+        else if (kind == 1) go(static_cast<const uint32_t*>(data));
+        else go(static_cast<const uint64_t*>(data));
     });
 }
 

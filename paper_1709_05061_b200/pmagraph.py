@@ -414,6 +414,40 @@ class DynamicGraph:
         self._check(self._lib.gpma_last_timing(self.h, C.byref(t)))
         return t
 
+    # -- read API (graph.hpp:94-126, 208-223), derived from device snapshots --
+    def edge_list(self):
+        """graph.hpp:208-217: (src, dst, weight) of every edge in key order."""
+        ro, col, val = self.csr_snapshot()
+        src = np.repeat(np.arange(self._nv, dtype=np.uint32), np.diff(ro.astype(np.int64)))
+        return src, col, val
+
+    def degree(self, v: int) -> int:
+        """graph.hpp:116-120: Valid non-guard slots of row v (its guard is the
+        row's last Valid slot)."""
+        if not 0 <= v < self._nv:
+            raise IndexError("vertex out of range")
+        ro = self.row_offsets()
+        return self.pma().count_valid_in(int(ro[v]), int(ro[v + 1])) - 1
+
+    def edge_weight(self, src: int, dst: int):
+        """graph.hpp:122-126: the weight, or None when the edge is absent."""
+        v = self.pma().search((int(src) << 32) | int(dst))
+        return None if v is None else float(np.array([v], np.uint64).view(np.float64)[0])
+
+    def neighbors(self, v: int):
+        """for_each_neighbor (graph.hpp:105-114) as arrays: (dst, weight) of row v."""
+        ro = self.row_offsets()
+        k, val, s = self.pma().slots()
+        a, b = int(ro[v]), int(ro[v + 1])
+        k, val, s = k[a:b], val[a:b], s[a:b]
+        m = (s == 1) & ((k & np.uint64(0xFFFFFFFF)) != np.uint64(0xFFFFFFFF))
+        return (k[m] & np.uint64(0xFFFFFFFF)).astype(np.uint32), val[m].view(np.float64)
+
+    def guard_count(self) -> int:
+        """graph.hpp:219-223"""
+        k, _, s = self.pma().slots()
+        return int(((s == 1) & ((k & np.uint64(0xFFFFFFFF)) == np.uint64(0xFFFFFFFF))).sum())
+
 
 class RebuildCsrGraph:
     """The rebuild-the-CSR-per-batch baseline (baselines.hpp:85-181) on the

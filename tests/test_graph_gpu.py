@@ -283,3 +283,36 @@ def test_leaf_bucket_overflow_redo():
     rs = r.apply_batch(a2, b2, None, a[:9000], b[:9000])
     assert gs.parity() == ref_parity(r, rs)
     assert_same_slots(g.pma().slots(), r.slots(), "after cool-down")
+
+
+def test_read_api_matches_reference():
+    """edge_list / degree / edge_weight / neighbors / guard_count
+    (graph.hpp:94-126, 208-223) after a few window slides."""
+    stream = _window_stream("rmat", 2**11, 20000)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    rng = np.random.default_rng(8)
+    w = rng.integers(1, 50, len(s)).astype(float)
+    g = DynamicGraph.from_edges(2**11, s[:half], d[:half], w[:half])
+    r = RefGraph(2**11, s[:half], d[:half], w[:half])
+    win = RefWindow(stream)
+    for _ in range(3):
+        args = win.slide(900)
+        g.apply_batch(*args)
+        r.apply_batch(*args)
+    ro, col, val = r.csr_snapshot()
+    es, ed, ew = g.edge_list()
+    deg = np.diff(ro.astype(np.int64))
+    assert (es == np.repeat(np.arange(2**11), deg)).all() and (ed == col).all() and (ew == val).all()
+    assert g.guard_count() == 2**11
+    for v in rng.integers(0, 2**11, 40):
+        v = int(v)
+        assert g.degree(v) == deg[v]
+        nd, nw = g.neighbors(v)
+        assert (nd == col[ro[v]:ro[v + 1]]).all() and (nw == val[ro[v]:ro[v + 1]]).all()
+        if deg[v]:
+            j = int(rng.integers(ro[v], ro[v + 1]))
+            assert g.edge_weight(v, int(col[j])) == val[j]
+    assert g.edge_weight(0, 2**11 - 1) is None or (0, 2**11 - 1) in set(zip(es.tolist(), ed.tolist()))
+    with pytest.raises(IndexError):
+        g.degree(2**11)
