@@ -23,6 +23,7 @@ value = all ranks' updates / max-over-ranks time ("scaling": "weak").
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import statistics
@@ -290,15 +291,25 @@ def run_ours(args):
     e1 = torch.cuda.Event(enable_timing=True)
     h2d = d2h = 0
     e2e_updates = 0
+    e2e_stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
     e0.record(ext2)
     for a, b, c, d, _ in host[W:]:
         st = g2.apply_batch(a, b, None, c, d, with_touched=False)
+        tm2 = g2.last_timing()
+        for k in e2e_stage:
+            e2e_stage[k] += getattr(tm2, k)
         e2e_updates += st.batch_size
         h2d += a.nbytes + b.nbytes + c.nbytes + d.nbytes
         d2h += 632  # pma_stats read back every step
     e1.record(ext2)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
+    # the link the inputs cross: a step's bytes of page-locked memory moved by
+    # the copy engines and read in place by SM loads (best of 5 each)
+    hbuf = torch.empty(h2d // K, dtype=torch.uint8).pin_memory()
+    cp_gbps, zc_gbps = C.c_double(), C.c_double()
+    lib.gpma_probe_h2d(dev, C.c_void_p(hbuf.data_ptr()), hbuf.numel(), 5, C.byref(cp_gbps), C.byref(zc_gbps))
+    del hbuf
     if world > 1:
         t = torch.tensor([e2e_ms], device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -306,7 +317,10 @@ def run_ours(args):
         torch.distributed.all_reduce(u)
         e2e_ms, e2e_updates = float(t.item()), float(u.item())
     e2e = {"value": e2e_updates / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
-           "d2h_bytes_per_step": d2h // K}
+           "d2h_bytes_per_step": d2h // K, "ms_per_step": e2e_ms / K,
+           "stage_ms_per_step": {k: round(v / K, 4) for k, v in e2e_stage.items()},
+           "link_GBps": {"memcpy": round(cp_gbps.value, 1), "zero_copy_read": round(zc_gbps.value, 1)},
+           "inputs": "page-locked host arrays, read in place over PCIe by the front-end kernel"}
     del g2
 
     # ---- roofline of the dominant kernel (warp-tier commit: decide+merge+scatter) ----

@@ -360,6 +360,12 @@ int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local);
  * loading never lands inside a timed region (call once per process/device). */
 int gpma_warmup(int device);
 
+/* Link diagnostic: best-of-`reps` rate of moving `bytes` of page-locked host
+ * memory to the device by cudaMemcpyAsync (copy engines) and by SM loads in
+ * place (zero-copy, as gpma_apply_batch reads pinned batches).  GB/s. */
+int gpma_probe_h2d(int device, const void* host, size_t bytes, int reps, double* memcpy_gbps,
+                   double* zero_copy_gbps);
+
 /* ---- Rebuild-CSR baseline (the paper's rebuild-per-batch comparison point)
  * RebuildCsrGraph (baselines.hpp:85-181) on the device: sorted unique edge
  * list + CSR arrays rebuilt from scratch after every batch.  Same contract as

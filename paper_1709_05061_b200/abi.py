@@ -219,6 +219,7 @@ SIGNATURES = [
     ("gpma_pr_finish", C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_double, C.POINTER(C.c_double)]),
     ("gpma_shard_spmv", C.c_int, [_P, _P, _P]),
     ("gpma_warmup", C.c_int, [C.c_int]),
+    ("gpma_probe_h2d", C.c_int, [C.c_int, _P, C.c_size_t, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("gpma_rebuild_create", C.c_int, [C.c_int, C.c_size_t, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
     ("gpma_rebuild_create_device", C.c_int, [C.c_int, C.c_size_t, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
     ("gpma_rebuild_destroy", C.c_int, [_P]),

@@ -562,6 +562,7 @@ __global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_de
 // --------------------------------------------------------------- commit args
 
 struct CommitArgs {
+    u64* tlist;  // touched ranges (b, e) of merge commits, appended at ctr->ntouched_next
     u64* keys;
     u64* vals;
     u8* st;
@@ -752,6 +753,15 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// touched range of a merge commit (update_stats.hpp touched_ranges): appended
+// in any order; pma_touched_ranges sorts them into the reference's order
+// (level by level = by range size, segments ascending within a level)
+__device__ __forceinline__ void touched_append(const CommitArgs& a, u64 b, u64 e) {
+    const ull slot = atomicAdd(&a.ctr->ntouched_next, 1ull);
+    a.tlist[2 * slot] = b;
+    a.tlist[2 * slot + 1] = e;
+}
+
 // Only launched at level 0 (m == leaf == 16), where the pending list is the
 // identity (a.pidx == nullptr): a tile's updates are one contiguous range.
 // Staging is asynchronous (cp.async, no registers held): phase 1 brings the
@@ -859,12 +869,25 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             if (s > kBigSlice) {
                 mode = 3;
             } else {
-                for (u32 q = 0; q < s; ++q) {
-                    const u32 i = soff + q;
-                    const u8 oq = i < staged ? s_op[obase + i] : a.uop[lo + q];
-                    ins += oq == kOpInsert;
+                // op bytes are 0 (insert) / 1 (delete): deletes = popc of the
+                // slice's op words (masked at both ends)
+                static_assert(kOpInsert == 0 && kOpDelete == 1, "op encoding");
+                u32 dels = 0;
+                if (soff + s <= staged) {
+                    const u32 st0 = obase + soff, st1 = st0 + s;
+                    for (u32 wd = st0 >> 2; wd < (st1 + 3) >> 2; ++wd) {
+                        u32 x = s_uo[w][wd];
+                        if (wd == (st0 >> 2)) x &= 0xffffffffu << (8 * (st0 & 3u));
+                        if (wd == ((st1 - 1) >> 2) && (st1 & 3u)) x &= 0xffffffffu >> (8 * (4 - (st1 & 3u)));
+                        dels += __popc(x);
+                    }
+                } else {
+                    for (u32 q = 0; q < s; ++q) {
+                        const u32 i = soff + q;
+                        dels += (i < staged ? s_op[obase + i] : a.uop[lo + q]) == kOpDelete;
+                    }
                 }
-                const u32 dels = s - ins;
+                ins = s - dels;
                 if (!a.eager && ins == 0) mode = 1;
                 else if (!(nv + ins > a.mx || (a.eager && a.cap_gt_min && u64(nv) < u64(dels) + a.mn))) mode = 2;
             }
@@ -986,19 +1009,15 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
         __syncwarp();
         // write back: states (own leaf), keys/values (merge groups, coalesced)
         if (mode == 1 || mode == 2) {
+            // 4 mask bits -> 4 bytes (bit i -> bit 0 of byte i) by one multiply;
+            // Valid = 1, Tombstone = 2 (newvalid and tombs are disjoint)
+            static_assert(kValid == 1 && kTombstone == 2 && kEmpty == 0, "state encoding");
+            auto bytes4 = [](u32 m) { return ((m & 0xfu) * 0x00204081u) & 0x01010101u; };
             uint4 ns;
-            u32* o = reinterpret_cast<u32*>(&ns);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                u32 word = 0;
-#pragma unroll
-                for (int by = 0; by < 4; ++by) {
-                    const int i = q * 4 + by;
-                    const u32 x = ((newvalid >> i) & 1u) ? kValid : (((tombs >> i) & 1u) ? kTombstone : kEmpty);
-                    word |= x << (8 * by);
-                }
-                o[q] = word;
-            }
+            ns.x = bytes4(newvalid) | (bytes4(tombs) << 1);
+            ns.y = bytes4(newvalid >> 4) | (bytes4(tombs >> 4) << 1);
+            ns.z = bytes4(newvalid >> 8) | (bytes4(tombs >> 8) << 1);
+            ns.w = bytes4(newvalid >> 12) | (bytes4(tombs >> 12) << 1);
             *reinterpret_cast<uint4*>(a.st + b) = ns;
         }
         if (mergemask) {
@@ -1020,6 +1039,19 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
                 const ull slot = atomicAdd(&a.ctr->nrefresh, 1ull);
                 a.rlist[2 * slot] = b;
                 a.rlist[2 * slot + 1] = b + 16;
+            }
+        }
+        {
+            const unsigned mm = __ballot_sync(FULL, act && mode == 2);
+            if (mm) {
+                ull base = 0;
+                if (lane == 0) base = atomicAdd(&a.ctr->ntouched_next, ull(__popc(mm)));
+                base = __shfl_sync(FULL, base, 0);
+                if (act && mode == 2) {
+                    const ull slot = base + __popc(mm & ((1u << lane) - 1u));
+                    a.tlist[2 * slot] = b;
+                    a.tlist[2 * slot + 1] = b + 16;
+                }
             }
         }
         if (act) {
@@ -1240,6 +1272,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
             }
             if (hl == 0 && act && !big) {
                 a.gflag[gid_] = u8(mode);
+                if (mode == 2) touched_append(a, b, b + m);
                 acc.bytes += alg_bytes(m, s, mode);
                 if (mode == 1) {
                     const unsigned added = __popc(hits);
@@ -1360,6 +1393,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
         }
         if (threadIdx.x == 0) {
             a.gflag[g] = flag;
+            if (flag == 2) touched_append(a, b, b + m);
             acc.bytes += alg_bytes(m, s, flag);
             if (flag) acc.committed++;
         }
@@ -1936,6 +1970,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             }
             // commit (decide + merge + scatter)
             CommitArgs a{};
+            a.tlist = touched_ptr;
             a.keys = d_keys;
             a.vals = d_vals;
             a.st = d_st;
@@ -1998,34 +2033,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             GPMA_LAUNCH_CHECK();
             GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));
             ++launches;
-            // touched list (merge commits, in segment order) + the level's stats
-            {
-                const u8* gf = gflag.ptr;
-                const u32* gg = gseg.ptr;
-                u64* tp = touched_ptr;
-                Ctr* ctr = d_ctr;
-                const int lv = level;
-                run_compact(
-                    stream_, ws, &d_ctr->ngroups, 0, npend, [=] __device__(ull g) { return gf[g] == 2; },
-                    [=] __device__(ull g, unsigned f, ull x) {
-                        if (!f) return;
-                        const u64 base = ctr->ntouched_base;
-                        const u64 seg = gg[g];
-                        tp[2 * (base + x)] = seg * m;
-                        tp[2 * (base + x) + 1] = seg * m + m;
-                    },
-                    [=] __device__(ull total) {
-                        ctr->ntouched_next = ctr->ntouched_base + total;
-                        ctr->lvl_committed[lv] = ctr->committed;
-                        ctr->lvl_groups[lv] = ctr->ngroups;
-                        ctr->lvl_big[lv] = ctr->nbig;
-                        ctr->lvl_maxslice[lv] = ctr->max_slice;
-                        ctr->committed = 0;
-                        ctr->nbig = 0;
-                        ctr->max_slice = 0;
-                    });
-                ++launches;
-            }
             // advance_round: keep deferred groups' updates
             {
                 const u8* gf = gflag.ptr;
@@ -2033,6 +2040,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 const u32* pp = pcur;
                 u32* pn = pnext;
                 Ctr* ctr = d_ctr;
+                const int lv = level;
                 run_compact(
                     stream_, ws, np_cur, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
                     [=] __device__(ull p, unsigned f, ull x) {
@@ -2040,7 +2048,14 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                     },
                     [=] __device__(ull total) {
                         *np_next = total;
-                        ctr->ntouched_base = ctr->ntouched_next;
+                        // the level's stats (read at the next host sync)
+                        ctr->lvl_committed[lv] = ctr->committed;
+                        ctr->lvl_groups[lv] = ctr->ngroups;
+                        ctr->lvl_big[lv] = ctr->nbig;
+                        ctr->lvl_maxslice[lv] = ctr->max_slice;
+                        ctr->committed = 0;
+                        ctr->nbig = 0;
+                        ctr->max_slice = 0;
                     });
                 ++launches;
             }
@@ -2326,8 +2341,20 @@ void Pma::touched_ranges(u64* pairs, size_t capn, size_t* count) {
     *count = last_ntouched;
     const size_t n = std::min<size_t>(capn, last_ntouched);
     if (n && pairs) {
-        GPMA_CUDA(cudaMemcpyAsync(pairs, touched.ptr, n * 16, cudaMemcpyDeviceToHost, stream_));
+        // the commit kernels append in any order: restore the reference's
+        // (rounds in level order, segments ascending inside a round; a level's
+        // ranges all have the same size, larger at each level)
+        std::vector<std::pair<u64, u64>> all(last_ntouched);
+        GPMA_CUDA(cudaMemcpyAsync(all.data(), touched.ptr, last_ntouched * 16, cudaMemcpyDeviceToHost, stream_));
         GPMA_CUDA(cudaStreamSynchronize(stream_));
+        std::sort(all.begin(), all.end(), [](const std::pair<u64, u64>& x, const std::pair<u64, u64>& y) {
+            const u64 sx = x.second - x.first, sy = y.second - y.first;
+            return sx != sy ? sx < sy : x.first < y.first;
+        });
+        for (size_t i = 0; i < n; ++i) {
+            pairs[2 * i] = all[i].first;
+            pairs[2 * i + 1] = all[i].second;
+        }
     }
 }
 
