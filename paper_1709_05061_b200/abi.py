@@ -17,7 +17,8 @@ PMA_STRATEGY_AUTO, PMA_STRATEGY_SMALL, PMA_STRATEGY_MEDIUM, PMA_STRATEGY_LARGE =
 GPMA_UNREACHED = 0xFFFFFFFF
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpmagraph_cuda.so")
+# GPMA_LIB: an alternative build of the same library (A/B experiments)
+LIB_PATH = os.environ.get("GPMA_LIB") or os.path.join(HERE, "libpmagraph_cuda.so")
 
 
 class pma_profile(C.Structure):

@@ -311,7 +311,7 @@ __device__ __forceinline__ void bucket_n(const BucketArgs& ba, const u64* idx, c
             }
         }
     }
-    for (;;) {
+    for (;;) {  // lock-stepped bisections over hdr
         bool more = false;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
@@ -388,7 +388,7 @@ __device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib
 // `oor` (the batch is then redone on the generic path).  kBucket: also the
 // leaf bucket of every update (leaf-bucket front end, see batch_update_device).
 template <bool kBucket>
-__global__ void __launch_bounds__(256, kBucket ? 5 : 1) k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr,
+__global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr,
                              BucketArgs ba) {
     PrepAcc acc;
     if (f.mk) {
@@ -724,7 +724,6 @@ __device__ __forceinline__ void load_group_tile(const CommitArgs& a, ull g0, ull
 // Groups with more than kBigSlice updates (RMAT hub rows) are handed to the
 // CTA kernel through `biglist`.
 constexpr int kLeafWarps = 4;
-constexpr int kRow = 17;        // padded u64 row (conflict-free column access)
 constexpr u32 kBigSlice = 32;   // leaf kernel: larger slices go to the CTA kernel
 constexpr u32 kLaneBig = 64;    // lane kernels: larger slices go to the CTA kernel
 constexpr u32 kStage = 64;      // updates of a 32-group tile staged in smem (overflow read from HBM)

@@ -113,7 +113,7 @@ __global__ void k_route_scatter(RouteIn in, const u32* __restrict__ bounds, int 
     for (int i = threadIdx.x; i <= world; i += blockDim.x) s_b[i] = bounds[i];
     for (int i = threadIdx.x; i < kRouteItems * kWarps * world; i += blockDim.x) s_wc[i] = 0;
     __syncthreads();
-    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const unsigned warp = threadIdx.x >> 5;
     const u64 base = u64(blockIdx.x) * kRouteTile;
     int own[kRouteItems];
     unsigned rank[kRouteItems];
