@@ -65,6 +65,20 @@ int gpma_window_destroy(gpma_window* w);
 int gpma_window_info(const gpma_window* w, gpma_window_info_t* out);
 int gpma_window_reserve(gpma_window* w, size_t max_deletions);
 int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out);
+/* std::mt19937_64 owned by the caller (the reference passes it by reference;
+ * its state advances across slides). */
+typedef struct gpma_rng gpma_rng;
+int gpma_rng_create(uint64_t seed, gpma_rng** out);
+int gpma_rng_destroy(gpma_rng* r);
+/* SlidingWindow::slide_explicit_random (streaming.hpp:129-158): the next
+ * `batch` arrivals, and min(batch, window size) expiring edges drawn uniformly
+ * without replacement from the window before the arrivals; deletions are the
+ * expiries whose key leaves the window (multiplicity filtered), in window
+ * order, appended like gpma_window_slide's.  FIFO and explicit slides may be
+ * mixed on one window. */
+int gpma_window_slide_explicit_random(gpma_window* w, size_t batch, gpma_rng* rng, gpma_slide_t* out);
+/* SlidingWindow::window_size (streaming.hpp:101) */
+uint64_t gpma_window_size(const gpma_window* w);
 /* Copy deletions [offset, offset+n) of the window to host arrays. */
 int gpma_window_deletions_host(gpma_window* w, size_t offset, size_t n, uint32_t* src, uint32_t* dst);
 

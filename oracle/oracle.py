@@ -456,12 +456,38 @@ class RefWindow:
         _check(ref_lib(), ref_lib().ref_window_last(self.h, _p(a), _p(b), _p(w), _p(c), _p(d)), "ref_last_error")
         return a, b, w, c, d
 
+    def slide_explicit_random(self, batch, rng: "RefRng"):
+        """streaming.hpp:129-158 (rng state advances across calls)"""
+        ni, nd = C.c_uint64(), C.c_uint64()
+        _check(ref_lib(), ref_lib().ref_window_slide_explicit_random(self.h, C.c_size_t(batch), rng.h, C.byref(ni),
+                                                                     C.byref(nd)), "ref_last_error")
+        return self._last(ni.value, nd.value)
+
+    def _last(self, ni, nd):
+        a, b, w = np.zeros(ni, np.uint32), np.zeros(ni, np.uint32), np.zeros(ni, np.float64)
+        c, d = np.zeros(nd, np.uint32), np.zeros(nd, np.uint32)
+        _check(ref_lib(), ref_lib().ref_window_last(self.h, _p(a), _p(b), _p(w), _p(c), _p(d)), "ref_last_error")
+        return a, b, w, c, d
+
     def remaining(self):
         return int(ref_lib().ref_window_remaining(self.h))
 
     def __del__(self):
         if getattr(self, "h", None) and _ref is not None:
             _ref.ref_window_destroy(self.h)
+            self.h = None
+
+
+class RefRng:
+    """std::mt19937_64(seed) owned by the caller (streaming.hpp:129)."""
+
+    def __init__(self, seed):
+        self.h = C.c_void_p()
+        _check(ref_lib(), ref_lib().ref_rng_create(C.c_uint64(seed), C.byref(self.h)), "ref_last_error")
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_rng_destroy(self.h)
             self.h = None
 
 
@@ -476,7 +502,7 @@ def hardware_concurrency():
     return int(ref_lib().ref_hardware_concurrency())
 
 
-__all__ = ["RefPMA", "PortPMA", "RefGraph", "PortGraph", "RefStream", "RefWindow", "OracleError", "build",
+__all__ = ["RefPMA", "PortPMA", "RefGraph", "PortGraph", "RefStream", "RefWindow", "RefRng", "OracleError", "build",
            "have_ref", "stats_dict", "draw_below_sequence", "hardware_concurrency", "PMA_MAX_LEVELS"]
 
 

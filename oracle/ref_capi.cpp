@@ -542,12 +542,21 @@ int ref_window_slide(ref_window* w, size_t batch, uint64_t* n_ins, uint64_t* n_d
     });
 }
 
-int ref_window_slide_explicit_random(ref_window* w, size_t batch, uint64_t seed_state_id, uint64_t* n_ins,
-                                     uint64_t* n_del) {
-    (void)seed_state_id;
+// SlidingWindow::slide_explicit_random (streaming.hpp:129-158) with a caller-owned
+// engine (its state advances across calls, as the reference's std::mt19937_64&)
+struct ref_rng {
+    std::mt19937_64 r;
+};
+int ref_rng_create(uint64_t seed, ref_rng** out) {
+    return guarded([&] { *out = new ref_rng{std::mt19937_64(seed)}; });
+}
+int ref_rng_destroy(ref_rng* r) {
+    delete r;
+    return 0;
+}
+int ref_window_slide_explicit_random(ref_window* w, size_t batch, ref_rng* rng, uint64_t* n_ins, uint64_t* n_del) {
     return guarded([&] {
-        static thread_local std::mt19937_64 rng(1);
-        w->last = w->w->slide_explicit_random(batch, rng);
+        w->last = w->w->slide_explicit_random(batch, rng->r);
         *n_ins = w->last.inserts.size();
         *n_del = w->last.deletions.size();
     });

@@ -247,6 +247,10 @@ SIGNATURES = [
     ("gpma_window_reserve", C.c_int, [_P, C.c_size_t]),
     ("gpma_window_slide", C.c_int, [_P, C.c_size_t, C.POINTER(gpma_slide_t)]),
     ("gpma_window_deletions_host", C.c_int, [_P, C.c_size_t, C.c_size_t, _P, _P]),
+    ("gpma_rng_create", C.c_int, [C.c_uint64, C.POINTER(_P)]),
+    ("gpma_rng_destroy", C.c_int, [_P]),
+    ("gpma_window_slide_explicit_random", C.c_int, [_P, C.c_size_t, _P, C.POINTER(gpma_slide_t)]),
+    ("gpma_window_size", C.c_uint64, [_P]),
 ]
 
 _lib = None

@@ -54,16 +54,65 @@ __global__ void k_pack_stream(const u32* s, const u32* d, u64 n, u64* k, u32* p)
     }
 }
 
+// Window state.  FIFO mode (every slide so far was a FIFO slide): the
+// resident set is the position range [lo, cursor) and deletions come from
+// next-occurrence positions.  General mode (after the first explicit random
+// slide, streaming.hpp:129-158, whose evictions leave holes): the resident
+// positions in window order + a multiplicity per distinct key (dense key ids
+// from the stream's key sort), so an expiry's deletion is decided by counts.
 struct Window {
     int device = 0;
     cudaStream_t stream = nullptr;
     uint64_t n = 0, lo = 0, cursor = 0;
     DevBuf<u32> src, dst, next;
+    DevBuf<u32> kid;               // stream position -> dense key id
     DevBuf<u32> del_src, del_dst;  // all deletions emitted so far (appended)
     uint64_t ndel = 0;
     ScanWorkspace ws;
     DevBuf<ull> cnt;
+    // general mode
+    bool general = false;
+    uint64_t wsize = 0;          // resident entries
+    DevBuf<u32> res, res2;       // resident stream positions, window order
+    DevBuf<u32> mult, lastpick;  // per key id: multiplicity; 1 + its last expiring index
+    DevBuf<u8> picked;           // per index of (resident ++ arrivals): expires now
+    DevBuf<u32> plist;           // drawn indices (explicit slides)
 };
+
+__global__ void k_key_ids(const u32* sp, const u32* sorted_kid, u64 n, u32* kid) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        kid[sp[i]] = sorted_kid[i];
+}
+
+__global__ void k_iota_from(u32* out, u64 first, u64 n) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        out[i] = u32(first + i);
+}
+
+// multiplicity += 1 for stream positions [first, first + n)
+__global__ void k_count_keys(u64 n, u64 first, const u32* kid, u32* mult) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+        atomicAdd(&mult[kid[first + i]], 1u);
+}
+
+// the expiring indices of (resident ++ arrivals): the drawn list, or the FIFO
+// front [0, ne).  release: flag it, drop its key's count, record the key's
+// last expiring index; else: clear that record again
+__global__ void k_mark_release(const u32* plist, u64 ne, const u32* res, u64 old, u64 cursor, const u32* kid,
+                               u32* mult, u32* lastpick, u8* picked, int release) {
+    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < ne; t += u64(gridDim.x) * blockDim.x) {
+        const u32 i = plist ? plist[t] : u32(t);
+        const u32 p = i < old ? res[i] : u32(cursor + (i - old));
+        const u32 k = kid[p];
+        if (release) {
+            picked[i] = 1;
+            atomicSub(&mult[k], 1u);
+            atomicMax(&lastpick[k], i + 1);
+        } else {
+            lastpick[k] = 0;
+        }
+    }
+}
 
 }  // namespace gpma
 
@@ -93,9 +142,153 @@ int sguard(F&& f) {
 }
 }  // namespace
 
+struct gpma_rng {
+    std::mt19937_64 r;
+};
+
+namespace gpma {
+
+// A slide in general mode: FIFO (rng == nullptr, streaming.hpp:107-123) or
+// explicit random eviction (streaming.hpp:129-158).  Arrivals are admitted
+// first; the expiring indices of (resident ++ arrivals) release their keys;
+// an expiry emits a deletion iff its key's multiplicity ends at zero and it
+// is that key's last expiry in window order — what the reference's
+// sequential releases give, since no admission happens between releases.
+// The caller has reserved room for `take` more deletions.
+static void slide_general(Window& W, size_t batch, std::mt19937_64* rng, gpma_slide_t* out) {
+    const uint64_t remaining = W.n - W.cursor;
+    const uint64_t take = batch < remaining ? batch : remaining;
+    const uint64_t old = W.wsize, tot = old + take;
+    out->ins_offset = W.cursor;
+    out->n_ins = take;
+    out->del_offset = W.ndel;
+    out->final_partial = take < batch ? 1 : 0;
+    out->n_del = 0;
+    if (take == 0) return;
+    // explicit: the expiring entries are drawn uniformly without replacement
+    // among the window before the arrivals — the reference's exact draws
+    uint64_t ne = take;
+    const u32* plist = nullptr;
+    if (rng) {
+        ne = take < old ? take : old;
+        std::vector<char> hp(old, 0);
+        std::vector<u32> hl;
+        hl.reserve(ne);
+        for (uint64_t drawn = 0; drawn < ne;) {
+            const uint64_t idx = draw_below(*rng, old);
+            if (hp[idx]) continue;
+            hp[idx] = 1;
+            hl.push_back(u32(idx));
+            ++drawn;
+        }
+        W.plist.reserve(ne + 1);
+        if (ne) GPMA_CUDA(cudaMemcpy(W.plist.ptr, hl.data(), ne * 4, cudaMemcpyHostToDevice));
+        plist = W.plist.ptr;
+    }
+    W.picked.reserve(tot + 1);
+    W.res2.reserve(tot + 1);
+    k_count_keys<<<grid_for(take, 256), 256, 0, W.stream>>>(take, W.cursor, W.kid.ptr, W.mult.ptr);  // admit
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaMemsetAsync(W.picked.ptr, 0, tot, W.stream));
+    if (ne) {
+        k_mark_release<<<grid_for(ne, 256), 256, 0, W.stream>>>(plist, ne, W.res.ptr, old, W.cursor, W.kid.ptr,
+                                                                W.mult.ptr, W.lastpick.ptr, W.picked.ptr, 1);
+        GPMA_LAUNCH_CHECK();
+    }
+    uint64_t nd = 0;
+    {
+        const u8* pk = W.picked.ptr;
+        const u32* res = W.res.ptr;
+        const u32* kid = W.kid.ptr;
+        const u32* mult = W.mult.ptr;
+        const u32* lp = W.lastpick.ptr;
+        const u32* ss = W.src.ptr;
+        const u32* dd = W.dst.ptr;
+        u32* os = W.del_src.ptr + W.ndel;
+        u32* od = W.del_dst.ptr + W.ndel;
+        u32* r2 = W.res2.ptr;
+        ull* cnt = W.cnt.ptr;
+        const uint64_t cur = W.cursor;
+        GPMA_CUDA(cudaMemsetAsync(cnt, 0, 8, W.stream));
+        // deletions, in window order
+        run_compact(
+            W.stream, W.ws, nullptr, tot, tot,
+            [=] __device__(ull i) {
+                if (!pk[i]) return false;
+                const u32 k = kid[i < old ? res[i] : u32(cur + (i - old))];
+                return mult[k] == 0 && lp[k] == u32(i + 1);
+            },
+            [=] __device__(ull i, unsigned f, ull x) {
+                if (f) {
+                    const u32 p = i < old ? res[i] : u32(cur + (i - old));
+                    os[x] = ss[p];
+                    od[x] = dd[p];
+                }
+            },
+            [=] __device__(ull total) { *cnt = total; });
+        // the new window: survivors, then the arrivals, in order
+        run_compact(
+            W.stream, W.ws, nullptr, tot, tot, [=] __device__(ull i) { return pk[i] == 0; },
+            [=] __device__(ull i, unsigned f, ull x) {
+                if (f) r2[x] = i < old ? res[i] : u32(cur + (i - old));
+            },
+            NoFin{});
+        GPMA_CUDA(cudaMemcpyAsync(&nd, cnt, 8, cudaMemcpyDeviceToHost, W.stream));
+    }
+    if (ne) {
+        k_mark_release<<<grid_for(ne, 256), 256, 0, W.stream>>>(plist, ne, W.res.ptr, old, W.cursor, W.kid.ptr,
+                                                                W.mult.ptr, W.lastpick.ptr, W.picked.ptr, 0);
+        GPMA_LAUNCH_CHECK();
+    }
+    GPMA_CUDA(cudaStreamSynchronize(W.stream));
+    std::swap(W.res.ptr, W.res2.ptr);
+    std::swap(W.res.cap, W.res2.cap);
+    W.wsize = tot - ne;
+    out->n_del = nd;
+    W.ndel += nd;
+    W.cursor += take;
+}
+
+// FIFO -> general mode: resident = positions [lo, cursor), counts from them
+static void to_general(Window& W) {
+    if (W.general) return;
+    const uint64_t ws = W.cursor - W.lo;
+    W.res.reserve(W.n + 1);
+    W.res2.reserve(W.n + 1);
+    W.mult.reserve(W.n + 1);
+    W.lastpick.reserve(W.n + 1);
+    GPMA_CUDA(cudaMemsetAsync(W.mult.ptr, 0, W.n * 4, W.stream));
+    GPMA_CUDA(cudaMemsetAsync(W.lastpick.ptr, 0, W.n * 4, W.stream));
+    if (ws) {
+        k_iota_from<<<grid_for(ws, 256), 256, 0, W.stream>>>(W.res.ptr, W.lo, ws);
+        GPMA_LAUNCH_CHECK();
+        k_count_keys<<<grid_for(ws, 256), 256, 0, W.stream>>>(ws, W.lo, W.kid.ptr, W.mult.ptr);
+        GPMA_LAUNCH_CHECK();
+    }
+    GPMA_CUDA(cudaStreamSynchronize(W.stream));
+    W.wsize = ws;
+    W.general = true;
+}
+
+}  // namespace gpma
+
 extern "C" {
 
 const char* gpma_stream_last_error(void) { return g_stream_err.c_str(); }
+
+int gpma_rng_create(uint64_t seed, gpma_rng** out) {
+    return sguard([&] { *out = new gpma_rng{std::mt19937_64(seed)}; });
+}
+
+int gpma_rng_destroy(gpma_rng* r) {
+    delete r;
+    return PMA_OK;
+}
+
+uint64_t gpma_window_size(const gpma_window* w) {
+    if (!w) return 0;
+    return w->w.general ? w->w.wsize : w->w.cursor - w->w.lo;
+}
 
 // gen_rmat (generators.hpp:26-63)
 int gpma_stream_rmat(size_t nv, size_t ne, double a, double b, double c, double d, uint64_t seed,
@@ -239,6 +432,20 @@ int gpma_window_create(const gpma_stream* s, int device, gpma_window** out) {
                                                       W.stream));
             gpma::k_next_occ<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(k1.ptr, p1.ptr, n, W.next.ptr);
             GPMA_LAUNCH_CHECK();
+            // dense key ids (general mode's multiplicity index): the rank of
+            // the distinct key in the sorted order
+            W.kid.reserve(n);
+            {
+                const gpma::u64* sk = k1.ptr;
+                gpma::u32* sid = p0.ptr;  // reused: per sorted index
+                gpma::run_compact(
+                    W.stream, W.ws, nullptr, n, n,
+                    [=] __device__(gpma::ull i) { return i == 0 || sk[i] != sk[i - 1]; },
+                    [=] __device__(gpma::ull i, unsigned f, gpma::ull x) { sid[i] = gpma::u32(x + f - 1); },
+                    gpma::NoFin{});
+                gpma::k_key_ids<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(p1.ptr, sid, n, W.kid.ptr);
+                GPMA_LAUNCH_CHECK();
+            }
             GPMA_CUDA(cudaStreamSynchronize(W.stream));
         }
         W.lo = 0;
@@ -306,6 +513,10 @@ int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out) {
             int rc = gpma_window_reserve(w, want);
             if (rc) throw ApiError(rc, g_stream_err);
         }
+        if (W.general) {  // after an explicit random slide the window has holes
+            gpma::slide_general(W, batch, nullptr, out);
+            return;
+        }
         out->ins_offset = W.cursor;
         out->n_ins = take;
         out->del_offset = W.ndel;
@@ -337,6 +548,26 @@ int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out) {
         W.ndel += nd;
         W.lo += take;
         W.cursor = end;
+    });
+}
+
+// SlidingWindow::slide_explicit_random (streaming.hpp:129-158): arrivals as
+// in gpma_window_slide; the expiring edges are drawn by `rng` (its state
+// advances) uniformly without replacement from the window as it stood before
+// the arrivals; deletions appended as gpma_window_slide's.
+int gpma_window_slide_explicit_random(gpma_window* w, size_t batch, gpma_rng* rng, gpma_slide_t* out) {
+    return sguard([&] {
+        auto& W = w->w;
+        if (!rng) throw ApiError(PMA_EINVAL, "slide_explicit_random: null rng");
+        GPMA_CUDA(cudaSetDevice(W.device));
+        const uint64_t remaining = W.n - W.cursor;
+        const uint64_t take = batch < remaining ? batch : remaining;
+        if (W.ndel + take > W.del_src.cap) {
+            int rc = gpma_window_reserve(w, size_t((W.ndel + take) * 2 + 1024));
+            if (rc) throw ApiError(rc, g_stream_err);
+        }
+        gpma::to_general(W);
+        gpma::slide_general(W, batch, &rng->r, out);
     });
 }
 

@@ -642,6 +642,20 @@ def draw_below_sequence(seed: int, bound: int, n: int):
     return out
 
 
+class Mt19937_64:
+    """A caller-owned std::mt19937_64 (streaming.hpp:129 takes one by reference)."""
+
+    def __init__(self, seed: int):
+        self._lib = load_library()
+        self.h = C.c_void_p()
+        EdgeStream._chk(self._lib, self._lib.gpma_rng_create(C.c_uint64(seed), C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.gpma_rng_destroy(self.h)
+            self.h = None
+
+
 class SlidingWindow:
     """Device sliding window (streaming.hpp:76-123): slides return device
     offsets into the stream (inserts) and the window's deletion arrays."""
@@ -668,6 +682,20 @@ class SlidingWindow:
         EdgeStream._chk(self._lib, self._lib.gpma_window_slide(self.h, batch, C.byref(s)))
         return s
 
+    def slide_explicit_random(self, batch: int, rng: "Mt19937_64"):
+        """streaming.hpp:129-158: expiries drawn by `rng` (its state advances)."""
+        from .abi import gpma_slide_t
+        s = gpma_slide_t()
+        EdgeStream._chk(self._lib, self._lib.gpma_window_slide_explicit_random(self.h, batch, rng.h, C.byref(s)))
+        return s
+
+    def window_size(self) -> int:
+        return int(self._lib.gpma_window_size(self.h))
+
+    def remaining(self) -> int:
+        i = self.info()
+        return int(i.stream_size - i.cursor)
+
     def deletions_host(self, offset: int, n: int, src=None, dst=None):
         """Copy deletions [offset, offset+n) to host arrays (pinned if given)."""
         s = np.zeros(n, np.uint32) if src is None else src
@@ -681,6 +709,6 @@ class SlidingWindow:
             self.h = None
 
 
-__all__ = ["EdgeStream", "SlidingWindow", "draw_below_sequence", "PackedMemoryArray", "DynamicGraph", "DensityProfile", "UpdateStats", "SegmentEngineConfig",
+__all__ = ["EdgeStream", "SlidingWindow", "Mt19937_64", "draw_below_sequence", "PackedMemoryArray", "DynamicGraph", "DensityProfile", "UpdateStats", "SegmentEngineConfig",
            "GraphConfig", "PageRankResult", "batch_update", "bfs", "connected_components", "pagerank", "spmv",
            "LogicError", "kUnreached", "kMinCapacity", "PMA_LAZY", "PMA_EAGER"]

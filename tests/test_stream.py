@@ -3,8 +3,8 @@ reference generators.hpp / streaming.hpp through the oracle."""
 import numpy as np
 import pytest
 
-from oracle.oracle import RefStream, RefWindow, draw_below_sequence as ref_draw
-from paper_1709_05061_b200.pmagraph import EdgeStream, SlidingWindow, draw_below_sequence
+from oracle.oracle import RefRng, RefStream, RefWindow, draw_below_sequence as ref_draw
+from paper_1709_05061_b200.pmagraph import EdgeStream, Mt19937_64, SlidingWindow, draw_below_sequence
 
 
 @pytest.mark.parametrize("kind", ["rmat", "er", "rmat_params"])
@@ -52,3 +52,45 @@ def test_device_window_matches_reference(batch):
         assert (d[sl.ins_offset:sl.ins_offset + sl.n_ins] == rb).all()
         c, dd = w.deletions_host(sl.del_offset, sl.n_del)
         assert (c == rc).all() and (dd == rd).all()
+
+
+def _same_slide(w, sl, s, d, ref):
+    ra, rb, _, rc, rd = ref
+    assert (s[sl.ins_offset:sl.ins_offset + sl.n_ins] == ra).all()
+    assert (d[sl.ins_offset:sl.ins_offset + sl.n_ins] == rb).all()
+    c, dd = w.deletions_host(sl.del_offset, sl.n_del)
+    assert len(c) == len(rc) and (c == rc).all() and (dd == rd).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("batch", [1, 16, 300, 5000])
+def test_device_explicit_random_slides_match_reference(batch):
+    """slide_explicit_random (streaming.hpp:129-158; test_streaming.cpp:137-190):
+    the drawn evictions, the multiplicity-filtered deletions (in window order)
+    and the arrivals equal the reference's for the same engine seed — also
+    when FIFO and explicit slides are mixed on one window."""
+    a = EdgeStream.rmat(2**8, 20000, seed=6)      # many duplicate arrivals
+    b = RefStream.rmat(2**8, 20000, seed=6)
+    w, rw = SlidingWindow(a, 0), RefWindow(b)
+    rng, rrng = Mt19937_64(11), RefRng(11)
+    s, d = a.arrays()
+    for i in range(14 if batch > 100 else 30):
+        if i % 3 == 2:
+            sl, ref = w.slide(batch), rw.slide(batch)
+        else:
+            sl, ref = w.slide_explicit_random(batch, rng), rw.slide_explicit_random(batch, rrng)
+        _same_slide(w, sl, s, d, ref)
+    assert w.window_size() == int(__import__("oracle").oracle.ref_lib().ref_window_size(rw.h))
+
+
+@pytest.mark.gpu
+def test_explicit_random_full_batch_replaces_window():
+    """test_streaming.cpp:137-150: a full-window batch evicts every old edge."""
+    a = EdgeStream.erdos_renyi(64, 0.5, seed=2)
+    b = RefStream.erdos_renyi(64, 0.5, seed=2)
+    w, rw = SlidingWindow(a, 0), RefWindow(b)
+    n0 = w.window_size()
+    s, d = a.arrays()
+    sl = w.slide_explicit_random(n0, Mt19937_64(5))
+    _same_slide(w, sl, s, d, rw.slide_explicit_random(n0, RefRng(5)))
+    assert w.window_size() == sl.n_ins
