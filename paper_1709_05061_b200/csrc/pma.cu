@@ -1729,8 +1729,10 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // one per 8 bits.  Skipped after a batch whose buckets overflowed.
         BucketArgs ba{};
         const u64 L = num_leaves();
+        // (its passes over the L leaf counters must stay small next to the
+        // radix passes over the n updates: measured break-even near L = 4n)
         bucket = ib && ro_base() && n >= kBucketMinBatch && n < (1ull << 31) && L + 2 < (1ull << 31) &&
-                 bucket_skip_ == 0;
+                 L <= 4 * n && bucket_skip_ == 0;
         if (bucket_skip_) --bucket_skip_;
         if (bucket) {
             bcnt.reserve(L + 2);

@@ -231,7 +231,7 @@ def test_pinned_host_batches_read_in_place():
 
 
 @pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
-@pytest.mark.parametrize("kind,nv,param,batch", [("er", 2**15, 2**-6, 70000), ("rmat", 2**16, 600000, 90000)])
+@pytest.mark.parametrize("kind,nv,param,batch", [("er", 2**14, 2**-6, 100000), ("rmat", 2**16, 600000, 90000)])
 def test_leaf_bucket_front_end_parity(mode, kind, nv, param, batch):
     """Batches >= 2^16 updates take the leaf-bucket front end (leaf found per
     update, counting sort by leaf, in-bucket rank): slot arrays, stats and row
