@@ -175,8 +175,8 @@ def test_bad_insert_reports_first_offender_and_leaves_graph_unchanged():
 
 @pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
 def test_large_batches_parity(mode):
-    """Batches of >= 2^16 updates take the sample-sort front end (sorted
-    packed words, csrc/sample_sort.cuh): slots, stats and row offsets stay
+    """Batches of >= 2^16 updates take the leaf-bucket front end when the
+    leaf count is within 4x the batch: slots, stats and row offsets stay
     bit-exact with the reference over several 150K-arrival slides."""
     nv = 2**16
     stream = _window_stream("rmat", nv, 900000, shuffle=2)
@@ -316,3 +316,40 @@ def test_read_api_matches_reference():
     assert g.edge_weight(0, 2**11 - 1) is None or (0, 2**11 - 1) in set(zip(es.tolist(), ed.tolist()))
     with pytest.raises(IndexError):
         g.degree(2**11)
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_leaf_bucket_edge_cases(mode):
+    """The leaf-bucket front end (batch >= 2^16, few leaves) with guard
+    deletes (bucket L), duplicate and cancelling updates inside one leaf,
+    deletes outside the key layout (generic redo), and a bad insert (rejected,
+    graph unchanged) — all as the reference."""
+    rng = np.random.default_rng(21)
+    nv = 2**12
+    s, d = rng.integers(0, nv, 30000), rng.integers(0, nv, 30000)
+    g = DynamicGraph.from_edges(nv, s, d, None, GraphConfig(deletion_mode=mode))
+    r = RefGraph(nv, s, d, None, graph_config(deletion_mode=mode))
+
+    def both(args, ctx, fronts=(1, 2)):
+        gs = g.apply_batch(*args)
+        assert int(g.last_timing().front_end) in fronts, ctx
+        rs = r.apply_batch(*args)
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
+
+    a, b = rng.integers(0, nv, 60000), rng.integers(0, nv, 60000)
+    a[:300], b[:300] = 9, 33  # one key inserted 300 times
+    c = np.concatenate([s[:9000], np.full(400, 9), rng.integers(0, nv, 500)]).astype(np.uint32)
+    dd = np.concatenate([d[:9000], np.full(400, 33), np.full(500, 0xFFFFFFFF)]).astype(np.uint32)  # + guard deletes
+    both((a, b, rng.integers(0, 9, 60000).astype(float), c, dd), "guards + duplicates")
+    c2 = np.concatenate([s[9000:20000], [2**20, 5]]).astype(np.uint32)  # a delete outside the layout
+    d2 = np.concatenate([d[9000:20000], [3, 2**30]]).astype(np.uint32)
+    a2, b2 = rng.integers(0, nv, 60000), rng.integers(0, nv, 60000)
+    both((a2, b2, None, c2, d2), "out-of-layout deletes", (0,))  # redone on the generic key path
+    before = g.pma().slots()
+    a3 = rng.integers(0, nv, 70000)
+    a3[40000] = nv + 3
+    with pytest.raises(ValueError, match=rf"edge \({nv + 3}, \d+\) outside vertex range {nv}"):
+        g.apply_batch(a3, rng.integers(0, nv, 70000), None, [], [])
+    assert all((x == y).all() for x, y in zip(before, g.pma().slots()))
