@@ -579,11 +579,13 @@ def analytics(pg, g, ext, nv):
     roots = pg.draw_below_sequence(ROOT_SEED, nv, 5)
     # steady state of a window loop: one untimed call of each analytic first
     # (pinned result buffers of the caching host allocator, lazy module loads)
+    # (two results alive at once, as in the timed loops below: the caching
+    # host allocator then holds both page-locked blocks before timing starts)
     _w = pg.pagerank(g, max_iters=2)
     _w2 = pg.pagerank(g, warm_start=_w.ranks, max_iters=2)
-    del _w, _w2
-    pg.bfs(g, 0)
-    pg.connected_components(g)
+    _b1, _b2 = pg.bfs(g, 0), pg.bfs(g, 0)
+    _c1, _c2 = pg.connected_components(g), pg.connected_components(g)
+    del _w, _w2, _b1, _b2, _c1, _c2
     bfs_ms, reached = [], []
     for r in roots:
         torch.cuda.synchronize()

@@ -106,33 +106,89 @@ __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64*
     }
 }
 
-__global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, u32 nf,
+// (frontier sizes are read from the device: levels run back to back, the
+// host only syncs once per window of levels)
+// four slots per thread per call (t, t + S, t + 2S, t + 3S; S = the
+// caller's stride, so each of the four rounds of loads is coalesced across the
+// warp): the key/state loads, then the dist probes, then the CASes are each
+// issued four at a time — the probes are random L2 reads, latency is the cost
+__device__ __forceinline__ void bfs_visit4(const u64* __restrict__ ro, const u64* __restrict__ keys,
+                                           const u8* __restrict__ st, u32* __restrict__ dist, u32 depth, u64 t,
+                                           u64 S, u64 e, u32* __restrict__ next, u32* __restrict__ hnext,
+                                           u32* __restrict__ qn) {
+    const unsigned lane = threadIdx.x & 31u;
+    u32 v[4];
+    bool cand[4], won[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const u64 tj = t + j * S;
+        cand[j] = false;
+        v[j] = 0;
+        if (tj < e && st[tj] == kValid) {
+            const u64 k = keys[tj];
+            if (!is_guard(k)) {
+                v[j] = dst_of(k);
+                cand[j] = true;
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cand[j] = cand[j] && dist[v[j]] == GPMA_UNREACHED;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) won[j] = cand[j] && atomicCAS(&dist[v[j]], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const bool heavy = won[j] && (ro[v[j] + 1] - ro[v[j]]) > kHeavyRow;
+        const unsigned lm = __ballot_sync(FULL, won[j] && !heavy), hm = __ballot_sync(FULL, heavy);
+        if (lm) {
+            u32 base = 0;
+            if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
+            base = __shfl_sync(FULL, base, 0);
+            if (won[j] && !heavy) next[base + __popc(lm & lanemask_lt())] = v[j];
+        }
+        if (hm) {
+            u32 base = 0;
+            if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
+            base = __shfl_sync(FULL, base, 0);
+            if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v[j];
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, const u32* nfp,
                                                     const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                     const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
                                                     u32* __restrict__ next, u32* __restrict__ hnext,
                                                     u32* __restrict__ qn) {
+    const u32 nf = *nfp;
     const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
     for (u64 f = warp; f < nf; f += nwarps) {
         const u32 u = frontier[f];
         const u64 b = ro[u], e = ro[u + 1];
-        for (u64 t0 = b; t0 < e; t0 += 32) bfs_visit(ro, keys, st, dist, depth, t0 + lane, e, next, hnext, qn);
+        u64 t0 = b;
+        for (; t0 + 96 < e; t0 += 128) bfs_visit4(ro, keys, st, dist, depth, t0 + lane, 32, e, next, hnext, qn);
+        for (; t0 < e; t0 += 32) bfs_visit(ro, keys, st, dist, depth, t0 + lane, e, next, hnext, qn);
     }
 }
 
-__global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, u32 nh,
+__global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, const u32* nhp,
                                                           const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                           const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
                                                           u32* __restrict__ next, u32* __restrict__ hnext,
                                                           u32* __restrict__ qn) {
+    const u32 nh = *nhp;
     for (u64 task = blockIdx.x; task < u64(nh) * kHeavyParts; task += gridDim.x) {
         const u32 u = hfrontier[task / kHeavyParts];
         const u64 p = task % kHeavyParts;
         const u64 b0 = ro[u], e0 = ro[u + 1], len = e0 - b0;
         const u64 b = b0 + (len * p) / kHeavyParts, e = b0 + (len * (p + 1)) / kHeavyParts;
-        for (u64 t0 = b; t0 < e; t0 += blockDim.x)  // whole warps iterate together (ballots inside)
-            bfs_visit(ro, keys, st, dist, depth, t0 + threadIdx.x, e, next, hnext, qn);
+        // whole warps iterate together (ballots inside)
+        u64 t0 = b;
+        for (; t0 + 3 * blockDim.x < e; t0 += 4 * blockDim.x)
+            bfs_visit4(ro, keys, st, dist, depth, t0 + threadIdx.x, blockDim.x, e, next, hnext, qn);
+        for (; t0 < e; t0 += blockDim.x) bfs_visit(ro, keys, st, dist, depth, t0 + threadIdx.x, e, next, hnext, qn);
     }
 }
 
@@ -440,33 +496,57 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     GPMA_CUDA(cudaStreamSynchronize(s));
     const bool root_heavy = rr[1] - rr[0] > kHeavyRow;
     GPMA_CUDA(cudaMemcpyAsync(root_heavy ? h0.ptr : q0.ptr, &root, 4, cudaMemcpyHostToDevice, s));
-    u32 nf = root_heavy ? 0 : 1, nh = root_heavy ? 1 : 0;
+    // per level L: (light, heavy) vertices discovered, qn[2L], qn[2L + 1];
+    // level 0 = the root.  Levels are launched kBfsWindow at a time with
+    // their frontier sizes read on the device; the host syncs once per
+    // window and stops at the first empty level (later launches of the
+    // window found empty frontiers and did nothing).
+    constexpr u32 kBfsWindow = 4;
+    u64 cap_levels = 0;
+    const u32 first[2] = {root_heavy ? 0u : 1u, root_heavy ? 1u : 0u};
     u64 total = 1;
     u32 depth = 0;
     u32 *cur = q0.ptr, *nxt = q1.ptr, *hcur = h0.ptr, *hnxt = h1.ptr;
     u64 launches = 3;
-    while (nf + nh > 0) {
-        ++depth;
-        GPMA_CUDA(cudaMemsetAsync(qn.ptr, 0, 8, s));
-        if (nf) {
-            k_bfs_expand<<<grid_for(u64(nf) * 32, 256, 148 * 16), 256, 0, s>>>(cur, nf, ro.ptr, pma.d_keys, pma.d_st,
-                                                                               dist.ptr, depth, nxt, hnxt, qn.ptr);
-            GPMA_LAUNCH_CHECK();
-            ++launches;
+    for (bool done = false; !done;) {
+        if (depth + kBfsWindow + 1 > cap_levels) {  // grow the counter ring (keeps earlier levels)
+            const u64 nc = (depth + kBfsWindow + 1) * 2 + 64;
+            DevBuf<u32> q2;
+            q2.reserve(2 * nc);
+            GPMA_CUDA(cudaMemsetAsync(q2.ptr, 0, 2 * nc * 4, s));
+            if (cap_levels) GPMA_CUDA(cudaMemcpyAsync(q2.ptr, qn.ptr, 2 * cap_levels * 4, cudaMemcpyDeviceToDevice, s));
+            else GPMA_CUDA(cudaMemcpyAsync(q2.ptr, first, 8, cudaMemcpyHostToDevice, s));
+            GPMA_CUDA(cudaStreamSynchronize(s));
+            std::swap(qn.ptr, q2.ptr);
+            std::swap(qn.cap, q2.cap);
+            cap_levels = nc;
         }
-        if (nh) {
-            k_bfs_expand_heavy<<<grid_for(u64(nh) * kHeavyParts, 1, 148 * 8), 256, 0, s>>>(
-                hcur, nh, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt, hnxt, qn.ptr);
+        const u32 d0 = depth;
+        for (u32 w = 0; w < kBfsWindow; ++w) {
+            ++depth;
+            const u32* cnt_in = qn.ptr + 2 * (depth - 1);
+            u32* cnt_out = qn.ptr + 2 * depth;
+            k_bfs_expand<<<148 * 16, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt,
+                                                 hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
-            ++launches;
+            k_bfs_expand_heavy<<<148 * 8, 256, 0, s>>>(hcur, cnt_in + 1, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
+                                                       depth, nxt, hnxt, cnt_out);
+            GPMA_LAUNCH_CHECK();
+            launches += 2;
+            std::swap(cur, nxt);
+            std::swap(hcur, hnxt);
         }
-        GPMA_CUDA(cudaMemcpyAsync(h_nf_, qn.ptr, 8, cudaMemcpyDeviceToHost, s));
+        h_lv_.resize(2 * kBfsWindow);
+        GPMA_CUDA(cudaMemcpyAsync(h_lv_.data(), qn.ptr + 2 * (d0 + 1), 2 * kBfsWindow * 4, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
-        nf = h_nf_[0];
-        nh = h_nf_[1];
-        total += u64(nf) + nh;
-        std::swap(cur, nxt);
-        std::swap(hcur, hnxt);
+        for (u32 w = 0; w < kBfsWindow; ++w) {
+            const u64 c = u64(h_lv_[2 * w]) + h_lv_[2 * w + 1];
+            if (c == 0) {
+                done = true;
+                break;
+            }
+            total += c;
+        }
     }
     GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
     if (h_dist) GPMA_CUDA(cudaMemcpyAsync(h_dist, dist.ptr, nv * 4, cudaMemcpyDeviceToHost, s));

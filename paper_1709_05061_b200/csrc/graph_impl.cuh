@@ -65,6 +65,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     void prepare_hot(const u32* outdeg, u64 n);
     DevBuf<u64> rt_offsets, rt_totals;
     u32 h_nf_store_[2] = {0, 0};
+    std::vector<u32> h_lv_;  // per-level frontier counts of one BFS window
     u32* h_nf_ = h_nf_store_;
     cudaEvent_t evs_[4]{};
 };

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--analytics", action="store_true", help="profile BFS + CC + one warm PageRank instead")
+    ap.add_argument("--bfs-root", type=int, default=-1, help="with --analytics: this BFS root (default: the largest hub)")
     args = ap.parse_args()
     import torch
 
@@ -49,7 +50,7 @@ def main():
     if args.analytics:
         import numpy as np
         ro = g.row_offsets()
-        root = int(np.argmax(np.diff(ro.astype(np.int64))))  # a hub root: a non-trivial traversal
+        root = int(np.argmax(np.diff(ro.astype(np.int64)))) if args.bfs_root < 0 else args.bfs_root
         pr = pg.pagerank(g)
         pg.bfs(g, root)
         torch.cuda.synchronize()
