@@ -418,8 +418,10 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
 
 // bucket scatter: update i -> position off[bucket] + ordinal (bucket order,
 // arbitrary order inside a bucket)
-__global__ void k_bucket_scatter(const u64* __restrict__ ck, const u32* __restrict__ lf, const u32* __restrict__ od,
-                                 const u32* __restrict__ off, u64 n, u64* __restrict__ out) {
+// (ci / oci: the arrival payloads when key and index do not fit one word)
+__global__ void k_bucket_scatter(const u64* __restrict__ ck, const u32* __restrict__ ci, const u32* __restrict__ lf,
+                                 const u32* __restrict__ od, const u32* __restrict__ off, u64 n, u64* __restrict__ out,
+                                 u32* __restrict__ oci) {
     // four updates per thread per step: four independent offset lookups in flight
     const u64 nt = u64(gridDim.x) * blockDim.x;
     for (u64 i0 = blockIdx.x * u64(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * nt) {
@@ -439,9 +441,21 @@ __global__ void k_bucket_scatter(const u64* __restrict__ ck, const u32* __restri
         for (int j = 0; j < 4; ++j)
             if (i0 + j * nt < n) p[j] = off[b[j]] + o[j];
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (i0 + j * nt < n) out[p[j]] = w[j];
+        for (int j = 0; j < 4; ++j) {
+            if (i0 + j * nt < n) {
+                out[p[j]] = w[j];
+                if (ci) oci[p[j]] = ci[i0 + j * nt];
+            }
+        }
     }
+}
+
+// (key word, payload) order of the in-bucket sort: the packed word alone, or
+// the key then the arrival payload (index << 1 | is_insert: indices are unique)
+__device__ __forceinline__ bool bucket_before(u64 x, u32 xc, u32 xt, u64 w, u32 wc, u32 wt, bool pairs) {
+    if (x != w) return x < w;
+    if (pairs) return xc < wc;
+    return xt < wt;  // identical packed delete words: by position
 }
 
 // in-bucket sort by the whole packed word (key, then arrival index): a warp
@@ -455,8 +469,10 @@ __global__ void k_bucket_scatter(const u64* __restrict__ ck, const u32* __restri
 // copied as is.  `out` is the front end's word array, so positions of an
 // overflowed bucket (batch redone) keep valid words of this batch.
 constexpr u32 kSmallRun = 16;
-__global__ void k_bucket_sort_small(const u64* __restrict__ in, const u32* __restrict__ off, u64 L,
-                                    u64* __restrict__ out, u32* __restrict__ slf, u32* __restrict__ big, Ctr* ctr) {
+__global__ void k_bucket_sort_small(const u64* __restrict__ in, const u32* __restrict__ inc,
+                                    const u32* __restrict__ off, u64 L, u64* __restrict__ out,
+                                    u32* __restrict__ outc, u32* __restrict__ slf, u32* __restrict__ big, Ctr* ctr) {
+    const bool pairs = inc != nullptr;
     const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
@@ -487,42 +503,47 @@ __global__ void k_bucket_sort_small(const u64* __restrict__ in, const u32* __res
             const u64 b = b0 + k;
             slf[p] = u32(b);
             const u64 w = in[p];
+            const u32 wc = pairs ? inc[p] : 0u;
             if (e - a == 1 || b == L) {
                 out[p] = w;
+                if (pairs) outc[p] = wc;
                 continue;
             }
             if (e - a > kSmallRun) continue;
             u32 r = 0;
-            for (u32 t = a; t < e; ++t) {
-                const u64 x = in[t];
-                r += (x < w) || (x == w && t < p);
-            }
+            for (u32 t = a; t < e; ++t) r += bucket_before(in[t], pairs ? inc[t] : 0u, t, w, wc, p, pairs);
             out[a + r] = w;
+            if (pairs) outc[a + r] = wc;
         }
     }
 }
 
 // the long buckets, one CTA each: staged in shared memory, ranked there
-__global__ void __launch_bounds__(256) k_bucket_sort_big(const u64* __restrict__ in, const u32* __restrict__ off,
-                                                         const u32* __restrict__ big, const ull* nbig,
-                                                         u64* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_bucket_sort_big(const u64* __restrict__ in, const u32* __restrict__ inc,
+                                                         const u32* __restrict__ off, const u32* __restrict__ big,
+                                                         const ull* nbig, u64* __restrict__ out,
+                                                         u32* __restrict__ outc) {
     __shared__ u64 sm[kRunMax];
+    __shared__ u32 smc[kRunMax];
+    const bool pairs = inc != nullptr;
     const u64 nb = *nbig;
     for (u64 k = blockIdx.x; k < nb; k += gridDim.x) {
         const u32 b = big[k];
         const u32 a = off[b], len = off[b + 1] - a;
         if (len > kRunMax) continue;  // flagged: the batch is redone
         __syncthreads();
-        for (u32 q = threadIdx.x; q < len; q += blockDim.x) sm[q] = in[a + q];
+        for (u32 q = threadIdx.x; q < len; q += blockDim.x) {
+            sm[q] = in[a + q];
+            smc[q] = pairs ? inc[a + q] : 0u;
+        }
         __syncthreads();
         for (u32 q = threadIdx.x; q < len; q += blockDim.x) {
             const u64 w = sm[q];
+            const u32 wc = smc[q];
             u32 r = 0;
-            for (u32 t = 0; t < len; ++t) {
-                const u64 x = sm[t];
-                r += (x < w) || (x == w && t < q);
-            }
+            for (u32 t = 0; t < len; ++t) r += bucket_before(sm[t], smc[t], t, w, wc, q, pairs);
             out[a + r] = w;
+            if (pairs) outc[a + r] = wc;
         }
     }
 }
@@ -1729,10 +1750,13 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // one per 8 bits.  Skipped after a batch whose buckets overflowed.
         BucketArgs ba{};
         const u64 L = num_leaves();
-        // (its passes over the L leaf counters must stay small next to the
-        // radix passes over the n updates: measured break-even near L = 4n)
-        bucket = ib && ro_base() && n >= kBucketMinBatch && n < (1ull << 31) && L + 2 < (1ull << 31) &&
-                 L <= 4 * n && bucket_skip_ == 0;
+        // Taken while the leaf headers stay L2-resident (the unsorted leaf
+        // searches then hit L2; past that they are HBM-latency bound) and the
+        // passes over the L leaf counters stay small next to the radix passes
+        // over the n updates (measured: C2 and C3 gain, C4's 33.5M and C5's
+        // 16.7M leaves lose).
+        bucket = ro_base() && n >= kBucketMinBatch && n < (1ull << 31) && L <= kBucketMaxLeaves &&
+                 L <= 8 * n && bucket_skip_ == 0;
         if (bucket_skip_) --bucket_skip_;
         if (bucket) {
             bcnt.reserve(L + 2);
@@ -1791,15 +1815,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         cub::DeviceScan::ExclusiveSum(nullptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_);
         sort_tmp.reserve(tmp);
         GPMA_CUDA(cub::DeviceScan::ExclusiveSum(sort_tmp.ptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_));
-        k_bucket_scatter<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(sk_in.ptr, blf.ptr, bod.ptr, boff.ptr, n,
-                                                                         sk_out.ptr);
+        const bool pairs = packed_ib == 0;
+        k_bucket_scatter<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
+            sk_in.ptr, pairs ? si_in.ptr : nullptr, blf.ptr, bod.ptr, boff.ptr, n, sk_out.ptr, si_out.ptr);
         GPMA_LAUNCH_CHECK();
         bbig.reserve(n / (kSmallRun + 1) + 1);
         k_bucket_sort_small<<<grid_for((L + 1 + 31) / 32 * 32, 256, 148 * 16), 256, 0, stream_>>>(
-            sk_out.ptr, boff.ptr, L, sk_in.ptr, bslf.ptr, bbig.ptr, d_ctr);
+            sk_out.ptr, pairs ? si_out.ptr : nullptr, boff.ptr, L, sk_in.ptr, si_in.ptr, bslf.ptr, bbig.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
-        k_bucket_sort_big<<<148 * 2, 256, 0, stream_>>>(sk_out.ptr, boff.ptr, bbig.ptr, &d_ctr->nbig_buckets,
-                                                         sk_in.ptr);
+        k_bucket_sort_big<<<148 * 2, 256, 0, stream_>>>(sk_out.ptr, pairs ? si_out.ptr : nullptr, boff.ptr, bbig.ptr,
+                                                         &d_ctr->nbig_buckets, sk_in.ptr, si_in.ptr);
         GPMA_LAUNCH_CHECK();
         launches += 5;
     } else if (packed_ib && n > 1) {

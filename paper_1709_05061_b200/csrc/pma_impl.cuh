@@ -237,6 +237,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u32> bcnt, boff, blf, bod, bslf, bbig;
     int bucket_skip_ = 0;  // batches left on the radix sort after a bucket overflow
     static constexpr u64 kBucketMinBatch = 1u << 16;
+    static constexpr u64 kBucketMaxLeaves = 8ull << 20;  // 64 MB of leaf headers
     static constexpr int kBucketCooldown = 16;
     DevBuf<u64> uk, uv;
     DevBuf<u8> uop;

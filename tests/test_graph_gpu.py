@@ -353,3 +353,24 @@ def test_leaf_bucket_edge_cases(mode):
     with pytest.raises(ValueError, match=rf"edge \({nv + 3}, \d+\) outside vertex range {nv}"):
         g.apply_batch(a3, rng.integers(0, nv, 70000), None, [], [])
     assert all((x == y).all() for x, y in zip(before, g.pma().slots()))
+
+
+def test_leaf_bucket_pairs_front_end():
+    """When key and arrival index do not fit one 64-bit word (|V| = 2^22,
+    batch > 2^19) the leaf-bucket front end sorts (key, payload) pairs:
+    still bit-exact with the reference."""
+    rng = np.random.default_rng(31)
+    nv = 2**22
+    s, d = rng.integers(0, nv, 600000), rng.integers(0, nv, 600000)
+    g = DynamicGraph.from_edges(nv, s, d)
+    r = RefGraph(nv, s, d)
+    a, b = rng.integers(0, nv, 400000), rng.integers(0, nv, 400000)
+    a[:200], b[:200] = 5, 6  # a duplicated key
+    c = np.concatenate([s[:250000], np.full(100, 5)]).astype(np.uint32)
+    dd = np.concatenate([d[:250000], np.full(100, 6)]).astype(np.uint32)
+    gs = g.apply_batch(a, b, None, c, dd)
+    assert int(g.last_timing().front_end) in (1, 2)
+    rs = r.apply_batch(a, b, None, c, dd)
+    assert gs.parity() == ref_parity(r, rs)
+    assert_same_slots(g.pma().slots(), r.slots(), "pairs")
+    assert (g.row_offsets() == r.row_offsets()).all()
