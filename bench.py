@@ -83,6 +83,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-analytics", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no sweep/baseline/analytics)")
+    ap.add_argument("--routing", default="fused", choices=["fused", "all_to_all"],
+                    help="sharded update routing: the partition kernel stores into the owners' receive buffers "
+                         "over peer memory (fused), or an NCCL all-to-all after it")
     ap.add_argument("--sharded", action="store_true",
                     help="run the key-range sharded (multi-GPU) path even at N = 1 (NCCL with one rank)")
     return ap.parse_args()
@@ -415,7 +418,8 @@ def run_sharded(args, rank, world, local):
     bounds = sh.vertex_bounds(nv, world, deg)
     comm = TorchComm()
     t1 = time.time()
-    G = ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev])
+    G = ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev],
+                                       routing=args.routing)
     load_s = time.time() - t1
     slides = [win.slide(B * world) for _ in range(W + K)]
     info = win.info()
@@ -467,7 +471,8 @@ def run_sharded(args, rank, world, local):
     value = total_updates / (ms_max / 1e3)
 
     # ---- e2e: the same slides from pinned host buffers (H2D of each rank's share inside the region)
-    G2 = ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev])
+    G2 = ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev],
+                                        routing=args.routing)
     host = []
     for sl in slides:
         a, b, _, c, d = my_slice(sl)
@@ -506,7 +511,9 @@ def run_sharded(args, rank, world, local):
                                   f"of {world} x {B} arrivals, each rank ingests 1/{world} of it, routes by NCCL "
                                   f"all-to-all and applies its shard's share",
                       "batch_per_gpu": B, "num_vertices": nv, "stream_edges": ne,
-                      "parallelism": f"key-range shards x{world} (one GPMA+ per GPU, NCCL all-to-all routing)",
+                      "parallelism": f"key-range shards x{world} (one GPMA+ per GPU, "
+                                     + ("fused partition+transfer routing over peer memory)" if args.routing == "fused"
+                                        else "NCCL all-to-all routing)"),
                       "vertex_bounds": [int(x) for x in bounds],
                       "l2": "inputs larger than L2 (each shard's slot array > 126 MB)", "deletion_mode": "lazy"},
            "e2e": e2e, "gpu_launches": launches,

@@ -360,6 +360,30 @@ int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local);
  * loading never lands inside a timed region (call once per process/device). */
 int gpma_warmup(int device);
 
+/* ---- Fused routing (partition + transfer in one kernel over peer memory)
+ * Instead of gpma_route_batch + an all-to-all: (1) gpma_route_count counts
+ * this rank's slice per owner (d_counts[world], stream-ordered); (2) the
+ * caller exchanges the counts (world x world) and derives, for every owner r,
+ * this sender's first slot in r's receive buffer (the sum of the counts of
+ * the lower senders for r) and the size of its own receive batch; (3)
+ * gpma_route_scatter_peer writes the slice straight into the owners' receive
+ * buffers (device pointers: same device, peer-enabled devices, or IPC
+ * mappings from gpma_ipc_open); (4) after every sender finished, each owner
+ * calls gpma_apply_batch_routed_device on its buffer.  The receive order is
+ * the all-to-all's (sender-rank order, arrival order within a sender). */
+int gpma_route_count(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, size_t n_ins,
+                     const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del, const uint32_t* d_bounds,
+                     int world, uint64_t* d_counts);
+int gpma_route_scatter_peer(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
+                            const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
+                            const uint32_t* d_del_dst, size_t n_del, const uint32_t* d_bounds, int world,
+                            uint64_t* const* d_dst_keys, double* const* d_dst_w, const uint64_t* d_dst_offsets);
+/* cudaMalloc + cudaIpcGetMemHandle (64-byte handle out) / open / close / free */
+int gpma_ipc_alloc(int device, size_t bytes, void** d_ptr, void* handle64);
+int gpma_ipc_open(int device, const void* handle64, void** d_ptr);
+int gpma_ipc_close(void* d_ptr);
+int gpma_ipc_free(void* d_ptr);
+
 /* Link diagnostic: best-of-`reps` rate of moving `bytes` of page-locked host
  * memory to the device by cudaMemcpyAsync (copy engines) and by SM loads in
  * place (zero-copy, as gpma_apply_batch reads pinned batches).  GB/s. */

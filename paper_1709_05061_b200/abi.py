@@ -211,6 +211,12 @@ SIGNATURES = [
     ("gpma_apply_batch_routed_device", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
     ("gpma_route_batch_async", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, _P, C.c_int, _P, _P, _P]),
     ("gpma_set_stream", C.c_int, [_P, _P, C.c_int]),
+    ("gpma_route_count", C.c_int, [_P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, _P, C.c_int, _P]),
+    ("gpma_route_scatter_peer", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, _P, C.c_int, _P, _P, _P]),
+    ("gpma_ipc_alloc", C.c_int, [C.c_int, C.c_size_t, C.POINTER(_P), _P]),
+    ("gpma_ipc_open", C.c_int, [C.c_int, _P, C.POINTER(_P)]),
+    ("gpma_ipc_close", C.c_int, [_P]),
+    ("gpma_ipc_free", C.c_int, [_P]),
     ("gpma_shard_bfs_mark", C.c_int, [_P, _P, C.c_uint32, _P]),
     ("gpma_shard_bfs_update", C.c_int, [_P, _P, _P, C.c_uint32, _P, C.POINTER(C.c_uint32)]),
     ("gpma_shard_cc_hook", C.c_int, [_P, _P]),

@@ -436,6 +436,51 @@ int gpma_route_batch_async(gpma_graph* g, const uint32_t* d_ins_src, const uint3
     });
 }
 
+int gpma_route_count(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, size_t n_ins,
+                     const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del, const uint32_t* d_bounds,
+                     int world, uint64_t* d_counts) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->route_partition(d_ins_src, d_ins_dst, nullptr, n_ins, d_del_src, d_del_dst, n_del, d_bounds, world,
+                                 nullptr, nullptr, nullptr, d_counts);
+    });
+}
+
+int gpma_route_scatter_peer(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
+                            const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
+                            const uint32_t* d_del_dst, size_t n_del, const uint32_t* d_bounds, int world,
+                            uint64_t* const* d_dst_keys, double* const* d_dst_w, const uint64_t* d_dst_offsets) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->route_scatter_peer(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, d_bounds,
+                                    world, d_dst_keys, d_dst_w, d_dst_offsets);
+    });
+}
+
+// ---- IPC receive buffers for fused routing across processes
+int gpma_ipc_alloc(int device, size_t bytes, void** d_ptr, void* handle64) {
+    return guarded(nullptr, [&] {
+        GPMA_CUDA(cudaSetDevice(device));
+        GPMA_CUDA(cudaMalloc(d_ptr, bytes ? bytes : 8));
+        cudaIpcMemHandle_t h;
+        GPMA_CUDA(cudaIpcGetMemHandle(&h, *d_ptr));
+        std::memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+int gpma_ipc_open(int device, const void* handle64, void** d_ptr) {
+    return guarded(nullptr, [&] {
+        GPMA_CUDA(cudaSetDevice(device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        GPMA_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int gpma_ipc_close(void* d_ptr) { return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? PMA_OK : PMA_ECUDA; }
+
+int gpma_ipc_free(void* d_ptr) { return cudaFree(d_ptr) == cudaSuccess ? PMA_OK : PMA_ECUDA; }
+
 int gpma_set_stream(gpma_graph* g, void* stream, int own) {
     if (!g || !g->impl) return PMA_EINVAL;
     g->impl->pma.set_stream(static_cast<cudaStream_t>(stream), own != 0);

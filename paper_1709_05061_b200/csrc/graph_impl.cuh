@@ -35,6 +35,10 @@ public:
     void route_partition(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
                          u64 nd, const u32* d_bounds, int world, u64* okeys, double* ow, u64* h_counts,
                          u64* d_counts = nullptr);
+    void route_scatter_peer(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
+                            u64 nd, const u32* d_bounds, int world, u64* const* dst_keys, double* const* dst_w,
+                            const u64* dst_off);
+    u64 rt_ntiles = 0;
     // apply_batch with routed EdgeKeys, bit 63 = delete (arrival order kept among inserts)
     void apply_batch_mixed_device(const u64* keys, const double* w, u64 n, pma_stats* out);
     void apply_batch_impl(const u32* is, const u32* id, const u64* mk, const double* iw, u64 ni, const u32* ds,

@@ -102,8 +102,23 @@ __global__ void k_route_scan(const u32* __restrict__ tile_counts, u64 ntiles, in
     }
 }
 
+// Destinations: okeys/ow (owner-major, for an all-to-all), or — fused
+// routing — straight into every owner's receive buffer (peer memory over
+// NVLink / IPC): owner r's element lands at dst_keys[r][dst_off[r] + its rank
+// among this sender's elements for r], i.e. the position an all-to-all in
+// sender-rank order would give it.
+struct RouteDst {
+    u64* okeys;
+    double* ow;
+    u64* const* dst_keys;   // [world] receive buffers (device pointers), or null
+    double* const* dst_w;   // [world] or null
+    const u64* dst_off;     // [world] this sender's first slot in each receive buffer
+};
+
 __global__ void k_route_scatter(RouteIn in, const u32* __restrict__ bounds, int world,
-                                const u64* __restrict__ tile_offsets, u64* __restrict__ okeys, double* __restrict__ ow) {
+                                const u64* __restrict__ tile_offsets, RouteDst dst) {
+    u64* __restrict__ okeys = dst.okeys;
+    double* __restrict__ ow = dst.ow;
     const u64 n = in.ni + in.nd;
     constexpr int kWarps = kRouteThreads / 32;
     __shared__ u32 s_b[kMaxWorld + 1];
@@ -141,8 +156,16 @@ __global__ void k_route_scatter(RouteIn in, const u32* __restrict__ bounds, int 
         const u64 i = base + u64(j) * kRouteThreads + threadIdx.x;
         const u64 o = tile_offsets[u64(own[j]) * gridDim.x + blockIdx.x] + s_wc[(j * kWarps + warp) * world + own[j]] +
                       rank[j];
-        okeys[o] = in.key(i);  // EdgeKey (graph.hpp:27-37) + delete bit: one 8-B word on the wire
-        if (ow) ow[o] = (i < in.ni && in.iw) ? in.iw[i] : 1.0;
+        const u64 key = in.key(i);  // EdgeKey (graph.hpp:27-37) + delete bit: one 8-B word on the wire
+        const double wt = (i < in.ni && in.iw) ? in.iw[i] : 1.0;
+        if (dst.dst_keys) {
+            const u64 q = dst.dst_off[own[j]] + (o - tile_offsets[u64(own[j]) * gridDim.x]);
+            dst.dst_keys[own[j]][q] = key;
+            if (dst.dst_w) dst.dst_w[own[j]][q] = wt;
+        } else {
+            okeys[o] = key;
+            if (ow) ow[o] = wt;
+        }
     }
 }
 
@@ -271,12 +294,32 @@ void Graph::route_partition(const u32* is, const u32* id, const double* iw, u64 
     u64* totals = d_counts ? d_counts : rt_totals.ptr;
     k_route_scan<<<1, 1024, 0, s>>>(rt_counts.ptr, ntiles, world, rt_offsets.ptr, totals);
     GPMA_LAUNCH_CHECK();
-    k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_offsets.ptr, okeys, ow);
-    GPMA_LAUNCH_CHECK();
+    if (okeys) {
+        k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_offsets.ptr,
+                                                                   RouteDst{okeys, ow, nullptr, nullptr, nullptr});
+        GPMA_LAUNCH_CHECK();
+    }
+    rt_ntiles = ntiles;
     if (h_counts) {  // host counts: one round trip; device counts: stream-ordered, no sync
         GPMA_CUDA(cudaMemcpyAsync(h_counts, totals, world * sizeof(u64), cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
     }
+}
+
+// Fused routing, second half: after route_partition(..., okeys = nullptr)
+// counted the same slice, scatter it straight into the owners' receive
+// buffers (stream-ordered; the caller makes the owners wait for every sender).
+void Graph::route_scatter_peer(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
+                               u64 nd, const u32* d_bounds, int world, u64* const* dst_keys, double* const* dst_w,
+                               const u64* dst_off) {
+    const u64 n = ni + nd;
+    if (n == 0) return;
+    const u64 ntiles = (n + kRouteTile - 1) / kRouteTile;
+    if (ntiles != rt_ntiles) throw ApiError(PMA_ELOGIC, "route_scatter_peer: slice differs from the counted one");
+    const RouteIn in{is, id, iw, ni, ds, dd, nd};
+    k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, pma.stream()>>>(
+        in, d_bounds, world, rt_offsets.ptr, RouteDst{nullptr, nullptr, dst_keys, dst_w, dst_off});
+    GPMA_LAUNCH_CHECK();
 }
 
 void Graph::shard_bfs_mark(const u32* frontier, u32 nf, u8* flags) {

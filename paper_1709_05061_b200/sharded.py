@@ -164,7 +164,11 @@ class ShardStats:
 class ShardedGraph:
     """Key-range sharded DynamicGraph; `shards[i]` is local rank comm.ranks[i]."""
 
-    def __init__(self, comm, num_vertices: int, bounds, handles, devices):
+    def __init__(self, comm, num_vertices: int, bounds, handles, devices, routing: str = "all_to_all"):
+        if routing not in ("all_to_all", "fused"):
+            raise ValueError("routing: 'all_to_all' or 'fused'")
+        self.routing = routing
+        self._rx = None  # fused routing: receive buffers (see _ensure_rx)
         self.comm = comm
         self.nv = int(num_vertices)
         self.bounds = np.asarray(bounds, np.int64)
@@ -182,7 +186,7 @@ class ShardedGraph:
     # ---- construction
     @classmethod
     def from_edges_device(cls, comm, num_vertices: int, bounds, edges, config: GraphConfig | None = None,
-                          devices=None):
+                          devices=None, routing: str = "all_to_all"):
         """edges[i] = (src, dst, weights|None) device tensors given to local
         rank i — typically the same global edge list: each shard keeps the
         edges of its own sources (gpma_shard_from_edges_device)."""
@@ -200,9 +204,10 @@ class ShardedGraph:
             if rc:
                 _raise(rc, lib.gpma_last_error(None).decode())
             hs.append(h)
-        return cls(comm, num_vertices, bounds, hs, devices)
+        return cls(comm, num_vertices, bounds, hs, devices, routing)
 
     def __del__(self):
+        self._free_rx()
         for h in getattr(self, "h", []) or []:
             if h:
                 self._lib.gpma_destroy(h)
@@ -240,13 +245,150 @@ class ShardedGraph:
             torch.cuda.ExternalStream(self._lib.gpma_cuda_stream(self.h[i]), device=a.device).synchronize()
         return keys[:n], (ow[:n] if ow is not None else None), counts
 
+    # ---- fused routing: partition + transfer in one kernel (peer memory)
+    def _free_rx(self):
+        rx = getattr(self, "_rx", None)
+        if not rx:
+            return
+        for p in rx.get("opened", []):
+            self._lib.gpma_ipc_close(C.c_void_p(p))
+        for p in rx.get("owned", []):
+            self._lib.gpma_ipc_free(C.c_void_p(p))
+        self._rx = None
+
+    def _ensure_rx(self, need: int, weighted: bool):
+        """Receive buffers of `need` EdgeKeys (+ weights) on every rank; every
+        rank derives `need` from the same count matrix, so re-allocations are
+        collective.  In one process the buffers are plain device tensors; across
+        processes each rank exports its buffers as CUDA IPC handles and maps
+        its peers' (cudaIpcOpenMemHandle)."""
+        torch = _torch()
+        rx = self._rx
+        if rx and rx["cap"] >= need and rx["weighted"] == weighted:
+            return rx
+        self._free_rx()
+        cap = max(1024, int(need * 1.25))
+        W, L = self.comm.world, len(self.h)
+        rx = {"cap": cap, "weighted": weighted, "owned": [], "opened": []}
+        if isinstance(self.comm, LocalComm):
+            keys = [torch.empty(cap, dtype=torch.int64, device=f"cuda:{d}") for d in self.devices]
+            ws = [torch.empty(cap, dtype=torch.float64, device=f"cuda:{d}") for d in self.devices] if weighted else None
+            kptr = [t.data_ptr() for t in keys]
+            wptr = [t.data_ptr() for t in ws] if weighted else None
+            rx.update(keys=keys, ws=ws, kptr_all=[kptr] * L, wptr_all=[wptr] * L,
+                      mine_k=kptr, mine_w=wptr if weighted else [0] * L)
+        else:
+            (dev,), me = self.devices, self.comm.ranks[0]
+            mine = []
+            for nbytes in ([cap * 8, cap * 8] if weighted else [cap * 8]):
+                ptr, hnd = C.c_void_p(), (C.c_char * 64)()
+                self._check(0, self._lib.gpma_ipc_alloc(dev, nbytes, C.byref(ptr), hnd))
+                rx["owned"].append(ptr.value)
+                mine.append((ptr.value, bytes(hnd)))
+            allh = [None] * W
+            self.comm.dist.all_gather_object(allh, [h for _, h in mine], group=self.comm.group)
+            ptrs = []
+            for r in range(W):
+                row = []
+                for j, hb in enumerate(allh[r]):
+                    if r == me:
+                        row.append(mine[j][0])
+                    else:
+                        q = C.c_void_p()
+                        self._check(0, self._lib.gpma_ipc_open(dev, (C.c_char * 64).from_buffer_copy(hb), C.byref(q)))
+                        rx["opened"].append(q.value)
+                        row.append(q.value)
+                ptrs.append(row)
+            kptr = [row[0] for row in ptrs]
+            wptr = [row[1] for row in ptrs] if weighted else None
+            rx.update(kptr_all=[kptr], wptr_all=[wptr], mine_k=[mine[0][0]],
+                      mine_w=[mine[1][0]] if weighted else [0])
+        # per local sender: device arrays of the W destination pointers
+        rx["kdev"] = [torch.tensor(kp, dtype=torch.int64, device=f"cuda:{d}")
+                      for kp, d in zip(rx["kptr_all"], self.devices)]
+        rx["wdev"] = [torch.tensor(wp, dtype=torch.int64, device=f"cuda:{d}") if wp else None
+                      for wp, d in zip(rx["wptr_all"], self.devices)]
+        self._rx = rx
+        return rx
+
+    def _apply_fused(self, slices) -> ShardStats:
+        torch = _torch()
+        L, W = len(self.h), self.comm.world
+        weighted = slices[0][2] is not None
+        counts = []
+        for i in range(L):
+            a, b, w, c, d = slices[i]
+            cnt = torch.empty(W, dtype=torch.int64, device=a.device)
+            if not self._ordered:
+                _sync(a)
+            self._check(i, self._lib.gpma_route_count(self.h[i], _vp(a), _vp(b), a.numel(), _vp(c), _vp(d),
+                                                       c.numel() if c is not None else 0, _vp(self._dbounds[i]), W,
+                                                       _vp(cnt)))
+            counts.append(cnt)
+        if not self._ordered:
+            for i in range(L):
+                torch.cuda.ExternalStream(self._lib.gpma_cuda_stream(self.h[i]),
+                                          device=counts[i].device).synchronize()
+        # the count matrix M[sender][owner] on every rank
+        if isinstance(self.comm, LocalComm):
+            M = np.stack([c.cpu().numpy() for c in counts])
+        else:
+            (cnt,) = counts
+            if self.comm.dist.get_backend(self.comm.group) == "gloo":
+                cnt = cnt.cpu()  # gloo: host tensors
+            parts = [torch.empty_like(cnt) for _ in range(W)]
+            self.comm.dist.all_gather(parts, cnt, group=self.comm.group)
+            M = torch.stack(parts).cpu().numpy()
+        before = np.cumsum(M, axis=0) - M  # before[s][r]: slots of lower senders at owner r
+        nrecv = M.sum(axis=0)
+        rx = self._ensure_rx(int(nrecv.max()) if W else 0, weighted)
+        for i in range(L):
+            a, b, w, c, d = slices[i]
+            me = self.comm.ranks[i]
+            off = torch.as_tensor(before[me].astype(np.int64), device=a.device)
+            self._check(i, self._lib.gpma_route_scatter_peer(self.h[i], _vp(a), _vp(b), _vp(w), a.numel(), _vp(c),
+                                                              _vp(d), c.numel() if c is not None else 0,
+                                                              _vp(self._dbounds[i]), W, _vp(rx["kdev"][i]),
+                                                              _vp(rx["wdev"][i]), _vp(off)))
+        # every sender's stores land before any owner reads its buffer: with
+        # NCCL a one-element all-reduce on the stream is that barrier (it runs
+        # on every rank after the rank's scatter kernel); otherwise host syncs
+        nccl = (not isinstance(self.comm, LocalComm) and self._ordered
+                and self.comm.dist.get_backend(self.comm.group) == "nccl")
+        if nccl:
+            self.comm.dist.all_reduce(torch.zeros(1, device=f"cuda:{self.devices[0]}"), group=self.comm.group)
+        else:
+            for i in range(L):
+                if self._ordered:
+                    torch.cuda.current_stream(self.devices[i]).synchronize()
+                else:
+                    torch.cuda.ExternalStream(self._lib.gpma_cuda_stream(self.h[i]),
+                                              device=torch.device("cuda", self.devices[i])).synchronize()
+            if not isinstance(self.comm, LocalComm):
+                self.comm.dist.barrier(group=self.comm.group)
+        out, routed, sent = [], [], []
+        for i in range(L):
+            me = self.comm.ranks[i]
+            st = pma_stats()
+            n = int(nrecv[me])
+            self._check(i, self._lib.gpma_apply_batch_routed_device(
+                self.h[i], C.c_void_p(rx["mine_k"][i]), C.c_void_p(rx["mine_w"][i]) if weighted else None, n,
+                C.byref(st)))
+            out.append(UpdateStats.from_c(st))
+            routed.append(n)
+            sent.append(int(M[me].sum() - M[me][me]))
+        return ShardStats(out, routed, sent)
+
     def apply_batch(self, slices) -> ShardStats:
         """slices[i] = (ins_src, ins_dst, ins_w|None, del_src, del_dst):
         local rank i's share of the global batch (device tensors, u32 ids as
         int32; weights given on every rank or on none).  One owner partition
         (gpma_route_batch) and one all-to-all of 8-B EdgeKeys per batch, then
         each shard applies its routed batch (DynamicGraph::apply_batch,
-        graph.hpp:130-162)."""
+        graph.hpp:130-162).  routing="fused": the owner partition writes
+        straight into the owners' receive buffers instead (_apply_fused)."""
+        if self.routing == "fused":
+            return self._apply_fused(slices)
         L = len(self.h)
         ks, ws, cs = [], [], []
         for i in range(L):

@@ -39,9 +39,14 @@ def _ref_row_offsets(slots, lo, hi):
     return ro
 
 
-@pytest.mark.parametrize("world,mode,kind,weighted", [(2, PMA_LAZY, "rmat", False), (3, PMA_EAGER, "rmat", True),
-                                                      (4, PMA_LAZY, "er", True)])
-def test_sharded_window_parity(world, mode, kind, weighted):
+@pytest.mark.parametrize("world,mode,kind,weighted,routing", [(2, PMA_LAZY, "rmat", False, "all_to_all"),
+                                                              (3, PMA_EAGER, "rmat", True, "all_to_all"),
+                                                              (4, PMA_LAZY, "er", True, "all_to_all"),
+                                                              (2, PMA_EAGER, "rmat", True, "fused"),
+                                                              (4, PMA_LAZY, "rmat", False, "fused")])
+def test_sharded_window_parity(world, mode, kind, weighted, routing):
+    """routing="fused": the owner partition writes straight into the owners'
+    receive buffers (gpma_route_scatter_peer) instead of an all-to-all."""
     rng = np.random.default_rng(11)
     nv = 2**12
     stream = RefStream.rmat(nv, 40000, 5) if kind == "rmat" else RefStream.erdos_renyi(nv, 2**-8, 5)
@@ -54,7 +59,8 @@ def test_sharded_window_parity(world, mode, kind, weighted):
     bounds = sh.vertex_bounds(nv, world, deg)
     comm = LocalComm(world)
     edges = (_dev(s[:half], "u32"), _dev(d[:half], "u32"), _dev(w0, "f64") if weighted else None)
-    G = ShardedGraph.from_edges_device(comm, nv, bounds, [edges] * world, GraphConfig(deletion_mode=mode))
+    G = ShardedGraph.from_edges_device(comm, nv, bounds, [edges] * world, GraphConfig(deletion_mode=mode),
+                                       routing=routing)
     refs = []
     for r in range(world):
         lo, hi = int(bounds[r]), int(bounds[r + 1])
