@@ -358,8 +358,20 @@ __device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib
         const u64 nq = (n - head) / 4;
         const uint4* s4 = reinterpret_cast<const uint4*>(sa + head);
         const uint4* d4 = reinterpret_cast<const uint4*>(da + head);
+        // the next quad's loads are issued before this quad's leaf searches:
+        // read in place over PCIe (pinned host batches) the link stays busy
+        // while the searches run
+        uint4 na = make_uint4(0, 0, 0, 0), nb = na;
+        if (tid < nq) {
+            na = s4[tid];
+            nb = d4[tid];
+        }
         for (u64 q = tid; q < nq; q += nt) {
-            const uint4 a = s4[q], b = d4[q];
+            const uint4 a = na, b = nb;
+            if (q + nt < nq) {
+                na = s4[q + nt];
+                nb = d4[q + nt];
+            }
             const u64 i = base + head + 4 * q;
             const u32 ss[4] = {a.x, a.y, a.z, a.w}, dd[4] = {b.x, b.y, b.z, b.w};
             const u64 ii[4] = {i, i + 1, i + 2, i + 3};
