@@ -40,7 +40,7 @@ __device__ __forceinline__ void st_volatile(ull* p, ull v) { *reinterpret_cast<v
 // (j < kScanItems, i < n) at once: bit j of fm = flag, x[j] = exclusive prefix.
 // Lets a caller interleave independent per-item work (e.g. 8 binary searches).
 template <class Flag, class EmitTile, class Fin>
-__global__ void __launch_bounds__(kScanThreads) compact_kernel(const ull* n_dev, ull n_host, Flag flag,
+__global__ void __launch_bounds__(kScanThreads, 7) compact_kernel(const ull* n_dev, ull n_host, Flag flag,
                                                                EmitTile emit_tile, Fin fin, ull* tiles, ull epoch) {
     __shared__ unsigned s_off[kScanItems * kScanWarps];  // (item row, warp) counts -> exclusive offsets
     __shared__ ull s_prefix, s_total;
