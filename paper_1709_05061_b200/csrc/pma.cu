@@ -2051,7 +2051,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             if (m <= 32) {
                 // warp tiers; hub groups (large slices) are appended to biglist
                 if (m == 16 && leaf_ == 16 && pcur == nullptr) {  // level 0: identity pending list
-                    const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, 148 * 16);
+                    // exactly the resident CTAs (persistent: the grid-stride tile
+                    // loop balances; a partial last wave costs ~10%, measured)
+                    static const unsigned resident = [] {
+                        int per_sm = 0, dev = 0, sms = 0;
+                        cudaGetDevice(&dev);
+                        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_commit_leaf, kLeafWarps * 32, 0);
+                        return unsigned((per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148));
+                    }();
+                    const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, resident);
                     k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
                 } else {
                     // grid for the host bound; the kernel sizes its tiles from the
