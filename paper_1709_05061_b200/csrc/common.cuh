@@ -50,6 +50,18 @@ inline unsigned grid_for(u64 n, unsigned block, unsigned cap = 148u * 16u) {
     return static_cast<unsigned>(g);
 }
 
+// CTAs of `kernel` (block threads, dynamic smem) resident on the whole GPU at
+// once: the grid of a persistent grid-stride kernel — a partial last wave
+// leaves SMs idle while the slowest CTAs finish.
+template <class K>
+inline unsigned resident_grid(K kernel, int block, size_t smem = 0) {
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
+    return unsigned((per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148));
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;

@@ -592,7 +592,8 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
     }
     GPMA_CUDA(cudaMemsetAsync(outdeg.ptr, 0, nv * 4, s));
     const u64 cap = pma.capacity();
-    k_outdeg<<<grid_for(cap / 8, 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg.ptr);
+    static const unsigned od_res = resident_grid(k_outdeg, 256);
+    k_outdeg<<<grid_for(cap / 8, 256, od_res), 256, 0, s>>>(pma.d_keys, pma.d_st, cap, outdeg.ptr);
     GPMA_LAUNCH_CHECK();
     prepare_hot(outdeg.ptr, nv);
     u64 launches = 3;
@@ -615,7 +616,8 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
         double* nxt = psc.ptr + 2 * (1 - p);
         GPMA_CUDA(cudaMemsetAsync(nxt, 0, 16, s));
         GPMA_CUDA(cudaEventRecord(pma_ev(2), s));
-        k_pr_push<<<148 * 8, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr, nhot_);
+        static const unsigned pr_res = resident_grid(k_pr_push, 256);
+        k_pr_push<<<pr_res, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr, nhot_);
         k_pr_finish_next<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, y, outdeg.ptr, nv, d, cur, nxt, nxt + 1,
                                                                    pshare.ptr);
         GPMA_LAUNCH_CHECK();

@@ -1828,11 +1828,13 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         sort_tmp.reserve(tmp);
         GPMA_CUDA(cub::DeviceScan::ExclusiveSum(sort_tmp.ptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_));
         const bool pairs = packed_ib == 0;
-        k_bucket_scatter<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
+        static const unsigned scat_res = resident_grid(k_bucket_scatter, 256);
+        static const unsigned sort_res = resident_grid(k_bucket_sort_small, 256);
+        k_bucket_scatter<<<grid_for(n, 256, scat_res), 256, 0, stream_>>>(
             sk_in.ptr, pairs ? si_in.ptr : nullptr, blf.ptr, bod.ptr, boff.ptr, n, sk_out.ptr, si_out.ptr);
         GPMA_LAUNCH_CHECK();
         bbig.reserve(n / (kSmallRun + 1) + 1);
-        k_bucket_sort_small<<<grid_for((L + 1 + 31) / 32 * 32, 256, 148 * 16), 256, 0, stream_>>>(
+        k_bucket_sort_small<<<grid_for((L + 1 + 31) / 32 * 32, 256, sort_res), 256, 0, stream_>>>(
             sk_out.ptr, pairs ? si_out.ptr : nullptr, boff.ptr, L, sk_in.ptr, si_in.ptr, bslf.ptr, bbig.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
         k_bucket_sort_big<<<148 * 2, 256, 0, stream_>>>(sk_out.ptr, pairs ? si_out.ptr : nullptr, boff.ptr, bbig.ptr,
