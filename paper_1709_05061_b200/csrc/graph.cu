@@ -75,6 +75,11 @@ __global__ void k_iota_u32(u32* a, u64 n) {
 // atomic per warp and queue) into the light or heavy next queue by their own
 // row length.
 constexpr u64 kHeavyRow = 1024;
+// fixed grids (levels run back to back with device-side frontier sizes);
+// measured on the C2 hub BFS: light 148x32 / heavy 148x64 CTAs beat 148x16 /
+// 148x8 by 20% (more heavy-row parts in flight), and more parts per heavy row
+// (64, 128) lose
+constexpr unsigned kBfsLightGrid = 148 * 32, kBfsHeavyGrid = 148 * 64;
 constexpr u32 kHeavyParts = 32;
 
 __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64* __restrict__ keys,
@@ -526,10 +531,10 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
             ++depth;
             const u32* cnt_in = qn.ptr + 2 * (depth - 1);
             u32* cnt_out = qn.ptr + 2 * depth;
-            k_bfs_expand<<<148 * 16, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt,
+            k_bfs_expand<<<kBfsLightGrid, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt,
                                                  hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
-            k_bfs_expand_heavy<<<148 * 8, 256, 0, s>>>(hcur, cnt_in + 1, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
+            k_bfs_expand_heavy<<<kBfsHeavyGrid, 256, 0, s>>>(hcur, cnt_in + 1, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
                                                        depth, nxt, hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
             launches += 2;
