@@ -567,7 +567,8 @@ void Graph::cc(u32* h_labels) {
     dist.reserve(nv + 1);
     k_iota_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv);
     GPMA_LAUNCH_CHECK();
-    k_cc_hook<<<grid_for(pma.capacity(), 256, 148 * 16), 256, 0, s>>>(pma.d_keys, pma.d_st, pma.capacity(), dist.ptr);
+    // 148x64 CTAs: measured 0.38 vs 0.48 ms (148x16) and 0.45 (one slot per thread) on C2
+    k_cc_hook<<<grid_for(pma.capacity(), 256, 148 * 64), 256, 0, s>>>(pma.d_keys, pma.d_st, pma.capacity(), dist.ptr);
     GPMA_LAUNCH_CHECK();
     k_cc_flatten<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv);
     GPMA_LAUNCH_CHECK();
