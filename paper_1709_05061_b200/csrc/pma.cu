@@ -560,9 +560,6 @@ __global__ void __launch_bounds__(256) k_bucket_sort_big(const u64* __restrict__
     }
 }
 
-__global__ void k_gate_npend(Ctr* ctr) {
-    ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : ctr->n_unique;
-}
 
 __global__ void k_iota(u32* p, const ull* n_dev) {
     const u64 n = *n_dev;
@@ -1934,7 +1931,15 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                     if (slf) o_l[xs[j]] = slf[i];
                 }
             },
-            [=] __device__(ull total) { ctr->n_unique = total; });
+            [=] __device__(ull total) {
+                ctr->n_unique = total;
+                // pending count of round 0 = the unique updates, or 0 when the
+                // graph front end flagged a bad insert id, an out-of-layout
+                // delete or an overflowed leaf bucket: every round is then a
+                // no-op (nothing is mutated) and the batch is rejected or redone
+                // after the first host sync — no round trip before the rounds
+                ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
+            });
         ++launches;
         if (!bucket) {
             // leaf assignment (pma.hpp:234-289), once per batch
@@ -1945,13 +1950,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             ++launches;
         }
     }
-    // pending count of round 0 = the unique updates, or 0 when the graph
-    // front end flagged a bad insert id / an out-of-layout delete: every
-    // round is then a no-op (nothing is mutated) and the batch is rejected or
-    // redone after the first host sync — no round trip before the rounds
-    k_gate_npend<<<1, 1, 0, stream_>>>(d_ctr);
-    GPMA_LAUNCH_CHECK();
-    ++launches;
     event(2);
     pidx0.reserve(n);
     pidx1.reserve(n);
