@@ -374,3 +374,33 @@ def test_leaf_bucket_pairs_front_end():
     assert gs.parity() == ref_parity(r, rs)
     assert_same_slots(g.pma().slots(), r.slots(), "pairs")
     assert (g.row_offsets() == r.row_offsets()).all()
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_graph_edge_cases_match_reference(mode):
+    """Empty batches, a batch deleting every edge (eager: the array shrinks),
+    re-inserting them, deletes of absent edges only, and edges on the highest
+    vertex id — stats, slots and row offsets as the reference."""
+    rng = np.random.default_rng(41)
+    nv = 2**12
+    s = np.concatenate([rng.integers(0, nv, 6000), [nv - 1] * 5])
+    d = np.concatenate([rng.integers(0, nv, 6000), [0, 1, nv - 1, 7, nv - 2]])
+    g = DynamicGraph.from_edges(nv, s, d, None, GraphConfig(deletion_mode=mode))
+    r = RefGraph(nv, s, d, None, graph_config(deletion_mode=mode))
+
+    def both(args, ctx):
+        gs = g.apply_batch(*args)
+        rs = r.apply_batch(*args)
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
+
+    e = np.zeros(0, np.uint32)
+    both((e, e, None, e, e), "empty batch")
+    both((e, e, None, rng.integers(0, nv, 300).astype(np.uint32), rng.integers(0, nv, 300).astype(np.uint32)),
+         "absent deletes")
+    both((e, e, None, s.astype(np.uint32), d.astype(np.uint32)), "delete everything")
+    assert g.num_edges() == 0
+    both((s.astype(np.uint32), d.astype(np.uint32), None, e, e), "re-insert everything")
+    both(([nv - 1], [nv - 1], [2.5], [nv - 1], [nv - 1]), "insert + delete of one key in one batch")
+    assert (bfs(g, nv - 1) == r.bfs(nv - 1)).all()
