@@ -128,6 +128,7 @@ typedef struct pma_timing {
     uint64_t level_big[16];    /* hub groups sent to the CTA kernel per level */
     uint64_t level_max_slice[16]; /* largest update slice per level */
     uint64_t commit_bytes; /* algorithmic HBM bytes of the commit kernels */
+    uint64_t level_bytes[16]; /* the same, per tree level */
     uint64_t front_end;    /* 0 radix sort, 1 leaf buckets, 2 leaf buckets overflowed -> radix sort redo */
 } pma_timing;
 

@@ -88,6 +88,7 @@ class pma_timing(C.Structure):
         ("level_big", C.c_uint64 * 16),
         ("level_max_slice", C.c_uint64 * 16),
         ("commit_bytes", C.c_uint64),
+        ("level_bytes", C.c_uint64 * 16),
         ("front_end", C.c_uint64),
     ]
 

@@ -2097,6 +2097,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                         *np_next = total;
                         // the level's stats (read at the next host sync)
                         ctr->lvl_committed[lv] = ctr->committed;
+                        ctr->lvl_bytes[lv] = ctr->commit_bytes;  // cumulative up to this level
                         ctr->lvl_groups[lv] = ctr->ngroups;
                         ctr->lvl_big[lv] = ctr->nbig;
                         ctr->lvl_maxslice[lv] = ctr->max_slice;
@@ -2117,6 +2118,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 seg_ms += ms;
                 if (l < 16) {
                     timing.level_ms[l] += ms;
+                    timing.level_bytes[l] += h_ctr->lvl_bytes[l] - (l > 0 ? h_ctr->lvl_bytes[l - 1] : 0);
                     timing.level_groups[l] += h_ctr->lvl_groups[l];
                     timing.level_big[l] += h_ctr->lvl_big[l];
                     timing.level_max_slice[l] = std::max<u64>(timing.level_max_slice[l], h_ctr->lvl_maxslice[l]);

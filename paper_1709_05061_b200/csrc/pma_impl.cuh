@@ -68,6 +68,7 @@ struct Ctr {
     ull lvl_groups[kMaxLevels];
     ull lvl_big[kMaxLevels];
     ull lvl_maxslice[kMaxLevels];
+    ull lvl_bytes[kMaxLevels];  // commit_bytes after each level (cumulative)
     ull pad[4];
 };
 
