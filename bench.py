@@ -176,11 +176,31 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ ours --
 
+def gpu_local_cpus(dev):
+    """The CPUs on the GPU's NUMA node (NVML): page-locked batches allocated
+    from there sit next to the GPU's PCIe root, which the zero-copy reads of
+    the front end feel directly.  None when NVML cannot tell."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    all_cpus = os.sched_getaffinity(0)
+    near = gpu_local_cpus(local)
+    if near:  # host work and page-locked buffers on the GPU's NUMA node
+        os.sched_setaffinity(0, near)
     if world > 1 or args.sharded:
         import torch.distributed as dist
         if world == 1:
@@ -329,7 +349,8 @@ def run_ours(args):
            "d2h_bytes_per_step": d2h // K, "ms_per_step": e2e_ms / K,
            "stage_ms_per_step": {k: round(v / K, 4) for k, v in e2e_stage.items()},
            "link_GBps": {"memcpy": round(cp_gbps.value, 1), "zero_copy_read": round(zc_gbps.value, 1)},
-           "inputs": "page-locked host arrays, read in place over PCIe by the front-end kernel"}
+           "inputs": "page-locked host arrays, read in place over PCIe by the front-end kernel",
+           "host_cpus": f"{len(near)} GPU-local of {len(all_cpus)}" if near else f"all {len(all_cpus)}"}
     del g2
 
     # ---- roofline of the dominant kernel (warp-tier commit: decide+merge+scatter) ----
@@ -384,6 +405,7 @@ def run_ours(args):
             out["analytics"] = analytics(pg, g, ext, nvx)
         out["sweep"] = sweep(pg, stream, dev, [int(x) for x in args.sweep.split(",") if x], nvx)
         if world == 1 and not args.no_cpu_baseline and args.config in ("C1", "C2"):
+            os.sched_setaffinity(0, all_cpus)  # the reference baseline gets every host thread
             out["cpu_baseline"] = cpu_baseline(stream, slides, win, W, nvx)
     if world > 1:
         torch.distributed.barrier()
