@@ -39,6 +39,50 @@ __device__ __forceinline__ void sweep_edges8(const u64* __restrict__ keys, const
     }
 }
 
+// The same sweep, but the Valid non-guard keys of each 256-slot step are
+// first packed into the warp's shared queue (ballot + popc ranks), then `f`
+// runs over the queue with every lane busy.  With C/E ~ 4.5 most slots are
+// gaps or guards: calling `f` straight from the slot lanes leaves ~1/3 of
+// them active, which is what bounds an `f` with real work (PageRank's
+// hot-table probe + atomics).  `queue` = 256 keys per warp of the block.
+template <class F>
+__device__ __forceinline__ void sweep_edges8_packed(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
+                                                    u64* queue, F f) {
+    const unsigned lane = threadIdx.x & 31u;
+    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    u64* q = queue + (threadIdx.x >> 5) * 256;
+    const unsigned below = lanemask_lt();
+    for (u64 base = warp * 256; base < cap; base += nwarps * 256) {
+        ulonglong2 kk[4];
+        unsigned short ss[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const u64 t = base + 64 * j + 2 * lane;
+            if (t < cap) {
+                ss[j] = __ldcs(reinterpret_cast<const unsigned short*>(st + t));
+                kk[j] = __ldcs(reinterpret_cast<const ulonglong2*>(keys + t));
+            } else {
+                ss[j] = 0;
+            }
+        }
+        unsigned n = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const bool a = (ss[j] & 0xFF) == kValid && !is_guard(kk[j].x);
+            const bool b = (ss[j] >> 8) == kValid && !is_guard(kk[j].y);
+            const unsigned ma = __ballot_sync(FULL, a), mb = __ballot_sync(FULL, b);
+            if (a) q[n + __popc(ma & below)] = kk[j].x;
+            n += __popc(ma);
+            if (b) q[n + __popc(mb & below)] = kk[j].y;
+            n += __popc(mb);
+        }
+        __syncwarp();
+        for (unsigned i = lane; i < n; i += 32) f(q[i]);
+        __syncwarp();
+    }
+}
+
 // out-degree: Valid non-guard slots per row.  Rows are contiguous slot runs,
 // so lanes holding the same source (match_any) add their count once — one
 // atomic per source per 32 slots, never one per edge of a hub row.
@@ -132,12 +176,13 @@ static __global__ void __launch_bounds__(256) k_pr_push(const u64* __restrict__ 
                                                         u32 nhot) {
     __shared__ u32 s_tab[2 * kHotTable];
     __shared__ double s_acc[kHotMax];
+    __shared__ u64 s_q[8 * 256];  // the block's 8 warp queues
     if (nhot) {
         for (u32 i = threadIdx.x; i < 2 * kHotTable; i += blockDim.x) s_tab[i] = hot_table[i];
         for (u32 i = threadIdx.x; i < nhot; i += blockDim.x) s_acc[i] = 0.0;
         __syncthreads();
     }
-    sweep_edges8(keys, st, cap, [&](u64 k) {
+    sweep_edges8_packed(keys, st, cap, s_q, [&](u64 k) {
         const u32 v = dst_of(k);
         const double sh = __ldg(&share[src_of(k)]);
         if (nhot) {
