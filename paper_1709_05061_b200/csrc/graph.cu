@@ -212,11 +212,11 @@ __device__ __forceinline__ u32 cc_find(u32* parent, u32 x) {
     return x;
 }
 
-__global__ void k_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u32* parent) {
-    for (u64 t = blockIdx.x * u64(blockDim.x) + threadIdx.x; t < cap; t += u64(gridDim.x) * blockDim.x) {
-        if (st[t] != kValid) continue;
-        const u64 k = keys[t];
-        if (is_guard(k)) continue;
+// (over warp-packed edge queues: the pointer chases run with every lane busy)
+__global__ void __launch_bounds__(256) k_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
+                                                 u32* parent) {
+    __shared__ u64 s_q[8 * 256];
+    sweep_edges8_packed(keys, st, cap, s_q, [&](u64 k) {
         u32 a = src_of(k), b = dst_of(k);
         for (;;) {
             a = cc_find(parent, a);
@@ -227,7 +227,7 @@ __global__ void k_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ s
             a = hi;
             b = lo;
         }
-    }
+    });
 }
 
 __global__ void k_cc_flatten(u32* parent, u64 nv) {
@@ -567,8 +567,10 @@ void Graph::cc(u32* h_labels) {
     dist.reserve(nv + 1);
     k_iota_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv);
     GPMA_LAUNCH_CHECK();
-    // 148x64 CTAs: measured 0.38 vs 0.48 ms (148x16) and 0.45 (one slot per thread) on C2
-    k_cc_hook<<<grid_for(pma.capacity(), 256, 148 * 64), 256, 0, s>>>(pma.d_keys, pma.d_st, pma.capacity(), dist.ptr);
+    // 8x the resident CTAs (the hooks are pointer chases: more warps queued
+    // keep the SMs fed; measured 1x 0.29, 4x 0.24, 8x 0.23 ms on C2)
+    static const unsigned cc_res = resident_grid(k_cc_hook, 256) * 8;
+    k_cc_hook<<<grid_for(pma.capacity() / 256 * 8, 256, cc_res), 256, 0, s>>>(pma.d_keys, pma.d_st, pma.capacity(), dist.ptr);
     GPMA_LAUNCH_CHECK();
     k_cc_flatten<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv);
     GPMA_LAUNCH_CHECK();
