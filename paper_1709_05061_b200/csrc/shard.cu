@@ -215,7 +215,8 @@ __global__ void k_shard_bfs_update(const u8* __restrict__ flags, u64 lo, u64 nlo
 // id — the reference's labels.
 __global__ void __launch_bounds__(256) k_shard_cc_hook(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
                                                        u32* labels) {
-    sweep_edges8(keys, st, cap, [&](u64 k) {
+    __shared__ u64 s_q[8 * 256];
+    sweep_edges8_packed(keys, st, cap, s_q, [&](u64 k) {
         const u32 u = src_of(k), v = dst_of(k);
         const u32 a = labels[u], b = labels[v];
         if (a == b) return;
