@@ -111,6 +111,67 @@ __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64*
     }
 }
 
+// Valid non-guard neighbours are packed into a per-warp queue (ballot ranks)
+// across 128-slot chunks and rows, then probed 32 at a time with every lane
+// busy: most slots of a row are gaps and short rows are the norm.
+struct BfsWarpQueue {
+    u32* q;    // 256 entries of shared memory
+    u32 cnt;   // warp-uniform
+    __device__ __forceinline__ void drain(const u64* __restrict__ ro, u32* __restrict__ dist, u32 depth,
+                                          u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
+        const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
+        __syncwarp();
+        for (u32 base = 0; base < cnt; base += 32) {
+            const bool act = base + lane < cnt;
+            const u32 v = act ? q[base + lane] : 0u;
+            bool won = false;
+            if (act && dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+            const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
+            const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
+            if (lm) {
+                u32 o = 0;
+                if (lane == 0) o = atomicAdd(&qn[0], u32(__popc(lm)));
+                o = __shfl_sync(FULL, o, 0);
+                if (won && !heavy) next[o + __popc(lm & below)] = v;
+            }
+            if (hm) {
+                u32 o = 0;
+                if (lane == 0) o = atomicAdd(&qn[1], u32(__popc(hm)));
+                o = __shfl_sync(FULL, o, 0);
+                if (heavy) hnext[o + __popc(hm & below)] = v;
+            }
+        }
+        __syncwarp();
+        cnt = 0;
+    }
+    // the 128 slots [t0, t0 + 128) ∩ [., e): lane l reads t0 + 32 j + l
+    __device__ __forceinline__ void push128(const u64* __restrict__ keys, const u8* __restrict__ st, u64 t0, u64 e,
+                                            const u64* __restrict__ ro, u32* __restrict__ dist, u32 depth,
+                                            u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
+        const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
+        u32 vv[4];
+        bool ok[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const u64 t = t0 + 32 * j + lane;
+            ok[j] = false;
+            vv[j] = 0;
+            if (t < e && st[t] == kValid) {
+                const u64 k = keys[t];
+                ok[j] = !is_guard(k);
+                vv[j] = dst_of(k);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const unsigned m = __ballot_sync(FULL, ok[j]);
+            if (ok[j]) q[cnt + __popc(m & below)] = vv[j];
+            cnt += __popc(m);
+        }
+        if (cnt >= 128) drain(ro, dist, depth, next, hnext, qn);  // room for the next chunk stays
+    }
+};
+
 // (frontier sizes are read from the device: levels run back to back, the
 // host only syncs once per window of levels)
 // four slots per thread per call (t, t + S, t + 2S, t + 3S; S = the
@@ -165,70 +226,17 @@ __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ fron
                                                     const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
                                                     u32* __restrict__ next, u32* __restrict__ hnext,
                                                     u32* __restrict__ qn) {
-    // Valid non-guard neighbours of the warp's rows are packed into a warp
-    // queue (ballot ranks) across rows, and probed 32 at a time with every
-    // lane busy: most slots of a row are gaps, and short rows are the norm.
     __shared__ u32 s_q[8][256];
     const u32 nf = *nfp;
-    const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
-    u32* q = s_q[threadIdx.x >> 5];
-    const unsigned below = lanemask_lt();
-    u32 cnt = 0;
-    auto drain = [&](u32 upto) {  // probe the first `upto` queued vertices (warp-uniform)
-        __syncwarp();
-        for (u32 base = 0; base < upto; base += 32) {
-            const bool act = base + lane < upto;
-            const u32 v = act ? q[base + lane] : 0u;
-            bool won = false;
-            if (act && dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
-            const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
-            const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
-            if (lm) {
-                u32 o = 0;
-                if (lane == 0) o = atomicAdd(&qn[0], u32(__popc(lm)));
-                o = __shfl_sync(FULL, o, 0);
-                if (won && !heavy) next[o + __popc(lm & below)] = v;
-            }
-            if (hm) {
-                u32 o = 0;
-                if (lane == 0) o = atomicAdd(&qn[1], u32(__popc(hm)));
-                o = __shfl_sync(FULL, o, 0);
-                if (heavy) hnext[o + __popc(hm & below)] = v;
-            }
-        }
-        __syncwarp();
-    };
+    BfsWarpQueue wq{s_q[threadIdx.x >> 5], 0};
     for (u64 f = warp; f < nf; f += nwarps) {
         const u32 u = frontier[f];
         const u64 b = ro[u], e = ro[u + 1];
-        for (u64 t0 = b; t0 < e; t0 += 128) {
-            u32 vv[4];
-            bool ok[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const u64 t = t0 + 32 * j + lane;
-                ok[j] = false;
-                if (t < e && st[t] == kValid) {
-                    const u64 k = keys[t];
-                    ok[j] = !is_guard(k);
-                    vv[j] = dst_of(k);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const unsigned m = __ballot_sync(FULL, ok[j]);
-                if (ok[j]) q[cnt + __popc(m & below)] = vv[j];
-                cnt += __popc(m);
-            }
-            if (cnt >= 128) {  // room for the next 128-slot chunk stays
-                drain(cnt);
-                cnt = 0;
-            }
-        }
+        for (u64 t0 = b; t0 < e; t0 += 128) wq.push128(keys, st, t0, e, ro, dist, depth, next, hnext, qn);
     }
-    drain(cnt);
+    wq.drain(ro, dist, depth, next, hnext, qn);
 }
 
 __global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, const u32* nhp,
@@ -236,6 +244,7 @@ __global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict_
                                                           const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
                                                           u32* __restrict__ next, u32* __restrict__ hnext,
                                                           u32* __restrict__ qn) {
+    // (a packed warp queue here measured slower: 1.03 vs 0.93 ms on the C2 hub BFS)
     const u32 nh = *nhp;
     for (u64 task = blockIdx.x; task < u64(nh) * kHeavyParts; task += gridDim.x) {
         const u32 u = hfrontier[task / kHeavyParts];
