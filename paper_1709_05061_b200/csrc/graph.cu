@@ -688,7 +688,8 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
         GPMA_CUDA(cudaEventRecord(pma_ev(2), s));
         static const unsigned pr_res = resident_grid(k_pr_push, 256);  // measured best vs 0.5x / 2x
         k_pr_push<<<pr_res, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr, nhot_);
-        k_pr_finish_next<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, y, outdeg.ptr, nv, d, cur, nxt, nxt + 1,
+        // (148x4 CTAs: fewer per-CTA reductions; measured 1% better than 148x8)
+        k_pr_finish_next<<<grid_for(nv, 256, 148 * 4), 256, 0, s>>>(x, y, outdeg.ptr, nv, d, cur, nxt, nxt + 1,
                                                                    pshare.ptr);
         GPMA_LAUNCH_CHECK();
         GPMA_CUDA(cudaEventRecord(pma_ev(3), s));
