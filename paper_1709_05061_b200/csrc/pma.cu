@@ -276,7 +276,7 @@ __device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u6
         // packed: key above the arrival index for inserts, all-ones for
         // deletes — among equal keys the inserts keep arrival order and the
         // deletes sort after them, which is all duplicate resolution needs
-        ck[i] = (c << ib) | (ins ? u64(i) : ((1ull << ib) - 1));
+        ck[i] = (c << ib) | (ins ? (f.opbit ? 0ull : u64(i)) : ((1ull << ib) - 1));
     } else {
         ck[i] = c;
         ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
@@ -1750,7 +1750,19 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         int ib = 1;
         while ((1ull << ib) < n) ++ib;
         while ((1ull << ib) <= n) ++ib;  // the all-ones index is reserved for deletes
-        if (nbits + ib > 64) ib = 0;     // no room: key + payload pairs
+        gf->opbit = 0;
+        if (nbits + ib > 64) {
+            // no room for the index: unweighted batches carry the op alone
+            // (inserts precede deletes in arrival order, so the stable key
+            // sort still yields arrival order; the weight is 1.0) — keys-only
+            // passes of 8 B instead of (key, payload) pairs of 12 B
+            if (!gf->iw && nbits + 1 <= 64) {
+                ib = 1;
+                gf->opbit = 1;
+            } else {
+                ib = 0;  // key + payload pairs
+            }
+        }
         packed_ib = ib;
         // leaf-bucket front end for large batches: the leaf of every update is
         // found up front and the batch counting-sorted by leaf (one scatter)

@@ -103,6 +103,10 @@ struct GraphFront {
     u64* bk;
     u64* bv;
     u8* bo;
+    // unweighted batch whose key + arrival index overflow one word: the packed
+    // word carries just the op (key << 1 | is_delete) — the stable sort keeps
+    // arrival order, and no weight is gathered by index
+    int opbit = 0;
     // results
     u64 guard_deletes = 0;
     long long bad_insert = -1;  // first insert index with an id >= nv

@@ -355,10 +355,12 @@ def test_leaf_bucket_edge_cases(mode):
     assert all((x == y).all() for x, y in zip(before, g.pma().slots()))
 
 
-def test_leaf_bucket_pairs_front_end():
+@pytest.mark.parametrize("weighted", [True, False])
+def test_leaf_bucket_pairs_front_end(weighted):
     """When key and arrival index do not fit one 64-bit word (|V| = 2^22,
-    batch > 2^19) the leaf-bucket front end sorts (key, payload) pairs:
-    still bit-exact with the reference."""
+    batch > 2^19) the leaf-bucket front end sorts (key, payload) pairs —
+    or, unweighted, words carrying only the op: still bit-exact with the
+    reference."""
     rng = np.random.default_rng(31)
     nv = 2**22
     s, d = rng.integers(0, nv, 600000), rng.integers(0, nv, 600000)
@@ -366,11 +368,12 @@ def test_leaf_bucket_pairs_front_end():
     r = RefGraph(nv, s, d)
     a, b = rng.integers(0, nv, 400000), rng.integers(0, nv, 400000)
     a[:200], b[:200] = 5, 6  # a duplicated key
+    w = rng.integers(1, 9, 400000).astype(float) if weighted else None
     c = np.concatenate([s[:250000], np.full(100, 5)]).astype(np.uint32)
     dd = np.concatenate([d[:250000], np.full(100, 6)]).astype(np.uint32)
-    gs = g.apply_batch(a, b, None, c, dd)
+    gs = g.apply_batch(a, b, w, c, dd)
     assert int(g.last_timing().front_end) in (1, 2)
-    rs = r.apply_batch(a, b, None, c, dd)
+    rs = r.apply_batch(a, b, w, c, dd)
     assert gs.parity() == ref_parity(r, rs)
     assert_same_slots(g.pma().slots(), r.slots(), "pairs")
     assert (g.row_offsets() == r.row_offsets()).all()
@@ -404,3 +407,26 @@ def test_graph_edge_cases_match_reference(mode):
     both((s.astype(np.uint32), d.astype(np.uint32), None, e, e), "re-insert everything")
     both(([nv - 1], [nv - 1], [2.5], [nv - 1], [nv - 1]), "insert + delete of one key in one batch")
     assert (bfs(g, nv - 1) == r.bfs(nv - 1)).all()
+
+
+@pytest.mark.parametrize("weighted", [True, False])
+def test_radix_front_end_wide_keys(weighted):
+    """|V| = 2^24 (49 key bits) with a 70K-update batch (17 index bits) and
+    far more leaves than updates: the radix front end sorts (key, payload)
+    pairs (weighted) or op-carrying words (unweighted) — bit-exact with the
+    reference either way."""
+    rng = np.random.default_rng(33)
+    nv = 2**24
+    s, d = rng.integers(0, nv, 200000), rng.integers(0, nv, 200000)
+    g = DynamicGraph.from_edges(nv, s, d)
+    r = RefGraph(nv, s, d)
+    a, b = rng.integers(0, nv, 40000), rng.integers(0, nv, 40000)
+    a[:50], b[:50] = 9, 9
+    w = rng.integers(1, 9, 40000).astype(float) if weighted else None
+    c = np.concatenate([s[:30000], np.full(30, 9)]).astype(np.uint32)
+    dd = np.concatenate([d[:30000], np.full(30, 9)]).astype(np.uint32)
+    gs = g.apply_batch(a, b, w, c, dd)
+    assert int(g.last_timing().front_end) == 0
+    rs = r.apply_batch(a, b, w, c, dd)
+    assert gs.parity() == ref_parity(r, rs)
+    assert_same_slots(g.pma().slots(), r.slots(), "wide keys")
