@@ -2227,11 +2227,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                             ctr->nmatched = total;
                             mbv[ctr->nv] = u32(total);
                         });
-                    // the compaction's fin is skipped when nv == 0: seed mb[0]
-                    if (true) {
-                        // nv may be zero: make mb[nv] valid via a tiny kernel-free path
-                        // (handled below by k_root_scatter_ins reading mb[r] with r<=nv)
-                    }
+                    // (nv == 0: mb[0] is seeded after the sync below, before the
+                    // insert scatter reads mb[r] for r <= nv)
                     k_root_scatter_surv<<<grid_for(cap_, 256, 148 * 16), 256, 0, stream_>>>(
                         dek, dev, &d_ctr->nv, mf, mbv, irr, &d_ctr->nins, ok.ptr, ov.ptr);
                     GPMA_LAUNCH_CHECK();
