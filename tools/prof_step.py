@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--analytics", action="store_true", help="profile BFS + CC + one warm PageRank instead")
     ap.add_argument("--bfs-root", type=int, default=-1, help="with --analytics: this BFS root (default: the largest hub)")
+    ap.add_argument("--config", default="C2", help="bench.CONFIGS key (stream and |V|)")
     args = ap.parse_args()
     import torch
 
@@ -32,11 +33,13 @@ def main():
     from paper_1709_05061_b200.abi import load_library
 
     load_library().gpma_warmup(0)
-    stream = pg.EdgeStream.rmat(bench.NV, bench.NE, seed=bench.GEN_SEED).shuffle(bench.SHUFFLE_SEED)
+    cfg = bench.CONFIGS[args.config]
+    stream = bench.make_stream(pg, cfg, bench.GEN_SEED)
+    nv = cfg["nv"]
     win = pg.SlidingWindow(stream, 0)
     win.reserve((args.warmup + args.steps) * args.batch + 16)
     info = win.info()
-    g = pg.DynamicGraph.from_edges_device(bench.NV, info.stream_src, info.stream_dst, None, info.initial_size, device=0)
+    g = pg.DynamicGraph.from_edges_device(nv, info.stream_src, info.stream_dst, None, info.initial_size, device=0)
     slides = [win.slide(args.batch) for _ in range(args.warmup + args.steps)]
     info = win.info()
 
