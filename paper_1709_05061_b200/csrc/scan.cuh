@@ -22,6 +22,7 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kScanTile = kScanThreads * kScanItems;
+static_assert(kScanItems * kScanWarps == 64, "compact_kernel's warp-0 scan takes two (row, warp) counts per lane");
 // status word: [63:36] epoch | [35:34] flag (1 aggregate, 2 inclusive) | [33:0] value
 constexpr int kEpochShift = 36;
 constexpr int kFlagShift = 34;
