@@ -152,6 +152,15 @@ class TorchComm:
         return [torch.cat([o[:int(k)] for o, k in zip(outs, ns)])]
 
 
+def fused_offsets(M):
+    """Fused routing's placement from the count matrix M[sender][owner]:
+    sender s writes its owner-r updates at [before[s][r], before[s][r] +
+    M[s][r]) of r's receive buffer — the senders' segments tile [0, nrecv[r])
+    in sender-rank order, exactly where an all-to-all would put them."""
+    M = np.asarray(M, np.int64)
+    return np.cumsum(M, axis=0) - M, M.sum(axis=0)
+
+
 # ------------------------------------------------------------------ graph
 
 @dataclass
@@ -339,8 +348,7 @@ class ShardedGraph:
             parts = [torch.empty_like(cnt) for _ in range(W)]
             self.comm.dist.all_gather(parts, cnt, group=self.comm.group)
             M = torch.stack(parts).cpu().numpy()
-        before = np.cumsum(M, axis=0) - M  # before[s][r]: slots of lower senders at owner r
-        nrecv = M.sum(axis=0)
+        before, nrecv = fused_offsets(M)
         rx = self._ensure_rx(int(nrecv.max()) if W else 0, weighted)
         for i in range(L):
             a, b, w, c, d = slices[i]
