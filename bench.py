@@ -124,6 +124,7 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
         self._nvml = None
+        self.started = False
         try:
             import pynvml
             pynvml.nvmlInit()
@@ -144,6 +145,7 @@ class ClockSampler:
         self.samples.append((sm, r))
 
     def start(self):
+        self.started = True
         if self._nvml is None:
             return
         self._sample()
@@ -175,6 +177,90 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ ours --
+
+PMA_STATS_BYTES = 632  # sizeof(pma_stats), read back by every apply_batch
+
+
+def full_slides(info, B):
+    """Number of FULL slides of B arrivals the stream holds after the initial
+    window (SlidingWindow::slide takes min(batch, remaining()),
+    streaming.hpp:111): the bench never times a partial or empty slide."""
+    P = int(info.stream_size - info.initial_size) // B
+    if P < 1:
+        raise SystemExit(f"bench: the stream holds no full slide of batch {B}")
+    return P
+
+
+def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks):
+    """Drive W untimed warm-up steps then K timed steps over `slides` (the
+    first min(W + K, P) full slides of the window, in order).  When a pass has
+    used every slide the stream holds, the graph is rebuilt from the initial
+    window (untimed) and the next pass replays the same slides — so every
+    timed step is a full slide on a window in the state the reference would
+    have.  Timed segments are bracketed by barrier + synchronize and timed by
+    CUDA events on the library's stream; returns (graph, summed ms, passes)."""
+    import torch
+    lib = g._lib
+    n_sl = len(slides)
+    total = 0.0
+    cur = step = 0
+    passes = 1
+    while step < W + K:
+        if cur == n_sl:
+            g = None
+            g = make_graph()
+            cur = 0
+            passes += 1
+        timed = step >= W
+        n = min(n_sl - cur, (W + K if timed else W) - step)
+        if not timed:
+            for s in slides[cur:cur + n]:
+                on_step(g, s, False)
+        else:
+            ext = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
+            if world > 1:
+                torch.distributed.barrier()
+            torch.cuda.synchronize()
+            if clocks is not None and not clocks.started:
+                clocks.start()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(ext)
+            for s in slides[cur:cur + n]:
+                on_step(g, s, True)
+            e1.record(ext)
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            total += e0.elapsed_time(e1)
+        step += n
+        cur += n
+    return g, total, passes
+
+
+def reduce_max_sum(ms, n, world):
+    """(max over ranks of ms, sum over ranks of n)."""
+    if world == 1:
+        return ms, float(n)
+    import torch
+    t = torch.tensor([ms], device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    u = torch.tensor([float(n)], device="cuda")
+    torch.distributed.all_reduce(u)
+    return float(t.item()), float(u.item())
+
+
+def ncu_traffic(config):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture of THIS config, or None when none was
+    taken (profiles/ncu_summary.json, keyed by config)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            rec = json.load(f).get("configs", {}).get(config)
+        return None if rec is None else rec.get("commit_kernel_dram_bytes_per_launch")
+    except Exception:
+        return None
+
 
 def gpu_local_cpus(dev):
     """The CPUs on the GPU's NUMA node (NVML): page-locked batches allocated
@@ -224,32 +310,43 @@ def run_ours(args):
     gen_s = time.time() - t0
     win = pg.SlidingWindow(stream, dev)
     info = win.info()
-    win.reserve((W + K) * B + 16)
+    # Every step is a FULL slide of B arrivals (streaming.hpp:108-112 takes
+    # min(batch, remaining)): the stream holds P full slides after the initial
+    # window, so W + K steps run in passes of at most P slides, the graph
+    # rebuilt from the initial window (untimed) between passes.
+    P = full_slides(info, B)
+    win.reserve(min(W + K, P) * B + 16)
     info = win.info()
+    slides = [win.slide(B) for _ in range(min(W + K, P))]
+    for s in slides:
+        assert s.n_ins == B and not s.final_partial, "bench slide is not a full slide"
+    info = win.info()
+
+    def make_graph():
+        return pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size,
+                                                 device=dev)
+
     t1 = time.time()
-    g = pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
+    g = make_graph()
     load_s = time.time() - t1
     cap = g.pma().capacity()
-    slides = [win.slide(B) for _ in range(W + K)]
-    info = win.info()
     lib = g._lib
-    ext = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
 
     def apply_dev(graph, s):
         return graph.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset,
                                         None, s.n_ins, info.del_src + 4 * s.del_offset,
                                         info.del_dst + 4 * s.del_offset, s.n_del)
 
-    for s in slides[:W]:
-        apply_dev(g, s)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
     clocks = ClockSampler(dev)
-    clocks.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(ext)
+    per_step = []  # (stats, timing) kept raw; digested after the timed region
+
+    def on_step(graph, s, timed):
+        st = apply_dev(graph, s)
+        if timed:
+            per_step.append((st, graph.last_timing()))
+
+    g, ms, passes = run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks)
+    clk = clocks.stop()
     updates = 0
     seg_ms = 0.0
     merge_slots = 0
@@ -262,12 +359,6 @@ def run_ours(args):
     level_groups = [0] * 16
     level_big = [0] * 16
     level_maxs = [0] * 16
-    per_step = []  # (stats, timing) kept raw; digested after the timed region
-    for s in slides[W:]:
-        st = apply_dev(g, s)
-        per_step.append((st, g.last_timing()))
-    ev1.record(ext)
-    torch.cuda.synchronize()
     for st, tm in per_step:
         updates += st.batch_size
         seg_ms += st.segment_phase_ns / 1e6
@@ -283,23 +374,14 @@ def run_ours(args):
             level_groups[lv] += tm.level_groups[lv]
             level_big[lv] += tm.level_big[lv]
             level_maxs[lv] = max(level_maxs[lv], tm.level_max_slice[lv])
-    if world > 1:
-        torch.distributed.barrier()
-    clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
-    # max over ranks
-    if world > 1:
-        t = torch.tensor([ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        u = torch.tensor([float(updates)], device="cuda")
-        torch.distributed.all_reduce(u)
-        ms_max, total_updates = float(t.item()), float(u.item())
-    else:
-        ms_max, total_updates = ms, float(updates)
+    ms_max, total_updates = reduce_max_sum(ms, updates, world)
     value = total_updates / (ms_max / 1e3)
 
     # ---- e2e through the host C ABI from pinned buffers (same slides) ----
-    g2 = pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size, device=dev)
+    # the drop-in call as a C++ caller makes it: page-locked inputs in, the
+    # UpdateStats out including touched_ranges (update_stats.hpp:29, fetched
+    # by include/pmagraph/update_stats.hpp every batch)
+    del g
     hs, hd = stream.arrays()
     host = []
     for s in slides:
@@ -310,48 +392,42 @@ def run_ours(args):
         win.deletions_host(s.del_offset, s.n_del, c.numpy().view(np.uint32), d.numpy().view(np.uint32))
         host.append((a.numpy().view(np.uint32), b.numpy().view(np.uint32), c.numpy().view(np.uint32),
                      d.numpy().view(np.uint32), (a, b, c, d)))
-    for a, b, c, d, _ in host[:W]:
-        g2.apply_batch(a, b, None, c, d, with_touched=False)
-    ext2 = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g2.h), device=torch.device("cuda", dev))
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    h2d = d2h = 0
-    e2e_updates = 0
-    e2e_stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
+    host_by_slide = {id(s): h for s, h in zip(slides, host)}
     e2e_steps = []
-    e0.record(ext2)
-    for a, b, c, d, _ in host[W:]:
-        st = g2.apply_batch(a, b, None, c, d, with_touched=False)
-        e2e_steps.append((st, g2.last_timing()))
-        h2d += a.nbytes + b.nbytes + c.nbytes + d.nbytes
-        d2h += 632  # pma_stats read back every step
-    e1.record(ext2)
-    torch.cuda.synchronize()
+    io = {"h2d": 0, "d2h": 0}
+
+    def on_e2e(graph, s, timed):
+        a, b, c, d, _ = host_by_slide[id(s)]
+        st = graph.apply_batch(a, b, None, c, d, with_touched=True)
+        if timed:
+            e2e_steps.append((st, graph.last_timing()))
+            io["h2d"] += a.nbytes + b.nbytes + c.nbytes + d.nbytes
+            io["d2h"] += PMA_STATS_BYTES + 16 * len(st.touched_ranges)
+
+    g2, e2e_ms, _ = run_passes(make_graph(), make_graph, slides, P, W, K, on_e2e, dev, world, None)
+    e2e_stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
+    e2e_updates = 0
     for st, tm2 in e2e_steps:
         for k in e2e_stage:
             e2e_stage[k] += getattr(tm2, k)
         e2e_updates += st.batch_size
-    e2e_ms = e0.elapsed_time(e1)
+    h2d, d2h = io["h2d"], io["d2h"]
     # the link the inputs cross: a step's bytes of page-locked memory moved by
     # the copy engines and read in place by SM loads (best of 5 each)
     hbuf = torch.empty(h2d // K, dtype=torch.uint8).pin_memory()
     cp_gbps, zc_gbps = C.c_double(), C.c_double()
     lib.gpma_probe_h2d(dev, C.c_void_p(hbuf.data_ptr()), hbuf.numel(), 5, C.byref(cp_gbps), C.byref(zc_gbps))
     del hbuf
-    if world > 1:
-        t = torch.tensor([e2e_ms], device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        u = torch.tensor([float(e2e_updates)], device="cuda")
-        torch.distributed.all_reduce(u)
-        e2e_ms, e2e_updates = float(t.item()), float(u.item())
+    e2e_ms, e2e_updates = reduce_max_sum(e2e_ms, e2e_updates, world)
     e2e = {"value": e2e_updates / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
            "d2h_bytes_per_step": d2h // K, "ms_per_step": e2e_ms / K,
            "stage_ms_per_step": {k: round(v / K, 4) for k, v in e2e_stage.items()},
            "link_GBps": {"memcpy": round(cp_gbps.value, 1), "zero_copy_read": round(zc_gbps.value, 1)},
            "inputs": "page-locked host arrays, read in place over PCIe by the front-end kernel",
+           "outputs": "pma_stats + UpdateStats.touched_ranges (reference order) read back every step",
            "host_cpus": f"{len(near)} GPU-local of {len(all_cpus)}" if near else f"all {len(all_cpus)}"}
-    del g2
+    g = g2
+    ext = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
 
     # ---- roofline of the dominant kernel (warp-tier commit: decide+merge+scatter) ----
     peak, peak_kind = measured_peak()
@@ -367,21 +443,17 @@ def run_ours(args):
     l0_ms = level_ms[0] / K
     achieved = (level_bytes[0] / K) / (l0_ms / 1e3) / 1e9 if l0_ms > 0 else None
     all_achieved = (commit_bytes / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            traffic = json.load(f).get("commit_kernel_dram_bytes_per_launch")
-    except Exception:
-        pass
+    traffic = ncu_traffic(args.config)
     roofline = {"bound": "hbm", "kernel": "leaf-level commit: k_commit_leaf (decide + merge + even re-dispatch + fused "
                                           "header/row-offset refresh) + k_commit_cta for its hub groups",
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "algorithmic_bytes_per_step": level_bytes[0] // K, "kernel_ms_per_launch": l0_ms,
+                "algorithmic_bytes_per_step": level_bytes[0] // K, "kernel_ms_per_step": l0_ms,
+                "launches_per_step": "one k_commit_leaf launch (+ one k_commit_cta launch when the level has hub groups) per step: ms and bytes are per step = per launch",
                 "all_levels": {"algorithmic_bytes_per_step": commit_bytes // K, "ms_per_step": seg_ms / K,
                                "achieved": all_achieved, "frac": (all_achieved / peak) if all_achieved else None},
                 "scatter_bytes_per_step": BYTES_PER_MERGE_SLOT * merge_slots // K,
-                "kernel_ms_per_step": seg_ms / K, "step_ms": ms / K,
+                "commit_ms_per_step_all_levels": seg_ms / K, "step_ms": ms / K,
                 "stage_ms_per_step": {k: v / K for k, v in stage.items()},
                 "commit_ms_per_level": [round(x / K, 4) for x in level_ms if x > 0],
                 "groups_per_level": [x / K for x in level_groups if x > 0],
@@ -395,7 +467,8 @@ def run_ours(args):
            "config": {"workload": cfg["workload"],
                       "batch": B, "num_vertices": nvx, "stream_edges": len(stream), "pma_capacity": cap,
                       "parallelism": f"dp{world} (independent source-range shards)",
-                      "l2": "inputs larger than L2 (PMA slot array 1.1 GB per GPU)",
+                      "l2": f"inputs larger than L2 (PMA slot array {17 * cap / 1e9:.2f} GB per GPU vs 126 MB L2)",
+                      "full_slides_per_pass": P, "passes": passes,
                       "deletion_mode": "lazy", "rounds_per_step": rounds / K},
            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "clocks": clk,
            "setup_s": {"generate": round(gen_s, 2), "from_edges": round(load_s, 3)}}
@@ -753,9 +826,16 @@ def cpu_baseline(stream, slides, win, W, nv):
         st, ms = ref.apply_batch_timed(a, b, None, c, dd, cores)
         ms_total += ms
         n_total += st.batch_size
+    # the next slide with one worker (workers = hardware threads and 1)
+    sl = slides[2]
+    a, b = s[sl.ins_offset:sl.ins_offset + sl.n_ins], d[sl.ins_offset:sl.ins_offset + sl.n_ins]
+    c, dd = win.deletions_host(sl.del_offset, sl.n_del)
+    st1, ms1 = ref.apply_batch_timed(a, b, None, c, dd, 1)
     return {"value": n_total / (ms_total / 1e3), "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"2 slides of batch {slides[0].n_ins} on the same window via reference apply_batch "
-                      f"({cores} workers); reference from_edges setup {build_s:.1f}s excluded"}
+            "sample": f"2 full slides of batch {slides[0].n_ins} on the same window via reference apply_batch "
+                      f"({cores} workers); reference from_edges setup {build_s:.1f}s excluded",
+            "one_worker": {"value": st1.batch_size / (ms1 / 1e3), "unit": UNIT, "cores": 1,
+                           "sample": "the third slide through apply_batch with workers = 1"}}
 
 
 # ------------------------------------------------------------- reference --
@@ -779,11 +859,23 @@ def run_reference(args):
         st.shuffle(cfg["shuffle"])
     s, d, w, _ = st.arrays()
     half = (len(s) + 1) // 2
-    ref = oracle.RefGraph(nvx, s[:half], d[:half], w[:half])
+    # the same full-slide passes as our arm (run_passes): P full slides per
+    # pass, the reference graph rebuilt from the initial window between passes
+    P = (len(s) - half) // B
+    if P < 1:
+        raise SystemExit(f"bench: the stream holds no full slide of batch {B}")
     win = oracle.RefWindow(st)
+    slides = [win.slide(B) for _ in range(min(W + K, P))]
+    assert all(len(x[0]) == B for x in slides), "reference slide is not a full slide"
     total_ms, total_n = 0.0, 0
+    ref, cur = None, len(slides)
     for i in range(W + K):
-        a, b, ww, c, dd = win.slide(B)
+        if cur == len(slides):
+            ref = None
+            ref = oracle.RefGraph(nvx, s[:half], d[:half], w[:half])
+            cur = 0
+        a, b, ww, c, dd = slides[cur]
+        cur += 1
         stt, ms = ref.apply_batch_timed(a, b, ww, c, dd, cores)
         if i >= W:
             total_ms += ms

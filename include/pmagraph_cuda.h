@@ -423,6 +423,25 @@ int gpma_rebuild_csr(gpma_rebuild* r, uint64_t* row_offsets, uint32_t* col, doub
 uint64_t gpma_rebuild_num_edges(const gpma_rebuild* r);
 void* gpma_rebuild_cuda_stream(gpma_rebuild* r);
 
+/* ---- data-parallel primitives (primitives.hpp:21-84) ------------------
+ * The library's own device primitives behind the batch pipeline, exposed on
+ * their own: a onesweep LSD radix sort (8-bit digits, digits every key shares
+ * are skipped as primitives.hpp:38-46 does) and a single-pass exclusive scan.
+ * Errors: gpma_primitives_last_error(). */
+
+/* sort_by_key / sort_pairs_by_key (primitives.hpp:21-60): stable ascending
+ * sort of n 64-bit keys by key bits [begin_bit, end_bit) (0, 64 = the whole
+ * key), the u32 payload (may be NULL) moving with its key; equal keys keep
+ * their input order.  Sorted in place; host arrays, or device arrays with
+ * the _device variant. */
+int gpma_sort_by_key(int device, uint64_t* keys, uint32_t* payload, size_t n, int begin_bit, int end_bit);
+int gpma_sort_by_key_device(int device, uint64_t* d_keys, uint32_t* d_payload, size_t n, int begin_bit,
+                            int end_bit);
+/* exclusive_scan (primitives.hpp:74-84): d_out[0] = 0, d_out[i] = d_out[i-1]
+ * + d_in[i-1], n u32 device values (the totals must fit 32 bits). */
+int gpma_exclusive_scan_device(int device, const uint32_t* d_in, uint32_t* d_out, size_t n);
+const char* gpma_primitives_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -237,6 +237,10 @@ SIGNATURES = [
     ("gpma_rebuild_csr", C.c_int, [_P, _P, _P, _P]),
     ("gpma_rebuild_num_edges", C.c_uint64, [_P]),
     ("gpma_rebuild_cuda_stream", _P, [_P]),
+    ("gpma_sort_by_key", C.c_int, [C.c_int, _P, _P, C.c_size_t, C.c_int, C.c_int]),
+    ("gpma_sort_by_key_device", C.c_int, [C.c_int, _P, _P, C.c_size_t, C.c_int, C.c_int]),
+    ("gpma_exclusive_scan_device", C.c_int, [C.c_int, _P, _P, C.c_size_t]),
+    ("gpma_primitives_last_error", C.c_char_p, []),
     # pmagraph_stream.h
     ("gpma_stream_last_error", C.c_char_p, []),
     ("gpma_stream_rmat", C.c_int, [C.c_size_t, C.c_size_t, C.c_double, C.c_double, C.c_double, C.c_double, C.c_uint64, C.POINTER(_P)]),

@@ -5,7 +5,6 @@
 // Valid non-guard slots are its edges in ascending destination order, the
 // interval also holds gaps, tombstones and the row's guard (graph.hpp:100-114).
 // The analytics read keys+states (9 B/slot) and, for SpMV, values (17 B/slot).
-#include <cub/device/device_radix_sort.cuh>
 
 #include <cmath>
 #include <cstring>
@@ -359,12 +358,13 @@ Graph::Graph(const gpma_graph_config* cfg, int device, u64 nv_, u64 lo_, u64 hi_
     pma.ro_lo = lo;
 }
 
-static void sort_pairs(cudaStream_t s, DevBuf<unsigned char>& tmpb, u64* kin, u64* kout, u32* vin, u32* vout, u64 n,
-                       int nbits) {
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, int(n), 0, nbits, s);
-    tmpb.reserve(tmp);
-    GPMA_CUDA(cub::DeviceRadixSort::SortPairs(tmpb.ptr, tmp, kin, kout, vin, vout, int(n), 0, nbits, s));
+// stable (key, arrival index) sort of the edge keys by key bits [0, nbits):
+// the result pair of buffers (kin/vin or kout/vout)
+static std::pair<const u64*, const u32*> sort_pairs(cudaStream_t s, RadixWorkspace& ws, u64* kin, u64* kout, u32* vin,
+                                                    u32* vout, u64 n, int nbits) {
+    const int alt = radix_sort(s, ws, kin, kout, vin, vout, n, 0, nbits);
+    using R = std::pair<const u64*, const u32*>;
+    return alt ? R(kout, vout) : R(kin, vin);
 }
 
 static int bits_for(u64 v) {
@@ -395,7 +395,6 @@ void Graph::from_edges_device(const u32* d_src, const u32* d_dst, const double* 
     }
     DevBuf<u64> k0, k1, uk, uvv, mk, mv;
     DevBuf<u32> i0, i1;
-    DevBuf<unsigned char> tmp;
     k0.reserve(n + 1);
     k1.reserve(n + 1);
     i0.reserve(n + 1);
@@ -412,10 +411,10 @@ void Graph::from_edges_device(const u32* d_src, const u32* d_dst, const double* 
             k_pack_edges<<<grid_for(n, 256), 256, 0, s>>>(d_src, d_dst, n, k0.ptr, i0.ptr);
         }
         GPMA_LAUNCH_CHECK();
-        sort_pairs(s, tmp, k0.ptr, k1.ptr, i0.ptr, i1.ptr, n, nbits);
+        const auto sorted = sort_pairs(s, pma.rws, k0.ptr, k1.ptr, i0.ptr, i1.ptr, n, nbits);
         // dedupe, last arrival wins (stable sort keeps arrival order)
-        const u64* sk = k1.ptr;
-        const u32* si = i1.ptr;
+        const u64* sk = sorted.first;
+        const u32* si = sorted.second;
         u64* ok_ = uk.ptr;
         u64* ov_ = uvv.ptr;
         Ctr* c = ctr;

@@ -16,8 +16,6 @@
 //      root path with grow / forced merge / eager shrink on device-wide
 //      kernels (segment_engine.hpp:435-463, pma.hpp:390-402, 597-601)
 //   5. refresh of leaf headers (+ row offsets for graphs) over touched ranges.
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <cmath>
@@ -1832,10 +1830,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     const u32* sorted_ci = si_in.ptr;
     if (bucket) {
         const u64 L = num_leaves();
-        size_t tmp = 0;
-        cub::DeviceScan::ExclusiveSum(nullptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_);
-        sort_tmp.reserve(tmp);
-        GPMA_CUDA(cub::DeviceScan::ExclusiveSum(sort_tmp.ptr, tmp, bcnt.ptr, boff.ptr, int(L + 2), stream_));
+        exclusive_sum(stream_, ws, bcnt.ptr, boff.ptr, L + 2);
         const bool pairs = packed_ib == 0;
         static const unsigned scat_res = resident_grid(k_bucket_scatter, 256);
         static const unsigned sort_res = resident_grid(k_bucket_sort_small, 256);
@@ -1851,24 +1846,15 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         GPMA_LAUNCH_CHECK();
         launches += 5;
     } else if (packed_ib && n > 1) {
-        size_t tmp = 0;
-        cub::DeviceRadixSort::SortKeys(nullptr, tmp, sk_in.ptr, sk_out.ptr, int(n), packed_ib, packed_ib + nbits,
-                                       stream_);
-        sort_tmp.reserve(tmp);
-        GPMA_CUDA(cub::DeviceRadixSort::SortKeys(sort_tmp.ptr, tmp, sk_in.ptr, sk_out.ptr, int(n), packed_ib,
-                                                 packed_ib + nbits, stream_));
-        launches += (nbits + 7) / 8 + 1;
-        sorted_ck = sk_out.ptr;
+        // keys-only: the arrival index rides in the low bits below the key
+        const int alt = radix_sort(stream_, rws, sk_in.ptr, sk_out.ptr, nullptr, nullptr, n, packed_ib,
+                                   packed_ib + nbits, &launches);
+        sorted_ck = alt ? sk_out.ptr : sk_in.ptr;
     } else if (nbits > 0 && n > 1) {
-        size_t tmp = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr, int(n), 0, nbits,
-                                        stream_);
-        sort_tmp.reserve(tmp);
-        GPMA_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.ptr, tmp, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr,
-                                                  int(n), 0, nbits, stream_));
-        launches += (nbits + 7) / 8 + 1;
-        sorted_ck = sk_out.ptr;
-        sorted_ci = si_out.ptr;
+        const int alt = radix_sort(stream_, rws, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr, n, 0, nbits,
+                                   &launches);
+        sorted_ck = alt ? sk_out.ptr : sk_in.ptr;
+        sorted_ci = alt ? si_out.ptr : si_in.ptr;
     }
     // ---- 2+3. resolve duplicates (run ends -> unique updates) fused with the
     // leaf assignment of each unique key (computed once per batch) ----

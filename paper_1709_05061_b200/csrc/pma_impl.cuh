@@ -16,7 +16,7 @@
 #include <vector>
 
 #include "common.cuh"
-#include "scan.cuh"
+#include "radix.cuh"
 
 namespace gpma {
 
@@ -236,7 +236,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     // batch scratch
     DevBuf<u64> sk_in, sk_out;   // compressed keys
     DevBuf<u32> si_in, si_out;   // arrival index payload
-    DevBuf<unsigned char> sort_tmp;
+    RadixWorkspace rws;           // onesweep radix sort (radix.cuh)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
     // update bucket + ordinal, per sorted position bucket
     DevBuf<u32> bcnt, boff, blf, bod, bslf, bbig;

@@ -5,7 +5,7 @@
 // sorted, duplicates resolved (last insert wins), merged into the edge list
 // (matches removed, inserts added) and the whole CSR rebuilt.  Its cost is
 // O(|E|) per batch whatever the batch size — the point of the comparison.
-#include <cub/device/device_radix_sort.cuh>
+#include "radix.cuh"
 
 #include <chrono>
 #include <cstring>
@@ -222,12 +222,9 @@ public:
         }
         k_rb_pack<<<grid_for(n, 256, 148 * 8), 256, 0, s>>>(is, id, iw, ni, ds, dd, nd, k0.ptr, i0.ptr);
         GPMA_LAUNCH_CHECK();
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.ptr, k1.ptr, i0.ptr, i1.ptr, int(n), 0, 64, s);
-        tmp.reserve(tb);
-        GPMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, k0.ptr, k1.ptr, i0.ptr, i1.ptr, int(n), 0, 64, s));
-        const u64* k = k1.ptr;
-        const u32* ix = i1.ptr;
+        const int alt = radix_sort(s, rws, k0.ptr, k1.ptr, i0.ptr, i1.ptr, n, 0, 64);
+        const u64* k = alt ? k1.ptr : k0.ptr;
+        const u32* ix = alt ? i1.ptr : i0.ptr;
         u64* ok = uk.ptr;
         u64* ov = uv.ptr;
         u8* oo = uop.ptr;
@@ -281,7 +278,7 @@ public:
     DevBuf<u32> i0, i1, col;
     DevBuf<double> val;
     DevBuf<u8> uop, gone;
-    DevBuf<unsigned char> tmp;
+    RadixWorkspace rws;
     DevBuf<u32> sa, sb, sc, sd;
     DevBuf<double> sw;
     ScanWorkspace ws;

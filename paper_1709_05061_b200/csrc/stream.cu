@@ -12,7 +12,7 @@
 // next_occurrence(p) >= cursor + take.  With next_occurrence precomputed once
 // by a stable sort of (key, position), every slide is one ordered compaction
 // — no hash map, and the emitted batches are byte-identical to the reference.
-#include <cub/device/device_radix_sort.cuh>
+#include "radix.cuh"
 
 #include <cmath>
 #include <cstring>
@@ -418,32 +418,31 @@ int gpma_window_create(const gpma_stream* s, int device, gpma_window** out) {
         {
             gpma::DevBuf<gpma::u64> k0, k1;
             gpma::DevBuf<gpma::u32> p0, p1;
-            gpma::DevBuf<unsigned char> tmp;
+            gpma::RadixWorkspace rws;
             k0.reserve(n);
             k1.reserve(n);
             p0.reserve(n);
             p1.reserve(n);
             gpma::k_pack_stream<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(W.src.ptr, W.dst.ptr, n, k0.ptr, p0.ptr);
             GPMA_LAUNCH_CHECK();
-            size_t tb = 0;
-            cub::DeviceRadixSort::SortPairs(nullptr, tb, k0.ptr, k1.ptr, p0.ptr, p1.ptr, int(n), 0, 64, W.stream);
-            tmp.reserve(tb);
-            GPMA_CUDA(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, k0.ptr, k1.ptr, p0.ptr, p1.ptr, int(n), 0, 64,
-                                                      W.stream));
-            gpma::k_next_occ<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(k1.ptr, p1.ptr, n, W.next.ptr);
+            const int alt = gpma::radix_sort(W.stream, rws, k0.ptr, k1.ptr, p0.ptr, p1.ptr, n, 0, 64);
+            const gpma::u64* ks = alt ? k1.ptr : k0.ptr;  // sorted keys
+            const gpma::u32* ps = alt ? p1.ptr : p0.ptr;  // their stream positions
+            gpma::u32* pfree = alt ? p0.ptr : p1.ptr;     // the other payload buffer
+            gpma::k_next_occ<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(ks, ps, n, W.next.ptr);
             GPMA_LAUNCH_CHECK();
             // dense key ids (general mode's multiplicity index): the rank of
             // the distinct key in the sorted order
             W.kid.reserve(n);
             {
-                const gpma::u64* sk = k1.ptr;
-                gpma::u32* sid = p0.ptr;  // reused: per sorted index
+                const gpma::u64* sk = ks;
+                gpma::u32* sid = pfree;  // reused: per sorted index
                 gpma::run_compact(
                     W.stream, W.ws, nullptr, n, n,
                     [=] __device__(gpma::ull i) { return i == 0 || sk[i] != sk[i - 1]; },
                     [=] __device__(gpma::ull i, unsigned f, gpma::ull x) { sid[i] = gpma::u32(x + f - 1); },
                     gpma::NoFin{});
-                gpma::k_key_ids<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(p1.ptr, sid, n, W.kid.ptr);
+                gpma::k_key_ids<<<gpma::grid_for(n, 256), 256, 0, W.stream>>>(ps, sid, n, W.kid.ptr);
                 GPMA_LAUNCH_CHECK();
             }
             GPMA_CUDA(cudaStreamSynchronize(W.stream));

@@ -712,3 +712,39 @@ class SlidingWindow:
 __all__ = ["EdgeStream", "SlidingWindow", "Mt19937_64", "draw_below_sequence", "PackedMemoryArray", "DynamicGraph", "DensityProfile", "UpdateStats", "SegmentEngineConfig",
            "GraphConfig", "PageRankResult", "batch_update", "bfs", "connected_components", "pagerank", "spmv",
            "LogicError", "kUnreached", "kMinCapacity", "PMA_LAZY", "PMA_EAGER"]
+
+
+# -- data-parallel primitives (primitives.hpp:21-84) on the device ----------
+
+def _prim_check(lib, rc):
+    if rc:
+        _raise(rc, lib.gpma_primitives_last_error().decode())
+
+
+def sort_by_key(keys, payload=None, begin_bit: int = 0, end_bit: int = 64, device: int = 0):
+    """sort_by_key / sort_pairs_by_key (primitives.hpp:21-60): stable sort of
+    64-bit keys by bits [begin_bit, end_bit), a u32 payload moving with its
+    key.  Returns sorted copies (keys, payload or None)."""
+    lib = load_library()
+    k = np.array(keys, dtype=np.uint64, copy=True)
+    p = None if payload is None else np.array(payload, dtype=np.uint32, copy=True)
+    if p is not None and len(p) != len(k):
+        raise ValueError("sort_by_key: payload size mismatch")
+    _prim_check(lib, lib.gpma_sort_by_key(device, _p(k), _p(p) if p is not None else None, len(k), begin_bit,
+                                          end_bit))
+    return k, p
+
+
+def sort_by_key_device(d_keys: int, d_payload: int | None, n: int, begin_bit: int = 0, end_bit: int = 64,
+                       device: int = 0):
+    """The same on device arrays (sorted in place)."""
+    lib = load_library()
+    _prim_check(lib, lib.gpma_sort_by_key_device(device, C.c_void_p(d_keys),
+                                                 C.c_void_p(d_payload) if d_payload else None, n, begin_bit,
+                                                 end_bit))
+
+
+def exclusive_scan_device(d_in: int, d_out: int, n: int, device: int = 0):
+    """exclusive_scan (primitives.hpp:74-84) of n u32 device values."""
+    lib = load_library()
+    _prim_check(lib, lib.gpma_exclusive_scan_device(device, C.c_void_p(d_in), C.c_void_p(d_out), n))
