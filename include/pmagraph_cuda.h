@@ -180,6 +180,14 @@ int pma_batch_update_device(pma_handle* h, const uint64_t* d_keys, const uint64_
  * `pairs` (2*cap entries); *count receives the total number of ranges. */
 int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count);
 
+/* Parity digest of slots() (pma.hpp:214) without downloading it: one u64 per
+ * segment of `level` (capacity / (leaf_size << level) values), the wrapping
+ * sum over the segment's slots i of mix(key + mix(value ^ (i * 0x9E3779B97F4A7C15
+ * + state))), mix = the splitmix64 finaliser.  Pins keys, values, states and
+ * gap positions; tests/golden/hashing.py computes the same from a host copy.
+ * PMA_ERANGE when level > height. */
+int pma_slot_hash(pma_handle* h, int level, uint64_t* hashes);
+
 /* binary_search_leaf for n keys (pma.hpp:234-245); any order. */
 int pma_binary_search_leaf(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* leaves);
 

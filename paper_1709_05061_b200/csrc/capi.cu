@@ -186,6 +186,14 @@ int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count
     });
 }
 
+int pma_slot_hash(pma_handle* h, int level, uint64_t* hashes) {
+    return guarded(err_of(h), [&] {
+        if (!hashes) throw ApiError(PMA_EINVAL, "pma_slot_hash: hashes is NULL");
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->slot_hash(level, hashes);
+    });
+}
+
 int pma_binary_search_leaf(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* leaves) {
     return guarded(err_of(h), [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));

@@ -1578,6 +1578,31 @@ __global__ void k_count_valid(const u8* __restrict__ st, u64 b, u64 e, Ctr* ctr)
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(&ctr->nv, c);
 }
 
+// Parity digest of the slot array (tests/golden/hashing.py restates it in
+// numpy): slot i contributes mix(key + mix(value ^ (i * phi + state))) and a
+// chunk's hash is the wrapping sum over its slots, so keys, values, states
+// and gap positions are all pinned without downloading the array.
+__device__ __forceinline__ u64 mix64(u64 x) {
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__global__ void k_slot_hash(const u64* __restrict__ keys, const u64* __restrict__ vals, const u8* __restrict__ st,
+                            u64 cap, int chunk_log2, ull* out) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < cap; i += u64(gridDim.x) * blockDim.x) {
+        const u64 a = i * 0x9E3779B97F4A7C15ull + st[i];
+        ull h = mix64(keys[i] + mix64(vals[i] ^ a));
+        if (chunk_log2 >= 5) {  // a warp's 32 consecutive slots share one chunk
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) h += __shfl_xor_sync(FULL, h, d);
+            if ((threadIdx.x & 31) == 0) atomicAdd(&out[i >> chunk_log2], h);
+        } else {
+            atomicAdd(&out[i >> chunk_log2], h);
+        }
+    }
+}
+
 // ========================================================== host pipeline
 
 void Pma::headers_closed_form(const u64* d_ek, u64 k) {
@@ -2423,6 +2448,21 @@ void Pma::search(const u64* keys, size_t n, u64* values, u8* found) {
     GPMA_LAUNCH_CHECK();
     GPMA_CUDA(cudaMemcpyAsync(values, stage_v.ptr, n * 8, cudaMemcpyDeviceToHost, stream_));
     GPMA_CUDA(cudaMemcpyAsync(found, stage_o.ptr, n, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Pma::slot_hash(int level, u64* hashes) {
+    if (level < 0 || level > height_) throw ApiError(PMA_ERANGE, "slot_hash: level out of range");
+    int lg = 0;
+    while ((u64(1) << lg) < (leaf_ << level)) ++lg;
+    const u64 nh = cap_ >> lg;
+    DevBuf<ull> out;
+    out.reserve(nh);
+    GPMA_CUDA(cudaMemsetAsync(out.ptr, 0, nh * sizeof(ull), stream_));
+    // cap_ is a power of two >= 16: whole warps stay inside the array
+    k_slot_hash<<<grid_for(cap_, 256, 148 * 8), 256, 0, stream_>>>(d_keys, d_vals, d_st, cap_, lg, out.ptr);
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaMemcpyAsync(hashes, out.ptr, nh * 8, cudaMemcpyDeviceToHost, stream_));
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 

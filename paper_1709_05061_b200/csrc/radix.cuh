@@ -107,7 +107,8 @@ __device__ __forceinline__ void radix_rank_tile(const u64 (&k)[kRadixIpt], u32 w
     }
     *count = run;
     u32 total;
-    s_start[t] = block_excl_scan(run, &total, s_w);  // syncs inside
+    s_start[t] = block_excl_scan(run, &total, s_w);
+    __syncthreads();  // every digit's start visible before the positions read them
 #pragma unroll
     for (int i = 0; i < kRadixIpt; ++i) {
         const u32 d = item_digit(k, i, wvalid, shift, mask);

@@ -233,6 +233,13 @@ class PackedMemoryArray:
         self._check(self._lib.pma_bounds(self.h, level, None, None, C.byref(rho), C.byref(tau)))
         return rho.value, tau.value
 
+    def slot_hash(self, level: int):
+        """Per-segment parity digest of slots() at `level` (pma_slot_hash)."""
+        n = self.capacity() // (self.leaf_size() << level) if 0 <= level <= self.height() else 1
+        out = np.zeros(max(n, 1), np.uint64)
+        self._check(self._lib.pma_slot_hash(self.h, level, _p(out)))
+        return out[:n]
+
     def binary_search_leaf(self, keys):
         scalar = np.isscalar(keys)
         k = _u64(np.atleast_1d(keys))
