@@ -398,11 +398,11 @@ def run_ours(args):
 
     def on_e2e(graph, s, timed):
         a, b, c, d, _ = host_by_slide[id(s)]
-        st = graph.apply_batch(a, b, None, c, d, with_touched=True)
+        st = graph.apply_batch(a, b, None, c, d, with_touched="array")
         if timed:
             e2e_steps.append((st, graph.last_timing()))
             io["h2d"] += a.nbytes + b.nbytes + c.nbytes + d.nbytes
-            io["d2h"] += PMA_STATS_BYTES + 16 * len(st.touched_ranges)
+            io["d2h"] += PMA_STATS_BYTES + 8 * len(st.touched_ranges)  # one sortable word per range
 
     g2, e2e_ms, _ = run_passes(make_graph(), make_graph, slides, P, W, K, on_e2e, dev, world, None)
     e2e_stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
@@ -455,6 +455,7 @@ def run_ours(args):
                 "scatter_bytes_per_step": BYTES_PER_MERGE_SLOT * merge_slots // K,
                 "commit_ms_per_step_all_levels": seg_ms / K, "step_ms": ms / K,
                 "stage_ms_per_step": {k: v / K for k, v in stage.items()},
+                "device_ms_each_step": [round(tm.device_ms, 4) for _, tm in per_step],
                 "commit_ms_per_level": [round(x / K, 4) for x in level_ms if x > 0],
                 "groups_per_level": [x / K for x in level_groups if x > 0],
                 "hub_groups_per_level": [x / K for x, g in zip(level_big, level_groups) if g > 0],

@@ -307,14 +307,20 @@ int gpma_shard_range(const gpma_graph* g, uint64_t* lo, uint64_t* hi);
  * d_bounds[r+1], world + 1 entries, world <= 64; ids >= |V| go to the last
  * rank) into EdgeKeys d_out_keys (owner-major, arrival order kept inside each
  * owner; bit 63 set on deletes, so |V| <= 2^31), with the insert weights in
- * d_out_w (NULL: none; deletes get 1.0); counts[r] (host) = updates for rank
- * r.  One all-to-all of these words (8 B / update) is the whole exchange. */
+ * d_out_w (NULL: none; deletes get 1.0); counts[r] (host, world + 1 entries)
+ * = updates for rank r, and counts[world] = inserts naming a vertex >= |V|:
+ * when any sender reports one, every rank must reject the batch before any
+ * shard applies (check_ids throws invalid_argument before any mutation,
+ * graph.hpp:133-137).  A delete naming a vertex >= |V| travels as a key no
+ * graph holds, so it is counted missed (graph.hpp:140-145) and never aliases
+ * a real edge through the delete bit.  One all-to-all of these words
+ * (8 B / update) is the whole exchange. */
 int gpma_route_batch(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
                      size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
                      const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w, uint64_t* counts);
 
 /* As gpma_route_batch, but the per-rank counts go to device memory d_counts
- * (world u64) and nothing is synchronised: with gpma_set_stream on the
+ * (world + 1 u64, as above) and nothing is synchronised: with gpma_set_stream on the
  * caller's stream, routing, the NCCL exchange and the apply are
  * stream-ordered without host round trips. */
 int gpma_route_batch_async(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
@@ -371,7 +377,8 @@ int gpma_warmup(int device);
 
 /* ---- Fused routing (partition + transfer in one kernel over peer memory)
  * Instead of gpma_route_batch + an all-to-all: (1) gpma_route_count counts
- * this rank's slice per owner (d_counts[world], stream-ordered); (2) the
+ * this rank's slice per owner (d_counts[world + 1], [world] = inserts naming
+ * a vertex >= |V| as in gpma_route_batch; stream-ordered); (2) the
  * caller exchanges the counts (world x world) and derives, for every owner r,
  * this sender's first slot in r's receive buffer (the sum of the counts of
  * the lower senders for r) and the size of its own receive batch; (3)

@@ -703,7 +703,7 @@ extern "C" int gpma_warmup(int device) {
             gpma_graph* sg = nullptr;
             if (gpma_shard_from_edges_device(nullptr, device, nv, 0, uint32_t(nv / 2), ds_, dd_, nullptr, ne, &sg))
                 throw ApiError(PMA_ECUDA, gpma_last_error(nullptr));
-            uint64_t cnt[2] = {0, 0};
+            uint64_t cnt[3] = {0, 0, 0};
             gpma_route_batch(sg, ds_, dd_, nullptr, 300, ds_ + 300, dd_ + 300, 300, db_, 2, dk_, nullptr, cnt);
             gpma_apply_batch_routed_device(sg, dk_, nullptr, cnt[0], &st);
             uint32_t nf = 0;

@@ -2406,24 +2406,42 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     if (out) *out = st;
 }
 
+// touched range (b, e) -> one sortable word: (log2(e - b) << 40) | b.  Every
+// range is a whole segment (power-of-two size <= 2^31, aligned), so the word
+// orders ranges by size then begin — the reference's order (rounds in level
+// order, segments ascending inside a round) — and decodes back exactly.
+__global__ void k_touched_words(const u64* __restrict__ pairs, u64 n, u64* __restrict__ words) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const u64 b = pairs[2 * i], e = pairs[2 * i + 1];
+        words[i] = (u64(63 - __clzll(e - b)) << 40) | b;
+    }
+}
+
 void Pma::touched_ranges(u64* pairs, size_t capn, size_t* count) {
     *count = last_ntouched;
     const size_t n = std::min<size_t>(capn, last_ntouched);
-    if (n && pairs) {
-        // the commit kernels append in any order: restore the reference's
-        // (rounds in level order, segments ascending inside a round; a level's
-        // ranges all have the same size, larger at each level)
-        std::vector<std::pair<u64, u64>> all(last_ntouched);
-        GPMA_CUDA(cudaMemcpyAsync(all.data(), touched.ptr, last_ntouched * 16, cudaMemcpyDeviceToHost, stream_));
-        GPMA_CUDA(cudaStreamSynchronize(stream_));
-        std::sort(all.begin(), all.end(), [](const std::pair<u64, u64>& x, const std::pair<u64, u64>& y) {
-            const u64 sx = x.second - x.first, sy = y.second - y.first;
-            return sx != sy ? sx < sy : x.first < y.first;
-        });
-        for (size_t i = 0; i < n; ++i) {
-            pairs[2 * i] = all[i].first;
-            pairs[2 * i + 1] = all[i].second;
-        }
+    if (!n || !pairs) return;
+    // the commit kernels append in any order: put them in the reference's
+    // order on the device (one keys-only radix sort of 45-bit words), bring
+    // back 8 B per range and expand on the host
+    const u64 m = last_ntouched;
+    tw0.reserve(m);
+    tw1.reserve(m);
+    k_touched_words<<<grid_for(m, 256, 148 * 8), 256, 0, stream_>>>(touched.ptr, m, tw0.ptr);
+    GPMA_LAUNCH_CHECK();
+    const int alt = radix_sort(stream_, rws, tw0.ptr, tw1.ptr, nullptr, nullptr, m, 0, 45);
+    const u64* sorted = alt ? tw1.ptr : tw0.ptr;
+    // words into the upper half of the caller's array, expanded in place from
+    // the front (pair i is written at 2i, 2i+1 < n + i + 1: never over an
+    // unread word)
+    u64* w = pairs + n;
+    GPMA_CUDA(cudaMemcpyAsync(w, sorted, n * 8, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    for (size_t i = 0; i < n; ++i) {
+        const u64 x = w[i];
+        const u64 b = x & ((1ull << 40) - 1);
+        pairs[2 * i] = b;
+        pairs[2 * i + 1] = b + (1ull << (x >> 40));
     }
 }
 

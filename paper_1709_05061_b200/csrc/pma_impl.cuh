@@ -253,6 +253,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u32> biglist;  // leaf groups with > kBigSlice updates (lane-parallel kernel)
     DevBuf<u8> gflag;
     DevBuf<u64> touched;  // pairs (b, e)
+    DevBuf<u64> tw0, tw1;  // touched ranges as sortable words (touched_ranges)
     DevBuf<u64> ik, iv;   // insert lists (pending space)
     DevBuf<u32> ir;
     // slot-space merge scratch (CTA/grid tiers, root path)

@@ -34,11 +34,23 @@ struct RouteIn {
     const u32* ds;
     const u32* dd;
     u64 nd;
+    u32 nv;  // |V| <= 2^31
     __device__ __forceinline__ u32 src(u64 i) const { return i < ni ? is[i] : ds[i - ni]; }
-    // EdgeKey on the wire; bit 63 marks a delete (ids < 2^31)
+    // An insert naming a vertex >= |V| rejects the whole batch (check_ids,
+    // graph.hpp:133-137, before any mutation): counted by the senders, the
+    // caller rejects the batch on every rank before any shard applies.
+    __device__ __forceinline__ bool bad_insert(u64 i) const { return i < ni && (is[i] >= nv || id[i] >= nv); }
+    // EdgeKey on the wire; bit 63 marks a delete.  A delete naming a vertex
+    // >= |V| can never match (graph.hpp:140-145 counts it missed); it travels
+    // as kAbsentDelete, whose ids no graph holds (dst 2^32-2 >= |V|), so an id
+    // in [2^31, 2^32) never aliases a real edge through the delete bit.
     __device__ __forceinline__ u64 key(u64 i) const {
-        return i < ni ? pack_edge(is[i], id[i]) : (pack_edge(ds[i - ni], dd[i - ni]) | (1ull << 63));
+        if (i < ni) return pack_edge(is[i], id[i]);
+        const u32 s_ = ds[i - ni], d_ = dd[i - ni];
+        if (s_ >= nv || d_ >= nv) return kAbsentDelete;
+        return pack_edge(s_, d_) | (1ull << 63);
     }
+    static constexpr u64 kAbsentDelete = (0x7FFFFFFFull << 32 | 0xFFFFFFFEull) | (1ull << 63);
 };
 
 __device__ __forceinline__ int owner_of(u32 s, const u32* __restrict__ b, int world) {
@@ -51,7 +63,8 @@ __device__ __forceinline__ int owner_of(u32 s, const u32* __restrict__ b, int wo
     return lo;
 }
 
-__global__ void k_route_hist(RouteIn in, const u32* __restrict__ bounds, int world, u32* __restrict__ tile_counts) {
+__global__ void k_route_hist(RouteIn in, const u32* __restrict__ bounds, int world, u32* __restrict__ tile_counts,
+                             u64* __restrict__ bad) {
     const u64 n = in.ni + in.nd;
     __shared__ u32 s_b[kMaxWorld + 1];
     __shared__ u32 s_c[kMaxWorld];
@@ -59,9 +72,17 @@ __global__ void k_route_hist(RouteIn in, const u32* __restrict__ bounds, int wor
     for (int i = threadIdx.x; i < world; i += blockDim.x) s_c[i] = 0;
     __syncthreads();
     const u64 base = u64(blockIdx.x) * kRouteTile;
+    unsigned nbad = 0;
     for (int j = 0; j < kRouteItems; ++j) {
         const u64 i = base + u64(j) * kRouteThreads + threadIdx.x;
-        if (i < n) atomicAdd(&s_c[owner_of(in.src(i), s_b, world)], 1u);
+        if (i < n) {
+            atomicAdd(&s_c[owner_of(in.src(i), s_b, world)], 1u);
+            nbad += in.bad_insert(i);
+        }
+    }
+    if (__any_sync(FULL, nbad != 0)) {
+        for (int d = 16; d > 0; d >>= 1) nbad += __shfl_xor_sync(FULL, nbad, d);
+        if ((threadIdx.x & 31u) == 0 && nbad) atomicAdd(reinterpret_cast<ull*>(bad), ull(nbad));
     }
     __syncthreads();
     for (int r = threadIdx.x; r < world; r += blockDim.x) tile_counts[u64(r) * gridDim.x + blockIdx.x] = s_c[r];
@@ -278,21 +299,23 @@ void Graph::route_partition(const u32* is, const u32* id, const double* iw, u64 
     if (world < 1 || world > kMaxWorld) throw ApiError(PMA_EINVAL, "route: world size must be in [1, 64]");
     if (nv > (1ull << 31)) throw ApiError(PMA_EINVAL, "route: vertex ids must be < 2^31 (bit 63 marks deletes)");
     cudaStream_t s = pma.stream();
-    const RouteIn in{is, id, iw, ni, ds, dd, nd};
+    const RouteIn in{is, id, iw, ni, ds, dd, nd, u32(nv)};
     const u64 n = ni + nd;
+    // counts: world owners + [world] = inserts naming a vertex >= |V|
     if (n == 0) {
         if (h_counts)
-            for (int r = 0; r < world; ++r) h_counts[r] = 0;
-        if (d_counts) GPMA_CUDA(cudaMemsetAsync(d_counts, 0, world * sizeof(u64), s));
+            for (int r = 0; r <= world; ++r) h_counts[r] = 0;
+        if (d_counts) GPMA_CUDA(cudaMemsetAsync(d_counts, 0, (world + 1) * sizeof(u64), s));
         return;
     }
     const u64 ntiles = (n + kRouteTile - 1) / kRouteTile;
     rt_counts.reserve(ntiles * world);
     rt_offsets.reserve(ntiles * world);
-    rt_totals.reserve(world);
-    k_route_hist<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_counts.ptr);
-    GPMA_LAUNCH_CHECK();
+    rt_totals.reserve(world + 1);
     u64* totals = d_counts ? d_counts : rt_totals.ptr;
+    GPMA_CUDA(cudaMemsetAsync(totals + world, 0, sizeof(u64), s));
+    k_route_hist<<<unsigned(ntiles), kRouteThreads, 0, s>>>(in, d_bounds, world, rt_counts.ptr, totals + world);
+    GPMA_LAUNCH_CHECK();
     k_route_scan<<<1, 1024, 0, s>>>(rt_counts.ptr, ntiles, world, rt_offsets.ptr, totals);
     GPMA_LAUNCH_CHECK();
     if (okeys) {
@@ -302,7 +325,7 @@ void Graph::route_partition(const u32* is, const u32* id, const double* iw, u64 
     }
     rt_ntiles = ntiles;
     if (h_counts) {  // host counts: one round trip; device counts: stream-ordered, no sync
-        GPMA_CUDA(cudaMemcpyAsync(h_counts, totals, world * sizeof(u64), cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaMemcpyAsync(h_counts, totals, (world + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
     }
 }
@@ -317,7 +340,7 @@ void Graph::route_scatter_peer(const u32* is, const u32* id, const double* iw, u
     if (n == 0) return;
     const u64 ntiles = (n + kRouteTile - 1) / kRouteTile;
     if (ntiles != rt_ntiles) throw ApiError(PMA_ELOGIC, "route_scatter_peer: slice differs from the counted one");
-    const RouteIn in{is, id, iw, ni, ds, dd, nd};
+    const RouteIn in{is, id, iw, ni, ds, dd, nd, u32(nv)};
     k_route_scatter<<<unsigned(ntiles), kRouteThreads, 0, pma.stream()>>>(
         in, d_bounds, world, rt_offsets.ptr, RouteDst{nullptr, nullptr, dst_keys, dst_w, dst_off});
     GPMA_LAUNCH_CHECK();

@@ -289,12 +289,21 @@ class PackedMemoryArray:
         k, v = _u64(keys), _u64(values if len(values) else np.zeros(len(keys), np.uint64))
         self._check(self._lib.pma_redispatch(self.h, level, seg_index, _p(k), _p(v), len(k)))
 
+    def touched_ranges_array(self, n: int | None = None):
+        """UpdateStats::touched_ranges of the last batch as an (n, 2) u64 array
+        in the reference's order (n: the count from pma_stats, saves a call)."""
+        if n is None:
+            c = C.c_size_t(0)
+            self._check(self._lib.pma_touched_ranges(self.h, None, 0, C.byref(c)))
+            n = c.value
+        out = np.empty(2 * max(n, 1), np.uint64)
+        c = C.c_size_t(0)
+        self._check(self._lib.pma_touched_ranges(self.h, _p(out), n, C.byref(c)))
+        return out[:2 * n].reshape(n, 2)
+
     def touched_ranges(self):
-        n = C.c_size_t(0)
-        self._check(self._lib.pma_touched_ranges(self.h, None, 0, C.byref(n)))
-        out = np.zeros(2 * max(n.value, 1), np.uint64)
-        self._check(self._lib.pma_touched_ranges(self.h, _p(out), n.value, C.byref(n)))
-        return [(int(out[2 * i]), int(out[2 * i + 1])) for i in range(n.value)]
+        a = self.touched_ranges_array()
+        return [(int(x), int(y)) for x, y in a]
 
     def last_timing(self) -> pma_timing:
         t = pma_timing()
@@ -384,12 +393,17 @@ class DynamicGraph:
         return PackedMemoryArray(_handle=self._lib.gpma_pma(self.h), _owner=self)
 
     def apply_batch(self, ins_src, ins_dst, ins_w, del_src, del_dst, pool=None,
-                    with_touched: bool = True) -> UpdateStats:
+                    with_touched=True) -> UpdateStats:
+        """with_touched: True = touched_ranges as a list of pairs (the
+        reference's vector), "array" = an (n, 2) u64 array (same fetch, no
+        Python list), False = not fetched."""
         a, b, w = _u32(ins_src), _u32(ins_dst), _f64(ins_w)
         c, d = _u32(del_src), _u32(del_dst)
         st = pma_stats()
         self._check(self._lib.gpma_apply_batch(self.h, _p(a), _p(b), _p(w), len(a), _p(c), _p(d), len(c),
                                                C.byref(st)))
+        if with_touched == "array":
+            return UpdateStats.from_c(st, self.pma().touched_ranges_array(st.num_touched_ranges))
         return UpdateStats.from_c(st, self.pma().touched_ranges() if with_touched else None)
 
     def apply_batch_device(self, d_is: int, d_id: int, d_iw: int | None, ni: int, d_ds: int, d_dd: int,

@@ -183,6 +183,10 @@ class ShardedGraph:
         self.bounds = np.asarray(bounds, np.int64)
         self.h = handles
         self.devices = devices
+        if isinstance(comm, LocalComm) and len(set(devices)) > 1:
+            # its collectives combine the shards' tensors directly and the fused
+            # scatter stores into the others' buffers: one device only
+            raise ValueError("LocalComm shards must share one device (use TorchComm across GPUs)")
         self._lib = load_library()
         torch = _torch()
         self._dbounds = [torch.as_tensor(self.bounds.astype(np.uint32).view(np.int32), device=f"cuda:{d}")
@@ -244,7 +248,7 @@ class ShardedGraph:
         n = ni + nd
         keys = torch.empty(max(n, 1), dtype=torch.int64, device=a.device)
         ow = torch.empty(max(n, 1), dtype=torch.float64, device=a.device) if w is not None else None
-        counts = torch.empty(self.comm.world, dtype=torch.int64, device=a.device)
+        counts = torch.empty(self.comm.world + 1, dtype=torch.int64, device=a.device)
         if not self._ordered:
             _sync(a)
         self._check(i, self._lib.gpma_route_batch_async(self.h[i], _vp(a), _vp(b), _vp(w), ni, _vp(c), _vp(d), nd,
@@ -253,6 +257,24 @@ class ShardedGraph:
         if not self._ordered:  # the async route ran on the library's own stream
             torch.cuda.ExternalStream(self._lib.gpma_cuda_stream(self.h[i]), device=a.device).synchronize()
         return keys[:n], (ow[:n] if ow is not None else None), counts
+
+    def _reject_bad_inserts(self, slices, bad):
+        """bad[r] = inserts of sender r naming a vertex >= |V| (counted by the
+        routing kernels).  The reference rejects such a batch before any
+        mutation (check_ids, graph.hpp:133-137), so every rank raises here,
+        before any shard applies — never a half-applied batch or a rank left
+        waiting in the next collective."""
+        if not any(int(x) for x in bad):
+            return
+        for i, sl in enumerate(slices):
+            if int(bad[self.comm.ranks[i]]):
+                a = sl[0].cpu().numpy().view(np.uint32)
+                b = sl[1].cpu().numpy().view(np.uint32)
+                j = int(np.nonzero((a >= self.nv) | (b >= self.nv))[0][0])
+                raise ValueError(f"edge ({a[j]}, {b[j]}) outside vertex range {self.nv}")
+        r = next(r for r, x in enumerate(bad) if int(x))
+        raise ValueError(f"apply_batch rejected on every shard: rank {r} holds an insert outside vertex range "
+                         f"{self.nv}")
 
     # ---- fused routing: partition + transfer in one kernel (peer memory)
     def _free_rx(self):
@@ -327,7 +349,7 @@ class ShardedGraph:
         counts = []
         for i in range(L):
             a, b, w, c, d = slices[i]
-            cnt = torch.empty(W, dtype=torch.int64, device=a.device)
+            cnt = torch.empty(W + 1, dtype=torch.int64, device=a.device)
             if not self._ordered:
                 _sync(a)
             self._check(i, self._lib.gpma_route_count(self.h[i], _vp(a), _vp(b), a.numel(), _vp(c), _vp(d),
@@ -348,6 +370,8 @@ class ShardedGraph:
             parts = [torch.empty_like(cnt) for _ in range(W)]
             self.comm.dist.all_gather(parts, cnt, group=self.comm.group)
             M = torch.stack(parts).cpu().numpy()
+        self._reject_bad_inserts(slices, M[:, W])  # M[s][W]: sender s's inserts outside the vertex range
+        M = M[:, :W]
         before, nrecv = fused_offsets(M)
         rx = self._ensure_rx(int(nrecv.max()) if W else 0, weighted)
         for i in range(L):
@@ -398,13 +422,25 @@ class ShardedGraph:
         if self.routing == "fused":
             return self._apply_fused(slices)
         L = len(self.h)
-        ks, ws, cs = [], [], []
+        ks, ws, cs, bads = [], [], [], []
         for i in range(L):
             a, b, w, c, d = slices[i]
             k, ww, cnt = self._route(i, a, b, w, c, d)
             ks.append(k)
             ws.append(ww)
-            cs.append(cnt)
+            cs.append(cnt[:-1])
+            bads.append(cnt[-1:])
+        # one scalar all-reduce: every rank learns of a bad insert anywhere
+        # before any shard applies (or the all-to-all runs)
+        tot = [x.clone() for x in bads]
+        self.comm.all_reduce(tot, "sum")
+        if int(tot[0].item()):
+            bad = [0] * self.comm.world
+            for i in range(L):
+                bad[self.comm.ranks[i]] = int(bads[i].item())
+            if not any(bad):
+                bad[next(r for r in range(self.comm.world) if r not in self.comm.ranks)] = 1
+            self._reject_bad_inserts(slices, bad)
         rk, _, scl = self.comm.all_to_all_v(ks, cs)
         rw = self.comm.all_to_all_v(ws, scl)[0] if ws[0] is not None else [None] * L
         cs = scl
@@ -501,6 +537,8 @@ class ShardedGraph:
         n = self.nv
         if n == 0:
             raise ValueError("pagerank: empty vertex set")
+        if warm_start is not None and len(warm_start) != n:
+            raise ValueError("pagerank: warm start size mismatch")
         od, x, y = [], [], []
         for i in range(L):
             dev = f"cuda:{self.devices[i]}"

@@ -146,3 +146,47 @@ def test_route_partition_is_stable_and_exact():
         assert counts.cpu().tolist() == list(np.bincount(own, minlength=world))
         assert (keys.cpu().numpy().view(np.uint64) == exp).all()
         assert (ow.cpu().numpy() == wexp).all()
+
+
+@pytest.mark.parametrize("routing", ["all_to_all", "fused"])
+def test_sharded_bad_insert_rejected_everywhere(routing):
+    """An insert naming a vertex >= |V| on ONE sender rejects the whole batch
+    on every shard before any applies (check_ids, graph.hpp:133-137): no shard
+    is left half-updated."""
+    nv, world = 4096, 2
+    rng = np.random.default_rng(3)
+    s = rng.integers(0, nv, 5000).astype(np.uint32)
+    d = rng.integers(0, nv, 5000).astype(np.uint32)
+    bounds = np.array([0, nv // 2, nv], np.int64)
+    G = ShardedGraph.from_edges_device(LocalComm(world), nv, bounds,
+                                       [(_dev(s, "u32"), _dev(d, "u32"), None)] * world, routing=routing)
+    before = [G.shard_slots(r) for r in range(world)]
+    good = (_dev(np.array([1, 2], np.uint32), "u32"), _dev(np.array([3, 4], np.uint32), "u32"), None,
+            _dev(np.array([], np.uint32), "u32"), _dev(np.array([], np.uint32), "u32"))
+    bad = (_dev(np.array([nv - 1, 7], np.uint32), "u32"), _dev(np.array([5, nv + 3], np.uint32), "u32"), None,
+           _dev(np.array([], np.uint32), "u32"), _dev(np.array([], np.uint32), "u32"))
+    with pytest.raises(ValueError, match=f"edge \\(7, {nv + 3}\\) outside vertex range {nv}"):
+        G.apply_batch([good, bad])
+    for r in range(world):
+        assert all((x == y).all() for x, y in zip(G.shard_slots(r), before[r])), f"shard {r} changed"
+
+
+@pytest.mark.parametrize("routing", ["all_to_all", "fused"])
+def test_sharded_delete_high_id_never_aliases(routing):
+    """A delete whose source lies in [2^31, 2^32) must not remove the edge
+    (src - 2^31, dst) through the wire's delete bit: it is counted missed,
+    as the reference counts an absent delete (graph.hpp:140-145)."""
+    nv, world = 4096, 2
+    s = np.array([2050, 10, 3000], np.uint32)
+    d = np.array([7, 11, 12], np.uint32)
+    bounds = np.array([0, nv // 2, nv], np.int64)
+    G = ShardedGraph.from_edges_device(LocalComm(world), nv, bounds,
+                                       [(_dev(s, "u32"), _dev(d, "u32"), None)] * world, routing=routing)
+    before = [G.shard_slots(r) for r in range(world)]
+    empty = _dev(np.array([], np.uint32), "u32")
+    dels = (empty, empty, None, _dev(np.array([2 ** 31 + 2050, 5000], np.uint32), "u32"),
+            _dev(np.array([7, 1], np.uint32), "u32"))
+    res = G.apply_batch([dels, (empty, empty, None, empty, empty)])
+    assert sum(st.deletes_missed for st in res.stats) == 2
+    for r in range(world):
+        assert all((x == y).all() for x, y in zip(G.shard_slots(r), before[r])), f"shard {r} changed"
