@@ -323,8 +323,10 @@ def run_ours(args):
     info = win.info()
 
     def make_graph():
-        return pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size,
-                                                 device=dev)
+        gr = pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size,
+                                               device=dev)
+        gr.pma().reserve_batch(2 * B + 16)  # a slide = B inserts + <= B deletes: no allocation in a step
+        return gr
 
     t1 = time.time()
     g = make_graph()

@@ -180,6 +180,13 @@ int pma_batch_update_device(pma_handle* h, const uint64_t* d_keys, const uint64_
  * `pairs` (2*cap entries); *count receives the total number of ranges. */
 int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count);
 
+/* Size every per-batch buffer for batches of up to max_updates updates (and
+ * the slot-space scratch of the CTA/grid tiers) now, so that no device
+ * allocation lands inside a later batch_update / apply_batch (the
+ * std::vector::reserve of the batch pipeline; no reference counterpart,
+ * state unchanged).  Buffers only grow. */
+int pma_reserve_batch(pma_handle* h, size_t max_updates);
+
 /* Parity digest of slots() (pma.hpp:214) without downloading it: one u64 per
  * segment of `level` (capacity / (leaf_size << level) values), the wrapping
  * sum over the segment's slots i of mix(key + mix(value ^ (i * 0x9E3779B97F4A7C15

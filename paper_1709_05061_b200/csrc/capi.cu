@@ -186,6 +186,13 @@ int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count
     });
 }
 
+int pma_reserve_batch(pma_handle* h, size_t max_updates) {
+    return guarded(err_of(h), [&] {
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        h->impl->reserve_batch(max_updates);
+    });
+}
+
 int pma_slot_hash(pma_handle* h, int level, uint64_t* hashes) {
     return guarded(err_of(h), [&] {
         if (!hashes) throw ApiError(PMA_EINVAL, "pma_slot_hash: hashes is NULL");
@@ -618,6 +625,9 @@ extern "C" int gpma_warmup(int device) {
             std::vector<uint8_t> bo(60000, 0);
             for (size_t i = 0; i < bk.size(); ++i) bk[i] = 50000000ull + i;  // forces root growth
             pma_batch_update(h, bk.data(), bv.data(), bo.data(), bk.size(), &lazy, &st);
+            std::vector<uint64_t> tr(2 * st.num_touched_ranges + 2);
+            size_t c = 0;
+            pma_touched_ranges(h, tr.data(), st.num_touched_ranges, &c);  // touched-word sort + decode
         }
         {
             uint64_t q[4] = {1000, 2000, 5001, 77}, lv[4], vals[4];

@@ -2406,6 +2406,46 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     if (out) *out = st;
 }
 
+// Every per-batch buffer sized for batches of up to n updates (and the
+// slot-space scratch of the CTA/grid tiers), so no allocation lands inside
+// a later batch.  Buffers only grow; batch_update sizes them anyway.
+void Pma::reserve_batch(u64 n) {
+    if (n == 0) return;
+    sk_in.reserve(n);
+    sk_out.reserve(n);
+    si_in.reserve(n);
+    si_out.reserve(n);
+    const u64 L = num_leaves();
+    if (ro_base() && n >= kBucketMinBatch && L <= kBucketMaxLeaves) {
+        bcnt.reserve(L + 2);
+        boff.reserve(L + 2);
+        blf.reserve(n);
+        bod.reserve(n);
+        bslf.reserve(n);
+        bbig.reserve(n / (kSmallRun + 1) + 1);
+    }
+    uk.reserve(n + 4);
+    uv.reserve(n + 4);
+    uop.reserve(n + 32);
+    ul.reserve(n);
+    pidx0.reserve(n);
+    pidx1.reserve(n);
+    gid.reserve(n);
+    gstart.reserve(n + 1);
+    gseg.reserve(n + 1);
+    gflag.reserve(n);
+    touched.reserve(2 * n + 2);
+    tw0.reserve(n + 1);
+    tw1.reserve(n + 1);
+    rlist.reserve(2 * n + 4);
+    ik.reserve(n);
+    iv.reserve(n);
+    ir.reserve(n);
+    biglist.reserve(n + 1);
+    ensure_slot_scratch();
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+}
+
 // touched range (b, e) -> one sortable word: (log2(e - b) << 40) | b.  Every
 // range is a whole segment (power-of-two size <= 2^31, aligned), so the word
 // orders ranges by size then begin — the reference's order (rounds in level
@@ -2417,32 +2457,32 @@ __global__ void k_touched_words(const u64* __restrict__ pairs, u64 n, u64* __res
     }
 }
 
+__global__ void k_touched_pairs(const u64* __restrict__ words, u64 n, u64* __restrict__ pairs) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        const u64 x = words[i];
+        const u64 b = x & ((1ull << 40) - 1);
+        reinterpret_cast<ulonglong2*>(pairs)[i] = make_ulonglong2(b, b + (1ull << (x >> 40)));
+    }
+}
+
 void Pma::touched_ranges(u64* pairs, size_t capn, size_t* count) {
     *count = last_ntouched;
     const size_t n = std::min<size_t>(capn, last_ntouched);
     if (!n || !pairs) return;
     // the commit kernels append in any order: put them in the reference's
-    // order on the device (one keys-only radix sort of 45-bit words), bring
-    // back 8 B per range and expand on the host
+    // order on the device (one keys-only radix sort of 45-bit words)
     const u64 m = last_ntouched;
     tw0.reserve(m);
     tw1.reserve(m);
     k_touched_words<<<grid_for(m, 256, 148 * 8), 256, 0, stream_>>>(touched.ptr, m, tw0.ptr);
     GPMA_LAUNCH_CHECK();
     const int alt = radix_sort(stream_, rws, tw0.ptr, tw1.ptr, nullptr, nullptr, m, 0, 45);
-    const u64* sorted = alt ? tw1.ptr : tw0.ptr;
-    // words into the upper half of the caller's array, expanded in place from
-    // the front (pair i is written at 2i, 2i+1 < n + i + 1: never over an
-    // unread word)
-    u64* w = pairs + n;
-    GPMA_CUDA(cudaMemcpyAsync(w, sorted, n * 8, cudaMemcpyDeviceToHost, stream_));
+    // decoded back into (b, e) pairs on the device (the commit list is free
+    // again) and copied straight into the caller's array (page-locked: DMA)
+    k_touched_pairs<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(alt ? tw1.ptr : tw0.ptr, n, touched.ptr);
+    GPMA_LAUNCH_CHECK();
+    GPMA_CUDA(cudaMemcpyAsync(pairs, touched.ptr, n * 16, cudaMemcpyDeviceToHost, stream_));
     GPMA_CUDA(cudaStreamSynchronize(stream_));
-    for (size_t i = 0; i < n; ++i) {
-        const u64 x = w[i];
-        const u64 b = x & ((1ull << 40) - 1);
-        pairs[2 * i] = b;
-        pairs[2 * i + 1] = b + (1ull << (x >> 40));
-    }
 }
 
 void Pma::binary_search_leaf(const u64* keys, size_t n, u64* leaves) {

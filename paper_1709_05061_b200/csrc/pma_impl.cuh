@@ -139,6 +139,7 @@ public:
     void search(const u64* keys, size_t n, u64* values, u8* found);
     u64 count_valid_in(u64 b, u64 e);
     void slot_hash(int level, u64* hashes);
+    void reserve_batch(u64 n);
     void touched_ranges(u64* pairs, size_t cap, size_t* count);
 
     // sequential single-key ops (pma.hpp:294-386, 471-479)

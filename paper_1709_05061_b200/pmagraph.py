@@ -233,6 +233,10 @@ class PackedMemoryArray:
         self._check(self._lib.pma_bounds(self.h, level, None, None, C.byref(rho), C.byref(tau)))
         return rho.value, tau.value
 
+    def reserve_batch(self, max_updates: int):
+        """Pre-size every per-batch buffer (pma_reserve_batch)."""
+        self._check(self._lib.pma_reserve_batch(self.h, max_updates))
+
     def slot_hash(self, level: int):
         """Per-segment parity digest of slots() at `level` (pma_slot_hash)."""
         n = self.capacity() // (self.leaf_size() << level) if 0 <= level <= self.height() else 1
@@ -296,7 +300,7 @@ class PackedMemoryArray:
             c = C.c_size_t(0)
             self._check(self._lib.pma_touched_ranges(self.h, None, 0, C.byref(c)))
             n = c.value
-        out = np.empty(2 * max(n, 1), np.uint64)
+        out = _host_out(2 * max(n, 1), np.uint64)  # page-locked: the copy is one DMA
         c = C.c_size_t(0)
         self._check(self._lib.pma_touched_ranges(self.h, _p(out), n, C.byref(c)))
         return out[:2 * n].reshape(n, 2)
@@ -540,7 +544,7 @@ class RebuildCsrGraph:
     csr = csr_snapshot
 
 
-_TORCH_DT = {np.uint32: "int32", np.float64: "float64"}
+_TORCH_DT = {np.uint32: "int32", np.float64: "float64", np.uint64: "int64"}
 
 
 def _host_out(n: int, dtype):
