@@ -140,10 +140,17 @@ def test_route_partition_is_stable_and_exact():
                                     _dev(src[ni:], "u32"), _dev(dst[ni:], "u32"))
         own = np.minimum(np.searchsorted(bounds, src.astype(np.int64), side="right") - 1, world - 1)
         order = np.argsort(own, kind="stable")
-        dbit = (np.arange(n) >= ni).astype(np.uint64) << np.uint64(63)
-        exp = ((src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64) | dbit)[order]
+        isdel = np.arange(n) >= ni
+        dbit = isdel.astype(np.uint64) << np.uint64(63)
+        exp = (src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64) | dbit
+        # a delete whose source is >= |V| travels as a key no graph holds (a
+        # guard delete stays a guard delete): never an alias through bit 63
+        absent = isdel & (src >= nv)
+        sentinel = np.where(dst == 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFE).astype(np.uint64)
+        exp = np.where(absent, (np.uint64(0x7FFFFFFF) << np.uint64(32)) | sentinel | dbit, exp)[order]
         wexp = np.where(np.arange(n) < ni, w, 1.0)[order]
-        assert counts.cpu().tolist() == list(np.bincount(own, minlength=world))
+        bad = int(((src[:ni] >= nv) | (dst[:ni] >= nv)).sum())  # inserts outside the vertex range
+        assert counts.cpu().tolist() == list(np.bincount(own, minlength=world)) + [bad]
         assert (keys.cpu().numpy().view(np.uint64) == exp).all()
         assert (ow.cpu().numpy() == wexp).all()
 
