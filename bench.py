@@ -191,17 +191,20 @@ def full_slides(info, B):
     return P
 
 
-def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks):
+def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segments=None):
     """Drive W untimed warm-up steps then K timed steps over `slides` (the
     first min(W + K, P) full slides of the window, in order).  When a pass has
     used every slide the stream holds, the graph is rebuilt from the initial
     window (untimed) and the next pass replays the same slides — so every
     timed step is a full slide on a window in the state the reference would
     have.  Timed segments are bracketed by barrier + synchronize and timed by
-    CUDA events on the library's stream; returns (graph, summed ms, passes)."""
+    CUDA events on the library's stream; returns (graph, summed ms, passes);
+    `segments` (if given) receives each timed segment's steps / event ms /
+    host wall ms."""
     import torch
     lib = g._lib
     n_sl = len(slides)
+    segments = [] if segments is None else segments
     total = 0.0
     cur = step = 0
     passes = 1
@@ -225,14 +228,17 @@ def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks):
                 clocks.start()
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
             e0.record(ext)
             for s in slides[cur:cur + n]:
                 on_step(g, s, True)
             e1.record(ext)
             torch.cuda.synchronize()
+            wall = (time.perf_counter() - t0) * 1e3
             if world > 1:
                 torch.distributed.barrier()
             total += e0.elapsed_time(e1)
+            segments.append({"steps": n, "ms": round(e0.elapsed_time(e1), 4), "wall_ms": round(wall, 4)})
         step += n
         cur += n
     return g, total, passes
@@ -347,7 +353,8 @@ def run_ours(args):
         if timed:
             per_step.append((st, graph.last_timing()))
 
-    g, ms, passes = run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks)
+    segs = []
+    g, ms, passes = run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs)
     clk = clocks.stop()
     updates = 0
     seg_ms = 0.0
@@ -401,10 +408,12 @@ def run_ours(args):
     def on_e2e(graph, s, timed):
         a, b, c, d, _ = host_by_slide[id(s)]
         st = graph.apply_batch(a, b, None, c, d, with_touched="array")
+        ntr = len(st.touched_ranges)
+        st.touched_ranges = None  # the caller consumed them (the page-locked block goes back to the cache)
         if timed:
             e2e_steps.append((st, graph.last_timing()))
             io["h2d"] += a.nbytes + b.nbytes + c.nbytes + d.nbytes
-            io["d2h"] += PMA_STATS_BYTES + 8 * len(st.touched_ranges)  # one sortable word per range
+            io["d2h"] += PMA_STATS_BYTES + 16 * ntr  # (begin, end) per touched range
 
     g2, e2e_ms, _ = run_passes(make_graph(), make_graph, slides, P, W, K, on_e2e, dev, world, None)
     e2e_stage = {"sort_ms": 0.0, "search_ms": 0.0, "rounds_ms": 0.0, "refresh_ms": 0.0}
@@ -458,6 +467,7 @@ def run_ours(args):
                 "commit_ms_per_step_all_levels": seg_ms / K, "step_ms": ms / K,
                 "stage_ms_per_step": {k: v / K for k, v in stage.items()},
                 "device_ms_each_step": [round(tm.device_ms, 4) for _, tm in per_step],
+                "timed_segments": segs,
                 "commit_ms_per_level": [round(x / K, 4) for x in level_ms if x > 0],
                 "groups_per_level": [x / K for x in level_groups if x > 0],
                 "hub_groups_per_level": [x / K for x, g in zip(level_big, level_groups) if g > 0],
