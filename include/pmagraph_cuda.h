@@ -187,6 +187,17 @@ int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count
  * state unchanged).  Buffers only grow. */
 int pma_reserve_batch(pma_handle* h, size_t max_updates);
 
+/* try_insert_plus(pma, level, seg, slice, cfg, result) (segment_engine.hpp:
+ * 320-341) for one group on the device: the n updates (sorted by key,
+ * duplicates resolved, all inside segment `seg` of `level`) are decided by the
+ * same rules as the batch engine's rounds and, when allowed, committed (lazy
+ * tombstones, or a merge + even re-dispatch).  *outcome: 0 deferred (nothing
+ * changed), 1 tombstones committed, 2 merged.  PMA_ERANGE for a level or
+ * segment outside the layout. */
+int pma_try_insert_plus(pma_handle* h, int level, size_t seg, const uint64_t* keys, const uint64_t* values,
+                        const uint8_t* ops, size_t n, const pma_engine_config* cfg, int* outcome,
+                        uint64_t* deletes_missed, uint64_t* tombstones_added);
+
 /* Parity digest of slots() (pma.hpp:214) without downloading it: one u64 per
  * segment of `level` (capacity / (leaf_size << level) values), the wrapping
  * sum over the segment's slots i of mix(key + mix(value ^ (i * 0x9E3779B97F4A7C15

@@ -79,3 +79,39 @@ def build_cpp_tests() -> str:
     subprocess.check_call(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", out,
                            "-L" + HERE, "-lpmagraph_cuda", "-Wl,-rpath,$ORIGIN/../../paper_1709_05061_b200"])
     return out
+
+
+REF_TESTS = "/root/reference/proj/tests"
+# the reference's unit-test files whose cases are reusable parity gates
+# (SURVEY §4): compiled UNMODIFIED from where they lie, against OUR drop-in
+# headers (include/pmagraph) and the Catch2 stand-in (tests/cpp/shim)
+REF_SUITE_FILES = ["test_pma.cpp", "test_segment_engine.cpp", "test_graph.cpp", "test_analytics.cpp",
+                   "test_primitives.cpp"]
+
+
+def build_ref_suite() -> str | None:
+    """tests/cpp/ref_suite: the reference's own unit tests built against the
+    drop-in headers and linked to libpmagraph_cuda.so.  Needs /root/reference
+    (this container); the binary travels to the GPU box like the .so."""
+    out = os.path.join(ROOT, "tests", "cpp", "ref_suite")
+    if not os.path.isdir(REF_TESTS):
+        return out if os.path.exists(out) else None
+    srcs = [os.path.join(REF_TESTS, f) for f in REF_SUITE_FILES] + [os.path.join(ROOT, "tests", "cpp", "shim",
+                                                                             "main.cpp")]
+    deps = srcs + glob.glob(os.path.join(ROOT, "include", "pmagraph", "*.hpp")) + [OUT] + \
+        glob.glob(os.path.join(ROOT, "tests", "cpp", "shim", "catch2", "*.hpp"))
+    if os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(d) for d in deps):
+        return out
+    objdir = os.path.join(HERE, "build", "ref_suite")
+    os.makedirs(objdir, exist_ok=True)
+    procs, objs = [], []
+    for src in srcs:
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        objs.append(obj)
+        procs.append(subprocess.Popen(["g++", "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "tests", "cpp", "shim"),
+                                       "-I" + os.path.join(ROOT, "include"), "-I" + REF_TESTS, "-c", src, "-o", obj]))
+    if any(p.wait() for p in procs):
+        raise RuntimeError("reference unit tests failed to build against the drop-in headers")
+    subprocess.check_call(["g++", *objs, "-o", out, "-L" + HERE, "-lpmagraph_cuda",
+                           "-Wl,-rpath,$ORIGIN/../../paper_1709_05061_b200"])
+    return out

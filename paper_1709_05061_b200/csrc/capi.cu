@@ -5,11 +5,13 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "graph_impl.cuh"
 #include "pmagraph_cuda.h"
 
 using gpma::ApiError;
+using gpma::u64;
 
 struct pma_handle {
     gpma::Pma* impl = nullptr;
@@ -183,6 +185,23 @@ int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count
         size_t c = 0;
         h->impl->touched_ranges(pairs, cap, &c);
         if (count) *count = c;
+    });
+}
+
+int pma_try_insert_plus(pma_handle* h, int level, size_t seg, const uint64_t* keys, const uint64_t* values,
+                        const uint8_t* ops, size_t n, const pma_engine_config* cfg, int* outcome,
+                        uint64_t* deletes_missed, uint64_t* tombstones_added) {
+    return guarded(err_of(h), [&] {
+        if (n && (!keys || !ops)) throw ApiError(PMA_EINVAL, "pma_try_insert_plus: keys / ops are NULL");
+        GPMA_CUDA(cudaSetDevice(h->impl->device()));
+        std::vector<uint64_t> zeros;
+        if (!values) zeros.assign(n, 0);
+        u64 missed = 0, tombs = 0;
+        const int r = h->impl->try_group(level, seg, keys, values ? values : zeros.data(), ops, n, to_cfg(cfg),
+                                         &missed, &tombs);
+        if (outcome) *outcome = r;
+        if (deletes_missed) *deletes_missed = missed;
+        if (tombstones_added) *tombstones_added = tombs;
     });
 }
 

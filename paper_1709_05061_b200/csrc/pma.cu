@@ -2485,6 +2485,118 @@ void Pma::touched_ranges(u64* pairs, size_t capn, size_t* count) {
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 
+// try_insert_plus (segment_engine.hpp:320-341) for ONE group on the device:
+// the group is set up exactly as a round of the batch engine would hand it to
+// the CTA tier (slice = sorted, duplicate-resolved updates of segment `seg`
+// at `level`), decided and committed by k_commit_cta, then the counters and
+// the leaf headers / row offsets are brought up to date as after a round.
+__global__ void k_group_leaves(const u64* __restrict__ uk, u64 n, const u64* __restrict__ hdr, u64 L,
+                               const u8* __restrict__ st, u64 leaf, const u64* __restrict__ ro, u64 rlo, u64 rhi,
+                               u64 first, u64 last, u32* __restrict__ ul) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
+        // a key whose leaf lies outside the segment cannot be in it: the
+        // clamped leaf never holds it (the reference scans [b, e) only)
+        u64 l = leaf_for_key(uk[i], hdr, L, st, leaf, ro, rlo, rhi);
+        ul[i] = u32(l < first ? first : (l > last ? last : l));
+    }
+}
+
+int Pma::try_group(int level, u64 seg, const u64* keys, const u64* vals, const u8* ops, u64 n, const EngineCfg& cfg,
+                   u64* missed, u64* tombs) {
+    if (level < 0 || level > height_) throw ApiError(PMA_ERANGE, "try_insert_plus: level out of range");
+    const u64 m = leaf_ << level;
+    if (seg >= cap_ / m) throw ApiError(PMA_ERANGE, "try_insert_plus: segment index out of range");
+    uk.reserve(n + 4);
+    uv.reserve(n + 4);
+    uop.reserve(n + 32);
+    ul.reserve(n + 1);
+    gstart.reserve(2);
+    gseg.reserve(2);
+    gflag.reserve(1);
+    touched.reserve(2 * n + 2);
+    rlist.reserve(4);
+    ik.reserve(n + 1);
+    iv.reserve(n + 1);
+    ir.reserve(n + 1);
+    ensure_slot_scratch();
+    if (n) {
+        GPMA_CUDA(cudaMemcpyAsync(uk.ptr, keys, n * 8, cudaMemcpyHostToDevice, stream_));
+        GPMA_CUDA(cudaMemcpyAsync(uv.ptr, vals, n * 8, cudaMemcpyHostToDevice, stream_));
+        GPMA_CUDA(cudaMemcpyAsync(uop.ptr, ops, n, cudaMemcpyHostToDevice, stream_));
+        const u64 first = seg * (m / leaf_), last = first + m / leaf_ - 1;
+        k_group_leaves<<<grid_for(n, 256), 256, 0, stream_>>>(uk.ptr, n, d_hdr, num_leaves(), d_st, leaf_,
+                                                              ro_base(), ro_lo, ro_lo + num_vertices, first, last,
+                                                              ul.ptr);
+        GPMA_LAUNCH_CHECK();
+    }
+    const u32 gs[2] = {0, u32(n)};
+    const u32 gg[1] = {u32(seg)};
+    GPMA_CUDA(cudaMemcpyAsync(gstart.ptr, gs, sizeof(gs), cudaMemcpyHostToDevice, stream_));
+    GPMA_CUDA(cudaMemcpyAsync(gseg.ptr, gg, sizeof(gg), cudaMemcpyHostToDevice, stream_));
+    GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
+    const ull one = 1;
+    GPMA_CUDA(cudaMemcpyAsync(&d_ctr->ngroups, &one, sizeof(ull), cudaMemcpyHostToDevice, stream_));
+    CommitArgs a{};
+    a.tlist = touched.ptr;
+    a.keys = d_keys;
+    a.vals = d_vals;
+    a.st = d_st;
+    a.uk = uk.ptr;
+    a.uv = uv.ptr;
+    a.uop = uop.ptr;
+    a.ul = ul.ptr;
+    a.pidx = nullptr;
+    a.gstart = gstart.ptr;
+    a.gseg = gseg.ptr;
+    a.gflag = gflag.ptr;
+    a.ctr = d_ctr;
+    a.hdr = d_hdr;
+    a.ro = ro_base();
+    a.rlist = rlist.ptr;
+    a.biglist = nullptr;
+    a.level = level;
+    a.m = m;
+    a.leaf = leaf_;
+    a.mn = mn_[level];
+    a.mx = mx_[level];
+    a.eager = cfg.eager;
+    a.large = cfg.large_for(m);
+    a.cap_gt_min = cap_ > 16;
+    a.ek = ek.ptr;
+    a.ev = ev.ptr;
+    a.es = es.ptr;
+    a.mflag = mflag.ptr;
+    a.ok = ok.ptr;
+    a.ov = ov.ptr;
+    a.ik = ik.ptr;
+    a.iv = iv.ptr;
+    a.ir = ir.ptr;
+    k_commit_cta<<<1, kCtaThreads, 0, stream_>>>(a);
+    GPMA_LAUNCH_CHECK();
+    u8 flag = 0;
+    GPMA_CUDA(cudaMemcpyAsync(&flag, gflag.ptr, 1, cudaMemcpyDeviceToHost, stream_));
+    sync_ctr();
+    valid_count = u64((long long)valid_count + h_ctr->valid_delta);
+    tombstone_count = u64((long long)tombstone_count + h_ctr->tomb_delta);
+    slot_writes += h_ctr->slot_writes;
+    if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
+    if (h_ctr->nrefresh > 0) {
+        k_refresh_ranges<<<grid_for(h_ctr->nrefresh * 32, 256, 148 * 16), 256, 0, stream_>>>(
+            rlist.ptr, nullptr, h_ctr->nrefresh, d_keys, d_st, cap_, leaf_, d_hdr, ro_base());
+        GPMA_LAUNCH_CHECK();
+    }
+    if (h_ctr->ntouched_next > 0 && empty_leaves != 0) {
+        k_left_walk<<<grid_for(h_ctr->ntouched_next, 128, 148 * 8), 128, 0, stream_>>>(
+            touched.ptr, h_ctr->ntouched_next, d_st, leaf_, d_hdr);
+        GPMA_LAUNCH_CHECK();
+    }
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    last_ntouched = 0;
+    if (missed) *missed = h_ctr->missed;
+    if (tombs) *tombs = h_ctr->tomb_added;
+    return flag;  // 0 deferred, 1 tombstones committed, 2 merged
+}
+
 void Pma::binary_search_leaf(const u64* keys, size_t n, u64* leaves) {
     if (n == 0) return;
     const u64* dq = stage(stage_k, keys, n);

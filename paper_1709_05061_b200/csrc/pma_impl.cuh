@@ -140,6 +140,8 @@ public:
     u64 count_valid_in(u64 b, u64 e);
     void slot_hash(int level, u64* hashes);
     void reserve_batch(u64 n);
+    int try_group(int level, u64 seg, const u64* keys, const u64* vals, const u8* ops, u64 n, const EngineCfg& cfg,
+                  u64* missed, u64* tombs);
     void touched_ranges(u64* pairs, size_t cap, size_t* count);
 
     // sequential single-key ops (pma.hpp:294-386, 471-479)

@@ -1,0 +1,27 @@
+"""The reference's OWN unit tests (proj/tests/test_pma.cpp,
+test_segment_engine.cpp, test_graph.cpp, test_analytics.cpp,
+test_primitives.cpp), compiled unmodified against the drop-in headers
+include/pmagraph/*.hpp and linked to libpmagraph_cuda.so
+(paper_1709_05061_b200/build.py build_ref_suite, SURVEY §4 "reusable as
+parity gates").  Every case runs on the B200 through the C ABI.  Skipped as
+out of scope: the lock-engine-backed graph (the GPMA lock engine is not part
+of this path)."""
+import os
+import subprocess
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "ref_suite")
+SKIP = "lock-engine-backed graph"
+
+
+def test_reference_unit_tests_pass_on_the_device():
+    assert os.path.exists(BIN), "build first: python -c 'import __graft_entry__ as g; g.build()'"
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=1200, env={**os.environ, "SHIM_SKIP": SKIP})
+    summary = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else ""
+    assert r.returncode == 0, f"{summary}\n{r.stderr[-4000:]}"
+    cases = int(summary.split()[0])
+    assert cases >= 80, summary
