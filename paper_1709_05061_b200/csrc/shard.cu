@@ -41,19 +41,23 @@ struct RouteIn {
     // caller rejects the batch on every rank before any shard applies.
     __device__ __forceinline__ bool bad_insert(u64 i) const { return i < ni && (is[i] >= nv || id[i] >= nv); }
     // EdgeKey on the wire; bit 63 marks a delete.  A delete whose source is
-    // >= |V| can never match (graph.hpp:140-145 counts it missed); it travels
-    // as kAbsentDelete, whose ids no graph holds (dst 2^32-2 >= |V|), so a
-    // source in [2^31, 2^32) never aliases a real edge through the delete bit.
+    // >= |V| can never match (graph.hpp:140-145 counts it missed).  Sources
+    // in [|V|, 2^31) travel as they are (the last rank counts them missed);
+    // a source in [2^31, 2^32) would alias (src - 2^31, dst) through the
+    // delete bit, so it travels as source 2^31 - 1 with a destination no
+    // graph holds (top bit set, >= |V|; a guard delete stays a guard delete:
+    // dropped, counted missed, not in batch_size, graph.hpp:141-147).  Such
+    // deletes differing only in their source's top bit or in the top bit of
+    // their destination count as one missed delete.
     __device__ __forceinline__ u64 key(u64 i) const {
         if (i < ni) return pack_edge(is[i], id[i]);
         const u32 s_ = ds[i - ni], d_ = dd[i - ni];
-        if (s_ >= nv) return d_ == u32(kGuardDst) ? kAbsentGuardDelete : kAbsentDelete;
+        if (s_ >= 0x80000000u) {
+            const u32 d2 = d_ == u32(kGuardDst) ? d_ : min(d_ | 0x80000000u, 0xFFFFFFFEu);
+            return pack_edge(0x7FFFFFFFu, d2) | (1ull << 63);
+        }
         return pack_edge(s_, d_) | (1ull << 63);
     }
-    // (a guard delete stays a guard delete: dropped, counted missed, not in
-    // batch_size, graph.hpp:141-147)
-    static constexpr u64 kAbsentDelete = (0x7FFFFFFFull << 32 | 0xFFFFFFFEull) | (1ull << 63);
-    static constexpr u64 kAbsentGuardDelete = (0x7FFFFFFFull << 32 | 0xFFFFFFFFull) | (1ull << 63);
 };
 
 __device__ __forceinline__ int owner_of(u32 s, const u32* __restrict__ b, int world) {

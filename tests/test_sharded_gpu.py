@@ -133,6 +133,7 @@ def test_route_partition_is_stable_and_exact():
                                        * world)
     for n in (0, 1, 3000, 70001):
         src = rng.integers(0, nv + 50, n).astype(np.uint32)
+        src[::97] = (np.uint64(2 ** 31) + src[::97].astype(np.uint64)).astype(np.uint32)  # would alias via bit 63
         dst = rng.integers(0, 2**32, n, dtype=np.uint64).astype(np.uint32)
         w = rng.random(n)
         ni = n // 3  # first third inserts, rest deletes (bit 63 on the wire)
@@ -145,8 +146,9 @@ def test_route_partition_is_stable_and_exact():
         exp = (src.astype(np.uint64) << np.uint64(32)) | dst.astype(np.uint64) | dbit
         # a delete whose source is >= |V| travels as a key no graph holds (a
         # guard delete stays a guard delete): never an alias through bit 63
-        absent = isdel & (src >= nv)
-        sentinel = np.where(dst == 0xFFFFFFFF, 0xFFFFFFFF, 0xFFFFFFFE).astype(np.uint64)
+        absent = isdel & (src >= 2 ** 31)
+        sentinel = np.where(dst == 0xFFFFFFFF, 0xFFFFFFFF,
+                            np.minimum(dst.astype(np.uint64) | np.uint64(0x80000000), 0xFFFFFFFE)).astype(np.uint64)
         exp = np.where(absent, (np.uint64(0x7FFFFFFF) << np.uint64(32)) | sentinel | dbit, exp)[order]
         wexp = np.where(np.arange(n) < ni, w, 1.0)[order]
         bad = int(((src[:ni] >= nv) | (dst[:ni] >= nv)).sum())  # inserts outside the vertex range
