@@ -81,6 +81,18 @@ int gpma_window_slide_explicit_random(gpma_window* w, size_t batch, gpma_rng* rn
 uint64_t gpma_window_size(const gpma_window* w);
 /* Copy deletions [offset, offset+n) of the window to host arrays. */
 int gpma_window_deletions_host(gpma_window* w, size_t offset, size_t n, uint32_t* src, uint32_t* dst);
+/* SlideBatch::expiries (streaming.hpp:69-74) of the last slide: the stream
+ * positions of the raw edges that left the window, in window order (FIFO:
+ * the oldest; explicit: the drawn ones).  *n = their count; up to cap are
+ * written. */
+int gpma_window_last_expiries(gpma_window* w, uint32_t* positions, size_t cap, size_t* n);
+/* SlidingWindow::distinct_edges (streaming.hpp:162-169), ascending key order
+ * (the reference's is a hash map's, unspecified).  cap = 0: count only. */
+int gpma_window_distinct_edges(gpma_window* w, uint32_t* src, uint32_t* dst, size_t cap, size_t* n);
+/* A caller's std::mt19937_64 in and out of a gpma_rng (its standard text
+ * state), so the caller's generator advances exactly as in the reference. */
+int gpma_rng_set_state(gpma_rng* r, const char* text);
+int gpma_rng_get_state(const gpma_rng* r, char* buf, size_t cap, size_t* len);
 
 #ifdef __cplusplus
 }

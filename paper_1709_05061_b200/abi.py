@@ -266,6 +266,10 @@ SIGNATURES = [
     ("gpma_rng_destroy", C.c_int, [_P]),
     ("gpma_window_slide_explicit_random", C.c_int, [_P, C.c_size_t, _P, C.POINTER(gpma_slide_t)]),
     ("gpma_window_size", C.c_uint64, [_P]),
+    ("gpma_window_last_expiries", C.c_int, [_P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("gpma_window_distinct_edges", C.c_int, [_P, _P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
+    ("gpma_rng_set_state", C.c_int, [_P, C.c_char_p]),
+    ("gpma_rng_get_state", C.c_int, [_P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
 ]
 
 _lib = None

@@ -86,7 +86,7 @@ REF_TESTS = "/root/reference/proj/tests"
 # (SURVEY §4): compiled UNMODIFIED from where they lie, against OUR drop-in
 # headers (include/pmagraph) and the Catch2 stand-in (tests/cpp/shim)
 REF_SUITE_FILES = ["test_pma.cpp", "test_segment_engine.cpp", "test_graph.cpp", "test_analytics.cpp",
-                   "test_primitives.cpp"]
+                   "test_primitives.cpp", "test_streaming.cpp"]
 
 
 def build_ref_suite() -> str | None:

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <random>
+#include <sstream>
 #include <vector>
 
 #include "pmagraph_cuda.h"
@@ -77,6 +78,11 @@ struct Window {
     DevBuf<u32> mult, lastpick;  // per key id: multiplicity; 1 + its last expiring index
     DevBuf<u8> picked;           // per index of (resident ++ arrivals): expires now
     DevBuf<u32> plist;           // drawn indices (explicit slides)
+    // the last slide's expiries (SlideBatch::expiries): FIFO = stream
+    // positions [exp_lo, exp_lo + exp_n); general = the picked entries of the
+    // window before the slide (res2 after the swap + the arrivals from exp_cur)
+    int exp_kind = 0;  // 0 none, 1 FIFO range, 2 general
+    uint64_t exp_lo = 0, exp_n = 0, exp_old = 0, exp_tot = 0, exp_cur = 0;
 };
 
 __global__ void k_key_ids(const u32* sp, const u32* sorted_kid, u64 n, u32* kid) {
@@ -164,6 +170,9 @@ static void slide_general(Window& W, size_t batch, std::mt19937_64* rng, gpma_sl
     out->del_offset = W.ndel;
     out->final_partial = take < batch ? 1 : 0;
     out->n_del = 0;
+    W.exp_kind = 1;
+    W.exp_lo = 0;
+    W.exp_n = 0;
     if (take == 0) return;
     // explicit: the expiring entries are drawn uniformly without replacement
     // among the window before the arrivals — the reference's exact draws
@@ -243,6 +252,11 @@ static void slide_general(Window& W, size_t batch, std::mt19937_64* rng, gpma_sl
     GPMA_CUDA(cudaStreamSynchronize(W.stream));
     std::swap(W.res.ptr, W.res2.ptr);
     std::swap(W.res.cap, W.res2.cap);
+    W.exp_kind = 2;
+    W.exp_n = ne;
+    W.exp_old = old;
+    W.exp_tot = tot;
+    W.exp_cur = W.cursor;
     W.wsize = tot - ne;
     out->n_del = nd;
     W.ndel += nd;
@@ -545,8 +559,122 @@ int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out) {
         }
         out->n_del = nd;
         W.ndel += nd;
+        W.exp_kind = 1;
+        W.exp_lo = W.lo;
+        W.exp_n = take;
         W.lo += take;
         W.cursor = end;
+    });
+}
+
+// SlideBatch::expiries of the last slide as stream positions, window order.
+int gpma_window_last_expiries(gpma_window* w, uint32_t* positions, size_t cap, size_t* n) {
+    return sguard([&] {
+        auto& W = w->w;
+        GPMA_CUDA(cudaSetDevice(W.device));
+        if (n) *n = W.exp_n;
+        const uint64_t m = std::min<uint64_t>(cap, W.exp_n);
+        if (!positions || m == 0) return;
+        if (W.exp_kind == 1) {
+            for (uint64_t i = 0; i < m; ++i) positions[i] = uint32_t(W.exp_lo + i);
+            return;
+        }
+        gpma::DevBuf<gpma::u32> out;
+        out.reserve(W.exp_n + 1);
+        const gpma::u8* pk = W.picked.ptr;
+        const gpma::u32* res = W.res2.ptr;  // the window before the slide
+        const uint64_t old = W.exp_old, cur = W.exp_cur;
+        gpma::u32* o = out.ptr;
+        gpma::run_compact(
+            W.stream, W.ws, nullptr, W.exp_tot, W.exp_tot, [=] __device__(gpma::ull i) { return pk[i] != 0; },
+            [=] __device__(gpma::ull i, unsigned f, gpma::ull x) {
+                if (f) o[x] = i < old ? res[i] : gpma::u32(cur + (i - old));
+            },
+            gpma::NoFin{});
+        GPMA_CUDA(cudaMemcpyAsync(positions, out.ptr, m * 4, cudaMemcpyDeviceToHost, W.stream));
+        GPMA_CUDA(cudaStreamSynchronize(W.stream));
+    });
+}
+
+// SlidingWindow::distinct_edges (streaming.hpp:162-169): the window's
+// distinct edges, ascending key order (the reference's order is a hash map's,
+// i.e. unspecified).  Two-call protocol: cap = 0 returns the count.
+int gpma_window_distinct_edges(gpma_window* w, uint32_t* src, uint32_t* dst, size_t cap, size_t* n) {
+    return sguard([&] {
+        auto& W = w->w;
+        GPMA_CUDA(cudaSetDevice(W.device));
+        const uint64_t ws = W.general ? W.wsize : W.cursor - W.lo;
+        gpma::DevBuf<gpma::u64> k0, k1;
+        k0.reserve(ws + 1);
+        k1.reserve(ws + 1);
+        W.cnt.reserve(2);
+        gpma::ull* cnt = W.cnt.ptr;
+        uint64_t nd = 0;
+        if (ws) {
+            gpma::u64* kk = k0.ptr;
+            const gpma::u32* ss = W.src.ptr;
+            const gpma::u32* dd = W.dst.ptr;
+            const gpma::u32* res = W.res.ptr;
+            const bool gen = W.general;
+            const uint64_t lo = W.lo;
+            gpma::run_compact(
+                W.stream, W.ws, nullptr, ws, ws, [=] __device__(gpma::ull) { return true; },
+                [=] __device__(gpma::ull i, unsigned, gpma::ull) {
+                    const gpma::u32 p = gen ? res[i] : gpma::u32(lo + i);
+                    kk[i] = gpma::pack_edge(ss[p], dd[p]);
+                },
+                gpma::NoFin{});
+            gpma::RadixWorkspace rws;
+            const int alt = gpma::radix_sort(W.stream, rws, k0.ptr, k1.ptr, nullptr, nullptr, ws, 0, 64);
+            const gpma::u64* sk = alt ? k1.ptr : k0.ptr;
+            gpma::u64* uq = alt ? k0.ptr : k1.ptr;
+            gpma::run_compact(
+                W.stream, W.ws, nullptr, ws, ws, [=] __device__(gpma::ull i) { return i == 0 || sk[i] != sk[i - 1]; },
+                [=] __device__(gpma::ull i, unsigned f, gpma::ull x) {
+                    if (f) uq[x] = sk[i];
+                },
+                [=] __device__(gpma::ull total) { *cnt = total; });
+            GPMA_CUDA(cudaMemcpyAsync(&nd, cnt, 8, cudaMemcpyDeviceToHost, W.stream));
+            GPMA_CUDA(cudaStreamSynchronize(W.stream));
+            if (n) *n = nd;
+            const uint64_t m = std::min<uint64_t>(cap, nd);
+            if (m && src && dst) {
+                std::vector<gpma::u64> h(m);
+                GPMA_CUDA(cudaMemcpyAsync(h.data(), uq, m * 8, cudaMemcpyDeviceToHost, W.stream));
+                GPMA_CUDA(cudaStreamSynchronize(W.stream));
+                for (uint64_t i = 0; i < m; ++i) {
+                    src[i] = gpma::src_of(h[i]);
+                    dst[i] = gpma::dst_of(h[i]);
+                }
+            }
+            return;
+        }
+        if (n) *n = 0;
+    });
+}
+
+// std::mt19937_64 state through its standard text form, so a caller's
+// generator can drive gpma_window_slide_explicit_random and advance exactly
+// as the reference's would (streaming.hpp:129 takes it by reference).
+int gpma_rng_set_state(gpma_rng* r, const char* text) {
+    return sguard([&] {
+        std::istringstream is(text ? text : "");
+        is >> r->r;
+        if (!is) throw ApiError(PMA_EINVAL, "rng state: not a std::mt19937_64 text state");
+    });
+}
+
+int gpma_rng_get_state(const gpma_rng* r, char* buf, size_t cap, size_t* len) {
+    return sguard([&] {
+        std::ostringstream os;
+        os << r->r;
+        const std::string t = os.str();
+        if (len) *len = t.size() + 1;
+        if (buf && cap) {
+            const size_t m = std::min(cap - 1, t.size());
+            std::memcpy(buf, t.data(), m);
+            buf[m] = 0;
+        }
     });
 }
 

@@ -1,6 +1,6 @@
 """The reference's OWN unit tests (proj/tests/test_pma.cpp,
 test_segment_engine.cpp, test_graph.cpp, test_analytics.cpp,
-test_primitives.cpp), compiled unmodified against the drop-in headers
+test_primitives.cpp, test_streaming.cpp), compiled unmodified against the drop-in headers
 include/pmagraph/*.hpp and linked to libpmagraph_cuda.so
 (paper_1709_05061_b200/build.py build_ref_suite, SURVEY §4 "reusable as
 parity gates").  Every case runs on the B200 through the C ABI.  Skipped as
@@ -24,4 +24,4 @@ def test_reference_unit_tests_pass_on_the_device():
     summary = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else ""
     assert r.returncode == 0, f"{summary}\n{r.stderr[-4000:]}"
     cases = int(summary.split()[0])
-    assert cases >= 80, summary
+    assert cases >= 87, summary
