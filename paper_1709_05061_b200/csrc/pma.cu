@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
 
 #include "block_ops.cuh"
 #include "merge.cuh"
@@ -66,6 +67,9 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     stream_ = own_stream_;
     GPMA_CUDA(cudaMalloc(&d_ctr, sizeof(Ctr)));
     GPMA_CUDA(cudaMallocHost(&h_ctr, sizeof(Ctr)));
+    GPMA_CUDA(cudaMallocHost(&h_desc_, sizeof(GraphFront)));
+    GPMA_CUDA(cudaMalloc(&d_desc_, sizeof(GraphFront)));
+    if (const char* e = std::getenv("GPMA_NO_GRAPHS")) small_graphs_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     for (auto& e : lev_ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -79,6 +83,9 @@ Pma::~Pma() {
     free_arrays();
     if (d_ctr) cudaFree(d_ctr);
     if (h_ctr) cudaFreeHost(h_ctr);
+    if (small_exec_) cudaGraphExecDestroy(small_exec_);
+    if (h_desc_) cudaFreeHost(h_desc_);
+    if (d_desc_) cudaFree(d_desc_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
     for (auto& e : lev_ev_)
@@ -398,8 +405,8 @@ __device__ __forceinline__ void prep_segment(const GraphFront& f, int db, int ib
 // `oor` (the batch is then redone on the generic path).  kBucket: also the
 // leaf bucket of every update (leaf-bucket front end, see batch_update_device).
 template <bool kBucket>
-__global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr,
-                             BucketArgs ba) {
+__device__ __forceinline__ void prep_graph_body(const GraphFront& f, int db, int ib, u64* __restrict__ ck,
+                                                u32* __restrict__ ci, Ctr* ctr, const BucketArgs& ba) {
     PrepAcc acc;
     if (f.mk) {
         const u64 n = f.ni + f.nd;
@@ -424,6 +431,21 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
         if (acc.oor) atomicOr(&ctr->oor, 1ull);
         if (acc.bigrun) atomicOr(&ctr->bigrun, 1ull);
     }
+}
+template <bool kBucket>
+__global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck,
+                                                                     u32* __restrict__ ci, Ctr* ctr, BucketArgs ba) {
+    prep_graph_body<kBucket>(f, db, ib, ck, ci, ctr, ba);
+}
+
+// The same front end with the batch descriptor in device memory (written by
+// a copy node of a captured CUDA graph), so one instantiated graph serves
+// every small batch; the batch size goes to ctr->nsort for the next nodes.
+__global__ void __launch_bounds__(256) k_prep_graph_dev(const GraphFront* __restrict__ fp, int db, int ib,
+                                                        u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
+    const GraphFront f = *fp;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->nsort = f.ni + f.nd;
+    prep_graph_body<false>(f, db, ib, ck, ci, ctr, BucketArgs{});
 }
 
 // bucket scatter: update i -> position off[bucket] + ordinal (bucket order,
@@ -1468,7 +1490,8 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_de
 
 // Empty leaves left of a touched range inherit its first header.
 __global__ void k_left_walk(const u64* __restrict__ ranges, u64 nranges, const u8* __restrict__ st, u64 leaf,
-                            u64* __restrict__ hdr) {
+                            u64* __restrict__ hdr, const ull* n_dev = nullptr) {
+    if (n_dev) nranges = *n_dev;
     for (u64 r = blockIdx.x * u64(blockDim.x) + threadIdx.x; r < nranges; r += u64(gridDim.x) * blockDim.x) {
         const u64 la = ranges[2 * r] / leaf;
         const u64 v = hdr[la];
@@ -1736,6 +1759,298 @@ void Pma::rebuild_at_capacity(u64 cap) {
     place_root_from(dek, dev, n);
 }
 
+// One round (level) of the engine (segment_engine.hpp:78-105, 320-341):
+// group the pending list by segment (unique_segments), decide + commit every
+// group, keep the deferred groups' updates (advance_round).  Every kernel
+// reads its counts on the device; npend is a host-known upper bound of the
+// pending count.  events: record the level's commit span (lev_ev_).
+void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
+                        ScanWorkspace& ws, bool events, u64& launches) {
+    const u64 m = leaf_ << level;
+    ull* np_cur = &d_ctr->np[level & 1];
+    ull* np_next = &d_ctr->np[(level + 1) & 1];
+    // group = segment heads (unique_segments)
+    {
+        const u32* ulp = ul.ptr;
+        const u32* pp = pcur;
+        u32* gs = gstart.ptr;
+        u32* gg = gseg.ptr;
+        u32* gi = gid.ptr;
+        Ctr* ctr = d_ctr;
+        const int lv = level;
+        run_compact(
+            stream_, ws, np_cur, 0, npend,
+            [=] __device__(ull p) {
+                return p == 0 || (ulp[pp ? pp[p] : p] >> lv) != (ulp[pp ? pp[p - 1] : p - 1] >> lv);
+            },
+            [=] __device__(ull p, unsigned f, ull x) {
+                if (f) {
+                    gs[x] = u32(p);
+                    gg[x] = ulp[pp ? pp[p] : p] >> lv;
+                }
+                gi[p] = u32(x + f - 1);
+            },
+            [=] __device__(ull total) {
+                ctr->ngroups = total;
+                gs[total] = u32(*np_cur);
+                ctr->lvl_npend[lv] = *np_cur;
+            });
+        ++launches;
+    }
+    // commit (decide + merge + scatter)
+    CommitArgs a{};
+    a.tlist = touched_ptr;
+    a.keys = d_keys;
+    a.vals = d_vals;
+    a.st = d_st;
+    a.uk = uk.ptr;
+    a.uv = uv.ptr;
+    a.uop = uop.ptr;
+    a.ul = ul.ptr;
+    a.pidx = pcur;
+    a.gstart = gstart.ptr;
+    a.gseg = gseg.ptr;
+    a.gflag = gflag.ptr;
+    a.ctr = d_ctr;
+    a.hdr = d_hdr;
+    a.ro = ro_base();
+    a.rlist = rlist.ptr;
+    a.level = level;
+    a.m = m;
+    a.leaf = leaf_;
+    a.mn = mn_[level];
+    a.mx = mx_[level];
+    a.eager = cfg.eager;
+    a.large = cfg.large_for(m);
+    a.cap_gt_min = cap_ > 16;
+    if (events) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level], stream_));
+    ensure_slot_scratch();
+    ik.reserve(n);
+    iv.reserve(n);
+    ir.reserve(n);
+    biglist.reserve(npend + 1);
+    a.ek = ek.ptr;
+    a.ev = ev.ptr;
+    a.es = es.ptr;
+    a.mflag = mflag.ptr;
+    a.ok = ok.ptr;
+    a.ov = ov.ptr;
+    a.ik = ik.ptr;
+    a.iv = iv.ptr;
+    a.ir = ir.ptr;
+    a.biglist = biglist.ptr;
+    if (m <= 32) {
+        // warp tiers; hub groups (large slices) are appended to biglist
+        if (m == 16 && leaf_ == 16 && pcur == nullptr) {  // level 0: identity pending list
+            // exactly the resident CTAs (persistent: the grid-stride tile
+            // loop balances; a partial last wave costs ~10%, measured)
+            static const unsigned resident = [] {
+                int per_sm = 0, dev = 0, sms = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_commit_leaf, kLeafWarps * 32, 0);
+                return unsigned((per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148));
+            }();
+            const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, resident);
+            k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
+        } else {
+            // grid for the host bound; the kernel sizes its tiles from the
+            // device-side group count (<= npend)
+            const unsigned grid = grid_for(npend, kWarpTierWarps, 148 * 8);
+            if (m <= 16) k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+            else k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+        }
+        GPMA_LAUNCH_CHECK();
+        // CTA kernel over the hub groups only (grid bounded by npend / kBigSlice)
+        k_commit_cta<<<grid_for(npend / kBigSlice + 1, 1, 148 * 2), kCtaThreads, 0, stream_>>>(a);
+    } else {
+        a.biglist = nullptr;
+        const unsigned grid = grid_for(npend, 1, 148 * 4);
+        k_commit_cta<<<grid, kCtaThreads, 0, stream_>>>(a);
+    }
+    GPMA_LAUNCH_CHECK();
+    if (events) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));
+    ++launches;
+    // advance_round: keep deferred groups' updates
+    {
+        const u8* gf = gflag.ptr;
+        const u32* gi = gid.ptr;
+        const u32* pp = pcur;
+        u32* pn = pnext;
+        Ctr* ctr = d_ctr;
+        const int lv = level;
+        run_compact(
+            stream_, ws, np_cur, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
+            [=] __device__(ull p, unsigned f, ull x) {
+                if (f) pn[x] = pp ? pp[p] : u32(p);
+            },
+            [=] __device__(ull total) {
+                *np_next = total;
+                // the level's stats (read at the next host sync)
+                ctr->lvl_committed[lv] = ctr->committed;
+                ctr->lvl_bytes[lv] = ctr->commit_bytes;  // cumulative up to this level
+                ctr->lvl_groups[lv] = ctr->ngroups;
+                ctr->lvl_big[lv] = ctr->nbig;
+                ctr->lvl_maxslice[lv] = ctr->max_slice;
+                ctr->committed = 0;
+                ctr->nbig = 0;
+                ctr->max_slice = 0;
+            });
+        ++launches;
+    }
+}
+
+// ---- small graph batches ----------------------------------------------
+// A batch of up to kSmallGraphMax graph updates is latency-bound: a dozen
+// tiny kernels whose cost is their launches and the host round trips between
+// rounds.  Its whole front end (pack + checks, one-CTA radix sort, duplicate
+// resolution, leaf search) and the first rounds are captured ONCE as a CUDA
+// graph whose nodes read the batch descriptor and every count from device
+// memory; each batch then costs one descriptor write, one graph launch and
+// one synchronisation.  The graph embeds array and scratch pointers, the
+// layout and the engine config; any change re-captures it.
+bool Pma::small_graph_ok(u64 n, const GraphFront& gf) const {
+    if (!small_graphs_ || gf.mk || n == 0 || n > kSmallGraphMax || height_ < 1 || !ro_base() || !stream_) return false;
+    int db = 1;
+    while (db < 32 && (1ull << db) < gf.nv) ++db;
+    return 2 * db + 1 + kSmallIb <= 64;
+}
+
+std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int levels) const {
+    const void* ptrs[] = {d_keys, d_vals, d_st, d_hdr, ro_base(), d_ctr, d_desc_, h_desc_, h_ctr, sk_in.ptr,
+                          sk_out.ptr, uk.ptr, uv.ptr, uop.ptr, ul.ptr, pidx0.ptr, pidx1.ptr, gid.ptr, gstart.ptr,
+                          gseg.ptr, gflag.ptr, touched.ptr, rlist.ptr, ik.ptr, iv.ptr, ir.ptr, biglist.ptr, ek.ptr,
+                          ev.ptr, es.ptr, mflag.ptr, ok.ptr, ov.ptr, small_ws_.tiles.ptr, stream_};
+    std::vector<uintptr_t> k;
+    for (const void* p : ptrs) k.push_back(reinterpret_cast<uintptr_t>(p));
+    const u64 vals[] = {cap_, leaf_, u64(height_), ro_lo, num_vertices, u64(db), u64(cfg.eager), cfg.small_max,
+                        cfg.medium_max, u64(cfg.force), u64(levels)};
+    for (const u64 v : vals) k.push_back(uintptr_t(v));
+    return k;
+}
+
+void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
+    if (small_exec_) {
+        GPMA_CUDA(cudaGraphExecDestroy(small_exec_));
+        small_exec_ = nullptr;
+    }
+    const int ib = kSmallIb;
+    const int nbits = 2 * db + 1;
+    radix_prepare();
+    u64 dummy = 0;
+    cudaGraph_t graph = nullptr;
+    GPMA_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+    try {
+        GPMA_CUDA(cudaMemcpyAsync(d_desc_, h_desc_, sizeof(GraphFront), cudaMemcpyHostToDevice, stream_));
+        // the graph's own look-back words start clean on every replay
+        GPMA_CUDA(cudaMemsetAsync(small_ws_.tiles.ptr, 0, small_ws_.tiles.cap * sizeof(ull), stream_));
+        GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
+        k_prep_graph_dev<<<kSmallGraphMax / 256, 256, 0, stream_>>>(d_desc_, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
+        GPMA_LAUNCH_CHECK();
+        radix_sort_small_dev(stream_, sk_in.ptr, sk_out.ptr, &d_ctr->nsort, ib, ib + nbits);
+        {
+            // duplicate resolution as in batch_update_device (packed words:
+            // key << ib | arrival index, all-ones index = a delete)
+            const u64* ck = sk_out.ptr;
+            const GraphFront* fd = d_desc_;
+            const ull* ndp = &d_ctr->nsort;
+            const int gdb = db;
+            const u64 skipkey = 1ull << (nbits - 1);
+            const int pib = ib;
+            const u64 pmask = (1ull << pib) - 1;
+            auto KEY = [=] __device__(ull i) -> u64 { return ck[i] >> pib; };
+            auto PAY = [=] __device__(ull i) -> u32 {
+                const u32 a = u32(ck[i] & pmask);
+                return (a << 1) | (a != u32(pmask) ? 1u : 0u);
+            };
+            u64* o_k = uk.ptr;
+            u64* o_v = uv.ptr;
+            u8* o_o = uop.ptr;
+            Ctr* ctr = d_ctr;
+            run_compact_tile(
+                stream_, small_ws_, ndp, 0, kSmallGraphMax,
+                [=] __device__(ull i) {
+                    const ull nn = *ndp;
+                    const u64 c = KEY(i);
+                    return ((i + 1 == nn) || KEY(i + 1) != c) && c < skipkey;
+                },
+                [=] __device__(ull i0, ull nn, unsigned fm, const ull* xs) {
+                    const double* gw = fd->iw;
+#pragma unroll
+                    for (int j = 0; j < kScanItems; ++j) {
+                        if (!((fm >> j) & 1u)) continue;
+                        const ull i = i0 + ull(j) * kScanThreads;
+                        const u64 c = KEY(i);
+                        u32 p = PAY(i);
+                        if (!(p & 1u) && i > 0 && KEY(i - 1) == c) {
+                            for (long long t = (long long)i - 1; t >= 0 && KEY(t) == c; --t) {
+                                const u32 q = PAY(t);
+                                if (q & 1u) {
+                                    p = q;
+                                    break;
+                                }
+                            }
+                        }
+                        const u32 a = p >> 1;
+                        const bool ins = p & 1u;
+                        o_k[xs[j]] = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
+                        o_v[xs[j]] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
+                        o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
+                    }
+                },
+                [=] __device__(ull total) {
+                    ctr->n_unique = total;
+                    ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
+                });
+        }
+        k_leaf_search_sorted<<<kSmallGraphMax / 256, 256, 0, stream_>>>(
+            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
+        GPMA_LAUNCH_CHECK();
+        u32* pcur = nullptr;
+        u32* pnext = pidx0.ptr;
+        for (int level = 0; level < levels; ++level) {
+            enqueue_level(level, kSmallGraphMax, pcur, pnext, touched.ptr, kSmallGraphMax, cfg, small_ws_, false, dummy);
+            pcur = pnext;
+            pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
+        }
+        // headers / row offsets of the rewritten ranges, left walks
+        k_refresh_ranges<<<64, 256, 0, stream_>>>(rlist.ptr, &d_ctr->nrefresh, 0, d_keys, d_st, cap_, leaf_, d_hdr,
+                                                  ro_base());
+        GPMA_LAUNCH_CHECK();
+        k_left_walk<<<16, 128, 0, stream_>>>(touched.ptr, 0, d_st, leaf_, d_hdr, &d_ctr->ntouched_next);
+        GPMA_LAUNCH_CHECK();
+        GPMA_CUDA(cudaMemcpyAsync(h_ctr, d_ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, stream_));
+    } catch (...) {
+        cudaStreamEndCapture(stream_, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    GPMA_CUDA(cudaStreamEndCapture(stream_, &graph));
+    const cudaError_t e = cudaGraphInstantiate(&small_exec_, graph, 0);
+    cudaGraphDestroy(graph);
+    GPMA_CUDA(e);
+}
+
+int Pma::run_small_graph(const GraphFront& gf, const EngineCfg& cfg) {
+    int db = 1;
+    while (db < 32 && (1ull << db) < gf.nv) ++db;
+    const int levels = std::min(kSmallGraphLevels, height_);
+    auto key = small_graph_key(db, cfg, levels);
+    if (!small_exec_ || key != small_key_) {
+        // every buffer the nodes touch, at its final size, before capture
+        reserve_batch(kSmallGraphMax);
+        small_ws_.tiles.reserve(64);
+        small_ws_.epoch = 0;
+        key = small_graph_key(db, cfg, levels);
+        capture_small_graph(db, cfg, levels);
+        small_key_ = key;
+    }
+    *h_desc_ = gf;  // read by the graph's first node (the previous replay finished: synchronous calls)
+    GPMA_CUDA(cudaGraphLaunch(small_exec_, stream_));
+    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    return levels;
+}
+
 void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n, const EngineCfg& cfg,
                               pma_stats* out, GraphFront* gf) {
     using Clock = std::chrono::steady_clock;
@@ -1755,6 +2070,15 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         return;
     }
     event(0);
+    bool bucket = false;
+    // ---- small graph batches: the front end and the first rounds replayed
+    // as one captured CUDA graph (no per-kernel launch cost, no host round
+    // trip); the host loop below continues only if updates are still pending
+    const int graph_levels = (gf && small_graph_ok(n, *gf)) ? run_small_graph(*gf, cfg) : 0;
+    if (graph_levels) {
+        event(1);
+        event(2);
+    } else {
     // ---- 1. sort (stable, varying bits only) ----
     GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
     sk_in.reserve(n);
@@ -1763,7 +2087,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     si_out.reserve(n);
     int nbits = 0;
     int packed_ib = 0;
-    bool bucket = false;
     if (gf) {
         // graph front end: pack + id check + compression in one pass; the
         // key layout is fixed by |V| (src, dst < 2^db), so no host round trip
@@ -1974,6 +2297,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         }
     }
     event(2);
+    }  // front end
     pidx0.reserve(n);
     pidx1.reserve(n);
     gid.reserve(n);
@@ -1995,141 +2319,32 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     u32* pnext = pidx0.ptr;
     float seg_ms = 0.f;
     bool root_done = false;
+    int synced_upto = -1;  // per-level stats collected for levels <= synced_upto
+    int level0 = 0;
+    if (graph_levels) {
+        // the graph ran levels [0, graph_levels) and brought the counters back
+        for (int l = 0; l < graph_levels; ++l) {
+            if (l < 16) {
+                timing.level_bytes[l] += h_ctr->lvl_bytes[l] - (l > 0 ? h_ctr->lvl_bytes[l - 1] : 0);
+                timing.level_groups[l] += h_ctr->lvl_groups[l];
+                timing.level_big[l] += h_ctr->lvl_big[l];
+                timing.level_max_slice[l] = std::max<u64>(timing.level_max_slice[l], h_ctr->lvl_maxslice[l]);
+            }
+            if (h_ctr->lvl_npend[l] > 0) st.rounds++;
+            st.segments_per_level[l] += h_ctr->lvl_committed[l];
+        }
+        synced_upto = graph_levels - 1;
+        ntouched = h_ctr->ntouched_next;
+        npend = h_ctr->np[graph_levels & 1];
+        pcur = ((graph_levels - 1) & 1) == 0 ? pidx0.ptr : pidx1.ptr;  // the last advance's output
+        pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
+        level0 = graph_levels;
+        launches += 1;
+    }
+    const bool host_levels = npend > 0;
     if (npend > 0) {
-        int synced_upto = -1;  // per-level stats collected for levels <= synced_upto
-        for (int level = 0;; ++level) {
-            const u64 m = leaf_ << level;
-            ull* np_cur = &d_ctr->np[level & 1];
-            ull* np_next = &d_ctr->np[(level + 1) & 1];
-            // group = segment heads (unique_segments)
-            {
-                const u32* ulp = ul.ptr;
-                const u32* pp = pcur;
-                u32* gs = gstart.ptr;
-                u32* gg = gseg.ptr;
-                u32* gi = gid.ptr;
-                Ctr* ctr = d_ctr;
-                const int lv = level;
-                run_compact(
-                    stream_, ws, np_cur, 0, npend,
-                    [=] __device__(ull p) {
-                        return p == 0 || (ulp[pp ? pp[p] : p] >> lv) != (ulp[pp ? pp[p - 1] : p - 1] >> lv);
-                    },
-                    [=] __device__(ull p, unsigned f, ull x) {
-                        if (f) {
-                            gs[x] = u32(p);
-                            gg[x] = ulp[pp ? pp[p] : p] >> lv;
-                        }
-                        gi[p] = u32(x + f - 1);
-                    },
-                    [=] __device__(ull total) {
-                        ctr->ngroups = total;
-                        gs[total] = u32(*np_cur);
-                        ctr->lvl_npend[lv] = *np_cur;
-                    });
-                ++launches;
-            }
-            // commit (decide + merge + scatter)
-            CommitArgs a{};
-            a.tlist = touched_ptr;
-            a.keys = d_keys;
-            a.vals = d_vals;
-            a.st = d_st;
-            a.uk = uk.ptr;
-            a.uv = uv.ptr;
-            a.uop = uop.ptr;
-            a.ul = ul.ptr;
-            a.pidx = pcur;
-            a.gstart = gstart.ptr;
-            a.gseg = gseg.ptr;
-            a.gflag = gflag.ptr;
-            a.ctr = d_ctr;
-            a.hdr = d_hdr;
-            a.ro = ro_base();
-            a.rlist = rlist.ptr;
-            a.level = level;
-            a.m = m;
-            a.leaf = leaf_;
-            a.mn = mn_[level];
-            a.mx = mx_[level];
-            a.eager = cfg.eager;
-            a.large = cfg.large_for(m);
-            a.cap_gt_min = cap_ > 16;
-            GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level], stream_));
-            ensure_slot_scratch();
-            ik.reserve(n);
-            iv.reserve(n);
-            ir.reserve(n);
-            biglist.reserve(npend + 1);
-            a.ek = ek.ptr;
-            a.ev = ev.ptr;
-            a.es = es.ptr;
-            a.mflag = mflag.ptr;
-            a.ok = ok.ptr;
-            a.ov = ov.ptr;
-            a.ik = ik.ptr;
-            a.iv = iv.ptr;
-            a.ir = ir.ptr;
-            a.biglist = biglist.ptr;
-            if (m <= 32) {
-                // warp tiers; hub groups (large slices) are appended to biglist
-                if (m == 16 && leaf_ == 16 && pcur == nullptr) {  // level 0: identity pending list
-                    // exactly the resident CTAs (persistent: the grid-stride tile
-                    // loop balances; a partial last wave costs ~10%, measured)
-                    static const unsigned resident = [] {
-                        int per_sm = 0, dev = 0, sms = 0;
-                        cudaGetDevice(&dev);
-                        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-                        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_commit_leaf, kLeafWarps * 32, 0);
-                        return unsigned((per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148));
-                    }();
-                    const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, resident);
-                    k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
-                } else {
-                    // grid for the host bound; the kernel sizes its tiles from the
-                    // device-side group count (<= npend)
-                    const unsigned grid = grid_for(npend, kWarpTierWarps, 148 * 8);
-                    if (m <= 16) k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
-                    else k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
-                }
-                GPMA_LAUNCH_CHECK();
-                // CTA kernel over the hub groups only (grid bounded by npend / kBigSlice)
-                k_commit_cta<<<grid_for(npend / kBigSlice + 1, 1, 148 * 2), kCtaThreads, 0, stream_>>>(a);
-            } else {
-                a.biglist = nullptr;
-                const unsigned grid = grid_for(npend, 1, 148 * 4);
-                k_commit_cta<<<grid, kCtaThreads, 0, stream_>>>(a);
-            }
-            GPMA_LAUNCH_CHECK();
-            GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));
-            ++launches;
-            // advance_round: keep deferred groups' updates
-            {
-                const u8* gf = gflag.ptr;
-                const u32* gi = gid.ptr;
-                const u32* pp = pcur;
-                u32* pn = pnext;
-                Ctr* ctr = d_ctr;
-                const int lv = level;
-                run_compact(
-                    stream_, ws, np_cur, 0, npend, [=] __device__(ull p) { return gf[gi[p]] == 0; },
-                    [=] __device__(ull p, unsigned f, ull x) {
-                        if (f) pn[x] = pp ? pp[p] : u32(p);
-                    },
-                    [=] __device__(ull total) {
-                        *np_next = total;
-                        // the level's stats (read at the next host sync)
-                        ctr->lvl_committed[lv] = ctr->committed;
-                        ctr->lvl_bytes[lv] = ctr->commit_bytes;  // cumulative up to this level
-                        ctr->lvl_groups[lv] = ctr->ngroups;
-                        ctr->lvl_big[lv] = ctr->nbig;
-                        ctr->lvl_maxslice[lv] = ctr->max_slice;
-                        ctr->committed = 0;
-                        ctr->nbig = 0;
-                        ctr->max_slice = 0;
-                    });
-                ++launches;
-            }
+        for (int level = level0;; ++level) {
+            enqueue_level(level, npend, pcur, pnext, touched_ptr, n, cfg, ws, true, launches);
             pcur = pnext;
             pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
             const bool speculate = npend >= (1u << 16) && (level & 1) == 0 && level < height_;
@@ -2324,6 +2539,9 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // whole array re-placed: headers rebuilt in closed form already
         if (d_row_offsets) rebuild_row_offsets_full();
         ++launches;
+    } else if (graph_levels && !host_levels) {
+        // the graph refreshed the headers / row offsets and walked left
+        if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
     } else {
         if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
         const u64 nref = h_ctr->nrefresh;

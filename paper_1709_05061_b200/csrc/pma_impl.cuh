@@ -58,6 +58,7 @@ struct Ctr {
     ull gdel;       // graph front end: guard deletes (dropped, counted missed)
     ull bigrun;     // leaf-bucket front end: a bucket reached kRunMax updates
     ull nbig_buckets;  // leaf-bucket front end: buckets sorted by the CTA kernel
+    ull nsort;      // graph-captured small batches: the batch size, written by the front end
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
     // host sync (rounds may run back to back without one)
@@ -140,6 +141,16 @@ public:
     u64 count_valid_in(u64 b, u64 e);
     void slot_hash(int level, u64* hashes);
     void reserve_batch(u64 n);
+    // small graph batches (pma.cu): captured front end + first rounds
+    static constexpr u64 kSmallGraphMax = 4096;
+    static constexpr int kSmallIb = 13;  // index bits of the packed sort word ((1 << 13) - 1 > 4096: delete marker)
+    static constexpr int kSmallGraphLevels = 2;
+    bool small_graph_ok(u64 n, const GraphFront& gf) const;
+    std::vector<uintptr_t> small_graph_key(int db, const EngineCfg& cfg, int levels) const;
+    void capture_small_graph(int db, const EngineCfg& cfg, int levels);
+    int run_small_graph(const GraphFront& gf, const EngineCfg& cfg);
+    void enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
+                       ScanWorkspace& ws, bool events, u64& launches);
     int try_group(int level, u64 seg, const u64* keys, const u64* vals, const u8* ops, u64 n, const EngineCfg& cfg,
                   u64* missed, u64* tombs);
     void touched_ranges(u64* pairs, size_t cap, size_t* count);
@@ -241,6 +252,13 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u64> sk_in, sk_out;   // compressed keys
     DevBuf<u32> si_in, si_out;   // arrival index payload
     RadixWorkspace rws;           // onesweep radix sort (radix.cuh)
+    // small graph batches
+    bool small_graphs_ = true;          // GPMA_NO_GRAPHS=1 disables (A/B measurements)
+    cudaGraphExec_t small_exec_ = nullptr;
+    std::vector<uintptr_t> small_key_;  // what the captured graph embeds
+    GraphFront* h_desc_ = nullptr;      // page-locked batch descriptor (copied by the graph's first node)
+    GraphFront* d_desc_ = nullptr;
+    ScanWorkspace small_ws_;            // the graph's own look-back words (cleared by every replay)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
     // update bucket + ordinal, per sorted position bucket
     DevBuf<u32> bcnt, boff, blf, bod, bslf, bbig;

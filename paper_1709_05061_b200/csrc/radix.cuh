@@ -248,7 +248,8 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
 template <bool kVals>
 __global__ void __launch_bounds__(kRadixThreads, 1)
     k_radix_small(const u64* __restrict__ kin, u64* __restrict__ kout, const u32* __restrict__ vin,
-                  u32* __restrict__ vout, u32 n, int begin, int end) {
+                  u32* __restrict__ vout, u32 n, const ull* n_dev, int begin, int end) {
+    if (n_dev) n = u32(*n_dev);  // device-resident count (graph-captured small batches)
     extern __shared__ __align__(16) unsigned char smem[];
     using S = RadixSmem<kVals>;
     u64* sk = reinterpret_cast<u64*>(smem);
@@ -300,6 +301,33 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
     }
 }
 
+// Dynamic shared memory beyond 48 KB for the rank/scatter kernels, once per
+// device (the attribute is per function and device).
+inline void radix_prepare() {
+    static unsigned long long attr_set = 0;
+    int dev = 0;
+    GPMA_CUDA(cudaGetDevice(&dev));
+    if ((attr_set >> (dev & 63)) & 1ull) return;
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<true>::kBytes)));
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<false>::kBytes)));
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<true>::kBytes)));
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<false>::kBytes)));
+    attr_set |= 1ull << (dev & 63);
+}
+
+// Keys-only one-CTA sort of a device-resident count (<= kRadixTile) of keys:
+// one launch with no host-side size, for CUDA-graph-captured pipelines.
+inline void radix_sort_small_dev(cudaStream_t s, const u64* k0, u64* k1, const ull* n_dev, int begin, int end) {
+    radix_prepare();
+    k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, 0u, n_dev,
+                                                                           begin, end);
+    GPMA_LAUNCH_CHECK();
+}
+
 // Stable sort of n keys (+ payload when v0 != nullptr) by key bits
 // [begin, end).  Double-buffer contract: the input is in k0/v0, k1/v1 are the
 // alternate buffers (both may be overwritten); returns 1 when the result is
@@ -310,26 +338,14 @@ inline int radix_sort(cudaStream_t s, RadixWorkspace& ws, u64* k0, u64* k1, u32*
     const bool vals = v0 != nullptr;
     const int npass = (end - begin + 7) / 8;
     if (npass > kRadixMaxPasses) throw ApiError(PMA_EINVAL, "radix_sort: more than 64 key bits");
-    static unsigned long long attr_set = 0;  // per device: the attribute is per (function, device)
-    int dev = 0;
-    GPMA_CUDA(cudaGetDevice(&dev));
-    if (!((attr_set >> (dev & 63)) & 1ull)) {
-        GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(RadixSmem<true>::kBytes)));
-        GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(RadixSmem<false>::kBytes)));
-        GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(RadixSmem<true>::kBytes)));
-        GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(RadixSmem<false>::kBytes)));
-        attr_set |= 1ull << (dev & 63);
-    }
+    radix_prepare();
     if (n <= u64(kRadixTile)) {
         if (vals)
-            k_radix_small<true><<<1, kRadixThreads, RadixSmem<true>::kBytes, s>>>(k0, k1, v0, v1, u32(n), begin, end);
+            k_radix_small<true><<<1, kRadixThreads, RadixSmem<true>::kBytes, s>>>(k0, k1, v0, v1, u32(n), nullptr, begin,
+                                                                                  end);
         else
             k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, u32(n),
-                                                                                   begin, end);
+                                                                                   nullptr, begin, end);
         GPMA_LAUNCH_CHECK();
         if (launches) *launches += 1;
         return 1;
