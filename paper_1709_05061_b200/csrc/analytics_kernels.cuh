@@ -173,7 +173,8 @@ static __global__ void k_hot_select(const u32* __restrict__ outdeg, u64 n, u32 m
 static __global__ void __launch_bounds__(256) k_pr_push(const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
                                                         const double* __restrict__ share, double* __restrict__ y,
                                                         const u32* __restrict__ hot_table, const u32* __restrict__ hot_ids,
-                                                        u32 nhot) {
+                                                        u32 nhot, const u32* done = nullptr) {
+    if (done && *done) return;  // converged earlier in this window of iterations
     __shared__ u32 s_tab[2 * kHotTable];
     __shared__ double s_acc[kHotMax];
     __shared__ u64 s_q[8 * 256];  // the block's 8 warp queues

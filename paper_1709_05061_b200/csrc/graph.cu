@@ -319,9 +319,38 @@ __global__ void k_pr_prep(const double* __restrict__ x, const u32* __restrict__ 
 // base + pushed mass (base from the current dangling mass), L1 += |y - x|,
 // and already the next iteration's inputs — share = d y / outdeg, the next
 // dangling mass.
+// Gate of iteration `it` inside a window of iterations launched without a
+// host round trip: once the previous iteration's L1 residual fell below
+// epsilon (analytics.hpp:136-140 stops there) the sticky `done` flag turns
+// every later kernel of the window into a no-op; otherwise it clears the
+// push accumulator y and the next dangling sum.
+__global__ void k_pr_gate(const double* __restrict__ l1_prev, double eps, u32* done, double* __restrict__ y, u64 n,
+                          double* next_dangling) {
+    __shared__ bool skip;
+    if (threadIdx.x == 0) {
+        bool d = *done != 0;
+        if (!d && l1_prev && *l1_prev < eps) d = true;
+        skip = d;
+        if (d && blockIdx.x == 0) *done = 1;
+    }
+    __syncthreads();
+    if (skip) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *next_dangling = 0.0;
+    double2* y2 = reinterpret_cast<double2*>(y);
+    const u64 n2 = n / 2;
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n2; i += u64(gridDim.x) * blockDim.x)
+        y2[i] = make_double2(0.0, 0.0);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) y[n - 1] = 0.0;
+}
+
+__global__ void k_fill_f64(double* __restrict__ x, u64 n, double v) {
+    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) x[i] = v;
+}
+
 __global__ void k_pr_finish_next(double* __restrict__ x, double* __restrict__ y, const u32* __restrict__ outdeg, u64 n,
                                  double d, const double* dangling, double* next_dangling, double* l1,
-                                 double* __restrict__ share) {
+                                 double* __restrict__ share, const u32* done = nullptr) {
+    if (done && *done) return;
     const double nn = double(n);
     const double base = __dadd_rn(__ddiv_rn(1.0 - d, nn), __ddiv_rn(__dmul_rn(d, *dangling), nn));
     double acc = 0.0, dang = 0.0;
@@ -655,9 +684,8 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
     if (h_warm) {
         GPMA_CUDA(cudaMemcpyAsync(px.ptr, h_warm, nv * 8, cudaMemcpyHostToDevice, s));
     } else {
-        std::vector<double> x0(nv, 1.0 / double(nv));
-        GPMA_CUDA(cudaMemcpyAsync(px.ptr, x0.data(), nv * 8, cudaMemcpyHostToDevice, s));
-        GPMA_CUDA(cudaStreamSynchronize(s));
+        k_fill_f64<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(px.ptr, nv, 1.0 / double(nv));
+        GPMA_LAUNCH_CHECK();
     }
     GPMA_CUDA(cudaMemsetAsync(outdeg.ptr, 0, nv * 4, s));
     const u64 cap = pma.capacity();
@@ -669,43 +697,67 @@ void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, 
     double* x = px.ptr;
     double* y = py.ptr;
     *converged = 0;
-    u64 it;
+    u64 it = 1;
     pr_iter_ms_ = 0.0;
-    // psc = [dangling_A, l1_A, dangling_B, l1_B]: iteration parity p reads
-    // dangling at psc[2p] and produces the next dangling + this L1 at psc[2(1-p)]
+    // psc = [dangling_A, -, dangling_B, -]: iteration parity p reads the
+    // dangling sum at psc[2p] and produces the next one at psc[2(1-p)]; the L1
+    // residual of iteration i goes to the ring pl1[(i - 1) % kRing].
+    // Iterations run in windows of kWin without a host round trip: the gate
+    // of each iteration turns the rest of the window into no-ops once an L1
+    // fell below epsilon, and the host reads the window's residuals once.
+    constexpr u64 kWin = 4, kRing = 16;
     psc.reserve(4);
+    pl1.reserve(kRing);
+    pdone.reserve(1);
     GPMA_CUDA(cudaMemsetAsync(psc.ptr, 0, 32, s));
-    GPMA_CUDA(cudaMemsetAsync(y, 0, nv * 8, s));
+    GPMA_CUDA(cudaMemsetAsync(pdone.ptr, 0, 4, s));
     k_pr_prep<<<grid_for(nv, 256, 148 * 8), 256, 0, s>>>(x, outdeg.ptr, nv, d, pshare.ptr, psc.ptr);
     GPMA_LAUNCH_CHECK();
     ++launches;
-    for (it = 1; it <= max_iters; ++it) {
-        const int p = int(it & 1) ^ 1;  // it = 1 -> p = 0
-        double* cur = psc.ptr + 2 * p;
-        double* nxt = psc.ptr + 2 * (1 - p);
-        GPMA_CUDA(cudaMemsetAsync(nxt, 0, 16, s));
+    static const unsigned pr_res = resident_grid(k_pr_push, 256);  // measured best vs 0.5x / 2x
+    u64 last = 0;  // the iteration whose result is in x
+    while (it <= max_iters) {
+        const u64 win = std::min(kWin, max_iters - it + 1);
+        const u64 r0 = (it - 1) % kRing;
+        GPMA_CUDA(cudaMemsetAsync(pl1.ptr + r0, 0, win * 8, s));
         GPMA_CUDA(cudaEventRecord(pma_ev(2), s));
-        static const unsigned pr_res = resident_grid(k_pr_push, 256);  // measured best vs 0.5x / 2x
-        k_pr_push<<<pr_res, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr, nhot_);
-        // (148x4 CTAs: fewer per-CTA reductions; measured 1% better than 148x8)
-        k_pr_finish_next<<<grid_for(nv, 256, 148 * 4), 256, 0, s>>>(x, y, outdeg.ptr, nv, d, cur, nxt, nxt + 1,
-                                                                   pshare.ptr);
-        GPMA_LAUNCH_CHECK();
+        for (u64 j = 0; j < win; ++j) {
+            const u64 i = it + j;
+            const int p = int(i & 1) ^ 1;  // i = 1 -> p = 0
+            double* cur = psc.ptr + 2 * p;
+            double* nxt = psc.ptr + 2 * (1 - p);
+            const double* l1_prev = i > 1 ? pl1.ptr + (i - 2) % kRing : nullptr;
+            k_pr_gate<<<grid_for(nv / 2 + 1, 256, 148 * 4), 256, 0, s>>>(l1_prev, eps, pdone.ptr, y, nv, nxt);
+            k_pr_push<<<pr_res, 256, 0, s>>>(pma.d_keys, pma.d_st, cap, pshare.ptr, y, hot_table.ptr, hot_ids.ptr,
+                                             nhot_, pdone.ptr);
+            // (148x4 CTAs: fewer per-CTA reductions; measured 1% better than 148x8)
+            k_pr_finish_next<<<grid_for(nv, 256, 148 * 4), 256, 0, s>>>(x, y, outdeg.ptr, nv, d, cur, nxt,
+                                                                       pl1.ptr + (i - 1) % kRing, pshare.ptr,
+                                                                       pdone.ptr);
+            GPMA_LAUNCH_CHECK();
+            launches += 3;
+            std::swap(x, y);  // y (finished) is the next x; the gate clears the next accumulator
+        }
         GPMA_CUDA(cudaEventRecord(pma_ev(3), s));
-        launches += 2;
-        double l1 = 0;
-        GPMA_CUDA(cudaMemcpyAsync(&l1, nxt + 1, 8, cudaMemcpyDeviceToHost, s));
+        double l1[kWin] = {};
+        GPMA_CUDA(cudaMemcpyAsync(l1, pl1.ptr + r0, win * 8, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
         float ms = 0;
         cudaEventElapsedTime(&ms, pma_ev(2), pma_ev(3));
         pr_iter_ms_ += ms;
-        std::swap(x, y);  // y (finished) is the next x; x (zeroed) accumulates the next pushes
-        GPMA_CUDA(cudaMemsetAsync(y, 0, nv * 8, s));
-        if (l1 < eps) {
+        u64 j = 0;
+        while (j < win && !(l1[j] < eps)) ++j;
+        if (j < win) {  // iteration it + j converged; later ones were no-ops
             *converged = 1;
+            last = it + j;
             break;
         }
+        last = it + win - 1;
+        it += win;
     }
+    // iteration i finished into py when i is odd, px when even (x started as px)
+    x = last == 0 ? px.ptr : ((last & 1) ? py.ptr : px.ptr);
+    it = last;
     *iters = *converged ? it : max_iters;
     GPMA_CUDA(cudaEventRecord(pma_ev(1), s));
     GPMA_CUDA(cudaMemcpyAsync(h_ranks, x, nv * 8, cudaMemcpyDeviceToHost, s));

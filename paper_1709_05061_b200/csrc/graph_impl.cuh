@@ -62,7 +62,8 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u64> bk, bv;
     DevBuf<u8> bo;
     DevBuf<u32> dist, q0, q1, h0, h1, qn, outdeg;
-    DevBuf<double> px, py, pshare, psc;
+    DevBuf<double> px, py, pshare, psc, pl1;
+    DevBuf<u32> pdone;
     DevBuf<u32> rt_counts, hot_table, hot_ids, hot_hist;
     u32 nhot_ = 0;
     bool hot_ready_ = false;

@@ -70,6 +70,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     GPMA_CUDA(cudaMallocHost(&h_desc_, sizeof(GraphFront)));
     GPMA_CUDA(cudaMalloc(&d_desc_, sizeof(GraphFront)));
     if (const char* e = std::getenv("GPMA_NO_GRAPHS")) small_graphs_ = e[0] == '0';
+    if (const char* e = std::getenv("GPMA_NO_BUCKETS")) buckets_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     for (auto& e : lev_ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -2123,7 +2124,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // over the n updates (measured: C2 and C3 gain, C4's 33.5M and C5's
         // 16.7M leaves lose).
         bucket = ro_base() && n >= kBucketMinBatch && n < (1ull << 31) && L <= kBucketMaxLeaves &&
-                 L <= 8 * n && bucket_skip_ == 0;
+                 L <= 8 * n && bucket_skip_ == 0 && buckets_;
         if (bucket_skip_) --bucket_skip_;
         if (bucket) {
             bcnt.reserve(L + 2);

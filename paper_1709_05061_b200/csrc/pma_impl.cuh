@@ -263,6 +263,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     // update bucket + ordinal, per sorted position bucket
     DevBuf<u32> bcnt, boff, blf, bod, bslf, bbig;
     int bucket_skip_ = 0;  // batches left on the radix sort after a bucket overflow
+    bool buckets_ = true;  // GPMA_NO_BUCKETS=1: always the radix front end (A/B measurements)
     static constexpr u64 kBucketMinBatch = 1u << 16;
     static constexpr u64 kBucketMaxLeaves = 8ull << 20;  // 64 MB of leaf headers
     static constexpr int kBucketCooldown = 16;
