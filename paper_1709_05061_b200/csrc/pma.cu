@@ -1925,7 +1925,7 @@ std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int le
     std::vector<uintptr_t> k;
     for (const void* p : ptrs) k.push_back(reinterpret_cast<uintptr_t>(p));
     const u64 vals[] = {cap_, leaf_, u64(height_), ro_lo, num_vertices, u64(db), u64(cfg.eager), cfg.small_max,
-                        cfg.medium_max, u64(cfg.force), u64(levels)};
+                        cfg.medium_max, u64(cfg.force), u64(levels), u64(empty_leaves != 0)};
     for (const u64 v : vals) k.push_back(uintptr_t(v));
     return k;
 }
@@ -1948,7 +1948,9 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
         k_prep_graph_dev<<<kSmallGraphMax / 256, 256, 0, stream_>>>(d_desc_, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
         GPMA_LAUNCH_CHECK();
-        radix_sort_small_dev(stream_, sk_in.ptr, sk_out.ptr, &d_ctr->nsort, ib, ib + nbits);
+        static_assert(kSmallGraphMax <= kBitonicMax, "small graph batches sort in one CTA");
+        k_bitonic_small<<<1, 1024, 0, stream_>>>(sk_in.ptr, sk_out.ptr, &d_ctr->nsort);
+        GPMA_LAUNCH_CHECK();
         {
             // duplicate resolution as in batch_update_device (packed words:
             // key << ib | arrival index, all-ones index = a delete)
@@ -1967,7 +1969,14 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
             u64* o_k = uk.ptr;
             u64* o_v = uv.ptr;
             u8* o_o = uop.ptr;
+            u32* o_l = ul.ptr;
             Ctr* ctr = d_ctr;
+            const u64* hdr = d_hdr;
+            const u64 L = num_leaves();
+            const u8* stt = d_st;
+            const u64 lf = leaf_;
+            const u64* ro = ro_base();
+            const u64 rlo = ro_lo, rhi = ro_lo + num_vertices;
             run_compact_tile(
                 stream_, small_ws_, ndp, 0, kSmallGraphMax,
                 [=] __device__(ull i) {
@@ -1994,9 +2003,12 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
                         }
                         const u32 a = p >> 1;
                         const bool ins = p & 1u;
-                        o_k[xs[j]] = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
+                        const u64 key = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
+                        o_k[xs[j]] = key;
                         o_v[xs[j]] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
                         o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
+                        // the leaf of the unique update (pma.hpp:234-289), fused
+                        o_l[xs[j]] = u32(leaf_for_key(key, hdr, L, stt, lf, ro, rlo, rhi));
                     }
                 },
                 [=] __device__(ull total) {
@@ -2004,9 +2016,6 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
                     ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
                 });
         }
-        k_leaf_search_sorted<<<kSmallGraphMax / 256, 256, 0, stream_>>>(
-            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
-        GPMA_LAUNCH_CHECK();
         u32* pcur = nullptr;
         u32* pnext = pidx0.ptr;
         for (int level = 0; level < levels; ++level) {
@@ -2018,8 +2027,10 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         k_refresh_ranges<<<64, 256, 0, stream_>>>(rlist.ptr, &d_ctr->nrefresh, 0, d_keys, d_st, cap_, leaf_, d_hdr,
                                                   ro_base());
         GPMA_LAUNCH_CHECK();
-        k_left_walk<<<16, 128, 0, stream_>>>(touched.ptr, 0, d_st, leaf_, d_hdr, &d_ctr->ntouched_next);
-        GPMA_LAUNCH_CHECK();
+        if (empty_leaves != 0) {  // headers of empty leaves inherit the next leaf's first key
+            k_left_walk<<<16, 128, 0, stream_>>>(touched.ptr, 0, d_st, leaf_, d_hdr, &d_ctr->ntouched_next);
+            GPMA_LAUNCH_CHECK();
+        }
         GPMA_CUDA(cudaMemcpyAsync(h_ctr, d_ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, stream_));
     } catch (...) {
         cudaStreamEndCapture(stream_, &graph);

@@ -144,7 +144,7 @@ public:
     // small graph batches (pma.cu): captured front end + first rounds
     static constexpr u64 kSmallGraphMax = 4096;
     static constexpr int kSmallIb = 13;  // index bits of the packed sort word ((1 << 13) - 1 > 4096: delete marker)
-    static constexpr int kSmallGraphLevels = 2;
+    static constexpr int kSmallGraphLevels = 1;  // most small batches finish in round 0; more rounds: host loop
     bool small_graph_ok(u64 n, const GraphFront& gf) const;
     std::vector<uintptr_t> small_graph_key(int db, const EngineCfg& cfg, int levels) const;
     void capture_small_graph(int db, const EngineCfg& cfg, int levels);
