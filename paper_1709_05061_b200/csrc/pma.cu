@@ -1969,14 +1969,7 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
             u64* o_k = uk.ptr;
             u64* o_v = uv.ptr;
             u8* o_o = uop.ptr;
-            u32* o_l = ul.ptr;
             Ctr* ctr = d_ctr;
-            const u64* hdr = d_hdr;
-            const u64 L = num_leaves();
-            const u8* stt = d_st;
-            const u64 lf = leaf_;
-            const u64* ro = ro_base();
-            const u64 rlo = ro_lo, rhi = ro_lo + num_vertices;
             run_compact_tile(
                 stream_, small_ws_, ndp, 0, kSmallGraphMax,
                 [=] __device__(ull i) {
@@ -2007,8 +2000,6 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
                         o_k[xs[j]] = key;
                         o_v[xs[j]] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
                         o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
-                        // the leaf of the unique update (pma.hpp:234-289), fused
-                        o_l[xs[j]] = u32(leaf_for_key(key, hdr, L, stt, lf, ro, rlo, rhi));
                     }
                 },
                 [=] __device__(ull total) {
@@ -2016,6 +2007,11 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
                     ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
                 });
         }
+        // leaf of every unique update (pma.hpp:234-289): a thread per key, the
+        // dependent header loads of different keys in flight together
+        k_leaf_search_sorted<<<kSmallGraphMax / 256, 256, 0, stream_>>>(
+            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
+        GPMA_LAUNCH_CHECK();
         u32* pcur = nullptr;
         u32* pnext = pidx0.ptr;
         for (int level = 0; level < levels; ++level) {
