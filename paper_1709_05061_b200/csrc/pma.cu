@@ -2669,6 +2669,19 @@ void Pma::reserve_batch(u64 n) {
     ir.reserve(n);
     biglist.reserve(n + 1);
     ensure_slot_scratch();
+    // look-back words of the compactions / exclusive sums and the radix
+    // sort's per-tile digit words (the first batch would allocate them)
+    const u64 tiles = std::max<u64>(n, L + 2) / kScanTile + 2;
+    if (tiles > ws.tiles.cap) {
+        ws.tiles.reserve(tiles);
+        GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), stream_));
+    }
+    const u64 rt = (n / kRadixTile + 2) * kRadixBins;
+    if (rt > rws.status.cap) {
+        rws.status.reserve(rt);
+        GPMA_CUDA(cudaMemsetAsync(rws.status.ptr, 0, rws.status.cap * sizeof(ull), stream_));
+    }
+    rws.hist.reserve(kRadixMaxPasses * kRadixBins);
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 
