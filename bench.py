@@ -331,7 +331,7 @@ def run_ours(args):
     def make_graph():
         gr = pg.DynamicGraph.from_edges_device(nvx, info.stream_src, info.stream_dst, None, info.initial_size,
                                                device=dev)
-        gr.pma().reserve_batch(2 * B + 16)  # a slide = B inserts + <= B deletes: no allocation in a step
+        gr.reserve_batch(2 * B + 16)  # a slide = B inserts + <= B deletes: no allocation in a step
         return gr
 
     t1 = time.time()

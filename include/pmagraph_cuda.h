@@ -269,6 +269,11 @@ int gpma_apply_batch_device(gpma_graph* g, const uint32_t* d_ins_src, const uint
                             const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
                             const uint32_t* d_del_dst, size_t n_del, pma_stats* out);
 
+/* pma_reserve_batch for the graph: every per-batch buffer of apply_batch
+ * for batches of up to max_updates inserts + deletes, so no allocation lands
+ * inside a later call (no reference counterpart; state unchanged). */
+int gpma_reserve_batch(gpma_graph* g, size_t max_updates);
+
 /* row_offsets() (graph.hpp:97): num_vertices + 1 entries. */
 int gpma_row_offsets(gpma_graph* g, uint64_t* out);
 /* rebuild_row_offsets() (graph.hpp:182-190). */

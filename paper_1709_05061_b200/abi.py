@@ -200,6 +200,7 @@ SIGNATURES = [
     ("gpma_num_edges", C.c_uint64, [_P]),
     ("gpma_apply_batch", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
     ("gpma_apply_batch_device", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t, C.POINTER(pma_stats)]),
+    ("gpma_reserve_batch", C.c_int, [_P, C.c_size_t]),
     ("gpma_row_offsets", C.c_int, [_P, _P]),
     ("gpma_rebuild_row_offsets", C.c_int, [_P]),
     ("gpma_csr_snapshot", C.c_int, [_P, _P, _P, _P]),

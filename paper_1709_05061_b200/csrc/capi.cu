@@ -205,6 +205,13 @@ int pma_try_insert_plus(pma_handle* h, int level, size_t seg, const uint64_t* ke
     });
 }
 
+int gpma_reserve_batch(gpma_graph* g, size_t max_updates) {
+    return guarded(err_of(g), [&] {
+        GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
+        g->impl->reserve_batch(max_updates);
+    });
+}
+
 int pma_reserve_batch(pma_handle* h, size_t max_updates) {
     return guarded(err_of(h), [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));

@@ -482,6 +482,13 @@ Graph::~Graph() {
 }
 
 // DynamicGraph::apply_batch (graph.hpp:130-162)
+void Graph::reserve_batch(u64 n) {
+    bk.reserve(n + 1);
+    bv.reserve(n + 1);
+    bo.reserve(n + 1);
+    pma.reserve_batch(n);
+}
+
 void Graph::apply_batch_device(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
                                u64 nd, pma_stats* out) {
     apply_batch_impl(is, id, nullptr, iw, ni, ds, dd, nd, out);

@@ -32,6 +32,7 @@ public:
 
     // key-range sharding (shard.cu): routing partition and the device steps of
     // the sharded analytics (collectives run in the caller between them)
+    void reserve_batch(u64 n);  // every per-batch buffer of apply_batch for n updates
     void route_partition(const u32* is, const u32* id, const double* iw, u64 ni, const u32* ds, const u32* dd,
                          u64 nd, const u32* d_bounds, int world, u64* okeys, double* ow, u64* h_counts,
                          u64* d_counts = nullptr);

@@ -418,6 +418,10 @@ class DynamicGraph:
                                                       vp(d_ds), vp(d_dd), nd, C.byref(st)))
         return UpdateStats.from_c(st)
 
+    def reserve_batch(self, max_updates: int):
+        """Pre-size every per-batch buffer of apply_batch (gpma_reserve_batch)."""
+        self._check(self._lib.gpma_reserve_batch(self.h, max_updates))
+
     def row_offsets(self):
         out = np.zeros(self._nv + 1, np.uint64)
         self._check(self._lib.gpma_row_offsets(self.h, _p(out)))

@@ -30,7 +30,7 @@ def main():
 
     def run(tag, with_timing, sampler, n=12):
         g = pg.DynamicGraph.from_edges_device(cfg["nv"], info.stream_src, info.stream_dst, None, info.initial_size)
-        g.pma().reserve_batch(2 * B + 16)
+        g.reserve_batch(2 * B + 16)
         ext = torch.cuda.ExternalStream(g._lib.gpma_cuda_stream(g.h), device=torch.device("cuda", 0))
         for s in slides[:3]:
             bench_apply(g, info, s)

@@ -28,7 +28,7 @@ def main():
 
     def make():
         g = pg.DynamicGraph.from_edges_device(cfg["nv"], info.stream_src, info.stream_dst, None, info.initial_size)
-        g.pma().reserve_batch(2 * B + 16)
+        g.reserve_batch(2 * B + 16)
         return g
 
     def run(tag, g, sl):
