@@ -1766,12 +1766,12 @@ void Pma::rebuild_at_capacity(u64 cap) {
 // reads its counts on the device; npend is a host-known upper bound of the
 // pending count.  events: record the level's commit span (lev_ev_).
 void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
-                        ScanWorkspace& ws, bool events, u64& launches, bool grouped) {
+                        ScanWorkspace& ws, bool events, u64& launches) {
     const u64 m = leaf_ << level;
     ull* np_cur = &d_ctr->np[level & 1];
     ull* np_next = &d_ctr->np[(level + 1) & 1];
-    // group = segment heads (unique_segments); `grouped`: done by the caller
-    if (!grouped) {
+    // group = segment heads (unique_segments)
+    {
         const u32* ulp = ul.ptr;
         const u32* pp = pcur;
         u32* gs = gstart.ptr;
@@ -1901,199 +1901,6 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
     }
 }
 
-// ---- small graph batches: the whole front end in one CTA ---------------
-// Pack + checks (prep_word), bitonic sort of the packed words, duplicate
-// resolution (run ends, block scan), the leaf of every unique update
-// (lock-stepped bisections, pma.hpp:234-289) and round 0's grouping
-// (unique_segments at the leaf level, segment_engine.hpp:78-86) for a batch of
-// <= kSmallFrontMax updates, with block scans instead of device-wide passes:
-// the same arrays and counters the multi-kernel front end produces.
-constexpr int kSmallThreads = 1024;
-constexpr int kSmallFrontMax = 4096;
-constexpr int kSmallPer = kSmallFrontMax / kSmallThreads;  // items per thread (blocked)
-constexpr int kSmallFrontSmem = kSmallFrontMax * 8 + kSmallFrontMax * 4 + 32 * 4;
-
-struct SmallFrontArgs {
-    const GraphFront* f;
-    int db, ib;
-    u64* ck;  // packed words (global scratch, n)
-    u64* uk;
-    u64* uv;
-    u8* uop;
-    u32* ul;
-    u32* gstart;
-    u32* gseg;
-    u32* gid;
-    Ctr* ctr;
-    const u64* hdr;
-    u64 L;
-    const u8* st;
-    u64 leaf;
-    const u64* ro;
-    u64 rlo, rhi;
-};
-
-__global__ void __launch_bounds__(kSmallThreads, 1) k_small_front(SmallFrontArgs A) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    u64* s = reinterpret_cast<u64*>(smem_raw);                // sorted words, then unique keys
-    u32* sl = reinterpret_cast<u32*>(s + kSmallFrontMax);     // leaf of each unique update
-    u32* s_w = sl + kSmallFrontMax;                           // block-scan scratch (32)
-    __shared__ ull s_gate;
-    const GraphFront f = *A.f;
-    const u32 n = u32(f.ni + f.nd);
-    const unsigned t = threadIdx.x;
-    // ---- pack + checks (counters via atomics, as the multi-CTA front end)
-    prep_graph_body<false>(f, A.db, A.ib, A.ck, nullptr, A.ctr, BucketArgs{});
-    __syncthreads();
-    u32 P = 2;
-    while (P < n) P <<= 1;
-    for (u32 i = t; i < P; i += kSmallThreads) s[i] = i < n ? A.ck[i] : ~0ull;
-    if (t == 0) {  // (L2 reads of the counters the block's atomics just set)
-        const volatile Ctr* vc = A.ctr;
-        s_gate = (vc->bad_ins || vc->oor) ? 1ull : 0ull;
-    }
-    __syncthreads();
-    // ---- bitonic sort (all words distinct: the arrival index breaks ties)
-    for (u32 k = 2; k <= P; k <<= 1) {
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
-            for (u32 i = t; i < P; i += kSmallThreads) {
-                const u32 ixj = i ^ j;
-                if (ixj > i) {
-                    const u64 a = s[i], b = s[ixj];
-                    if ((a > b) == ((i & k) == 0)) {
-                        s[i] = b;
-                        s[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    // ---- duplicate resolution (segment_engine.hpp:346-363): run ends of
-    // equal keys, the last insert wins; items blocked per thread
-    const int ib = A.ib, gdb = A.db;
-    const u64 skipkey = 1ull << (2 * gdb);
-    const u64 pmask = (1ull << ib) - 1;
-    auto KEY = [&](u32 i) -> u64 { return s[i] >> ib; };
-    auto PAY = [&](u32 i) -> u32 {
-        const u32 a = u32(s[i] & pmask);
-        return (a << 1) | (a != u32(pmask) ? 1u : 0u);
-    };
-    bool fl[kSmallPer];
-    u32 cnt = 0;
-#pragma unroll
-    for (int q = 0; q < kSmallPer; ++q) {
-        const u32 i = t * kSmallPer + q;
-        fl[q] = i < n && ((i + 1 == n) || KEY(i + 1) != KEY(i)) && KEY(i) < skipkey;
-        cnt += fl[q];
-    }
-    u32 total;
-    u32 x = block_excl_scan(cnt, &total, s_w);
-    const u32 nu = total;
-    u64 ukey[kSmallPer];
-    u32 upos[kSmallPer];
-#pragma unroll
-    for (int q = 0; q < kSmallPer; ++q) {
-        upos[q] = ~0u;
-        if (!fl[q]) continue;
-        const u32 i = t * kSmallPer + q;
-        const u64 c = KEY(i);
-        u32 p = PAY(i);
-        if (!(p & 1u) && i > 0 && KEY(i - 1) == c) {
-            for (int tt = int(i) - 1; tt >= 0 && KEY(u32(tt)) == c; --tt) {
-                const u32 qq = PAY(u32(tt));
-                if (qq & 1u) {
-                    p = qq;
-                    break;
-                }
-            }
-        }
-        const u32 a = p >> 1;
-        const bool ins = p & 1u;
-        const u64 key = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
-        A.uk[x] = key;
-        A.uv[x] = ins ? u64(__double_as_longlong(f.iw ? f.iw[a] : 1.0)) : 0;
-        A.uop[x] = ins ? kOpInsert : kOpDelete;
-        ukey[q] = key;
-        upos[q] = x;
-        ++x;
-    }
-    if (t == 0) {
-        A.ctr->n_unique = nu;
-        A.ctr->np[0] = s_gate ? 0ull : nu;
-    }
-    // ---- the leaf of every unique update: up to kSmallPer lock-stepped
-    // bisections per thread (row-offset bracket first, as leaf_for_key)
-    {
-        u64 lo[kSmallPer], hi[kSmallPer];
-#pragma unroll
-        for (int q = 0; q < kSmallPer; ++q) {
-            lo[q] = 0;
-            hi[q] = 1;
-            if (upos[q] == ~0u) continue;
-            const u64 key = ukey[q], u = key >> 32;
-            if (A.ro && u >= A.rlo && u < A.rhi && !is_guard(key)) {
-                const u64 ra = __ldg(&A.ro[u]), rb = __ldg(&A.ro[u + 1]);
-                lo[q] = ra ? (ra - 1) / A.leaf : 0;
-                hi[q] = (rb - 1) / A.leaf + 1;
-                if (hi[q] > A.L) hi[q] = A.L;
-            } else {
-                lo[q] = leaf_for_key(key, A.hdr, A.L, A.st, A.leaf, A.ro, A.rlo, A.rhi);
-                hi[q] = lo[q] + 1;
-            }
-        }
-        for (;;) {
-            bool more = false;
-#pragma unroll
-            for (int q = 0; q < kSmallPer; ++q) {
-                if (hi[q] - lo[q] > 1) {
-                    const u64 mid = (lo[q] + hi[q]) >> 1;
-                    if (__ldg(&A.hdr[mid]) <= ukey[q]) lo[q] = mid;
-                    else hi[q] = mid;
-                    more |= hi[q] - lo[q] > 1;
-                }
-            }
-            if (!more) break;
-        }
-        __syncthreads();  // the sorted words are dead: s holds nothing needed from here
-#pragma unroll
-        for (int q = 0; q < kSmallPer; ++q) {
-            if (upos[q] == ~0u) continue;
-            A.ul[upos[q]] = u32(lo[q]);
-            sl[upos[q]] = u32(lo[q]);
-        }
-    }
-    __syncthreads();
-    // ---- round 0 grouping: segment heads of the unique updates (level 0)
-    const u32 np0 = s_gate ? 0u : nu;
-    bool hd[kSmallPer];
-    u32 hc = 0;
-#pragma unroll
-    for (int q = 0; q < kSmallPer; ++q) {
-        const u32 pidx = t * kSmallPer + q;
-        hd[q] = pidx < np0 && (pidx == 0 || sl[pidx] != sl[pidx - 1]);
-        hc += hd[q];
-    }
-    u32 gtot;
-    u32 gx = block_excl_scan(hc, &gtot, s_w);
-#pragma unroll
-    for (int q = 0; q < kSmallPer; ++q) {
-        const u32 pidx = t * kSmallPer + q;
-        if (pidx >= np0) continue;
-        if (hd[q]) {
-            A.gstart[gx] = pidx;
-            A.gseg[gx] = sl[pidx];
-            ++gx;
-        }
-        A.gid[pidx] = gx - 1;
-    }
-    if (t == 0) {
-        A.ctr->ngroups = gtot;
-        A.gstart[gtot] = np0;
-        A.ctr->lvl_npend[0] = np0;
-    }
-}
-
 // ---- small graph batches ----------------------------------------------
 // A batch of up to kSmallGraphMax graph updates is latency-bound: a dozen
 // tiny kernels whose cost is their launches and the host round trips between
@@ -2129,11 +1936,8 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         small_exec_ = nullptr;
     }
     const int ib = kSmallIb;
-    static unsigned long long attr = 0;  // > 48 KB of dynamic shared memory (per function and device)
-    if (!((attr >> (device_ & 63)) & 1ull)) {
-        GPMA_CUDA(cudaFuncSetAttribute(k_small_front, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallFrontSmem));
-        attr |= 1ull << (device_ & 63);
-    }
+    const int nbits = 2 * db + 1;
+    radix_prepare();
     u64 dummy = 0;
     cudaGraph_t graph = nullptr;
     GPMA_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
@@ -2142,17 +1946,76 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         // the graph's own look-back words start clean on every replay
         GPMA_CUDA(cudaMemsetAsync(small_ws_.tiles.ptr, 0, small_ws_.tiles.cap * sizeof(ull), stream_));
         GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
-        static_assert(kSmallGraphMax <= kSmallFrontMax, "small graph batches run their front end in one CTA");
-        SmallFrontArgs fa{d_desc_, db,    ib,         sk_in.ptr, uk.ptr,  uv.ptr,        uop.ptr,
-                          ul.ptr,  gstart.ptr, gseg.ptr, gid.ptr, d_ctr, d_hdr, num_leaves(),
-                          d_st,    leaf_, ro_base(), ro_lo,     ro_lo + num_vertices};
-        k_small_front<<<1, kSmallThreads, kSmallFrontSmem, stream_>>>(fa);
+        k_prep_graph_dev<<<kSmallGraphMax / 256, 256, 0, stream_>>>(d_desc_, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
+        GPMA_LAUNCH_CHECK();
+        static_assert(kSmallGraphMax <= kBitonicMax, "small graph batches sort in one CTA");
+        k_bitonic_small<<<1, 1024, 0, stream_>>>(sk_in.ptr, sk_out.ptr, &d_ctr->nsort);
+        GPMA_LAUNCH_CHECK();
+        {
+            // duplicate resolution as in batch_update_device (packed words:
+            // key << ib | arrival index, all-ones index = a delete)
+            const u64* ck = sk_out.ptr;
+            const GraphFront* fd = d_desc_;
+            const ull* ndp = &d_ctr->nsort;
+            const int gdb = db;
+            const u64 skipkey = 1ull << (nbits - 1);
+            const int pib = ib;
+            const u64 pmask = (1ull << pib) - 1;
+            auto KEY = [=] __device__(ull i) -> u64 { return ck[i] >> pib; };
+            auto PAY = [=] __device__(ull i) -> u32 {
+                const u32 a = u32(ck[i] & pmask);
+                return (a << 1) | (a != u32(pmask) ? 1u : 0u);
+            };
+            u64* o_k = uk.ptr;
+            u64* o_v = uv.ptr;
+            u8* o_o = uop.ptr;
+            Ctr* ctr = d_ctr;
+            run_compact_tile(
+                stream_, small_ws_, ndp, 0, kSmallGraphMax,
+                [=] __device__(ull i) {
+                    const ull nn = *ndp;
+                    const u64 c = KEY(i);
+                    return ((i + 1 == nn) || KEY(i + 1) != c) && c < skipkey;
+                },
+                [=] __device__(ull i0, ull nn, unsigned fm, const ull* xs) {
+                    const double* gw = fd->iw;
+#pragma unroll
+                    for (int j = 0; j < kScanItems; ++j) {
+                        if (!((fm >> j) & 1u)) continue;
+                        const ull i = i0 + ull(j) * kScanThreads;
+                        const u64 c = KEY(i);
+                        u32 p = PAY(i);
+                        if (!(p & 1u) && i > 0 && KEY(i - 1) == c) {
+                            for (long long t = (long long)i - 1; t >= 0 && KEY(t) == c; --t) {
+                                const u32 q = PAY(t);
+                                if (q & 1u) {
+                                    p = q;
+                                    break;
+                                }
+                            }
+                        }
+                        const u32 a = p >> 1;
+                        const bool ins = p & 1u;
+                        const u64 key = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
+                        o_k[xs[j]] = key;
+                        o_v[xs[j]] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
+                        o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
+                    }
+                },
+                [=] __device__(ull total) {
+                    ctr->n_unique = total;
+                    ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
+                });
+        }
+        // leaf of every unique update (pma.hpp:234-289): a thread per key, the
+        // dependent header loads of different keys in flight together
+        k_leaf_search_sorted<<<kSmallGraphMax / 256, 256, 0, stream_>>>(
+            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
         GPMA_LAUNCH_CHECK();
         u32* pcur = nullptr;
         u32* pnext = pidx0.ptr;
         for (int level = 0; level < levels; ++level) {
-            enqueue_level(level, kSmallGraphMax, pcur, pnext, touched.ptr, kSmallGraphMax, cfg, small_ws_, false, dummy,
-                          level == 0);
+            enqueue_level(level, kSmallGraphMax, pcur, pnext, touched.ptr, kSmallGraphMax, cfg, small_ws_, false, dummy);
             pcur = pnext;
             pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
         }

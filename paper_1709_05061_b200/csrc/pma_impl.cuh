@@ -150,7 +150,7 @@ public:
     void capture_small_graph(int db, const EngineCfg& cfg, int levels);
     int run_small_graph(const GraphFront& gf, const EngineCfg& cfg);
     void enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
-                       ScanWorkspace& ws, bool events, u64& launches, bool grouped = false);
+                       ScanWorkspace& ws, bool events, u64& launches);
     int try_group(int level, u64 seg, const u64* keys, const u64* vals, const u8* ops, u64 n, const EngineCfg& cfg,
                   u64* missed, u64* tombs);
     void touched_ranges(u64* pairs, size_t cap, size_t* count);
