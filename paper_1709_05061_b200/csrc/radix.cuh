@@ -215,13 +215,27 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     }
     ull excl = 0;
     if (tile > 0) {
-        const ull* p = status + (tile - 1) * kRadixBins + t;
-        for (;;) {
-            ull st = ld_volatile(p);
-            while ((st & ~((1ull << kEpochShift) - 1)) != ep || ((st >> kFlagShift) & 3ull) == 0) st = ld_volatile(p);
-            excl += st & kValueMask;
-            if (((st >> kFlagShift) & 3ull) == 2) break;
-            p -= kRadixBins;
+        // walk back kLook tiles per step with the loads of a step in flight
+        // together (a serial walk costs one L2 round trip per tile, and the
+        // first wave of tiles has no inclusive predecessor nearby)
+        constexpr int kLook = 8;
+        const ull inclusive0 = ep | (2ull << kFlagShift);  // "tile -1": inclusive prefix 0
+        auto ready = [&](ull w) { return (w & ~((1ull << kEpochShift) - 1)) == ep && ((w >> kFlagShift) & 3ull); };
+        long long j = (long long)tile - 1;
+        bool found = false;
+        while (!found) {
+            ull w[kLook];
+#pragma unroll
+            for (int q = 0; q < kLook; ++q)
+                w[q] = j - q >= 0 ? ld_volatile(status + u64(j - q) * kRadixBins + t) : inclusive0;
+#pragma unroll
+            for (int q = 0; q < kLook; ++q) {
+                if (found) continue;
+                while (!ready(w[q])) w[q] = ld_volatile(status + u64(j - q) * kRadixBins + t);
+                excl += w[q] & kValueMask;
+                found = ((w[q] >> kFlagShift) & 3ull) == 2;
+            }
+            j -= kLook;
         }
         st_volatile(my, ep | (2ull << kFlagShift) | (excl + count));
     }
