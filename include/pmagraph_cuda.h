@@ -394,6 +394,49 @@ int gpma_pr_finish(gpma_graph* g, const double* d_x, double* d_y, size_t n, cons
  * [lo, hi), same ordered accumulation as gpma_spmv. */
 int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local);
 
+/* ---- shard group: the sharded store with its collectives in the library
+ * (SURVEY §8b gpma_shard_group_*, §8e).  One process per GPU; each rank owns
+ * the source range [bounds[rank], bounds[rank+1]) (world + 1 host entries,
+ * bounds[0] = 0, bounds[world] = num_vertices <= 2^31).  The library issues
+ * the NCCL collectives itself on the shard's stream: per batch a count
+ * exchange + a grouped send/recv all-to-all of EdgeKeys (+ weights) and one
+ * scalar all-reduce (bad inserts reject the batch on every rank before any
+ * shard applies); BFS reduce-scatters candidate flags to the owners and
+ * gathers the distances, CC all-reduces MIN labels, PageRank all-reduces SUM
+ * contributions.  NCCL is bound at run time (libnccl.so.2): without it these
+ * entries return PMA_ECUDA, everything else works.  Errors:
+ * gpma_shard_group_last_error(). */
+typedef struct gpma_shard_group gpma_shard_group;
+/* ncclGetUniqueId into 128 bytes (rank 0 creates it; the caller broadcasts it). */
+int gpma_nccl_unique_id(void* id128);
+/* DynamicGraph::from_edges (graph.hpp:66-92) for this rank's shard; the
+ * communicator is the caller's ncclComm_t (nccl_comm, not owned) or created
+ * from nccl_id128 (owned).  Every rank may pass the same global edge list. */
+int gpma_shard_group_create(const gpma_graph_config* cfg, int device, size_t num_vertices, const uint32_t* bounds,
+                            int world, int rank, const void* nccl_id128, void* nccl_comm, const uint32_t* d_src,
+                            const uint32_t* d_dst, const double* d_weights, size_t n, gpma_shard_group** out);
+int gpma_shard_group_destroy(gpma_shard_group* g);
+const char* gpma_shard_group_last_error(const gpma_shard_group* g);
+/* This rank's shard as a graph handle (row offsets, slots, stats, stream). */
+gpma_graph* gpma_shard_group_graph(gpma_shard_group* g);
+/* DynamicGraph::apply_batch (graph.hpp:130-162) of this rank's share of a
+ * global batch (device arrays): routed to the owners, applied by each owner.
+ * stats: this shard's UpdateStats; *routed: updates this shard applied;
+ * *sent: updates this rank sent to other ranks. */
+int gpma_shard_group_apply_batch(gpma_shard_group* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
+                                 const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
+                                 const uint32_t* d_del_dst, size_t n_del, pma_stats* stats, uint64_t* routed,
+                                 uint64_t* sent);
+/* bfs (analytics.hpp:22-48): dist (host, num_vertices, may be NULL) on every rank. */
+int gpma_shard_group_bfs(gpma_shard_group* g, uint32_t root, uint32_t* dist, uint64_t* reached);
+/* connected_components (analytics.hpp:53-82): labels (host, num_vertices). */
+int gpma_shard_group_cc(gpma_shard_group* g, uint32_t* labels);
+/* pagerank (analytics.hpp:84-143) on every rank (host vectors). */
+int gpma_shard_group_pagerank(gpma_shard_group* g, double damping, double epsilon, size_t max_iters,
+                              const double* warm, double* ranks, uint64_t* iterations, int* converged);
+/* spmv (analytics.hpp:147-158): y on every rank (host vectors). */
+int gpma_shard_group_spmv(gpma_shard_group* g, const double* x, double* y);
+
 /* Drive every kernel once on small synthetic inputs so CUDA's lazy module
  * loading never lands inside a timed region (call once per process/device). */
 int gpma_warmup(int device);

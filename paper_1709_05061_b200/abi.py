@@ -231,6 +231,19 @@ SIGNATURES = [
     ("gpma_shard_pr_push", C.c_int, [_P, _P, _P, C.c_double, _P]),
     ("gpma_pr_finish", C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_double, C.POINTER(C.c_double)]),
     ("gpma_shard_spmv", C.c_int, [_P, _P, _P]),
+    ("gpma_nccl_unique_id", C.c_int, [_P]),
+    ("gpma_shard_group_create", C.c_int, [C.POINTER(gpma_graph_config), C.c_int, C.c_size_t, _P, C.c_int, C.c_int,
+                                          _P, _P, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
+    ("gpma_shard_group_destroy", C.c_int, [_P]),
+    ("gpma_shard_group_last_error", C.c_char_p, [_P]),
+    ("gpma_shard_group_graph", _P, [_P]),
+    ("gpma_shard_group_apply_batch", C.c_int, [_P, _P, _P, _P, C.c_size_t, _P, _P, C.c_size_t,
+                                               C.POINTER(pma_stats), _U64P, _U64P]),
+    ("gpma_shard_group_bfs", C.c_int, [_P, C.c_uint32, _P, _U64P]),
+    ("gpma_shard_group_cc", C.c_int, [_P, _P]),
+    ("gpma_shard_group_pagerank", C.c_int, [_P, C.c_double, C.c_double, C.c_size_t, _P, _P, _U64P,
+                                            C.POINTER(C.c_int)]),
+    ("gpma_shard_group_spmv", C.c_int, [_P, _P, _P]),
     ("gpma_warmup", C.c_int, [C.c_int]),
     ("gpma_probe_h2d", C.c_int, [C.c_int, _P, C.c_size_t, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     ("gpma_rebuild_create", C.c_int, [C.c_int, C.c_size_t, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),

@@ -59,7 +59,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             failed = True
     if failed:
         raise RuntimeError("nvcc failed")
-    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", *objs, "-o", OUT]
+    link = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static", *objs, "-o", OUT, "-ldl"]
     subprocess.check_call(link)
     return OUT
 

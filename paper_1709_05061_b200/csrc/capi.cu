@@ -60,6 +60,10 @@ std::string* err_of(pma_handle* h) { return h && h->impl ? &h->impl->err : nullp
 std::string* err_of(gpma_graph* g) { return g && g->impl ? &g->impl->err : nullptr; }
 }  // namespace
 
+namespace gpma {
+Graph* graph_impl(gpma_graph* g) { return g ? g->impl : nullptr; }  // for shard_group.cu
+}
+
 extern "C" {
 
 int pma_create(const pma_profile* profile, int device, pma_handle** out) {

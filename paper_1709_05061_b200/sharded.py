@@ -35,7 +35,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .abi import load_library, pma_stats
-from .pmagraph import GraphConfig, UpdateStats, _raise
+from .pmagraph import GraphConfig, PackedMemoryArray, UpdateStats, _raise
 
 UNREACHED = 0xFFFFFFFF
 
@@ -610,3 +610,105 @@ class ShardedGraph:
 
     def cuda_stream(self, i=0):
         return self._lib.gpma_cuda_stream(self.h[i])
+
+
+# ------------------------------------------------------- C-ABI shard group
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) through the library (rank 0 creates it)."""
+    lib = load_library()
+    buf = (C.c_char * 128)()
+    rc = lib.gpma_nccl_unique_id(buf)
+    if rc:
+        _raise(rc, lib.gpma_shard_group_last_error(None).decode())
+    return bytes(buf)
+
+
+class ShardGroup:
+    """This rank's shard of the key-range sharded graph with every collective
+    issued by the library over NCCL (gpma_shard_group_*, csrc/shard_group.cu):
+    the host only hands over device arrays.  bounds: world + 1 vertex bounds;
+    nccl_id: the same 128-byte ncclUniqueId on every rank."""
+
+    def __init__(self, num_vertices: int, bounds, rank: int, world: int, nccl_id: bytes, edges,
+                 config: GraphConfig | None = None, device: int = 0):
+        self._lib = load_library()
+        self.nv, self.rank, self.world, self.device = int(num_vertices), rank, world, device
+        self.bounds = np.ascontiguousarray(np.asarray(bounds, np.uint32))
+        s, d, w = edges
+        cfg = (config or GraphConfig()).c()
+        idb = (C.c_char * 128).from_buffer_copy(nccl_id)
+        self.h = C.c_void_p()
+        rc = self._lib.gpma_shard_group_create(C.byref(cfg), device, self.nv, _vp_np(self.bounds), world, rank, idb,
+                                               None, _vp(s), _vp(d), _vp(w), s.numel(), C.byref(self.h))
+        if rc:
+            self.h = None
+            _raise(rc, self._lib.gpma_shard_group_last_error(None).decode())
+        self.lo, self.hi = int(self.bounds[rank]), int(self.bounds[rank + 1])
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.gpma_shard_group_destroy(self.h)
+            self.h = None
+
+    def _check(self, rc):
+        if rc:
+            _raise(rc, self._lib.gpma_shard_group_last_error(self.h).decode())
+
+    def graph_handle(self):
+        return self._lib.gpma_shard_group_graph(self.h)
+
+    def cuda_stream(self):
+        return self._lib.gpma_cuda_stream(self.graph_handle())
+
+    def apply_batch(self, a, b, w, c, d):
+        """(UpdateStats of this shard, updates this shard applied, updates sent away)."""
+        st = pma_stats()
+        routed, sent = C.c_uint64(), C.c_uint64()
+        self._check(self._lib.gpma_shard_group_apply_batch(self.h, _vp(a), _vp(b), _vp(w), a.numel(), _vp(c), _vp(d),
+                                                           c.numel() if c is not None else 0, C.byref(st),
+                                                           C.byref(routed), C.byref(sent)))
+        return UpdateStats.from_c(st), routed.value, sent.value
+
+    def bfs(self, root: int):
+        dist = np.empty(self.nv, np.uint32)
+        reached = C.c_uint64()
+        self._check(self._lib.gpma_shard_group_bfs(self.h, C.c_uint32(root), _vp_np(dist), C.byref(reached)))
+        return dist, reached.value
+
+    def connected_components(self):
+        lab = np.empty(self.nv, np.uint32)
+        self._check(self._lib.gpma_shard_group_cc(self.h, _vp_np(lab)))
+        return lab
+
+    def pagerank(self, damping=0.85, epsilon=1e-3, max_iters=200, warm_start=None):
+        if warm_start is not None and len(warm_start) != self.nv:
+            raise ValueError("pagerank: warm start size mismatch")
+        ranks = np.empty(self.nv, np.float64)
+        it, conv = C.c_uint64(), C.c_int()
+        warm = None if warm_start is None else np.ascontiguousarray(warm_start, np.float64)
+        self._check(self._lib.gpma_shard_group_pagerank(self.h, C.c_double(damping), C.c_double(epsilon), max_iters,
+                                                        _vp_np(warm) if warm is not None else None, _vp_np(ranks),
+                                                        C.byref(it), C.byref(conv)))
+        return ranks, it.value, bool(conv.value)
+
+    def spmv(self, x):
+        xx = np.ascontiguousarray(x, np.float64)
+        if len(xx) != self.nv:
+            raise ValueError("spmv: dimension mismatch")
+        y = np.empty(self.nv, np.float64)
+        self._check(self._lib.gpma_shard_group_spmv(self.h, _vp_np(xx), _vp_np(y)))
+        return y
+
+    def shard_slots(self):
+        h = self._lib.gpma_pma(self.graph_handle())
+        return PackedMemoryArray(_handle=h, _owner=self).slots()
+
+    def shard_row_offsets(self):
+        out = np.zeros(self.hi - self.lo + 1, np.uint64)
+        self._check(self._lib.gpma_row_offsets(self.graph_handle(), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+
+def _vp_np(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None

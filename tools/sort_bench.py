@@ -17,8 +17,8 @@ def main():
     rng = np.random.default_rng(1)
     for n, lo, hi, pay in [(2_000_000, 21, 64, False), (5_400_000, 1, 50, False), (2_000_000, 0, 43, True),
                            (32_000_000, 0, 64, True)]:
-        k = (rng.integers(0, 2 ** 63, n, dtype=np.uint64) >> np.uint64(64 - hi)) << np.uint64(lo) if lo else \
-            rng.integers(0, 2 ** 63, n, dtype=np.uint64) >> np.uint64(63 - hi)
+        width = min(hi - lo, 63)
+        k = rng.integers(0, 2 ** width, n, dtype=np.uint64) << np.uint64(lo)
         dk = torch.from_numpy(k.view(np.int64)).cuda()
         dp = torch.arange(n, dtype=torch.int32, device="cuda") if pay else None
         work = dk.clone()
