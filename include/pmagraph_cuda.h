@@ -409,6 +409,11 @@ int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local);
 typedef struct gpma_shard_group gpma_shard_group;
 /* ncclGetUniqueId into 128 bytes (rank 0 creates it; the caller broadcasts it). */
 int gpma_nccl_unique_id(void* id128);
+/* An NCCL communicator of `world` ranks from a unique id (ncclCommInitRank;
+ * the ncclComm_t as void*), for callers without NCCL bindings; several shard
+ * groups (e.g. rebuilt graphs) may share it.  Destroy after every group. */
+int gpma_nccl_comm_create(const void* id128, int world, int rank, int device, void** comm);
+int gpma_nccl_comm_destroy(void* comm);
 /* DynamicGraph::from_edges (graph.hpp:66-92) for this rank's shard; the
  * communicator is the caller's ncclComm_t (nccl_comm, not owned) or created
  * from nccl_id128 (owned).  Every rank may pass the same global edge list. */

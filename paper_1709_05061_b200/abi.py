@@ -232,6 +232,8 @@ SIGNATURES = [
     ("gpma_pr_finish", C.c_int, [_P, _P, _P, C.c_size_t, _P, C.c_double, C.POINTER(C.c_double)]),
     ("gpma_shard_spmv", C.c_int, [_P, _P, _P]),
     ("gpma_nccl_unique_id", C.c_int, [_P]),
+    ("gpma_nccl_comm_create", C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("gpma_nccl_comm_destroy", C.c_int, [_P]),
     ("gpma_shard_group_create", C.c_int, [C.POINTER(gpma_graph_config), C.c_int, C.c_size_t, _P, C.c_int, C.c_int,
                                           _P, _P, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),
     ("gpma_shard_group_destroy", C.c_int, [_P]),

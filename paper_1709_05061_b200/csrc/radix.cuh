@@ -88,13 +88,16 @@ __device__ __forceinline__ void radix_rank_tile(const u64 (&k)[kRadixIpt], u32 w
     for (int i = 0; i < kRadixIpt; ++i) {
         const u32 d = item_digit(k, i, wvalid, shift, mask);
         const unsigned peers = __match_any_sync(FULL, d);
-        const bool ok = d < kNoDigit;
-        const u32 c = ok ? h[d] : 0;
+        const int leader = __ffs(peers) - 1;
+        // the group's leader claims popc(peers) slots of digit d; shared
+        // atomics of one warp retire in program order, so item row i gets
+        // lower slots than row i + 1 (stability)
+        u32 c = 0;
+        if (int(lane) == leader && d < kNoDigit) c = atomicAdd(&h[d], u32(__popc(peers)));
+        c = __shfl_sync(FULL, c, leader);
         pos[i] = c + __popc(peers & lt);
-        __syncwarp();
-        if (ok && (peers & lt) == 0) h[d] = c + __popc(peers);
-        __syncwarp();
     }
+    __syncwarp();
     __syncthreads();
     // thread t = digit t: exclusive over warps (warp order = input order)
     const unsigned t = threadIdx.x;
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
         // walk back kLook tiles per step with the loads of a step in flight
         // together (a serial walk costs one L2 round trip per tile, and the
         // first wave of tiles has no inclusive predecessor nearby)
-        constexpr int kLook = 8;
+        constexpr int kLook = 32;
         const ull inclusive0 = ep | (2ull << kFlagShift);  // "tile -1": inclusive prefix 0
         auto ready = [&](ull w) { return (w & ~((1ull << kEpochShift) - 1)) == ep && ((w >> kFlagShift) & 3ull); };
         long long j = (long long)tile - 1;

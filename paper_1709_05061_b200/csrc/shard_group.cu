@@ -221,6 +221,24 @@ int gpma_nccl_unique_id(void* id128) {
     });
 }
 
+int gpma_nccl_comm_create(const void* id128, int world, int rank, int device, void** comm) {
+    return group_guard(nullptr, [&] {
+        if (!id128 || !comm) throw ApiError(PMA_EINVAL, "gpma_nccl_comm_create: NULL argument");
+        GPMA_CUDA(cudaSetDevice(device));
+        ncclUniqueId id;
+        std::memcpy(&id, id128, sizeof(id));
+        ncclComm_t c = nullptr;
+        GPMA_NCCL(nccl().CommInitRank(&c, world, id, rank));
+        *comm = c;
+    });
+}
+
+int gpma_nccl_comm_destroy(void* comm) {
+    return group_guard(nullptr, [&] {
+        if (comm) GPMA_NCCL(nccl().CommDestroy(static_cast<ncclComm_t>(comm)));
+    });
+}
+
 int gpma_shard_group_create(const gpma_graph_config* cfg, int device, size_t num_vertices, const uint32_t* bounds,
                             int world, int rank, const void* nccl_id128, void* nccl_comm, const uint32_t* d_src,
                             const uint32_t* d_dst, const double* d_weights, size_t n, gpma_shard_group** out) {

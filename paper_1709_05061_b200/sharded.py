@@ -624,23 +624,44 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+class NcclComm:
+    """An NCCL communicator created by the library (gpma_nccl_comm_create)
+    from a unique id every rank holds; shard groups may share it."""
+
+    def __init__(self, nccl_id: bytes, world: int, rank: int, device: int = 0):
+        self._lib = load_library()
+        self.h = C.c_void_p()
+        idb = (C.c_char * 128).from_buffer_copy(nccl_id)
+        rc = self._lib.gpma_nccl_comm_create(idb, world, rank, device, C.byref(self.h))
+        if rc:
+            self.h = None
+            _raise(rc, self._lib.gpma_shard_group_last_error(None).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.gpma_nccl_comm_destroy(self.h)
+            self.h = None
+
+
 class ShardGroup:
     """This rank's shard of the key-range sharded graph with every collective
     issued by the library over NCCL (gpma_shard_group_*, csrc/shard_group.cu):
     the host only hands over device arrays.  bounds: world + 1 vertex bounds;
     nccl_id: the same 128-byte ncclUniqueId on every rank."""
 
-    def __init__(self, num_vertices: int, bounds, rank: int, world: int, nccl_id: bytes, edges,
-                 config: GraphConfig | None = None, device: int = 0):
+    def __init__(self, num_vertices: int, bounds, rank: int, world: int, nccl_id: bytes | None, edges,
+                 config: GraphConfig | None = None, device: int = 0, comm: "NcclComm | None" = None):
         self._lib = load_library()
         self.nv, self.rank, self.world, self.device = int(num_vertices), rank, world, device
         self.bounds = np.ascontiguousarray(np.asarray(bounds, np.uint32))
         s, d, w = edges
         cfg = (config or GraphConfig()).c()
-        idb = (C.c_char * 128).from_buffer_copy(nccl_id)
+        idb = (C.c_char * 128).from_buffer_copy(nccl_id) if nccl_id is not None else None
+        self._comm = comm  # keeps a shared communicator alive while the group lives
         self.h = C.c_void_p()
         rc = self._lib.gpma_shard_group_create(C.byref(cfg), device, self.nv, _vp_np(self.bounds), world, rank, idb,
-                                               None, _vp(s), _vp(d), _vp(w), s.numel(), C.byref(self.h))
+                                               comm.h if comm is not None else None, _vp(s), _vp(d), _vp(w),
+                                               s.numel(), C.byref(self.h))
         if rc:
             self.h = None
             _raise(rc, self._lib.gpma_shard_group_last_error(None).decode())
