@@ -83,9 +83,13 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-analytics", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no sweep/baseline/analytics)")
-    ap.add_argument("--routing", default="fused", choices=["fused", "all_to_all"],
-                    help="sharded update routing: the partition kernel stores into the owners' receive buffers "
-                         "over peer memory (fused), or an NCCL all-to-all after it")
+    ap.add_argument("--routing", default="group", choices=["group", "fused", "all_to_all"],
+                    help="sharded update routing: the library's own NCCL collectives through the C ABI (group), "
+                         "the partition kernel storing into the owners' receive buffers over peer memory (fused), "
+                         "or an NCCL all-to-all via torch.distributed")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: weak = the config scaled by N (default for C1-C3), strong = the config itself "
+                         "(default for C4, C5)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the key-range sharded (multi-GPU) path even at N = 1 (NCCL with one rank)")
     return ap.parse_args()
@@ -191,7 +195,7 @@ def full_slides(info, B):
     return P
 
 
-def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segments=None):
+def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segments=None, stream_of=None):
     """Drive W untimed warm-up steps then K timed steps over `slides` (the
     first min(W + K, P) full slides of the window, in order).  When a pass has
     used every slide the stream holds, the graph is rebuilt from the initial
@@ -202,7 +206,8 @@ def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segm
     `segments` (if given) receives each timed segment's steps / event ms /
     host wall ms."""
     import torch
-    lib = g._lib
+    from paper_1709_05061_b200.abi import load_library
+    lib = load_library()
     n_sl = len(slides)
     segments = [] if segments is None else segments
     total = 0.0
@@ -220,7 +225,8 @@ def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segm
             for s in slides[cur:cur + n]:
                 on_step(g, s, False)
         else:
-            ext = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
+            sp = stream_of(g) if stream_of else lib.gpma_cuda_stream(g.h)
+            ext = torch.cuda.ExternalStream(sp, device=torch.device("cuda", dev))
             if world > 1:
                 torch.distributed.barrier()
             torch.cuda.synchronize()
@@ -502,47 +508,74 @@ def run_ours(args):
 
 
 def run_sharded(args, rank, world, local):
-    """N > 1: the key-range sharded deployment, weak scaling.
+    """The key-range sharded deployment: one GPMA+ shard per GPU
+    over an edge-balanced source range (fixed from the initial window).
 
-    Workload "C2 per GPU": an RMAT (2^21 N)-vertex / (30.6M N)-edge stream
-    (gen_rmat seed 1, shuffle 2 — N = 1 is exactly C2), first half = initial
-    window, edge-balanced source ranges (fixed from the initial window).  A
-    step is one global slide of N x B arrivals; rank r holds the r-th
-    contiguous share of its inserts and deletes (arrival at r), routes them on
-    the device (gpma_route_partition + NCCL all-to-all, counts first) and
-    applies the routed batch to its shard.  value = all ranks' updates / the
-    max-over-ranks device time of the K steps."""
+    Workload: BASELINE config --config; --scaling weak (default; C2, C3, C1):
+    the config's stream scaled by N (RMAT: 2^k N vertices, N x edges; ER: N x
+    vertices at density / N), a step = one global slide of N x batch arrivals;
+    --scaling strong (default for C4, C5): the config itself, a step = one
+    slide of its batch.  Rank r ingests the r-th contiguous share of every
+    slide's inserts and deletes; --routing group (default): the library routes
+    and applies it with its own NCCL collectives (gpma_shard_group_*, C ABI);
+    fused / all_to_all: the Python ShardedGraph over torch.distributed.  Every
+    timed step is a full slide (passes with untimed rebuilds, as run_ours);
+    value = all ranks' updates / the max-over-ranks time of the K steps."""
     import torch
     import torch.distributed as dist
 
     from paper_1709_05061_b200 import pmagraph as pg
     from paper_1709_05061_b200 import sharding as sh
     from paper_1709_05061_b200.abi import load_library
-    from paper_1709_05061_b200.sharded import ShardedGraph, TorchComm
+    from paper_1709_05061_b200.sharded import NcclComm, ShardedGraph, ShardGroup, TorchComm, nccl_unique_id
 
     dev = local
     load_library().gpma_warmup(dev)
-    B, K, W = args.batch or 1_000_000, args.steps, args.warmup
-    nv, ne = NV * world, NE * world
+    cfg = CONFIGS[args.config]
+    scaling = args.scaling or ("strong" if args.config in ("C4", "C5") else "weak")
+    K, W = args.steps, args.warmup
+    base_b = args.batch or cfg["batch"]
+    if scaling == "weak":
+        nv = cfg["nv"] * world
+        param = int(cfg["param"]) * world if cfg["gen"] == "rmat" else cfg["param"] / world
+        B = base_b * world
+    else:
+        nv, param, B = cfg["nv"], cfg["param"], base_b
     t0 = time.time()
-    stream = pg.EdgeStream.rmat(nv, ne, seed=GEN_SEED).shuffle(SHUFFLE_SEED)
+    stream = (pg.EdgeStream.rmat(nv, int(param), seed=GEN_SEED) if cfg["gen"] == "rmat"
+              else pg.EdgeStream.erdos_renyi(nv, param, seed=GEN_SEED))
+    if cfg["shuffle"] is not None:
+        stream.shuffle(cfg["shuffle"])
     win = pg.SlidingWindow(stream, dev)
-    win.reserve((W + K) * B * world + 16)
+    info = win.info()
+    P = full_slides(info, B)
+    win.reserve(min(W + K, P) * B + 16)
+    info = win.info()
+    slides = [win.slide(B) for _ in range(min(W + K, P))]
+    for s_ in slides:
+        assert s_.n_ins == B and not s_.final_partial, "bench slide is not a full slide"
     info = win.info()
     gen_s = time.time() - t0
     init = info.initial_size
     e_src = _wrap_device(info.stream_src, init, torch.int32, dev)
     e_dst = _wrap_device(info.stream_dst, init, torch.int32, dev)
-    # edge-balanced source ranges from the initial window's out-degrees (fixed for the run)
     deg = torch.bincount(e_src.long(), minlength=nv).cpu().numpy()
     bounds = sh.vertex_bounds(nv, world, deg)
-    comm = TorchComm()
-    t1 = time.time()
-    G = ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev],
-                                       routing=args.routing)
-    load_s = time.time() - t1
-    slides = [win.slide(B * world) for _ in range(W + K)]
-    info = win.info()
+    group = args.routing == "group"
+    if group:
+        idt = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{dev}")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        ncomm = NcclComm(bytes(idt.cpu().numpy()), world, rank, dev)
+    else:
+        comm = TorchComm()
+
+    def make_graph():
+        if group:
+            return ShardGroup(nv, bounds, rank, world, None, (e_src, e_dst, None), device=dev, comm=ncomm)
+        return ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev],
+                                              routing=args.routing)
 
     def share(n, r):
         q, m = divmod(n, world)
@@ -557,97 +590,107 @@ def run_sharded(args, rank, world, local):
                 _wrap_device(info.del_src + 4 * (sl.del_offset + d0), d1 - d0, torch.int32, dev),
                 _wrap_device(info.del_dst + 4 * (sl.del_offset + d0), d1 - d0, torch.int32, dev))
 
-    for sl in slides[:W]:
-        G.apply_batch([my_slice(sl)])
-    dist.barrier()
-    torch.cuda.synchronize()
+    def apply(G, sl_tensors):
+        if group:
+            st, routed, sent = G.apply_batch(*sl_tensors)
+            return st, routed, sent, G
+        res = G.apply_batch([sl_tensors])
+        return res.stats[0], res.routed[0], res.sent[0], G
+
+    def stream_of(G):
+        return G.cuda_stream() if group else G.cuda_stream(0)
+
+    t1 = time.time()
+    G = make_graph()
+    load_s = time.time() - t1
+    acc = {"updates": 0, "routed": 0, "sent": 0, "launches": 0, "seg_ms": 0.0, "commit_bytes": 0.0}
+
+    def on_step(g, sl, timed):
+        st, routed, sent, _ = apply(g, my_slice(sl))
+        if timed:
+            acc["updates"] += st.batch_size
+            acc["routed"] += routed
+            acc["sent"] += sent
+            acc["seg_ms"] += st.segment_phase_ns / 1e6
+            tm = pg.pma_timing()
+            load_library().gpma_last_timing(g.graph_handle() if group else g.h[0], C.byref(tm))
+            acc["launches"] += tm.kernel_launches + (4 if group else 6)
+            acc["commit_bytes"] += tm.commit_bytes
+
     clocks = ClockSampler(dev)
-    clocks.start()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    updates = routed = sent = launches = 0
-    seg_ms = commit_bytes = 0.0
-    for sl in slides[W:]:
-        res = G.apply_batch([my_slice(sl)])
-        st = res.stats[0]
-        updates += st.batch_size
-        routed += res.routed[0]
-        sent += res.sent[0]
-        tm = G.last_timing()
-        launches += tm.kernel_launches + 6
-        seg_ms += st.segment_phase_ns / 1e6
-        commit_bytes += tm.commit_bytes
-    ev1.record()
-    torch.cuda.synchronize()
-    dist.barrier()
+    segs = []
+    G, ms, passes = run_passes(G, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs, stream_of=stream_of)
     clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    u = torch.tensor([float(updates), float(sent)], device="cuda")
+    u = torch.tensor([float(acc["updates"]), float(acc["sent"])], device="cuda")
     dist.all_reduce(u)
     ms_max, total_updates, total_sent = float(t.item()), float(u[0].item()), float(u[1].item())
     value = total_updates / (ms_max / 1e3)
 
-    # ---- e2e: the same slides from pinned host buffers (H2D of each rank's share inside the region)
-    G2 = ShardedGraph.from_edges_device(comm, nv, bounds, [(e_src, e_dst, None)], devices=[dev],
-                                        routing=args.routing)
-    host = []
+    # ---- e2e: the same slides from page-locked host buffers (each rank's share copied in the region)
+    host = {}
     for sl in slides:
         a, b, _, c, d = my_slice(sl)
-        host.append(tuple(x.cpu().pin_memory() for x in (a, b, c, d)))
-    for hb in host[:W]:
-        a, b, c, d = (x.cuda(non_blocking=True) for x in hb)
-        G2.apply_batch([(a, b, None, c, d)])
-    dist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    h2d = e2e_n = 0
-    for hb in host[W:]:
-        a, b, c, d = (x.cuda(non_blocking=True) for x in hb)
-        h2d += sum(x.numel() * 4 for x in hb)
-        e2e_n += G2.apply_batch([(a, b, None, c, d)]).stats[0].batch_size
-    e1.record()
-    torch.cuda.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+        host[id(sl)] = tuple(x.cpu().pin_memory() for x in (a, b, c, d))
+    e2e_acc = {"n": 0, "h2d": 0}
+
+    def on_e2e(g, sl, timed):
+        a, b, c, d = (x.cuda(non_blocking=True) for x in host[id(sl)])
+        st, _, _, _ = apply(g, (a, b, None, c, d))
+        if timed:
+            e2e_acc["n"] += st.batch_size
+            e2e_acc["h2d"] += sum(x.numel() * 4 for x in host[id(sl)])
+
+    del G
+    G2, e2e_ms, _ = run_passes(make_graph(), make_graph, slides, P, W, K, on_e2e, dev, world, None,
+                               stream_of=stream_of)
+    t = torch.tensor([e2e_ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    u = torch.tensor([float(e2e_n)], device="cuda")
-    dist.all_reduce(u)
-    e2e = {"value": float(u.item()) / (float(t.item()) / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // K,
-           "d2h_bytes_per_step": 632}
-    del G2
+    uu = torch.tensor([float(e2e_acc["n"])], device="cuda")
+    dist.all_reduce(uu)
+    e2e = {"value": float(uu.item()) / (float(t.item()) / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": e2e_acc["h2d"] // K, "d2h_bytes_per_step": PMA_STATS_BYTES,
+           "inputs": "each rank's share of the slide in page-locked host memory, copied in the timed region"}
 
     peak, peak_kind = measured_peak()
-    achieved = (commit_bytes / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
+    achieved = (acc["commit_bytes"] / K) / ((acc["seg_ms"] / K) / 1e3) / 1e9 if acc["seg_ms"] > 0 else None
+    routing_desc = {"group": "the library's own NCCL all-to-all (gpma_shard_group_apply_batch, C ABI)",
+                    "fused": "fused partition+transfer over CUDA IPC peer memory (Python ShardedGraph)",
+                    "all_to_all": "NCCL all-to-all via torch.distributed (Python ShardedGraph)"}[args.routing]
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-           "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": scaling, "vs_baseline": None,
            "dtype": "u64",
-           "data": f"synthetic: RMAT stream restated from generators.hpp ({nv} vertices, {ne} edges, seed 1, shuffle 2)",
-           "config": {"workload": f"C2 per GPU, key-range sharded over {world} GPUs: RMAT 2^21*{world} vertices / "
-                                  f"30.6M*{world}-edge stream, first half = initial window; a step = one global slide "
-                                  f"of {world} x {B} arrivals, each rank ingests 1/{world} of it, routes by NCCL "
-                                  f"all-to-all and applies its shard's share",
-                      "batch_per_gpu": B, "num_vertices": nv, "stream_edges": ne,
-                      "parallelism": f"key-range shards x{world} (one GPMA+ per GPU, "
-                                     + ("fused partition+transfer routing over peer memory)" if args.routing == "fused"
-                                        else "NCCL all-to-all routing)"),
-                      "vertex_bounds": [int(x) for x in bounds],
+           "data": f"synthetic: {cfg['gen'].upper()} stream restated from generators.hpp ({nv} vertices, seed 1"
+                   f"{', shuffle 2' if cfg['shuffle'] else ''})",
+           "config": {"workload": (f"{args.config} x{world} (weak: the stream scaled by {world}, a step = one global "
+                                   f"slide of {world} x {base_b})" if scaling == "weak" else
+                                   f"{args.config} (strong: one slide of {B} per step over {world} shards)")
+                                  + f"; each rank ingests 1/{world} of every slide and routes it to the owners",
+                      "batch": B, "batch_per_gpu": B // world, "num_vertices": nv, "stream_edges": len(stream),
+                      "parallelism": f"key-range shards x{world}, routing: {routing_desc}",
+                      "vertex_bounds": [int(x) for x in bounds], "full_slides_per_pass": P, "passes": passes,
                       "l2": "inputs larger than L2 (each shard's slot array > 126 MB)", "deletion_mode": "lazy"},
-           "e2e": e2e, "gpu_launches": launches,
+           "e2e": e2e, "gpu_launches": acc["launches"],
            "routing": {"updates_sent_to_other_ranks_per_step": total_sent / K,
-                       "wire_bytes_per_step": 8 * total_sent / K},
+                       "wire_bytes_per_step": 8 * total_sent / K,
+                       "nvlink_roofline": {"bound": "nvlink", "bytes_per_step": 8 * total_sent / K,
+                                           "achieved_GBps": (8 * total_sent / K) / (ms_max / K / 1e3) / 1e9,
+                                           "peak_GBps": 900.0 * world,
+                                           "note": "wire bytes over the whole step time (an upper-bound view: the "
+                                                   "exchange is a small part of the step)"}},
            "roofline": {"bound": "hbm", "kernel": "commit tier kernels (rank 0)", "achieved": achieved, "peak": peak,
                         "peak_kind": peak_kind, "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-                        "traffic": None, "algorithmic_bytes_per_step": commit_bytes / K,
-                        "kernel_ms_per_step": seg_ms / K},
+                        "traffic": None, "algorithmic_bytes_per_step": acc["commit_bytes"] / K,
+                        "kernel_ms_per_step": acc["seg_ms"] / K, "timed_segments": segs},
            "clocks": clk, "setup_s": {"generate": round(gen_s, 2), "from_edges": round(load_s, 3)}}
     if not args.no_analytics and not args.profile:
-        out["analytics"] = sharded_analytics(G, nv, rank)
+        out["analytics"] = sharded_analytics(G2, nv, rank, group)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    del G2
+    if group:
+        ncomm.close()
     dist.barrier()
     dist.destroy_process_group()
 
@@ -667,7 +710,7 @@ def _wrap_device(ptr, n, dtype, dev):
     return torch.as_tensor(_CAI(), device=f"cuda:{dev}")
 
 
-def sharded_analytics(G, nv, rank):
+def sharded_analytics(G, nv, rank, group=False):
     """Per-window analytics on the sharded graph (all ranks take part)."""
     import torch
     import torch.distributed as dist
@@ -678,9 +721,13 @@ def sharded_analytics(G, nv, rank):
     for r in roots:
         dist.barrier()
         t = time.perf_counter()
-        d = G.bfs(r)[0]
+        if group:
+            _, n = G.bfs(r)
+        else:
+            d = G.bfs(r)[0]
+            n = int((d != -1).sum().item())
         torch.cuda.synchronize()
-        ms.append(((time.perf_counter() - t) * 1e3, int((d != -1).sum().item())))
+        ms.append(((time.perf_counter() - t) * 1e3, n))
     out["bfs_ms"] = [x[0] for x in ms]
     out["bfs_reached"] = [x[1] for x in ms]
     dist.barrier()
@@ -688,7 +735,8 @@ def sharded_analytics(G, nv, rank):
     G.connected_components()
     torch.cuda.synchronize()
     out["cc_ms"] = (time.perf_counter() - t) * 1e3
-    out["cc_rounds"] = G.cc_rounds
+    if not group:
+        out["cc_rounds"] = G.cc_rounds
     dist.barrier()
     t = time.perf_counter()
     _, it, _ = G.pagerank()

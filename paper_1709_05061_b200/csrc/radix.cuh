@@ -30,6 +30,8 @@
 // single-pass scans assume).
 #pragma once
 
+#include <cstdlib>
+
 #include "block_ops.cuh"
 #include "scan.cuh"
 
@@ -44,8 +46,10 @@ constexpr int kRadixMaxPasses = 8;
 constexpr u32 kNoDigit = 0x100u;  // past-the-end items of a partial tile
 
 struct RadixWorkspace {
-    DevBuf<ull> status;  // per pass launch: ntiles x 256 epoch-tagged words
+    DevBuf<ull> status;  // look-back mode: per pass launch, ntiles x 256 epoch-tagged words
     DevBuf<u32> hist;    // kRadixMaxPasses x 256 global digit counts
+    DevBuf<u32> thist, toff;  // reduce-then-scan mode: 256 x ntiles digit counts / offsets
+    ScanWorkspace scan;
     ull epoch = 0;
 };
 
@@ -152,12 +156,48 @@ static __global__ void __launch_bounds__(256) k_radix_hist(const u64* __restrict
         if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
+// Reduce-then-scan form of a digit pass, step 1: every tile's count of every
+// digit, digit-major (tile_hist[d * ntiles + tile]), so one exclusive scan
+// gives each (digit, tile) its global output offset — no look-back chains
+// (whose first wave walks back across every resident tile).  Per-warp
+// counters with match_any aggregation (skewed digits would serialise plain
+// shared atomics).
+static __global__ void __launch_bounds__(kRadixThreads) k_radix_upsweep(const u64* __restrict__ kin, u64 n, int shift,
+                                                                 u32 mask, const u32* __restrict__ ghist,
+                                                                 u32* __restrict__ tile_hist) {
+    __shared__ u32 wh[kRadixWarps][kRadixBins];
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, t = threadIdx.x;
+    if (__syncthreads_or(ghist[t] == n)) return;  // constant digit: the pass copies through
+#pragma unroll
+    for (int j = 0; j < kRadixBins / 32; ++j) wh[warp][lane + 32 * j] = 0;
+    __syncwarp();
+    const u64 base = u64(blockIdx.x) * kRadixTile;
+    u64 k[kRadixIpt];
+#pragma unroll
+    for (int i = 0; i < kRadixIpt; ++i) {
+        const u64 idx = base + u64(i) * kRadixThreads + t;
+        k[i] = idx < n ? __ldcs(reinterpret_cast<const unsigned long long*>(kin + idx)) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < kRadixIpt; ++i) {
+        const u64 idx = base + u64(i) * kRadixThreads + t;
+        const u32 d = idx < n ? radix_digit(k[i], shift, mask) : kNoDigit;
+        const unsigned peers = __match_any_sync(FULL, d);
+        if (d < kNoDigit && (peers & lanemask_lt()) == 0) atomicAdd(&wh[warp][d], u32(__popc(peers)));
+    }
+    __syncthreads();
+    u32 c = 0;
+#pragma unroll
+    for (int w = 0; w < kRadixWarps; ++w) c += wh[w][t];
+    tile_hist[u64(t) * gridDim.x + blockIdx.x] = c;
+}
+
 // One digit pass over the whole array (a tile per CTA, tile id = block id).
 template <bool kVals>
 __global__ void __launch_bounds__(kRadixThreads, 2)
     k_radix_pass(const u64* __restrict__ kin, u64* __restrict__ kout, const u32* __restrict__ vin,
                  u32* __restrict__ vout, u64 n, int shift, u32 mask, const u32* __restrict__ ghist, ull* status,
-                 ull epoch) {
+                 ull epoch, const u32* __restrict__ tile_off) {
     extern __shared__ __align__(16) unsigned char smem[];
     using S = RadixSmem<kVals>;
     u64* sk = reinterpret_cast<u64*>(smem);
@@ -200,13 +240,13 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     radix_rank_tile(k, wvalid, shift, mask, pos, wh, s_start, s_w, &count);
 
     // publish this tile's count of digit t, then look back for the counts of
-    // digit t in all earlier tiles
+    // digit t in all earlier tiles (look-back mode; with tile_off the digit
+    // offsets of every tile were scanned beforehand)
     const ull ep = (epoch & kEpochMask) << kEpochShift;
     ull* my = status + tile * kRadixBins + t;
-    if (tile == 0) {
-        st_volatile(my, ep | (2ull << kFlagShift) | count);
-    } else {
-        st_volatile(my, ep | (1ull << kFlagShift) | count);
+    if (!tile_off) {
+        if (tile == 0) st_volatile(my, ep | (2ull << kFlagShift) | count);
+        else st_volatile(my, ep | (1ull << kFlagShift) | count);
     }
     // stage the tile in digit order while earlier tiles finish
 #pragma unroll
@@ -217,7 +257,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
         }
     }
     ull excl = 0;
-    if (tile > 0) {
+    if (tile > 0 && !tile_off) {
         // walk back kLook tiles per step with the loads of a step in flight
         // together (a serial walk costs one L2 round trip per tile, and the
         // first wave of tiles has no inclusive predecessor nearby)
@@ -244,9 +284,13 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
     }
     // global start of digit t = digits below t over the whole array + digit t
     // in earlier tiles; minus the tile-local start so out = gbase[d] + j
-    u32 gtot;
-    const u32 gex = block_excl_scan(ghist[t], &gtot, s_w);
-    s_gbase[t] = u64(gex) + excl - s_start[t];
+    if (tile_off) {
+        s_gbase[t] = u64(tile_off[u64(t) * gridDim.x + tile]) - s_start[t];
+    } else {
+        u32 gtot;
+        const u32 gex = block_excl_scan(ghist[t], &gtot, s_w);
+        s_gbase[t] = u64(gex) + excl - s_start[t];
+    }
     __syncthreads();
     const u64 nv = n - base < u64(kRadixTile) ? n - base : u64(kRadixTile);
 #pragma unroll 4
@@ -316,125 +360,6 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
             if (kVals) vout[idx] = v[i];
         }
     }
-}
-
-// Dynamic shared memory beyond 48 KB for the rank/scatter kernels, once per
-// device (the attribute is per function and device).
-inline void radix_prepare() {
-    static unsigned long long attr_set = 0;
-    int dev = 0;
-    GPMA_CUDA(cudaGetDevice(&dev));
-    if ((attr_set >> (dev & 63)) & 1ull) return;
-    GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(RadixSmem<true>::kBytes)));
-    GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(RadixSmem<false>::kBytes)));
-    GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(RadixSmem<true>::kBytes)));
-    GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   int(RadixSmem<false>::kBytes)));
-    attr_set |= 1ull << (dev & 63);
-}
-
-// Keys-only one-CTA sort of a device-resident count (<= kRadixTile) of keys:
-// one launch with no host-side size, for CUDA-graph-captured pipelines.
-inline void radix_sort_small_dev(cudaStream_t s, const u64* k0, u64* k1, const ull* n_dev, int begin, int end) {
-    radix_prepare();
-    k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, 0u, n_dev,
-                                                                           begin, end);
-    GPMA_LAUNCH_CHECK();
-}
-
-// n <= kBitonicMax distinct words (the small graph path sorts packed words
-// key << ib | arrival index, all distinct): an in-shared-memory bitonic
-// network over the next power of two, 1024 threads, ~log^2 n barrier steps
-// instead of the radix passes' per-digit ranking — the order is the stable
-// key order because the arrival index breaks every tie.
-constexpr int kBitonicMax = 4096;
-static __global__ void __launch_bounds__(1024) k_bitonic_small(const u64* __restrict__ in, u64* __restrict__ out,
-                                                        const ull* n_dev) {
-    __shared__ u64 s[kBitonicMax];
-    const u32 n = u32(*n_dev);
-    u32 P = 2;
-    while (P < n) P <<= 1;
-    for (u32 i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < n ? in[i] : ~0ull;
-    __syncthreads();
-    for (u32 k = 2; k <= P; k <<= 1) {
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
-            for (u32 i = threadIdx.x; i < P; i += blockDim.x) {
-                const u32 ixj = i ^ j;
-                if (ixj > i) {
-                    const u64 a = s[i], b = s[ixj];
-                    if ((a > b) == ((i & k) == 0)) {
-                        s[i] = b;
-                        s[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (u32 i = threadIdx.x; i < n; i += blockDim.x) out[i] = s[i];
-}
-
-// Stable sort of n keys (+ payload when v0 != nullptr) by key bits
-// [begin, end).  Double-buffer contract: the input is in k0/v0, k1/v1 are the
-// alternate buffers (both may be overwritten); returns 1 when the result is
-// in k1/v1, 0 when in k0/v0.  *launches (optional) counts kernel launches.
-inline int radix_sort(cudaStream_t s, RadixWorkspace& ws, u64* k0, u64* k1, u32* v0, u32* v1, u64 n, int begin,
-                      int end, u64* launches = nullptr) {
-    if (n <= 1 || end <= begin) return 0;
-    const bool vals = v0 != nullptr;
-    const int npass = (end - begin + 7) / 8;
-    if (npass > kRadixMaxPasses) throw ApiError(PMA_EINVAL, "radix_sort: more than 64 key bits");
-    radix_prepare();
-    if (n <= u64(kRadixTile)) {
-        if (vals)
-            k_radix_small<true><<<1, kRadixThreads, RadixSmem<true>::kBytes, s>>>(k0, k1, v0, v1, u32(n), nullptr, begin,
-                                                                                  end);
-        else
-            k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, u32(n),
-                                                                                   nullptr, begin, end);
-        GPMA_LAUNCH_CHECK();
-        if (launches) *launches += 1;
-        return 1;
-    }
-    const u64 ntiles = (n + kRadixTile - 1) / kRadixTile;
-    if (ntiles > 0x7fffffffull) throw ApiError(PMA_EINVAL, "radix_sort: too many keys");
-    if (ntiles * kRadixBins > ws.status.cap) {
-        ws.status.reserve(ntiles * kRadixBins);
-        GPMA_CUDA(cudaMemsetAsync(ws.status.ptr, 0, ws.status.cap * sizeof(ull), s));  // epoch 0 never issued
-    }
-    ws.hist.reserve(kRadixMaxPasses * kRadixBins);
-    GPMA_CUDA(cudaMemsetAsync(ws.hist.ptr, 0, size_t(npass) * kRadixBins * sizeof(u32), s));
-    static const unsigned hist_grid = resident_grid(k_radix_hist, 256);
-    const unsigned hg = unsigned(std::min<u64>(hist_grid, (n + 511) / 512));
-    k_radix_hist<<<hg, 256, 0, s>>>(k0, n, begin, end, ws.hist.ptr);
-    GPMA_LAUNCH_CHECK();
-    u64* ki = k0;
-    u64* ko = k1;
-    u32* vi = v0;
-    u32* vo = v1;
-    for (int p = 0; p < npass; ++p) {
-        ws.epoch = (ws.epoch + 1) & kEpochMask;
-        if (ws.epoch == 0) {
-            GPMA_CUDA(cudaMemsetAsync(ws.status.ptr, 0, ws.status.cap * sizeof(ull), s));
-            ws.epoch = 1;
-        }
-        const int sh_ = begin + 8 * p;
-        const u32 m = (1u << std::min(8, end - sh_)) - 1u;
-        if (vals)
-            k_radix_pass<true><<<unsigned(ntiles), kRadixThreads, RadixSmem<true>::kBytes, s>>>(
-                ki, ko, vi, vo, n, sh_, m, ws.hist.ptr + p * kRadixBins, ws.status.ptr, ws.epoch);
-        else
-            k_radix_pass<false><<<unsigned(ntiles), kRadixThreads, RadixSmem<false>::kBytes, s>>>(
-                ki, ko, nullptr, nullptr, n, sh_, m, ws.hist.ptr + p * kRadixBins, ws.status.ptr, ws.epoch);
-        GPMA_LAUNCH_CHECK();
-        std::swap(ki, ko);
-        std::swap(vi, vo);
-    }
-    if (launches) *launches += 1 + npass;
-    return ki == k1 ? 1 : 0;
 }
 
 // ---- single-pass exclusive sum (decoupled look-back) ----------------------
@@ -526,6 +451,141 @@ inline void exclusive_sum(cudaStream_t s, ScanWorkspace& ws, const u32* in, u32*
     }
     k_exclusive_sum<<<unsigned(ntiles), kScanThreads, 0, s>>>(in, out, n, ws.tiles.ptr, ws.epoch);
     GPMA_LAUNCH_CHECK();
+}
+
+// Dynamic shared memory beyond 48 KB for the rank/scatter kernels, once per
+// device (the attribute is per function and device).
+inline void radix_prepare() {
+    static unsigned long long attr_set = 0;
+    int dev = 0;
+    GPMA_CUDA(cudaGetDevice(&dev));
+    if ((attr_set >> (dev & 63)) & 1ull) return;
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<true>::kBytes)));
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_pass<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<false>::kBytes)));
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<true>::kBytes)));
+    GPMA_CUDA(cudaFuncSetAttribute(k_radix_small<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(RadixSmem<false>::kBytes)));
+    attr_set |= 1ull << (dev & 63);
+}
+
+// Keys-only one-CTA sort of a device-resident count (<= kRadixTile) of keys:
+// one launch with no host-side size, for CUDA-graph-captured pipelines.
+inline void radix_sort_small_dev(cudaStream_t s, const u64* k0, u64* k1, const ull* n_dev, int begin, int end) {
+    radix_prepare();
+    k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, 0u, n_dev,
+                                                                           begin, end);
+    GPMA_LAUNCH_CHECK();
+}
+
+// n <= kBitonicMax distinct words (the small graph path sorts packed words
+// key << ib | arrival index, all distinct): an in-shared-memory bitonic
+// network over the next power of two, 1024 threads, ~log^2 n barrier steps
+// instead of the radix passes' per-digit ranking — the order is the stable
+// key order because the arrival index breaks every tie.
+constexpr int kBitonicMax = 4096;
+static __global__ void __launch_bounds__(1024) k_bitonic_small(const u64* __restrict__ in, u64* __restrict__ out,
+                                                        const ull* n_dev) {
+    __shared__ u64 s[kBitonicMax];
+    const u32 n = u32(*n_dev);
+    u32 P = 2;
+    while (P < n) P <<= 1;
+    for (u32 i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < n ? in[i] : ~0ull;
+    __syncthreads();
+    for (u32 k = 2; k <= P; k <<= 1) {
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            for (u32 i = threadIdx.x; i < P; i += blockDim.x) {
+                const u32 ixj = i ^ j;
+                if (ixj > i) {
+                    const u64 a = s[i], b = s[ixj];
+                    if ((a > b) == ((i & k) == 0)) {
+                        s[i] = b;
+                        s[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (u32 i = threadIdx.x; i < n; i += blockDim.x) out[i] = s[i];
+}
+
+// Stable sort of n keys (+ payload when v0 != nullptr) by key bits
+// [begin, end).  Double-buffer contract: the input is in k0/v0, k1/v1 are the
+// alternate buffers (both may be overwritten); returns 1 when the result is
+// in k1/v1, 0 when in k0/v0.  *launches (optional) counts kernel launches.
+inline int radix_sort(cudaStream_t s, RadixWorkspace& ws, u64* k0, u64* k1, u32* v0, u32* v1, u64 n, int begin,
+                      int end, u64* launches = nullptr) {
+    if (n <= 1 || end <= begin) return 0;
+    const bool vals = v0 != nullptr;
+    const int npass = (end - begin + 7) / 8;
+    if (npass > kRadixMaxPasses) throw ApiError(PMA_EINVAL, "radix_sort: more than 64 key bits");
+    radix_prepare();
+    if (n <= u64(kRadixTile)) {
+        if (vals)
+            k_radix_small<true><<<1, kRadixThreads, RadixSmem<true>::kBytes, s>>>(k0, k1, v0, v1, u32(n), nullptr, begin,
+                                                                                  end);
+        else
+            k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, u32(n),
+                                                                                   nullptr, begin, end);
+        GPMA_LAUNCH_CHECK();
+        if (launches) *launches += 1;
+        return 1;
+    }
+    const u64 ntiles = (n + kRadixTile - 1) / kRadixTile;
+    if (ntiles > 0x7fffffffull) throw ApiError(PMA_EINVAL, "radix_sort: too many keys");
+    if (ntiles * kRadixBins > ws.status.cap) {
+        ws.status.reserve(ntiles * kRadixBins);
+        GPMA_CUDA(cudaMemsetAsync(ws.status.ptr, 0, ws.status.cap * sizeof(ull), s));  // epoch 0 never issued
+    }
+    ws.hist.reserve(kRadixMaxPasses * kRadixBins);
+    static const bool lookback = [] {
+        const char* e = std::getenv("GPMA_RADIX_LOOKBACK");
+        return e && e[0] == '1';
+    }();
+    if (!lookback) {
+        ws.thist.reserve(ntiles * kRadixBins);
+        ws.toff.reserve(ntiles * kRadixBins);
+    }
+    GPMA_CUDA(cudaMemsetAsync(ws.hist.ptr, 0, size_t(npass) * kRadixBins * sizeof(u32), s));
+    static const unsigned hist_grid = resident_grid(k_radix_hist, 256);
+    const unsigned hg = unsigned(std::min<u64>(hist_grid, (n + 511) / 512));
+    k_radix_hist<<<hg, 256, 0, s>>>(k0, n, begin, end, ws.hist.ptr);
+    GPMA_LAUNCH_CHECK();
+    u64* ki = k0;
+    u64* ko = k1;
+    u32* vi = v0;
+    u32* vo = v1;
+    for (int p = 0; p < npass; ++p) {
+        ws.epoch = (ws.epoch + 1) & kEpochMask;
+        if (ws.epoch == 0) {
+            GPMA_CUDA(cudaMemsetAsync(ws.status.ptr, 0, ws.status.cap * sizeof(ull), s));
+            ws.epoch = 1;
+        }
+        const int sh_ = begin + 8 * p;
+        const u32 m = (1u << std::min(8, end - sh_)) - 1u;
+        const u32* gh = ws.hist.ptr + p * kRadixBins;
+        const u32* toff = nullptr;
+        if (!lookback) {  // reduce-then-scan: per-tile digit counts -> offsets
+            k_radix_upsweep<<<unsigned(ntiles), kRadixThreads, 0, s>>>(ki, n, sh_, m, gh, ws.thist.ptr);
+            GPMA_LAUNCH_CHECK();
+            exclusive_sum(s, ws.scan, ws.thist.ptr, ws.toff.ptr, ntiles * kRadixBins);
+            toff = ws.toff.ptr;
+        }
+        if (vals)
+            k_radix_pass<true><<<unsigned(ntiles), kRadixThreads, RadixSmem<true>::kBytes, s>>>(
+                ki, ko, vi, vo, n, sh_, m, gh, ws.status.ptr, ws.epoch, toff);
+        else
+            k_radix_pass<false><<<unsigned(ntiles), kRadixThreads, RadixSmem<false>::kBytes, s>>>(
+                ki, ko, nullptr, nullptr, n, sh_, m, gh, ws.status.ptr, ws.epoch, toff);
+        GPMA_LAUNCH_CHECK();
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+    }
+    if (launches) *launches += 1 + npass * (lookback ? 1 : 3);
+    return ki == k1 ? 1 : 0;
 }
 
 }  // namespace gpma
