@@ -55,6 +55,21 @@ struct RadixWorkspace {
 
 __device__ __forceinline__ u32 radix_digit(u64 k, int shift, u32 mask) { return u32(k >> shift) & mask; }
 
+// Lanes holding the same 9-bit value d (8-bit digit or kNoDigit) as this
+// lane: nine ballots, one per bit — a few cycles each, where match.any's cost
+// grows with the number of distinct values in the warp (a random 8-bit digit
+// has ~30 of them).
+__device__ __forceinline__ unsigned warp_match9(u32 d) {
+    unsigned peers = FULL;
+#pragma unroll
+    for (int b = 0; b < 9; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned bal = __ballot_sync(FULL, bit);
+        peers &= bit ? bal : ~bal;
+    }
+    return peers;
+}
+
 // Shared-memory layout of a rank/scatter tile (dynamic smem): the per-warp
 // digit counters alias the key/value staging (they are dead by then).
 template <bool kVals>
@@ -91,7 +106,7 @@ __device__ __forceinline__ void radix_rank_tile(const u64 (&k)[kRadixIpt], u32 w
 #pragma unroll
     for (int i = 0; i < kRadixIpt; ++i) {
         const u32 d = item_digit(k, i, wvalid, shift, mask);
-        const unsigned peers = __match_any_sync(FULL, d);
+        const unsigned peers = warp_match9(d);
         const int leader = __ffs(peers) - 1;
         // the group's leader claims popc(peers) slots of digit d; shared
         // atomics of one warp retire in program order, so item row i gets
@@ -182,7 +197,7 @@ static __global__ void __launch_bounds__(kRadixThreads) k_radix_upsweep(const u6
     for (int i = 0; i < kRadixIpt; ++i) {
         const u64 idx = base + u64(i) * kRadixThreads + t;
         const u32 d = idx < n ? radix_digit(k[i], shift, mask) : kNoDigit;
-        const unsigned peers = __match_any_sync(FULL, d);
+        const unsigned peers = warp_match9(d);
         if (d < kNoDigit && (peers & lanemask_lt()) == 0) atomicAdd(&wh[warp][d], u32(__popc(peers)));
     }
     __syncthreads();
