@@ -613,7 +613,9 @@ __global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_de
 // --------------------------------------------------------------- commit args
 
 struct CommitArgs {
-    u64* tlist;  // touched ranges (b, e) of merge commits, appended at ctr->ntouched_next
+    u64* t0;     // level 0: one touched word per group (its merge range, or ~0)
+    u64* tlist;  // levels >= 1: touched words of merge commits, appended at ctr->ntouched_next
+    int cb;      // touched word = (log2(size) << cb) | begin
     u64* keys;
     u64* vals;
     u8* st;
@@ -803,13 +805,19 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// touched range of a merge commit (update_stats.hpp touched_ranges): appended
-// in any order; pma_touched_ranges sorts them into the reference's order
-// (level by level = by range size, segments ascending within a level)
+// touched range of a merge commit (update_stats.hpp touched_ranges), as one
+// sortable word (log2(size) << cb) | begin.  Level 0 (>= 99.5% of them) writes
+// one word per GROUP at the group's index — groups are in ascending segment
+// order, so an ordered compaction yields them in the reference's order with
+// no sort and no shared counter; higher levels append (see touched_ranges).
+__device__ __forceinline__ u64 touched_word(const CommitArgs& a, u64 b, u64 m) {
+    return (u64(63 - __clzll(m)) << a.cb) | b;
+}
+// level >= 1 (a few hundred groups at most): appended in any order, sorted
+// at fetch time
 __device__ __forceinline__ void touched_append(const CommitArgs& a, u64 b, u64 e) {
     const ull slot = atomicAdd(&a.ctr->ntouched_next, 1ull);
-    a.tlist[2 * slot] = b;
-    a.tlist[2 * slot + 1] = e;
+    a.tlist[slot] = touched_word(a, b, e - b);
 }
 
 // Only launched at level 0 (m == leaf == 16), where the pending list is the
@@ -1091,19 +1099,9 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
                 a.rlist[2 * slot + 1] = b + 16;
             }
         }
-        {
-            const unsigned mm = __ballot_sync(FULL, act && mode == 2);
-            if (mm) {
-                ull base = 0;
-                if (lane == 0) base = atomicAdd(&a.ctr->ntouched_next, ull(__popc(mm)));
-                base = __shfl_sync(FULL, base, 0);
-                if (act && mode == 2) {
-                    const ull slot = base + __popc(mm & ((1u << lane) - 1u));
-                    a.tlist[2 * slot] = b;
-                    a.tlist[2 * slot + 1] = b + 16;
-                }
-            }
-        }
+        // touched word of the group (level 0: dense by group index; a hub
+        // group's word is written again by the CTA kernel)
+        if (act) a.t0[gl] = mode == 2 ? touched_word(a, b, 16) : ~0ull;
         if (act) {
             a.gflag[gl] = u8(mode == 3 ? 0 : mode);
             if (mode != 3) acc.bytes += alg_bytes(16, s, mode);
@@ -1317,12 +1315,14 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
             const u32 gid_ = __shfl_sync(FULL, t_gid, gi & 31u);
             if (hl == 0 && act && big) {
                 a.gflag[gid_] = 0;
+                if (a.level == 0) a.t0[gid_] = ~0ull;  // the CTA kernel writes it
                 const ull slot = atomicAdd(&a.ctr->nbig, 1ull);
                 a.biglist[slot] = gid_;
             }
             if (hl == 0 && act && !big) {
                 a.gflag[gid_] = u8(mode);
-                if (mode == 2) touched_append(a, b, b + m);
+                if (a.level == 0) a.t0[gid_] = mode == 2 ? touched_word(a, b, m) : ~0ull;
+                else if (mode == 2) touched_append(a, b, b + m);
                 acc.bytes += alg_bytes(m, s, mode);
                 if (mode == 1) {
                     const unsigned added = __popc(hits);
@@ -1443,7 +1443,8 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
         }
         if (threadIdx.x == 0) {
             a.gflag[g] = flag;
-            if (flag == 2) touched_append(a, b, b + m);
+            if (a.level == 0) a.t0[g] = flag == 2 ? touched_word(a, b, m) : ~0ull;
+            else if (flag == 2) touched_append(a, b, b + m);
             acc.bytes += alg_bytes(m, s, flag);
             if (flag) acc.committed++;
         }
@@ -1490,11 +1491,15 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_de
 }
 
 // Empty leaves left of a touched range inherit its first header.
-__global__ void k_left_walk(const u64* __restrict__ ranges, u64 nranges, const u8* __restrict__ st, u64 leaf,
-                            u64* __restrict__ hdr, const ull* n_dev = nullptr) {
-    if (n_dev) nranges = *n_dev;
-    for (u64 r = blockIdx.x * u64(blockDim.x) + threadIdx.x; r < nranges; r += u64(gridDim.x) * blockDim.x) {
-        const u64 la = ranges[2 * r] / leaf;
+// (over the batch's touched words: level 0's dense words t0 — ~0 = none —
+// then the appended rest)
+__global__ void k_left_walk(const u64* __restrict__ t0, u64 n0, const u64* __restrict__ trest, u64 nrest, int cb,
+                            const u8* __restrict__ st, u64 leaf, u64* __restrict__ hdr, const ull* n0_dev = nullptr) {
+    if (n0_dev) n0 = *n0_dev;
+    for (u64 r = blockIdx.x * u64(blockDim.x) + threadIdx.x; r < n0 + nrest; r += u64(gridDim.x) * blockDim.x) {
+        const u64 w = r < n0 ? t0[r] : trest[r - n0];
+        if (w == ~0ull) continue;
+        const u64 la = (w & ((1ull << cb) - 1)) / leaf;
         const u64 v = hdr[la];
         for (u64 i = la; i-- > 0;) {
             bool empty = true;
@@ -1800,7 +1805,9 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
     }
     // commit (decide + merge + scatter)
     CommitArgs a{};
-    a.tlist = touched_ptr;
+    a.t0 = touched_ptr;
+    a.tlist = touched_ptr + touched_split_;
+    a.cb = touched_cb_;
     a.keys = d_keys;
     a.vals = d_vals;
     a.st = d_st;
@@ -1893,6 +1900,7 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
                 ctr->lvl_groups[lv] = ctr->ngroups;
                 ctr->lvl_big[lv] = ctr->nbig;
                 ctr->lvl_maxslice[lv] = ctr->max_slice;
+                ctr->lvl_merge[lv] = ctr->merge_slots;
                 ctr->committed = 0;
                 ctr->nbig = 0;
                 ctr->max_slice = 0;
@@ -2024,7 +2032,8 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
                                                   ro_base());
         GPMA_LAUNCH_CHECK();
         if (empty_leaves != 0) {  // headers of empty leaves inherit the next leaf's first key
-            k_left_walk<<<16, 128, 0, stream_>>>(touched.ptr, 0, d_st, leaf_, d_hdr, &d_ctr->ntouched_next);
+            k_left_walk<<<16, 128, 0, stream_>>>(touched.ptr, 0, nullptr, 0, touched_cb_, d_st, leaf_, d_hdr,
+                                                 &d_ctr->ngroups);
             GPMA_LAUNCH_CHECK();
         }
         GPMA_CUDA(cudaMemcpyAsync(h_ctr, d_ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, stream_));
@@ -2068,8 +2077,13 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     st.batch_size = n;
     st.num_levels = height_ + 1;
     last_ntouched = 0;
+    last_ngroups0_ = last_nrest_ = 0;
     last_resized = false;
     timing = pma_timing{};
+    touched_cb_ = 1;
+    while ((1ull << touched_cb_) <= cap_) ++touched_cb_;  // begin < 2^cb
+    touched_split_ = n;  // level-0 groups <= n
+    const u64 leaf0 = leaf_;  // (a root grow may re-derive the leaf size)
     u64 launches = 0;
     const u64 writes_base = slot_writes;
     if (n == 0) {
@@ -2514,7 +2528,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 st.resized = st.grow_events > 0 || st.shrink_events > 0;
                 if (!st.resized) {
                     const u64 pair[2] = {0, cap_};
-                    GPMA_CUDA(cudaMemcpyAsync(touched_ptr + 2 * ntouched, pair, 16, cudaMemcpyHostToDevice, stream_));
+                    int lg = 0;
+                    while ((1ull << lg) < pair[1]) ++lg;
+                    const u64 word = (u64(lg) << touched_cb_) | pair[0];
+                    GPMA_CUDA(cudaMemcpyAsync(touched_ptr + touched_split_ + ntouched, &word, 8, cudaMemcpyHostToDevice,
+                                              stream_));
+                    GPMA_CUDA(cudaStreamSynchronize(stream_));  // (word lives on the host stack)
                     ntouched++;
                 }
                 // counters already applied; clear device deltas
@@ -2542,7 +2561,11 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     // segments were queued on rlist; left walks are needed only while empty
     // leaves exist (their headers inherit the next leaf's first key).
     last_resized = st.resized;
-    last_ntouched = ntouched;
+    // touched ranges: level 0's merges (dense words) + the appended rest
+    const u64 ntouched0 = h_ctr->lvl_groups[0] ? h_ctr->lvl_merge[0] / leaf0 : 0;
+    last_ngroups0_ = h_ctr->lvl_groups[0];
+    last_nrest_ = ntouched;
+    last_ntouched = ntouched0 + ntouched;
     if (root_done) {
         // whole array re-placed: headers rebuilt in closed form already
         if (d_row_offsets) rebuild_row_offsets_full();
@@ -2559,8 +2582,9 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             GPMA_LAUNCH_CHECK();
             ++launches;
         }
-        if (ntouched > 0 && empty_leaves != 0) {
-            k_left_walk<<<grid_for(ntouched, 128, 148 * 8), 128, 0, stream_>>>(touched_ptr, ntouched, d_st, leaf_,
+        if (last_ntouched > 0 && empty_leaves != 0) {
+            k_left_walk<<<grid_for(last_ngroups0_ + ntouched, 128, 148 * 8), 128, 0, stream_>>>(
+                touched_ptr, last_ngroups0_, touched_ptr + touched_split_, ntouched, touched_cb_, d_st, leaf_,
                                                                                d_hdr);
             GPMA_LAUNCH_CHECK();
             ++launches;
@@ -2569,7 +2593,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     event(4);
     GPMA_CUDA(cudaStreamSynchronize(stream_));
     st.slot_writes = slot_writes - writes_base;
-    st.num_touched_ranges = ntouched;
+    st.num_touched_ranges = last_ntouched;
     st.segment_phase_ns = u64(double(seg_ms) * 1e6);
     float a = 0, b = 0, c = 0, d = 0;
     cudaEventElapsedTime(&a, ev_[0], ev_[1]);
@@ -2662,7 +2686,7 @@ void Pma::reserve_batch(u64 n) {
     gflag.reserve(n);
     touched.reserve(2 * n + 2);
     tw0.reserve(n + 1);
-    tw1.reserve(n + 1);
+    tw1.reserve(2 * n + 2);
     rlist.reserve(2 * n + 4);
     ik.reserve(n);
     iv.reserve(n);
@@ -2685,22 +2709,14 @@ void Pma::reserve_batch(u64 n) {
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 
-// touched range (b, e) -> one sortable word: (log2(e - b) << 40) | b.  Every
-// range is a whole segment (power-of-two size <= 2^31, aligned), so the word
-// orders ranges by size then begin — the reference's order (rounds in level
-// order, segments ascending inside a round) — and decodes back exactly.
-__global__ void k_touched_words(const u64* __restrict__ pairs, u64 n, u64* __restrict__ words) {
-    for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
-        const u64 b = pairs[2 * i], e = pairs[2 * i + 1];
-        words[i] = (u64(63 - __clzll(e - b)) << 40) | b;
-    }
-}
-
-__global__ void k_touched_pairs(const u64* __restrict__ words, u64 n, u64* __restrict__ pairs) {
+// touched word (log2(size) << cb) | begin -> (begin, end): every range is a
+// whole aligned segment of power-of-two size, so the word orders ranges by
+// size then begin and decodes back exactly.
+__global__ void k_touched_pairs(const u64* __restrict__ words, u64 n, int cb, u64* __restrict__ pairs) {
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
         const u64 x = words[i];
-        const u64 b = x & ((1ull << 40) - 1);
-        reinterpret_cast<ulonglong2*>(pairs)[i] = make_ulonglong2(b, b + (1ull << (x >> 40)));
+        const u64 b = x & ((1ull << cb) - 1);
+        reinterpret_cast<ulonglong2*>(pairs)[i] = make_ulonglong2(b, b + (1ull << (x >> cb)));
     }
 }
 
@@ -2708,19 +2724,38 @@ void Pma::touched_ranges(u64* pairs, size_t capn, size_t* count) {
     *count = last_ntouched;
     const size_t n = std::min<size_t>(capn, last_ntouched);
     if (!n || !pairs) return;
-    // the commit kernels append in any order: put them in the reference's
-    // order on the device (one keys-only radix sort of 45-bit words)
+    // the reference's order (rounds in level order = by size, segments
+    // ascending inside a round): level 0's dense words by one ordered
+    // compaction (groups are in segment order), then the few words of the
+    // higher levels sorted (they are larger ranges, so they follow)
     const u64 m = last_ntouched;
-    tw0.reserve(m);
-    tw1.reserve(m);
-    k_touched_words<<<grid_for(m, 256, 148 * 8), 256, 0, stream_>>>(touched.ptr, m, tw0.ptr);
+    tw0.reserve(m + 1);
+    tw1.reserve(2 * m + 2);  // sort alternate, then the decoded pairs
+    const u64* t0 = touched.ptr;
+    u64* o = tw0.ptr;
+    if (last_ngroups0_)
+        run_compact(
+            stream_, ws, nullptr, last_ngroups0_, last_ngroups0_, [=] __device__(ull i) { return t0[i] != ~0ull; },
+            [=] __device__(ull i, unsigned f, ull x) {
+                if (f) o[x] = t0[i];
+            },
+            NoFin{});
+    const u64 n0 = m - last_nrest_;
+    const u64* words = tw0.ptr;
+    if (last_nrest_) {
+        GPMA_CUDA(cudaMemcpyAsync(tw0.ptr + n0, touched.ptr + touched_split_, last_nrest_ * 8,
+                                  cudaMemcpyDeviceToDevice, stream_));
+        const int alt = radix_sort(stream_, rws, tw0.ptr + n0, tw1.ptr + n0, nullptr, nullptr, last_nrest_, 0,
+                                   touched_cb_ + 6);
+        if (alt)
+            GPMA_CUDA(cudaMemcpyAsync(tw0.ptr + n0, tw1.ptr + n0, last_nrest_ * 8, cudaMemcpyDeviceToDevice,
+                                      stream_));
+    }
+    // decoded into (b, e) pairs on the device and copied straight into the
+    // caller's array (page-locked: one DMA)
+    k_touched_pairs<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(words, n, touched_cb_, tw1.ptr);
     GPMA_LAUNCH_CHECK();
-    const int alt = radix_sort(stream_, rws, tw0.ptr, tw1.ptr, nullptr, nullptr, m, 0, 45);
-    // decoded back into (b, e) pairs on the device (the commit list is free
-    // again) and copied straight into the caller's array (page-locked: DMA)
-    k_touched_pairs<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(alt ? tw1.ptr : tw0.ptr, n, touched.ptr);
-    GPMA_LAUNCH_CHECK();
-    GPMA_CUDA(cudaMemcpyAsync(pairs, touched.ptr, n * 16, cudaMemcpyDeviceToHost, stream_));
+    GPMA_CUDA(cudaMemcpyAsync(pairs, tw1.ptr, n * 16, cudaMemcpyDeviceToHost, stream_));
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -2776,7 +2811,11 @@ int Pma::try_group(int level, u64 seg, const u64* keys, const u64* vals, const u
     const ull one = 1;
     GPMA_CUDA(cudaMemcpyAsync(&d_ctr->ngroups, &one, sizeof(ull), cudaMemcpyHostToDevice, stream_));
     CommitArgs a{};
-    a.tlist = touched.ptr;
+    touched_cb_ = 1;
+    while ((1ull << touched_cb_) <= cap_) ++touched_cb_;
+    a.t0 = touched.ptr;  // (one group: g = 0)
+    a.tlist = touched.ptr + 1;
+    a.cb = touched_cb_;
     a.keys = d_keys;
     a.vals = d_vals;
     a.st = d_st;
@@ -2824,9 +2863,9 @@ int Pma::try_group(int level, u64 seg, const u64* keys, const u64* vals, const u
             rlist.ptr, nullptr, h_ctr->nrefresh, d_keys, d_st, cap_, leaf_, d_hdr, ro_base());
         GPMA_LAUNCH_CHECK();
     }
-    if (h_ctr->ntouched_next > 0 && empty_leaves != 0) {
-        k_left_walk<<<grid_for(h_ctr->ntouched_next, 128, 148 * 8), 128, 0, stream_>>>(
-            touched.ptr, h_ctr->ntouched_next, d_st, leaf_, d_hdr);
+    if (empty_leaves != 0) {
+        k_left_walk<<<1, 32, 0, stream_>>>(touched.ptr, 1, touched.ptr + 1, h_ctr->ntouched_next, touched_cb_, d_st,
+                                          leaf_, d_hdr);
         GPMA_LAUNCH_CHECK();
     }
     GPMA_CUDA(cudaStreamSynchronize(stream_));

@@ -64,6 +64,7 @@ struct Ctr {
     // host sync (rounds may run back to back without one)
     ull np[2];
     ull ntouched_base;
+    ull lvl_merge[kMaxLevels];  // cumulative merged slots after each level (level-0 touched count)
     ull lvl_npend[kMaxLevels];
     ull lvl_committed[kMaxLevels];
     ull lvl_groups[kMaxLevels];
@@ -276,6 +277,11 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u8> gflag;
     DevBuf<u64> touched;  // pairs (b, e)
     DevBuf<u64> tw0, tw1;  // touched ranges as sortable words (touched_ranges)
+    // touched words of the last batch: level 0 dense by group index in
+    // touched[0, last_ngroups0_), higher levels + the root appended at
+    // touched[touched_split_ ...] (last_nrest_ of them)
+    int touched_cb_ = 32;
+    u64 touched_split_ = 0, last_ngroups0_ = 0, last_nrest_ = 0;
     DevBuf<u64> ik, iv;   // insert lists (pending space)
     DevBuf<u32> ir;
     // slot-space merge scratch (CTA/grid tiers, root path)
