@@ -255,7 +255,7 @@ struct BucketArgs {
 };
 
 // one update of the graph front end: checks + the packed sort word; returns
-// the bucket class: -1 guard delete (bucket L), -2 outside the layout, else 0
+// the bucket class: -2 outside the layout (or a guard delete: the batch is redone), else 0
 __device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u64* ck, u32* ci, u64 i, u32 s, u32 d,
                                          bool ins, PrepAcc& acc) {
     const u64 lim = 1ull << db;
@@ -269,8 +269,13 @@ __device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u6
     u64 c;
     int cls = 0;
     if (skip) {
-        c = 1ull << (2 * db);
-        cls = -1;
+        // a guard delete (graph.hpp:141-147 drops it, counted missed): never
+        // in a window stream, so instead of a skip bit that costs every batch
+        // a wider sort key, the batch takes the generic redo path, which
+        // drops guard deletes before the engine
+        c = 0;
+        acc.oor = 1;
+        cls = -2;
     } else if (s >= lim || d >= lim) {
         c = 0;
         acc.oor |= !ins;
@@ -1922,7 +1927,7 @@ bool Pma::small_graph_ok(u64 n, const GraphFront& gf) const {
     if (!small_graphs_ || gf.mk || n == 0 || n > kSmallGraphMax || height_ < 1 || !ro_base() || !stream_) return false;
     int db = 1;
     while (db < 32 && (1ull << db) < gf.nv) ++db;
-    return 2 * db + 1 + kSmallIb <= 64;
+    return 2 * db + kSmallIb <= 64;
 }
 
 std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int levels) const {
@@ -1944,7 +1949,7 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         small_exec_ = nullptr;
     }
     const int ib = kSmallIb;
-    const int nbits = 2 * db + 1;
+    const int nbits = 2 * db;
     radix_prepare();
     u64 dummy = 0;
     cudaGraph_t graph = nullptr;
@@ -1966,7 +1971,7 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
             const GraphFront* fd = d_desc_;
             const ull* ndp = &d_ctr->nsort;
             const int gdb = db;
-            const u64 skipkey = 1ull << (nbits - 1);
+            const u64 skipkey = 1ull << nbits;  // (no key reaches it: guard deletes redo the batch)
             const int pib = ib;
             const u64 pmask = (1ull << pib) - 1;
             auto KEY = [=] __device__(ull i) -> u64 { return ck[i] >> pib; };
@@ -2114,7 +2119,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // key layout is fixed by |V| (src, dst < 2^db), so no host round trip
         int db = 1;
         while (db < 32 && (1ull << db) < gf->nv) ++db;
-        nbits = 2 * db + 1;  // + the skip bit (guard deletes sort last)
+        nbits = 2 * db;  // key = src << db | dst (guard deletes take the redo path)
         int ib = 1;
         while ((1ull << ib) < n) ++ib;
         while ((1ull << ib) <= n) ++ib;  // the all-ones index is reserved for deletes
@@ -2239,8 +2244,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         const u64* kk = dk;
         const u64* vv = dv;
         const double* gw = gf ? gf->iw : nullptr;
-        const int gdb = gf ? (nbits - 1) / 2 : 0;  // graph layout: key = src << gdb | dst
-        const u64 skipkey = gf ? (1ull << (nbits - 1)) : ~0ull;
+        const int gdb = gf ? nbits / 2 : 0;  // graph layout: key = src << gdb | dst
+        const u64 skipkey = gf ? (1ull << nbits) : ~0ull;
         const int pib = packed_ib;
         const u64 pmask = (1ull << pib) - 1;
 
