@@ -320,10 +320,10 @@ def test_read_api_matches_reference():
 
 @pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
 def test_leaf_bucket_edge_cases(mode):
-    """The leaf-bucket front end (batch >= 2^16, few leaves) with guard
-    deletes (bucket L), duplicate and cancelling updates inside one leaf,
-    deletes outside the key layout (generic redo), and a bad insert (rejected,
-    graph unchanged) — all as the reference."""
+    """The leaf-bucket front end (batch >= 2^16, few leaves) with duplicate
+    and cancelling updates inside one leaf; guard deletes and deletes outside
+    the key layout (both: the generic redo path, which drops guard deletes);
+    a bad insert (rejected, graph unchanged) — all as the reference."""
     rng = np.random.default_rng(21)
     nv = 2**12
     s, d = rng.integers(0, nv, 30000), rng.integers(0, nv, 30000)
@@ -342,7 +342,8 @@ def test_leaf_bucket_edge_cases(mode):
     a[:300], b[:300] = 9, 33  # one key inserted 300 times
     c = np.concatenate([s[:9000], np.full(400, 9), rng.integers(0, nv, 500)]).astype(np.uint32)
     dd = np.concatenate([d[:9000], np.full(400, 33), np.full(500, 0xFFFFFFFF)]).astype(np.uint32)  # + guard deletes
-    both((a, b, rng.integers(0, 9, 60000).astype(float), c, dd), "guards + duplicates")
+    both((a, b, rng.integers(0, 9, 60000).astype(float), c, dd), "guards + duplicates", (0,))
+    both((a[1000:], b[1000:], rng.integers(0, 9, 59000).astype(float), c[:9400], dd[:9400]), "duplicates")
     c2 = np.concatenate([s[9000:20000], [2**20, 5]]).astype(np.uint32)  # a delete outside the layout
     d2 = np.concatenate([d[9000:20000], [3, 2**30]]).astype(np.uint32)
     a2, b2 = rng.integers(0, nv, 60000), rng.integers(0, nv, 60000)
