@@ -81,35 +81,6 @@ constexpr u64 kHeavyRow = 1024;
 constexpr unsigned kBfsLightGrid = 148 * 32, kBfsHeavyGrid = 148 * 64;
 constexpr u32 kHeavyParts = 32;
 
-// warp-aggregated enqueue of discovered vertices into the light / heavy
-// next queues; qn[2] accumulates the next frontier's row slots (the cost of
-// expanding it from the queues — the sweep decision of the next level)
-__device__ __forceinline__ void bfs_enqueue(bool won, u32 v, const u64* __restrict__ ro, u32* __restrict__ next,
-                                            u32* __restrict__ hnext, u32* __restrict__ qn) {
-    const unsigned lane = threadIdx.x & 31u;
-    const u64 len = won ? ro[v + 1] - ro[v] : 0;
-    const bool heavy = won && len > kHeavyRow;
-    const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
-    if (lm | hm) {
-        u32 sl = u32(len < 0xFFFFFFFFull ? len : 0xFFFFFFFFull);
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) sl += __shfl_xor_sync(FULL, sl, d);
-        if (lane == 0) atomicAdd(&qn[2], sl);
-    }
-    if (lm) {
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
-        base = __shfl_sync(FULL, base, 0);
-        if (won && !heavy) next[base + __popc(lm & lanemask_lt())] = v;
-    }
-    if (hm) {
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
-        base = __shfl_sync(FULL, base, 0);
-        if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v;
-    }
-}
-
 __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64* __restrict__ keys,
                                           const u8* __restrict__ st, u32* __restrict__ dist, u32 depth, u64 t, u64 e,
                                           u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
@@ -123,7 +94,20 @@ __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64*
             if (dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
         }
     }
-    bfs_enqueue(won, v, ro, next, hnext, qn);
+    const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
+    const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
+    if (lm) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
+        base = __shfl_sync(FULL, base, 0);
+        if (won && !heavy) next[base + __popc(lm & lanemask_lt())] = v;
+    }
+    if (hm) {
+        u32 base = 0;
+        if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
+        base = __shfl_sync(FULL, base, 0);
+        if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v;
+    }
 }
 
 // Valid non-guard neighbours are packed into a per-warp queue (ballot ranks)
@@ -141,14 +125,25 @@ struct BfsWarpQueue {
             const u32 v = act ? q[base + lane] : 0u;
             bool won = false;
             if (act && dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
-            bfs_enqueue(won, v, ro, next, hnext, qn);
+            const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
+            const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
+            if (lm) {
+                u32 o = 0;
+                if (lane == 0) o = atomicAdd(&qn[0], u32(__popc(lm)));
+                o = __shfl_sync(FULL, o, 0);
+                if (won && !heavy) next[o + __popc(lm & below)] = v;
+            }
+            if (hm) {
+                u32 o = 0;
+                if (lane == 0) o = atomicAdd(&qn[1], u32(__popc(hm)));
+                o = __shfl_sync(FULL, o, 0);
+                if (heavy) hnext[o + __popc(hm & below)] = v;
+            }
         }
         __syncwarp();
         cnt = 0;
     }
-    // the 128 slots [t0, t0 + 128) ∩ [., e): lane l reads t0 + 32 j + l;
-    // kSweep: only edges whose source sits on the frontier (dist == depth - 1)
-    template <bool kSweep = false>
+    // the 128 slots [t0, t0 + 128) ∩ [., e): lane l reads t0 + 32 j + l
     __device__ __forceinline__ void push128(const u64* __restrict__ keys, const u8* __restrict__ st, u64 t0, u64 e,
                                             const u64* __restrict__ ro, u32* __restrict__ dist, u32 depth,
                                             u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
@@ -162,7 +157,7 @@ struct BfsWarpQueue {
             vv[j] = 0;
             if (t < e && st[t] == kValid) {
                 const u64 k = keys[t];
-                ok[j] = !is_guard(k) && (!kSweep || dist[src_of(k)] == depth - 1);
+                ok[j] = !is_guard(k);
                 vv[j] = dst_of(k);
             }
         }
@@ -207,16 +202,30 @@ __device__ __forceinline__ void bfs_visit4(const u64* __restrict__ ro, const u64
 #pragma unroll
     for (int j = 0; j < 4; ++j) won[j] = cand[j] && atomicCAS(&dist[v[j]], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) bfs_enqueue(won[j], v[j], ro, next, hnext, qn);
+    for (int j = 0; j < 4; ++j) {
+        const bool heavy = won[j] && (ro[v[j] + 1] - ro[v[j]]) > kHeavyRow;
+        const unsigned lm = __ballot_sync(FULL, won[j] && !heavy), hm = __ballot_sync(FULL, heavy);
+        if (lm) {
+            u32 base = 0;
+            if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
+            base = __shfl_sync(FULL, base, 0);
+            if (won[j] && !heavy) next[base + __popc(lm & lanemask_lt())] = v[j];
+        }
+        if (hm) {
+            u32 base = 0;
+            if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
+            base = __shfl_sync(FULL, base, 0);
+            if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v[j];
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, const u32* nfp,
                                                     const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                     const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
                                                     u32* __restrict__ next, u32* __restrict__ hnext,
-                                                    u32* __restrict__ qn, u64 sweep_slots) {
+                                                    u32* __restrict__ qn) {
     __shared__ u32 s_q[8][256];
-    if (u64(nfp[2]) > sweep_slots) return;  // a big frontier: k_bfs_sweep expands this level
     const u32 nf = *nfp;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
@@ -229,14 +238,13 @@ __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ fron
     wq.drain(ro, dist, depth, next, hnext, qn);
 }
 
-__global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, const u32* cnt_in,
+__global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, const u32* nhp,
                                                           const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                           const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
                                                           u32* __restrict__ next, u32* __restrict__ hnext,
-                                                          u32* __restrict__ qn, u64 sweep_slots) {
+                                                          u32* __restrict__ qn) {
     // (a packed warp queue here measured slower: 1.03 vs 0.93 ms on the C2 hub BFS)
-    if (u64(cnt_in[2]) > sweep_slots) return;
-    const u32 nh = cnt_in[1];
+    const u32 nh = *nhp;
     for (u64 task = blockIdx.x; task < u64(nh) * kHeavyParts; task += gridDim.x) {
         const u32 u = hfrontier[task / kHeavyParts];
         const u64 p = task % kHeavyParts;
@@ -248,26 +256,6 @@ __global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict_
             bfs_visit4(ro, keys, st, dist, depth, t0 + threadIdx.x, blockDim.x, e, next, hnext, qn);
         for (; t0 < e; t0 += blockDim.x) bfs_visit(ro, keys, st, dist, depth, t0 + threadIdx.x, e, next, hnext, qn);
     }
-}
-
-// A level whose frontier rows hold more than sweep_slots slots is expanded by
-// one coalesced sweep of the whole slot array instead (edges kept when their
-// source is on the frontier, dist == depth - 1): reading every key once costs
-// less than visiting that many scattered row slots through the queues.  The
-// distances are the same (level-synchronous BFS: the first level that reaches
-// a vertex is its distance, whichever frontier edge claims it).
-__global__ void __launch_bounds__(256) k_bfs_sweep(const u32* cnt_in, u64 sweep_slots, const u64* __restrict__ ro,
-                                                   const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap,
-                                                   u32* __restrict__ dist, u32 depth, u32* __restrict__ next,
-                                                   u32* __restrict__ hnext, u32* __restrict__ qn) {
-    if (u64(cnt_in[2]) <= sweep_slots) return;
-    __shared__ u32 s_q[8][256];
-    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
-    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
-    BfsWarpQueue wq{s_q[threadIdx.x >> 5], 0};
-    for (u64 t0 = warp * 128; t0 < cap; t0 += nwarps * 128)
-        wq.push128<true>(keys, st, t0, cap, ro, dist, depth, next, hnext, qn);
-    wq.drain(ro, dist, depth, next, hnext, qn);
 }
 
 // -------- CC (analytics.hpp:53-82): min-root union-find over every stored
@@ -600,7 +588,7 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     q1.reserve(nv + 1);
     h0.reserve(nv + 1);
     h1.reserve(nv + 1);
-    qn.reserve(3);
+    qn.reserve(2);
     k_fill_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv, GPMA_UNREACHED);
     GPMA_LAUNCH_CHECK();
     const u32 zero = 0;
@@ -617,11 +605,7 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     // window found empty frontiers and did nothing).
     constexpr u32 kBfsWindow = 4;
     u64 cap_levels = 0;
-    // per level: (light, heavy, row slots of the frontier); a level whose
-    // frontier rows exceed sweep_slots is expanded by one sweep of the array
-    const u32 first[3] = {root_heavy ? 0u : 1u, root_heavy ? 1u : 0u, u32(rr[1] - rr[0])};
-    const u64 cap = pma.capacity();
-    const u64 sweep_slots = cap / 3;
+    const u32 first[2] = {root_heavy ? 0u : 1u, root_heavy ? 1u : 0u};
     u64 total = 1;
     u32 depth = 0;
     u32 *cur = q0.ptr, *nxt = q1.ptr, *hcur = h0.ptr, *hnxt = h1.ptr;
@@ -630,10 +614,10 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
         if (depth + kBfsWindow + 1 > cap_levels) {  // grow the counter ring (keeps earlier levels)
             const u64 nc = (depth + kBfsWindow + 1) * 2 + 64;
             DevBuf<u32> q2;
-            q2.reserve(3 * nc);
-            GPMA_CUDA(cudaMemsetAsync(q2.ptr, 0, 3 * nc * 4, s));
-            if (cap_levels) GPMA_CUDA(cudaMemcpyAsync(q2.ptr, qn.ptr, 3 * cap_levels * 4, cudaMemcpyDeviceToDevice, s));
-            else GPMA_CUDA(cudaMemcpyAsync(q2.ptr, first, 12, cudaMemcpyHostToDevice, s));
+            q2.reserve(2 * nc);
+            GPMA_CUDA(cudaMemsetAsync(q2.ptr, 0, 2 * nc * 4, s));
+            if (cap_levels) GPMA_CUDA(cudaMemcpyAsync(q2.ptr, qn.ptr, 2 * cap_levels * 4, cudaMemcpyDeviceToDevice, s));
+            else GPMA_CUDA(cudaMemcpyAsync(q2.ptr, first, 8, cudaMemcpyHostToDevice, s));
             GPMA_CUDA(cudaStreamSynchronize(s));
             std::swap(qn.ptr, q2.ptr);
             std::swap(qn.cap, q2.cap);
@@ -642,27 +626,23 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
         const u32 d0 = depth;
         for (u32 w = 0; w < kBfsWindow; ++w) {
             ++depth;
-            const u32* cnt_in = qn.ptr + 3 * (depth - 1);
-            u32* cnt_out = qn.ptr + 3 * depth;
+            const u32* cnt_in = qn.ptr + 2 * (depth - 1);
+            u32* cnt_out = qn.ptr + 2 * depth;
             k_bfs_expand<<<kBfsLightGrid, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt,
-                                                 hnxt, cnt_out, sweep_slots);
+                                                 hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
-            k_bfs_expand_heavy<<<kBfsHeavyGrid, 256, 0, s>>>(hcur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
-                                                       depth, nxt, hnxt, cnt_out, sweep_slots);
+            k_bfs_expand_heavy<<<kBfsHeavyGrid, 256, 0, s>>>(hcur, cnt_in + 1, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
+                                                       depth, nxt, hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
-            static const unsigned sw_grid = resident_grid(k_bfs_sweep, 256);
-            k_bfs_sweep<<<sw_grid, 256, 0, s>>>(cnt_in, sweep_slots, ro.ptr, pma.d_keys, pma.d_st, cap, dist.ptr,
-                                                depth, nxt, hnxt, cnt_out);
-            GPMA_LAUNCH_CHECK();
-            launches += 3;
+            launches += 2;
             std::swap(cur, nxt);
             std::swap(hcur, hnxt);
         }
-        h_lv_.resize(3 * kBfsWindow);
-        GPMA_CUDA(cudaMemcpyAsync(h_lv_.data(), qn.ptr + 3 * (d0 + 1), 3 * kBfsWindow * 4, cudaMemcpyDeviceToHost, s));
+        h_lv_.resize(2 * kBfsWindow);
+        GPMA_CUDA(cudaMemcpyAsync(h_lv_.data(), qn.ptr + 2 * (d0 + 1), 2 * kBfsWindow * 4, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
         for (u32 w = 0; w < kBfsWindow; ++w) {
-            const u64 c = u64(h_lv_[3 * w]) + h_lv_[3 * w + 1];
+            const u64 c = u64(h_lv_[2 * w]) + h_lv_[2 * w + 1];
             if (c == 0) {
                 done = true;
                 break;
