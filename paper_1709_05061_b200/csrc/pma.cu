@@ -125,41 +125,6 @@ void Pma::reset_layout(u64 cap) {
         mn_[l] = mn0 << l;
         mx_[l] = mx0 << l;
     }
-    apply_l2_policy();
-}
-
-// Keep the leaf headers resident in L2 (persisting access-policy window on
-// the library stream): the front end's leaf searches are chains of dependent
-// header loads, and the commit kernels stream the whole slot array through
-// L2 every batch, which would otherwise evict the headers each time.
-// GPMA_L2_PERSIST=0 disables (A/B measurements).
-void Pma::apply_l2_policy() {
-    static const bool enabled = [] {
-        const char* e = std::getenv("GPMA_L2_PERSIST");
-        return !(e && e[0] == '0');
-    }();
-    if (!enabled || !stream_ || !d_hdr) return;
-    cudaDeviceProp prop{};
-    if (cudaGetDeviceProperties(&prop, device_) != cudaSuccess || prop.persistingL2CacheMaxSize <= 0 ||
-        prop.accessPolicyMaxWindowSize <= 0) {
-        cudaGetLastError();
-        return;
-    }
-    const size_t hbytes = (cap_ / leaf_) * 8;
-    const size_t win = std::min<size_t>(hbytes, size_t(prop.accessPolicyMaxWindowSize));
-    const size_t carve = std::min<size_t>(win, size_t(prop.persistingL2CacheMaxSize));
-    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    cudaStreamAttrValue attr{};
-    attr.accessPolicyWindow.base_ptr = d_hdr;
-    attr.accessPolicyWindow.num_bytes = win;
-    attr.accessPolicyWindow.hitRatio = float(std::min(1.0, double(carve) / double(win)));
-    attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    if (cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess)
-        cudaGetLastError();
 }
 
 void Pma::ensure_slot_scratch() {

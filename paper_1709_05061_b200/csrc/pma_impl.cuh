@@ -197,11 +197,7 @@ public:
     cudaStream_t stream() const { return stream_; }
     // run every call on a caller-provided stream (own: back to the handle's own;
     // a null caller stream is the legacy default stream)
-    void set_stream(cudaStream_t s, bool own) {
-        stream_ = own ? own_stream_ : s;
-        apply_l2_policy();
-    }
-    void apply_l2_policy();
+    void set_stream(cudaStream_t s, bool own) { stream_ = own ? own_stream_ : s; }
     int device() const { return device_; }
     std::string err;
     pma_timing timing{};
