@@ -5,10 +5,10 @@
 // advance_round (segment_engine.hpp:90-105) and the touched-range list.
 //
 // One pass: every element is read once by `flag(i)` and handed to
-// `emit(i, f, exclusive_prefix)`.  A tile is 4096 elements, one CTA of 256
+// `emit(i, f, exclusive_prefix)`.  A tile is 2048 elements, one CTA of 256
 // threads, items STRIPED (item j of thread t is element base + 256 j + t) so
 // every flag/emit access of a warp is one contiguous run; ranks come from warp
-// ballots, the 16 x 8 (item row, warp) counts are scanned by one warp, and that
+// ballots, the 8 x 8 (item row, warp) counts are scanned by one warp, and that
 // warp runs the look-back.  Tile ids are block ids (blocks are dispatched in
 // order, as CUB's single-pass scans assume), and tile status words carry a
 // launch epoch, so no memset / ticket is needed between launches.
@@ -19,11 +19,10 @@
 namespace gpma {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanItems = 16;
+constexpr int kScanItems = 8;
 constexpr int kScanWarps = kScanThreads / 32;
 constexpr int kScanTile = kScanThreads * kScanItems;
-constexpr int kScanPerLane = kScanItems * kScanWarps / 32;  // (row, warp) counts per lane in warp 0's scan
-static_assert(kScanItems * kScanWarps % 32 == 0 && kScanItems <= 32, "compact_kernel's tile shape");
+static_assert(kScanItems * kScanWarps == 64, "compact_kernel's warp-0 scan takes two (row, warp) counts per lane");
 // status word: [63:36] epoch | [35:34] flag (1 aggregate, 2 inclusive) | [33:0] value
 constexpr int kEpochShift = 36;
 constexpr int kFlagShift = 34;
@@ -42,7 +41,7 @@ __device__ __forceinline__ void st_volatile(ull* p, ull v) { *reinterpret_cast<v
 // (j < kScanItems, i < n) at once: bit j of fm = flag, x[j] = exclusive prefix.
 // Lets a caller interleave independent per-item work (e.g. 8 binary searches).
 template <class Flag, class EmitTile, class Fin>
-__global__ void __launch_bounds__(kScanThreads, 4) compact_kernel(const ull* n_dev, ull n_host, Flag flag,
+__global__ void __launch_bounds__(kScanThreads, 7) compact_kernel(const ull* n_dev, ull n_host, Flag flag,
                                                                EmitTile emit_tile, Fin fin, ull* tiles, ull epoch) {
     __shared__ unsigned s_off[kScanItems * kScanWarps];  // (item row, warp) counts -> exclusive offsets
     __shared__ ull s_prefix, s_total;
@@ -74,27 +73,18 @@ __global__ void __launch_bounds__(kScanThreads, 4) compact_kernel(const ull* n_d
     }
     __syncthreads();
     if (warp == 0) {
-        // counts in element order: (row j, warp w) -> index j * kScanWarps + w;
-        // kScanPerLane consecutive ones per lane
-        unsigned a[kScanPerLane];
-        unsigned sum = 0;
-#pragma unroll
-        for (int c = 0; c < kScanPerLane; ++c) {
-            a[c] = s_off[kScanPerLane * lane + c];
-            sum += a[c];
-        }
+        // counts in element order: (row j, warp w) -> index j * 8 + w; two per lane
+        const unsigned a0 = s_off[2 * lane], a1 = s_off[2 * lane + 1];
+        const unsigned sum = a0 + a1;
         unsigned inc = sum;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const unsigned o = __shfl_up_sync(FULL, inc, d);
             if (lane >= unsigned(d)) inc += o;
         }
-        unsigned run = inc - sum;
-#pragma unroll
-        for (int c = 0; c < kScanPerLane; ++c) {
-            s_off[kScanPerLane * lane + c] = run;
-            run += a[c];
-        }
+        const unsigned ex = inc - sum;
+        s_off[2 * lane] = ex;
+        s_off[2 * lane + 1] = ex + a0;
         const ull total = __shfl_sync(FULL, inc, 31);
         const ull ep = (epoch & kEpochMask) << kEpochShift;
         ull prefix = 0;
