@@ -845,8 +845,16 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
     u64* rv = &s_v[w][lane * kRowB];
     const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
     const ull ngroups = a.ctr->ngroups;
-    const ull gstride = ull(gridDim.x) * kLeafWarps * 32;
-    ull g0 = (ull(blockIdx.x) * kLeafWarps + w) * 32;
+    // tiles handed out dynamically (one counter per launch): tiles differ in
+    // cost (merges vs tombstone flips vs deferrals), a static stride left
+    // warps idle at the end of the launch
+    auto grab = [&]() -> ull {
+        ull t = 0;
+        if (lane == 0) t = atomicAdd(&a.ctr->leaf_tiles, 1ull);
+        return __shfl_sync(FULL, t, 0) * 32;
+    };
+    ull g0 = grab();
+    ull gnext = 0;
     // descriptors of the first tile; each iteration prefetches the next tile's
     u32 n_lo = 0, n_hi = 0, n_seg = 0;
     if (g0 + lane < ngroups) {
@@ -855,7 +863,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
         n_seg = a.gseg[g0 + lane];
     }
     Acc acc;
-    for (; g0 < ngroups; g0 += gstride) {
+    for (; g0 < ngroups; g0 = gnext) {
         const ull gl = g0 + lane;
         const bool act = gl < ngroups;
         const u32 lo = n_lo, hi = n_hi;
@@ -884,8 +892,9 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             if (row < tile_n) cp_async16(&s_k[w][row * kRowB + 2 * part], a.keys + s_b[w][row] + 2 * part);
         }
         // descriptors of the next tile while the copies fly
+        gnext = grab();
         {
-            const ull gn = gl + gstride;
+            const ull gn = gnext + lane;
             n_lo = n_hi = n_seg = 0;
             if (gn < ngroups) {
                 n_lo = a.gstart[gn];

@@ -59,6 +59,7 @@ struct Ctr {
     ull bigrun;     // leaf-bucket front end: a bucket reached kRunMax updates
     ull nbig_buckets;  // leaf-bucket front end: buckets sorted by the CTA kernel
     ull nsort;      // graph-captured small batches: the batch size, written by the front end
+    ull leaf_tiles; // k_commit_leaf's dynamic tile counter (level 0 runs once per batch)
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
     // host sync (rounds may run back to back without one)
