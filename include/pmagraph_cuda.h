@@ -187,6 +187,13 @@ int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count
  * state unchanged).  Buffers only grow. */
 int pma_reserve_batch(pma_handle* h, size_t max_updates);
 
+/* Segments of at least min_slots slots (default 65536) are merged by the
+ * grid tier — device-wide compaction, ranking, scatter and placement over the
+ * segment (commit_in_place's range, segment_engine.hpp:147-230) — instead of
+ * one CTA per segment; smaller ones by the warp / CTA tiers.  The slot arrays
+ * and UpdateStats are identical either way (a tuning knob, >= 64). */
+int pma_set_grid_segment(pma_handle* h, uint64_t min_slots);
+
 /* try_insert_plus(pma, level, seg, slice, cfg, result) (segment_engine.hpp:
  * 320-341) for one group on the device: the n updates (sorted by key,
  * duplicates resolved, all inside segment `seg` of `level`) are decided by the

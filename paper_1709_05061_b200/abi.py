@@ -181,6 +181,7 @@ SIGNATURES = [
     ("pma_touched_ranges", C.c_int, [_P, _P, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("pma_slot_hash", C.c_int, [_P, C.c_int, _P]),
     ("pma_reserve_batch", C.c_int, [_P, C.c_size_t]),
+    ("pma_set_grid_segment", C.c_int, [_P, C.c_uint64]),
     ("pma_try_insert_plus", C.c_int, [_P, C.c_int, C.c_size_t, _P, _P, _P, C.c_size_t, C.POINTER(pma_engine_config),
                                       C.POINTER(C.c_int), _U64P, _U64P]),
     ("pma_binary_search_leaf", C.c_int, [_P, _P, C.c_size_t, _P]),

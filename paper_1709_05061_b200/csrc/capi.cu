@@ -216,6 +216,13 @@ int gpma_reserve_batch(gpma_graph* g, size_t max_updates) {
     });
 }
 
+int pma_set_grid_segment(pma_handle* h, uint64_t min_slots) {
+    return guarded(err_of(h), [&] {
+        if (min_slots < 64) throw ApiError(PMA_EINVAL, "pma_set_grid_segment: at least 64 slots");
+        h->impl->grid_seg_ = min_slots;
+    });
+}
+
 int pma_reserve_batch(pma_handle* h, size_t max_updates) {
     return guarded(err_of(h), [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));

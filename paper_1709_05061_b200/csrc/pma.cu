@@ -618,6 +618,7 @@ __global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_de
 // --------------------------------------------------------------- commit args
 
 struct CommitArgs {
+    u32* gridlist;  // non-null: merges of this level are handed to the grid tier (Pma::grid_merge)
     u64* t0;     // level 0: one touched word per group (its merge range, or ~0)
     u64* tlist;  // levels >= 1: touched words of merge commits, appended at ctr->ntouched_next
     int cb;      // touched word = (log2(size) << cb) | begin
@@ -1430,6 +1431,17 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
             flag = 1;
         } else if (nv + ins > a.mx || (a.eager && a.cap_gt_min && nv < dels + a.mn)) {
             flag = 0;
+        } else if (a.gridlist) {
+            // grid tier (large segments, commit_in_place segment_engine.hpp:
+            // 147-230): decided here, merged by device-wide kernels afterwards
+            // (Pma::grid_merge); headers and touched range queued as usual
+            if (threadIdx.x == 0) {
+                a.gridlist[atomicAdd(&a.ctr->ngrid, 1ull)] = u32(g);
+                const ull slot = atomicAdd(&a.ctr->nrefresh, 1ull);
+                a.rlist[2 * slot] = b;
+                a.rlist[2 * slot + 1] = b + m;
+            }
+            flag = 4;
         } else {
             const u64 nleaves = m / a.leaf;
             ull old_empty = 0;
@@ -1458,14 +1470,72 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
         if (threadIdx.x == 0) {
             a.gflag[g] = flag;
             if (a.level == 0) a.t0[g] = flag == 2 ? touched_word(a, b, m) : ~0ull;
-            else if (flag == 2) touched_append(a, b, b + m);
-            acc.bytes += alg_bytes(m, s, flag);
+            else if (flag == 2 || flag == 4) touched_append(a, b, b + m);
+            acc.bytes += alg_bytes(m, s, flag == 4 ? 2 : flag);
             if (flag) acc.committed++;
         }
         __syncthreads();
     }
     if (threadIdx.x != 0) acc = Acc{};
     block_flush(acc, a.ctr);
+}
+
+// ------------------------------------------------------------- grid tier
+// A large segment (>= grid_seg_ slots) is merged by device-wide kernels, the
+// root path's algorithm on the range [b, b + m): Valid entries compacted to
+// E (tombstones purged), the slice ranked in E, survivors and inserts
+// scattered to O by rank, destination-driven even placement back.  The
+// slice is the group's pending indices; counts live in the Ctr.
+__global__ void k_grid_ranks(const u64* __restrict__ uk, const u8* __restrict__ uop, const u32* __restrict__ plist,
+                             u64 s, const u64* __restrict__ ek, const ull* nv_dev, u8* __restrict__ mflag, Ctr* ctr) {
+    const u64 nv = *nv_dev;
+    ull missed = 0;
+    for (u64 q = blockIdx.x * u64(blockDim.x) + threadIdx.x; q < s; q += u64(gridDim.x) * blockDim.x) {
+        const u32 pi = plist[q];
+        const u64 u = uk[pi];
+        const u64 r = lower_bound_dev(ek, nv, u);
+        const bool isins = uop[pi] == kOpInsert;
+        if (r < nv && ek[r] == u) mflag[r] = isins ? 2 : 1;
+        else if (!isins) ++missed;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) missed += __shfl_xor_sync(FULL, missed, d);
+    if ((threadIdx.x & 31) == 0 && missed) atomicAdd(&ctr->missed, missed);
+}
+
+// tombstones and empty leaves of [b, b + m) before the merge
+__global__ void k_grid_seg_counts(const u8* __restrict__ st, u64 b, u64 m, u64 leaf, Ctr* ctr) {
+    ull nt = 0, ne = 0;
+    for (u64 l = blockIdx.x * u64(blockDim.x) + threadIdx.x; l < m / leaf; l += u64(gridDim.x) * blockDim.x) {
+        bool empty = true;
+        for (u64 t = b + l * leaf; t < b + (l + 1) * leaf; ++t) {
+            const u8 x = st[t];
+            nt += x == kTombstone;
+            empty &= x == kEmpty;
+        }
+        ne += empty;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        nt += __shfl_xor_sync(FULL, nt, d);
+        ne += __shfl_xor_sync(FULL, ne, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (nt) atomicAdd(&ctr->seg_tomb, nt);
+        if (ne) atomicAdd(&ctr->seg_empty, ne);
+    }
+}
+
+// the merge's counters, as k_commit_cta's accumulator would add them
+__global__ void k_grid_account(Ctr* ctr, u64 m, u64 leaf, int large) {
+    const ull k = ctr->k, nv = ctr->nv, moves = large ? ctr->moves : 0;
+    const u64 nleaves = m / leaf;
+    const long long new_empty = k >= nleaves ? 0 : (long long)(nleaves - k);
+    ctr->slot_writes += m + moves;
+    ctr->merge_slots += m;
+    ctr->valid_delta += (long long)k - (long long)nv;
+    ctr->tomb_delta -= (long long)ctr->seg_tomb;
+    ctr->empty_delta += new_empty - (long long)ctr->seg_empty;
 }
 
 // ------------------------------------------------------------- refresh
@@ -1779,6 +1849,86 @@ void Pma::rebuild_at_capacity(u64 cap) {
     place_root_from(dek, dev, n);
 }
 
+// Grid tier: merge segment [b, b + m) with the group's slice (pending
+// indices plist[0, s)) by device-wide kernels (see k_grid_ranks).  The
+// counters land in the Ctr as a CTA-tier merge's would (k_grid_account);
+// headers / row offsets and the touched range were queued by k_commit_cta.
+void Pma::grid_merge(u64 b, u64 m, const u32* plist, u64 s, bool large) {
+    ensure_slot_scratch();
+    GPMA_CUDA(cudaMemsetAsync(&d_ctr->seg_tomb, 0, 2 * sizeof(ull), stream_));
+    k_grid_seg_counts<<<grid_for(m / leaf_, 256, 148 * 8), 256, 0, stream_>>>(d_st, b, m, leaf_, d_ctr);
+    GPMA_LAUNCH_CHECK();
+    u64* dek = ek.ptr + b;
+    u64* dev = ev.ptr + b;
+    u32* des = es.ptr + b;
+    u8* mf = mflag.ptr + b;
+    u32* mbv = mb.ptr + b;
+    const u64* kk = d_keys + b;
+    const u64* vv = d_vals + b;
+    const u8* ss = d_st + b;
+    Ctr* ctr = d_ctr;
+    run_compact(
+        stream_, ws, nullptr, m, m, [=] __device__(ull i) { return ss[i] == kValid; },
+        [=] __device__(ull i, unsigned f, ull x) {
+            if (f) {
+                dek[x] = kk[i];
+                dev[x] = vv[i];
+                des[x] = u32(i);
+                mf[x] = 0;
+            }
+        },
+        [=] __device__(ull total) { ctr->nv = total; });
+    k_grid_ranks<<<grid_for(s, 256, 148 * 8), 256, 0, stream_>>>(uk.ptr, uop.ptr, plist, s, dek, &d_ctr->nv, mf,
+                                                               d_ctr);
+    GPMA_LAUNCH_CHECK();
+    {
+        const u64* uuk = uk.ptr;
+        const u64* uuv = uv.ptr;
+        const u8* uuo = uop.ptr;
+        u64* ikk = ik.ptr;
+        u64* ivv = iv.ptr;
+        u32* irr = ir.ptr;
+        const ull* nvp = &d_ctr->nv;
+        run_compact(
+            stream_, ws, nullptr, s, s, [=] __device__(ull q) { return uuo[plist[q]] == kOpInsert; },
+            [=] __device__(ull q, unsigned f, ull x) {
+                if (!f) return;
+                const u64 u = uuk[plist[q]];
+                ikk[x] = u;
+                ivv[x] = uuv[plist[q]];
+                irr[x] = u32(lower_bound_dev(dek, *nvp, u));
+            },
+            [=] __device__(ull total) { ctr->nins = total; });
+    }
+    run_compact(
+        stream_, ws, &d_ctr->nv, 0, m + 1, [=] __device__(ull j) { return mf[j] != 0; },
+        [=] __device__(ull j, unsigned, ull x) { mbv[j] = u32(x); },
+        [=] __device__(ull total) {
+            ctr->nmatched = total;
+            mbv[ctr->nv] = u32(total);
+        });
+    k_root_scatter_surv<<<grid_for(m, 256, 148 * 16), 256, 0, stream_>>>(dek, dev, &d_ctr->nv, mf, mbv, ir.ptr,
+                                                                        &d_ctr->nins, ok.ptr + b, ov.ptr + b);
+    GPMA_LAUNCH_CHECK();
+    k_root_scatter_ins<<<grid_for(s, 256, 148 * 8), 256, 0, stream_>>>(ik.ptr, iv.ptr, ir.ptr, &d_ctr->nins, mbv,
+                                                                      ok.ptr + b, ov.ptr + b, d_ctr);
+    GPMA_LAUNCH_CHECK();
+    if (large) {  // commit_in_place counts the compaction moves (segment_engine.hpp:147-230)
+        GPMA_CUDA(cudaMemsetAsync(&d_ctr->moves, 0, sizeof(ull), stream_));
+        run_compact(
+            stream_, ws, &d_ctr->nv, 0, m + 1, [=] __device__(ull j) { return mf[j] != 1; },
+            [=] __device__(ull j, unsigned f, ull x) {
+                if (f && u64(des[j]) != x) atomicAdd(&ctr->moves, 1ull);
+            },
+            NoFin{});
+    }
+    k_place_evenly<<<grid_for(m, 256, 148 * 32), 256, 0, stream_>>>(d_keys, d_vals, d_st, b, m, ok.ptr + b, ov.ptr + b,
+                                                                   &d_ctr->k, 0);
+    GPMA_LAUNCH_CHECK();
+    k_grid_account<<<1, 1, 0, stream_>>>(d_ctr, m, leaf_, large ? 1 : 0);
+    GPMA_LAUNCH_CHECK();
+}
+
 // One round (level) of the engine (segment_engine.hpp:78-105, 320-341):
 // group the pending list by segment (unique_segments), decide + commit every
 // group, keep the deferred groups' updates (advance_round).  Every kernel
@@ -1887,8 +2037,35 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
         k_commit_cta<<<grid_for(npend / kBigSlice + 1, 1, 148 * 2), kCtaThreads, 0, stream_>>>(a);
     } else {
         a.biglist = nullptr;
+        const bool grid_tier = m >= grid_seg_;
+        if (grid_tier) {
+            a.gridlist = biglist.ptr;
+            GPMA_CUDA(cudaMemsetAsync(&d_ctr->ngrid, 0, sizeof(ull), stream_));
+        }
         const unsigned grid = grid_for(npend, 1, 148 * 4);
         k_commit_cta<<<grid, kCtaThreads, 0, stream_>>>(a);
+        GPMA_LAUNCH_CHECK();
+        if (grid_tier) {
+            // large segments: the CTAs decided; the merges run device-wide,
+            // one group at a time (a handful per level at most)
+            sync_ctr();
+            const u64 ng = h_ctr->ngrid;
+            if (ng) {
+                std::vector<u32> gl(ng), gsv, gst;
+                GPMA_CUDA(cudaMemcpyAsync(gl.data(), biglist.ptr, ng * 4, cudaMemcpyDeviceToHost, stream_));
+                const u64 ngr = h_ctr->ngroups;
+                gst.resize(ngr + 1);
+                gsv.resize(ngr);
+                GPMA_CUDA(cudaMemcpyAsync(gst.data(), gstart.ptr, (ngr + 1) * 4, cudaMemcpyDeviceToHost, stream_));
+                GPMA_CUDA(cudaMemcpyAsync(gsv.data(), gseg.ptr, ngr * 4, cudaMemcpyDeviceToHost, stream_));
+                GPMA_CUDA(cudaStreamSynchronize(stream_));
+                std::sort(gl.begin(), gl.end());
+                for (const u32 g : gl) {
+                    grid_merge(u64(gsv[g]) * m, m, pcur + gst[g], u64(gst[g + 1] - gst[g]), cfg.large_for(m));
+                    launches += 9;
+                }
+            }
+        }
     }
     GPMA_LAUNCH_CHECK();
     if (events) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));

@@ -60,6 +60,8 @@ struct Ctr {
     ull nbig_buckets;  // leaf-bucket front end: buckets sorted by the CTA kernel
     ull nsort;      // graph-captured small batches: the batch size, written by the front end
     ull leaf_tiles; // k_commit_leaf's dynamic tile counter (level 0 runs once per batch)
+    ull ngrid;      // grid tier: groups handed over by k_commit_cta at this level
+    ull seg_tomb, seg_empty;  // grid tier: tombstones / empty leaves of the segment before its merge
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
     // host sync (rounds may run back to back without one)
@@ -143,6 +145,9 @@ public:
     u64 count_valid_in(u64 b, u64 e);
     void slot_hash(int level, u64* hashes);
     void reserve_batch(u64 n);
+    // grid tier: segments of at least grid_seg_ slots are merged device-wide
+    u64 grid_seg_ = u64(1) << 16;
+    void grid_merge(u64 b, u64 m, const u32* plist, u64 s, bool large);
     // small graph batches (pma.cu): captured front end + first rounds
     static constexpr u64 kSmallGraphMax = 4096;
     static constexpr int kSmallIb = 13;  // index bits of the packed sort word ((1 << 13) - 1 > 4096: delete marker)

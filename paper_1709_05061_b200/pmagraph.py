@@ -237,6 +237,10 @@ class PackedMemoryArray:
         """Pre-size every per-batch buffer (pma_reserve_batch)."""
         self._check(self._lib.pma_reserve_batch(self.h, max_updates))
 
+    def set_grid_segment(self, min_slots: int):
+        """Segments of >= min_slots slots merge in the grid tier (pma_set_grid_segment)."""
+        self._check(self._lib.pma_set_grid_segment(self.h, min_slots))
+
     def slot_hash(self, level: int):
         """Per-segment parity digest of slots() at `level` (pma_slot_hash)."""
         n = self.capacity() // (self.leaf_size() << level) if 0 <= level <= self.height() else 1

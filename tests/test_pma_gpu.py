@@ -271,3 +271,31 @@ def test_shrink_disabled_profile():
     for i in range(40):
         g.erase(i)
     assert g.capacity() == grown and g.valid_count() == 0
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+@pytest.mark.parametrize("force", [-1, PMA_STRATEGY_LARGE])
+def test_grid_tier_matches_reference(mode, force):
+    """The grid tier (pma_set_grid_segment): segments from 64 slots up are
+    merged by device-wide kernels instead of one CTA each — slot arrays,
+    counters and every UpdateStats field (incl. commit_in_place's slot_writes
+    under the large tier) must stay bit-exact."""
+    rng = np.random.default_rng(2024 + 10 * mode + force)
+    for trial in range(6):
+        universe = int(rng.integers(2000, 200000))
+        keys = np.unique(rng.integers(0, universe, int(rng.integers(500, 6000)), dtype=np.uint64))
+        vals = rng.integers(0, 2**63, len(keys), dtype=np.uint64)
+        g = PackedMemoryArray.from_sorted(keys, vals, 0.5)
+        g.set_grid_segment(64)
+        r = RefPMA().from_sorted(keys, vals, 0.5)
+        base = 0
+        for b in range(10):
+            if b % 2:  # hot key runs: groups escalate to large segments
+                n = int(rng.integers(200, 3000))
+                k = (base + np.arange(n, dtype=np.uint64) * int(rng.integers(1, 3))).astype(np.uint64)
+                o = (rng.random(n) < 0.3).astype(np.uint8)
+                v = rng.integers(0, 2**63, n, dtype=np.uint64)
+                base += int(rng.integers(0, 5000))
+            else:
+                k, v, o = random_batch(rng, int(rng.integers(0, 3000)), universe, float(rng.random()))
+            run_both(g, r, k, v, o, mode, force, f"grid tier trial {trial} batch {b}")
