@@ -130,6 +130,7 @@ typedef struct pma_timing {
     uint64_t commit_bytes; /* algorithmic HBM bytes of the commit kernels */
     uint64_t level_bytes[16]; /* the same, per tree level */
     uint64_t front_end;    /* 0 radix sort, 1 leaf buckets, 2 leaf buckets overflowed -> radix sort redo */
+    uint64_t grid_merges;  /* segments merged by the grid tier (pma_set_grid_segment) */
 } pma_timing;
 
 typedef struct pma_handle pma_handle;

@@ -90,6 +90,7 @@ class pma_timing(C.Structure):
         ("commit_bytes", C.c_uint64),
         ("level_bytes", C.c_uint64 * 16),
         ("front_end", C.c_uint64),
+        ("grid_merges", C.c_uint64),
     ]
 
 

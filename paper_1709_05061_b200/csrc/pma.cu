@@ -2063,6 +2063,7 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
                 for (const u32 g : gl) {
                     grid_merge(u64(gsv[g]) * m, m, pcur + gst[g], u64(gst[g + 1] - gst[g]), cfg.large_for(m));
                     launches += 9;
+                    timing.grid_merges++;
                 }
             }
         }

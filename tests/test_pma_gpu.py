@@ -281,6 +281,7 @@ def test_grid_tier_matches_reference(mode, force):
     counters and every UpdateStats field (incl. commit_in_place's slot_writes
     under the large tier) must stay bit-exact."""
     rng = np.random.default_rng(2024 + 10 * mode + force)
+    grid_merges = 0
     for trial in range(6):
         universe = int(rng.integers(2000, 200000))
         keys = np.unique(rng.integers(0, universe, int(rng.integers(500, 6000)), dtype=np.uint64))
@@ -299,3 +300,5 @@ def test_grid_tier_matches_reference(mode, force):
             else:
                 k, v, o = random_batch(rng, int(rng.integers(0, 3000)), universe, float(rng.random()))
             run_both(g, r, k, v, o, mode, force, f"grid tier trial {trial} batch {b}")
+            grid_merges += int(g.last_timing().grid_merges)
+    assert grid_merges > 0, "the batches never reached the grid tier"
