@@ -81,8 +81,21 @@ constexpr u64 kHeavyRow = 1024;
 constexpr unsigned kBfsLightGrid = 148 * 32, kBfsHeavyGrid = 148 * 64;
 constexpr u32 kHeavyParts = 32;
 
+// Discovery: a visited bitmap (|V| bits: 256 KB at C2, L1/L2-resident) is
+// probed first and claimed with atomicOr; only the winner writes dist.  The
+// probes of the frontier's edges are the BFS's dominant cost, and the bitmap
+// is 32x smaller than dist.  (A stale "unset" bit only costs an atomic.)
+__device__ __forceinline__ bool bfs_claim(u32* __restrict__ vis, u32* __restrict__ dist, u32 v, u32 depth) {
+    const u32 bit = 1u << (v & 31u);
+    if (vis[v >> 5] & bit) return false;
+    if (atomicOr(&vis[v >> 5], bit) & bit) return false;
+    dist[v] = depth;
+    return true;
+}
+
 __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64* __restrict__ keys,
-                                          const u8* __restrict__ st, u32* __restrict__ dist, u32 depth, u64 t, u64 e,
+                                          const u8* __restrict__ st, u32* __restrict__ dist, u32* __restrict__ vis,
+                                          u32 depth, u64 t, u64 e,
                                           u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
     const unsigned lane = threadIdx.x & 31u;
     bool won = false;
@@ -91,7 +104,7 @@ __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64*
         const u64 k = keys[t];
         if (!is_guard(k)) {
             v = dst_of(k);
-            if (dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+            won = bfs_claim(vis, dist, v, depth);
         }
     }
     const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
@@ -116,7 +129,8 @@ __device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64*
 struct BfsWarpQueue {
     u32* q;    // 256 entries of shared memory
     u32 cnt;   // warp-uniform
-    __device__ __forceinline__ void drain(const u64* __restrict__ ro, u32* __restrict__ dist, u32 depth,
+    __device__ __forceinline__ void drain(const u64* __restrict__ ro, u32* __restrict__ dist, u32* __restrict__ vis,
+                                          u32 depth,
                                           u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
         const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
         __syncwarp();
@@ -124,7 +138,7 @@ struct BfsWarpQueue {
             const bool act = base + lane < cnt;
             const u32 v = act ? q[base + lane] : 0u;
             bool won = false;
-            if (act && dist[v] == GPMA_UNREACHED) won = atomicCAS(&dist[v], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+            if (act) won = bfs_claim(vis, dist, v, depth);
             const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
             const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
             if (lm) {
@@ -145,8 +159,9 @@ struct BfsWarpQueue {
     }
     // the 128 slots [t0, t0 + 128) ∩ [., e): lane l reads t0 + 32 j + l
     __device__ __forceinline__ void push128(const u64* __restrict__ keys, const u8* __restrict__ st, u64 t0, u64 e,
-                                            const u64* __restrict__ ro, u32* __restrict__ dist, u32 depth,
-                                            u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
+                                            const u64* __restrict__ ro, u32* __restrict__ dist, u32* __restrict__ vis,
+                                            u32 depth, u32* __restrict__ next, u32* __restrict__ hnext,
+                                            u32* __restrict__ qn) {
         const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
         u32 vv[4];
         bool ok[4];
@@ -167,7 +182,7 @@ struct BfsWarpQueue {
             if (ok[j]) q[cnt + __popc(m & below)] = vv[j];
             cnt += __popc(m);
         }
-        if (cnt >= 128) drain(ro, dist, depth, next, hnext, qn);  // room for the next chunk stays
+        if (cnt >= 128) drain(ro, dist, vis, depth, next, hnext, qn);  // room for the next chunk stays
     }
 };
 
@@ -178,7 +193,8 @@ struct BfsWarpQueue {
 // warp): the key/state loads, then the dist probes, then the CASes are each
 // issued four at a time — the probes are random L2 reads, latency is the cost
 __device__ __forceinline__ void bfs_visit4(const u64* __restrict__ ro, const u64* __restrict__ keys,
-                                           const u8* __restrict__ st, u32* __restrict__ dist, u32 depth, u64 t,
+                                           const u8* __restrict__ st, u32* __restrict__ dist, u32* __restrict__ vis,
+                                           u32 depth, u64 t,
                                            u64 S, u64 e, u32* __restrict__ next, u32* __restrict__ hnext,
                                            u32* __restrict__ qn) {
     const unsigned lane = threadIdx.x & 31u;
@@ -198,9 +214,9 @@ __device__ __forceinline__ void bfs_visit4(const u64* __restrict__ ro, const u64
         }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) cand[j] = cand[j] && dist[v[j]] == GPMA_UNREACHED;
+    for (int j = 0; j < 4; ++j) cand[j] = cand[j] && !((vis[v[j] >> 5] >> (v[j] & 31u)) & 1u);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) won[j] = cand[j] && atomicCAS(&dist[v[j]], GPMA_UNREACHED, depth) == GPMA_UNREACHED;
+    for (int j = 0; j < 4; ++j) won[j] = cand[j] && bfs_claim(vis, dist, v[j], depth);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const bool heavy = won[j] && (ro[v[j] + 1] - ro[v[j]]) > kHeavyRow;
@@ -222,9 +238,9 @@ __device__ __forceinline__ void bfs_visit4(const u64* __restrict__ ro, const u64
 
 __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, const u32* nfp,
                                                     const u64* __restrict__ ro, const u64* __restrict__ keys,
-                                                    const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
-                                                    u32* __restrict__ next, u32* __restrict__ hnext,
-                                                    u32* __restrict__ qn) {
+                                                    const u8* __restrict__ st, u32* __restrict__ dist,
+                                                    u32* __restrict__ vis, u32 depth, u32* __restrict__ next,
+                                                    u32* __restrict__ hnext, u32* __restrict__ qn) {
     __shared__ u32 s_q[8][256];
     const u32 nf = *nfp;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
@@ -233,16 +249,16 @@ __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ fron
     for (u64 f = warp; f < nf; f += nwarps) {
         const u32 u = frontier[f];
         const u64 b = ro[u], e = ro[u + 1];
-        for (u64 t0 = b; t0 < e; t0 += 128) wq.push128(keys, st, t0, e, ro, dist, depth, next, hnext, qn);
+        for (u64 t0 = b; t0 < e; t0 += 128) wq.push128(keys, st, t0, e, ro, dist, vis, depth, next, hnext, qn);
     }
-    wq.drain(ro, dist, depth, next, hnext, qn);
+    wq.drain(ro, dist, vis, depth, next, hnext, qn);
 }
 
 __global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, const u32* nhp,
                                                           const u64* __restrict__ ro, const u64* __restrict__ keys,
-                                                          const u8* __restrict__ st, u32* __restrict__ dist, u32 depth,
-                                                          u32* __restrict__ next, u32* __restrict__ hnext,
-                                                          u32* __restrict__ qn) {
+                                                          const u8* __restrict__ st, u32* __restrict__ dist,
+                                                          u32* __restrict__ vis, u32 depth, u32* __restrict__ next,
+                                                          u32* __restrict__ hnext, u32* __restrict__ qn) {
     // (a packed warp queue here measured slower: 1.03 vs 0.93 ms on the C2 hub BFS)
     const u32 nh = *nhp;
     for (u64 task = blockIdx.x; task < u64(nh) * kHeavyParts; task += gridDim.x) {
@@ -253,8 +269,9 @@ __global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict_
         // whole warps iterate together (ballots inside)
         u64 t0 = b;
         for (; t0 + 3 * blockDim.x < e; t0 += 4 * blockDim.x)
-            bfs_visit4(ro, keys, st, dist, depth, t0 + threadIdx.x, blockDim.x, e, next, hnext, qn);
-        for (; t0 < e; t0 += blockDim.x) bfs_visit(ro, keys, st, dist, depth, t0 + threadIdx.x, e, next, hnext, qn);
+            bfs_visit4(ro, keys, st, dist, vis, depth, t0 + threadIdx.x, blockDim.x, e, next, hnext, qn);
+        for (; t0 < e; t0 += blockDim.x)
+            bfs_visit(ro, keys, st, dist, vis, depth, t0 + threadIdx.x, e, next, hnext, qn);
     }
 }
 
@@ -593,6 +610,10 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     GPMA_LAUNCH_CHECK();
     const u32 zero = 0;
     GPMA_CUDA(cudaMemcpyAsync(dist.ptr + root, &zero, 4, cudaMemcpyHostToDevice, s));
+    bvis.reserve(nv / 32 + 1);
+    GPMA_CUDA(cudaMemsetAsync(bvis.ptr, 0, (nv / 32 + 1) * 4, s));
+    const u32 rbit = 1u << (root & 31u);
+    GPMA_CUDA(cudaMemcpyAsync(bvis.ptr + root / 32, &rbit, 4, cudaMemcpyHostToDevice, s));
     u64 rr[2] = {0, 0};
     GPMA_CUDA(cudaMemcpyAsync(rr, ro.ptr + root, 16, cudaMemcpyDeviceToHost, s));
     GPMA_CUDA(cudaStreamSynchronize(s));
@@ -628,11 +649,11 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
             ++depth;
             const u32* cnt_in = qn.ptr + 2 * (depth - 1);
             u32* cnt_out = qn.ptr + 2 * depth;
-            k_bfs_expand<<<kBfsLightGrid, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, depth, nxt,
-                                                 hnxt, cnt_out);
+            k_bfs_expand<<<kBfsLightGrid, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, bvis.ptr,
+                                                 depth, nxt, hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
             k_bfs_expand_heavy<<<kBfsHeavyGrid, 256, 0, s>>>(hcur, cnt_in + 1, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
-                                                       depth, nxt, hnxt, cnt_out);
+                                                       bvis.ptr, depth, nxt, hnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
             launches += 2;
             std::swap(cur, nxt);
