@@ -115,3 +115,14 @@ def build_ref_suite() -> str | None:
     subprocess.check_call(["g++", *objs, "-o", out, "-L" + HERE, "-lpmagraph_cuda",
                            "-Wl,-rpath,$ORIGIN/../../paper_1709_05061_b200"])
     return out
+
+
+def build_tools() -> str:
+    """tools/cpp/small_batch_latency: the C-ABI small-batch latency probe."""
+    src = os.path.join(ROOT, "tools", "cpp", "small_batch_latency.cpp")
+    out = os.path.join(ROOT, "tools", "cpp", "small_batch_latency")
+    if os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(src), os.path.getmtime(OUT)):
+        return out
+    subprocess.check_call(["g++", "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", out,
+                           "-L" + HERE, "-lpmagraph_cuda", "-Wl,-rpath,$ORIGIN/../../paper_1709_05061_b200"])
+    return out

@@ -2290,8 +2290,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     // trip); the host loop below continues only if updates are still pending
     const int graph_levels = (gf && small_graph_ok(n, *gf)) ? run_small_graph(*gf, cfg) : 0;
     if (graph_levels) {
-        event(1);
-        event(2);
+        // (stage events skipped: a small batch's whole device span is the
+        // graph, ev_[0] -> ev_[4]; every host API call counts at this size)
     } else {
     // ---- 1. sort (stable, varying bits only) ----
     GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
@@ -2747,7 +2747,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.merge_slots = h_ctr->merge_slots;
     timing.commit_bytes = h_ctr->commit_bytes;
     timing.tombstone_flips = st.tombstones_added;
-    event(3);
+    if (!graph_levels) event(3);
     // ---- 5. refresh leaf headers / row offsets ----
     // The warp tier refreshed dense segments in place; sparse and CTA-tier
     // segments were queued on rlist; left walks are needed only while empty
@@ -2788,10 +2788,14 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     st.num_touched_ranges = last_ntouched;
     st.segment_phase_ns = u64(double(seg_ms) * 1e6);
     float a = 0, b = 0, c = 0, d = 0;
-    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
-    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
-    cudaEventElapsedTime(&c, ev_[2], ev_[3]);
-    cudaEventElapsedTime(&d, ev_[3], ev_[4]);
+    if (graph_levels) {
+        cudaEventElapsedTime(&a, ev_[0], ev_[4]);  // the graph + any host-loop levels: reported as one stage
+    } else {
+        cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+        cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+        cudaEventElapsedTime(&c, ev_[2], ev_[3]);
+        cudaEventElapsedTime(&d, ev_[3], ev_[4]);
+    }
     timing.sort_ms = a;
     timing.search_ms = b;
     timing.rounds_ms = c;
