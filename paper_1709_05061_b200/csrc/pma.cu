@@ -254,10 +254,10 @@ struct BucketArgs {
     u32* od;   // per update: ordinal in the bucket
 };
 
-// one update of the graph front end: checks + the packed sort word; returns
-// the bucket class: -2 outside the layout (or a guard delete: the batch is redone), else 0
-__device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u64* ck, u32* ci, u64 i, u32 s, u32 d,
-                                         bool ins, PrepAcc& acc) {
+// one update of the graph front end: checks + the compressed key; cls = the
+// bucket class: -2 outside the layout (or a guard delete: the batch is redone), else 0
+__device__ __forceinline__ u64 prep_code(const GraphFront& f, int db, u32 s, u32 d, u64 i, bool ins, PrepAcc& acc,
+                                         int& cls) {
     const u64 lim = 1ull << db;
     bool skip = false;
     if (ins) {
@@ -267,7 +267,7 @@ __device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u6
         acc.guards += skip;
     }
     u64 c;
-    int cls = 0;
+    cls = 0;
     if (skip) {
         // a guard delete (graph.hpp:141-147 drops it, counted missed): never
         // in a window stream, so instead of a skip bit that costs every batch
@@ -283,11 +283,24 @@ __device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u6
     } else {
         c = (u64(s) << db) | d;
     }
+    return c;
+}
+
+// packed word of a graph update with ib index bits (ib > 0)
+__device__ __forceinline__ u64 pack_word(const GraphFront& f, int ib, u64 c, u64 i, bool ins) {
+    return (c << ib) | (ins ? (f.opbit ? 0ull : i) : ((1ull << ib) - 1));
+}
+
+// checks + the sort input of one update (packed word, or key + payload); returns cls
+__device__ __forceinline__ int prep_word(const GraphFront& f, int db, int ib, u64* ck, u32* ci, u64 i, u32 s, u32 d,
+                                         bool ins, PrepAcc& acc) {
+    int cls;
+    const u64 c = prep_code(f, db, s, d, i, ins, acc, cls);
     if (ib) {
         // packed: key above the arrival index for inserts, all-ones for
         // deletes — among equal keys the inserts keep arrival order and the
         // deletes sort after them, which is all duplicate resolution needs
-        ck[i] = (c << ib) | (ins ? (f.opbit ? 0ull : u64(i)) : ((1ull << ib) - 1));
+        ck[i] = pack_word(f, ib, c, i, ins);
     } else {
         ck[i] = c;
         ci[i] = (u32(i) << 1) | (ins ? 1u : 0u);
@@ -444,14 +457,225 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
     prep_graph_body<kBucket>(f, db, ib, ck, ci, ctr, ba);
 }
 
-// The same front end with the batch descriptor in device memory (written by
-// a copy node of a captured CUDA graph), so one instantiated graph serves
-// every small batch; the batch size goes to ctr->nsort for the next nodes.
-__global__ void __launch_bounds__(256) k_prep_graph_dev(const GraphFront* __restrict__ fp, int db, int ib,
-                                                        u64* __restrict__ ck, u32* __restrict__ ci, Ctr* ctr) {
-    const GraphFront f = *fp;
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->nsort = f.ni + f.nd;
-    prep_graph_body<false>(f, db, ib, ck, ci, ctr, BucketArgs{});
+// Whole front end of a captured small batch in ONE CTA (n <= kSmallFrontMax):
+// zero the counters and the graph's look-back words, read the descriptor
+// straight from page-locked host memory, pack + check every update
+// (prep_word), bitonic-sort the packed words (compare-exchange partners
+// inside a warp by shuffles, across warps through shared memory, across a
+// thread's own items in registers), then resolve duplicates and compact the
+// unique updates with a CTA-wide scan — the same output as k_prep_graph, the
+// sort and the duplicate-resolution compaction of the general path, without
+// their launches and the look-back between CTAs.
+constexpr int kSmallFrontThreads = 1024;
+constexpr int kSmallFrontItems = 4;
+constexpr u32 kSmallFrontMax = kSmallFrontThreads * kSmallFrontItems;
+constexpr int kSmallFrontSmem = 2 * kSmallFrontMax * 8;  // double-buffered exchange
+
+__global__ void __launch_bounds__(kSmallFrontThreads, 1)
+    k_small_front(const GraphFront* __restrict__ hf, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
+                  u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
+    extern __shared__ u64 sbuf[];  // [2][kSmallFrontMax]
+    __shared__ u64 s_desc[(sizeof(GraphFront) + 7) / 8];
+    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
+    __shared__ ull s_acc[4];
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    // descriptor: one word per thread over PCIe; counters + look-back words zeroed
+    if (t < (sizeof(GraphFront) + 7) / 8) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
+    for (u32 i = t; i < sizeof(Ctr) / 8; i += kSmallFrontThreads) reinterpret_cast<ull*>(ctr)[i] = 0;
+    for (u64 i = t; i < ws_words; i += kSmallFrontThreads) ws_tiles[i] = 0;
+    if (t < 4) s_acc[t] = 0;
+    __syncthreads();
+    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
+    const u32 n = u32(f.ni + f.nd);
+    u32 P = 32;
+    while (P < n) P <<= 1;
+    // pack: item e of thread t is element t + e * 1024 (coalesced reads)
+    PrepAcc acc;
+    u64 x[kSmallFrontItems];
+#pragma unroll
+    for (int e = 0; e < kSmallFrontItems; ++e) {
+        const u32 i = t + u32(e) * kSmallFrontThreads;
+        x[e] = ~0ull;
+        if (i < n) {
+            const bool ins = i < f.ni;
+            const u32 s = ins ? f.is[i] : f.ds[i - f.ni];
+            const u32 d = ins ? f.id[i] : f.dd[i - f.ni];
+            int cls;
+            x[e] = pack_word(f, ib, prep_code(f, db, s, d, i, ins, acc, cls), i, ins);
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
+        acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
+        acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
+    }
+    if (lane == 0) {
+        if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
+        if (acc.bad) atomicMax(&s_acc[1], acc.bad);
+        if (acc.oor) atomicOr(&s_acc[2], 1ull);
+    }
+    // bitonic network over the first P elements (P >= 32: whole warps in or out)
+    u64* sb = sbuf;
+    for (u32 k = 2; k <= P; k <<= 1) {
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            if (j >= kSmallFrontThreads) {
+                // partners are this thread's own items (static indices: registers)
+                static_assert(kSmallFrontItems == 4, "register exchanges below assume 4 items");
+                auto cas = [&](u64& a, u64& b, u32 i) {
+                    const u64 lo = min(a, b), hi = max(a, b);
+                    const bool asc = (i & k) == 0;
+                    a = asc ? lo : hi;
+                    b = asc ? hi : lo;
+                };
+                if (j == kSmallFrontThreads) {
+                    cas(x[0], x[1], t);
+                    if (P > 2 * kSmallFrontThreads) cas(x[2], x[3], t + 2 * kSmallFrontThreads);
+                } else {
+                    cas(x[0], x[2], t);
+                    cas(x[1], x[3], t + kSmallFrontThreads);
+                }
+            } else if (j >= 32) {
+#pragma unroll
+                for (int e = 0; e < kSmallFrontItems; ++e) {
+                    const u32 i = t + u32(e) * kSmallFrontThreads;
+                    if (i < P) sb[i] = x[e];
+                }
+                __syncthreads();
+#pragma unroll
+                for (int e = 0; e < kSmallFrontItems; ++e) {
+                    const u32 i = t + u32(e) * kSmallFrontThreads;
+                    if (i < P) {
+                        const u64 y = sb[i ^ j];
+                        const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                        x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+                    }
+                }
+                sb = (sb == sbuf) ? sbuf + kSmallFrontMax : sbuf;  // the next exchange writes the other buffer
+            } else {
+#pragma unroll
+                for (int e = 0; e < kSmallFrontItems; ++e) {
+                    const u32 i = t + u32(e) * kSmallFrontThreads;
+                    if (i - lane < P) {  // warp-uniform
+                        const u64 y = __shfl_xor_sync(FULL, x[e], j);
+                        const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                        x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+                    }
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int e = 0; e < kSmallFrontItems; ++e) {
+        const u32 i = t + u32(e) * kSmallFrontThreads;
+        if (i < P) sb[i] = x[e];
+    }
+    __syncthreads();
+    // duplicate resolution (segment_engine.hpp:346-363): the last word of each
+    // equal-key run survives; a delete there takes the run's last insert.
+    // Thread t owns the contiguous items [4t, 4t + 4) for the ordered scan.
+    const u64* ck = sb;
+    const u64 pmask = (1ull << ib) - 1;
+    const u64 skipkey = 1ull << (2 * db);
+    unsigned fm = 0;
+#pragma unroll
+    for (int e = 0; e < kSmallFrontItems; ++e) {
+        const u32 i = t * kSmallFrontItems + u32(e);
+        if (i < n) {
+            const u64 c = ck[i] >> ib;
+            if (((i + 1 == n) || (ck[i + 1] >> ib) != c) && c < skipkey) fm |= 1u << e;
+        }
+    }
+    const u32 cnt = __popc(fm);
+    u32 inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const u32 y = __shfl_up_sync(FULL, inc, d);
+        if (lane >= u32(d)) inc += y;
+    }
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        u32 w = s_wsum[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(FULL, w, d);
+            if (lane >= u32(d)) w += y;
+        }
+        s_wsum[lane] = w;  // inclusive over warps
+    }
+    __syncthreads();
+    u32 x0 = inc - cnt + (warp ? s_wsum[warp - 1] : 0u);
+    const double* gw = f.iw;
+#pragma unroll
+    for (int e = 0; e < kSmallFrontItems; ++e) {
+        if (!((fm >> e) & 1u)) continue;
+        const u32 i = t * kSmallFrontItems + u32(e);
+        const u64 c = ck[i] >> ib;
+        u64 a = ck[i] & pmask;
+        bool ins = a != pmask;
+        if (!ins) {  // delete at a run end: any earlier insert of the key wins
+            for (long long q = (long long)i - 1; q >= 0 && (ck[q] >> ib) == c; --q) {
+                const u64 aq = ck[q] & pmask;
+                if (aq != pmask) {
+                    a = aq;
+                    ins = true;
+                    break;
+                }
+            }
+        }
+        o_k[x0] = ((c >> db) << 32) | (c & ((1ull << db) - 1));
+        o_v[x0] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
+        o_o[x0] = ins ? kOpInsert : kOpDelete;
+        ++x0;
+    }
+    if (t == 0) {
+        const ull total = s_wsum[kSmallFrontThreads / 32 - 1];
+        ctr->nsort = n;
+        ctr->gdel = s_acc[0];
+        ctr->bad_ins = s_acc[1];
+        ctr->oor = s_acc[2];
+        ctr->n_unique = total;
+        ctr->np[0] = (s_acc[1] || s_acc[2]) ? 0ull : total;
+    }
+}
+
+// Leaf of every unique update of a small batch (leaf_for_key), a warp per
+// key: each step loads 32 evenly spaced headers of the row's leaf bracket and
+// keeps the sub-range the ballot picks, so a bracket of 2^k leaves takes
+// ceil(k / 5) dependent loads instead of k (the latency is the cost at this
+// size).  Keys outside the row-offset range fall back to one lane's search.
+__global__ void __launch_bounds__(256) k_leaf_search_warp(const u64* __restrict__ uk, const ull* n_dev,
+                                                         const u64* __restrict__ hdr, u64 L, const u8* __restrict__ st,
+                                                         u64 leaf, const u64* __restrict__ ro, u64 rlo, u64 rhi,
+                                                         u32* __restrict__ ul) {
+    const u64 n = *n_dev;
+    const u32 lane = threadIdx.x & 31;
+    for (u64 w = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; w < n; w += (u64(gridDim.x) * blockDim.x) >> 5) {
+        const u64 key = uk[w];
+        const u64 u = key >> 32;
+        if (!(ro && u >= rlo && u < rhi && !is_guard(key))) {
+            if (lane == 0) ul[w] = u32(leaf_for_key(key, hdr, L, st, leaf, ro, rlo, rhi));
+            continue;
+        }
+        const u64 a = __ldg(&ro[u]), b = __ldg(&ro[u + 1]);
+        u64 lo = a ? (a - 1) / leaf : 0;
+        u64 hi = (b - 1) / leaf + 1;
+        if (hi > L) hi = L;
+        while (hi - lo > 1) {  // largest index in [lo, hi) with hdr <= key (as the bisection)
+            const u64 m = hi - lo - 1;  // candidates lo + 1 .. hi - 1
+            const u64 q = lo + 1 + (m * lane) / 32;
+            const unsigned bal = __ballot_sync(FULL, __ldg(&hdr[q]) <= key);
+            const int c = __popc(bal);
+            const u64 q_lo = lo + 1 + (m * u64(c - 1)) / 32, q_hi = lo + 1 + (m * u64(c)) / 32;
+            if (c == 0) hi = lo + 1;
+            else {
+                lo = q_lo;
+                if (c < 32) hi = q_hi;
+            }
+        }
+        if (lane == 0) ul[w] = u32(lo);
+    }
 }
 
 // bucket scatter: update i -> position off[bucket] + ordinal (bucket order,
@@ -2136,80 +2360,24 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         small_exec_ = nullptr;
     }
     const int ib = kSmallIb;
-    const int nbits = 2 * db;
-    radix_prepare();
+    static const bool attr = [] {
+        GPMA_CUDA(cudaFuncSetAttribute(k_small_front, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallFrontSmem));
+        return true;
+    }();
+    (void)attr;
+    if (!h_desc_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_desc_dev_), h_desc_, 0));
     u64 dummy = 0;
     cudaGraph_t graph = nullptr;
     GPMA_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
     try {
-        GPMA_CUDA(cudaMemcpyAsync(d_desc_, h_desc_, sizeof(GraphFront), cudaMemcpyHostToDevice, stream_));
-        // the graph's own look-back words start clean on every replay
-        GPMA_CUDA(cudaMemsetAsync(small_ws_.tiles.ptr, 0, small_ws_.tiles.cap * sizeof(ull), stream_));
-        GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
-        k_prep_graph_dev<<<kSmallGraphMax / 256, 256, 0, stream_>>>(d_desc_, db, ib, sk_in.ptr, si_in.ptr, d_ctr);
+        // front end in one CTA (counters and look-back words zeroed there,
+        // descriptor read in place from page-locked memory), then the leaf of
+        // every unique update (pma.hpp:234-289), a warp per key
+        static_assert(kSmallGraphMax <= kSmallFrontMax, "small graph batches sort in one CTA");
+        k_small_front<<<1, kSmallFrontThreads, kSmallFrontSmem, stream_>>>(
+            h_desc_dev_, db, ib, d_ctr, small_ws_.tiles.ptr, small_ws_.tiles.cap, uk.ptr, uv.ptr, uop.ptr);
         GPMA_LAUNCH_CHECK();
-        static_assert(kSmallGraphMax <= kBitonicMax, "small graph batches sort in one CTA");
-        k_bitonic_small<<<1, 1024, 0, stream_>>>(sk_in.ptr, sk_out.ptr, &d_ctr->nsort);
-        GPMA_LAUNCH_CHECK();
-        {
-            // duplicate resolution as in batch_update_device (packed words:
-            // key << ib | arrival index, all-ones index = a delete)
-            const u64* ck = sk_out.ptr;
-            const GraphFront* fd = d_desc_;
-            const ull* ndp = &d_ctr->nsort;
-            const int gdb = db;
-            const u64 skipkey = 1ull << nbits;  // (no key reaches it: guard deletes redo the batch)
-            const int pib = ib;
-            const u64 pmask = (1ull << pib) - 1;
-            auto KEY = [=] __device__(ull i) -> u64 { return ck[i] >> pib; };
-            auto PAY = [=] __device__(ull i) -> u32 {
-                const u32 a = u32(ck[i] & pmask);
-                return (a << 1) | (a != u32(pmask) ? 1u : 0u);
-            };
-            u64* o_k = uk.ptr;
-            u64* o_v = uv.ptr;
-            u8* o_o = uop.ptr;
-            Ctr* ctr = d_ctr;
-            run_compact_tile(
-                stream_, small_ws_, ndp, 0, kSmallGraphMax,
-                [=] __device__(ull i) {
-                    const ull nn = *ndp;
-                    const u64 c = KEY(i);
-                    return ((i + 1 == nn) || KEY(i + 1) != c) && c < skipkey;
-                },
-                [=] __device__(ull i0, ull nn, unsigned fm, const ull* xs) {
-                    const double* gw = fd->iw;
-#pragma unroll
-                    for (int j = 0; j < kScanItems; ++j) {
-                        if (!((fm >> j) & 1u)) continue;
-                        const ull i = i0 + ull(j) * kScanThreads;
-                        const u64 c = KEY(i);
-                        u32 p = PAY(i);
-                        if (!(p & 1u) && i > 0 && KEY(i - 1) == c) {
-                            for (long long t = (long long)i - 1; t >= 0 && KEY(t) == c; --t) {
-                                const u32 q = PAY(t);
-                                if (q & 1u) {
-                                    p = q;
-                                    break;
-                                }
-                            }
-                        }
-                        const u32 a = p >> 1;
-                        const bool ins = p & 1u;
-                        const u64 key = ((c >> gdb) << 32) | (c & ((1ull << gdb) - 1));
-                        o_k[xs[j]] = key;
-                        o_v[xs[j]] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
-                        o_o[xs[j]] = ins ? kOpInsert : kOpDelete;
-                    }
-                },
-                [=] __device__(ull total) {
-                    ctr->n_unique = total;
-                    ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
-                });
-        }
-        // leaf of every unique update (pma.hpp:234-289): a thread per key, the
-        // dependent header loads of different keys in flight together
-        k_leaf_search_sorted<<<kSmallGraphMax / 256, 256, 0, stream_>>>(
+        k_leaf_search_warp<<<kSmallGraphMax / 8, 256, 0, stream_>>>(
             uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
         GPMA_LAUNCH_CHECK();
         u32* pcur = nullptr;

@@ -486,47 +486,6 @@ inline void radix_prepare() {
     attr_set |= 1ull << (dev & 63);
 }
 
-// Keys-only one-CTA sort of a device-resident count (<= kRadixTile) of keys:
-// one launch with no host-side size, for CUDA-graph-captured pipelines.
-inline void radix_sort_small_dev(cudaStream_t s, const u64* k0, u64* k1, const ull* n_dev, int begin, int end) {
-    radix_prepare();
-    k_radix_small<false><<<1, kRadixThreads, RadixSmem<false>::kBytes, s>>>(k0, k1, nullptr, nullptr, 0u, n_dev,
-                                                                           begin, end);
-    GPMA_LAUNCH_CHECK();
-}
-
-// n <= kBitonicMax distinct words (the small graph path sorts packed words
-// key << ib | arrival index, all distinct): an in-shared-memory bitonic
-// network over the next power of two, 1024 threads, ~log^2 n barrier steps
-// instead of the radix passes' per-digit ranking — the order is the stable
-// key order because the arrival index breaks every tie.
-constexpr int kBitonicMax = 4096;
-static __global__ void __launch_bounds__(1024) k_bitonic_small(const u64* __restrict__ in, u64* __restrict__ out,
-                                                        const ull* n_dev) {
-    __shared__ u64 s[kBitonicMax];
-    const u32 n = u32(*n_dev);
-    u32 P = 2;
-    while (P < n) P <<= 1;
-    for (u32 i = threadIdx.x; i < P; i += blockDim.x) s[i] = i < n ? in[i] : ~0ull;
-    __syncthreads();
-    for (u32 k = 2; k <= P; k <<= 1) {
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
-            for (u32 i = threadIdx.x; i < P; i += blockDim.x) {
-                const u32 ixj = i ^ j;
-                if (ixj > i) {
-                    const u64 a = s[i], b = s[ixj];
-                    if ((a > b) == ((i & k) == 0)) {
-                        s[i] = b;
-                        s[ixj] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (u32 i = threadIdx.x; i < n; i += blockDim.x) out[i] = s[i];
-}
-
 // Stable sort of n keys (+ payload when v0 != nullptr) by key bits
 // [begin, end).  Double-buffer contract: the input is in k0/v0, k1/v1 are the
 // alternate buffers (both may be overwritten); returns 1 when the result is
