@@ -6,6 +6,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "pmagraph_cuda.h"
 
@@ -60,6 +61,41 @@ inline unsigned resident_grid(K kernel, int block, size_t smem = 0) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem);
     return unsigned((per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148));
+}
+
+// Programmatic dependent launch (captured small-batch chains): a kernel of
+// the chain lets its successor's CTAs be scheduled at once
+// (launch_dependents) and waits for its predecessor's completion and memory
+// (wait) before touching anything the predecessor wrote.  Both are no-ops for
+// an ordinary launch, so the kernels call them unconditionally.
+static __device__ int g_pdl_early = 0;  // 1: successors scheduled at entry (GPMA_PDL_EARLY=1; measured slower)
+__device__ __forceinline__ void pdl_enter() {
+    if (g_pdl_early) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Host side: while pdl_chain() is set on this thread (a small-batch capture),
+// launch_k adds the programmatic-serialization attribute, so the captured
+// edge to the previous kernel becomes a programmatic one.
+inline bool& pdl_chain() {
+    static thread_local bool on = false;
+    return on;
+}
+template <typename... P, typename... A>
+inline void launch_k(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    if (pdl_chain()) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    GPMA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }

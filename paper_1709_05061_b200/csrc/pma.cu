@@ -457,6 +457,13 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
     prep_graph_body<kBucket>(f, db, ib, ck, ci, ctr, ba);
 }
 
+// last node of a captured small batch: the counters to page-locked host
+// memory (one kernel instead of a copy node, so the chain stays programmatic)
+__global__ void k_words_out(const ull* __restrict__ src, ull* dst, u32 nwords) {
+    pdl_enter();
+    for (u32 i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
+}
+
 // Whole front end of a captured small batch in ONE CTA (n <= kSmallFrontMax):
 // zero the counters and the graph's look-back words, read the descriptor
 // straight from page-locked host memory, pack + check every update
@@ -466,6 +473,64 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
 // unique updates with a CTA-wide scan — the same output as k_prep_graph, the
 // sort and the duplicate-resolution compaction of the general path, without
 // their launches and the look-back between CTAs.
+// In-place ascending bitonic sort of buf[0, P) (P a power of two >= 32) by
+// the A = P / E threads t < A, item e of thread t = element t + A e, held in
+// registers: partners j >= A are the thread's own items, 32 <= j < A go
+// through the exchange buffer xb (named barrier 1 over the A threads),
+// j < 32 are warp shuffles.  The sorted words end in buf.
+template <int E>
+__device__ __forceinline__ void bitonic_block(u64* buf, u64* xb, u32 t, u32 A, u32 P) {
+    u64 x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) x[e] = buf[t + A * u32(e)];
+    auto bar = [A]() { asm volatile("bar.sync 1, %0;" ::"r"(A) : "memory"); };
+    u64* sb = xb;
+    for (u32 k = 2; k <= P; k <<= 1) {
+        for (u32 j = k >> 1; j >= 32; j >>= 1) {
+            if (j >= A) {
+                const u32 ej = j / A;
+#pragma unroll
+                for (int e = 0; e < E; ++e)
+#pragma unroll
+                    for (int g = e + 1; g < E; ++g)
+                        if (u32(e ^ g) == ej) {
+                            const u64 lo = min(x[e], x[g]), hi = max(x[e], x[g]);
+                            const bool asc = ((t + A * u32(e)) & k) == 0;
+                            x[e] = asc ? lo : hi;
+                            x[g] = asc ? hi : lo;
+                        }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) sb[t + A * u32(e)] = x[e];
+                bar();
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const u32 i = t + A * u32(e);
+                    const u64 y = sb[i ^ j];
+                    const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                    x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+                }
+                sb = (sb == xb) ? buf : xb;  // the next exchange writes the other buffer
+            }
+        }
+#pragma unroll
+        for (u32 j = 16; j > 0; j >>= 1) {
+            if (j < k) {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const u32 i = t + A * u32(e);
+                    const u64 y = __shfl_xor_sync(FULL, x[e], j);
+                    const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                    x[e] = keep_min ? min(x[e], y) : max(x[e], y);
+                }
+            }
+        }
+    }
+    bar();  // every exchange read done before buf is overwritten
+#pragma unroll
+    for (int e = 0; e < E; ++e) buf[t + A * u32(e)] = x[e];
+}
+
 constexpr int kSmallFrontThreads = 1024;
 constexpr int kSmallFrontItems = 4;
 constexpr u32 kSmallFrontMax = kSmallFrontThreads * kSmallFrontItems;
@@ -479,6 +544,7 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     __shared__ u32 s_wsum[kSmallFrontThreads / 32];
     __shared__ ull s_acc[4];
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    pdl_enter();  // (the chain's head: launched without the attribute, lets the leaf search be scheduled early)
     // descriptor: one word per thread over PCIe; counters + look-back words zeroed
     if (t < (sizeof(GraphFront) + 7) / 8) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
     for (u32 i = t; i < sizeof(Ctr) / 8; i += kSmallFrontThreads) reinterpret_cast<ull*>(ctr)[i] = 0;
@@ -489,19 +555,20 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     const u32 n = u32(f.ni + f.nd);
     u32 P = 32;
     while (P < n) P <<= 1;
-    // pack: item e of thread t is element t + e * 1024 (coalesced reads)
+    // pack: item e of thread t is element t + e * 1024 (coalesced reads); the
+    // words go to shared memory, ~0 pads up to P
     PrepAcc acc;
-    u64 x[kSmallFrontItems];
 #pragma unroll
     for (int e = 0; e < kSmallFrontItems; ++e) {
         const u32 i = t + u32(e) * kSmallFrontThreads;
-        x[e] = ~0ull;
         if (i < n) {
             const bool ins = i < f.ni;
             const u32 s = ins ? f.is[i] : f.ds[i - f.ni];
             const u32 d = ins ? f.id[i] : f.dd[i - f.ni];
             int cls;
-            x[e] = pack_word(f, ib, prep_code(f, db, s, d, i, ins, acc, cls), i, ins);
+            sbuf[i] = pack_word(f, ib, prep_code(f, db, s, d, i, ins, acc, cls), i, ins);
+        } else if (i < P) {
+            sbuf[i] = ~0ull;
         }
     }
 #pragma unroll
@@ -515,66 +582,20 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
         if (acc.bad) atomicMax(&s_acc[1], acc.bad);
         if (acc.oor) atomicOr(&s_acc[2], 1ull);
     }
-    // bitonic network over the first P elements (P >= 32: whole warps in or out)
-    u64* sb = sbuf;
-    for (u32 k = 2; k <= P; k <<= 1) {
-        for (u32 j = k >> 1; j > 0; j >>= 1) {
-            if (j >= kSmallFrontThreads) {
-                // partners are this thread's own items (static indices: registers)
-                static_assert(kSmallFrontItems == 4, "register exchanges below assume 4 items");
-                auto cas = [&](u64& a, u64& b, u32 i) {
-                    const u64 lo = min(a, b), hi = max(a, b);
-                    const bool asc = (i & k) == 0;
-                    a = asc ? lo : hi;
-                    b = asc ? hi : lo;
-                };
-                if (j == kSmallFrontThreads) {
-                    cas(x[0], x[1], t);
-                    if (P > 2 * kSmallFrontThreads) cas(x[2], x[3], t + 2 * kSmallFrontThreads);
-                } else {
-                    cas(x[0], x[2], t);
-                    cas(x[1], x[3], t + kSmallFrontThreads);
-                }
-            } else if (j >= 32) {
-#pragma unroll
-                for (int e = 0; e < kSmallFrontItems; ++e) {
-                    const u32 i = t + u32(e) * kSmallFrontThreads;
-                    if (i < P) sb[i] = x[e];
-                }
-                __syncthreads();
-#pragma unroll
-                for (int e = 0; e < kSmallFrontItems; ++e) {
-                    const u32 i = t + u32(e) * kSmallFrontThreads;
-                    if (i < P) {
-                        const u64 y = sb[i ^ j];
-                        const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
-                        x[e] = keep_min ? min(x[e], y) : max(x[e], y);
-                    }
-                }
-                sb = (sb == sbuf) ? sbuf + kSmallFrontMax : sbuf;  // the next exchange writes the other buffer
-            } else {
-#pragma unroll
-                for (int e = 0; e < kSmallFrontItems; ++e) {
-                    const u32 i = t + u32(e) * kSmallFrontThreads;
-                    if (i - lane < P) {  // warp-uniform
-                        const u64 y = __shfl_xor_sync(FULL, x[e], j);
-                        const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
-                        x[e] = keep_min ? min(x[e], y) : max(x[e], y);
-                    }
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int e = 0; e < kSmallFrontItems; ++e) {
-        const u32 i = t + u32(e) * kSmallFrontThreads;
-        if (i < P) sb[i] = x[e];
+    __syncthreads();
+    // only P / E threads sort (idle warps would take issue slots every stage)
+    if (P <= kSmallFrontThreads) {
+        if (t < P) bitonic_block<1>(sbuf, sbuf + kSmallFrontMax, t, P, P);
+    } else if (P == 2 * kSmallFrontThreads) {
+        bitonic_block<2>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
+    } else {
+        bitonic_block<4>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
     }
     __syncthreads();
     // duplicate resolution (segment_engine.hpp:346-363): the last word of each
     // equal-key run survives; a delete there takes the run's last insert.
     // Thread t owns the contiguous items [4t, 4t + 4) for the ordered scan.
-    const u64* ck = sb;
+    const u64* ck = sbuf;
     const u64 pmask = (1ull << ib) - 1;
     const u64 skipkey = 1ull << (2 * db);
     unsigned fm = 0;
@@ -649,6 +670,7 @@ __global__ void __launch_bounds__(256) k_leaf_search_warp(const u64* __restrict_
                                                          const u64* __restrict__ hdr, u64 L, const u8* __restrict__ st,
                                                          u64 leaf, const u64* __restrict__ ro, u64 rlo, u64 rhi,
                                                          u32* __restrict__ ul) {
+    pdl_enter();
     const u64 n = *n_dev;
     const u32 lane = threadIdx.x & 31;
     for (u64 w = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; w < n; w += (u64(gridDim.x) * blockDim.x) >> 5) {
@@ -1069,6 +1091,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
     u64* rk = &s_k[w][lane * kRowB];
     u64* rv = &s_v[w][lane * kRowB];
     const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
+    pdl_enter();
     const ull ngroups = a.ctr->ngroups;
     // tiles handed out dynamically (one counter per launch): tiles differ in
     // cost (merges vs tombstone flips vs deferrals), a static stride left
@@ -1392,6 +1415,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
     __shared__ u64 s_vk[kWarpTierWarps][32];             // Valid keys of the segment, compacted
     __shared__ unsigned char s_vl[kWarpTierWarps][32];   // their lanes
     __shared__ unsigned char s_ir[kWarpTierWarps][32];   // insert p: # Valid keys below it
+    pdl_enter();
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     const unsigned hb = G == 32 ? 0u : (lane & 16u), hl = lane & unsigned(G - 1);
     const ull ngroups = a.ctr->ngroups;
@@ -1598,6 +1622,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
 // by destination-driven placement.  Also the engine of the sequential ops.
 __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
     __shared__ ull s_w64[kCtaThreads / 32];
+    pdl_enter();
     // biglist mode: only the hub groups the warp tiers handed over
     const ull ngroups = a.biglist ? a.ctr->nbig : a.ctr->ngroups;
     Acc acc;
@@ -1771,6 +1796,7 @@ __global__ void k_grid_account(Ctr* ctr, u64 m, u64 leaf, int large) {
 __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_dev, u64 n_host,
                                  const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u64 leaf,
                                  u64* __restrict__ hdr, u64* __restrict__ ro) {
+    pdl_enter();
     const u64 nranges = n_dev ? *n_dev : n_host;
     const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
@@ -1803,6 +1829,7 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_de
 // then the appended rest)
 __global__ void k_left_walk(const u64* __restrict__ t0, u64 n0, const u64* __restrict__ trest, u64 nrest, int cb,
                             const u8* __restrict__ st, u64 leaf, u64* __restrict__ hdr, const ull* n0_dev = nullptr) {
+    pdl_enter();
     if (n0_dev) n0 = *n0_dev;
     for (u64 r = blockIdx.x * u64(blockDim.x) + threadIdx.x; r < n0 + nrest; r += u64(gridDim.x) * blockDim.x) {
         const u64 w = r < n0 ? t0[r] : trest[r - n0];
@@ -2248,17 +2275,17 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
                 return unsigned((per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148));
             }();
             const unsigned grid = grid_for((npend + 31) / 32, kLeafWarps, resident);
-            k_commit_leaf<<<grid, kLeafWarps * 32, 0, stream_>>>(a);
+            launch_k(k_commit_leaf, dim3(grid), dim3(kLeafWarps * 32), 0, stream_, a);
         } else {
             // grid for the host bound; the kernel sizes its tiles from the
             // device-side group count (<= npend)
             const unsigned grid = grid_for(npend, kWarpTierWarps, 148 * 8);
-            if (m <= 16) k_commit_lanes<16><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
-            else k_commit_lanes<32><<<grid, kWarpTierWarps * 32, 0, stream_>>>(a);
+            if (m <= 16) launch_k(k_commit_lanes<16>, dim3(grid), dim3(kWarpTierWarps * 32), 0, stream_, a);
+            else launch_k(k_commit_lanes<32>, dim3(grid), dim3(kWarpTierWarps * 32), 0, stream_, a);
         }
         GPMA_LAUNCH_CHECK();
         // CTA kernel over the hub groups only (grid bounded by npend / kBigSlice)
-        k_commit_cta<<<grid_for(npend / kBigSlice + 1, 1, 148 * 2), kCtaThreads, 0, stream_>>>(a);
+        launch_k(k_commit_cta, dim3(grid_for(npend / kBigSlice + 1, 1, 148 * 2)), dim3(kCtaThreads), 0, stream_, a);
     } else {
         a.biglist = nullptr;
         const bool grid_tier = m >= grid_seg_;
@@ -2366,6 +2393,19 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
     }();
     (void)attr;
     if (!h_desc_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_desc_dev_), h_desc_, 0));
+    if (!h_ctr_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_ctr_dev_), h_ctr, 0));
+    static const bool no_pdl = [] {
+        const char* e = std::getenv("GPMA_NO_PDL");
+        return e && *e && *e != '0';
+    }();
+    pdl_ = !no_pdl;
+    static const bool early = [] {
+        const char* e = std::getenv("GPMA_PDL_EARLY");
+        const int v = (e && *e) ? std::atoi(e) : 0;  // measured: early triggers cost ~3 us at B = 1000
+        GPMA_CUDA(cudaMemcpyToSymbol(g_pdl_early, &v, sizeof(int)));
+        return v != 0;
+    }();
+    (void)early;
     u64 dummy = 0;
     cudaGraph_t graph = nullptr;
     GPMA_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
@@ -2377,9 +2417,10 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         k_small_front<<<1, kSmallFrontThreads, kSmallFrontSmem, stream_>>>(
             h_desc_dev_, db, ib, d_ctr, small_ws_.tiles.ptr, small_ws_.tiles.cap, uk.ptr, uv.ptr, uop.ptr);
         GPMA_LAUNCH_CHECK();
-        k_leaf_search_warp<<<kSmallGraphMax / 8, 256, 0, stream_>>>(
-            uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
-        GPMA_LAUNCH_CHECK();
+        // the rest of the chain: programmatic edges (GPMA_NO_PDL=1: ordinary ones)
+        pdl_chain() = pdl_;
+        launch_k(k_leaf_search_warp, dim3(kSmallGraphMax / 8), dim3(256), 0, stream_, uk.ptr, &d_ctr->n_unique, d_hdr,
+                 num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, ul.ptr);
         u32* pcur = nullptr;
         u32* pnext = pidx0.ptr;
         for (int level = 0; level < levels; ++level) {
@@ -2388,16 +2429,17 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
             pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
         }
         // headers / row offsets of the rewritten ranges, left walks
-        k_refresh_ranges<<<64, 256, 0, stream_>>>(rlist.ptr, &d_ctr->nrefresh, 0, d_keys, d_st, cap_, leaf_, d_hdr,
-                                                  ro_base());
-        GPMA_LAUNCH_CHECK();
-        if (empty_leaves != 0) {  // headers of empty leaves inherit the next leaf's first key
-            k_left_walk<<<16, 128, 0, stream_>>>(touched.ptr, 0, nullptr, 0, touched_cb_, d_st, leaf_, d_hdr,
-                                                 &d_ctr->ngroups);
-            GPMA_LAUNCH_CHECK();
-        }
-        GPMA_CUDA(cudaMemcpyAsync(h_ctr, d_ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, stream_));
+        launch_k(k_refresh_ranges, dim3(64), dim3(256), 0, stream_, rlist.ptr, &d_ctr->nrefresh, u64(0), d_keys, d_st,
+                 cap_, leaf_, d_hdr, ro_base());
+        if (empty_leaves != 0)  // headers of empty leaves inherit the next leaf's first key
+            launch_k(k_left_walk, dim3(16), dim3(128), 0, stream_, touched.ptr, u64(0), static_cast<const u64*>(nullptr),
+                     u64(0), touched_cb_, d_st, leaf_, d_hdr, &d_ctr->ngroups);
+        static_assert(sizeof(Ctr) % 8 == 0, "counters copied as words");
+        launch_k(k_words_out, dim3(1), dim3(128), 0, stream_, reinterpret_cast<const ull*>(d_ctr),
+                 reinterpret_cast<ull*>(h_ctr_dev_), u32(sizeof(Ctr) / 8));
+        pdl_chain() = false;
     } catch (...) {
+        pdl_chain() = false;
         cudaStreamEndCapture(stream_, &graph);
         if (graph) cudaGraphDestroy(graph);
         throw;

@@ -266,6 +266,8 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     GraphFront* h_desc_ = nullptr;      // page-locked batch descriptor (copied by the graph's first node)
     GraphFront* d_desc_ = nullptr;
     GraphFront* h_desc_dev_ = nullptr;  // device view of h_desc_ (read in place by the small graph)
+    Ctr* h_ctr_dev_ = nullptr;          // device view of h_ctr (written by the small graph's last node)
+    bool pdl_ = true;                   // small graph: programmatic edges between its kernels
     ScanWorkspace small_ws_;            // the graph's own look-back words (cleared by every replay)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
     // update bucket + ordinal, per sorted position bucket

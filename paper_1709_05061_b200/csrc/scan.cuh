@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kScanThreads, 7) compact_kernel(const ull* n_d
                                                                EmitTile emit_tile, Fin fin, ull* tiles, ull epoch) {
     __shared__ unsigned s_off[kScanItems * kScanWarps];  // (item row, warp) counts -> exclusive offsets
     __shared__ ull s_prefix, s_total;
+    pdl_enter();
     const ull n = n_dev ? *n_dev : n_host;
     const ull ntiles = (n + kScanTile - 1) / kScanTile;
     const ull tile = blockIdx.x;
@@ -153,9 +154,8 @@ void run_compact_tile(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n
         GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), s));
         ws.epoch = 1;
     }
-    compact_kernel<<<static_cast<unsigned>(ntiles), kScanThreads, 0, s>>>(n_dev, n_host, flag, emit_tile, fin,
-                                                                          ws.tiles.ptr, ws.epoch);
-    GPMA_LAUNCH_CHECK();
+    launch_k(compact_kernel<Flag, EmitTile, Fin>, dim3(unsigned(ntiles)), dim3(kScanThreads), 0, s, n_dev, n_host, flag,
+             emit_tile, fin, ws.tiles.ptr, ws.epoch);
 }
 
 template <class Flag, class Emit, class Fin>

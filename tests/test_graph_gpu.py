@@ -79,8 +79,11 @@ def _window_stream(kind, nv, param, seed=1, shuffle=2):
 
 
 @pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+# (batches of up to 4096 updates take the captured small-batch graph; its
+# one-CTA sort runs 1, 2 or 4 items per thread: 512 -> 1024 updates, 700 ->
+# ~1400, 1500 -> ~3000)
 @pytest.mark.parametrize("kind,nv,param,batch", [("er", 4096, 2**-7, 512), ("rmat", 2**13, 60000, 1500),
-                                                  ("rmat", 2**12, 30000, 7)])
+                                                  ("rmat", 2**12, 30000, 7), ("er", 4096, 2**-7, 700)])
 def test_sliding_window_parity(mode, kind, nv, param, batch):
     stream = _window_stream(kind, nv, param, shuffle=2 if kind == "er" else None)
     s, d, w, _ = stream.arrays()
