@@ -457,22 +457,6 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
     prep_graph_body<kBucket>(f, db, ib, ck, ci, ctr, ba);
 }
 
-// last node of a captured small batch: the counters to page-locked host
-// memory (one kernel instead of a copy node, so the chain stays programmatic)
-__global__ void k_words_out(const ull* __restrict__ src, ull* dst, u32 nwords) {
-    pdl_enter();
-    for (u32 i = threadIdx.x; i < nwords; i += blockDim.x) dst[i] = src[i];
-}
-
-// Whole front end of a captured small batch in ONE CTA (n <= kSmallFrontMax):
-// zero the counters and the graph's look-back words, read the descriptor
-// straight from page-locked host memory, pack + check every update
-// (prep_word), bitonic-sort the packed words (compare-exchange partners
-// inside a warp by shuffles, across warps through shared memory, across a
-// thread's own items in registers), then resolve duplicates and compact the
-// unique updates with a CTA-wide scan — the same output as k_prep_graph, the
-// sort and the duplicate-resolution compaction of the general path, without
-// their launches and the look-back between CTAs.
 // In-place ascending bitonic sort of buf[0, P) (P a power of two >= 32) by
 // the A = P / E threads t < A, item e of thread t = element t + A e, held in
 // registers: partners j >= A are the thread's own items, 32 <= j < A go
@@ -544,6 +528,8 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     __shared__ u32 s_wsum[kSmallFrontThreads / 32];
     __shared__ ull s_acc[4];
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    u64 gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     pdl_enter();  // (the chain's head: launched without the attribute, lets the leaf search be scheduled early)
     // descriptor: one word per thread over PCIe; counters + look-back words zeroed
     if (t < (sizeof(GraphFront) + 7) / 8) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
@@ -653,6 +639,7 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     if (t == 0) {
         const ull total = s_wsum[kSmallFrontThreads / 32 - 1];
         ctr->nsort = n;
+        ctr->gt0 = gt0;
         ctr->gdel = s_acc[0];
         ctr->bad_ins = s_acc[1];
         ctr->oor = s_acc[2];
@@ -1795,7 +1782,8 @@ __global__ void k_grid_account(Ctr* ctr, u64 m, u64 leaf, int large) {
 // leaf i (the scan may run past the range end into untouched leaves).
 __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_dev, u64 n_host,
                                  const u64* __restrict__ keys, const u8* __restrict__ st, u64 cap, u64 leaf,
-                                 u64* __restrict__ hdr, u64* __restrict__ ro) {
+                                 u64* __restrict__ hdr, u64* __restrict__ ro, Ctr* cctr = nullptr,
+                                 Ctr* hctr = nullptr) {
     pdl_enter();
     const u64 nranges = n_dev ? *n_dev : n_host;
     const unsigned lane = threadIdx.x & 31u;
@@ -1820,6 +1808,29 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_de
                     if (is_guard(k)) ro[src_of(k) + 1] = t + 1;
                 }
             }
+        }
+    }
+    if (hctr) {
+        // captured small batches: the last CTA to finish stamps the end of
+        // the device span and returns the counters to page-locked host memory
+        // (no copy node, no event nodes)
+        __shared__ bool s_last;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(&cctr->refresh_done, 1ull) == gridDim.x - 1;
+            if (s_last) {
+                __threadfence();
+                u64 g;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+                cctr->gt1 = g;
+            }
+        }
+        __syncthreads();
+        if (s_last) {
+            const ull* src = reinterpret_cast<const ull*>(cctr);
+            ull* dst = reinterpret_cast<ull*>(hctr);
+            for (u32 i = threadIdx.x; i < sizeof(Ctr) / 8; i += blockDim.x) dst[i] = ld_volatile(src + i);
         }
     }
 }
@@ -2429,14 +2440,13 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
             pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
         }
         // headers / row offsets of the rewritten ranges, left walks
-        launch_k(k_refresh_ranges, dim3(64), dim3(256), 0, stream_, rlist.ptr, &d_ctr->nrefresh, u64(0), d_keys, d_st,
-                 cap_, leaf_, d_hdr, ro_base());
+        static_assert(sizeof(Ctr) % 8 == 0, "counters copied as words");
+        // (left walks first: the refresh's last CTA closes the device span)
         if (empty_leaves != 0)  // headers of empty leaves inherit the next leaf's first key
             launch_k(k_left_walk, dim3(16), dim3(128), 0, stream_, touched.ptr, u64(0), static_cast<const u64*>(nullptr),
                      u64(0), touched_cb_, d_st, leaf_, d_hdr, &d_ctr->ngroups);
-        static_assert(sizeof(Ctr) % 8 == 0, "counters copied as words");
-        launch_k(k_words_out, dim3(1), dim3(128), 0, stream_, reinterpret_cast<const ull*>(d_ctr),
-                 reinterpret_cast<ull*>(h_ctr_dev_), u32(sizeof(Ctr) / 8));
+        launch_k(k_refresh_ranges, dim3(64), dim3(256), 0, stream_, rlist.ptr, &d_ctr->nrefresh, u64(0), d_keys, d_st,
+                 cap_, leaf_, d_hdr, ro_base(), d_ctr, h_ctr_dev_);
         pdl_chain() = false;
     } catch (...) {
         pdl_chain() = false;
@@ -2493,12 +2503,14 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         if (out) *out = st;
         return;
     }
-    event(0);
     bool bucket = false;
+    const bool small_graph = gf && small_graph_ok(n, *gf);
+    if (!small_graph) event(0);  // (a graph batch is timed by the graph's own %globaltimer stamps)
     // ---- small graph batches: the front end and the first rounds replayed
     // as one captured CUDA graph (no per-kernel launch cost, no host round
     // trip); the host loop below continues only if updates are still pending
-    const int graph_levels = (gf && small_graph_ok(n, *gf)) ? run_small_graph(*gf, cfg) : 0;
+    const int graph_levels = small_graph ? run_small_graph(*gf, cfg) : 0;
+    const u64 graph_ns = graph_levels && h_ctr->gt1 > h_ctr->gt0 ? h_ctr->gt1 - h_ctr->gt0 : 0;
     if (graph_levels) {
         // (stage events skipped: a small batch's whole device span is the
         // graph, ev_[0] -> ev_[4]; every host API call counts at this size)
@@ -2766,6 +2778,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         launches += 1;
     }
     const bool host_levels = npend > 0;
+    if (graph_levels && host_levels) event(0);  // the host-loop levels' span (added to the graph's)
     if (npend > 0) {
         for (int level = level0;; ++level) {
             enqueue_level(level, npend, pcur, pnext, touched_ptr, n, cfg, ws, true, launches);
@@ -2992,14 +3005,20 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             ++launches;
         }
     }
-    event(4);
-    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    if (!graph_levels || host_levels) {  // (a graph-only batch: recorded by the graph, synchronised already)
+        event(4);
+        GPMA_CUDA(cudaStreamSynchronize(stream_));
+    }
     st.slot_writes = slot_writes - writes_base;
     st.num_touched_ranges = last_ntouched;
     st.segment_phase_ns = u64(double(seg_ms) * 1e6);
     float a = 0, b = 0, c = 0, d = 0;
     if (graph_levels) {
-        cudaEventElapsedTime(&a, ev_[0], ev_[4]);  // the graph + any host-loop levels: reported as one stage
+        // the graph (its %globaltimer span) + any host-loop levels: reported as one stage
+        a = float(double(graph_ns) * 1e-6);
+        float hl = 0;
+        if (host_levels) cudaEventElapsedTime(&hl, ev_[0], ev_[4]);
+        a += hl;
     } else {
         cudaEventElapsedTime(&a, ev_[0], ev_[1]);
         cudaEventElapsedTime(&b, ev_[1], ev_[2]);

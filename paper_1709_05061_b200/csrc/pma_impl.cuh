@@ -61,6 +61,8 @@ struct Ctr {
     ull nsort;      // graph-captured small batches: the batch size, written by the front end
     ull leaf_tiles; // k_commit_leaf's dynamic tile counter (level 0 runs once per batch)
     ull ngrid;      // grid tier: groups handed over by k_commit_cta at this level
+    ull gt0, gt1;   // captured small batches: %globaltimer at the first kernel's entry / the last refresh CTA's exit
+    ull refresh_done;  // captured small batches: refresh CTAs finished (the last returns the counters)
     ull seg_tomb, seg_empty;  // grid tier: tombstones / empty leaves of the segment before its merge
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
