@@ -457,64 +457,89 @@ __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront 
     prep_graph_body<kBucket>(f, db, ib, ck, ci, ctr, ba);
 }
 
-// In-place ascending bitonic sort of buf[0, P) (P a power of two >= 32) by
-// the A = P / E threads t < A, item e of thread t = element t + A e, held in
-// registers: partners j >= A are the thread's own items, 32 <= j < A go
-// through the exchange buffer xb (named barrier 1 over the A threads),
-// j < 32 are warp shuffles.  The sorted words end in buf.
+// In-place ascending sort of buf[0, P) (P a power of two >= 32 E) by the
+// A = P / E threads t < A (named barrier 1).  Each warp first sorts its
+// contiguous run of 32 E words in registers — item e of a lane is run
+// element 32 e + lane, so bitonic partners j < 32 are shuffles and j >= 32
+// the lane's own items: no shared memory, no barrier — then runs are merged
+// pairwise through shared memory (merge path: each thread finds the split
+// of its E consecutive outputs by bisection and merges them), log2(P / 32E)
+// rounds.  Words are distinct or identical, so stability is immaterial.
 template <int E>
-__device__ __forceinline__ void bitonic_block(u64* buf, u64* xb, u32 t, u32 A, u32 P) {
+__device__ __forceinline__ void sort_block(u64* buf, u64* xb, u32 t, u32 A, u32 P) {
+    constexpr u32 R0 = 32 * E;
+    const u32 lane = t & 31, base = (t >> 5) * R0;
     u64 x[E];
 #pragma unroll
-    for (int e = 0; e < E; ++e) x[e] = buf[t + A * u32(e)];
-    auto bar = [A]() { asm volatile("bar.sync 1, %0;" ::"r"(A) : "memory"); };
-    u64* sb = xb;
-    for (u32 k = 2; k <= P; k <<= 1) {
-        for (u32 j = k >> 1; j >= 32; j >>= 1) {
-            if (j >= A) {
-                const u32 ej = j / A;
+    for (int e = 0; e < E; ++e) x[e] = buf[base + 32 * u32(e) + lane];
+#pragma unroll
+    for (u32 k = 2; k <= R0; k <<= 1) {
+#pragma unroll
+        for (u32 j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
 #pragma unroll
                 for (int e = 0; e < E; ++e)
 #pragma unroll
                     for (int g = e + 1; g < E; ++g)
-                        if (u32(e ^ g) == ej) {
+                        if (u32(e ^ g) == j / 32) {
                             const u64 lo = min(x[e], x[g]), hi = max(x[e], x[g]);
-                            const bool asc = ((t + A * u32(e)) & k) == 0;
+                            const bool asc = ((32 * u32(e) + lane) & k) == 0;
                             x[e] = asc ? lo : hi;
                             x[g] = asc ? hi : lo;
                         }
             } else {
 #pragma unroll
-                for (int e = 0; e < E; ++e) sb[t + A * u32(e)] = x[e];
-                bar();
-#pragma unroll
                 for (int e = 0; e < E; ++e) {
-                    const u32 i = t + A * u32(e);
-                    const u64 y = sb[i ^ j];
-                    const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
-                    x[e] = keep_min ? min(x[e], y) : max(x[e], y);
-                }
-                sb = (sb == xb) ? buf : xb;  // the next exchange writes the other buffer
-            }
-        }
-#pragma unroll
-        for (u32 j = 16; j > 0; j >>= 1) {
-            if (j < k) {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const u32 i = t + A * u32(e);
+                    const u32 q = 32 * u32(e) + lane;
                     const u64 y = __shfl_xor_sync(FULL, x[e], j);
-                    const bool keep_min = ((i & k) == 0) == ((i & j) == 0);
+                    const bool keep_min = ((q & k) == 0) == ((q & j) == 0);
                     x[e] = keep_min ? min(x[e], y) : max(x[e], y);
                 }
             }
         }
     }
-    bar();  // every exchange read done before buf is overwritten
 #pragma unroll
-    for (int e = 0; e < E; ++e) buf[t + A * u32(e)] = x[e];
+    for (int e = 0; e < E; ++e) buf[base + 32 * u32(e) + lane] = x[e];
+    auto bar = [A]() { asm volatile("bar.sync 1, %0;" ::"r"(A) : "memory"); };
+    bar();
+    u64* src = buf;
+    u64* dst = xb;
+    for (u32 R = R0; R < P; R <<= 1) {
+        const u32 o0 = E * t;
+        const u32 ps = o0 & ~(2 * R - 1), d = o0 - ps;
+        const u64* Ar = src + ps;
+        const u64* Br = Ar + R;
+        u32 lo = d > R ? d - R : 0, hi = d < R ? d : R;
+        while (lo < hi) {  // first a with A[a] > B[d - a - 1]
+            const u32 mid = (lo + hi) >> 1;
+            if (Ar[mid] <= Br[d - mid - 1]) lo = mid + 1;
+            else hi = mid;
+        }
+        u32 ia = lo, ib = d - lo;
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const bool take_a = ib >= R || (ia < R && Ar[ia] <= Br[ib]);
+            dst[o0 + e] = take_a ? Ar[ia++] : Br[ib++];
+        }
+        bar();
+        u64* tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    if (src != buf) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) buf[E * t + e] = src[E * t + e];
+        bar();
+    }
 }
 
+// Whole front end of a captured small batch in ONE CTA (n <= kSmallFrontMax):
+// zero the counters and the graph's look-back words, read the descriptor
+// straight from page-locked host memory, pack + check every update
+// (prep_code), sort the packed words (sort_block), then resolve duplicates
+// and compact the unique updates with a CTA-wide scan — the same output as
+// k_prep_graph, the radix sort and the duplicate-resolution compaction of the
+// general path, without their launches and the look-back between CTAs.
 constexpr int kSmallFrontThreads = 1024;
 constexpr int kSmallFrontItems = 4;
 constexpr u32 kSmallFrontMax = kSmallFrontThreads * kSmallFrontItems;
@@ -571,11 +596,11 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     __syncthreads();
     // only P / E threads sort (idle warps would take issue slots every stage)
     if (P <= kSmallFrontThreads) {
-        if (t < P) bitonic_block<1>(sbuf, sbuf + kSmallFrontMax, t, P, P);
+        if (t < P) sort_block<1>(sbuf, sbuf + kSmallFrontMax, t, P, P);
     } else if (P == 2 * kSmallFrontThreads) {
-        bitonic_block<2>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
+        sort_block<2>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
     } else {
-        bitonic_block<4>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
+        sort_block<4>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
     }
     __syncthreads();
     // duplicate resolution (segment_engine.hpp:346-363): the last word of each

@@ -95,7 +95,7 @@ class UpdateStats:
     @classmethod
     def from_c(cls, s: pma_stats, touched=None) -> "UpdateStats":
         return cls(s.batch_size, s.rounds, s.slot_writes, s.wall_ns, s.segment_phase_ns,
-                   [s.segments_per_level[i] for i in range(s.num_levels)], s.grow_events, s.shrink_events,
+                   s.segments_per_level[:s.num_levels], s.grow_events, s.shrink_events,
                    s.deletes_missed, s.tombstones_added, touched if touched is not None else [], bool(s.resized))
 
     def parity(self) -> dict:
@@ -416,10 +416,14 @@ class DynamicGraph:
 
     def apply_batch_device(self, d_is: int, d_id: int, d_iw: int | None, ni: int, d_ds: int, d_dd: int,
                            nd: int) -> UpdateStats:
-        st = pma_stats()
-        vp = C.c_void_p
-        self._check(self._lib.gpma_apply_batch_device(self.h, vp(d_is), vp(d_id), vp(d_iw) if d_iw else None, ni,
-                                                      vp(d_ds), vp(d_dd), nd, C.byref(st)))
+        # (the small-batch latency path: argtypes convert the raw addresses,
+        # one stats struct per graph is reused)
+        st = self.__dict__.get("_dev_st")
+        if st is None:
+            st = self._dev_st = pma_stats()
+        rc = self._lib.gpma_apply_batch_device(self.h, d_is, d_id, d_iw or None, ni, d_ds, d_dd, nd, C.byref(st))
+        if rc:
+            self._check(rc)
         return UpdateStats.from_c(st)
 
     def reserve_batch(self, max_updates: int):
