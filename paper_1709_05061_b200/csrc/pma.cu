@@ -71,6 +71,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     GPMA_CUDA(cudaMalloc(&d_desc_, sizeof(GraphFront)));
     if (const char* e = std::getenv("GPMA_NO_GRAPHS")) small_graphs_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_BUCKETS")) buckets_ = e[0] == '0';
+    if (const char* e = std::getenv("GPMA_NO_PDL")) pdl_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     for (auto& e : lev_ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -1864,9 +1865,11 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_de
 // (over the batch's touched words: level 0's dense words t0 — ~0 = none —
 // then the appended rest)
 __global__ void k_left_walk(const u64* __restrict__ t0, u64 n0, const u64* __restrict__ trest, u64 nrest, int cb,
-                            const u8* __restrict__ st, u64 leaf, u64* __restrict__ hdr, const ull* n0_dev = nullptr) {
+                            const u8* __restrict__ st, u64 leaf, u64* __restrict__ hdr, const ull* n0_dev = nullptr,
+                            const ull* nrest_dev = nullptr) {
     pdl_enter();
     if (n0_dev) n0 = *n0_dev;
+    if (nrest_dev) nrest = *nrest_dev;
     for (u64 r = blockIdx.x * u64(blockDim.x) + threadIdx.x; r < n0 + nrest; r += u64(gridDim.x) * blockDim.x) {
         const u64 w = r < n0 ? t0[r] : trest[r - n0];
         if (w == ~0ull) continue;
@@ -2430,11 +2433,6 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
     (void)attr;
     if (!h_desc_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_desc_dev_), h_desc_, 0));
     if (!h_ctr_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_ctr_dev_), h_ctr, 0));
-    static const bool no_pdl = [] {
-        const char* e = std::getenv("GPMA_NO_PDL");
-        return e && *e && *e != '0';
-    }();
-    pdl_ = !no_pdl;
     static const bool early = [] {
         const char* e = std::getenv("GPMA_PDL_EARLY");
         const int v = (e && *e) ? std::atoi(e) : 0;  // measured: early triggers cost ~3 us at B = 1000
@@ -2469,7 +2467,7 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         // (left walks first: the refresh's last CTA closes the device span)
         if (empty_leaves != 0)  // headers of empty leaves inherit the next leaf's first key
             launch_k(k_left_walk, dim3(16), dim3(128), 0, stream_, touched.ptr, u64(0), static_cast<const u64*>(nullptr),
-                     u64(0), touched_cb_, d_st, leaf_, d_hdr, &d_ctr->ngroups);
+                     u64(0), touched_cb_, d_st, leaf_, d_hdr, &d_ctr->ngroups, static_cast<const ull*>(nullptr));
         launch_k(k_refresh_ranges, dim3(64), dim3(256), 0, stream_, rlist.ptr, &d_ctr->nrefresh, u64(0), d_keys, d_st,
                  cap_, leaf_, d_hdr, ro_base(), d_ctr, h_ctr_dev_);
         pdl_chain() = false;
@@ -2587,12 +2585,16 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                  L <= 8 * n && bucket_skip_ == 0 && buckets_;
         if (bucket_skip_) --bucket_skip_;
         if (bucket) {
+            const u32* bc0 = bcnt.ptr;
             bcnt.reserve(L + 2);
+            if (bcnt.ptr != bc0) bcnt_zero_ = 0;  // reallocated
             boff.reserve(L + 2);
             blf.reserve(n);
             bod.reserve(n);
             bslf.reserve(n);
-            GPMA_CUDA(cudaMemsetAsync(bcnt.ptr, 0, (L + 2) * sizeof(u32), stream_));
+            // the counters are left zeroed by the previous batch's scan
+            if (bcnt_zero_ < L + 2) GPMA_CUDA(cudaMemsetAsync(bcnt.ptr, 0, bcnt.cap * sizeof(u32), stream_));
+            bcnt_zero_ = 0;  // counted into below; zero again once the scan is enqueued
             ba = BucketArgs{d_hdr, L, d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices, bcnt.ptr, blf.ptr, bod.ptr};
             k_prep_graph<true><<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(*gf, db, ib, sk_in.ptr, si_in.ptr,
                                                                                d_ctr, ba);
@@ -2639,7 +2641,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     const u32* sorted_ci = si_in.ptr;
     if (bucket) {
         const u64 L = num_leaves();
-        exclusive_sum(stream_, ws, bcnt.ptr, boff.ptr, L + 2);
+        exclusive_sum(stream_, ws, bcnt.ptr, boff.ptr, L + 2, bcnt.ptr);  // (leaves bcnt[0, L + 2) zeroed)
+        bcnt_zero_ = bcnt.cap;  // (entries past L + 2 were never counted into)
         const bool pairs = packed_ib == 0;
         static const unsigned scat_res = resident_grid(k_bucket_scatter, 256);
         static const unsigned sort_res = resident_grid(k_bucket_sort_small, 256);
@@ -2804,14 +2807,58 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     }
     const bool host_levels = npend > 0;
     if (graph_levels && host_levels) event(0);  // the host-loop levels' span (added to the graph's)
+    // speculative tail before each sync of the host loop (not after the root
+    // path, which rebuilds headers in closed form; GPMA_NO_SPEC_TAIL=1 turns it off)
+    static const bool no_spec_tail = [] {
+        const char* e = std::getenv("GPMA_NO_SPEC_TAIL");
+        return e && *e && *e != '0';
+    }();
+    const bool spec_tail_ok = !no_spec_tail;
+    bool spec_tail = false, spec_walk = false;
     if (npend > 0) {
         for (int level = level0;; ++level) {
-            enqueue_level(level, npend, pcur, pnext, touched_ptr, n, cfg, ws, true, launches);
+            // the level's kernels chained by programmatic edges (each waits
+            // for its predecessor in pdl_enter; the launch overlaps its tail)
+            pdl_chain() = pdl_;
+            try {
+                enqueue_level(level, npend, pcur, pnext, touched_ptr, n, cfg, ws, true, launches);
+            } catch (...) {
+                pdl_chain() = false;
+                throw;
+            }
+            pdl_chain() = false;
             pcur = pnext;
             pnext = (pcur == pidx0.ptr) ? pidx1.ptr : pidx0.ptr;
             const bool speculate = npend >= (1u << 16) && (level & 1) == 0 && level < height_;
             if (speculate) continue;  // next round straight away; stats at the next sync
-            sync_ctr();
+            if (spec_tail_ok) {
+                // the counters first (the host waits for them only), then
+                // this may be the last level: the tail (header / row-offset
+                // refresh, left walks, end event) goes in before the sync,
+                // gated by the device counts, so the GPU does not idle while
+                // the host learns that nothing is left.  Both passes recompute
+                // from the current slots, so when more levels follow they are
+                // simply redone at the end.
+                GPMA_CUDA(cudaMemcpyAsync(h_ctr, d_ctr, sizeof(Ctr), cudaMemcpyDeviceToHost, stream_));
+                event(5);
+                if (!graph_levels) event(3);
+                k_refresh_ranges<<<148 * 4, 256, 0, stream_>>>(rlist.ptr, &d_ctr->nrefresh, 0, d_keys, d_st, cap_,
+                                                              leaf_, d_hdr, ro_base());
+                GPMA_LAUNCH_CHECK();
+                spec_walk = empty_leaves != 0;
+                if (spec_walk) {
+                    k_left_walk<<<148 * 8, 128, 0, stream_>>>(touched_ptr, 0, touched_ptr + touched_split_, 0,
+                                                              touched_cb_, d_st, leaf_, d_hdr, &d_ctr->lvl_groups[0],
+                                                              &d_ctr->ntouched_next);
+                    GPMA_LAUNCH_CHECK();
+                }
+                event(4);
+                launches += spec_walk ? 2 : 1;
+                spec_tail = true;
+                GPMA_CUDA(cudaEventSynchronize(ev_[5]));
+            } else {
+                sync_ctr();
+            }
             for (int l = synced_upto + 1; l <= level; ++l) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, lev_ev_[2 * l], lev_ev_[2 * l + 1]);
@@ -2830,6 +2877,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             ntouched = h_ctr->ntouched_next;
             const u64 left = h_ctr->np[(level + 1) & 1];
             if (left == 0) break;
+            spec_tail = false;  // more levels: the tail is redone after them
             npend = left;
             if (level == height_) {
                 // root path: everything left is the single root group
@@ -2995,7 +3043,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.merge_slots = h_ctr->merge_slots;
     timing.commit_bytes = h_ctr->commit_bytes;
     timing.tombstone_flips = st.tombstones_added;
-    if (!graph_levels) event(3);
+    if (!graph_levels && !spec_tail) event(3);
     // ---- 5. refresh leaf headers / row offsets ----
     // The warp tier refreshed dense segments in place; sparse and CTA-tier
     // segments were queued on rlist; left walks are needed only while empty
@@ -3013,6 +3061,17 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     } else if (graph_levels && !host_levels) {
         // the graph refreshed the headers / row offsets and walked left
         if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
+    } else if (spec_tail) {
+        // refreshed (and walked, if empty leaves were known) before the last
+        // sync; a walk is still due if this batch created the first empty leaves
+        if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
+        if (!spec_walk && last_ntouched > 0 && empty_leaves != 0) {
+            k_left_walk<<<grid_for(last_ngroups0_ + ntouched, 128, 148 * 8), 128, 0, stream_>>>(
+                touched_ptr, last_ngroups0_, touched_ptr + touched_split_, ntouched, touched_cb_, d_st, leaf_, d_hdr);
+            GPMA_LAUNCH_CHECK();
+            ++launches;
+            spec_tail = false;  // (synchronise below)
+        }
     } else {
         if (empty_leaves >= 0) empty_leaves += h_ctr->empty_delta;
         const u64 nref = h_ctr->nrefresh;
@@ -3031,7 +3090,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         }
     }
     if (!graph_levels || host_levels) {  // (a graph-only batch: recorded by the graph, synchronised already)
-        event(4);
+        if (!spec_tail) event(4);  // (a speculative tail recorded it)
         GPMA_CUDA(cudaStreamSynchronize(stream_));
     }
     st.slot_writes = slot_writes - writes_base;

@@ -274,6 +274,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
     // update bucket + ordinal, per sorted position bucket
     DevBuf<u32> bcnt, boff, blf, bod, bslf, bbig;
+    u64 bcnt_zero_ = 0;  // bcnt[0, bcnt_zero_) is known zero (the bucket scan clears what it reads)
     int bucket_skip_ = 0;  // batches left on the radix sort after a bucket overflow
     bool buckets_ = true;  // GPMA_NO_BUCKETS=1: always the radix front end (A/B measurements)
     static constexpr u64 kBucketMinBatch = 1u << 16;

@@ -381,23 +381,36 @@ __global__ void __launch_bounds__(kRadixThreads, 1)
 // out[i] = sum of in[0..i) for n values (u32 in, u32 out; totals must fit).
 // A tile is 256 threads x 8 consecutive values; warp 0 runs the look-back
 // over epoch-tagged tile words exactly as compact_kernel does.
-constexpr int kSumItems = 8;
+constexpr int kSumItems = 16;  // 4096-word tiles: half the look-back chain of 2048 (measured on 4M counters)
 constexpr int kSumTile = kScanThreads * kSumItems;
 
 static __global__ void __launch_bounds__(kScanThreads) k_exclusive_sum(const u32* __restrict__ in, u32* __restrict__ out,
-                                                                u64 n, ull* tiles, ull epoch) {
+                                                                u64 n, ull* tiles, ull epoch, u32* clear) {
     __shared__ u32 s_w[kScanWarps];
     __shared__ ull s_prefix;
     const u64 tile = blockIdx.x;
     const u64 i0 = tile * kSumTile + u64(threadIdx.x) * kSumItems;
     u32 x[kSumItems];
+    static_assert(kSumItems % 4 == 0, "vector loads of 4 words");
     if (i0 + kSumItems <= n && ((reinterpret_cast<uintptr_t>(in + i0) & 15) == 0)) {
-        const uint4 a = *reinterpret_cast<const uint4*>(in + i0);
-        const uint4 b = *reinterpret_cast<const uint4*>(in + i0 + 4);
-        x[0] = a.x, x[1] = a.y, x[2] = a.z, x[3] = a.w, x[4] = b.x, x[5] = b.y, x[6] = b.z, x[7] = b.w;
+#pragma unroll
+        for (int q = 0; q < kSumItems / 4; ++q) {
+            const uint4 a = *reinterpret_cast<const uint4*>(in + i0 + 4 * q);
+            x[4 * q] = a.x, x[4 * q + 1] = a.y, x[4 * q + 2] = a.z, x[4 * q + 3] = a.w;
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < kSumItems; ++j) x[j] = i0 + j < n ? in[i0 + j] : 0u;
+    }
+    if (clear) {  // the counters read here are zeroed for their next use (no separate memset)
+        if (i0 + kSumItems <= n && ((reinterpret_cast<uintptr_t>(clear + i0) & 15) == 0)) {
+#pragma unroll
+            for (int q = 0; q < kSumItems / 4; ++q) *reinterpret_cast<uint4*>(clear + i0 + 4 * q) = make_uint4(0, 0, 0, 0);
+        } else {
+#pragma unroll
+            for (int j = 0; j < kSumItems; ++j)
+                if (i0 + j < n) clear[i0 + j] = 0;
+        }
     }
     u32 sum = 0;
 #pragma unroll
@@ -443,8 +456,9 @@ static __global__ void __launch_bounds__(kScanThreads) k_exclusive_sum(const u32
         run += x[j];
     }
     if (i0 + kSumItems <= n && ((reinterpret_cast<uintptr_t>(out + i0) & 15) == 0)) {
-        *reinterpret_cast<uint4*>(out + i0) = make_uint4(y[0], y[1], y[2], y[3]);
-        *reinterpret_cast<uint4*>(out + i0 + 4) = make_uint4(y[4], y[5], y[6], y[7]);
+#pragma unroll
+        for (int q = 0; q < kSumItems / 4; ++q)
+            *reinterpret_cast<uint4*>(out + i0 + 4 * q) = make_uint4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
     } else {
 #pragma unroll
         for (int j = 0; j < kSumItems; ++j)
@@ -452,7 +466,8 @@ static __global__ void __launch_bounds__(kScanThreads) k_exclusive_sum(const u32
     }
 }
 
-inline void exclusive_sum(cudaStream_t s, ScanWorkspace& ws, const u32* in, u32* out, u64 n) {
+// clear (optional) = in: the input counters are left zeroed
+inline void exclusive_sum(cudaStream_t s, ScanWorkspace& ws, const u32* in, u32* out, u64 n, u32* clear = nullptr) {
     if (n == 0) return;
     const u64 ntiles = (n + kSumTile - 1) / kSumTile;
     if (ntiles > ws.tiles.cap) {
@@ -464,7 +479,7 @@ inline void exclusive_sum(cudaStream_t s, ScanWorkspace& ws, const u32* in, u32*
         GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), s));
         ws.epoch = 1;
     }
-    k_exclusive_sum<<<unsigned(ntiles), kScanThreads, 0, s>>>(in, out, n, ws.tiles.ptr, ws.epoch);
+    k_exclusive_sum<<<unsigned(ntiles), kScanThreads, 0, s>>>(in, out, n, ws.tiles.ptr, ws.epoch, clear);
     GPMA_LAUNCH_CHECK();
 }
 
