@@ -66,213 +66,267 @@ __global__ void k_iota_u32(u32* a, u64 n) {
 }
 
 // -------- BFS (analytics.hpp:22-48): frontier queues split by row length.
-// Light rows (<= kHeavyRow slots): a warp per frontier vertex, lanes stride
-// its slot interval (coalesced 8-B keys + 1-B states).  Heavy rows (RMAT
-// hubs): kHeavyParts CTAs per vertex, each striding 1/kHeavyParts of the row,
-// so one hub never serialises a level on a single warp.  Discovery is a CAS on
-// dist; discovered vertices are enqueued (warp-aggregated: ballot + popc + one
-// atomic per warp and queue) into the light or heavy next queue by their own
-// row length.
+// Light rows (<= kHeavyRow slots): a warp walks up to 32 frontier rows at
+// once (k_bfs_expand).  Heavy rows: kHeavyParts warps per row; huge rows
+// (hubs): kHugeParts CTAs per row, so one hub never serialises a level
+// (k_bfs_expand_heavy).  Discovery claims a visited bit; discovered vertices
+// are enqueued (warp-aggregated: ballot + popc + one atomic per warp and
+// queue) into the light, heavy or huge next queue by their own row length.
 constexpr u64 kHeavyRow = 1024;
 // fixed grids (levels run back to back with device-side frontier sizes);
 // measured on the C2 hub BFS: light 148x32 / heavy 148x64 CTAs beat 148x16 /
 // 148x8 by 20% (more heavy-row parts in flight), and more parts per heavy row
 // (64, 128) lose
 constexpr unsigned kBfsLightGrid = 148 * 32, kBfsHeavyGrid = 148 * 64;
-constexpr u32 kHeavyParts = 32;
+#ifndef GPMA_BFS_HEAVY_PARTS
+#define GPMA_BFS_HEAVY_PARTS 8
+#endif
+#ifndef GPMA_BFS_HUGE_ROW
+#define GPMA_BFS_HUGE_ROW 16384
+#endif
+constexpr u32 kHeavyParts = GPMA_BFS_HEAVY_PARTS;  // heavy rows (kHeavyRow, kHugeRow]: a warp per part
+constexpr u64 kHugeRow = GPMA_BFS_HUGE_ROW;        // huge rows (hubs): a CTA per part
+constexpr u32 kHugeParts = 32;
+constexpr u32 kBfsQueue = 512;  // per-warp candidate queue (shared memory)
 
 // Discovery: a visited bitmap (|V| bits: 256 KB at C2, L1/L2-resident) is
 // probed first and claimed with atomicOr; only the winner writes dist.  The
 // probes of the frontier's edges are the BFS's dominant cost, and the bitmap
 // is 32x smaller than dist.  (A stale "unset" bit only costs an atomic.)
-__device__ __forceinline__ bool bfs_claim(u32* __restrict__ vis, u32* __restrict__ dist, u32 v, u32 depth) {
-    const u32 bit = 1u << (v & 31u);
-    if (vis[v >> 5] & bit) return false;
-    if (atomicOr(&vis[v >> 5], bit) & bit) return false;
-    dist[v] = depth;
-    return true;
-}
+// Light rows: k_bfs_expand; heavy rows: k_bfs_expand_heavy; both claim
+// through bfs_claim4.
 
-__device__ __forceinline__ void bfs_visit(const u64* __restrict__ ro, const u64* __restrict__ keys,
-                                          const u8* __restrict__ st, u32* __restrict__ dist, u32* __restrict__ vis,
-                                          u32 depth, u64 t, u64 e,
-                                          u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
-    const unsigned lane = threadIdx.x & 31u;
-    bool won = false;
-    u32 v = 0;
-    if (t < e && st[t] == kValid) {
-        const u64 k = keys[t];
-        if (!is_guard(k)) {
-            v = dst_of(k);
-            won = bfs_claim(vis, dist, v, depth);
+// Claim up to 4 candidate neighbours per lane (v[j], cand[j]): the bitmap
+// CASes are issued together, then the winners' dist stores and row-bound
+// loads (light / heavy by their own row length), then ONE warp-aggregated
+// append per queue for all 4 rounds.
+__device__ __forceinline__ void bfs_claim4(const u64* __restrict__ ro, u32* __restrict__ dist, u32* __restrict__ vis,
+                                           u32 depth, const u32 (&v)[4], const bool (&cand)[4],
+                                           u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ gnext,
+                                           u32* __restrict__ qn) {
+    const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
+    u32 old[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) old[j] = cand[j] ? atomicOr(&vis[v[j] >> 5], 1u << (v[j] & 31u)) : ~0u;
+    bool won[4];
+    u64 lo[4], hi[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        won[j] = !((old[j] >> (v[j] & 31u)) & 1u);
+        lo[j] = hi[j] = 0;
+        if (won[j]) {
+            dist[v[j]] = depth;
+            lo[j] = ro[v[j]];
+            hi[j] = ro[v[j] + 1];
         }
     }
-    const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
-    const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
-    if (lm) {
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
-        base = __shfl_sync(FULL, base, 0);
-        if (won && !heavy) next[base + __popc(lm & lanemask_lt())] = v;
+    unsigned lm[4], hm[4], gm[4];
+    u32 nl = 0, nh = 0, ng = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const u64 len = hi[j] - lo[j];
+        const bool huge = won[j] && len > kHugeRow, heavy = won[j] && len > kHeavyRow && !huge;
+        lm[j] = __ballot_sync(FULL, won[j] && !heavy && !huge);
+        hm[j] = __ballot_sync(FULL, heavy);
+        gm[j] = __ballot_sync(FULL, huge);
+        nl += __popc(lm[j]);
+        nh += __popc(hm[j]);
+        ng += __popc(gm[j]);
     }
-    if (hm) {
-        u32 base = 0;
-        if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
-        base = __shfl_sync(FULL, base, 0);
-        if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v;
+    u32 bl = 0, bh = 0, bg = 0;
+    if (lane == 0) {
+        if (nl) bl = atomicAdd(&qn[0], nl);
+        if (nh) bh = atomicAdd(&qn[1], nh);
+        if (ng) bg = atomicAdd(&qn[2], ng);
+    }
+    bl = __shfl_sync(FULL, bl, 0);
+    bh = __shfl_sync(FULL, bh, 0);
+    bg = __shfl_sync(FULL, bg, 0);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if ((lm[j] >> lane) & 1u) next[bl + __popc(lm[j] & below)] = v[j];
+        if ((hm[j] >> lane) & 1u) hnext[bh + __popc(hm[j] & below)] = v[j];
+        if ((gm[j] >> lane) & 1u) gnext[bg + __popc(gm[j] & below)] = v[j];
+        bl += __popc(lm[j]);
+        bh += __popc(hm[j]);
+        bg += __popc(gm[j]);
     }
 }
 
-// Valid non-guard neighbours are packed into a per-warp queue (ballot ranks)
-// across 128-slot chunks and rows, then probed 32 at a time with every lane
-// busy: most slots of a row are gaps and short rows are the norm.
+// Unvisited-looking neighbours are packed into a per-warp queue (ballot
+// ranks) and claimed 128 at a time (bfs_claim4) with every lane busy.
 struct BfsWarpQueue {
-    u32* q;    // 256 entries of shared memory
+    u32* q;    // kBfsQueue entries of shared memory
     u32 cnt;   // warp-uniform
     __device__ __forceinline__ void drain(const u64* __restrict__ ro, u32* __restrict__ dist, u32* __restrict__ vis,
-                                          u32 depth,
-                                          u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ qn) {
-        const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
+                                          u32 depth, u32* __restrict__ next, u32* __restrict__ hnext,
+                                          u32* __restrict__ gnext, u32* __restrict__ qn) {
+        const unsigned lane = threadIdx.x & 31u;
         __syncwarp();
-        for (u32 base = 0; base < cnt; base += 32) {
-            const bool act = base + lane < cnt;
-            const u32 v = act ? q[base + lane] : 0u;
-            bool won = false;
-            if (act) won = bfs_claim(vis, dist, v, depth);
-            const bool heavy = won && (ro[v + 1] - ro[v]) > kHeavyRow;
-            const unsigned lm = __ballot_sync(FULL, won && !heavy), hm = __ballot_sync(FULL, heavy);
-            if (lm) {
-                u32 o = 0;
-                if (lane == 0) o = atomicAdd(&qn[0], u32(__popc(lm)));
-                o = __shfl_sync(FULL, o, 0);
-                if (won && !heavy) next[o + __popc(lm & below)] = v;
+        for (u32 base = 0; base < cnt; base += 128) {
+            u32 v[4];
+            bool c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const u32 i = base + 32 * j + lane;
+                c[j] = i < cnt;
+                v[j] = c[j] ? q[i] : 0u;
             }
-            if (hm) {
-                u32 o = 0;
-                if (lane == 0) o = atomicAdd(&qn[1], u32(__popc(hm)));
-                o = __shfl_sync(FULL, o, 0);
-                if (heavy) hnext[o + __popc(hm & below)] = v;
-            }
+            bfs_claim4(ro, dist, vis, depth, v, c, next, hnext, gnext, qn);
         }
         __syncwarp();
         cnt = 0;
     }
-    // the 128 slots [t0, t0 + 128) ∩ [., e): lane l reads t0 + 32 j + l
-    __device__ __forceinline__ void push128(const u64* __restrict__ keys, const u8* __restrict__ st, u64 t0, u64 e,
-                                            const u64* __restrict__ ro, u32* __restrict__ dist, u32* __restrict__ vis,
-                                            u32 depth, u32* __restrict__ next, u32* __restrict__ hnext,
-                                            u32* __restrict__ qn) {
-        const unsigned lane = threadIdx.x & 31u, below = lanemask_lt();
-        u32 vv[4];
-        bool ok[4];
+    // 4 candidates per lane (ballot-packed); drains when fewer than 128 slots remain
+    __device__ __forceinline__ void push4(const u32 (&v)[4], const bool (&c)[4], const u64* __restrict__ ro,
+                                          u32* __restrict__ dist, u32* __restrict__ vis, u32 depth,
+                                          u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ gnext,
+                                          u32* __restrict__ qn) {
+        const unsigned below = lanemask_lt();
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const u64 t = t0 + 32 * j + lane;
-            ok[j] = false;
-            vv[j] = 0;
-            if (t < e && st[t] == kValid) {
-                const u64 k = keys[t];
-                ok[j] = !is_guard(k);
-                vv[j] = dst_of(k);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const unsigned m = __ballot_sync(FULL, ok[j]);
-            if (ok[j]) q[cnt + __popc(m & below)] = vv[j];
+            const unsigned m = __ballot_sync(FULL, c[j]);
+            if (c[j]) q[cnt + __popc(m & below)] = v[j];
             cnt += __popc(m);
         }
-        if (cnt >= 128) drain(ro, dist, vis, depth, next, hnext, qn);  // room for the next chunk stays
+        if (cnt > kBfsQueue - 128) drain(ro, dist, vis, depth, next, hnext, gnext, qn);
     }
 };
 
-// (frontier sizes are read from the device: levels run back to back, the
-// host only syncs once per window of levels)
-// four slots per thread per call (t, t + S, t + 2S, t + 3S; S = the
-// caller's stride, so each of the four rounds of loads is coalesced across the
-// warp): the key/state loads, then the dist probes, then the CASes are each
-// issued four at a time — the probes are random L2 reads, latency is the cost
-__device__ __forceinline__ void bfs_visit4(const u64* __restrict__ ro, const u64* __restrict__ keys,
-                                           const u8* __restrict__ st, u32* __restrict__ dist, u32* __restrict__ vis,
-                                           u32 depth, u64 t,
-                                           u64 S, u64 e, u32* __restrict__ next, u32* __restrict__ hnext,
-                                           u32* __restrict__ qn) {
-    const unsigned lane = threadIdx.x & 31u;
-    u32 v[4];
-    bool cand[4], won[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const u64 tj = t + j * S;
-        cand[j] = false;
-        v[j] = 0;
-        if (tj < e && st[tj] == kValid) {
-            const u64 k = keys[tj];
-            if (!is_guard(k)) {
-                v[j] = dst_of(k);
-                cand[j] = true;
-            }
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) cand[j] = cand[j] && !((vis[v[j] >> 5] >> (v[j] & 31u)) & 1u);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) won[j] = cand[j] && bfs_claim(vis, dist, v[j], depth);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const bool heavy = won[j] && (ro[v[j] + 1] - ro[v[j]]) > kHeavyRow;
-        const unsigned lm = __ballot_sync(FULL, won[j] && !heavy), hm = __ballot_sync(FULL, heavy);
-        if (lm) {
-            u32 base = 0;
-            if (lane == 0) base = atomicAdd(&qn[0], u32(__popc(lm)));
-            base = __shfl_sync(FULL, base, 0);
-            if (won[j] && !heavy) next[base + __popc(lm & lanemask_lt())] = v[j];
-        }
-        if (hm) {
-            u32 base = 0;
-            if (lane == 0) base = atomicAdd(&qn[1], u32(__popc(hm)));
-            base = __shfl_sync(FULL, base, 0);
-            if (heavy) hnext[base + __popc(hm & lanemask_lt())] = v[j];
-        }
-    }
+// one slot: (neighbour, is it a candidate) — the state and the key are loaded
+// together (a key line with no Valid slot is rare at PMA densities), then the
+// visited bit is probed
+__device__ __forceinline__ void bfs_slot_load(const u64* __restrict__ keys, const u8* __restrict__ st, u64 t, bool in,
+                                              u8& s, u64& k) {
+    s = in ? st[t] : u8(kEmpty);
+    k = in ? keys[t] : 0ull;
 }
 
+// Light rows: a warp takes 32 frontier vertices at once (their row bounds load
+// together, one per lane), then walks their concatenated slot intervals 128
+// slots per step: each lane's 4 slots (state + key, then the visited bit) are
+// independent loads instead of one row's chain after another.
 __global__ void __launch_bounds__(256) k_bfs_expand(const u32* __restrict__ frontier, const u32* nfp,
                                                     const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                     const u8* __restrict__ st, u32* __restrict__ dist,
                                                     u32* __restrict__ vis, u32 depth, u32* __restrict__ next,
-                                                    u32* __restrict__ hnext, u32* __restrict__ qn) {
-    __shared__ u32 s_q[8][256];
+                                                    u32* __restrict__ hnext, u32* __restrict__ gnext,
+                                                    u32* __restrict__ qn) {
+    __shared__ u32 s_q[8][kBfsQueue];
     const u32 nf = *nfp;
+    const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
     BfsWarpQueue wq{s_q[threadIdx.x >> 5], 0};
-    for (u64 f = warp; f < nf; f += nwarps) {
-        const u32 u = frontier[f];
-        const u64 b = ro[u], e = ro[u + 1];
-        for (u64 t0 = b; t0 < e; t0 += 128) wq.push128(keys, st, t0, e, ro, dist, vis, depth, next, hnext, qn);
+    // vertices per warp batch: up to 32, fewer while the frontier is too
+    // small to give every warp a full batch (parallelism first)
+    u32 V = u32((u64(nf) + nwarps - 1) / nwarps);
+    V = V < 1 ? 1 : (V > 32 ? 32 : V);
+    for (u64 f0 = warp * V; f0 < nf; f0 += nwarps * V) {
+        u64 b = 0;
+        u32 len = 0;
+        if (lane < V && f0 + lane < nf) {
+            const u32 u = frontier[f0 + lane];
+            b = ro[u];
+            len = u32(ro[u + 1] - b);  // <= kHeavyRow
+        }
+        u32 inc = len;  // inclusive prefix of the row lengths over the lanes
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(FULL, inc, d);
+            if (lane >= unsigned(d)) inc += y;
+        }
+        const u32 total = __shfl_sync(FULL, inc, 31);
+        for (u32 s0 = 0; s0 < total; s0 += 128) {
+            u8 sv[4];
+            u64 kv[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const u32 sl = s0 + 32 * j + lane;
+                const u32 sc = sl < total ? sl : total - 1;
+                u32 r = 0;  // the row holding slot sc: first lane whose prefix exceeds it
+#pragma unroll
+                for (u32 step = 16; step > 0; step >>= 1)
+                    if (__shfl_sync(FULL, inc, r + step - 1) <= sc) r += step;
+                const u64 br = __shfl_sync(FULL, b, r);
+                const u32 er = __shfl_sync(FULL, inc, r), lr = __shfl_sync(FULL, len, r);
+                bfs_slot_load(keys, st, br + (sc - (er - lr)), sl < total, sv[j], kv[j]);
+            }
+            u32 v[4];
+            bool c[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[j] = dst_of(kv[j]);
+                c[j] = sv[j] == kValid && !is_guard(kv[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) c[j] = c[j] && !((vis[v[j] >> 5] >> (v[j] & 31u)) & 1u);
+            wq.push4(v, c, ro, dist, vis, depth, next, hnext, gnext, qn);
+        }
     }
-    wq.drain(ro, dist, vis, depth, next, hnext, qn);
+    wq.drain(ro, dist, vis, depth, next, hnext, gnext, qn);
 }
 
+// one step of a row part: 4 slots per lane at stride S (32 for a warp, the
+// CTA size for a CTA): state + key loads together, then the visited probes;
+// the unvisited-looking neighbours go to the warp's queue (claimed 128 at a
+// time when it fills: the claims' round trips no longer gate every step)
+__device__ __forceinline__ void bfs_step4(const u64* __restrict__ keys, const u8* __restrict__ st,
+                                          u32* __restrict__ vis, u64 t, u64 S, u64 e, BfsWarpQueue& wq,
+                                          const u64* __restrict__ ro, u32* __restrict__ dist, u32 depth,
+                                          u32* __restrict__ next, u32* __restrict__ hnext, u32* __restrict__ gnext,
+                                          u32* __restrict__ qn) {
+    u8 sv[4];
+    u64 kv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bfs_slot_load(keys, st, t + j * S, t + j * S < e, sv[j], kv[j]);
+    u32 v[4];
+    bool c[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        v[j] = dst_of(kv[j]);
+        c[j] = sv[j] == kValid && !is_guard(kv[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[j] = c[j] && !((vis[v[j] >> 5] >> (v[j] & 31u)) & 1u);
+    wq.push4(v, c, ro, dist, vis, depth, next, hnext, gnext, qn);
+}
+
+// Huge rows (hubs, > kHugeRow slots): kHugeParts CTAs per row; then heavy
+// rows (kHeavyRow, kHugeRow]: kHeavyParts WARPS per row (a CTA per part left
+// most of its threads idle on the shorter heavy rows).  One launch; a
+// per-warp candidate queue as in k_bfs_expand (measured 0.63 -> 0.58 ms on
+// the C2 BFS).
 __global__ void __launch_bounds__(256) k_bfs_expand_heavy(const u32* __restrict__ hfrontier, const u32* nhp,
+                                                          const u32* __restrict__ gfrontier, const u32* ngp,
                                                           const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                           const u8* __restrict__ st, u32* __restrict__ dist,
                                                           u32* __restrict__ vis, u32 depth, u32* __restrict__ next,
-                                                          u32* __restrict__ hnext, u32* __restrict__ qn) {
-    // (a packed warp queue here measured slower: 1.03 vs 0.93 ms on the C2 hub BFS)
-    const u32 nh = *nhp;
-    for (u64 task = blockIdx.x; task < u64(nh) * kHeavyParts; task += gridDim.x) {
+                                                          u32* __restrict__ hnext, u32* __restrict__ gnext,
+                                                          u32* __restrict__ qn) {
+    __shared__ u32 s_q[8][kBfsQueue];
+    BfsWarpQueue wq{s_q[threadIdx.x >> 5], 0};
+    const u32 ng = *ngp, nh = *nhp;
+    for (u64 task = blockIdx.x; task < u64(ng) * kHugeParts; task += gridDim.x) {
+        const u32 u = gfrontier[task / kHugeParts];
+        const u64 p = task % kHugeParts;
+        const u64 b0 = ro[u], len = ro[u + 1] - b0;
+        const u64 b = b0 + (len * p) / kHugeParts, e = b0 + (len * (p + 1)) / kHugeParts;
+        for (u64 t0 = b; t0 < e; t0 += 4 * blockDim.x)  // (whole CTAs: each warp's ballots stay converged)
+            bfs_step4(keys, st, vis, t0 + threadIdx.x, blockDim.x, e, wq, ro, dist, depth, next, hnext, gnext, qn);
+    }
+    const unsigned lane = threadIdx.x & 31u;
+    const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+    const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
+    for (u64 task = warp; task < u64(nh) * kHeavyParts; task += nwarps) {
         const u32 u = hfrontier[task / kHeavyParts];
         const u64 p = task % kHeavyParts;
-        const u64 b0 = ro[u], e0 = ro[u + 1], len = e0 - b0;
+        const u64 b0 = ro[u], len = ro[u + 1] - b0;
         const u64 b = b0 + (len * p) / kHeavyParts, e = b0 + (len * (p + 1)) / kHeavyParts;
-        // whole warps iterate together (ballots inside)
-        u64 t0 = b;
-        for (; t0 + 3 * blockDim.x < e; t0 += 4 * blockDim.x)
-            bfs_visit4(ro, keys, st, dist, vis, depth, t0 + threadIdx.x, blockDim.x, e, next, hnext, qn);
-        for (; t0 < e; t0 += blockDim.x)
-            bfs_visit(ro, keys, st, dist, vis, depth, t0 + threadIdx.x, e, next, hnext, qn);
+        for (u64 t0 = b; t0 < e; t0 += 128)
+            bfs_step4(keys, st, vis, t0 + lane, 32, e, wq, ro, dist, depth, next, hnext, gnext, qn);
     }
+    wq.drain(ro, dist, vis, depth, next, hnext, gnext, qn);
 }
 
 // -------- CC (analytics.hpp:53-82): min-root union-find over every stored
@@ -605,7 +659,9 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     q1.reserve(nv + 1);
     h0.reserve(nv + 1);
     h1.reserve(nv + 1);
-    qn.reserve(2);
+    g0.reserve(nv + 1);
+    g1.reserve(nv + 1);
+    qn.reserve(3);
     k_fill_u32<<<grid_for(nv, 256, 148 * 16), 256, 0, s>>>(dist.ptr, nv, GPMA_UNREACHED);
     GPMA_LAUNCH_CHECK();
     const u32 zero = 0;
@@ -617,28 +673,29 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
     u64 rr[2] = {0, 0};
     GPMA_CUDA(cudaMemcpyAsync(rr, ro.ptr + root, 16, cudaMemcpyDeviceToHost, s));
     GPMA_CUDA(cudaStreamSynchronize(s));
-    const bool root_heavy = rr[1] - rr[0] > kHeavyRow;
-    GPMA_CUDA(cudaMemcpyAsync(root_heavy ? h0.ptr : q0.ptr, &root, 4, cudaMemcpyHostToDevice, s));
-    // per level L: (light, heavy) vertices discovered, qn[2L], qn[2L + 1];
+    const int root_class = rr[1] - rr[0] > kHugeRow ? 2 : (rr[1] - rr[0] > kHeavyRow ? 1 : 0);
+    GPMA_CUDA(cudaMemcpyAsync(root_class == 2 ? g0.ptr : (root_class == 1 ? h0.ptr : q0.ptr), &root, 4,
+                              cudaMemcpyHostToDevice, s));
+    // per level L: (light, heavy, huge) vertices discovered, qn[3L .. 3L + 2];
     // level 0 = the root.  Levels are launched kBfsWindow at a time with
     // their frontier sizes read on the device; the host syncs once per
     // window and stops at the first empty level (later launches of the
     // window found empty frontiers and did nothing).
     constexpr u32 kBfsWindow = 4;
     u64 cap_levels = 0;
-    const u32 first[2] = {root_heavy ? 0u : 1u, root_heavy ? 1u : 0u};
+    const u32 first[3] = {root_class == 0 ? 1u : 0u, root_class == 1 ? 1u : 0u, root_class == 2 ? 1u : 0u};
     u64 total = 1;
     u32 depth = 0;
-    u32 *cur = q0.ptr, *nxt = q1.ptr, *hcur = h0.ptr, *hnxt = h1.ptr;
+    u32 *cur = q0.ptr, *nxt = q1.ptr, *hcur = h0.ptr, *hnxt = h1.ptr, *gcur = g0.ptr, *gnxt = g1.ptr;
     u64 launches = 3;
     for (bool done = false; !done;) {
         if (depth + kBfsWindow + 1 > cap_levels) {  // grow the counter ring (keeps earlier levels)
             const u64 nc = (depth + kBfsWindow + 1) * 2 + 64;
             DevBuf<u32> q2;
-            q2.reserve(2 * nc);
-            GPMA_CUDA(cudaMemsetAsync(q2.ptr, 0, 2 * nc * 4, s));
-            if (cap_levels) GPMA_CUDA(cudaMemcpyAsync(q2.ptr, qn.ptr, 2 * cap_levels * 4, cudaMemcpyDeviceToDevice, s));
-            else GPMA_CUDA(cudaMemcpyAsync(q2.ptr, first, 8, cudaMemcpyHostToDevice, s));
+            q2.reserve(3 * nc);
+            GPMA_CUDA(cudaMemsetAsync(q2.ptr, 0, 3 * nc * 4, s));
+            if (cap_levels) GPMA_CUDA(cudaMemcpyAsync(q2.ptr, qn.ptr, 3 * cap_levels * 4, cudaMemcpyDeviceToDevice, s));
+            else GPMA_CUDA(cudaMemcpyAsync(q2.ptr, first, 12, cudaMemcpyHostToDevice, s));
             GPMA_CUDA(cudaStreamSynchronize(s));
             std::swap(qn.ptr, q2.ptr);
             std::swap(qn.cap, q2.cap);
@@ -647,23 +704,24 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
         const u32 d0 = depth;
         for (u32 w = 0; w < kBfsWindow; ++w) {
             ++depth;
-            const u32* cnt_in = qn.ptr + 2 * (depth - 1);
-            u32* cnt_out = qn.ptr + 2 * depth;
+            const u32* cnt_in = qn.ptr + 3 * (depth - 1);
+            u32* cnt_out = qn.ptr + 3 * depth;
             k_bfs_expand<<<kBfsLightGrid, 256, 0, s>>>(cur, cnt_in, ro.ptr, pma.d_keys, pma.d_st, dist.ptr, bvis.ptr,
-                                                 depth, nxt, hnxt, cnt_out);
+                                                 depth, nxt, hnxt, gnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
-            k_bfs_expand_heavy<<<kBfsHeavyGrid, 256, 0, s>>>(hcur, cnt_in + 1, ro.ptr, pma.d_keys, pma.d_st, dist.ptr,
-                                                       bvis.ptr, depth, nxt, hnxt, cnt_out);
+            k_bfs_expand_heavy<<<kBfsHeavyGrid, 256, 0, s>>>(hcur, cnt_in + 1, gcur, cnt_in + 2, ro.ptr, pma.d_keys,
+                                                       pma.d_st, dist.ptr, bvis.ptr, depth, nxt, hnxt, gnxt, cnt_out);
             GPMA_LAUNCH_CHECK();
             launches += 2;
             std::swap(cur, nxt);
             std::swap(hcur, hnxt);
+            std::swap(gcur, gnxt);
         }
-        h_lv_.resize(2 * kBfsWindow);
-        GPMA_CUDA(cudaMemcpyAsync(h_lv_.data(), qn.ptr + 2 * (d0 + 1), 2 * kBfsWindow * 4, cudaMemcpyDeviceToHost, s));
+        h_lv_.resize(3 * kBfsWindow);
+        GPMA_CUDA(cudaMemcpyAsync(h_lv_.data(), qn.ptr + 3 * (d0 + 1), 3 * kBfsWindow * 4, cudaMemcpyDeviceToHost, s));
         GPMA_CUDA(cudaStreamSynchronize(s));
         for (u32 w = 0; w < kBfsWindow; ++w) {
-            const u64 c = u64(h_lv_[2 * w]) + h_lv_[2 * w + 1];
+            const u64 c = u64(h_lv_[3 * w]) + h_lv_[3 * w + 1] + h_lv_[3 * w + 2];
             if (c == 0) {
                 done = true;
                 break;

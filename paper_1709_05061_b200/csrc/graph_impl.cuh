@@ -62,7 +62,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     Ctr* d_ctr_ = nullptr;
     DevBuf<u64> bk, bv;
     DevBuf<u8> bo;
-    DevBuf<u32> dist, bvis, q0, q1, h0, h1, qn, outdeg;
+    DevBuf<u32> dist, bvis, q0, q1, h0, h1, g0, g1, qn, outdeg;
     DevBuf<double> px, py, pshare, psc, pl1;
     DevBuf<u32> pdone;
     DevBuf<u32> rt_counts, hot_table, hot_ids, hot_hist;

@@ -15,5 +15,5 @@ for f in paper_1709_05061_b200/csrc/*.cu; do
   objs="$objs $o"
 done
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $objs -o paper_1709_05061_b200/build/$name.so
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static $objs -ldl -o paper_1709_05061_b200/build/$name.so
 echo paper_1709_05061_b200/build/$name.so
