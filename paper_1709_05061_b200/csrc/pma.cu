@@ -1042,6 +1042,9 @@ __device__ __forceinline__ void load_group_tile(const CommitArgs& a, ull g0, ull
 // Groups with more than kBigSlice updates (RMAT hub rows) are handed to the
 // CTA kernel through `biglist`.
 constexpr int kLeafWarps = 4;
+#ifndef GPMA_LEAF_CTAS
+#define GPMA_LEAF_CTAS 6  // resident CTAs per SM the register budget is sized for
+#endif
 constexpr u32 kBigSlice = 32;   // leaf kernel: larger slices go to the CTA kernel
 constexpr u32 kLaneBig = 64;    // lane kernels: larger slices go to the CTA kernel
 constexpr u32 kStage = 64;      // updates of a 32-group tile staged in smem (overflow read from HBM)
@@ -1091,18 +1094,22 @@ __device__ __forceinline__ void touched_append(const CommitArgs& a, u64 b, u64 e
 // tile's states, keys and update slice in one round trip; the decision then
 // issues phase 2 (values of the merge groups only), which overlaps the
 // ranking of the slices.
-constexpr int kRowB = 18;  // u64 per staged row: 16 slots + 16 B pad (16-B aligned, conflict-free 16-B reads)
+// Staged rows are 16 slots (128 B) with their 16-byte chunks XOR-swizzled by
+// the row (chunk c of row r lives at chunk c ^ (r & 7)): the same bank spread
+// as a padded row, without the pad — 4 KB less shared memory per CTA, which
+// with u32 segment ids and <= 80 registers fits 6 CTAs (24 warps) per SM.
+__device__ __forceinline__ u32 swz(u32 row, u32 i) { return row * 16u + ((((i >> 1) ^ (row & 7u)) << 1) | (i & 1u)); }
 
-__global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a) {
-    __shared__ __align__(16) u64 s_k[kLeafWarps][32 * kRowB];
-    __shared__ __align__(16) u64 s_v[kLeafWarps][32 * kRowB];
+__global__ void __launch_bounds__(kLeafWarps * 32, GPMA_LEAF_CTAS) k_commit_leaf(CommitArgs a) {
+    __shared__ __align__(16) u64 s_k[kLeafWarps][32 * 16];
+    __shared__ __align__(16) u64 s_v[kLeafWarps][32 * 16];
     __shared__ u64 s_uk[kLeafWarps][kStage];
     __shared__ u64 s_uv[kLeafWarps][kStage];
     __shared__ u32 s_uo[kLeafWarps][kStage / 4 + 2];
-    __shared__ u64 s_b[kLeafWarps][32];  // slot base of each group of the tile
+    __shared__ u32 s_b[kLeafWarps][32];  // segment (= leaf) of each group of the tile
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    u64* rk = &s_k[w][lane * kRowB];
-    u64* rv = &s_v[w][lane * kRowB];
+    auto RK = [&](u32 i) -> u64& { return s_k[w][swz(lane, i)]; };  // slot i of this lane's leaf
+    auto RV = [&](u32 i) -> u64& { return s_v[w][swz(lane, i)]; };
     const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
     pdl_enter();
     const ull ngroups = a.ctr->ngroups;
@@ -1132,7 +1139,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
         const unsigned tile_n = (ngroups - g0) < 32 ? unsigned(ngroups - g0) : 32u;
         const u32 tlo = __shfl_sync(FULL, lo, 0);
         const u32 thi = __shfl_sync(FULL, hi, tile_n - 1);
-        s_b[w][lane] = b;
+        s_b[w][lane] = n_seg;
         __syncwarp();
         // ---- phase 1: states, keys, update slice of the tile
         uint4 sv = make_uint4(0, 0, 0, 0);
@@ -1150,7 +1157,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
 #pragma unroll
         for (int it = 0; it < 8; ++it) {  // 8 lanes per 128-byte key line
             const unsigned row = it * 4 + (lane >> 3), part = lane & 7u;
-            if (row < tile_n) cp_async16(&s_k[w][row * kRowB + 2 * part], a.keys + s_b[w][row] + 2 * part);
+            if (row < tile_n) cp_async16(&s_k[w][swz(row, 2 * part)], a.keys + u64(s_b[w][row]) * 16 + 2 * part);
         }
         // descriptors of the next tile while the copies fly
         gnext = grab();
@@ -1232,7 +1239,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             for (int it = 0; it < 8; ++it) {
                 const unsigned row = it * 4 + (lane >> 3), part = lane & 7u;
                 if ((mergemask >> row) & 1u)
-                    cp_async16(&s_v[w][row * kRowB + 2 * part], a.vals + s_b[w][row] + 2 * part);
+                    cp_async16(&s_v[w][swz(row, 2 * part)], a.vals + u64(s_b[w][row]) * 16 + 2 * part);
             }
         }
         unsigned newvalid = valid, tombs = 0;
@@ -1245,7 +1252,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             u64 K[16];
 #pragma unroll
             for (int i = 0; i < 16; i += 2) {  // 16-B row reads: conflict-free per quarter warp
-                const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(rk + i);
+                const ulonglong2 kk = *reinterpret_cast<const ulonglong2*>(&RK(i));
                 K[i] = kk.x;
                 K[i + 1] = kk.y;
             }
@@ -1262,7 +1269,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
                 for (int i = 0; i < 16; ++i) lt |= (K[i] < u ? 1u : 0u) << i;
                 const u32 cm = nonempty & ~lt;
                 const int c = __ffs(cm) - 1;  // the only slot that can hold u
-                const bool hit = cm != 0 && ((valid >> c) & 1u) && rk[c] == u;
+                const bool hit = cm != 0 && ((valid >> c) & 1u) && RK(c) == u;
                 if (op == kOpDelete) {
                     if (hit) del_hit |= 1u << c;
                     else ++missed;
@@ -1301,21 +1308,21 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             for (u32 m = right; m; m &= ~(1u << (31 - __clz(m)))) {
                 const int i = 31 - __clz(m);
                 const u32 x = u32(dst >> (4 * i)) & 0xfu;
-                rk[x] = rk[i];
-                rv[x] = rv[i];
+                RK(x) = RK(i);
+                RV(x) = RV(i);
             }
             for (u32 m = keepf & ~right; m; m &= m - 1) {
                 const int i = __ffs(m) - 1;
                 const u32 x = u32(dst >> (4 * i)) & 0xfu;
                 if (x != u32(i)) {
-                    rk[x] = rk[i];
-                    rv[x] = rv[i];
+                    RK(x) = RK(i);
+                    RV(x) = RV(i);
                 }
             }
             for (u32 m = nonempty & ~out; m; m &= m - 1) {
                 const int x = __ffs(m) - 1;
-                rk[x] = 0;
-                rv[x] = 0;
+                RK(x) = 0;
+                RV(x) = 0;
             }
             // inserts, in key order
             u32 nth = 0;
@@ -1326,8 +1333,8 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
                 if (op == kOpDelete) continue;
                 const u32 j = u32(insj >> (4 * nth)) & 0xfu;
                 const u32 x = (j * 16u * mk) >> 16;
-                rk[x] = u;
-                rv[x] = UVAL(q);
+                RK(x) = u;
+                RV(x) = UVAL(q);
                 out |= 1u << x;
                 ++nth;
             }
@@ -1336,7 +1343,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             for (u32 m = keepf & guards; m; m &= m - 1) {
                 const int i = __ffs(m) - 1;
                 const u32 x = u32(dst >> (4 * i)) & 0xfu;
-                a.ro[src_of(rk[x]) + 1] = b + x + 1;
+                a.ro[src_of(RK(x)) + 1] = b + x + 1;
             }
         }
         __syncwarp();
@@ -1358,16 +1365,16 @@ __global__ void __launch_bounds__(kLeafWarps * 32, 5) k_commit_leaf(CommitArgs a
             for (int it = 0; it < 8; ++it) {
                 const unsigned grp = it * 4 + (lane >> 3), part = lane & 7u;
                 if ((mergemask >> grp) & 1u) {
-                    const u64 gb = s_b[w][grp];
+                    const u64 gb = u64(s_b[w][grp]) * 16;
                     *reinterpret_cast<ulonglong2*>(a.keys + gb + 2 * part) =
-                        *reinterpret_cast<const ulonglong2*>(&s_k[w][grp * kRowB + 2 * part]);
+                        *reinterpret_cast<const ulonglong2*>(&s_k[w][swz(grp, 2 * part)]);
                     *reinterpret_cast<ulonglong2*>(a.vals + gb + 2 * part) =
-                        *reinterpret_cast<const ulonglong2*>(&s_v[w][grp * kRowB + 2 * part]);
+                        *reinterpret_cast<const ulonglong2*>(&s_v[w][swz(grp, 2 * part)]);
                 }
             }
         }
         if (mode == 2) {
-            if (k > 0) a.hdr[b / 16] = rk[0];  // entry 0 always lands on slot 0
+            if (k > 0) a.hdr[b / 16] = RK(0);  // entry 0 always lands on slot 0
             else {
                 const ull slot = atomicAdd(&a.ctr->nrefresh, 1ull);
                 a.rlist[2 * slot] = b;
