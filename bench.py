@@ -458,11 +458,19 @@ def run_ours(args):
     # level >= 1 commits (a few hundred groups, latency-bound) are reported
     # beside it in all_levels.
     l0_ms = level_ms[0] / K
+    kernel_desc = ("leaf-level commit: k_commit_leaf (decide + merge + even re-dispatch + fused "
+                   "header/row-offset refresh) + k_commit_cta for its hub groups")
+    if l0_ms == 0 and level_bytes[0] > 0:
+        # small batches (C1) run as one captured graph with no per-level
+        # events: the level-0 bytes over the graph's whole device span (its
+        # %globaltimer stamps) — a lower bound on the commit kernel's rate
+        l0_ms = stage["sort_ms"] / K
+        kernel_desc = ("small-batch graph (one-CTA front end, warp leaf search, round 0, refresh): level-0 commit "
+                       "bytes over the whole graph device span")
     achieved = (level_bytes[0] / K) / (l0_ms / 1e3) / 1e9 if l0_ms > 0 else None
     all_achieved = (commit_bytes / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
     traffic = ncu_traffic(args.config)
-    roofline = {"bound": "hbm", "kernel": "leaf-level commit: k_commit_leaf (decide + merge + even re-dispatch + fused "
-                                          "header/row-offset refresh) + k_commit_cta for its hub groups",
+    roofline = {"bound": "hbm", "kernel": kernel_desc,
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_bytes_per_step": level_bytes[0] // K, "kernel_ms_per_step": l0_ms,
@@ -496,6 +504,8 @@ def run_ours(args):
         if not args.no_analytics:
             out["analytics"] = analytics(pg, g, ext, nvx)
         out["sweep"] = sweep(pg, stream, dev, [int(x) for x in args.sweep.split(",") if x], nvx)
+        if args.config == "C2":
+            c_abi_sweep(out["sweep"], dev)
         if world == 1 and not args.no_cpu_baseline and args.config in ("C1", "C2"):
             os.sched_setaffinity(0, all_cpus)  # the reference baseline gets every host thread
             out["cpu_baseline"] = cpu_baseline(stream, slides, win, W, nvx)
@@ -869,6 +879,38 @@ def sweep(pg, stream, dev, batches, nv):
         res[str(B)]["rebuild_csr_us_per_batch"] = ms * 1e3 / 3
         del r, win
     return res
+
+
+def c_abi_sweep(res, dev):
+    """The same C2 slides through the drop-in C ABI with no Python in the
+    loop (tools/cpp/small_batch_latency: gpma_apply_batch_device on device
+    inputs, host steady_clock around each synchronous call, median of 200
+    slides after 8 untimed): the small-batch latency a C++ caller sees.  The
+    Python `us_per_batch` beside it adds ctypes and the UpdateStats object."""
+    import subprocess
+    tool = os.path.join(ROOT, "tools", "cpp", "small_batch_latency")
+    sizes = [b for b in map(int, res) if b <= 10000]
+    if not sizes or not os.path.exists(tool):
+        return
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(dev)))
+    try:
+        out = subprocess.run([tool, *map(str, sizes)], capture_output=True, text=True, timeout=600, env=env).stdout
+    except (OSError, subprocess.TimeoutExpired):
+        return
+    for line in out.splitlines():
+        # B=100: C ABI wall per batch median 38.2 us, p10 37.7, p90 38.9 (device 27.6 us, 196 updates)
+        if not line.startswith("B=") or "median" not in line:
+            continue
+        b = line[2:line.index(":")]
+        try:
+            med = float(line.split("median ")[1].split(" us")[0])
+            p10 = float(line.split("p10 ")[1].split(",")[0])
+            p90 = float(line.split("p90 ")[1].split(" ")[0])
+            devus = float(line.split("(device ")[1].split(" us")[0])
+        except (IndexError, ValueError):
+            continue
+        if b in res:
+            res[b]["c_abi_us_per_batch"] = {"median": med, "p10": p10, "p90": p90, "device_us": devus}
 
 
 def cpu_baseline(stream, slides, win, W, nv):
