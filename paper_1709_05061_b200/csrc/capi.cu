@@ -5,6 +5,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "graph_impl.cuh"
@@ -58,6 +59,17 @@ gpma::EngineCfg to_cfg(const pma_engine_config* c) {
 
 std::string* err_of(pma_handle* h) { return h && h->impl ? &h->impl->err : nullptr; }
 std::string* err_of(gpma_graph* g) { return g && g->impl ? &g->impl->err : nullptr; }
+
+// Entry points on an existing handle: a null (or destroyed) handle is an
+// invalid argument, reported through pma_last_error(NULL) / gpma_last_error(NULL)
+template <class H, class F>
+int guarded_on(H* h, F&& f) {
+    if (!h || !h->impl) {
+        g_create_err = "null handle";
+        return PMA_EINVAL;
+    }
+    return guarded(err_of(h), std::forward<F>(f));
+}
 }  // namespace
 
 namespace gpma {
@@ -95,7 +107,7 @@ const char* pma_last_error(const pma_handle* h) {
 }
 
 int pma_from_sorted(pma_handle* h, const uint64_t* keys, const uint64_t* values, size_t n, double fill_target) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         auto* p = h->impl;
         GPMA_CUDA(cudaSetDevice(p->device()));
         const uint64_t* dk = p->stage(p->stage_k, keys, n);
@@ -109,14 +121,14 @@ int pma_from_sorted(pma_handle* h, const uint64_t* keys, const uint64_t* values,
 
 int pma_load_slots(pma_handle* h, size_t capacity, const uint64_t* keys, const uint64_t* values,
                    const uint8_t* states) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->load_slots(capacity, keys, values, states);
     });
 }
 
 int pma_download(pma_handle* h, uint64_t* keys, uint64_t* values, uint8_t* states) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->download(keys, values, states);
     });
@@ -143,7 +155,7 @@ int pma_reset_slot_writes(pma_handle* h) {
 
 int pma_bounds(const pma_handle* h, int level, uint64_t* mn, uint64_t* mx, double* rho, double* tau) {
     auto* hh = const_cast<pma_handle*>(h);
-    return guarded(err_of(hh), [&] {
+    return guarded_on(hh, [&] {
         const auto* p = h->impl;
         if (level < 0 || level > p->height())
             throw ApiError(PMA_ERANGE, "level " + std::to_string(level) + " outside [0, " +
@@ -160,7 +172,7 @@ int pma_bounds(const pma_handle* h, int level, uint64_t* mn, uint64_t* mx, doubl
 
 int pma_batch_update(pma_handle* h, const uint64_t* keys, const uint64_t* values, const uint8_t* ops, size_t n,
                      const pma_engine_config* cfg, pma_stats* out) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         auto* p = h->impl;
         GPMA_CUDA(cudaSetDevice(p->device()));
         const auto t0 = std::chrono::steady_clock::now();
@@ -178,14 +190,14 @@ int pma_batch_update(pma_handle* h, const uint64_t* keys, const uint64_t* values
 
 int pma_batch_update_device(pma_handle* h, const uint64_t* d_keys, const uint64_t* d_values, const uint8_t* d_ops,
                             size_t n, const pma_engine_config* cfg, pma_stats* out) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->batch_update_device(d_keys, d_values, d_ops, n, to_cfg(cfg), out);
     });
 }
 
 int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         size_t c = 0;
         h->impl->touched_ranges(pairs, cap, &c);
         if (count) *count = c;
@@ -195,7 +207,7 @@ int pma_touched_ranges(pma_handle* h, uint64_t* pairs, size_t cap, size_t* count
 int pma_try_insert_plus(pma_handle* h, int level, size_t seg, const uint64_t* keys, const uint64_t* values,
                         const uint8_t* ops, size_t n, const pma_engine_config* cfg, int* outcome,
                         uint64_t* deletes_missed, uint64_t* tombstones_added) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         if (n && (!keys || !ops)) throw ApiError(PMA_EINVAL, "pma_try_insert_plus: keys / ops are NULL");
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         std::vector<uint64_t> zeros;
@@ -210,28 +222,28 @@ int pma_try_insert_plus(pma_handle* h, int level, size_t seg, const uint64_t* ke
 }
 
 int gpma_reserve_batch(gpma_graph* g, size_t max_updates) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->reserve_batch(max_updates);
     });
 }
 
 int pma_set_grid_segment(pma_handle* h, uint64_t min_slots) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         if (min_slots < 64) throw ApiError(PMA_EINVAL, "pma_set_grid_segment: at least 64 slots");
         h->impl->grid_seg_ = min_slots;
     });
 }
 
 int pma_reserve_batch(pma_handle* h, size_t max_updates) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->reserve_batch(max_updates);
     });
 }
 
 int pma_slot_hash(pma_handle* h, int level, uint64_t* hashes) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         if (!hashes) throw ApiError(PMA_EINVAL, "pma_slot_hash: hashes is NULL");
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->slot_hash(level, hashes);
@@ -239,35 +251,35 @@ int pma_slot_hash(pma_handle* h, int level, uint64_t* hashes) {
 }
 
 int pma_binary_search_leaf(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* leaves) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->binary_search_leaf(keys, n, leaves);
     });
 }
 
 int pma_search(pma_handle* h, const uint64_t* keys, size_t n, uint64_t* values, uint8_t* found) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->search(keys, n, values, found);
     });
 }
 
 int pma_count_valid_in(pma_handle* h, size_t begin, size_t end, uint64_t* count) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         *count = h->impl->count_valid_in(begin, end);
     });
 }
 
 int pma_insert(pma_handle* h, uint64_t key, uint64_t value) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->insert(key, value);
     });
 }
 
 int pma_erase(pma_handle* h, uint64_t key, int* erased) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         const bool r = h->impl->erase(key);
         if (erased) *erased = r ? 1 : 0;
@@ -275,7 +287,7 @@ int pma_erase(pma_handle* h, uint64_t key, int* erased) {
 }
 
 int pma_mark_tombstone(pma_handle* h, uint64_t key, int* marked) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         const bool r = h->impl->mark_tombstone(key);
         if (marked) *marked = r ? 1 : 0;
@@ -284,7 +296,7 @@ int pma_mark_tombstone(pma_handle* h, uint64_t key, int* marked) {
 
 int pma_redispatch(pma_handle* h, int level, size_t seg_index, const uint64_t* keys, const uint64_t* values,
                    size_t n) {
-    return guarded(err_of(h), [&] {
+    return guarded_on(h, [&] {
         GPMA_CUDA(cudaSetDevice(h->impl->device()));
         h->impl->redispatch(level, seg_index, keys, values, n);
     });
@@ -360,7 +372,7 @@ uint64_t gpma_num_edges(const gpma_graph* g) { return g ? g->impl->num_edges() :
 
 int gpma_apply_batch(gpma_graph* g, const uint32_t* ins_src, const uint32_t* ins_dst, const double* ins_w,
                      size_t n_ins, const uint32_t* del_src, const uint32_t* del_dst, size_t n_del, pma_stats* out) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         auto& p = g->impl->pma;
         GPMA_CUDA(cudaSetDevice(p.device()));
         const auto t0 = std::chrono::steady_clock::now();
@@ -383,36 +395,36 @@ int gpma_apply_batch(gpma_graph* g, const uint32_t* ins_src, const uint32_t* ins
 int gpma_apply_batch_device(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
                             const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst,
                             size_t n_del, pma_stats* out) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->apply_batch_device(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, out);
     });
 }
 
 int gpma_row_offsets(gpma_graph* g, uint64_t* out) {
-    return guarded(err_of(g), [&] { g->impl->row_offsets(out); });
+    return guarded_on(g, [&] { g->impl->row_offsets(out); });
 }
 
 int gpma_rebuild_row_offsets(gpma_graph* g) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         g->impl->pma.rebuild_row_offsets_full();
         GPMA_CUDA(cudaStreamSynchronize(g->impl->pma.stream()));
     });
 }
 
 int gpma_csr_snapshot(gpma_graph* g, uint64_t* row_offsets, uint32_t* col, double* vals) {
-    return guarded(err_of(g), [&] { g->impl->csr_snapshot(row_offsets, col, vals); });
+    return guarded_on(g, [&] { g->impl->csr_snapshot(row_offsets, col, vals); });
 }
 
 int gpma_bfs(gpma_graph* g, uint32_t root, uint32_t* dist, uint64_t* reached) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->bfs(root, dist, reached);
     });
 }
 
 int gpma_cc(gpma_graph* g, uint32_t* labels) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->cc(labels);
     });
@@ -420,7 +432,7 @@ int gpma_cc(gpma_graph* g, uint32_t* labels) {
 
 int gpma_pagerank(gpma_graph* g, double damping, double epsilon, size_t max_iters, const double* warm, double* ranks,
                   uint64_t* iterations, int* converged) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         uint64_t it = 0;
         int conv = 0;
@@ -431,7 +443,7 @@ int gpma_pagerank(gpma_graph* g, double damping, double epsilon, size_t max_iter
 }
 
 int gpma_spmv(gpma_graph* g, const double* x, double* y) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->spmv(x, y);
     });
@@ -470,7 +482,7 @@ int gpma_shard_range(const gpma_graph* g, uint64_t* lo, uint64_t* hi) {
 int gpma_route_batch(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, const double* d_ins_w,
                      size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
                      const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w, uint64_t* counts) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->route_partition(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, d_bounds, world,
                                  d_out_keys, d_out_w, counts);
@@ -481,7 +493,7 @@ int gpma_route_batch_async(gpma_graph* g, const uint32_t* d_ins_src, const uint3
                            size_t n_ins, const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del,
                            const uint32_t* d_bounds, int world, uint64_t* d_out_keys, double* d_out_w,
                            uint64_t* d_counts) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->route_partition(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, d_bounds, world,
                                  d_out_keys, d_out_w, nullptr, d_counts);
@@ -491,7 +503,7 @@ int gpma_route_batch_async(gpma_graph* g, const uint32_t* d_ins_src, const uint3
 int gpma_route_count(gpma_graph* g, const uint32_t* d_ins_src, const uint32_t* d_ins_dst, size_t n_ins,
                      const uint32_t* d_del_src, const uint32_t* d_del_dst, size_t n_del, const uint32_t* d_bounds,
                      int world, uint64_t* d_counts) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->route_partition(d_ins_src, d_ins_dst, nullptr, n_ins, d_del_src, d_del_dst, n_del, d_bounds, world,
                                  nullptr, nullptr, nullptr, d_counts);
@@ -502,7 +514,7 @@ int gpma_route_scatter_peer(gpma_graph* g, const uint32_t* d_ins_src, const uint
                             const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
                             const uint32_t* d_del_dst, size_t n_del, const uint32_t* d_bounds, int world,
                             uint64_t* const* d_dst_keys, double* const* d_dst_w, const uint64_t* d_dst_offsets) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->route_scatter_peer(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, d_bounds,
                                     world, d_dst_keys, d_dst_w, d_dst_offsets);
@@ -541,14 +553,14 @@ int gpma_set_stream(gpma_graph* g, void* stream, int own) {
 
 int gpma_apply_batch_routed_device(gpma_graph* g, const uint64_t* d_keys, const double* d_w, size_t n,
                                    pma_stats* stats) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->apply_batch_mixed_device(d_keys, d_w, n, stats);
     });
 }
 
 int gpma_shard_bfs_mark(gpma_graph* g, const uint32_t* d_frontier, uint32_t nf, uint8_t* d_flags) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->shard_bfs_mark(d_frontier, nf, d_flags);
     });
@@ -556,35 +568,35 @@ int gpma_shard_bfs_mark(gpma_graph* g, const uint32_t* d_frontier, uint32_t nf, 
 
 int gpma_shard_bfs_update(gpma_graph* g, const uint8_t* d_flags, uint32_t* d_dist_local, uint32_t depth,
                           uint32_t* d_next, uint32_t* nf) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->shard_bfs_update(d_flags, d_dist_local, depth, d_next, nf);
     });
 }
 
 int gpma_shard_cc_hook(gpma_graph* g, uint32_t* d_labels) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->shard_cc_hook(d_labels);
     });
 }
 
 int gpma_cc_jump(gpma_graph* g, uint32_t* d_labels, size_t n, const uint32_t* d_prev, int* changed) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->cc_jump(d_labels, n, d_prev, changed);
     });
 }
 
 int gpma_shard_outdeg(gpma_graph* g, uint32_t* d_outdeg) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->shard_outdeg(d_outdeg);
     });
 }
 
 int gpma_shard_pr_push(gpma_graph* g, const double* d_x, const uint32_t* d_outdeg, double damping, double* d_y) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->shard_pr_push(d_x, d_outdeg, damping, d_y);
     });
@@ -592,14 +604,14 @@ int gpma_shard_pr_push(gpma_graph* g, const double* d_x, const uint32_t* d_outde
 
 int gpma_pr_finish(gpma_graph* g, const double* d_x, double* d_y, size_t n, const uint32_t* d_outdeg, double damping,
                    double* l1) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->pr_finish(d_x, d_y, n, d_outdeg, damping, l1);
     });
 }
 
 int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local) {
-    return guarded(err_of(g), [&] {
+    return guarded_on(g, [&] {
         GPMA_CUDA(cudaSetDevice(g->impl->pma.device()));
         g->impl->shard_spmv(d_x, d_y_local);
     });

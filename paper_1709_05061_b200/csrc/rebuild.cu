@@ -368,6 +368,10 @@ const char* gpma_rebuild_last_error(const gpma_rebuild* r) {
 int gpma_rebuild_apply_batch_device(gpma_rebuild* r, const uint32_t* d_ins_src, const uint32_t* d_ins_dst,
                                     const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
                                     const uint32_t* d_del_dst, size_t n_del, pma_stats* stats) {
+    if (!r || !r->impl) {
+        g_rb_err = "null handle";
+        return PMA_EINVAL;
+    }
     return rb_guard(&r->impl->err, [&] {
         GPMA_CUDA(cudaSetDevice(r->impl->dev));
         r->impl->apply(d_ins_src, d_ins_dst, d_ins_w, n_ins, d_del_src, d_del_dst, n_del, stats);
@@ -377,6 +381,10 @@ int gpma_rebuild_apply_batch_device(gpma_rebuild* r, const uint32_t* d_ins_src, 
 int gpma_rebuild_apply_batch(gpma_rebuild* r, const uint32_t* ins_src, const uint32_t* ins_dst, const double* ins_w,
                              size_t n_ins, const uint32_t* del_src, const uint32_t* del_dst, size_t n_del,
                              pma_stats* stats) {
+    if (!r || !r->impl) {
+        g_rb_err = "null handle";
+        return PMA_EINVAL;
+    }
     return rb_guard(&r->impl->err, [&] {
         auto& g = *r->impl;
         GPMA_CUDA(cudaSetDevice(g.dev));
@@ -390,6 +398,10 @@ int gpma_rebuild_apply_batch(gpma_rebuild* r, const uint32_t* ins_src, const uin
 }
 
 int gpma_rebuild_csr(gpma_rebuild* r, uint64_t* row_offsets, uint32_t* col, double* vals) {
+    if (!r || !r->impl) {
+        g_rb_err = "null handle";
+        return PMA_EINVAL;
+    }
     return rb_guard(&r->impl->err, [&] {
         GPMA_CUDA(cudaSetDevice(r->impl->dev));
         r->impl->csr(row_offsets, col, vals);

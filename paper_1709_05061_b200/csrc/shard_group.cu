@@ -307,6 +307,10 @@ int gpma_shard_group_apply_batch(gpma_shard_group* sg, const uint32_t* d_ins_src
                                  const double* d_ins_w, size_t n_ins, const uint32_t* d_del_src,
                                  const uint32_t* d_del_dst, size_t n_del, pma_stats* stats, uint64_t* routed,
                                  uint64_t* sent) {
+    if (!sg) {
+        g_group_err = "null handle";
+        return PMA_EINVAL;
+    }
     return group_guard(sg, [&] {
         GPMA_CUDA(cudaSetDevice(sg->device));
         NcclApi& nc = nccl();
@@ -379,6 +383,10 @@ int gpma_shard_group_apply_batch(gpma_shard_group* sg, const uint32_t* d_ins_src
 }
 
 int gpma_shard_group_bfs(gpma_shard_group* sg, uint32_t root, uint32_t* dist_out, uint64_t* reached) {
+    if (!sg) {
+        g_group_err = "null handle";
+        return PMA_EINVAL;
+    }
     return group_guard(sg, [&] {
         if (root >= sg->nv) throw ApiError(PMA_EINVAL, "bfs: root out of range");
         GPMA_CUDA(cudaSetDevice(sg->device));
@@ -438,6 +446,10 @@ int gpma_shard_group_bfs(gpma_shard_group* sg, uint32_t root, uint32_t* dist_out
 }
 
 int gpma_shard_group_cc(gpma_shard_group* sg, uint32_t* labels_out) {
+    if (!sg) {
+        g_group_err = "null handle";
+        return PMA_EINVAL;
+    }
     return group_guard(sg, [&] {
         GPMA_CUDA(cudaSetDevice(sg->device));
         NcclApi& nc = nccl();
@@ -464,6 +476,10 @@ int gpma_shard_group_cc(gpma_shard_group* sg, uint32_t* labels_out) {
 
 int gpma_shard_group_pagerank(gpma_shard_group* sg, double damping, double eps, size_t max_iters, const double* warm,
                               double* ranks, uint64_t* iterations, int* converged) {
+    if (!sg) {
+        g_group_err = "null handle";
+        return PMA_EINVAL;
+    }
     return group_guard(sg, [&] {
         GPMA_CUDA(cudaSetDevice(sg->device));
         NcclApi& nc = nccl();
@@ -504,6 +520,10 @@ int gpma_shard_group_pagerank(gpma_shard_group* sg, double damping, double eps, 
 }
 
 int gpma_shard_group_spmv(gpma_shard_group* sg, const double* x, double* y) {
+    if (!sg) {
+        g_group_err = "null handle";
+        return PMA_EINVAL;
+    }
     return group_guard(sg, [&] {
         GPMA_CUDA(cudaSetDevice(sg->device));
         NcclApi& nc = nccl();

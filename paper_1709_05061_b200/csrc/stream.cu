@@ -367,6 +367,10 @@ int gpma_stream_erdos_renyi(size_t nv, double density, uint64_t seed, gpma_strea
 
 // assign_random_timestamps (streaming.hpp:58-67): Fisher-Yates with draw_below
 int gpma_stream_shuffle(gpma_stream* s, uint64_t seed) {
+    if (!s) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         std::mt19937_64 rng(seed);
         auto& a = s->s.src;
@@ -393,6 +397,10 @@ uint64_t gpma_stream_size(const gpma_stream* s) { return s ? s->s.src.size() : 0
 uint64_t gpma_stream_num_vertices(const gpma_stream* s) { return s ? s->s.nv : 0; }
 
 int gpma_stream_edges(const gpma_stream* s, uint32_t* src, uint32_t* dst) {
+    if (!s) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         if (src) std::memcpy(src, s->s.src.data(), s->s.src.size() * 4);
         if (dst) std::memcpy(dst, s->s.dst.data(), s->s.dst.size() * 4);
@@ -413,6 +421,10 @@ int gpma_draw_below_sequence(uint64_t seed, uint64_t bound, size_t n, uint64_t* 
 }
 
 int gpma_window_create(const gpma_stream* s, int device, gpma_window** out) {
+    if (!s) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         const uint64_t n = s->s.src.size();
         if (n < 2) throw ApiError(PMA_EINVAL, "SlidingWindow: stream needs at least two edges");
@@ -492,6 +504,10 @@ int gpma_window_info(const gpma_window* w, gpma_window_info_t* out) {
 // Reserve room for `max_deletions` appended deletions (device pointers in
 // gpma_window_info stay valid until the next reserve).
 int gpma_window_reserve(gpma_window* w, size_t max_deletions) {
+    if (!w) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         auto& W = w->w;
         if (max_deletions <= W.del_src.cap) return;
@@ -515,6 +531,10 @@ int gpma_window_reserve(gpma_window* w, size_t max_deletions) {
 // stream positions [ins_offset, ins_offset + n_ins); deletions are appended
 // at [del_offset, del_offset + n_del) of the window's deletion arrays.
 int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out) {
+    if (!w) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         auto& W = w->w;
         GPMA_CUDA(cudaSetDevice(W.device));
@@ -569,6 +589,10 @@ int gpma_window_slide(gpma_window* w, size_t batch, gpma_slide_t* out) {
 
 // SlideBatch::expiries of the last slide as stream positions, window order.
 int gpma_window_last_expiries(gpma_window* w, uint32_t* positions, size_t cap, size_t* n) {
+    if (!w) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         auto& W = w->w;
         GPMA_CUDA(cudaSetDevice(W.device));
@@ -600,6 +624,10 @@ int gpma_window_last_expiries(gpma_window* w, uint32_t* positions, size_t cap, s
 // distinct edges, ascending key order (the reference's order is a hash map's,
 // i.e. unspecified).  Two-call protocol: cap = 0 returns the count.
 int gpma_window_distinct_edges(gpma_window* w, uint32_t* src, uint32_t* dst, size_t cap, size_t* n) {
+    if (!w) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         auto& W = w->w;
         GPMA_CUDA(cudaSetDevice(W.device));
@@ -657,6 +685,10 @@ int gpma_window_distinct_edges(gpma_window* w, uint32_t* src, uint32_t* dst, siz
 // generator can drive gpma_window_slide_explicit_random and advance exactly
 // as the reference's would (streaming.hpp:129 takes it by reference).
 int gpma_rng_set_state(gpma_rng* r, const char* text) {
+    if (!r) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         std::istringstream is(text ? text : "");
         is >> r->r;
@@ -665,6 +697,10 @@ int gpma_rng_set_state(gpma_rng* r, const char* text) {
 }
 
 int gpma_rng_get_state(const gpma_rng* r, char* buf, size_t cap, size_t* len) {
+    if (!r) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         std::ostringstream os;
         os << r->r;
@@ -683,6 +719,10 @@ int gpma_rng_get_state(const gpma_rng* r, char* buf, size_t cap, size_t* len) {
 // advances) uniformly without replacement from the window as it stood before
 // the arrivals; deletions appended as gpma_window_slide's.
 int gpma_window_slide_explicit_random(gpma_window* w, size_t batch, gpma_rng* rng, gpma_slide_t* out) {
+    if (!w) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         auto& W = w->w;
         if (!rng) throw ApiError(PMA_EINVAL, "slide_explicit_random: null rng");
@@ -701,6 +741,10 @@ int gpma_window_slide_explicit_random(gpma_window* w, size_t batch, gpma_rng* rn
 }  // extern "C"
 
 extern "C" int gpma_window_deletions_host(gpma_window* w, size_t offset, size_t n, uint32_t* src, uint32_t* dst) {
+    if (!w) {
+        g_stream_err = "null handle";
+        return PMA_EINVAL;
+    }
     return sguard([&] {
         auto& W = w->w;
         if (offset + n > W.ndel) throw ApiError(PMA_ERANGE, "window deletions: range outside emitted deletions");

@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 from paper_1709_05061_b200 import abi
 
@@ -52,3 +53,44 @@ def test_struct_sizes_match_c_layout():
     assert ctypes.sizeof(abi.pma_stats) == 10 * 8 + 2 * 4 + 64 * 8
     assert ctypes.sizeof(abi.pma_profile) == 4 * 8 + 8
     assert ctypes.sizeof(abi.pma_engine_config) == 4 + 4 + 8 + 8 + 4 + 4
+
+
+# Every entry point that takes an existing handle first must reject a NULL
+# handle with PMA_EINVAL (checked before any CUDA call, so this runs on CPU)
+# instead of dereferencing it.  One subprocess for all of them: a crash
+# fails the test instead of killing the run.
+_NULL_PROBE = r"""
+import ctypes as C, sys
+sys.path.insert(0, sys.argv[1])
+from paper_1709_05061_b200 import abi
+lib = abi.load_library()
+bad = []
+for name, res, args in abi.SIGNATURES:
+    if not args or args[0] is not abi._P or res is not C.c_int:
+        continue
+    if name.endswith(("_destroy", "_create", "last_error")) or name in SKIP:
+        continue
+    vals = [None]
+    for t in args[1:]:
+        if t is abi._P or (isinstance(t, type) and issubclass(t, (C._Pointer, C.c_char_p, C.c_void_p))):
+            vals.append(None)
+        elif t in (C.c_double, C.c_float):
+            vals.append(0.0)
+        else:
+            vals.append(0)
+    print(name, flush=True)
+    rc = getattr(lib, name)(*vals)
+    if rc != abi.PMA_EINVAL:
+        bad.append((name, rc))
+print("BAD", bad)
+"""
+
+
+def test_null_handles_are_rejected():
+    # first argument is not a library handle: an id buffer / a device pointer
+    skip = {"gpma_nccl_unique_id", "gpma_ipc_close", "gpma_ipc_free"}
+    code = "SKIP = %r\n" % skip + _NULL_PROBE
+    p = subprocess.run([sys.executable, "-c", code, ROOT], capture_output=True, text=True, timeout=300)
+    last = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else ""
+    assert p.returncode == 0, f"crashed after {last!r}: {p.stderr[-500:]}"
+    assert last == "BAD []", last
