@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <atomic>
 #include <cstdlib>
 
 #include "block_ops.cuh"
@@ -72,6 +73,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     if (const char* e = std::getenv("GPMA_NO_GRAPHS")) small_graphs_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_BUCKETS")) buckets_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_PDL")) pdl_ = e[0] == '0';
+    if (const char* e = std::getenv("GPMA_NO_POLL")) small_poll_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     for (auto& e : lev_ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -666,6 +668,7 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
         const ull total = s_wsum[kSmallFrontThreads / 32 - 1];
         ctr->nsort = n;
         ctr->gt0 = gt0;
+        ctr->seq = f.seq;
         ctr->gdel = s_acc[0];
         ctr->bad_ins = s_acc[1];
         ctr->oor = s_acc[2];
@@ -1864,6 +1867,11 @@ __global__ void k_refresh_ranges(const u64* __restrict__ ranges, const ull* n_de
             const ull* src = reinterpret_cast<const ull*>(cctr);
             ull* dst = reinterpret_cast<ull*>(hctr);
             for (u32 i = threadIdx.x; i < sizeof(Ctr) / 8; i += blockDim.x) dst[i] = ld_volatile(src + i);
+            __syncthreads();
+            if (threadIdx.x == 0) {  // the counters landed first: the host may read them once it sees this
+                __threadfence_system();
+                st_volatile(&hctr->done_seq, ld_volatile(&cctr->seq));
+            }
         }
     }
 }
@@ -2504,9 +2512,30 @@ int Pma::run_small_graph(const GraphFront& gf, const EngineCfg& cfg) {
         capture_small_graph(db, cfg, levels);
         small_key_ = key;
     }
-    *h_desc_ = gf;  // read by the graph's first node (the previous replay finished: synchronous calls)
+    // read by the graph's first node (the previous replay is past it: its
+    // done_seq is written at the very end of the graph)
+    *h_desc_ = gf;
+    h_desc_->seq = ++small_seq_;
     GPMA_CUDA(cudaGraphLaunch(small_exec_, stream_));
-    GPMA_CUDA(cudaStreamSynchronize(stream_));
+    if (small_poll_) {
+        // the last refresh CTA writes the counters, then done_seq, to
+        // page-locked memory after every other kernel of the batch finished:
+        // poll it (the stream's completion would arrive a few µs later); a
+        // failed replay never writes it, so fall back to the stream sync,
+        // which reports the error
+        const volatile ull* done = &h_ctr->done_seq;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (u32 spin = 0; *done != small_seq_; ++spin) {
+            if ((spin & 1023u) == 1023u && std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(200)) {
+                GPMA_CUDA(cudaStreamSynchronize(stream_));
+                if (*done != small_seq_) throw ApiError(PMA_ECUDA, "small-batch graph did not complete");
+                break;
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+    } else {
+        GPMA_CUDA(cudaStreamSynchronize(stream_));
+    }
     return levels;
 }
 

@@ -63,6 +63,8 @@ struct Ctr {
     ull ngrid;      // grid tier: groups handed over by k_commit_cta at this level
     ull gt0, gt1;   // captured small batches: %globaltimer at the first kernel's entry / the last refresh CTA's exit
     ull refresh_done;  // captured small batches: refresh CTAs finished (the last returns the counters)
+    ull seq;           // captured small batches: the replay's sequence number (from the descriptor)
+    ull done_seq;      // ... written to the host copy LAST, after the counters (the host polls it)
     ull seg_tomb, seg_empty;  // grid tier: tombstones / empty leaves of the segment before its merge
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
@@ -117,6 +119,7 @@ struct GraphFront {
     // results
     u64 guard_deletes = 0;
     long long bad_insert = -1;  // first insert index with an id >= nv
+    u64 seq = 0;                // captured small batches: the replay's sequence number (echoed back when done)
 };
 
 class Pma {
@@ -270,6 +273,8 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     GraphFront* h_desc_dev_ = nullptr;  // device view of h_desc_ (read in place by the small graph)
     Ctr* h_ctr_dev_ = nullptr;          // device view of h_ctr (written by the small graph's last node)
     bool pdl_ = true;                   // small graph: programmatic edges between its kernels
+    bool small_poll_ = true;            // small graph: the host polls done_seq instead of synchronising the stream
+    u64 small_seq_ = 0;
     ScanWorkspace small_ws_;            // the graph's own look-back words (cleared by every replay)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
     // update bucket + ordinal, per sorted position bucket
