@@ -727,6 +727,10 @@ def sharded_analytics(G, nv, rank, group=False):
     rng = np.random.default_rng(ROOT_SEED)
     out = {}
     roots = [int(x) for x in rng.integers(0, nv, 3)]
+    if group:  # steady state of a window loop: one untimed call of each (buffers, NCCL paths)
+        G.bfs(roots[0])
+        G.connected_components()
+        G.pagerank(max_iters=2)
     ms = []
     for r in roots:
         dist.barrier()

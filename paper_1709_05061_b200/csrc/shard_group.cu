@@ -436,11 +436,12 @@ int gpma_shard_group_bfs(gpma_shard_group* sg, uint32_t root, uint32_t* dist_out
         if (dist_out) {  // every owner's range, gathered (padded chunks)
             sg->gath.reserve(W * C);
             GPMA_NCCL(nc.AllGather(sg->dist.ptr, sg->gath.ptr, C, ncclUint32, sg->comm, s));
-            std::vector<u32> all(W * C);
-            GPMA_CUDA(cudaMemcpyAsync(all.data(), sg->gath.ptr, W * C * 4, cudaMemcpyDeviceToHost, s));
-            GPMA_CUDA(cudaStreamSynchronize(s));
+            // each owner's chunk straight into the caller's array (one DMA per
+            // rank; no pageable staging copy)
             for (int r = 0; r < W; ++r)
-                std::memcpy(dist_out + sg->bounds[r], all.data() + u64(r) * C, (sg->bounds[r + 1] - sg->bounds[r]) * 4);
+                GPMA_CUDA(cudaMemcpyAsync(dist_out + sg->bounds[r], sg->gath.ptr + u64(r) * C,
+                                          (sg->bounds[r + 1] - sg->bounds[r]) * 4, cudaMemcpyDeviceToHost, s));
+            GPMA_CUDA(cudaStreamSynchronize(s));
         }
     });
 }
@@ -536,11 +537,10 @@ int gpma_shard_group_spmv(gpma_shard_group* sg, const double* x, double* y) {
         GPMA_CUDA(cudaMemcpyAsync(sg->x.ptr, x, nv * 8, cudaMemcpyHostToDevice, s));
         check_rc(gpma_shard_spmv(sg->g, sg->x.ptr, sg->y.ptr), sg->g);
         GPMA_NCCL(nc.AllGather(sg->y.ptr, sg->gy.ptr, C, ncclFloat64, sg->comm, s));
-        std::vector<double> all(W * C);
-        GPMA_CUDA(cudaMemcpyAsync(all.data(), sg->gy.ptr, W * C * 8, cudaMemcpyDeviceToHost, s));
-        GPMA_CUDA(cudaStreamSynchronize(s));
         for (int r = 0; r < W; ++r)
-            std::memcpy(y + sg->bounds[r], all.data() + u64(r) * C, (sg->bounds[r + 1] - sg->bounds[r]) * 8);
+            GPMA_CUDA(cudaMemcpyAsync(y + sg->bounds[r], sg->gy.ptr + u64(r) * C,
+                                      (sg->bounds[r + 1] - sg->bounds[r]) * 8, cudaMemcpyDeviceToHost, s));
+        GPMA_CUDA(cudaStreamSynchronize(s));
     });
 }
 

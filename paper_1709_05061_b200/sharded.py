@@ -35,7 +35,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from .abi import load_library, pma_stats
-from .pmagraph import GraphConfig, PackedMemoryArray, UpdateStats, _raise
+from .pmagraph import GraphConfig, PackedMemoryArray, UpdateStats, _host_out, _raise
 
 UNREACHED = 0xFFFFFFFF
 
@@ -692,20 +692,20 @@ class ShardGroup:
         return UpdateStats.from_c(st), routed.value, sent.value
 
     def bfs(self, root: int):
-        dist = np.empty(self.nv, np.uint32)
+        dist = _host_out(self.nv, np.uint32)  # (page-locked: the gathered result lands by DMA)
         reached = C.c_uint64()
         self._check(self._lib.gpma_shard_group_bfs(self.h, C.c_uint32(root), _vp_np(dist), C.byref(reached)))
         return dist, reached.value
 
     def connected_components(self):
-        lab = np.empty(self.nv, np.uint32)
+        lab = _host_out(self.nv, np.uint32)
         self._check(self._lib.gpma_shard_group_cc(self.h, _vp_np(lab)))
         return lab
 
     def pagerank(self, damping=0.85, epsilon=1e-3, max_iters=200, warm_start=None):
         if warm_start is not None and len(warm_start) != self.nv:
             raise ValueError("pagerank: warm start size mismatch")
-        ranks = np.empty(self.nv, np.float64)
+        ranks = _host_out(self.nv, np.float64)
         it, conv = C.c_uint64(), C.c_int()
         warm = None if warm_start is None else np.ascontiguousarray(warm_start, np.float64)
         self._check(self._lib.gpma_shard_group_pagerank(self.h, C.c_double(damping), C.c_double(epsilon), max_iters,
