@@ -95,27 +95,93 @@ __device__ __forceinline__ int owner_of_v(u32 v, const u32* b, int world) {
 // BFS (analytics.hpp:22-48), one level: the out-neighbours of the owned
 // frontier flagged in per-owner chunks (owner r's vertex v at r * chunk +
 // v - bounds[r]), ready for a reduce-scatter to the owners.
+// Owners' candidate flags for the frontier's out-neighbours (mark only: the
+// flags are idempotent stores, reduce-scattered to the owners afterwards).
+// Rows up to kGroupHubRow slots: a warp walks up to 32 frontier rows at once
+// (row bounds one per lane, then 128-slot steps of lane-parallel loads, as
+// graph.cu's k_bfs_expand); longer rows are set aside for
+// k_group_bfs_mark_hubs, which splits each over kGroupHubParts CTAs (one warp
+// walking an RMAT hub's row serialised the level).
+constexpr u64 kGroupHubRow = 4096;
+constexpr u32 kGroupHubParts = 32;
+
+__device__ __forceinline__ void group_flag(const u64* __restrict__ keys, const u8* __restrict__ st, u64 t,
+                                           const u32* s_b, int world, u64 chunk, u8* __restrict__ flags) {
+    if (st[t] != kValid) return;
+    const u64 k = keys[t];
+    if (is_guard(k)) return;
+    const u32 v = dst_of(k);
+    const int r = owner_of_v(v, s_b, world);
+    flags[u64(r) * chunk + (v - s_b[r])] = 1;
+}
+
 __global__ void __launch_bounds__(256) k_group_bfs_mark(const u32* __restrict__ frontier, u32 nf,
                                                         const u64* __restrict__ ro, const u64* __restrict__ keys,
                                                         const u8* __restrict__ st, const u32* __restrict__ bounds,
-                                                        int world, u64 chunk, u8* __restrict__ flags) {
+                                                        int world, u64 chunk, u8* __restrict__ flags,
+                                                        u32* __restrict__ hubs, u32* __restrict__ nhubs) {
     __shared__ u32 s_b[65];
     for (int i = threadIdx.x; i <= world; i += blockDim.x) s_b[i] = bounds[i];
     __syncthreads();
     const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
     const u64 nwarps = (u64(gridDim.x) * blockDim.x) >> 5;
-    for (u64 f = warp; f < nf; f += nwarps) {
-        const u32 u = frontier[f];
-        const u64 b = ro[u], e = ro[u + 1];
-        for (u64 t = b + lane; t < e; t += 32) {
-            if (st[t] != kValid) continue;
-            const u64 k = keys[t];
-            if (is_guard(k)) continue;
-            const u32 v = dst_of(k);
-            const int r = owner_of_v(v, s_b, world);
-            flags[u64(r) * chunk + (v - s_b[r])] = 1;
+    u32 V = u32((u64(nf) + nwarps - 1) / nwarps);  // rows per warp batch (fewer while the frontier is small)
+    V = V < 1 ? 1 : (V > 32 ? 32 : V);
+    for (u64 f0 = warp * V; f0 < nf; f0 += nwarps * V) {
+        u64 b = 0;
+        u32 len = 0;
+        if (lane < V && f0 + lane < nf) {
+            const u32 u = frontier[f0 + lane];
+            b = ro[u];
+            const u64 l = ro[u + 1] - b;
+            if (l > kGroupHubRow) hubs[atomicAdd(nhubs, 1u)] = u;
+            else len = u32(l);
         }
+        u32 inc = len;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const u32 y = __shfl_up_sync(FULL, inc, d);
+            if (lane >= unsigned(d)) inc += y;
+        }
+        const u32 total = __shfl_sync(FULL, inc, 31);
+        for (u32 s0 = 0; s0 < total; s0 += 128) {
+            u64 tt[4];
+            bool in[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const u32 sl = s0 + 32 * j + lane;
+                const u32 sc = sl < total ? sl : total - 1;
+                u32 r = 0;  // the row holding slot sc
+#pragma unroll
+                for (u32 step = 16; step > 0; step >>= 1)
+                    if (__shfl_sync(FULL, inc, r + step - 1) <= sc) r += step;
+                const u64 br = __shfl_sync(FULL, b, r);
+                const u32 er = __shfl_sync(FULL, inc, r), lr = __shfl_sync(FULL, len, r);
+                tt[j] = br + (sc - (er - lr));
+                in[j] = sl < total;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (in[j]) group_flag(keys, st, tt[j], s_b, world, chunk, flags);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_group_bfs_mark_hubs(const u32* __restrict__ hubs, const u32* nhubs,
+                                                             const u64* __restrict__ ro, const u64* __restrict__ keys,
+                                                             const u8* __restrict__ st, const u32* __restrict__ bounds,
+                                                             int world, u64 chunk, u8* __restrict__ flags) {
+    __shared__ u32 s_b[65];
+    for (int i = threadIdx.x; i <= world; i += blockDim.x) s_b[i] = bounds[i];
+    __syncthreads();
+    const u32 nh = *nhubs;
+    for (u64 task = blockIdx.x; task < u64(nh) * kGroupHubParts; task += gridDim.x) {
+        const u32 u = hubs[task / kGroupHubParts];
+        const u64 p = task % kGroupHubParts;
+        const u64 b0 = ro[u], len = ro[u + 1] - b0;
+        const u64 b = b0 + (len * p) / kGroupHubParts, e = b0 + (len * (p + 1)) / kGroupHubParts;
+        for (u64 t = b + threadIdx.x; t < e; t += blockDim.x) group_flag(keys, st, t, s_b, world, chunk, flags);
     }
 }
 
@@ -167,7 +233,7 @@ struct gpma_shard_group {
     DevBuf<u64> skeys, rkeys, counts, rcounts, bad;
     DevBuf<double> sw, rw;
     DevBuf<u8> flags, myflags;
-    DevBuf<u32> dist, frontier, next, nnext, labels, prev, od, gath;
+    DevBuf<u32> dist, frontier, next, nnext, labels, prev, od, gath, hubs;
     DevBuf<double> x, y, gy;
     std::string err;
 };
@@ -400,7 +466,8 @@ int gpma_shard_group_bfs(gpma_shard_group* sg, uint32_t root, uint32_t* dist_out
         sg->dist.reserve(C);
         sg->frontier.reserve(nloc + 1);
         sg->next.reserve(nloc + 1);
-        sg->nnext.reserve(2);
+        sg->nnext.reserve(3);
+        sg->hubs.reserve(nloc + 1);
         k_group_fill_u32<<<grid_for(C, 256, 148 * 4), 256, 0, s>>>(sg->dist.ptr, C, GPMA_UNREACHED);
         u32 nf = 0;
         if (root >= sg->lo && root < sg->hi) {  // the owner seeds the frontier
@@ -412,10 +479,16 @@ int gpma_shard_group_bfs(gpma_shard_group* sg, uint32_t root, uint32_t* dist_out
         u64 total = 1;
         for (u32 depth = 1;; ++depth) {
             GPMA_CUDA(cudaMemsetAsync(sg->flags.ptr, 0, W * C, s));
-            if (nf)
-                k_group_bfs_mark<<<grid_for(u64(nf) * 32, 256, 148 * 16), 256, 0, s>>>(
+            if (nf) {
+                GPMA_CUDA(cudaMemsetAsync(sg->nnext.ptr + 2, 0, 4, s));
+                k_group_bfs_mark<<<148 * 16, 256, 0, s>>>(
                     sg->frontier.ptr, nf, G.pma.ro_base(), G.pma.d_keys, G.pma.d_st, sg->d_bounds.ptr, W, C,
-                    sg->flags.ptr);
+                    sg->flags.ptr, sg->hubs.ptr, sg->nnext.ptr + 2);
+                GPMA_LAUNCH_CHECK();
+                k_group_bfs_mark_hubs<<<148 * 8, 256, 0, s>>>(sg->hubs.ptr, sg->nnext.ptr + 2, G.pma.ro_base(),
+                                                              G.pma.d_keys, G.pma.d_st, sg->d_bounds.ptr, W, C,
+                                                              sg->flags.ptr);
+            }
             GPMA_LAUNCH_CHECK();
             GPMA_NCCL(nc.ReduceScatter(sg->flags.ptr, sg->myflags.ptr, C, ncclUint8, ncclMax, sg->comm, s));
             GPMA_CUDA(cudaMemsetAsync(sg->nnext.ptr, 0, 8, s));
