@@ -274,6 +274,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     Ctr* h_ctr_dev_ = nullptr;          // device view of h_ctr (written by the small graph's last node)
     bool pdl_ = true;                   // small graph: programmatic edges between its kernels
     bool small_poll_ = true;            // small graph: the host polls done_seq instead of synchronising the stream
+    bool direct_touched_ = true;        // touched ranges written in place into a page-locked caller array
     u64 small_seq_ = 0;
     ScanWorkspace small_ws_;            // the graph's own look-back words (cleared by every replay)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
