@@ -1102,7 +1102,9 @@ __device__ __forceinline__ void touched_append(const CommitArgs& a, u64 b, u64 e
 // the row (chunk c of row r lives at chunk c ^ (r & 7)): the same bank spread
 // as a padded row, without the pad — 4 KB less shared memory per CTA, which
 // with u32 segment ids and <= 80 registers fits 6 CTAs (24 warps) per SM.
-__device__ __forceinline__ u32 swz(u32 row, u32 i) { return row * 16u + ((((i >> 1) ^ (row & 7u)) << 1) | (i & 1u)); }
+// (for i < 16, flipping bits 1-3 of i by the row's low 3 bits is exactly the
+// chunk XOR; bit 0 — the word inside a 16-byte chunk — stays)
+__device__ __forceinline__ u32 swz(u32 row, u32 i) { return row * 16u + (i ^ ((row & 7u) << 1)); }
 
 __global__ void __launch_bounds__(kLeafWarps * 32, GPMA_LEAF_CTAS) k_commit_leaf(CommitArgs a) {
     __shared__ __align__(16) u64 s_k[kLeafWarps][32 * 16];
@@ -1112,8 +1114,11 @@ __global__ void __launch_bounds__(kLeafWarps * 32, GPMA_LEAF_CTAS) k_commit_leaf
     __shared__ u32 s_uo[kLeafWarps][kStage / 4 + 2];
     __shared__ u32 s_b[kLeafWarps][32];  // segment (= leaf) of each group of the tile
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
-    auto RK = [&](u32 i) -> u64& { return s_k[w][swz(lane, i)]; };  // slot i of this lane's leaf
-    auto RV = [&](u32 i) -> u64& { return s_v[w][swz(lane, i)]; };
+    u64* const rowk = &s_k[w][lane * 16];
+    u64* const rowv = &s_v[w][lane * 16];
+    const u32 rx = (lane & 7u) << 1;
+    auto RK = [=](u32 i) -> u64& { return rowk[i ^ rx]; };  // slot i of this lane's leaf
+    auto RV = [=](u32 i) -> u64& { return rowv[i ^ rx]; };
     const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
     pdl_enter();
     const ull ngroups = a.ctr->ngroups;
