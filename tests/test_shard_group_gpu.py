@@ -71,3 +71,22 @@ def test_shard_group_rejects_out_of_range_insert():
         G.apply_batch(_dev(np.array([1, 3], np.uint32)), _dev(np.array([2, nv + 1], np.uint32)), None,
                       _dev(np.array([], np.uint32)), _dev(np.array([], np.uint32)))
     assert all((x == y).all() for x, y in zip(G.shard_slots(), before))
+
+
+def test_shard_group_bfs_hub_rows():
+    """Rows longer than the mark kernel's hub threshold (4096 slots) are
+    marked by CTA parts (k_group_bfs_mark_hubs): a dense RMAT whose top rows
+    exceed it, BFS from the hub and from an ordinary vertex vs the reference."""
+    nv = 1 << 12
+    stream = RefStream.rmat(nv, 400000, 5)
+    s, d, _, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    G = ShardGroup(nv, [0, nv], 0, 1, nccl_unique_id(), (_dev(s[:half]), _dev(d[:half]), None), GraphConfig())
+    ref = RefGraph(nv, s[:half], d[:half], None, graph_config())
+    ro = ref.row_offsets().astype(np.int64)
+    lens = np.diff(ro)
+    assert lens.max() > 4096, "the graph must have a hub row above the threshold"
+    for root in (int(np.argmax(lens)), int(np.argsort(lens)[len(lens) // 2])):
+        dist, reached = G.bfs(root)
+        rdist = ref.bfs(root)
+        assert (dist == rdist).all() and reached == int((rdist != 0xFFFFFFFF).sum())
