@@ -434,3 +434,40 @@ def test_radix_front_end_wide_keys(weighted):
     rs = r.apply_batch(a, b, w, c, dd)
     assert gs.parity() == ref_parity(r, rs)
     assert_same_slots(g.pma().slots(), r.slots(), "wide keys")
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_small_batch_sort_size_regimes(mode):
+    """Batches of exactly n updates at every size regime of the captured
+    small-batch graph's one-CTA sort (sort_block: P = 32 .. 4096 words, 1, 2
+    or 4 items per thread, and the boundaries between them), each with
+    duplicate inserts, insert + delete of one edge, deletes of present and
+    absent edges; slots and stats bit-exact after every batch."""
+    rng = np.random.default_rng(11)
+    nv = 1 << 14
+    stream = RefStream.rmat(nv, 200000, 9)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    cfg = GraphConfig(deletion_mode=mode)
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half], cfg)
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config(deletion_mode=mode))
+    present_s, present_d = s[:half].astype(np.uint32), d[:half].astype(np.uint32)
+    for n in (1, 2, 31, 32, 33, 100, 1023, 1024, 1025, 2047, 2048, 2049, 3000, 4095, 4096):
+        nd = n // 3
+        ni = n - nd
+        a = rng.integers(0, nv, ni).astype(np.uint32)
+        b = rng.integers(0, nv, ni).astype(np.uint32)
+        if ni >= 4:  # duplicate insert, and an insert also deleted in the same batch
+            a[1], b[1] = a[0], b[0]
+        ww = rng.random(ni) + 0.5
+        pick = rng.integers(0, len(present_s), nd)
+        c, dd = present_s[pick].copy(), present_d[pick].copy()
+        if nd >= 2:
+            c[0], dd[0] = a[0], b[0]
+            c[1], dd[1] = rng.integers(0, nv, 2).astype(np.uint32)  # (most likely) absent
+        gs = g.apply_batch(a, b, ww, c, dd)
+        rs = r.apply_batch(a, b, ww, c, dd)
+        ctx = f"n={n}"
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
