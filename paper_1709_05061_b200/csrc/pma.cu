@@ -2415,12 +2415,13 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
 // ---- small graph batches ----------------------------------------------
 // A batch of up to kSmallGraphMax graph updates is latency-bound: a dozen
 // tiny kernels whose cost is their launches and the host round trips between
-// rounds.  Its whole front end (pack + checks, one-CTA radix sort, duplicate
-// resolution, leaf search) and the first rounds are captured ONCE as a CUDA
-// graph whose nodes read the batch descriptor and every count from device
-// memory; each batch then costs one descriptor write, one graph launch and
-// one synchronisation.  The graph embeds array and scratch pointers, the
-// layout and the engine config; any change re-captures it.
+// rounds.  Its whole front end (k_small_front: pack + checks, one-CTA sort,
+// duplicate resolution; k_leaf_search_warp) and round 0 are captured ONCE as
+// a CUDA graph with programmatic edges, whose nodes read the batch descriptor
+// (in place, page-locked) and every count from device memory; each batch then
+// costs one descriptor write, one graph launch and a poll of the sequence
+// word the last node writes.  The graph embeds array and scratch pointers,
+// the layout and the engine config; any change re-captures it.
 bool Pma::small_graph_ok(u64 n, const GraphFront& gf) const {
     if (!small_graphs_ || gf.mk || n == 0 || n > kSmallGraphMax || height_ < 1 || !ro_base() || !stream_) return false;
     int db = 1;
