@@ -471,3 +471,51 @@ def test_small_batch_sort_size_regimes(mode):
         assert gs.parity() == ref_parity(r, rs), ctx
         assert_same_slots(g.pma().slots(), r.slots(), ctx)
         assert (g.row_offsets() == r.row_offsets()).all(), ctx
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_mixed_batch_sizes_through_growth_and_shrink(mode):
+    """Small (captured-graph) and large (host-loop) batches interleaved on one
+    graph while it grows past several capacities and, in eager mode, shrinks
+    back: every layout change re-captures the small-batch graph; slots, stats
+    and row offsets bit-exact after every batch."""
+    rng = np.random.default_rng(21)
+    nv = 1 << 13
+    s0 = rng.integers(0, nv, 2000).astype(np.uint32)
+    d0 = rng.integers(0, nv, 2000).astype(np.uint32)
+    cfg = GraphConfig(deletion_mode=mode)
+    g = DynamicGraph.from_edges(nv, s0, d0, None, cfg)
+    r = RefGraph(nv, s0, d0, None, graph_config(deletion_mode=mode))
+    live_s, live_d = list(s0), list(d0)
+    grows = shrinks = 0
+    for step, n in enumerate([100, 30000, 7, 4096, 60000, 1, 3000, 120000, 50, 2048]):
+        a = rng.integers(0, nv, n).astype(np.uint32)
+        b = rng.integers(0, nv, n).astype(np.uint32)
+        nd = min(len(live_s), n // 2)
+        pick = rng.choice(len(live_s), nd, replace=False) if nd else np.zeros(0, np.int64)
+        c = np.array([live_s[i] for i in pick], np.uint32)
+        dd = np.array([live_d[i] for i in pick], np.uint32)
+        gs = g.apply_batch(a, b, None, c, dd)
+        rs = r.apply_batch(a, b, None, c, dd)
+        ctx = f"step {step} n={n}"
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
+        grows += gs.grow_events
+        shrinks += gs.shrink_events
+        keep = np.ones(len(live_s), bool)
+        keep[pick] = False
+        live_s = [x for x, k in zip(live_s, keep) if k] + list(a)
+        live_d = [x for x, k in zip(live_d, keep) if k] + list(b)
+    # massive deletes at the end (eager mode shrinks the root)
+    c = np.array(live_s, np.uint32)
+    dd = np.array(live_d, np.uint32)
+    e = np.zeros(0, np.uint32)
+    gs = g.apply_batch(e, e, None, c, dd)
+    rs = r.apply_batch(e, e, None, c, dd)
+    assert gs.parity() == ref_parity(r, rs), "final deletes"
+    assert_same_slots(g.pma().slots(), r.slots(), "final deletes")
+    shrinks += gs.shrink_events
+    assert grows >= 2, "the graph must grow through several capacities"
+    if mode == PMA_EAGER:
+        assert shrinks >= 1, "eager deletes must shrink the root"
