@@ -519,3 +519,27 @@ def test_mixed_batch_sizes_through_growth_and_shrink(mode):
     assert grows >= 2, "the graph must grow through several capacities"
     if mode == PMA_EAGER:
         assert shrinks >= 1, "eager deletes must shrink the root"
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_small_batches_custom_profile(mode):
+    """A non-default DensityProfile (tighter leaf and root bounds) through the
+    captured small-batch graph, whose commit nodes bake the per-level bounds
+    in at capture: bit-exact against the reference with the same profile."""
+    from paper_1709_05061_b200.pmagraph import DensityProfile
+    rng = np.random.default_rng(8)
+    nv = 1 << 12
+    stream = RefStream.rmat(nv, 60000, 4)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    prof = DensityProfile(leaf_lower=0.2, leaf_upper=0.7, root_lower=0.3, root_upper=0.6)
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half], GraphConfig(deletion_mode=mode, profile=prof))
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config(deletion_mode=mode, profile=prof.c()))
+    win = RefWindow(stream)
+    for b in (10, 200, 1000, 1800, 3, 600):
+        a, bb, ww, c, dd = win.slide(b)
+        gs = g.apply_batch(a, bb, ww, c, dd)
+        rs = r.apply_batch(a, bb, ww, c, dd)
+        assert gs.parity() == ref_parity(r, rs), f"batch {b}"
+        assert_same_slots(g.pma().slots(), r.slots(), f"batch {b}")
+        assert (g.row_offsets() == r.row_offsets()).all(), f"batch {b}"
