@@ -723,6 +723,7 @@ __global__ void __launch_bounds__(256) k_leaf_search_warp(const u64* __restrict_
 __global__ void k_bucket_scatter(const u64* __restrict__ ck, const u32* __restrict__ ci, const u32* __restrict__ lf,
                                  const u32* __restrict__ od, const u32* __restrict__ off, u64 n, u64* __restrict__ out,
                                  u32* __restrict__ oci) {
+    pdl_enter();
     // four updates per thread per step: four independent offset lookups in flight
     const u64 nt = u64(gridDim.x) * blockDim.x;
     for (u64 i0 = blockIdx.x * u64(blockDim.x) + threadIdx.x; i0 < n; i0 += 4 * nt) {
@@ -773,6 +774,7 @@ constexpr u32 kSmallRun = 16;
 __global__ void k_bucket_sort_small(const u64* __restrict__ in, const u32* __restrict__ inc,
                                     const u32* __restrict__ off, u64 L, u64* __restrict__ out,
                                     u32* __restrict__ outc, u32* __restrict__ slf, u32* __restrict__ big, Ctr* ctr) {
+    pdl_enter();
     const bool pairs = inc != nullptr;
     const unsigned lane = threadIdx.x & 31u;
     const u64 warp = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
@@ -824,6 +826,7 @@ __global__ void __launch_bounds__(256) k_bucket_sort_big(const u64* __restrict__
                                                          const u32* __restrict__ off, const u32* __restrict__ big,
                                                          const ull* nbig, u64* __restrict__ out,
                                                          u32* __restrict__ outc) {
+    pdl_enter();
     __shared__ u64 sm[kRunMax];
     __shared__ u32 smc[kRunMax];
     const bool pairs = inc != nullptr;
@@ -2684,21 +2687,31 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     const u32* sorted_ci = si_in.ptr;
     if (bucket) {
         const u64 L = num_leaves();
-        exclusive_sum(stream_, ws, bcnt.ptr, boff.ptr, L + 2, bcnt.ptr);  // (leaves bcnt[0, L + 2) zeroed)
-        bcnt_zero_ = bcnt.cap;  // (entries past L + 2 were never counted into)
+        // (the bucket kernels chained by programmatic edges, as the rounds)
+        bbig.reserve(n / (kSmallRun + 1) + 1);
         const bool pairs = packed_ib == 0;
         static const unsigned scat_res = resident_grid(k_bucket_scatter, 256);
         static const unsigned sort_res = resident_grid(k_bucket_sort_small, 256);
-        k_bucket_scatter<<<grid_for(n, 256, scat_res), 256, 0, stream_>>>(
-            sk_in.ptr, pairs ? si_in.ptr : nullptr, blf.ptr, bod.ptr, boff.ptr, n, sk_out.ptr, si_out.ptr);
-        GPMA_LAUNCH_CHECK();
-        bbig.reserve(n / (kSmallRun + 1) + 1);
-        k_bucket_sort_small<<<grid_for((L + 1 + 31) / 32 * 32, 256, sort_res), 256, 0, stream_>>>(
-            sk_out.ptr, pairs ? si_out.ptr : nullptr, boff.ptr, L, sk_in.ptr, si_in.ptr, bslf.ptr, bbig.ptr, d_ctr);
-        GPMA_LAUNCH_CHECK();
-        k_bucket_sort_big<<<148 * 2, 256, 0, stream_>>>(sk_out.ptr, pairs ? si_out.ptr : nullptr, boff.ptr, bbig.ptr,
-                                                         &d_ctr->nbig_buckets, sk_in.ptr, si_in.ptr);
-        GPMA_LAUNCH_CHECK();
+        pdl_chain() = pdl_;
+        try {
+            exclusive_sum(stream_, ws, bcnt.ptr, boff.ptr, L + 2, bcnt.ptr);  // (leaves bcnt[0, L + 2) zeroed)
+            bcnt_zero_ = bcnt.cap;  // (entries past L + 2 were never counted into)
+            launch_k(k_bucket_scatter, dim3(grid_for(n, 256, scat_res)), dim3(256), 0, stream_,
+                     static_cast<const u64*>(sk_in.ptr), static_cast<const u32*>(pairs ? si_in.ptr : nullptr),
+                     static_cast<const u32*>(blf.ptr), static_cast<const u32*>(bod.ptr),
+                     static_cast<const u32*>(boff.ptr), n, sk_out.ptr, si_out.ptr);
+            launch_k(k_bucket_sort_small, dim3(grid_for((L + 1 + 31) / 32 * 32, 256, sort_res)), dim3(256), 0,
+                     stream_, static_cast<const u64*>(sk_out.ptr), static_cast<const u32*>(pairs ? si_out.ptr : nullptr),
+                     static_cast<const u32*>(boff.ptr), L, sk_in.ptr, si_in.ptr, bslf.ptr, bbig.ptr, d_ctr);
+            launch_k(k_bucket_sort_big, dim3(148 * 2), dim3(256), 0, stream_, static_cast<const u64*>(sk_out.ptr),
+                     static_cast<const u32*>(pairs ? si_out.ptr : nullptr), static_cast<const u32*>(boff.ptr),
+                     static_cast<const u32*>(bbig.ptr), static_cast<const ull*>(&d_ctr->nbig_buckets), sk_in.ptr,
+                     si_in.ptr);
+        } catch (...) {
+            pdl_chain() = false;
+            throw;
+        }
+        pdl_chain() = false;
         launches += 5;
     } else if (packed_ib && n > 1) {
         // keys-only: the arrival index rides in the low bits below the key

@@ -386,6 +386,7 @@ constexpr int kSumTile = kScanThreads * kSumItems;
 
 static __global__ void __launch_bounds__(kScanThreads) k_exclusive_sum(const u32* __restrict__ in, u32* __restrict__ out,
                                                                 u64 n, ull* tiles, ull epoch, u32* clear) {
+    pdl_enter();
     __shared__ u32 s_w[kScanWarps];
     __shared__ ull s_prefix;
     const u64 tile = blockIdx.x;
@@ -479,8 +480,8 @@ inline void exclusive_sum(cudaStream_t s, ScanWorkspace& ws, const u32* in, u32*
         GPMA_CUDA(cudaMemsetAsync(ws.tiles.ptr, 0, ws.tiles.cap * sizeof(ull), s));
         ws.epoch = 1;
     }
-    k_exclusive_sum<<<unsigned(ntiles), kScanThreads, 0, s>>>(in, out, n, ws.tiles.ptr, ws.epoch, clear);
-    GPMA_LAUNCH_CHECK();
+    launch_k(k_exclusive_sum, dim3(unsigned(ntiles)), dim3(kScanThreads), 0, s, in, out, n, ws.tiles.ptr, ws.epoch,
+             clear);
 }
 
 // Dynamic shared memory beyond 48 KB for the rank/scatter kernels, once per
