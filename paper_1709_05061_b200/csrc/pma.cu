@@ -2715,12 +2715,28 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         launches += 5;
     } else if (packed_ib && n > 1) {
         // keys-only: the arrival index rides in the low bits below the key
-        const int alt = radix_sort(stream_, rws, sk_in.ptr, sk_out.ptr, nullptr, nullptr, n, packed_ib,
-                                   packed_ib + nbits, &launches);
+        // (histogram and digit passes chained by PDL edges)
+        pdl_chain() = pdl_;
+        int alt = 0;
+        try {
+            alt = radix_sort(stream_, rws, sk_in.ptr, sk_out.ptr, nullptr, nullptr, n, packed_ib, packed_ib + nbits,
+                             &launches);
+        } catch (...) {
+            pdl_chain() = false;
+            throw;
+        }
+        pdl_chain() = false;
         sorted_ck = alt ? sk_out.ptr : sk_in.ptr;
     } else if (nbits > 0 && n > 1) {
-        const int alt = radix_sort(stream_, rws, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr, n, 0, nbits,
-                                   &launches);
+        pdl_chain() = pdl_;
+        int alt = 0;
+        try {
+            alt = radix_sort(stream_, rws, sk_in.ptr, sk_out.ptr, si_in.ptr, si_out.ptr, n, 0, nbits, &launches);
+        } catch (...) {
+            pdl_chain() = false;
+            throw;
+        }
+        pdl_chain() = false;
         sorted_ck = alt ? sk_out.ptr : sk_in.ptr;
         sorted_ci = alt ? si_out.ptr : si_in.ptr;
     }

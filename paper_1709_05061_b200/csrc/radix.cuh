@@ -143,6 +143,7 @@ __device__ __forceinline__ void radix_rank_tile(const u64 (&k)[kRadixIpt], u32 w
 static __global__ void __launch_bounds__(256) k_radix_hist(const u64* __restrict__ keys, u64 n, int begin, int end,
                                                     u32* __restrict__ hist) {
     __shared__ u32 sh[kRadixMaxPasses * kRadixBins];
+    pdl_enter();
     const int npass = (end - begin + 7) / 8;
     for (int i = threadIdx.x; i < npass * kRadixBins; i += blockDim.x) sh[i] = 0;
     __syncthreads();
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(kRadixThreads, 2)
                  u32* __restrict__ vout, u64 n, int shift, u32 mask, const u32* __restrict__ ghist, ull* status,
                  ull epoch, const u32* __restrict__ tile_off) {
     extern __shared__ __align__(16) unsigned char smem[];
+    pdl_enter();
     using S = RadixSmem<kVals>;
     u64* sk = reinterpret_cast<u64*>(smem);
     u32* sv = reinterpret_cast<u32*>(smem + S::kKeyBytes);
@@ -544,8 +546,7 @@ inline int radix_sort(cudaStream_t s, RadixWorkspace& ws, u64* k0, u64* k1, u32*
     GPMA_CUDA(cudaMemsetAsync(ws.hist.ptr, 0, size_t(npass) * kRadixBins * sizeof(u32), s));
     static const unsigned hist_grid = resident_grid(k_radix_hist, 256);
     const unsigned hg = unsigned(std::min<u64>(hist_grid, (n + 511) / 512));
-    k_radix_hist<<<hg, 256, 0, s>>>(k0, n, begin, end, ws.hist.ptr);
-    GPMA_LAUNCH_CHECK();
+    launch_k(k_radix_hist, dim3(hg), dim3(256), 0, s, static_cast<const u64*>(k0), n, begin, end, ws.hist.ptr);
     u64* ki = k0;
     u64* ko = k1;
     u32* vi = v0;
@@ -567,12 +568,13 @@ inline int radix_sort(cudaStream_t s, RadixWorkspace& ws, u64* k0, u64* k1, u32*
             toff = ws.toff.ptr;
         }
         if (vals)
-            k_radix_pass<true><<<unsigned(ntiles), kRadixThreads, RadixSmem<true>::kBytes, s>>>(
-                ki, ko, vi, vo, n, sh_, m, gh, ws.status.ptr, ws.epoch, toff);
+            launch_k(k_radix_pass<true>, dim3(unsigned(ntiles)), dim3(kRadixThreads), RadixSmem<true>::kBytes, s,
+                     static_cast<const u64*>(ki), ko, static_cast<const u32*>(vi), vo, n, sh_, m, gh, ws.status.ptr,
+                     ws.epoch, toff);
         else
-            k_radix_pass<false><<<unsigned(ntiles), kRadixThreads, RadixSmem<false>::kBytes, s>>>(
-                ki, ko, nullptr, nullptr, n, sh_, m, gh, ws.status.ptr, ws.epoch, toff);
-        GPMA_LAUNCH_CHECK();
+            launch_k(k_radix_pass<false>, dim3(unsigned(ntiles)), dim3(kRadixThreads), RadixSmem<false>::kBytes, s,
+                     static_cast<const u64*>(ki), ko, static_cast<const u32*>(nullptr), static_cast<u32*>(nullptr), n,
+                     sh_, m, gh, ws.status.ptr, ws.epoch, toff);
         std::swap(ki, ko);
         std::swap(vi, vo);
     }
