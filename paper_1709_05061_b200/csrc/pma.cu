@@ -876,6 +876,7 @@ __global__ void k_leaf_search(const u64* __restrict__ uk, const ull* n_dev, cons
 __global__ void k_leaf_search_sorted(const u64* __restrict__ uk, const ull* n_dev, const u64* __restrict__ hdr, u64 L,
                                      const u8* __restrict__ st, u64 leaf, const u64* __restrict__ ro, u64 rlo,
                                      u64 rhi, u32* __restrict__ ul) {
+    pdl_enter();
     const u64 n = *n_dev;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
         ul[i] = u32(leaf_for_key(uk[i], hdr, L, st, leaf, ro, rlo, rhi));
@@ -2825,10 +2826,18 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         ++launches;
         if (!bucket) {
             // leaf assignment (pma.hpp:234-289), once per batch
-            k_leaf_search_sorted<<<grid_for(n, 256, 148 * 8), 256, 0, stream_>>>(
-                uk.ptr, &d_ctr->n_unique, d_hdr, num_leaves(), d_st, leaf_, ro_base(), ro_lo, ro_lo + num_vertices,
-                ul.ptr);
-            GPMA_LAUNCH_CHECK();
+            // (a programmatic edge from the compaction: it overlaps the launch)
+            pdl_chain() = pdl_;
+            try {
+                launch_k(k_leaf_search_sorted, dim3(grid_for(n, 256, 148 * 8)), dim3(256), 0, stream_,
+                         static_cast<const u64*>(uk.ptr), static_cast<const ull*>(&d_ctr->n_unique),
+                         static_cast<const u64*>(d_hdr), num_leaves(), static_cast<const u8*>(d_st), leaf_,
+                         static_cast<const u64*>(ro_base()), ro_lo, ro_lo + num_vertices, ul.ptr);
+            } catch (...) {
+                pdl_chain() = false;
+                throw;
+            }
+            pdl_chain() = false;
             ++launches;
         }
     }
