@@ -76,7 +76,6 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     if (const char* e = std::getenv("GPMA_NO_POLL")) small_poll_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_DIRECT_TOUCHED")) direct_touched_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
-    for (auto& e : lev_ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
     headers_closed_form(nullptr, 0);
     GPMA_CUDA(cudaStreamSynchronize(stream_));
@@ -92,8 +91,6 @@ Pma::~Pma() {
     if (h_desc_) cudaFreeHost(h_desc_);
     if (d_desc_) cudaFree(d_desc_);
     for (auto& e : ev_)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : lev_ev_)
         if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(own_stream_);
 }
@@ -953,6 +950,16 @@ __device__ __forceinline__ void flush_acc(const Acc& a, Ctr* ctr) {
     if (a.bytes) atomicAdd(&ctr->commit_bytes, a.bytes);
 }
 
+// level span stamps of the commit kernels (Ctr::lvl_tmin / lvl_tmax)
+__device__ __forceinline__ void level_stamp(Ctr* c, int level, bool begin) {
+    if (level < 16 && threadIdx.x == 0) {
+        u64 g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        if (begin) atomicMax(&c->lvl_tmin[level], ~ull(g));
+        else atomicMax(&c->lvl_tmax[level], ull(g));
+    }
+}
+
 __device__ void block_flush(Acc acc, Ctr* ctr) {
     __shared__ ull s_acc[9];
     if (threadIdx.x < 9) s_acc[threadIdx.x] = 0;
@@ -1125,6 +1132,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, GPMA_LEAF_CTAS) k_commit_leaf
     auto RV = [=](u32 i) -> u64& { return rowv[i ^ rx]; };
     const u8* s_op = reinterpret_cast<const u8*>(&s_uo[w][0]);
     pdl_enter();
+    level_stamp(a.ctr, a.level, true);
     const ull ngroups = a.ctr->ngroups;
     // tiles handed out dynamically (one counter per launch): tiles differ in
     // cost (merges vs tombstone flips vs deferrals), a static stride left
@@ -1426,6 +1434,7 @@ __global__ void __launch_bounds__(kLeafWarps * 32, GPMA_LEAF_CTAS) k_commit_leaf
     warp_reduce_acc(acc);
     if ((threadIdx.x & 31u) != 0) acc = Acc{};
     block_flush(acc, a.ctr);
+    level_stamp(a.ctr, a.level, false);
 }
 
 // --- warp tiers.  G = 16 (half-warp per group: leaf-level segments, two
@@ -1449,6 +1458,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
     __shared__ unsigned char s_vl[kWarpTierWarps][32];   // their lanes
     __shared__ unsigned char s_ir[kWarpTierWarps][32];   // insert p: # Valid keys below it
     pdl_enter();
+    level_stamp(a.ctr, a.level, true);
     const unsigned lane = threadIdx.x & 31u, w = threadIdx.x >> 5;
     const unsigned hb = G == 32 ? 0u : (lane & 16u), hl = lane & unsigned(G - 1);
     const ull ngroups = a.ctr->ngroups;
@@ -1646,6 +1656,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
     warp_reduce_acc(acc);
     if (lane != 0) acc = Acc{};
     block_flush(acc, a.ctr);
+    level_stamp(a.ctr, a.level, false);
 }
 
 // ------------------------------------------------------------- CTA tier
@@ -1656,6 +1667,7 @@ __global__ void __launch_bounds__(kWarpTierWarps * 32, 4) k_commit_lanes(CommitA
 __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
     __shared__ ull s_w64[kCtaThreads / 32];
     pdl_enter();
+    level_stamp(a.ctr, a.level, true);
     // biglist mode: only the hub groups the warp tiers handed over
     const ull ngroups = a.biglist ? a.ctr->nbig : a.ctr->ngroups;
     Acc acc;
@@ -1760,6 +1772,7 @@ __global__ void __launch_bounds__(kCtaThreads) k_commit_cta(CommitArgs a) {
     }
     if (threadIdx.x != 0) acc = Acc{};
     block_flush(acc, a.ctr);
+    level_stamp(a.ctr, a.level, false);
 }
 
 // ------------------------------------------------------------- grid tier
@@ -2248,7 +2261,8 @@ void Pma::grid_merge(u64 b, u64 m, const u32* plist, u64 s, bool large) {
 // group the pending list by segment (unique_segments), decide + commit every
 // group, keep the deferred groups' updates (advance_round).  Every kernel
 // reads its counts on the device; npend is a host-known upper bound of the
-// pending count.  events: record the level's commit span (lev_ev_).
+// pending count.  (The commit kernels stamp the level's span into the
+// counters: lvl_tmin / lvl_tmax.)
 void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
                         ScanWorkspace& ws, bool events, u64& launches) {
     const u64 m = leaf_ << level;
@@ -2310,7 +2324,6 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
     a.eager = cfg.eager;
     a.large = cfg.large_for(m);
     a.cap_gt_min = cap_ > 16;
-    if (events) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level], stream_));
     ensure_slot_scratch();
     ik.reserve(n);
     iv.reserve(n);
@@ -2384,7 +2397,6 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
         }
     }
     GPMA_LAUNCH_CHECK();
-    if (events) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));
     ++launches;
     // advance_round: keep deferred groups' updates
     {
@@ -2942,7 +2954,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             }
             for (int l = synced_upto + 1; l <= level; ++l) {
                 float ms = 0.f;
-                cudaEventElapsedTime(&ms, lev_ev_[2 * l], lev_ev_[2 * l + 1]);
+                if (l < 16 && h_ctr->lvl_tmin[l] && h_ctr->lvl_tmax[l])
+                    ms = float(double(h_ctr->lvl_tmax[l] - ~h_ctr->lvl_tmin[l]) * 1e-6);
                 seg_ms += ms;
                 if (l < 16) {
                     timing.level_ms[l] += ms;

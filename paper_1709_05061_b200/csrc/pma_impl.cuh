@@ -63,6 +63,12 @@ struct Ctr {
     ull ngrid;      // grid tier: groups handed over by k_commit_cta at this level
     ull gt0, gt1;   // captured small batches: %globaltimer at the first kernel's entry / the last refresh CTA's exit
     ull refresh_done;  // captured small batches: refresh CTAs finished (the last returns the counters)
+    // commit-kernel span of each level (%globaltimer, levels < 16): the
+    // complement of the earliest CTA start (atomicMax of ~t) and the latest
+    // CTA end — no event records between a level's kernels, so their
+    // programmatic edges stay intact
+    ull lvl_tmin[16];
+    ull lvl_tmax[16];
     ull seq;           // captured small batches: the replay's sequence number (from the descriptor)
     ull done_seq;      // ... written to the host copy LAST, after the counters (the host polls it)
     ull seg_tomb, seg_empty;  // grid tier: tombstones / empty leaves of the segment before its merge
@@ -308,7 +314,6 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u8> mflag;
 
     cudaEvent_t ev_[8]{};
-    cudaEvent_t lev_ev_[2 * kMaxLevels]{};  // commit-kernel span of each level
 };
 
 }  // namespace gpma
