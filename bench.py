@@ -446,6 +446,33 @@ def run_ours(args):
     g = g2
     ext = torch.cuda.ExternalStream(lib.gpma_cuda_stream(g.h), device=torch.device("cuda", dev))
 
+    # ---- cross-check of the commit kernel's span with CUDA events ----
+    # The timed steps above take the level-0 commit span from %globaltimer
+    # stamps the commit kernels write (first CTA start -> last CTA end): event
+    # records between a level's kernels would break their programmatic (PDL)
+    # edges and slow the step.  A short extra pass with GPMA_LEVEL_EVENTS=1
+    # (events on the library's stream around the commit kernels) checks it.
+    chk = {"ms": 0.0, "bytes": 0, "steps": 0}
+
+    def on_chk(graph, s, timed):
+        graph.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset, None,
+                                 s.n_ins, info.del_src + 4 * s.del_offset, info.del_dst + 4 * s.del_offset, s.n_del)
+        if timed:
+            tm = graph.last_timing()
+            chk["ms"] += tm.level_ms[0]
+            chk["bytes"] += tm.level_bytes[0]
+            chk["steps"] += 1
+
+    os.environ["GPMA_LEVEL_EVENTS"] = "1"
+    try:
+        gchk = make_graph()
+    finally:
+        os.environ.pop("GPMA_LEVEL_EVENTS", None)
+    kchk = max(1, min(K, 5))
+    gchk, _, _ = run_passes(gchk, make_graph, slides[:min(P, 1 + kchk)], min(P, 1 + kchk), 1, kchk, on_chk, dev,
+                            world, None)
+    del gchk
+
     # ---- roofline of the dominant kernel (warp-tier commit: decide+merge+scatter) ----
     peak, peak_kind = measured_peak()
     # algorithmic bytes of the commit kernels, counted per examined group by the
@@ -470,7 +497,14 @@ def run_ours(args):
     achieved = (level_bytes[0] / K) / (l0_ms / 1e3) / 1e9 if l0_ms > 0 else None
     all_achieved = (commit_bytes / K) / ((seg_ms / K) / 1e3) / 1e9 if seg_ms > 0 else None
     traffic = ncu_traffic(args.config)
+    ev_ms = chk["ms"] / chk["steps"] if chk["steps"] else 0.0
+    ev_ach = (chk["bytes"] / chk["steps"]) / (ev_ms / 1e3) / 1e9 if ev_ms > 0 else None
     roofline = {"bound": "hbm", "kernel": kernel_desc,
+                "timing": "level-0 commit span from %globaltimer stamps written by the commit kernels during the "
+                          "timed steps (first CTA start -> last CTA end); events_check = the same span from CUDA "
+                          "events on the library's stream in a separate short pass (GPMA_LEVEL_EVENTS=1)",
+                "events_check": {"steps": chk["steps"], "kernel_ms_per_step": ev_ms, "achieved": ev_ach,
+                                 "frac": (ev_ach / peak) if ev_ach else None},
                 "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "algorithmic_bytes_per_step": level_bytes[0] // K, "kernel_ms_per_step": l0_ms,

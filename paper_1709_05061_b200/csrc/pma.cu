@@ -92,6 +92,8 @@ Pma::~Pma() {
     if (d_desc_) cudaFree(d_desc_);
     for (auto& e : ev_)
         if (e) cudaEventDestroy(e);
+    for (auto& e : lev_ev_)
+        if (e) cudaEventDestroy(e);
     if (own_stream_) cudaStreamDestroy(own_stream_);
 }
 
@@ -2324,6 +2326,7 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
     a.eager = cfg.eager;
     a.large = cfg.large_for(m);
     a.cap_gt_min = cap_ > 16;
+    if (level_events_ && events && level < 16) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level], stream_));
     ensure_slot_scratch();
     ik.reserve(n);
     iv.reserve(n);
@@ -2397,6 +2400,7 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
         }
     }
     GPMA_LAUNCH_CHECK();
+    if (level_events_ && events && level < 16) GPMA_CUDA(cudaEventRecord(lev_ev_[2 * level + 1], stream_));
     ++launches;
     // advance_round: keep deferred groups' updates
     {
@@ -2954,7 +2958,9 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             }
             for (int l = synced_upto + 1; l <= level; ++l) {
                 float ms = 0.f;
-                if (l < 16 && h_ctr->lvl_tmin[l] && h_ctr->lvl_tmax[l])
+                if (l < 16 && level_events_)  // (cross-check mode: CUDA events around the commit kernels)
+                    cudaEventElapsedTime(&ms, lev_ev_[2 * l], lev_ev_[2 * l + 1]);
+                else if (l < 16 && h_ctr->lvl_tmin[l] && h_ctr->lvl_tmax[l])
                     ms = float(double(h_ctr->lvl_tmax[l] - ~h_ctr->lvl_tmin[l]) * 1e-6);
                 seg_ms += ms;
                 if (l < 16) {

@@ -281,6 +281,8 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     bool pdl_ = true;                   // small graph: programmatic edges between its kernels
     bool small_poll_ = true;            // small graph: the host polls done_seq instead of synchronising the stream
     bool direct_touched_ = true;        // touched ranges written in place into a page-locked caller array
+    bool level_events_ = false;         // GPMA_LEVEL_EVENTS=1: level spans from CUDA events (cross-check of the stamps)
+    cudaEvent_t lev_ev_[32]{};          // (only with level_events_: before / after the commit kernels of levels < 16)
     u64 small_seq_ = 0;
     ScanWorkspace small_ws_;            // the graph's own look-back words (cleared by every replay)
     // leaf-bucket front end (graph batches): per-leaf counters / offsets, per
