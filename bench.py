@@ -352,12 +352,22 @@ def run_ours(args):
                                         info.del_dst + 4 * s.del_offset, s.n_del)
 
     clocks = ClockSampler(dev)
-    per_step = []  # (stats, timing) kept raw; digested after the timed region
+    # (stats, timing) of each timed step kept raw in structs allocated before
+    # the timed region, decoded after it (bench bookkeeping stays off the
+    # per-step host path)
+    raw = [(pg.pma_stats(), pg.pma_timing()) for _ in range(K)]
+    per_step = []
 
     def on_step(graph, s, timed):
-        st = apply_dev(graph, s)
         if timed:
-            per_step.append((st, graph.last_timing()))
+            st_raw, tm = raw[len(per_step)]
+            graph.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset, None,
+                                     s.n_ins, info.del_src + 4 * s.del_offset, info.del_dst + 4 * s.del_offset,
+                                     s.n_del, stats_out=st_raw)
+            graph.last_timing(out=tm)
+            per_step.append((st_raw, tm))
+        else:
+            apply_dev(graph, s)
 
     segs = []
     g, ms, passes = run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs)
@@ -374,6 +384,7 @@ def run_ours(args):
     level_groups = [0] * 16
     level_big = [0] * 16
     level_maxs = [0] * 16
+    per_step = [(pg.UpdateStats.from_c(st), tm) for st, tm in per_step]
     for st, tm in per_step:
         updates += st.batch_size
         seg_ms += st.segment_phase_ns / 1e6

@@ -415,16 +415,20 @@ class DynamicGraph:
         return UpdateStats.from_c(st, self.pma().touched_ranges() if with_touched else None)
 
     def apply_batch_device(self, d_is: int, d_id: int, d_iw: int | None, ni: int, d_ds: int, d_dd: int,
-                           nd: int) -> UpdateStats:
+                           nd: int, stats_out: pma_stats | None = None) -> UpdateStats | None:
+        """stats_out: fill this raw struct instead of building an UpdateStats
+        (for loops that decode the stats later: UpdateStats.from_c)."""
         # (the small-batch latency path: argtypes convert the raw addresses,
         # one stats struct per graph is reused)
-        st = self.__dict__.get("_dev_st")
+        st = stats_out
         if st is None:
-            st = self._dev_st = pma_stats()
+            st = self.__dict__.get("_dev_st")
+            if st is None:
+                st = self._dev_st = pma_stats()
         rc = self._lib.gpma_apply_batch_device(self.h, d_is, d_id, d_iw or None, ni, d_ds, d_dd, nd, C.byref(st))
         if rc:
             self._check(rc)
-        return UpdateStats.from_c(st)
+        return None if stats_out is not None else UpdateStats.from_c(st)
 
     def reserve_batch(self, max_updates: int):
         """Pre-size every per-batch buffer of apply_batch (gpma_reserve_batch)."""
@@ -446,8 +450,8 @@ class DynamicGraph:
         self._check(self._lib.gpma_csr_snapshot(self.h, _p(ro), _p(col), _p(val)))
         return ro, col[:ne], val[:ne]
 
-    def last_timing(self) -> pma_timing:
-        t = pma_timing()
+    def last_timing(self, out: pma_timing | None = None) -> pma_timing:
+        t = pma_timing() if out is None else out
         self._check(self._lib.gpma_last_timing(self.h, C.byref(t)))
         return t
 
