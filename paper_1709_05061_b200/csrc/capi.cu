@@ -304,7 +304,7 @@ int pma_redispatch(pma_handle* h, int level, size_t seg_index, const uint64_t* k
 
 int pma_last_timing(const pma_handle* h, pma_timing* out) {
     if (!h || !out) return PMA_EINVAL;
-    *out = h->impl->timing;
+    *out = h->impl->timing_now();
     return PMA_OK;
 }
 
@@ -619,7 +619,7 @@ int gpma_shard_spmv(gpma_graph* g, const double* d_x, double* d_y_local) {
 
 int gpma_last_timing(const gpma_graph* g, pma_timing* out) {
     if (!g || !out) return PMA_EINVAL;
-    *out = g->impl->pma.timing;
+    *out = g->impl->pma.timing_now();
     return PMA_OK;
 }
 

@@ -146,7 +146,25 @@ void Pma::sync_ctr() {
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void Pma::event(int idx) { GPMA_CUDA(cudaEventRecord(ev_[idx], stream_)); }
+void Pma::event(int idx) {
+    if (timing_pending_) resolve_timing();  // (the previous batch's stage events are about to be re-recorded)
+    GPMA_CUDA(cudaEventRecord(ev_[idx], stream_));
+}
+
+void Pma::resolve_timing() {
+    timing_pending_ = false;
+    GPMA_CUDA(cudaEventSynchronize(ev_[4]));
+    float a = 0, b = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
+    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
+    cudaEventElapsedTime(&c, ev_[2], ev_[3]);
+    cudaEventElapsedTime(&d, ev_[3], ev_[4]);
+    timing.sort_ms = a;
+    timing.search_ms = b;
+    timing.rounds_ms = c;
+    timing.refresh_ms = d;
+    timing.device_ms = a + b + c + d;
+}
 
 // ==================================================================== kernels
 
@@ -3189,7 +3207,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             ++launches;
         }
     }
-    if (!graph_levels || host_levels) {  // (a graph-only batch: recorded by the graph, synchronised already)
+    // a host-loop batch whose tail was enqueued before the last sync returns
+    // now: the counters are on the host, the refresh finishes on the stream
+    // (every later call on this Pma is ordered behind it) — the host's return
+    // and the next batch's set-up overlap it
+    const bool async_tail = spec_tail && !graph_levels;
+    if ((!graph_levels || host_levels) && !async_tail) {  // (a graph-only batch: synchronised already)
         if (!spec_tail) event(4);  // (a speculative tail recorded it)
         GPMA_CUDA(cudaStreamSynchronize(stream_));
     }
@@ -3203,7 +3226,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         float hl = 0;
         if (host_levels) cudaEventElapsedTime(&hl, ev_[0], ev_[4]);
         a += hl;
-    } else {
+    } else if (!async_tail) {
         cudaEventElapsedTime(&a, ev_[0], ev_[1]);
         cudaEventElapsedTime(&b, ev_[1], ev_[2]);
         cudaEventElapsedTime(&c, ev_[2], ev_[3]);
@@ -3214,6 +3237,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.rounds_ms = c;
     timing.refresh_ms = d;
     timing.device_ms = a + b + c + d;
+    timing_pending_ = async_tail;
     timing.kernel_launches = launches;
     timing.front_end = bucket ? 1 : 0;
     if (gf) {

@@ -218,6 +218,16 @@ public:
     int device() const { return device_; }
     std::string err;
     pma_timing timing{};
+    // A host-loop batch returns once its counters are on the host; its tail
+    // (header / row-offset refresh) may still be running on the stream, so
+    // the event-based stage times are resolved later: by the next event
+    // record on this Pma, or when the timing is read (timing_now()).
+    bool timing_pending_ = false;
+    void resolve_timing();
+    const pma_timing& timing_now() {
+        if (timing_pending_) resolve_timing();
+        return timing;
+    }
 
     u64 valid_count = 0;
     u64 tombstone_count = 0;
