@@ -195,7 +195,8 @@ def full_slides(info, B):
     return P
 
 
-def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segments=None, stream_of=None):
+def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segments=None, stream_of=None,
+               on_segment=None):
     """Drive W untimed warm-up steps then K timed steps over `slides` (the
     first min(W + K, P) full slides of the window, in order).  When a pass has
     used every slide the stream holds, the graph is rebuilt from the initial
@@ -204,7 +205,8 @@ def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segm
     have.  Timed segments are bracketed by barrier + synchronize and timed by
     CUDA events on the library's stream; returns (graph, summed ms, passes);
     `segments` (if given) receives each timed segment's steps / event ms /
-    host wall ms."""
+    host wall ms; on_segment(g, "start" | "end") runs just outside each timed
+    segment."""
     import torch
     from paper_1709_05061_b200.abi import load_library
     lib = load_library()
@@ -227,6 +229,8 @@ def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segm
         else:
             sp = stream_of(g) if stream_of else lib.gpma_cuda_stream(g.h)
             ext = torch.cuda.ExternalStream(sp, device=torch.device("cuda", dev))
+            if on_segment is not None:
+                on_segment(g, "start")
             if world > 1:
                 torch.distributed.barrier()
             torch.cuda.synchronize()
@@ -245,6 +249,8 @@ def run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segm
                 torch.distributed.barrier()
             total += e0.elapsed_time(e1)
             segments.append({"steps": n, "ms": round(e0.elapsed_time(e1), 4), "wall_ms": round(wall, 4)})
+            if on_segment is not None:
+                on_segment(g, "end")
         step += n
         cur += n
     return g, total, passes
@@ -352,25 +358,32 @@ def run_ours(args):
                                         info.del_dst + 4 * s.del_offset, s.n_del)
 
     clocks = ClockSampler(dev)
-    # (stats, timing) of each timed step kept raw in structs allocated before
-    # the timed region, decoded after it (bench bookkeeping stays off the
-    # per-step host path)
-    raw = [(pg.pma_stats(), pg.pma_timing()) for _ in range(K)]
+    # Each timed step's stats land in a struct allocated before the timed
+    # region (decoded after it); the timing records of the timed steps are
+    # summed by the library (gpma_timing_sum, read once per timed segment):
+    # reading every batch's record would wait for its deferred refresh tail.
+    raw = [pg.pma_stats() for _ in range(K)]
     per_step = []
+    tsums = []
 
     def on_step(graph, s, timed):
         if timed:
-            st_raw, tm = raw[len(per_step)]
+            st_raw = raw[len(per_step)]
             graph.apply_batch_device(info.stream_src + 4 * s.ins_offset, info.stream_dst + 4 * s.ins_offset, None,
                                      s.n_ins, info.del_src + 4 * s.del_offset, info.del_dst + 4 * s.del_offset,
                                      s.n_del, stats_out=st_raw)
-            graph.last_timing(out=tm)
-            per_step.append((st_raw, tm))
+            per_step.append(st_raw)
         else:
             apply_dev(graph, s)
 
+    def on_segment(graph, phase):
+        t, n = graph.timing_sum(reset=True)
+        if phase == "end":
+            tsums.append((t, n))
+
     segs = []
-    g, ms, passes = run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs)
+    g, ms, passes = run_passes(g, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs,
+                               on_segment=on_segment)
     clk = clocks.stop()
     updates = 0
     seg_ms = 0.0
@@ -384,14 +397,19 @@ def run_ours(args):
     level_groups = [0] * 16
     level_big = [0] * 16
     level_maxs = [0] * 16
-    per_step = [(pg.UpdateStats.from_c(st), tm) for st, tm in per_step]
-    for st, tm in per_step:
+    per_step = [pg.UpdateStats.from_c(st) for st in per_step]
+    for st in per_step:
         updates += st.batch_size
         seg_ms += st.segment_phase_ns / 1e6
+        rounds += st.rounds
+    tsum_batches = 0
+    device_ms_sum = 0.0
+    for tm, nb in tsums:
+        tsum_batches += nb
+        device_ms_sum += tm.device_ms
         merge_slots += tm.merge_slots
         commit_bytes += tm.commit_bytes
         launches += tm.kernel_launches
-        rounds += st.rounds
         for k in stage:
             stage[k] += getattr(tm, k)
         for lv in range(16):
@@ -400,6 +418,7 @@ def run_ours(args):
             level_groups[lv] += tm.level_groups[lv]
             level_big[lv] += tm.level_big[lv]
             level_maxs[lv] = max(level_maxs[lv], tm.level_max_slice[lv])
+    assert tsum_batches == K, f"timing sum covers {tsum_batches} batches, expected {K}"
     ms_max, total_updates = reduce_max_sum(ms, updates, world)
     value = total_updates / (ms_max / 1e3)
 
@@ -525,7 +544,7 @@ def run_ours(args):
                 "scatter_bytes_per_step": BYTES_PER_MERGE_SLOT * merge_slots // K,
                 "commit_ms_per_step_all_levels": seg_ms / K, "step_ms": ms / K,
                 "stage_ms_per_step": {k: v / K for k, v in stage.items()},
-                "device_ms_each_step": [round(tm.device_ms, 4) for _, tm in per_step],
+                "device_ms_mean": round(device_ms_sum / K, 4),
                 "timed_segments": segs,
                 "commit_ms_per_level": [round(x / K, 4) for x in level_ms if x > 0],
                 "groups_per_level": [x / K for x in level_groups if x > 0],

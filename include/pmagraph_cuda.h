@@ -309,6 +309,12 @@ int gpma_pagerank(gpma_graph* g, double damping, double epsilon, size_t max_iter
 int gpma_spmv(gpma_graph* g, const double* x, double* y);
 
 int gpma_last_timing(const gpma_graph* g, pma_timing* out);
+/* Sum of the pma_timing records of every update batch since the last reset
+ * (level_max_slice: the maximum), and how many batches it covers; reset != 0
+ * starts a new sum after copying.  Lets a driver time a loop of batches
+ * without reading each batch's record (which waits for a batch's deferred
+ * refresh tail). */
+int gpma_timing_sum(gpma_graph* g, pma_timing* out, uint64_t* batches, int reset);
 
 /* The cudaStream_t (as void*) every call on this handle runs on, so callers
  * can bracket calls with CUDA events on the launching stream. */

@@ -211,6 +211,7 @@ SIGNATURES = [
     ("gpma_pagerank", C.c_int, [_P, C.c_double, C.c_double, C.c_size_t, _P, _P, _U64P, C.POINTER(C.c_int)]),
     ("gpma_spmv", C.c_int, [_P, _P, _P]),
     ("gpma_last_timing", C.c_int, [_P, C.POINTER(pma_timing)]),
+    ("gpma_timing_sum", C.c_int, [_P, C.POINTER(pma_timing), C.POINTER(C.c_uint64), C.c_int]),
     ("gpma_cuda_stream", _P, [_P]),
     ("pma_cuda_stream", _P, [_P]),
     ("gpma_shard_from_edges_device", C.c_int, [C.POINTER(gpma_graph_config), C.c_int, C.c_size_t, C.c_uint32, C.c_uint32, _P, _P, _P, C.c_size_t, C.POINTER(_P)]),

@@ -623,6 +623,19 @@ int gpma_last_timing(const gpma_graph* g, pma_timing* out) {
     return PMA_OK;
 }
 
+int gpma_timing_sum(gpma_graph* g, pma_timing* out, uint64_t* batches, int reset) {
+    return guarded_on(g, [&] {
+        auto& p = g->impl->pma;
+        p.resolve_all();
+        if (out) *out = p.tsum_;
+        if (batches) *batches = p.tsum_n_;
+        if (reset) {
+            p.tsum_ = pma_timing{};
+            p.tsum_n_ = 0;
+        }
+    });
+}
+
 void* gpma_cuda_stream(gpma_graph* g) { return g ? (void*)g->impl->pma.stream() : nullptr; }
 void* pma_cuda_stream(pma_handle* h) { return h ? (void*)h->impl->stream() : nullptr; }
 

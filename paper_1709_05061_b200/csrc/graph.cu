@@ -907,7 +907,7 @@ cudaEvent_t Graph::pma_ev(int i) {
 void Graph::record_timing(u64 launches) {
     float ms = 0;
     cudaEventElapsedTime(&ms, pma_ev(0), pma_ev(1));
-    pma.timing_pending_ = false;  // (a batch's deferred stage times are superseded)
+    pma.resolve_all();  // (a batch's deferred record joins the sum first)
     pma.timing = pma_timing{};
     pma.timing.device_ms = ms;
     pma.timing.kernel_launches = launches;

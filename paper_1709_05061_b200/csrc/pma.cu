@@ -146,24 +146,56 @@ void Pma::sync_ctr() {
     GPMA_CUDA(cudaStreamSynchronize(stream_));
 }
 
-void Pma::event(int idx) {
-    if (timing_pending_) resolve_timing();  // (the previous batch's stage events are about to be re-recorded)
-    GPMA_CUDA(cudaEventRecord(ev_[idx], stream_));
+void Pma::event(int idx) { GPMA_CUDA(cudaEventRecord(E(idx), stream_)); }
+
+void Pma::accumulate_timing(const pma_timing& t) {
+    pma_timing& a = tsum_;
+    a.device_ms += t.device_ms;
+    a.sort_ms += t.sort_ms;
+    a.search_ms += t.search_ms;
+    a.rounds_ms += t.rounds_ms;
+    a.refresh_ms += t.refresh_ms;
+    a.kernel_launches += t.kernel_launches;
+    a.merge_slots += t.merge_slots;
+    a.tombstone_flips += t.tombstone_flips;
+    a.commit_bytes += t.commit_bytes;
+    a.front_end += t.front_end;
+    a.grid_merges += t.grid_merges;
+    for (int l = 0; l < 16; ++l) {
+        a.level_ms[l] += t.level_ms[l];
+        a.level_groups[l] += t.level_groups[l];
+        a.level_big[l] += t.level_big[l];
+        a.level_bytes[l] += t.level_bytes[l];
+        a.level_max_slice[l] = std::max(a.level_max_slice[l], t.level_max_slice[l]);
+    }
+    ++tsum_n_;
 }
 
-void Pma::resolve_timing() {
-    timing_pending_ = false;
-    GPMA_CUDA(cudaEventSynchronize(ev_[4]));
+// stage times of the deferred batch recorded in event set `set`
+void Pma::resolve_set(int set) {
+    pend_[set] = false;
+    const cudaEvent_t* e = ev_ + set * 6;
+    GPMA_CUDA(cudaEventSynchronize(e[4]));
     float a = 0, b = 0, c = 0, d = 0;
-    cudaEventElapsedTime(&a, ev_[0], ev_[1]);
-    cudaEventElapsedTime(&b, ev_[1], ev_[2]);
-    cudaEventElapsedTime(&c, ev_[2], ev_[3]);
-    cudaEventElapsedTime(&d, ev_[3], ev_[4]);
-    timing.sort_ms = a;
-    timing.search_ms = b;
-    timing.rounds_ms = c;
-    timing.refresh_ms = d;
-    timing.device_ms = a + b + c + d;
+    cudaEventElapsedTime(&a, e[0], e[1]);
+    cudaEventElapsedTime(&b, e[1], e[2]);
+    cudaEventElapsedTime(&c, e[2], e[3]);
+    cudaEventElapsedTime(&d, e[3], e[4]);
+    pma_timing& t = pend_t_[set];
+    t.sort_ms = a;
+    t.search_ms = b;
+    t.rounds_ms = c;
+    t.refresh_ms = d;
+    t.device_ms = a + b + c + d;
+    accumulate_timing(t);
+    if (set == ev_set_ && latest_pending_) {  // still the last batch's record: complete it
+        timing.sort_ms = a;
+        timing.search_ms = b;
+        timing.rounds_ms = c;
+        timing.refresh_ms = d;
+        timing.device_ms = t.device_ms;
+        latest_pending_ = false;
+    }
 }
 
 // ==================================================================== kernels
@@ -2608,6 +2640,11 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         return;
     }
     bool bucket = false;
+    // this batch's stage events: the other set (a deferred record two
+    // batches old is resolved first — its tail finished long ago)
+    latest_pending_ = false;  // (`timing` now belongs to this batch)
+    ev_set_ ^= 1;
+    if (pend_[ev_set_]) resolve_set(ev_set_);
     const bool small_graph = gf && small_graph_ok(n, *gf);
     if (!small_graph) event(0);  // (a graph batch is timed by the graph's own %globaltimer stamps)
     // ---- small graph batches: the front end and the first rounds replayed
@@ -2617,7 +2654,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     const u64 graph_ns = graph_levels && h_ctr->gt1 > h_ctr->gt0 ? h_ctr->gt1 - h_ctr->gt0 : 0;
     if (graph_levels) {
         // (stage events skipped: a small batch's whole device span is the
-        // graph, ev_[0] -> ev_[4]; every host API call counts at this size)
+        // graph, E(0) -> E(4); every host API call counts at this size)
     } else {
     // ---- 1. sort (stable, varying bits only) ----
     GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
@@ -2970,7 +3007,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 event(4);
                 launches += spec_walk ? 2 : 1;
                 spec_tail = true;
-                GPMA_CUDA(cudaEventSynchronize(ev_[5]));
+                GPMA_CUDA(cudaEventSynchronize(E(5)));
             } else {
                 sync_ctr();
             }
@@ -3224,20 +3261,26 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // the graph (its %globaltimer span) + any host-loop levels: reported as one stage
         a = float(double(graph_ns) * 1e-6);
         float hl = 0;
-        if (host_levels) cudaEventElapsedTime(&hl, ev_[0], ev_[4]);
+        if (host_levels) cudaEventElapsedTime(&hl, E(0), E(4));
         a += hl;
     } else if (!async_tail) {
-        cudaEventElapsedTime(&a, ev_[0], ev_[1]);
-        cudaEventElapsedTime(&b, ev_[1], ev_[2]);
-        cudaEventElapsedTime(&c, ev_[2], ev_[3]);
-        cudaEventElapsedTime(&d, ev_[3], ev_[4]);
+        cudaEventElapsedTime(&a, E(0), E(1));
+        cudaEventElapsedTime(&b, E(1), E(2));
+        cudaEventElapsedTime(&c, E(2), E(3));
+        cudaEventElapsedTime(&d, E(3), E(4));
     }
     timing.sort_ms = a;
     timing.search_ms = b;
     timing.rounds_ms = c;
     timing.refresh_ms = d;
     timing.device_ms = a + b + c + d;
-    timing_pending_ = async_tail;
+    if (async_tail) {
+        pend_t_[ev_set_] = timing;
+        pend_[ev_set_] = true;
+        latest_pending_ = true;
+    } else {
+        accumulate_timing(timing);
+    }
     timing.kernel_launches = launches;
     timing.front_end = bucket ? 1 : 0;
     if (gf) {

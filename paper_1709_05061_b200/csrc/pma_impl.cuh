@@ -220,12 +220,27 @@ public:
     pma_timing timing{};
     // A host-loop batch returns once its counters are on the host; its tail
     // (header / row-offset refresh) may still be running on the stream, so
-    // the event-based stage times are resolved later: by the next event
-    // record on this Pma, or when the timing is read (timing_now()).
-    bool timing_pending_ = false;
-    void resolve_timing();
+    // the event-based stage times are resolved later (resolve_set): when its
+    // event set comes round again, or when the timing is read (timing_now()).
+    // Stage events alternate between two sets per batch, so a batch's set is
+    // only re-recorded two batches later (its tail long finished): resolving
+    // a deferred record never waits inside the next batch.
+    int ev_set_ = 0;
+    bool pend_[2] = {false, false};
+    bool latest_pending_ = false;  // `timing` (the last batch's record) still lacks its stage times
+    pma_timing pend_t_[2]{};
+    cudaEvent_t E(int idx) const { return ev_[ev_set_ * 6 + idx]; }
+    void resolve_set(int set);
+    void resolve_all() {
+        for (int k = 0; k < 2; ++k)
+            if (pend_[k]) resolve_set(k);
+    }
+    // sum of the batches' records since the last reset (gpma_timing_sum)
+    pma_timing tsum_{};
+    u64 tsum_n_ = 0;
+    void accumulate_timing(const pma_timing& t);
     const pma_timing& timing_now() {
-        if (timing_pending_) resolve_timing();
+        resolve_all();
         return timing;
     }
 
@@ -325,7 +340,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     DevBuf<u32> es, mb;
     DevBuf<u8> mflag;
 
-    cudaEvent_t ev_[8]{};
+    cudaEvent_t ev_[12]{};  // two sets of six stage events, alternating per batch (ev_set_)
 };
 
 }  // namespace gpma

@@ -455,6 +455,14 @@ class DynamicGraph:
         self._check(self._lib.gpma_last_timing(self.h, C.byref(t)))
         return t
 
+    def timing_sum(self, reset: bool = False):
+        """(summed pma_timing of the batches since the last reset, batch count)
+        — gpma_timing_sum; reset starts a new sum."""
+        t = pma_timing()
+        n = C.c_uint64()
+        self._check(self._lib.gpma_timing_sum(self.h, C.byref(t), C.byref(n), 1 if reset else 0))
+        return t, n.value
+
     # -- read API (graph.hpp:94-126, 208-223), derived from device snapshots --
     def edge_list(self):
         """graph.hpp:208-217: (src, dst, weight) of every edge in key order."""
