@@ -686,14 +686,21 @@ def run_sharded(args, rank, world, local):
             acc["routed"] += routed
             acc["sent"] += sent
             acc["seg_ms"] += st.segment_phase_ns / 1e6
-            tm = pg.pma_timing()
-            load_library().gpma_last_timing(g.graph_handle() if group else g.h[0], C.byref(tm))
-            acc["launches"] += tm.kernel_launches + (4 if group else 6)
+            acc["launches"] += 4 if group else 6  # (the routing's own launches; the engine's come from the sum)
+
+    def on_segment(g, phase):
+        # the engine's timing records summed by the library over the segment
+        tm = pg.pma_timing()
+        nb = C.c_uint64()
+        load_library().gpma_timing_sum(g.graph_handle() if group else g.h[0], C.byref(tm), C.byref(nb), 1)
+        if phase == "end":
+            acc["launches"] += tm.kernel_launches
             acc["commit_bytes"] += tm.commit_bytes
 
     clocks = ClockSampler(dev)
     segs = []
-    G, ms, passes = run_passes(G, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs, stream_of=stream_of)
+    G, ms, passes = run_passes(G, make_graph, slides, P, W, K, on_step, dev, world, clocks, segs, stream_of=stream_of,
+                               on_segment=on_segment)
     clk = clocks.stop()
     t = torch.tensor([ms], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
