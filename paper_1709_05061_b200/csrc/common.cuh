@@ -98,6 +98,16 @@ inline void launch_k(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, c
     GPMA_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...));
 }
 
+// stage / span stamp: the complement of %globaltimer kept by atomicMax, so
+// the earliest caller wins and 0 means "not stamped" (thread 0 of each CTA)
+__device__ __forceinline__ void stamp_first(ull* slot) {
+    if (slot && threadIdx.x == 0) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        atomicMax(slot, ~g);
+    }
+}
+
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;

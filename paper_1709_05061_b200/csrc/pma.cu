@@ -176,14 +176,12 @@ void Pma::resolve_set(int set) {
     pend_[set] = false;
     const cudaEvent_t* e = ev_ + set * 6;
     GPMA_CUDA(cudaEventSynchronize(e[4]));
-    float a = 0, b = 0, c = 0, d = 0;
-    cudaEventElapsedTime(&a, e[0], e[1]);
-    cudaEventElapsedTime(&b, e[1], e[2]);
-    cudaEventElapsedTime(&c, e[2], e[3]);
-    cudaEventElapsedTime(&d, e[3], e[4]);
     pma_timing& t = pend_t_[set];
-    t.sort_ms = a;
-    t.search_ms = b;
+    float dev03 = 0, d = 0;
+    cudaEventElapsedTime(&dev03, e[0], e[3]);
+    cudaEventElapsedTime(&d, e[3], e[4]);
+    const float a = float(t.sort_ms), b = float(t.search_ms);  // (from the stage stamps, set at the batch's end)
+    const float c = std::max(0.f, dev03 - a - b);
     t.rounds_ms = c;
     t.refresh_ms = d;
     t.device_ms = a + b + c + d;
@@ -231,6 +229,7 @@ __global__ void k_validate_sorted(const u64* keys, u64 n, Ctr* ctr) {
 }
 
 __global__ void k_or_mask(const u64* keys, u64 n, Ctr* ctr) {
+    stamp_first(&ctr->t_front);
     const u64 k0 = keys[0];
     u64 acc = 0;
     for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
@@ -507,6 +506,7 @@ __device__ __forceinline__ void prep_graph_body(const GraphFront& f, int db, int
 template <bool kBucket>
 __global__ void __launch_bounds__(256, kBucket ? 4 : 1) k_prep_graph(GraphFront f, int db, int ib, u64* __restrict__ ck,
                                                                      u32* __restrict__ ci, Ctr* ctr, BucketArgs ba) {
+    stamp_first(&ctr->t_front);
     prep_graph_body<kBucket>(f, db, ib, ck, ci, ctr, ba);
 }
 
@@ -2345,7 +2345,8 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
                 ctr->ngroups = total;
                 gs[total] = u32(*np_cur);
                 ctr->lvl_npend[lv] = *np_cur;
-            });
+            },
+            level == 0 ? &d_ctr->t_rounds : nullptr);
         ++launches;
     }
     // commit (decide + merge + scatter)
@@ -2818,7 +2819,9 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     uv.reserve(n + 4);
     uop.reserve(n + 32);  // k_commit_leaf stages 16-byte aligned runs of uk / uv / uop
     ul.reserve(n);
-    event(1);
+    // (no event record here: the compaction stays on a programmatic edge
+    // from the sort and stamps the stage boundary itself, Ctr::t_dedup)
+    pdl_chain() = pdl_;
     {
         const u64* ck = sorted_ck;
         const u32* ci = sorted_ci;
@@ -2893,7 +2896,9 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                 // no-op (nothing is mutated) and the batch is rejected or redone
                 // after the first host sync — no round trip before the rounds
                 ctr->np[0] = (ctr->bad_ins || ctr->oor || ctr->bigrun) ? 0ull : total;
-            });
+            },
+            &d_ctr->t_dedup);
+        pdl_chain() = false;
         ++launches;
         if (!bucket) {
             // leaf assignment (pma.hpp:234-289), once per batch
@@ -2912,7 +2917,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             ++launches;
         }
     }
-    event(2);
     }  // front end
     pidx0.reserve(n);
     pidx1.reserve(n);
@@ -3263,17 +3267,27 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         float hl = 0;
         if (host_levels) cudaEventElapsedTime(&hl, E(0), E(4));
         a += hl;
-    } else if (!async_tail) {
-        cudaEventElapsedTime(&a, E(0), E(1));
-        cudaEventElapsedTime(&b, E(1), E(2));
-        cudaEventElapsedTime(&c, E(2), E(3));
-        cudaEventElapsedTime(&d, E(3), E(4));
+    } else {
+        // front end and resolve from the kernels' stage stamps, the rest from
+        // the events ev0 -> ev3 -> ev4 (a deferred batch: when resolved)
+        auto t = [](ull x) { return x ? ~x : 0ull; };
+        const ull tf = t(h_ctr->t_front), td = t(h_ctr->t_dedup), tr = t(h_ctr->t_rounds);
+        a = (tf && td >= tf) ? float(double(td - tf) * 1e-6) : 0.f;
+        b = (td && tr >= td) ? float(double(tr - td) * 1e-6) : 0.f;
+        if (!async_tail) {
+            float dev03 = 0;
+            cudaEventElapsedTime(&dev03, E(0), E(3));
+            cudaEventElapsedTime(&d, E(3), E(4));
+            c = std::max(0.f, dev03 - a - b);
+        }
     }
     timing.sort_ms = a;
     timing.search_ms = b;
     timing.rounds_ms = c;
     timing.refresh_ms = d;
     timing.device_ms = a + b + c + d;
+    timing.kernel_launches = launches;
+    timing.front_end = bucket ? 1 : 0;
     if (async_tail) {
         pend_t_[ev_set_] = timing;
         pend_[ev_set_] = true;
@@ -3281,8 +3295,6 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     } else {
         accumulate_timing(timing);
     }
-    timing.kernel_launches = launches;
-    timing.front_end = bucket ? 1 : 0;
     if (gf) {
         gf->guard_deletes = h_ctr->gdel;
         gf->bad_insert = h_ctr->bad_ins ? (long long)(~h_ctr->bad_ins) : -1;

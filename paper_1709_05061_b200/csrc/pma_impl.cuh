@@ -69,6 +69,10 @@ struct Ctr {
     // programmatic edges stay intact
     ull lvl_tmin[16];
     ull lvl_tmax[16];
+    // stage starts of a host-loop batch (complements of %globaltimer, the
+    // earliest CTA): front end, duplicate resolution, round 0 — no event
+    // records between the front end's kernels, whose PDL edges stay intact
+    ull t_front, t_dedup, t_rounds;
     ull seq;           // captured small batches: the replay's sequence number (from the descriptor)
     ull done_seq;      // ... written to the host copy LAST, after the counters (the host polls it)
     ull seg_tomb, seg_empty;  // grid tier: tombstones / empty leaves of the segment before its merge

@@ -42,10 +42,12 @@ __device__ __forceinline__ void st_volatile(ull* p, ull v) { *reinterpret_cast<v
 // Lets a caller interleave independent per-item work (e.g. 8 binary searches).
 template <class Flag, class EmitTile, class Fin>
 __global__ void __launch_bounds__(kScanThreads, 7) compact_kernel(const ull* n_dev, ull n_host, Flag flag,
-                                                               EmitTile emit_tile, Fin fin, ull* tiles, ull epoch) {
+                                                               EmitTile emit_tile, Fin fin, ull* tiles, ull epoch,
+                                                               ull* stamp) {
     __shared__ unsigned s_off[kScanItems * kScanWarps];  // (item row, warp) counts -> exclusive offsets
     __shared__ ull s_prefix, s_total;
     pdl_enter();
+    stamp_first(stamp);
     const ull n = n_dev ? *n_dev : n_host;
     const ull ntiles = (n + kScanTile - 1) / kScanTile;
     const ull tile = blockIdx.x;
@@ -142,7 +144,7 @@ struct PerItemEmit {
 
 template <class Flag, class EmitTile, class Fin>
 void run_compact_tile(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host, ull n_bound, Flag flag,
-                      EmitTile emit_tile, Fin fin) {
+                      EmitTile emit_tile, Fin fin, ull* stamp = nullptr) {
     const ull ntiles = (n_bound + kScanTile - 1) / kScanTile;
     if (ntiles == 0) return;
     if (ntiles > ws.tiles.cap) {
@@ -155,13 +157,13 @@ void run_compact_tile(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n
         ws.epoch = 1;
     }
     launch_k(compact_kernel<Flag, EmitTile, Fin>, dim3(unsigned(ntiles)), dim3(kScanThreads), 0, s, n_dev, n_host, flag,
-             emit_tile, fin, ws.tiles.ptr, ws.epoch);
+             emit_tile, fin, ws.tiles.ptr, ws.epoch, stamp);
 }
 
 template <class Flag, class Emit, class Fin>
 void run_compact(cudaStream_t s, ScanWorkspace& ws, const ull* n_dev, ull n_host, ull n_bound, Flag flag, Emit emit,
-                 Fin fin) {
-    run_compact_tile(s, ws, n_dev, n_host, n_bound, flag, PerItemEmit<Emit>{emit}, fin);
+                 Fin fin, ull* stamp = nullptr) {
+    run_compact_tile(s, ws, n_dev, n_host, n_bound, flag, PerItemEmit<Emit>{emit}, fin, stamp);
 }
 
 struct NoFin {
