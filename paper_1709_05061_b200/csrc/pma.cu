@@ -73,6 +73,13 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     if (const char* e = std::getenv("GPMA_NO_GRAPHS")) small_graphs_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_BUCKETS")) buckets_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_PDL")) pdl_ = e[0] == '0';
+    static const bool early = [] {  // (this TU's kernels; measured slower at B = 1000)
+        const char* e = std::getenv("GPMA_PDL_EARLY");
+        const int v = (e && *e) ? std::atoi(e) : 0;
+        if (v) GPMA_CUDA(cudaMemcpyToSymbol(g_pdl_early, &v, sizeof(int)));
+        return v != 0;
+    }();
+    (void)early;
     if (const char* e = std::getenv("GPMA_NO_POLL")) small_poll_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_NO_DIRECT_TOUCHED")) direct_touched_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
@@ -2526,13 +2533,6 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
     (void)attr;
     if (!h_desc_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_desc_dev_), h_desc_, 0));
     if (!h_ctr_dev_) GPMA_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_ctr_dev_), h_ctr, 0));
-    static const bool early = [] {
-        const char* e = std::getenv("GPMA_PDL_EARLY");
-        const int v = (e && *e) ? std::atoi(e) : 0;  // measured: early triggers cost ~3 us at B = 1000
-        GPMA_CUDA(cudaMemcpyToSymbol(g_pdl_early, &v, sizeof(int)));
-        return v != 0;
-    }();
-    (void)early;
     u64 dummy = 0;
     cudaGraph_t graph = nullptr;
     GPMA_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
