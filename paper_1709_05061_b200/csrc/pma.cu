@@ -81,6 +81,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     }();
     (void)early;
     if (const char* e = std::getenv("GPMA_NO_POLL")) small_poll_ = e[0] == '0';
+    if (const char* e = std::getenv("GPMA_SMALL_ONECTA")) small_onecta_ = std::strtoull(e, nullptr, 10);
     if (const char* e = std::getenv("GPMA_NO_DIRECT_TOUCHED")) direct_touched_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -94,7 +95,8 @@ Pma::~Pma() {
     free_arrays();
     if (d_ctr) cudaFree(d_ctr);
     if (h_ctr) cudaFreeHost(h_ctr);
-    if (small_exec_) cudaGraphExecDestroy(small_exec_);
+    for (auto& x : small_exec_)
+        if (x) cudaGraphExecDestroy(x);
     if (h_desc_) cudaFreeHost(h_desc_);
     if (d_desc_) cudaFree(d_desc_);
     for (auto& e : ev_)
@@ -593,80 +595,21 @@ __device__ __forceinline__ void sort_block(u64* buf, u64* xb, u32 t, u32 A, u32 
     }
 }
 
-// Whole front end of a captured small batch in ONE CTA (n <= kSmallFrontMax):
-// zero the counters and the graph's look-back words, read the descriptor
-// straight from page-locked host memory, pack + check every update
-// (prep_code), sort the packed words (sort_block), then resolve duplicates
-// and compact the unique updates with a CTA-wide scan — the same output as
-// k_prep_graph, the radix sort and the duplicate-resolution compaction of the
-// general path, without their launches and the look-back between CTAs.
 constexpr int kSmallFrontThreads = 1024;
 constexpr int kSmallFrontItems = 4;
 constexpr u32 kSmallFrontMax = kSmallFrontThreads * kSmallFrontItems;
 constexpr int kSmallFrontSmem = 2 * kSmallFrontMax * 8;  // double-buffered exchange
 
-__global__ void __launch_bounds__(kSmallFrontThreads, 1)
-    k_small_front(const GraphFront* __restrict__ hf, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
-                  u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
-    extern __shared__ u64 sbuf[];  // [2][kSmallFrontMax]
-    __shared__ u64 s_desc[(sizeof(GraphFront) + 7) / 8];
-    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
-    __shared__ ull s_acc[4];
+// Duplicate resolution of a small batch's sorted words ck[0, n) by one CTA of
+// kSmallFrontThreads (segment_engine.hpp:346-363): the last word of each
+// equal-key run survives; a delete there takes the run's last insert.  Thread
+// t owns the contiguous items [4t, 4t + 4) for the ordered scan; thread 0
+// publishes the front end's counters (s_acc: guard deletes, first bad insert,
+// out-of-layout delete).
+__device__ __forceinline__ void small_resolve(const u64* ck, u32 n, const GraphFront& f, int db, int ib, Ctr* ctr,
+                                              const ull* s_acc, u64 gt0, u32* s_wsum, u64* __restrict__ o_k,
+                                              u64* __restrict__ o_v, u8* __restrict__ o_o) {
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    u64 gt0;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
-    pdl_enter();  // (the chain's head: launched without the attribute, lets the leaf search be scheduled early)
-    // descriptor: one word per thread over PCIe; counters + look-back words zeroed
-    if (t < (sizeof(GraphFront) + 7) / 8) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
-    for (u32 i = t; i < sizeof(Ctr) / 8; i += kSmallFrontThreads) reinterpret_cast<ull*>(ctr)[i] = 0;
-    for (u64 i = t; i < ws_words; i += kSmallFrontThreads) ws_tiles[i] = 0;
-    if (t < 4) s_acc[t] = 0;
-    __syncthreads();
-    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
-    const u32 n = u32(f.ni + f.nd);
-    u32 P = 32;
-    while (P < n) P <<= 1;
-    // pack: item e of thread t is element t + e * 1024 (coalesced reads); the
-    // words go to shared memory, ~0 pads up to P
-    PrepAcc acc;
-#pragma unroll
-    for (int e = 0; e < kSmallFrontItems; ++e) {
-        const u32 i = t + u32(e) * kSmallFrontThreads;
-        if (i < n) {
-            const bool ins = i < f.ni;
-            const u32 s = ins ? f.is[i] : f.ds[i - f.ni];
-            const u32 d = ins ? f.id[i] : f.dd[i - f.ni];
-            int cls;
-            sbuf[i] = pack_word(f, ib, prep_code(f, db, s, d, i, ins, acc, cls), i, ins);
-        } else if (i < P) {
-            sbuf[i] = ~0ull;
-        }
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
-        acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
-        acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
-    }
-    if (lane == 0) {
-        if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
-        if (acc.bad) atomicMax(&s_acc[1], acc.bad);
-        if (acc.oor) atomicOr(&s_acc[2], 1ull);
-    }
-    __syncthreads();
-    // only P / E threads sort (idle warps would take issue slots every stage)
-    if (P <= kSmallFrontThreads) {
-        if (t < P) sort_block<1>(sbuf, sbuf + kSmallFrontMax, t, P, P);
-    } else if (P == 2 * kSmallFrontThreads) {
-        sort_block<2>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
-    } else {
-        sort_block<4>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
-    }
-    __syncthreads();
-    // duplicate resolution (segment_engine.hpp:346-363): the last word of each
-    // equal-key run survives; a delete there takes the run's last insert.
-    // Thread t owns the contiguous items [4t, 4t + 4) for the ordered scan.
-    const u64* ck = sbuf;
     const u64 pmask = (1ull << ib) - 1;
     const u64 skipkey = 1ull << (2 * db);
     unsigned fm = 0;
@@ -732,6 +675,231 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
         ctr->n_unique = total;
         ctr->np[0] = (s_acc[1] || s_acc[2]) ? 0ull : total;
     }
+}
+
+// Whole front end of a captured small batch in ONE CTA (n <= kSmallFrontMax):
+// zero the counters and the graph's look-back words, read the descriptor
+// straight from page-locked host memory, pack + check every update
+// (prep_code), sort the packed words (sort_block), then resolve duplicates
+// and compact the unique updates with a CTA-wide scan — the same output as
+// k_prep_graph, the radix sort and the duplicate-resolution compaction of the
+// general path, without their launches and the look-back between CTAs.
+
+__global__ void __launch_bounds__(kSmallFrontThreads, 1)
+    k_small_front(const GraphFront* __restrict__ hf, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
+                  u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
+    extern __shared__ u64 sbuf[];  // [2][kSmallFrontMax]
+    __shared__ u64 s_desc[(sizeof(GraphFront) + 7) / 8];
+    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
+    __shared__ ull s_acc[4];
+    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    u64 gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    pdl_enter();  // (the chain's head: launched without the attribute, lets the leaf search be scheduled early)
+    // descriptor: one word per thread over PCIe; counters + look-back words zeroed
+    if (t < (sizeof(GraphFront) + 7) / 8) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
+    for (u32 i = t; i < sizeof(Ctr) / 8; i += kSmallFrontThreads) reinterpret_cast<ull*>(ctr)[i] = 0;
+    for (u64 i = t; i < ws_words; i += kSmallFrontThreads) ws_tiles[i] = 0;
+    if (t < 4) s_acc[t] = 0;
+    __syncthreads();
+    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
+    const u32 n = u32(f.ni + f.nd);
+    u32 P = 32;
+    while (P < n) P <<= 1;
+    // pack: item e of thread t is element t + e * 1024 (coalesced reads); the
+    // words go to shared memory, ~0 pads up to P
+    PrepAcc acc;
+#pragma unroll
+    for (int e = 0; e < kSmallFrontItems; ++e) {
+        const u32 i = t + u32(e) * kSmallFrontThreads;
+        if (i < n) {
+            const bool ins = i < f.ni;
+            const u32 s = ins ? f.is[i] : f.ds[i - f.ni];
+            const u32 d = ins ? f.id[i] : f.dd[i - f.ni];
+            int cls;
+            sbuf[i] = pack_word(f, ib, prep_code(f, db, s, d, i, ins, acc, cls), i, ins);
+        } else if (i < P) {
+            sbuf[i] = ~0ull;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
+        acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
+        acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
+    }
+    if (lane == 0) {
+        if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
+        if (acc.bad) atomicMax(&s_acc[1], acc.bad);
+        if (acc.oor) atomicOr(&s_acc[2], 1ull);
+    }
+    __syncthreads();
+    // only P / E threads sort (idle warps would take issue slots every stage)
+    if (P <= kSmallFrontThreads) {
+        if (t < P) sort_block<1>(sbuf, sbuf + kSmallFrontMax, t, P, P);
+    } else if (P == 2 * kSmallFrontThreads) {
+        sort_block<2>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
+    } else {
+        sort_block<4>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
+    }
+    __syncthreads();
+    small_resolve(sbuf, n, f, db, ib, ctr, s_acc, gt0, s_wsum, o_k, o_v, o_o);
+}
+
+// The same front end over several SMs for small batches of more than
+// kSmallOneCta updates, where the one-CTA sort is issue-bound (a CTA's
+// shuffles and shared-memory bisections at 2048 - 4096 words cost more than
+// the two extra launches):
+//   k_small_chunks       a CTA per 256-update chunk: pack + checks, sort in
+//                        shared memory, sorted chunk + check partials to sb;
+//   k_small_merge_ranks  a CTA per chunk: each word's place in the merged
+//                        order = its index in its chunk + the words below it
+//                        in every other chunk (a bisection per chunk, equal
+//                        words ordered by chunk), scattered to sb;
+//   k_small_resolve      one CTA: duplicate resolution of the merged words
+//                        (small_resolve, as in k_small_front).
+// Scratch sb (u64 words): [0, 4096) sorted chunks, [4096, 8192) merged,
+// then 4 words per chunk (guard deletes, first bad insert, out-of-layout,
+// chunk 0: its %globaltimer entry stamp), the descriptor and its ready flag.
+// Only chunk 0 reads the descriptor over PCIe (concurrent reads of the same
+// host lines from 16 SMs serialise: ~14 µs for the last one); the other
+// chunks wait for its device copy — they never wait on a later CTA, the
+// order the look-back scans rely on too — and k_small_resolve clears the flag.
+constexpr u32 kChunk = 256;
+constexpr u32 kChunks = kSmallFrontMax / kChunk;
+constexpr u32 kSbMerged = kSmallFrontMax;
+constexpr u32 kSbPart = 2 * kSmallFrontMax;
+constexpr u32 kSbDesc = kSbPart + 4 * kChunks;
+constexpr u32 kDescWords = (sizeof(GraphFront) + 7) / 8;
+constexpr u32 kSbFlag = kSbDesc + kDescWords;
+constexpr u32 kSbWords = kSbFlag + 1;
+static_assert(kDescWords <= 32, "descriptor copied by one warp");
+
+__global__ void __launch_bounds__(kChunk) k_small_chunks(const GraphFront* __restrict__ hf, int db, int ib,
+                                                         u64* __restrict__ sb) {
+    __shared__ u64 s[2 * kChunk];
+    __shared__ u64 s_desc[kDescWords];
+    __shared__ ull s_acc[3];
+    const u32 t = threadIdx.x, lane = t & 31, c = blockIdx.x;
+    u64 gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    pdl_enter();
+    if (t < 3) s_acc[t] = 0;
+    if (c == 0) {
+        if (t < kDescWords) sb[kSbDesc + t] = s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
+        __syncthreads();
+        if (t == 0) {
+            __threadfence();
+            st_volatile(reinterpret_cast<ull*>(sb + kSbFlag), 1ull);
+        }
+    } else {
+        if (t == 0)
+            while (ld_volatile(reinterpret_cast<const ull*>(sb + kSbFlag)) == 0) {
+            }
+        __syncthreads();
+        if (t < kDescWords) s_desc[t] = ld_volatile(reinterpret_cast<const ull*>(sb + kSbDesc + t));
+        __syncthreads();
+    }
+    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
+    const u32 n = u32(f.ni + f.nd), i = c * kChunk + t;
+    if (c * kChunk >= n) return;  // (uniform over the CTA)
+    PrepAcc acc;
+    u64 w = ~0ull;  // pads sort last
+    if (i < n) {
+        const bool ins = i < f.ni;
+        const u32 su = ins ? f.is[i] : f.ds[i - f.ni];
+        const u32 dv = ins ? f.id[i] : f.dd[i - f.ni];
+        int cls;
+        w = pack_word(f, ib, prep_code(f, db, su, dv, i, ins, acc, cls), i, ins);
+    }
+    s[t] = w;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
+        acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
+        acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
+    }
+    if (lane == 0) {
+        if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
+        if (acc.bad) atomicMax(&s_acc[1], acc.bad);
+        if (acc.oor) atomicOr(&s_acc[2], 1ull);
+    }
+    __syncthreads();
+    sort_block<1>(s, s + kChunk, t, kChunk, kChunk);
+    __syncthreads();
+    sb[i] = s[t];
+    if (t < 3) sb[kSbPart + 4 * c + t] = s_acc[t];
+    if (c == 0 && t == 3) sb[kSbPart + 3] = gt0;
+}
+
+__global__ void __launch_bounds__(kChunk) k_small_merge_ranks(u64* __restrict__ sb) {
+    __shared__ u64 s[kSmallFrontMax];
+    pdl_enter();
+    const GraphFront* f = reinterpret_cast<const GraphFront*>(sb + kSbDesc);
+    const u32 n = u32(f->ni + f->nd), nch = (n + kChunk - 1) / kChunk, c = blockIdx.x, t = threadIdx.x;
+    if (c >= nch) return;
+    for (u32 i = t; i < nch * kChunk; i += kChunk) s[i] = sb[i];
+    __syncthreads();
+    if (c * kChunk + t >= n) return;  // a pad
+    const u64 x = s[c * kChunk + t];
+    u32 r = t;
+#pragma unroll
+    for (u32 q = 0; q < kChunks; ++q) {
+        if (q < nch && q != c) {  // (independent bisections: the loads overlap)
+            const u64* run = s + q * kChunk;
+            const bool le = q < c;
+            u32 lo = 0;
+#pragma unroll
+            for (u32 step = kChunk / 2; step > 0; step >>= 1) {
+                const u64 y = run[lo + step - 1];
+                if (le ? y <= x : y < x) lo += step;
+            }
+            const u64 y = run[lo];
+            if (le ? y <= x : y < x) ++lo;
+            r += lo;
+        }
+    }
+    sb[kSbMerged + r] = x;
+}
+
+__global__ void __launch_bounds__(kSmallFrontThreads, 1)
+    k_small_resolve(u64* __restrict__ sb, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
+                    u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
+    __shared__ u64 sbuf[kSmallFrontMax];
+    __shared__ u64 s_desc[kDescWords];
+    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
+    __shared__ ull s_acc[3];
+    const u32 t = threadIdx.x;
+    pdl_enter();
+    if (t < kDescWords) s_desc[t] = sb[kSbDesc + t];
+    if (t == 32) sb[kSbFlag] = 0;  // (every chunk CTA has finished)
+    for (u32 i = t; i < sizeof(Ctr) / 8; i += kSmallFrontThreads) reinterpret_cast<ull*>(ctr)[i] = 0;
+    for (u64 i = t; i < ws_words; i += kSmallFrontThreads) ws_tiles[i] = 0;
+    __syncthreads();
+    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
+    const u32 n = u32(f.ni + f.nd), nch = (n + kChunk - 1) / kChunk;
+    for (u32 i = t; i < n; i += kSmallFrontThreads) sbuf[i] = sb[kSbMerged + i];
+    if (t < 32) {
+        ull g = 0, b = 0, o = 0;
+        if (t < nch) {
+            g = sb[kSbPart + 4 * t];
+            b = sb[kSbPart + 4 * t + 1];
+            o = sb[kSbPart + 4 * t + 2];
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            g += __shfl_xor_sync(FULL, g, d);
+            b = max(b, __shfl_xor_sync(FULL, b, d));
+            o |= __shfl_xor_sync(FULL, o, d);
+        }
+        if (t == 0) {
+            s_acc[0] = g;
+            s_acc[1] = b;
+            s_acc[2] = o;
+        }
+    }
+    __syncthreads();
+    small_resolve(sbuf, n, f, db, ib, ctr, s_acc, sb[kSbPart + 3], s_wsum, o_k, o_v, o_o);
 }
 
 // Leaf of every unique update of a small batch (leaf_for_key), a warp per
@@ -2511,7 +2679,7 @@ std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int le
     const void* ptrs[] = {d_keys, d_vals, d_st, d_hdr, ro_base(), d_ctr, d_desc_, h_desc_, h_ctr, sk_in.ptr,
                           sk_out.ptr, uk.ptr, uv.ptr, uop.ptr, ul.ptr, pidx0.ptr, pidx1.ptr, gid.ptr, gstart.ptr,
                           gseg.ptr, gflag.ptr, touched.ptr, rlist.ptr, ik.ptr, iv.ptr, ir.ptr, biglist.ptr, ek.ptr,
-                          ev.ptr, es.ptr, mflag.ptr, ok.ptr, ov.ptr, small_ws_.tiles.ptr, stream_};
+                          ev.ptr, es.ptr, mflag.ptr, ok.ptr, ov.ptr, small_ws_.tiles.ptr, small_sb_.ptr, stream_};
     std::vector<uintptr_t> k;
     for (const void* p : ptrs) k.push_back(reinterpret_cast<uintptr_t>(p));
     const u64 vals[] = {cap_, leaf_, u64(height_), ro_lo, num_vertices, u64(db), u64(cfg.eager), cfg.small_max,
@@ -2520,10 +2688,11 @@ std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int le
     return k;
 }
 
-void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
-    if (small_exec_) {
-        GPMA_CUDA(cudaGraphExecDestroy(small_exec_));
-        small_exec_ = nullptr;
+void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels, int multi) {
+    cudaGraphExec_t& exec = small_exec_[multi];
+    if (exec) {
+        GPMA_CUDA(cudaGraphExecDestroy(exec));
+        exec = nullptr;
     }
     const int ib = kSmallIb;
     static const bool attr = [] {
@@ -2541,9 +2710,19 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         // descriptor read in place from page-locked memory), then the leaf of
         // every unique update (pma.hpp:234-289), a warp per key
         static_assert(kSmallGraphMax <= kSmallFrontMax, "small graph batches sort in one CTA");
-        k_small_front<<<1, kSmallFrontThreads, kSmallFrontSmem, stream_>>>(
-            h_desc_dev_, db, ib, d_ctr, small_ws_.tiles.ptr, small_ws_.tiles.cap, uk.ptr, uv.ptr, uop.ptr);
-        GPMA_LAUNCH_CHECK();
+        if (multi) {  // (more than small_onecta_ updates: chunks sorted on their own SMs, merged by rank)
+            k_small_chunks<<<kChunks, kChunk, 0, stream_>>>(h_desc_dev_, db, ib, small_sb_.ptr);
+            GPMA_LAUNCH_CHECK();
+            pdl_chain() = pdl_;
+            launch_k(k_small_merge_ranks, dim3(kChunks), dim3(kChunk), 0, stream_, small_sb_.ptr);
+            launch_k(k_small_resolve, dim3(1), dim3(kSmallFrontThreads), 0, stream_,
+                     small_sb_.ptr, db, ib, d_ctr, small_ws_.tiles.ptr,
+                     u64(small_ws_.tiles.cap), uk.ptr, uv.ptr, uop.ptr);
+        } else {
+            k_small_front<<<1, kSmallFrontThreads, kSmallFrontSmem, stream_>>>(
+                h_desc_dev_, db, ib, d_ctr, small_ws_.tiles.ptr, small_ws_.tiles.cap, uk.ptr, uv.ptr, uop.ptr);
+            GPMA_LAUNCH_CHECK();
+        }
         // the rest of the chain: programmatic edges (GPMA_NO_PDL=1: ordinary ones)
         pdl_chain() = pdl_;
         launch_k(k_leaf_search_warp, dim3(kSmallGraphMax / 8), dim3(256), 0, stream_, uk.ptr, &d_ctr->n_unique, d_hdr,
@@ -2571,7 +2750,7 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels) {
         throw;
     }
     GPMA_CUDA(cudaStreamEndCapture(stream_, &graph));
-    const cudaError_t e = cudaGraphInstantiate(&small_exec_, graph, 0);
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     GPMA_CUDA(e);
 }
@@ -2580,21 +2759,24 @@ int Pma::run_small_graph(const GraphFront& gf, const EngineCfg& cfg) {
     int db = 1;
     while (db < 32 && (1ull << db) < gf.nv) ++db;
     const int levels = std::min(kSmallGraphLevels, height_);
+    const int multi = gf.ni + gf.nd > small_onecta_ ? 1 : 0;
+    small_sb_.reserve(kSbWords);  // (both variants' keys name it)
     auto key = small_graph_key(db, cfg, levels);
-    if (!small_exec_ || key != small_key_) {
+    if (!small_exec_[multi] || key != small_key_[multi]) {
         // every buffer the nodes touch, at its final size, before capture
         reserve_batch(kSmallGraphMax);
         small_ws_.tiles.reserve(64);
         small_ws_.epoch = 0;
         key = small_graph_key(db, cfg, levels);
-        capture_small_graph(db, cfg, levels);
-        small_key_ = key;
+        GPMA_CUDA(cudaMemsetAsync(small_sb_.ptr + kSbFlag, 0, 8, stream_));
+        capture_small_graph(db, cfg, levels, multi);
+        small_key_[multi] = key;
     }
     // read by the graph's first node (the previous replay is past it: its
     // done_seq is written at the very end of the graph)
     *h_desc_ = gf;
     h_desc_->seq = ++small_seq_;
-    GPMA_CUDA(cudaGraphLaunch(small_exec_, stream_));
+    GPMA_CUDA(cudaGraphLaunch(small_exec_[multi], stream_));
     if (small_poll_) {
         // the last refresh CTA writes the counters, then done_seq, to
         // page-locked memory after every other kernel of the batch finished:

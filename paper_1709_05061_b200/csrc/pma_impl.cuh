@@ -169,7 +169,7 @@ public:
     static constexpr int kSmallGraphLevels = 1;  // most small batches finish in round 0; more rounds: host loop
     bool small_graph_ok(u64 n, const GraphFront& gf) const;
     std::vector<uintptr_t> small_graph_key(int db, const EngineCfg& cfg, int levels) const;
-    void capture_small_graph(int db, const EngineCfg& cfg, int levels);
+    void capture_small_graph(int db, const EngineCfg& cfg, int levels, int multi);
     int run_small_graph(const GraphFront& gf, const EngineCfg& cfg);
     void enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
                        ScanWorkspace& ws, bool events, u64& launches);
@@ -301,8 +301,10 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     RadixWorkspace rws;           // onesweep radix sort (radix.cuh)
     // small graph batches
     bool small_graphs_ = true;          // GPMA_NO_GRAPHS=1 disables (A/B measurements)
-    cudaGraphExec_t small_exec_ = nullptr;
-    std::vector<uintptr_t> small_key_;  // what the captured graph embeds
+    cudaGraphExec_t small_exec_[2] = {nullptr, nullptr};  // [one-CTA front end, multi-CTA front end]
+    std::vector<uintptr_t> small_key_[2];  // what each captured graph embeds
+    u64 small_onecta_ = 1024;           // larger small batches: the multi-CTA front end (GPMA_SMALL_ONECTA=n)
+    DevBuf<u64> small_sb_;              // its scratch (k_small_chunks)
     GraphFront* h_desc_ = nullptr;      // page-locked batch descriptor (copied by the graph's first node)
     GraphFront* d_desc_ = nullptr;
     GraphFront* h_desc_dev_ = nullptr;  // device view of h_desc_ (read in place by the small graph)

@@ -473,6 +473,61 @@ def test_small_batch_sort_size_regimes(mode):
         assert (g.row_offsets() == r.row_offsets()).all(), ctx
 
 
+@pytest.mark.parametrize("onecta", ["0", "1024", "4096"])
+def test_small_batch_front_end_variants(onecta, monkeypatch):
+    """The captured small-batch graph's two front ends — one CTA
+    (k_small_front) and chunks on separate SMs merged by rank
+    (k_small_chunks / k_small_merge_ranks / k_small_resolve) — forced per
+    batch size by GPMA_SMALL_ONECTA: the same words with the same
+    duplicates spread over different chunks (repeated inserts, a key deleted
+    twice, insert + delete of one key), guard deletes, deletes outside the
+    layout (redone on the generic path) and the first of two bad inserts
+    reported; slots, stats and row offsets bit-exact."""
+    monkeypatch.setenv("GPMA_SMALL_ONECTA", onecta)
+    rng = np.random.default_rng(int(onecta) + 5)
+    nv = 1 << 14
+    stream = RefStream.rmat(nv, 200000, 13)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half])
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config())
+    ps, pd = s[:half].astype(np.uint32), d[:half].astype(np.uint32)
+    for n in (100, 700, 1025, 1500, 2500, 4096):
+        nd = n // 3
+        ni = n - nd
+        a = rng.integers(0, nv, ni).astype(np.uint32)
+        b = rng.integers(0, nv, ni).astype(np.uint32)
+        for j in (1, ni // 2, ni - 1):  # one key inserted three times, in different chunks
+            a[j], b[j] = a[0], b[0]
+        pick = rng.integers(0, len(ps), nd)
+        c, dd = ps[pick].copy(), pd[pick].copy()
+        c[nd - 1], dd[nd - 1] = c[0], dd[0]  # a present key deleted twice
+        c[nd // 2], dd[nd // 2] = a[0], b[0]  # the inserted key deleted too
+        c[1], dd[1] = 7, 0xFFFFFFFF  # a guard delete
+        ww = rng.random(ni) + 0.5
+        gs = g.apply_batch(a, b, ww, c, dd)
+        rs = r.apply_batch(a, b, ww, c, dd)
+        ctx = f"n={n} onecta={onecta}"
+        assert gs.parity() == ref_parity(r, rs), ctx
+        assert_same_slots(g.pma().slots(), r.slots(), ctx)
+        assert (g.row_offsets() == r.row_offsets()).all(), ctx
+    # deletes outside the |V|-derived layout: the batch is redone on the generic path
+    c2 = np.concatenate([ps[:1800], [2**20]]).astype(np.uint32)
+    d2 = np.concatenate([pd[:1800], [3]]).astype(np.uint32)
+    a2, b2 = rng.integers(0, nv, 900), rng.integers(0, nv, 900)
+    gs = g.apply_batch(a2, b2, None, c2, d2)
+    rs = r.apply_batch(a2, b2, None, c2, d2)
+    assert gs.parity() == ref_parity(r, rs)
+    assert_same_slots(g.pma().slots(), r.slots(), "out-of-layout deletes")
+    # two bad inserts in different chunks: the first is reported, nothing changes
+    before = g.pma().slots()
+    a3 = rng.integers(0, nv, 3000)
+    a3[1700], a3[2900] = nv + 3, nv + 9
+    with pytest.raises(ValueError, match=rf"edge \({nv + 3}, \d+\) outside vertex range {nv}"):
+        g.apply_batch(a3, rng.integers(0, nv, 3000), None, [], [])
+    assert all((x == y).all() for x, y in zip(before, g.pma().slots()))
+
+
 @pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
 def test_mixed_batch_sizes_through_growth_and_shrink(mode):
     """Small (captured-graph) and large (host-loop) batches interleaved on one

@@ -59,6 +59,8 @@ int main(int argc, char** argv) {
         std::printf("B=%zu: C ABI wall per batch median %.1f us, p10 %.1f, p90 %.1f (device %.1f us, %llu updates)\n", B,
                     us[us.size() / 2], us[us.size() / 10], us[us.size() * 9 / 10], tm.device_ms * 1e3,
                     (unsigned long long)ps.batch_size);
+        std::printf("  last call: sort %.1f us, search %.1f, rounds %.1f, refresh %.1f\n", tm.sort_ms * 1e3,
+                    tm.search_ms * 1e3, tm.rounds_ms * 1e3, tm.refresh_ms * 1e3);
         gpma_destroy(g);
         gpma_window_destroy(w);
     }
