@@ -23,6 +23,8 @@
 #include <atomic>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "block_ops.cuh"
 #include "merge.cuh"
 #include "pma_impl.cuh"
@@ -82,6 +84,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     (void)early;
     if (const char* e = std::getenv("GPMA_NO_POLL")) small_poll_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_SMALL_ONECTA")) small_onecta_ = std::strtoull(e, nullptr, 10);
+    if (const char* e = std::getenv("GPMA_SMALL_CLUSTER")) small_cluster_ = e[0] != '0';
     if (const char* e = std::getenv("GPMA_NO_DIRECT_TOUCHED")) direct_touched_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -692,7 +695,7 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     __shared__ u64 s_desc[(sizeof(GraphFront) + 7) / 8];
     __shared__ u32 s_wsum[kSmallFrontThreads / 32];
     __shared__ ull s_acc[4];
-    const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const u32 t = threadIdx.x, lane = t & 31;
     u64 gt0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     pdl_enter();  // (the chain's head: launched without the attribute, lets the leaf search be scheduled early)
@@ -747,144 +750,164 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
 }
 
 // The same front end over several SMs for small batches of more than
-// kSmallOneCta updates, where the one-CTA sort is issue-bound (a CTA's
-// shuffles and shared-memory bisections at 2048 - 4096 words cost more than
-// the two extra launches):
-//   k_small_chunks       a CTA per 256-update chunk: pack + checks, sort in
-//                        shared memory, sorted chunk + check partials to sb;
-//   k_small_merge_ranks  a CTA per chunk: each word's place in the merged
-//                        order = its index in its chunk + the words below it
-//                        in every other chunk (a bisection per chunk, equal
-//                        words ordered by chunk), scattered to sb;
-//   k_small_resolve      one CTA: duplicate resolution of the merged words
-//                        (small_resolve, as in k_small_front).
-// Scratch sb (u64 words): [0, 4096) sorted chunks, [4096, 8192) merged,
-// then 4 words per chunk (guard deletes, first bad insert, out-of-layout,
-// chunk 0: its %globaltimer entry stamp), the descriptor and its ready flag.
-// Only chunk 0 reads the descriptor over PCIe (concurrent reads of the same
-// host lines from 16 SMs serialise: ~14 µs for the last one); the other
-// chunks wait for its device copy — they never wait on a later CTA, the
-// order the look-back scans rely on too — and k_small_resolve clears the flag.
+// small_onecta_ updates, where the one-CTA sort is issue-bound (a CTA's
+// shuffles and shared-memory bisections at 1024 - 4096 words cost more than
+// spreading the work):
+//   1. a CTA per 256-update chunk: pack + checks, sort in shared memory;
+//   2. merge by rank, in every chunk's CTA: each word's place in the merged
+//      order = its index in its chunk + the words below it in every other
+//      chunk (a bisection per chunk, equal words ordered by chunk; 4 threads
+//      per word, a quarter of the other chunks each), scattered;
+//   3. CTA 0: duplicate resolution of the merged words (small_resolve, as in
+//      k_small_front); its spare threads clear the counters during 1.
+// k_small_front_cluster runs the three stages in one 16-CTA cluster through
+// distributed shared memory; k_small_front_grid (where such a cluster cannot
+// be resident) in a cooperative grid through L2 scratch sb (u64 words):
+// [0, 4096) sorted chunks, [4096, 8192) merged, then 4 words per chunk
+// (guard deletes, first bad insert, out-of-layout), the descriptor, its ready
+// flag and two grid-barrier counters.  Only chunk 0 reads the descriptor over
+// PCIe (concurrent reads of the same host lines from 16 SMs serialise: ~14 µs
+// for the last one); the other chunks wait for its device copy.
 constexpr u32 kChunk = 256;
 constexpr u32 kChunks = kSmallFrontMax / kChunk;
 constexpr u32 kSbMerged = kSmallFrontMax;
 constexpr u32 kSbPart = 2 * kSmallFrontMax;
 constexpr u32 kSbDesc = kSbPart + 4 * kChunks;
 constexpr u32 kDescWords = (sizeof(GraphFront) + 7) / 8;
-constexpr u32 kSbFlag = kSbDesc + kDescWords;
-constexpr u32 kSbWords = kSbFlag + 1;
+constexpr u32 kSbFlag = kSbDesc + kDescWords;  // + two grid-barrier counters (k_small_front_grid)
+constexpr u32 kSbWords = kSbFlag + 3;
 static_assert(kDescWords <= 32, "descriptor copied by one warp");
 
-__global__ void __launch_bounds__(kChunk) k_small_chunks(const GraphFront* __restrict__ hf, int db, int ib,
-                                                         u64* __restrict__ sb) {
-    __shared__ u64 s[2 * kChunk];
+// Cooperative grid: grid barrier after the chunk sort, CTA 0 waits for every
+// chunk's scatter, then resets the flag and both counters.
+__global__ void __launch_bounds__(kSmallFrontThreads, 1)
+    k_small_front_grid(const GraphFront* __restrict__ hf, int db, int ib, u64* __restrict__ sb, Ctr* ctr,
+                       ull* ws_tiles, u64 ws_words, u64* __restrict__ o_k, u64* __restrict__ o_v,
+                       u8* __restrict__ o_o) {
+    __shared__ u64 s[kSmallFrontMax];
     __shared__ u64 s_desc[kDescWords];
-    __shared__ ull s_acc[3];
+    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
+    __shared__ u32 s_rank[kChunk];
+    __shared__ ull s_acc[3], s_tot[3];
     const u32 t = threadIdx.x, lane = t & 31, c = blockIdx.x;
+    ull* flag = reinterpret_cast<ull*>(sb + kSbFlag);
+    ull* cnt1 = flag + 1;
+    ull* cnt2 = flag + 2;
     u64 gt0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     pdl_enter();
     if (t < 3) s_acc[t] = 0;
+    if (t < kChunk) s_rank[t] = 0;
     if (c == 0) {
         if (t < kDescWords) sb[kSbDesc + t] = s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
         __syncthreads();
         if (t == 0) {
             __threadfence();
-            st_volatile(reinterpret_cast<ull*>(sb + kSbFlag), 1ull);
+            st_volatile(flag, 1ull);
         }
     } else {
         if (t == 0)
-            while (ld_volatile(reinterpret_cast<const ull*>(sb + kSbFlag)) == 0) {
+            while (ld_volatile(flag) == 0) {
             }
         __syncthreads();
         if (t < kDescWords) s_desc[t] = ld_volatile(reinterpret_cast<const ull*>(sb + kSbDesc + t));
-        __syncthreads();
     }
-    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
-    const u32 n = u32(f.ni + f.nd), i = c * kChunk + t;
-    if (c * kChunk >= n) return;  // (uniform over the CTA)
-    PrepAcc acc;
-    u64 w = ~0ull;  // pads sort last
-    if (i < n) {
-        const bool ins = i < f.ni;
-        const u32 su = ins ? f.is[i] : f.ds[i - f.ni];
-        const u32 dv = ins ? f.id[i] : f.dd[i - f.ni];
-        int cls;
-        w = pack_word(f, ib, prep_code(f, db, su, dv, i, ins, acc, cls), i, ins);
-    }
-    s[t] = w;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-        acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
-        acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
-        acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
-    }
-    if (lane == 0) {
-        if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
-        if (acc.bad) atomicMax(&s_acc[1], acc.bad);
-        if (acc.oor) atomicOr(&s_acc[2], 1ull);
-    }
-    __syncthreads();
-    sort_block<1>(s, s + kChunk, t, kChunk, kChunk);
-    __syncthreads();
-    sb[i] = s[t];
-    if (t < 3) sb[kSbPart + 4 * c + t] = s_acc[t];
-    if (c == 0 && t == 3) sb[kSbPart + 3] = gt0;
-}
-
-__global__ void __launch_bounds__(kChunk) k_small_merge_ranks(u64* __restrict__ sb) {
-    __shared__ u64 s[kSmallFrontMax];
-    pdl_enter();
-    const GraphFront* f = reinterpret_cast<const GraphFront*>(sb + kSbDesc);
-    const u32 n = u32(f->ni + f->nd), nch = (n + kChunk - 1) / kChunk, c = blockIdx.x, t = threadIdx.x;
-    if (c >= nch) return;
-    for (u32 i = t; i < nch * kChunk; i += kChunk) s[i] = sb[i];
-    __syncthreads();
-    if (c * kChunk + t >= n) return;  // a pad
-    const u64 x = s[c * kChunk + t];
-    u32 r = t;
-#pragma unroll
-    for (u32 q = 0; q < kChunks; ++q) {
-        if (q < nch && q != c) {  // (independent bisections: the loads overlap)
-            const u64* run = s + q * kChunk;
-            const bool le = q < c;
-            u32 lo = 0;
-#pragma unroll
-            for (u32 step = kChunk / 2; step > 0; step >>= 1) {
-                const u64 y = run[lo + step - 1];
-                if (le ? y <= x : y < x) lo += step;
-            }
-            const u64 y = run[lo];
-            if (le ? y <= x : y < x) ++lo;
-            r += lo;
-        }
-    }
-    sb[kSbMerged + r] = x;
-}
-
-__global__ void __launch_bounds__(kSmallFrontThreads, 1)
-    k_small_resolve(u64* __restrict__ sb, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
-                    u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
-    __shared__ u64 sbuf[kSmallFrontMax];
-    __shared__ u64 s_desc[kDescWords];
-    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
-    __shared__ ull s_acc[3];
-    const u32 t = threadIdx.x;
-    pdl_enter();
-    if (t < kDescWords) s_desc[t] = sb[kSbDesc + t];
-    if (t == 32) sb[kSbFlag] = 0;  // (every chunk CTA has finished)
-    for (u32 i = t; i < sizeof(Ctr) / 8; i += kSmallFrontThreads) reinterpret_cast<ull*>(ctr)[i] = 0;
-    for (u64 i = t; i < ws_words; i += kSmallFrontThreads) ws_tiles[i] = 0;
     __syncthreads();
     const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
     const u32 n = u32(f.ni + f.nd), nch = (n + kChunk - 1) / kChunk;
-    for (u32 i = t; i < n; i += kSmallFrontThreads) sbuf[i] = sb[kSbMerged + i];
+    if (c >= nch) return;  // (uniform over the CTA; never waited for)
+    if (t < kChunk) {
+        const u32 i = c * kChunk + t;
+        PrepAcc acc;
+        u64 w = ~0ull;  // pads sort last
+        if (i < n) {
+            const bool ins = i < f.ni;
+            const u32 su = ins ? f.is[i] : f.ds[i - f.ni];
+            const u32 dv = ins ? f.id[i] : f.dd[i - f.ni];
+            int cls;
+            w = pack_word(f, ib, prep_code(f, db, su, dv, i, ins, acc, cls), i, ins);
+        }
+        s[t] = w;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
+            acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
+            acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
+        }
+        if (lane == 0) {
+            if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
+            if (acc.bad) atomicMax(&s_acc[1], acc.bad);
+            if (acc.oor) atomicOr(&s_acc[2], 1ull);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kChunk) : "memory");
+        sort_block<1>(s, s + kChunk, t, kChunk, kChunk);
+        sb[i] = s[t];
+        if (t < 3) sb[kSbPart + 4 * c + t] = s_acc[t];
+    } else if (c == 0) {  // CTA 0's other threads: counters and look-back words
+        for (u32 i = t - kChunk; i < sizeof(Ctr) / 8; i += kSmallFrontThreads - kChunk)
+            reinterpret_cast<ull*>(ctr)[i] = 0;
+        for (u64 i = t - kChunk; i < ws_words; i += kSmallFrontThreads - kChunk) ws_tiles[i] = 0;
+    }
+    __syncthreads();
+    if (t == 0) {  // grid barrier: every chunk sorted
+        __threadfence();
+        atomicAdd(cnt1, 1ull);
+        while (ld_volatile(cnt1) < nch) {
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    for (u32 i = t; i < nch * kChunk; i += kSmallFrontThreads) s[i] = __ldcg(sb + i);
+    __syncthreads();
+    {
+        const u32 e = t & (kChunk - 1), part = t / kChunk;
+        const u64 x = s[c * kChunk + e];
+        u32 cnt = 0;
+        if (c * kChunk + e < n) {
+#pragma unroll
+            for (u32 k = 0; k < kChunks / 4; ++k) {
+                const u32 q = part + 4 * k;
+                if (q < nch && q != c) {
+                    const u64* run = s + q * kChunk;
+                    const bool le = q < c;  // equal words: earlier chunks first
+                    u32 lo = 0;
+#pragma unroll
+                    for (u32 step = kChunk / 2; step > 0; step >>= 1) {
+                        const u64 y = run[lo + step - 1];
+                        if (le ? y <= x : y < x) lo += step;
+                    }
+                    const u64 y = run[lo];
+                    if (le ? y <= x : y < x) ++lo;
+                    cnt += lo;
+                }
+            }
+            if (cnt) atomicAdd(&s_rank[e], cnt);
+        }
+        __syncthreads();
+        if (t < kChunk && c * kChunk + t < n) sb[kSbMerged + t + s_rank[t]] = x;
+    }
+    __syncthreads();
+    if (t == 0) {
+        __threadfence();
+        atomicAdd(cnt2, 1ull);
+    }
+    if (c != 0) return;
+    if (t == 0) {  // every chunk's words scattered
+        while (ld_volatile(cnt2) < nch) {
+        }
+        __threadfence();
+        *flag = 0;
+        *cnt1 = 0;
+        *cnt2 = 0;
+    }
+    __syncthreads();
+    for (u32 i = t; i < n; i += kSmallFrontThreads) s[i] = __ldcg(sb + kSbMerged + i);
     if (t < 32) {
         ull g = 0, b = 0, o = 0;
         if (t < nch) {
-            g = sb[kSbPart + 4 * t];
-            b = sb[kSbPart + 4 * t + 1];
-            o = sb[kSbPart + 4 * t + 2];
+            g = __ldcg(sb + kSbPart + 4 * t);
+            b = __ldcg(sb + kSbPart + 4 * t + 1);
+            o = __ldcg(sb + kSbPart + 4 * t + 2);
         }
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
@@ -893,13 +916,137 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
             o |= __shfl_xor_sync(FULL, o, d);
         }
         if (t == 0) {
-            s_acc[0] = g;
-            s_acc[1] = b;
-            s_acc[2] = o;
+            s_tot[0] = g;
+            s_tot[1] = b;
+            s_tot[2] = o;
         }
     }
     __syncthreads();
-    small_resolve(sbuf, n, f, db, ib, ctr, s_acc, sb[kSbPart + 3], s_wsum, o_k, o_v, o_o);
+    small_resolve(s, n, f, db, ib, ctr, s_tot, gt0, s_wsum, o_k, o_v, o_o);
+}
+
+// The same stages in ONE thread-block cluster of kChunks CTAs, exchanging
+// through distributed shared memory instead of L2: CTA 0 reads the
+// descriptor, the others copy it from CTA 0's shared memory; every chunk's
+// sorted words are copied from its CTA's shared memory, the merged words
+// are stored straight into CTA 0's, and the three hardware cluster barriers
+// replace the flag and counters (no global round trip between stages).
+constexpr int kSmallClusterSmem = (2 * kChunk + 2 * kSmallFrontMax) * 8;  // own chunk (x2), all chunks, merged
+
+__global__ void __launch_bounds__(kSmallFrontThreads, 1)
+    k_small_front_cluster(const GraphFront* __restrict__ hf, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
+                          u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
+    namespace cg = cooperative_groups;
+    extern __shared__ u64 dyn[];
+    u64* s_own = dyn;                     // [2 kChunk]: this chunk, sorted in place
+    u64* s_all = dyn + 2 * kChunk;        // [kSmallFrontMax]: every chunk
+    u64* s_mrg = s_all + kSmallFrontMax;  // [kSmallFrontMax]: merged words (CTA 0)
+    __shared__ u64 s_desc[kDescWords];
+    __shared__ u32 s_wsum[kSmallFrontThreads / 32];
+    __shared__ u32 s_rank[kChunk];
+    __shared__ ull s_acc[3], s_tot[3];
+    __shared__ ull s_part[kChunks * 3];  // CTA 0: every chunk's check partials
+    cg::cluster_group cl = cg::this_cluster();
+    const u32 t = threadIdx.x, lane = t & 31, c = cl.block_rank();
+    u64 gt0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
+    pdl_enter();
+    if (t < 3) s_acc[t] = 0;
+    if (t < kChunk) s_rank[t] = 0;
+    if (c == 0 && t < kDescWords) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
+    cl.sync();  // the descriptor is in CTA 0
+    if (c != 0 && t < kDescWords) s_desc[t] = cl.map_shared_rank(s_desc, 0)[t];
+    __syncthreads();
+    const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
+    const u32 n = u32(f.ni + f.nd), nch = (n + kChunk - 1) / kChunk;
+    const bool live = c < nch;
+    if (live && t < kChunk) {
+        const u32 i = c * kChunk + t;
+        PrepAcc acc;
+        u64 w = ~0ull;  // pads sort last
+        if (i < n) {
+            const bool ins = i < f.ni;
+            const u32 su = ins ? f.is[i] : f.ds[i - f.ni];
+            const u32 dv = ins ? f.id[i] : f.dd[i - f.ni];
+            int cls;
+            w = pack_word(f, ib, prep_code(f, db, su, dv, i, ins, acc, cls), i, ins);
+        }
+        s_own[t] = w;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            acc.guards += __shfl_xor_sync(FULL, acc.guards, d);
+            acc.bad = max(acc.bad, __shfl_xor_sync(FULL, acc.bad, d));
+            acc.oor |= __shfl_xor_sync(FULL, acc.oor, d);
+        }
+        if (lane == 0) {
+            if (acc.guards) atomicAdd(&s_acc[0], acc.guards);
+            if (acc.bad) atomicMax(&s_acc[1], acc.bad);
+            if (acc.oor) atomicOr(&s_acc[2], 1ull);
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kChunk) : "memory");
+        sort_block<1>(s_own, s_own + kChunk, t, kChunk, kChunk);
+        if (t < 3) cl.map_shared_rank(s_part, 0)[3 * c + t] = s_acc[t];
+    } else if (c == 0) {  // CTA 0's other threads: counters and look-back words
+        for (u32 i = t - kChunk; i < sizeof(Ctr) / 8; i += kSmallFrontThreads - kChunk)
+            reinterpret_cast<ull*>(ctr)[i] = 0;
+        for (u64 i = t - kChunk; i < ws_words; i += kSmallFrontThreads - kChunk) ws_tiles[i] = 0;
+    }
+    cl.sync();  // every chunk sorted
+    if (live) {
+        for (u32 i = t; i < nch * kChunk; i += kSmallFrontThreads) {
+            const u32 q = i / kChunk;
+            s_all[i] = q == c ? s_own[i - q * kChunk] : cl.map_shared_rank(s_own, q)[i - q * kChunk];
+        }
+        __syncthreads();
+        const u32 e = t & (kChunk - 1), part = t / kChunk;
+        const u64 x = s_all[c * kChunk + e];
+        if (c * kChunk + e < n) {
+            u32 cnt = 0;
+#pragma unroll
+            for (u32 k = 0; k < kChunks / 4; ++k) {
+                const u32 q = part + 4 * k;
+                if (q < nch && q != c) {
+                    const u64* run = s_all + q * kChunk;
+                    const bool le = q < c;  // equal words: earlier chunks first
+                    u32 lo = 0;
+#pragma unroll
+                    for (u32 step = kChunk / 2; step > 0; step >>= 1) {
+                        const u64 y = run[lo + step - 1];
+                        if (le ? y <= x : y < x) lo += step;
+                    }
+                    const u64 y = run[lo];
+                    if (le ? y <= x : y < x) ++lo;
+                    cnt += lo;
+                }
+            }
+            if (cnt) atomicAdd(&s_rank[e], cnt);
+        }
+        __syncthreads();
+        if (t < kChunk && c * kChunk + t < n) cl.map_shared_rank(s_mrg, 0)[t + s_rank[t]] = x;
+    }
+    cl.sync();  // merged words in CTA 0 (and no CTA reads another's shared memory past here)
+    if (c != 0) return;
+    if (t < 32) {
+        ull g = 0, b = 0, o = 0;
+        if (t < nch) {
+            g = s_part[3 * t];
+            b = s_part[3 * t + 1];
+            o = s_part[3 * t + 2];
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            g += __shfl_xor_sync(FULL, g, d);
+            b = max(b, __shfl_xor_sync(FULL, b, d));
+            o |= __shfl_xor_sync(FULL, o, d);
+        }
+        if (t == 0) {
+            s_tot[0] = g;
+            s_tot[1] = b;
+            s_tot[2] = o;
+        }
+    }
+    __syncthreads();
+    small_resolve(s_mrg, n, f, db, ib, ctr, s_tot, gt0, s_wsum, o_k, o_v, o_o);
 }
 
 // Leaf of every unique update of a small batch (leaf_for_key), a warp per
@@ -2683,7 +2830,7 @@ std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int le
     std::vector<uintptr_t> k;
     for (const void* p : ptrs) k.push_back(reinterpret_cast<uintptr_t>(p));
     const u64 vals[] = {cap_, leaf_, u64(height_), ro_lo, num_vertices, u64(db), u64(cfg.eager), cfg.small_max,
-                        cfg.medium_max, u64(cfg.force), u64(levels), u64(empty_leaves != 0)};
+                        cfg.medium_max, u64(cfg.force), u64(levels), u64(empty_leaves != 0), u64(small_cluster_)};
     for (const u64 v : vals) k.push_back(uintptr_t(v));
     return k;
 }
@@ -2710,14 +2857,59 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels, int mult
         // descriptor read in place from page-locked memory), then the leaf of
         // every unique update (pma.hpp:234-289), a warp per key
         static_assert(kSmallGraphMax <= kSmallFrontMax, "small graph batches sort in one CTA");
-        if (multi) {  // (more than small_onecta_ updates: chunks sorted on their own SMs, merged by rank)
-            k_small_chunks<<<kChunks, kChunk, 0, stream_>>>(h_desc_dev_, db, ib, small_sb_.ptr);
-            GPMA_LAUNCH_CHECK();
-            pdl_chain() = pdl_;
-            launch_k(k_small_merge_ranks, dim3(kChunks), dim3(kChunk), 0, stream_, small_sb_.ptr);
-            launch_k(k_small_resolve, dim3(1), dim3(kSmallFrontThreads), 0, stream_,
-                     small_sb_.ptr, db, ib, d_ctr, small_ws_.tiles.ptr,
-                     u64(small_ws_.tiles.cap), uk.ptr, uv.ptr, uop.ptr);
+        // (a 16-CTA cluster is non-portable: where it cannot be resident the
+        // cooperative grid takes its place)
+        static const bool cluster_ok = [this] {
+            GPMA_CUDA(cudaFuncSetAttribute(k_small_front_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           kSmallClusterSmem));
+            GPMA_CUDA(cudaFuncSetAttribute(k_small_front_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(kChunks);
+            lc.blockDim = dim3(kSmallFrontThreads);
+            lc.dynamicSmemBytes = kSmallClusterSmem;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kChunks;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            int nc = 0;
+            if (cudaOccupancyMaxActiveClusters(&nc, k_small_front_cluster, &lc) != cudaSuccess) {
+                cudaGetLastError();
+                nc = 0;
+            }
+            return nc > 0;
+        }();
+        if (multi && small_cluster_ && cluster_ok) {  // (one cluster: distributed shared memory between the chunks)
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(kChunks);
+            lc.blockDim = dim3(kSmallFrontThreads);
+            lc.dynamicSmemBytes = kSmallClusterSmem;
+            lc.stream = stream_;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = kChunks;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            GPMA_CUDA(cudaLaunchKernelEx(&lc, k_small_front_cluster, static_cast<const GraphFront*>(h_desc_dev_), db,
+                                         ib, d_ctr, small_ws_.tiles.ptr, u64(small_ws_.tiles.cap), uk.ptr, uv.ptr,
+                                         uop.ptr));
+        } else if (multi) {  // (one cooperative grid: its CTAs wait on each other)
+            cudaLaunchConfig_t lc{};
+            lc.gridDim = dim3(kChunks);
+            lc.blockDim = dim3(kSmallFrontThreads);
+            lc.stream = stream_;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeCooperative;
+            at[0].val.cooperative = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            GPMA_CUDA(cudaLaunchKernelEx(&lc, k_small_front_grid, static_cast<const GraphFront*>(h_desc_dev_), db, ib,
+                                         small_sb_.ptr, d_ctr, small_ws_.tiles.ptr, u64(small_ws_.tiles.cap), uk.ptr,
+                                         uv.ptr, uop.ptr));
         } else {
             k_small_front<<<1, kSmallFrontThreads, kSmallFrontSmem, stream_>>>(
                 h_desc_dev_, db, ib, d_ctr, small_ws_.tiles.ptr, small_ws_.tiles.cap, uk.ptr, uv.ptr, uop.ptr);
@@ -2768,7 +2960,7 @@ int Pma::run_small_graph(const GraphFront& gf, const EngineCfg& cfg) {
         small_ws_.tiles.reserve(64);
         small_ws_.epoch = 0;
         key = small_graph_key(db, cfg, levels);
-        GPMA_CUDA(cudaMemsetAsync(small_sb_.ptr + kSbFlag, 0, 8, stream_));
+        GPMA_CUDA(cudaMemsetAsync(small_sb_.ptr + kSbFlag, 0, 24, stream_));
         capture_small_graph(db, cfg, levels, multi);
         small_key_[multi] = key;
     }

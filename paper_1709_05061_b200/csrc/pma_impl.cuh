@@ -303,8 +303,9 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     bool small_graphs_ = true;          // GPMA_NO_GRAPHS=1 disables (A/B measurements)
     cudaGraphExec_t small_exec_[2] = {nullptr, nullptr};  // [one-CTA front end, multi-CTA front end]
     std::vector<uintptr_t> small_key_[2];  // what each captured graph embeds
-    u64 small_onecta_ = 1024;           // larger small batches: the multi-CTA front end (GPMA_SMALL_ONECTA=n)
-    DevBuf<u64> small_sb_;              // its scratch (k_small_chunks)
+    u64 small_onecta_ = 512;            // larger small batches: the multi-CTA front end (GPMA_SMALL_ONECTA=n)
+    DevBuf<u64> small_sb_;              // its scratch (k_small_front_grid)
+    bool small_cluster_ = true;         // ... in one 16-CTA cluster (GPMA_SMALL_CLUSTER=0: a cooperative grid)
     GraphFront* h_desc_ = nullptr;      // page-locked batch descriptor (copied by the graph's first node)
     GraphFront* d_desc_ = nullptr;
     GraphFront* h_desc_dev_ = nullptr;  // device view of h_desc_ (read in place by the small graph)

@@ -473,17 +473,18 @@ def test_small_batch_sort_size_regimes(mode):
         assert (g.row_offsets() == r.row_offsets()).all(), ctx
 
 
-@pytest.mark.parametrize("onecta", ["0", "1024", "4096"])
-def test_small_batch_front_end_variants(onecta, monkeypatch):
-    """The captured small-batch graph's two front ends — one CTA
-    (k_small_front) and chunks on separate SMs merged by rank
-    (k_small_chunks / k_small_merge_ranks / k_small_resolve) — forced per
-    batch size by GPMA_SMALL_ONECTA: the same words with the same
+@pytest.mark.parametrize("onecta,cluster", [("0", "1"), ("512", "1"), ("4096", "1"), ("0", "0")])
+def test_small_batch_front_end_variants(onecta, cluster, monkeypatch):
+    """The captured small-batch graph's front ends — one CTA (k_small_front)
+    and chunks on separate SMs merged by rank, in a 16-CTA cluster
+    (k_small_front_cluster) or a cooperative grid (k_small_front_grid) —
+    forced per batch size by GPMA_SMALL_ONECTA / GPMA_SMALL_CLUSTER: the same words with the same
     duplicates spread over different chunks (repeated inserts, a key deleted
     twice, insert + delete of one key), guard deletes, deletes outside the
     layout (redone on the generic path) and the first of two bad inserts
     reported; slots, stats and row offsets bit-exact."""
     monkeypatch.setenv("GPMA_SMALL_ONECTA", onecta)
+    monkeypatch.setenv("GPMA_SMALL_CLUSTER", cluster)
     rng = np.random.default_rng(int(onecta) + 5)
     nv = 1 << 14
     stream = RefStream.rmat(nv, 200000, 13)

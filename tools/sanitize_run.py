@@ -21,7 +21,7 @@ def main():
     from paper_1709_05061_b200.abi import PMA_EAGER, graph_config
 
     ok = True
-    for kind, nv, batches, mode in [("er", 1 << 12, [700, 1500, 20000, 70000], 0),
+    for kind, nv, batches, mode in [("er", 1 << 12, [200, 700, 1500, 20000, 70000], 0),
                                     ("rmat", 1 << 12, [1500, 3000, 70000], PMA_EAGER)]:
         rs = RefStream.erdos_renyi(nv, 2.0 ** -3, 1).shuffle(2) if kind == "er" else RefStream.rmat(nv, 400000, 5)
         s, d, w, _ = rs.arrays()
