@@ -605,8 +605,9 @@ constexpr int kSmallFrontSmem = 2 * kSmallFrontMax * 8;  // double-buffered exch
 
 // Duplicate resolution of a small batch's sorted words ck[0, n) by one CTA of
 // kSmallFrontThreads (segment_engine.hpp:346-363): the last word of each
-// equal-key run survives; a delete there takes the run's last insert.  Thread
-// t owns the contiguous items [4t, 4t + 4) for the ordered scan; thread 0
+// equal-key run survives; a delete there takes the run's last insert.  Warp
+// w owns the items [128 w, 128 w + 128), read 32 consecutive words at a time
+// (no bank conflicts) and compacted in order by ballots; thread 0
 // publishes the front end's counters (s_acc: guard deletes, first bad insert,
 // out-of-layout delete).
 __device__ __forceinline__ void small_resolve(const u64* ck, u32 n, const GraphFront& f, int db, int ib, Ctr* ctr,
@@ -615,23 +616,21 @@ __device__ __forceinline__ void small_resolve(const u64* ck, u32 n, const GraphF
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const u64 pmask = (1ull << ib) - 1;
     const u64 skipkey = 1ull << (2 * db);
-    unsigned fm = 0;
+    const u32 base = warp * (32 * kSmallFrontItems);
+    u32 fm[kSmallFrontItems];
+    u32 wcnt = 0;
 #pragma unroll
     for (int e = 0; e < kSmallFrontItems; ++e) {
-        const u32 i = t * kSmallFrontItems + u32(e);
+        const u32 i = base + 32 * u32(e) + lane;
+        bool keep = false;
         if (i < n) {
             const u64 c = ck[i] >> ib;
-            if (((i + 1 == n) || (ck[i + 1] >> ib) != c) && c < skipkey) fm |= 1u << e;
+            keep = ((i + 1 == n) || (ck[i + 1] >> ib) != c) && c < skipkey;
         }
+        fm[e] = __ballot_sync(FULL, keep);
+        wcnt += __popc(fm[e]);
     }
-    const u32 cnt = __popc(fm);
-    u32 inc = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-        const u32 y = __shfl_up_sync(FULL, inc, d);
-        if (lane >= u32(d)) inc += y;
-    }
-    if (lane == 31) s_wsum[warp] = inc;
+    if (lane == 0) s_wsum[warp] = wcnt;
     __syncthreads();
     if (warp == 0) {
         u32 w = s_wsum[lane];
@@ -643,29 +642,32 @@ __device__ __forceinline__ void small_resolve(const u64* ck, u32 n, const GraphF
         s_wsum[lane] = w;  // inclusive over warps
     }
     __syncthreads();
-    u32 x0 = inc - cnt + (warp ? s_wsum[warp - 1] : 0u);
+    u32 x0 = warp ? s_wsum[warp - 1] : 0u;
+    const u32 below = (1u << lane) - 1u;
     const double* gw = f.iw;
 #pragma unroll
     for (int e = 0; e < kSmallFrontItems; ++e) {
-        if (!((fm >> e) & 1u)) continue;
-        const u32 i = t * kSmallFrontItems + u32(e);
-        const u64 c = ck[i] >> ib;
-        u64 a = ck[i] & pmask;
-        bool ins = a != pmask;
-        if (!ins) {  // delete at a run end: any earlier insert of the key wins
-            for (long long q = (long long)i - 1; q >= 0 && (ck[q] >> ib) == c; --q) {
-                const u64 aq = ck[q] & pmask;
-                if (aq != pmask) {
-                    a = aq;
-                    ins = true;
-                    break;
+        if ((fm[e] >> lane) & 1u) {
+            const u32 i = base + 32 * u32(e) + lane;
+            const u32 x = x0 + __popc(fm[e] & below);
+            const u64 c = ck[i] >> ib;
+            u64 a = ck[i] & pmask;
+            bool ins = a != pmask;
+            if (!ins) {  // delete at a run end: any earlier insert of the key wins
+                for (long long q = (long long)i - 1; q >= 0 && (ck[q] >> ib) == c; --q) {
+                    const u64 aq = ck[q] & pmask;
+                    if (aq != pmask) {
+                        a = aq;
+                        ins = true;
+                        break;
+                    }
                 }
             }
+            o_k[x] = ((c >> db) << 32) | (c & ((1ull << db) - 1));
+            o_v[x] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
+            o_o[x] = ins ? kOpInsert : kOpDelete;
         }
-        o_k[x0] = ((c >> db) << 32) | (c & ((1ull << db) - 1));
-        o_v[x0] = ins ? u64(__double_as_longlong(gw ? gw[a] : 1.0)) : 0;
-        o_o[x0] = ins ? kOpInsert : kOpDelete;
-        ++x0;
+        x0 += __popc(fm[e]);
     }
     if (t == 0) {
         const ull total = s_wsum[kSmallFrontThreads / 32 - 1];
