@@ -70,6 +70,7 @@ class LocalComm:
         torch = _torch()
         acc = ts[0].clone()
         for t in ts[1:]:
+            t = t.to(acc.device)  # (shards on different devices reduce on the first one's)
             if op == "sum":
                 acc += t
             elif op == "max":
@@ -79,7 +80,7 @@ class LocalComm:
             else:
                 raise ValueError(op)
         for t in ts:
-            t.copy_(acc)
+            t.copy_(acc)  # (copy_ crosses devices)
 
     def all_to_all_v(self, sends, send_counts):
         """sends[i]: local rank i's buffer, owner-major; send_counts[i][r]:
