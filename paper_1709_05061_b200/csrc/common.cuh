@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <stdexcept>
@@ -125,6 +126,27 @@ __host__ __device__ __forceinline__ u32 dst_of(u64 key) { return u32(key & 0xFFF
 __host__ __device__ __forceinline__ bool is_guard(u64 key) { return (key & 0xFFFFFFFFull) == kGuardDst; }
 
 // Growable device buffer (grow-only; contents not preserved on growth).
+// NVTX ranges (SURVEY §5 tracing): one per batch / analytic call and one per
+// stage of a batch, for nsys / ncu --nvtx; no-ops when no tool is attached
+struct NvtxScope {
+    explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+    ~NvtxScope() { nvtxRangePop(); }
+    NvtxScope(const NvtxScope&) = delete;
+    NvtxScope& operator=(const NvtxScope&) = delete;
+};
+// the current stage of a batch: each call closes the previous one
+struct NvtxStages {
+    bool open = false;
+    void next(const char* name) {
+        if (open) nvtxRangePop();
+        nvtxRangePushA(name);
+        open = true;
+    }
+    ~NvtxStages() {
+        if (open) nvtxRangePop();
+    }
+};
+
 template <typename T>
 struct DevBuf {
     T* ptr = nullptr;

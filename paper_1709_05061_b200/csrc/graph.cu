@@ -650,6 +650,7 @@ void Graph::csr_snapshot(u64* h_ro, u32* h_col, double* h_val) {
 // ------------------------------------------------------------- analytics
 
 void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
+    NvtxScope nvtx_scope("gpma.bfs");
     if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     if (root >= nv) throw ApiError(PMA_EINVAL, "bfs: root outside vertex range");
     cudaStream_t s = pma.stream();
@@ -737,6 +738,7 @@ void Graph::bfs(u32 root, u32* h_dist, u64* reached) {
 }
 
 void Graph::cc(u32* h_labels) {
+    NvtxScope nvtx_scope("gpma.cc");
     if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     cudaStream_t s = pma.stream();
     GPMA_CUDA(cudaEventRecord(pma_ev(0), s));
@@ -758,6 +760,7 @@ void Graph::cc(u32* h_labels) {
 
 void Graph::pagerank(double d, double eps, u64 max_iters, const double* h_warm, double* h_ranks, u64* iters,
                      int* converged) {
+    NvtxScope nvtx_scope("gpma.pagerank");
     if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     if (nv == 0) throw ApiError(PMA_EINVAL, "pagerank: empty vertex set");
     cudaStream_t s = pma.stream();
@@ -882,6 +885,7 @@ void Graph::prepare_hot(const u32* od, u64 n) {
 }
 
 void Graph::spmv(const double* h_x, double* h_y) {
+    NvtxScope nvtx_scope("gpma.spmv");
     if (is_shard()) throw ApiError(PMA_ELOGIC, "whole-graph analytics on a shard: use the gpma_shard_* entry points");
     cudaStream_t s = pma.stream();
     px.reserve(nv + 1);

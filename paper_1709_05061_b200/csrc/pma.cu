@@ -85,6 +85,7 @@ Pma::Pma(const pma_profile* profile, int device) : device_(device) {
     if (const char* e = std::getenv("GPMA_NO_POLL")) small_poll_ = e[0] == '0';
     if (const char* e = std::getenv("GPMA_SMALL_ONECTA")) small_onecta_ = std::strtoull(e, nullptr, 10);
     if (const char* e = std::getenv("GPMA_SMALL_CLUSTER")) small_cluster_ = e[0] != '0';
+    if (const char* e = std::getenv("GPMA_CHECK_ROUNDS")) check_rounds_ = e[0] == '1';
     if (const char* e = std::getenv("GPMA_NO_DIRECT_TOUCHED")) direct_touched_ = e[0] == '0';
     for (auto& e : ev_) GPMA_CUDA(cudaEventCreate(&e));
     reset_layout(16);
@@ -2639,6 +2640,22 @@ void Pma::grid_merge(u64 b, u64 m, const u32* plist, u64 s, bool large) {
 // reads its counts on the device; npend is a host-known upper bound of the
 // pending count.  (The commit kernels stamp the level's span into the
 // counters: lvl_tmin / lvl_tmax.)
+// Round-disjointness check (the reference's assert, segment_engine.hpp:400-405,
+// live in its release builds): a level's groups name strictly
+// increasing segments, each with a non-empty slice of the pending updates,
+// so no two commits of a round touch the same slots.  Debug switch
+// GPMA_CHECK_ROUNDS=1; a violation fails the batch with PMA_ELOGIC.
+__global__ void k_check_rounds(const u32* __restrict__ gseg, const u32* __restrict__ gstart, Ctr* ctr) {
+    pdl_enter();
+    const ull ng = ctr->ngroups;
+    ull bad = 0;
+    for (ull g = blockIdx.x * u64(blockDim.x) + threadIdx.x; g < ng; g += u64(gridDim.x) * blockDim.x) {
+        if (gstart[g] >= gstart[g + 1]) ++bad;
+        if (g && gseg[g] <= gseg[g - 1]) ++bad;
+    }
+    if (bad) atomicAdd(&ctr->round_overlap, bad);
+}
+
 void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touched_ptr, u64 n, const EngineCfg& cfg,
                         ScanWorkspace& ws, bool events, u64& launches) {
     const u64 m = leaf_ << level;
@@ -2671,6 +2688,11 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
                 ctr->lvl_npend[lv] = *np_cur;
             },
             level == 0 ? &d_ctr->t_rounds : nullptr);
+        ++launches;
+    }
+    if (check_rounds_) {
+        launch_k(k_check_rounds, dim3(grid_for(npend, 256, 148 * 4)), dim3(256), 0, stream_,
+                 static_cast<const u32*>(gseg.ptr), static_cast<const u32*>(gstart.ptr), d_ctr);
         ++launches;
     }
     // commit (decide + merge + scatter)
@@ -2832,7 +2854,7 @@ std::vector<uintptr_t> Pma::small_graph_key(int db, const EngineCfg& cfg, int le
     std::vector<uintptr_t> k;
     for (const void* p : ptrs) k.push_back(reinterpret_cast<uintptr_t>(p));
     const u64 vals[] = {cap_, leaf_, u64(height_), ro_lo, num_vertices, u64(db), u64(cfg.eager), cfg.small_max,
-                        cfg.medium_max, u64(cfg.force), u64(levels), u64(empty_leaves != 0), u64(small_cluster_)};
+                        cfg.medium_max, u64(cfg.force), u64(levels), u64(empty_leaves != 0), u64(small_cluster_), u64(check_rounds_)};
     for (const u64 v : vals) k.push_back(uintptr_t(v));
     return k;
 }
@@ -2997,6 +3019,8 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
                               pma_stats* out, GraphFront* gf) {
     using Clock = std::chrono::steady_clock;
     const auto t0 = Clock::now();
+    NvtxScope nv_batch("gpma.apply_batch");
+    NvtxStages nv_stage;
     pma_stats st;
     std::memset(&st, 0, sizeof(st));
     st.batch_size = n;
@@ -3027,6 +3051,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     // ---- small graph batches: the front end and the first rounds replayed
     // as one captured CUDA graph (no per-kernel launch cost, no host round
     // trip); the host loop below continues only if updates are still pending
+    if (small_graph) nv_stage.next("gpma.small_graph");
     const int graph_levels = small_graph ? run_small_graph(*gf, cfg) : 0;
     const u64 graph_ns = graph_levels && h_ctr->gt1 > h_ctr->gt0 ? h_ctr->gt1 - h_ctr->gt0 : 0;
     if (graph_levels) {
@@ -3034,6 +3059,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         // graph, E(0) -> E(4); every host API call counts at this size)
     } else {
     // ---- 1. sort (stable, varying bits only) ----
+    nv_stage.next("gpma.sort");
     GPMA_CUDA(cudaMemsetAsync(d_ctr, 0, sizeof(Ctr), stream_));
     sk_in.reserve(n);
     sk_out.reserve(n);
@@ -3189,6 +3215,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
         sorted_ck = alt ? sk_out.ptr : sk_in.ptr;
         sorted_ci = alt ? si_out.ptr : si_in.ptr;
     }
+    nv_stage.next("gpma.resolve_search");
     // ---- 2+3. resolve duplicates (run ends -> unique updates) fused with the
     // leaf assignment of each unique key (computed once per batch) ----
     uk.reserve(n + 4);
@@ -3303,6 +3330,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     touched.reserve(2 * n + 2);
     rlist.reserve(2 * n + 4);
     // ---- 4. rounds ----
+    nv_stage.next("gpma.rounds");
     // Rounds are device-driven: every kernel reads its counts from d_ctr, the
     // per-level stats land in d_ctr->lvl_*, so while the pending list is large
     // (more rounds are near certain) the next round is launched without a host
@@ -3580,6 +3608,7 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
     timing.tombstone_flips = st.tombstones_added;
     if (!graph_levels && !spec_tail) event(3);
     // ---- 5. refresh leaf headers / row offsets ----
+    nv_stage.next("gpma.refresh");
     // The warp tier refreshed dense segments in place; sparse and CTA-tier
     // segments were queued on rlist; left walks are needed only while empty
     // leaves exist (their headers inherit the next leaf's first key).
@@ -3715,6 +3744,12 @@ void Pma::batch_update_device(const u64* dk, const u64* dv, const u8* dop, u64 n
             timing.front_end = 2;
             return;
         }
+    }
+    if (check_rounds_) {
+        sync_ctr();
+        if (h_ctr->round_overlap)
+            throw ApiError(PMA_ELOGIC, "segment engine: overlapping segments in one round (" +
+                                           std::to_string(h_ctr->round_overlap) + " groups)");
     }
     st.wall_ns = u64(std::chrono::duration_cast<std::chrono::nanoseconds>(Clock::now() - t0).count());
     if (out) *out = st;

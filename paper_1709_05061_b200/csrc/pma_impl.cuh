@@ -76,6 +76,7 @@ struct Ctr {
     ull seq;           // captured small batches: the replay's sequence number (from the descriptor)
     ull done_seq;      // ... written to the host copy LAST, after the counters (the host polls it)
     ull seg_tomb, seg_empty;  // grid tier: tombstones / empty leaves of the segment before its merge
+    ull round_overlap;  // GPMA_CHECK_ROUNDS=1: groups of a round that overlap (k_check_rounds)
     // device-driven rounds: pending counts alternate between np[level & 1] and
     // np[(level + 1) & 1]; per-level stats are kept here and read at the next
     // host sync (rounds may run back to back without one)
@@ -305,6 +306,7 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     std::vector<uintptr_t> small_key_[2];  // what each captured graph embeds
     u64 small_onecta_ = 512;            // larger small batches: the multi-CTA front end (GPMA_SMALL_ONECTA=n)
     DevBuf<u64> small_sb_;              // its scratch (k_small_front_grid)
+    bool check_rounds_ = false;         // GPMA_CHECK_ROUNDS=1: the round-disjointness check after every grouping
     bool small_cluster_ = true;         // ... in one 16-CTA cluster (GPMA_SMALL_CLUSTER=0: a cooperative grid)
     GraphFront* h_desc_ = nullptr;      // page-locked batch descriptor (copied by the graph's first node)
     GraphFront* d_desc_ = nullptr;

@@ -599,3 +599,29 @@ def test_small_batches_custom_profile(mode):
         assert gs.parity() == ref_parity(r, rs), f"batch {b}"
         assert_same_slots(g.pma().slots(), r.slots(), f"batch {b}")
         assert (g.row_offsets() == r.row_offsets()).all(), f"batch {b}"
+
+
+@pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
+def test_round_disjointness_check(mode, monkeypatch):
+    """GPMA_CHECK_ROUNDS=1 runs the reference's round-disjointness assert
+    (segment_engine.hpp:400-405) on the device after every grouping: small
+    (captured-graph) and large batches through several levels pass it and
+    stay bit-exact with the reference."""
+    monkeypatch.setenv("GPMA_CHECK_ROUNDS", "1")
+    rng = np.random.default_rng(3)
+    nv = 1 << 12
+    stream = RefStream.rmat(nv, 300000, 17)
+    s, d, w, _ = stream.arrays()
+    half = (len(s) + 1) // 2
+    cfg = GraphConfig(deletion_mode=mode)
+    g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half], cfg)
+    r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config(deletion_mode=mode))
+    for n in (50, 900, 3000, 40000, 150000):
+        a, b = rng.integers(0, nv, n).astype(np.uint32), rng.integers(0, nv, n).astype(np.uint32)
+        pick = rng.integers(0, half, n // 2)
+        c, dd = s[pick].astype(np.uint32), d[pick].astype(np.uint32)
+        ww = rng.random(n)
+        gs = g.apply_batch(a, b, ww, c, dd)
+        rs = r.apply_batch(a, b, ww, c, dd)
+        assert gs.parity() == ref_parity(r, rs), n
+        assert_same_slots(g.pma().slots(), r.slots(), f"n={n}")
