@@ -16,6 +16,7 @@ there is no CPU fallback (the import fails loudly without the library).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -110,6 +111,37 @@ class UpdateStats:
 
     def csv_row(self):
         return f"{self.batch_size},{self.rounds},{self.slot_writes},{self.wall_ns}"
+
+    @staticmethod
+    def csv_header_device():
+        """The reference's columns plus the device ones SURVEY §5 names."""
+        return UpdateStats.csv_header() + ",gpus,bytes_moved,hbm_frac,nvlink_frac"
+
+    def csv_row_device(self, timing, gpus: int = 1, hbm_peak_gbps: float = None, nvlink_bytes: int = 0,
+                       nvlink_peak_gbps: float = 900.0):
+        """`timing`: the same call's `pma_timing` (DynamicGraph.last_timing()).
+        bytes_moved = its algorithmic commit bytes (DESIGN.md §5);
+        hbm_frac = bytes_moved / device time / the HBM peak (MEASURED_PEAKS.json
+        when present, else 6650 GB/s); nvlink_frac = the routed bytes of a
+        sharded batch / device time / one GPU's NVLink peak per direction
+        (0 on one GPU)."""
+        if hbm_peak_gbps is None:
+            hbm_peak_gbps = _hbm_peak()
+        sec = float(timing.device_ms) * 1e-3
+        moved = int(timing.commit_bytes)
+        hbm = moved / sec / (hbm_peak_gbps * 1e9) if sec > 0 else 0.0
+        nvl = nvlink_bytes / sec / (nvlink_peak_gbps * 1e9) if sec > 0 and nvlink_bytes else 0.0
+        return f"{self.csv_row()},{gpus},{moved},{hbm:.4f},{nvl:.4f}"
+
+
+def _hbm_peak() -> float:
+    import json
+    p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        return 6650.0
 
 
 @dataclass

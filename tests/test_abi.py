@@ -94,3 +94,19 @@ def test_null_handles_are_rejected():
     last = p.stdout.strip().splitlines()[-1] if p.stdout.strip() else ""
     assert p.returncode == 0, f"crashed after {last!r}: {p.stderr[-500:]}"
     assert last == "BAD []", last
+
+
+def test_update_stats_csv_rows():
+    """UpdateStats.csv_row keeps the reference's schema (update_stats.hpp:27-34);
+    csv_row_device appends the device columns SURVEY §5 names (no GPU needed:
+    a timing record stands in)."""
+    from types import SimpleNamespace
+
+    from paper_1709_05061_b200.pmagraph import UpdateStats
+    u = UpdateStats(batch_size=10, rounds=2, slot_writes=40, wall_ns=1234)
+    assert UpdateStats.csv_header() == "batch_size,rounds,slot_writes,wall_ns"
+    assert u.csv_row() == "10,2,40,1234"
+    t = SimpleNamespace(device_ms=1.0, commit_bytes=3_000_000_000)
+    assert UpdateStats.csv_header_device().endswith(",gpus,bytes_moved,hbm_frac,nvlink_frac")
+    row = u.csv_row_device(t, gpus=2, hbm_peak_gbps=6000.0, nvlink_bytes=450_000_000)
+    assert row == "10,2,40,1234,2,3000000000,0.5000,0.5000"
