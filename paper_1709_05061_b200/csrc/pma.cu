@@ -100,7 +100,7 @@ Pma::~Pma() {
     if (d_ctr) cudaFree(d_ctr);
     if (h_ctr) cudaFreeHost(h_ctr);
     for (auto& x : small_exec_)
-        if (x) cudaGraphExecDestroy(x);
+        if (x) cudaGraphExecDestroy(x);  // (one per front-end variant)
     if (h_desc_) cudaFreeHost(h_desc_);
     if (d_desc_) cudaFree(d_desc_);
     for (auto& e : ev_)
@@ -607,21 +607,23 @@ constexpr int kSmallFrontSmem = 2 * kSmallFrontMax * 8;  // double-buffered exch
 // Duplicate resolution of a small batch's sorted words ck[0, n) by one CTA of
 // kSmallFrontThreads (segment_engine.hpp:346-363): the last word of each
 // equal-key run survives; a delete there takes the run's last insert.  Warp
-// w owns the items [128 w, 128 w + 128), read 32 consecutive words at a time
-// (no bank conflicts) and compacted in order by ballots; thread 0
+// w owns the words [32 w I, 32 (w + 1) I) (I = kItems per lane, n <= 1024 I),
+// read 32 consecutive words at a time (no bank conflicts) and compacted in
+// order by ballots; thread 0
 // publishes the front end's counters (s_acc: guard deletes, first bad insert,
 // out-of-layout delete).
+template <int kItems>
 __device__ __forceinline__ void small_resolve(const u64* ck, u32 n, const GraphFront& f, int db, int ib, Ctr* ctr,
                                               const ull* s_acc, u64 gt0, u32* s_wsum, u64* __restrict__ o_k,
                                               u64* __restrict__ o_v, u8* __restrict__ o_o) {
     const u32 t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const u64 pmask = (1ull << ib) - 1;
     const u64 skipkey = 1ull << (2 * db);
-    const u32 base = warp * (32 * kSmallFrontItems);
-    u32 fm[kSmallFrontItems];
+    const u32 base = warp * (32 * kItems);
+    u32 fm[kItems];
     u32 wcnt = 0;
 #pragma unroll
-    for (int e = 0; e < kSmallFrontItems; ++e) {
+    for (int e = 0; e < kItems; ++e) {
         const u32 i = base + 32 * u32(e) + lane;
         bool keep = false;
         if (i < n) {
@@ -647,7 +649,7 @@ __device__ __forceinline__ void small_resolve(const u64* ck, u32 n, const GraphF
     const u32 below = (1u << lane) - 1u;
     const double* gw = f.iw;
 #pragma unroll
-    for (int e = 0; e < kSmallFrontItems; ++e) {
+    for (int e = 0; e < kItems; ++e) {
         if ((fm[e] >> lane) & 1u) {
             const u32 i = base + 32 * u32(e) + lane;
             const u32 x = x0 + __popc(fm[e] & below);
@@ -749,7 +751,7 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
         sort_block<4>(sbuf, sbuf + kSmallFrontMax, t, kSmallFrontThreads, P);
     }
     __syncthreads();
-    small_resolve(sbuf, n, f, db, ib, ctr, s_acc, gt0, s_wsum, o_k, o_v, o_o);
+    small_resolve<kSmallFrontItems>(sbuf, n, f, db, ib, ctr, s_acc, gt0, s_wsum, o_k, o_v, o_o);
 }
 
 // The same front end over several SMs for small batches of more than
@@ -925,46 +927,63 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
         }
     }
     __syncthreads();
-    small_resolve(s, n, f, db, ib, ctr, s_tot, gt0, s_wsum, o_k, o_v, o_o);
+    small_resolve<kSmallFrontItems>(s, n, f, db, ib, ctr, s_tot, gt0, s_wsum, o_k, o_v, o_o);
 }
 
-// The same stages in ONE thread-block cluster of kChunks CTAs, exchanging
-// through distributed shared memory instead of L2: CTA 0 reads the
-// descriptor, the others copy it from CTA 0's shared memory; every chunk's
-// sorted words are copied from its CTA's shared memory, the merged words
-// are stored straight into CTA 0's, and the three hardware cluster barriers
-// replace the flag and counters (no global round trip between stages).
-constexpr int kSmallClusterSmem = (2 * kChunk + 2 * kSmallFrontMax) * 8;  // own chunk (x2), all chunks, merged
+// The same stages in ONE thread-block cluster of 16 CTAs, exchanging through
+// distributed shared memory instead of L2: chunks of kC = 256 words for up to
+// kSmallFrontMax updates, 1024 words (the whole CTA) for up to 16384.  CTA 0
+// reads the descriptor, the others copy it from CTA 0's shared memory; every
+// chunk's sorted words are copied from its CTA's shared memory and the
+// merged words stored straight into CTA 0's — for kC = 1024 into CTA 0's
+// copy of the chunks (shared memory holds one 16K-word array, not two),
+// after a fourth cluster barrier; hardware cluster barriers replace the
+// flag and counters (no global round trip between stages).  Chunk size,
+// bisections and run loops are compile-time: the runtime-chunk version of
+// this kernel measured +2.4 µs at B = 1000.
+constexpr u32 kClusterCtas = 16;
+constexpr u32 kSmallMultiMax = kClusterCtas * kSmallFrontThreads;
+template <u32 kC>
+constexpr int cluster_smem() {  // own chunk (x2), all chunks, merged words (kC < 1024: separate)
+    return int((2 * kC + (kC < kSmallFrontThreads ? 2 : 1) * kClusterCtas * kC) * 8);
+}
 
+template <u32 kC>
 __global__ void __launch_bounds__(kSmallFrontThreads, 1)
     k_small_front_cluster(const GraphFront* __restrict__ hf, int db, int ib, Ctr* ctr, ull* ws_tiles, u64 ws_words,
                           u64* __restrict__ o_k, u64* __restrict__ o_v, u8* __restrict__ o_o) {
     namespace cg = cooperative_groups;
+    constexpr bool kAlias = kC == kSmallFrontThreads;  // merged words over CTA 0's copy of the chunks
+    constexpr u32 kParts = kSmallFrontThreads / kC;     // threads per word in the rank step
     extern __shared__ u64 dyn[];
-    u64* s_own = dyn;                     // [2 kChunk]: this chunk, sorted in place
-    u64* s_all = dyn + 2 * kChunk;        // [kSmallFrontMax]: every chunk
-    u64* s_mrg = s_all + kSmallFrontMax;  // [kSmallFrontMax]: merged words (CTA 0)
+    u64* s_own = dyn;                                               // [2 kC]: this chunk, sorted in place
+    u64* s_all = dyn + 2 * kC;                                      // [16 kC]: every chunk
+    u64* s_mrg = kAlias ? s_all : s_all + kClusterCtas * kC;        // [16 kC]: merged words (CTA 0)
     __shared__ u64 s_desc[kDescWords];
     __shared__ u32 s_wsum[kSmallFrontThreads / 32];
-    __shared__ u32 s_rank[kChunk];
+    __shared__ u32 s_rank[kC];
     __shared__ ull s_acc[3], s_tot[3];
-    __shared__ ull s_part[kChunks * 3];  // CTA 0: every chunk's check partials
+    __shared__ ull s_part[kClusterCtas * 3];  // CTA 0: every chunk's check partials
     cg::cluster_group cl = cg::this_cluster();
     const u32 t = threadIdx.x, lane = t & 31, c = cl.block_rank();
     u64 gt0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt0));
     pdl_enter();
     if (t < 3) s_acc[t] = 0;
-    if (t < kChunk) s_rank[t] = 0;
+    if (t < kC) s_rank[t] = 0;
     if (c == 0 && t < kDescWords) s_desc[t] = reinterpret_cast<const volatile u64*>(hf)[t];
     cl.sync();  // the descriptor is in CTA 0
     if (c != 0 && t < kDescWords) s_desc[t] = cl.map_shared_rank(s_desc, 0)[t];
     __syncthreads();
     const GraphFront& f = *reinterpret_cast<const GraphFront*>(s_desc);
-    const u32 n = u32(f.ni + f.nd), nch = (n + kChunk - 1) / kChunk;
+    const u32 n = u32(f.ni + f.nd), nch = (n + kC - 1) / kC;
     const bool live = c < nch;
-    if (live && t < kChunk) {
-        const u32 i = c * kChunk + t;
+    auto clear_counters = [&](u32 from, u32 stride) {  // CTA 0: counters and look-back words
+        for (u32 i = from; i < sizeof(Ctr) / 8; i += stride) reinterpret_cast<ull*>(ctr)[i] = 0;
+        for (u64 i = from; i < ws_words; i += stride) ws_tiles[i] = 0;
+    };
+    if (live && t < kC) {
+        const u32 i = c * kC + t;
         PrepAcc acc;
         u64 w = ~0ull;  // pads sort last
         if (i < n) {
@@ -986,34 +1005,43 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
             if (acc.bad) atomicMax(&s_acc[1], acc.bad);
             if (acc.oor) atomicOr(&s_acc[2], 1ull);
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(kChunk) : "memory");
-        sort_block<1>(s_own, s_own + kChunk, t, kChunk, kChunk);
+        asm volatile("bar.sync 1, %0;" ::"r"(kC) : "memory");
+        sort_block<1>(s_own, s_own + kC, t, kC, kC);
         if (t < 3) cl.map_shared_rank(s_part, 0)[3 * c + t] = s_acc[t];
-    } else if (c == 0) {  // CTA 0's other threads: counters and look-back words
-        for (u32 i = t - kChunk; i < sizeof(Ctr) / 8; i += kSmallFrontThreads - kChunk)
-            reinterpret_cast<ull*>(ctr)[i] = 0;
-        for (u64 i = t - kChunk; i < ws_words; i += kSmallFrontThreads - kChunk) ws_tiles[i] = 0;
+    } else if (c == 0) {  // CTA 0's other threads clear the counters while the chunk sorts
+        clear_counters(t - kC, kSmallFrontThreads - kC);
+    }
+    if constexpr (kC == kSmallFrontThreads) {  // (no other threads)
+        if (c == 0) {
+            __syncthreads();
+            clear_counters(t, kSmallFrontThreads);
+        }
     }
     cl.sync();  // every chunk sorted
+    bool mine = false;
+    u32 my_r = 0;
+    u64 x = 0;
     if (live) {
-        for (u32 i = t; i < nch * kChunk; i += kSmallFrontThreads) {
-            const u32 q = i / kChunk;
-            s_all[i] = q == c ? s_own[i - q * kChunk] : cl.map_shared_rank(s_own, q)[i - q * kChunk];
+        for (u32 i = t; i < nch * kC; i += kSmallFrontThreads) {
+            const u32 q = i / kC;
+            s_all[i] = q == c ? s_own[i - q * kC] : cl.map_shared_rank(s_own, q)[i - q * kC];
         }
         __syncthreads();
-        const u32 e = t & (kChunk - 1), part = t / kChunk;
-        const u64 x = s_all[c * kChunk + e];
-        if (c * kChunk + e < n) {
+        // place in the merged order: index in the chunk + the words below it
+        // in every other chunk (kParts threads per word, independent bisections)
+        const u32 e = t % kC, part = t / kC;
+        x = s_all[c * kC + e];
+        if (c * kC + e < n) {
             u32 cnt = 0;
 #pragma unroll
-            for (u32 k = 0; k < kChunks / 4; ++k) {
-                const u32 q = part + 4 * k;
+            for (u32 k = 0; k < kClusterCtas / kParts; ++k) {
+                const u32 q = part + kParts * k;
                 if (q < nch && q != c) {
-                    const u64* run = s_all + q * kChunk;
+                    const u64* run = s_all + q * kC;
                     const bool le = q < c;  // equal words: earlier chunks first
                     u32 lo = 0;
 #pragma unroll
-                    for (u32 step = kChunk / 2; step > 0; step >>= 1) {
+                    for (u32 step = kC / 2; step > 0; step >>= 1) {
                         const u64 y = run[lo + step - 1];
                         if (le ? y <= x : y < x) lo += step;
                     }
@@ -1025,7 +1053,15 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
             if (cnt) atomicAdd(&s_rank[e], cnt);
         }
         __syncthreads();
-        if (t < kChunk && c * kChunk + t < n) cl.map_shared_rank(s_mrg, 0)[t + s_rank[t]] = x;
+        if (t < kC && c * kC + t < n) {
+            mine = true;
+            my_r = t + s_rank[t];
+        }
+        if (!kAlias && mine) cl.map_shared_rank(s_mrg, 0)[my_r] = x;
+    }
+    if constexpr (kAlias) {
+        cl.sync();  // every CTA has read its copy of the chunks: CTA 0's becomes the merged array
+        if (mine) cl.map_shared_rank(s_mrg, 0)[my_r] = x;
     }
     cl.sync();  // merged words in CTA 0 (and no CTA reads another's shared memory past here)
     if (c != 0) return;
@@ -1049,7 +1085,47 @@ __global__ void __launch_bounds__(kSmallFrontThreads, 1)
         }
     }
     __syncthreads();
-    small_resolve(s_mrg, n, f, db, ib, ctr, s_tot, gt0, s_wsum, o_k, o_v, o_o);
+    small_resolve<kClusterCtas * kC / kSmallFrontThreads>(s_mrg, n, f, db, ib, ctr, s_tot, gt0, s_wsum, o_k, o_v,
+                                                          o_o);
+}
+
+static cudaLaunchConfig_t cluster_front_config(cudaStream_t st, cudaLaunchAttribute* at, int smem) {  // 16 CTAs
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(kClusterCtas);
+    lc.blockDim = dim3(kSmallFrontThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kClusterCtas;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    return lc;
+}
+template <u32 kC>
+static bool cluster_variant_available() {
+    static const bool ok = [] {
+        if (cudaFuncSetAttribute(k_small_front_cluster<kC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 cluster_smem<kC>()) != cudaSuccess ||
+            cudaFuncSetAttribute(k_small_front_cluster<kC>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        cudaLaunchAttribute at[1];
+        const cudaLaunchConfig_t lc = cluster_front_config(nullptr, at, cluster_smem<kC>());
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, k_small_front_cluster<kC>, &lc) != cudaSuccess) {
+            cudaGetLastError();
+            nc = 0;
+        }
+        return nc > 0;
+    }();
+    return ok;
+}
+static bool cluster_front_available() {
+    return cluster_variant_available<256>() && cluster_variant_available<kSmallFrontThreads>();
 }
 
 // Leaf of every unique update of a small batch (leaf_for_key), a warp per
@@ -2841,6 +2917,8 @@ void Pma::enqueue_level(int level, u64 npend, u32* pcur, u32* pnext, u64* touche
 // the layout and the engine config; any change re-captures it.
 bool Pma::small_graph_ok(u64 n, const GraphFront& gf) const {
     if (!small_graphs_ || gf.mk || n == 0 || n > kSmallGraphMax || height_ < 1 || !ro_base() || !stream_) return false;
+    // (beyond one CTA's sort and the cooperative grid's chunks: the cluster only)
+    if (n > kSmallFrontMax && !(small_cluster_ && cluster_front_available())) return false;
     int db = 1;
     while (db < 32 && (1ull << db) < gf.nv) ++db;
     return 2 * db + kSmallIb <= 64;
@@ -2880,47 +2958,19 @@ void Pma::capture_small_graph(int db, const EngineCfg& cfg, int levels, int mult
         // front end in one CTA (counters and look-back words zeroed there,
         // descriptor read in place from page-locked memory), then the leaf of
         // every unique update (pma.hpp:234-289), a warp per key
-        static_assert(kSmallGraphMax <= kSmallFrontMax, "small graph batches sort in one CTA");
-        // (a 16-CTA cluster is non-portable: where it cannot be resident the
-        // cooperative grid takes its place)
-        static const bool cluster_ok = [this] {
-            GPMA_CUDA(cudaFuncSetAttribute(k_small_front_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           kSmallClusterSmem));
-            GPMA_CUDA(cudaFuncSetAttribute(k_small_front_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(kChunks);
-            lc.blockDim = dim3(kSmallFrontThreads);
-            lc.dynamicSmemBytes = kSmallClusterSmem;
+        static_assert(kSmallGraphMax <= kSmallMultiMax, "small graph batches fit the cluster front end");
+        if (multi && small_cluster_ && cluster_front_available()) {  // (one cluster: distributed shared memory)
             cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = kChunks;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            int nc = 0;
-            if (cudaOccupancyMaxActiveClusters(&nc, k_small_front_cluster, &lc) != cudaSuccess) {
-                cudaGetLastError();
-                nc = 0;
+            const GraphFront* hd = h_desc_dev_;
+            if (multi == 2) {
+                const cudaLaunchConfig_t lc = cluster_front_config(stream_, at, cluster_smem<kSmallFrontThreads>());
+                GPMA_CUDA(cudaLaunchKernelEx(&lc, k_small_front_cluster<kSmallFrontThreads>, hd, db, ib, d_ctr,
+                                             small_ws_.tiles.ptr, u64(small_ws_.tiles.cap), uk.ptr, uv.ptr, uop.ptr));
+            } else {
+                const cudaLaunchConfig_t lc = cluster_front_config(stream_, at, cluster_smem<256>());
+                GPMA_CUDA(cudaLaunchKernelEx(&lc, k_small_front_cluster<256>, hd, db, ib, d_ctr, small_ws_.tiles.ptr,
+                                             u64(small_ws_.tiles.cap), uk.ptr, uv.ptr, uop.ptr));
             }
-            return nc > 0;
-        }();
-        if (multi && small_cluster_ && cluster_ok) {  // (one cluster: distributed shared memory between the chunks)
-            cudaLaunchConfig_t lc{};
-            lc.gridDim = dim3(kChunks);
-            lc.blockDim = dim3(kSmallFrontThreads);
-            lc.dynamicSmemBytes = kSmallClusterSmem;
-            lc.stream = stream_;
-            cudaLaunchAttribute at[1];
-            at[0].id = cudaLaunchAttributeClusterDimension;
-            at[0].val.clusterDim.x = kChunks;
-            at[0].val.clusterDim.y = 1;
-            at[0].val.clusterDim.z = 1;
-            lc.attrs = at;
-            lc.numAttrs = 1;
-            GPMA_CUDA(cudaLaunchKernelEx(&lc, k_small_front_cluster, static_cast<const GraphFront*>(h_desc_dev_), db,
-                                         ib, d_ctr, small_ws_.tiles.ptr, u64(small_ws_.tiles.cap), uk.ptr, uv.ptr,
-                                         uop.ptr));
         } else if (multi) {  // (one cooperative grid: its CTAs wait on each other)
             cudaLaunchConfig_t lc{};
             lc.gridDim = dim3(kChunks);
@@ -2975,7 +3025,8 @@ int Pma::run_small_graph(const GraphFront& gf, const EngineCfg& cfg) {
     int db = 1;
     while (db < 32 && (1ull << db) < gf.nv) ++db;
     const int levels = std::min(kSmallGraphLevels, height_);
-    const int multi = gf.ni + gf.nd > small_onecta_ ? 1 : 0;
+    const u64 n = gf.ni + gf.nd;
+    const int multi = n > kSmallFrontMax ? 2 : n > std::min<u64>(small_onecta_, kSmallFrontMax) ? 1 : 0;
     small_sb_.reserve(kSbWords);  // (both variants' keys name it)
     auto key = small_graph_key(db, cfg, levels);
     if (!small_exec_[multi] || key != small_key_[multi]) {

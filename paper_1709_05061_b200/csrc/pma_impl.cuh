@@ -165,8 +165,8 @@ public:
     u64 grid_seg_ = u64(1) << 16;
     void grid_merge(u64 b, u64 m, const u32* plist, u64 s, bool large);
     // small graph batches (pma.cu): captured front end + first rounds
-    static constexpr u64 kSmallGraphMax = 4096;
-    static constexpr int kSmallIb = 13;  // index bits of the packed sort word ((1 << 13) - 1 > 4096: delete marker)
+    static constexpr u64 kSmallGraphMax = 16384;
+    static constexpr int kSmallIb = 15;  // index bits of the packed sort word ((1 << 15) - 1 > 16384: delete marker)
     static constexpr int kSmallGraphLevels = 1;  // most small batches finish in round 0; more rounds: host loop
     bool small_graph_ok(u64 n, const GraphFront& gf) const;
     std::vector<uintptr_t> small_graph_key(int db, const EngineCfg& cfg, int levels) const;
@@ -302,8 +302,8 @@ public:  // (extended __device__ lambdas need public enclosing functions)
     RadixWorkspace rws;           // onesweep radix sort (radix.cuh)
     // small graph batches
     bool small_graphs_ = true;          // GPMA_NO_GRAPHS=1 disables (A/B measurements)
-    cudaGraphExec_t small_exec_[2] = {nullptr, nullptr};  // [one-CTA front end, multi-CTA front end]
-    std::vector<uintptr_t> small_key_[2];  // what each captured graph embeds
+    cudaGraphExec_t small_exec_[3] = {nullptr, nullptr, nullptr};  // front end: one CTA, multi-CTA, multi-CTA > 4096
+    std::vector<uintptr_t> small_key_[3];  // what each captured graph embeds
     u64 small_onecta_ = 512;            // larger small batches: the multi-CTA front end (GPMA_SMALL_ONECTA=n)
     DevBuf<u64> small_sb_;              // its scratch (k_small_front_grid)
     bool check_rounds_ = false;         // GPMA_CHECK_ROUNDS=1: the round-disjointness check after every grouping

@@ -79,7 +79,7 @@ def _window_stream(kind, nv, param, seed=1, shuffle=2):
 
 
 @pytest.mark.parametrize("mode", [PMA_LAZY, PMA_EAGER])
-# (batches of up to 4096 updates take the captured small-batch graph; its
+# (batches of up to 16384 updates take the captured small-batch graph; its
 # one-CTA sort runs 1, 2 or 4 items per thread: 512 -> 1024 updates, 700 ->
 # ~1400, 1500 -> ~3000)
 @pytest.mark.parametrize("kind,nv,param,batch", [("er", 4096, 2**-7, 512), ("rmat", 2**13, 60000, 1500),
@@ -493,7 +493,7 @@ def test_small_batch_front_end_variants(onecta, cluster, monkeypatch):
     g = DynamicGraph.from_edges(nv, s[:half], d[:half], w[:half])
     r = RefGraph(nv, s[:half], d[:half], w[:half], graph_config())
     ps, pd = s[:half].astype(np.uint32), d[:half].astype(np.uint32)
-    for n in (100, 700, 1025, 1500, 2500, 4096):
+    for n in (100, 700, 1025, 1500, 2500, 4096, 4097, 9000, 16384):
         nd = n // 3
         ni = n - nd
         a = rng.integers(0, nv, ni).astype(np.uint32)
@@ -522,10 +522,11 @@ def test_small_batch_front_end_variants(onecta, cluster, monkeypatch):
     assert_same_slots(g.pma().slots(), r.slots(), "out-of-layout deletes")
     # two bad inserts in different chunks: the first is reported, nothing changes
     before = g.pma().slots()
-    a3 = rng.integers(0, nv, 3000)
-    a3[1700], a3[2900] = nv + 3, nv + 9
-    with pytest.raises(ValueError, match=rf"edge \({nv + 3}, \d+\) outside vertex range {nv}"):
-        g.apply_batch(a3, rng.integers(0, nv, 3000), None, [], [])
+    for m, j in ((3000, 1700), (12000, 7000)):
+        a3 = rng.integers(0, nv, m)
+        a3[j], a3[m - 100] = nv + 3, nv + 9
+        with pytest.raises(ValueError, match=rf"edge \({nv + 3}, \d+\) outside vertex range {nv}"):
+            g.apply_batch(a3, rng.integers(0, nv, m), None, [], [])
     assert all((x == y).all() for x, y in zip(before, g.pma().slots()))
 
 
