@@ -79,7 +79,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=None, help="default: the config's batch")
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
-    ap.add_argument("--sweep", default="100,1000,10000,100000,1000000")
+    ap.add_argument("--sweep", default="100,1000,5000,10000,100000,1000000")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-analytics", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no sweep/baseline/analytics)")
